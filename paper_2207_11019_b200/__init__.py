@@ -1,0 +1,6 @@
+"""pipeplan_b200: B200-native layer-wise partition-and-merge training step.
+
+Host-side mirror of the reference `pipeplan` API for the hot path
+(`train_partitioned` and the planner it consumes), backed by the C ABI in
+include/pipeplan_b200.h and hand-written sm_100a kernels.
+"""

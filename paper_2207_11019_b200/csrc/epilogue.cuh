@@ -1,0 +1,116 @@
+// Fused GEMM epilogues (shared by the tcgen05 and SIMT kernels).
+//
+// One call handles 32 consecutive accumulator columns [n0, n0+32) of row m,
+// which is exactly what one tcgen05.ld.32x32b.x32 hands a thread.
+#pragma once
+
+#include <cstdint>
+
+#include "gemm.h"
+
+namespace ppb {
+
+__device__ __forceinline__ bool aligned16(const void* p) {
+    return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+}
+
+__device__ __forceinline__ void store_row32(float* row, int n0, int nvalid, const float (&v)[32]) {
+    // row points at column 0 of the destination row; n0 is a multiple of 32.
+    float* p = row + n0;
+    if (nvalid >= 32 && aligned16(p)) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+            *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            if (i < nvalid) p[i] = v[i];
+        }
+    }
+}
+
+__device__ __forceinline__ void load_row32(const float* row, int n0, int nvalid, float (&v)[32]) {
+    const float* p = row + n0;
+    if (nvalid >= 32 && aligned16(p)) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+            float4 t = *reinterpret_cast<const float4*>(p + i);
+            v[i] = t.x;
+            v[i + 1] = t.y;
+            v[i + 2] = t.z;
+            v[i + 3] = t.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = i < nvalid ? p[i] : 0.f;
+    }
+}
+
+// Apply the epilogue to acc[0..32) = C(m, n0..n0+31).
+__device__ __forceinline__ void epilogue32(const EpiParams& p, int m, int n0, float (&acc)[32]) {
+    if (m >= p.M || n0 >= p.N) return;
+    const int nvalid = p.N - n0 < 32 ? p.N - n0 : 32;
+    switch (p.mode) {
+        case EPI_STORE: {
+            if (p.bias != nullptr) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) acc[i] += (i < nvalid) ? __ldg(p.bias + n0 + i) : 0.f;
+            }
+            if (p.relu) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) acc[i] = acc[i] > 0.f ? acc[i] : 0.f;
+            }
+            for (int d = 0; d < p.ndst; ++d) {
+                store_row32(p.dst[d] + static_cast<long long>(m) * p.ldd + p.col0, n0, nvalid, acc);
+            }
+            break;
+        }
+        case EPI_MASK: {
+            float mk[32];
+            load_row32(p.mask + static_cast<long long>(m) * p.ldm + p.mcol0, n0, nvalid, mk);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc[i] = mk[i] > 0.f ? acc[i] : 0.f;
+            store_row32(p.dst[0] + static_cast<long long>(m) * p.ldd + p.col0, n0, nvalid, acc);
+            break;
+        }
+        case EPI_SGD: {
+            float w[32];
+            float* row = p.W + static_cast<long long>(m) * p.ldw;
+            load_row32(row, n0, nvalid, w);
+            const float alpha = static_cast<float>(*p.alpha);
+            bool bad = false;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const float g = acc[i] * p.inv_b;
+                bad |= (i < nvalid) && !isfinite(g);
+                w[i] -= alpha * g;
+            }
+            if (bad && p.flag != nullptr) atomicOr(p.flag, 1);
+            store_row32(row, n0, nvalid, w);
+            break;
+        }
+        case EPI_SLOTS: {
+            for (int s = 0; s < p.nseg; ++s) {
+                const int lo = p.seg_lo[s] > n0 ? p.seg_lo[s] : n0;
+                int hi = p.seg_hi[s] < n0 + nvalid ? p.seg_hi[s] : n0 + nvalid;
+                if (lo >= hi) continue;
+                float* row = p.seg_dst[s] + static_cast<long long>(m) * p.seg_ld[s] - p.seg_lo[s];
+                if (lo == n0 && hi == n0 + 32) {
+                    store_row32(row, n0, 32, acc);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const int n = n0 + i;
+                        if (n >= lo && n < hi) row[n] = acc[i];
+                    }
+                }
+            }
+            break;
+        }
+        default:
+            break;
+    }
+}
+
+}  // namespace ppb

@@ -1,0 +1,326 @@
+// Persistent, warp-specialised tcgen05 TF32 GEMM for sm_100a.
+//
+//   warp 0      : TMA producer (one elected lane), SWIZZLE_128B tiles into a
+//                 kStages-deep shared-memory ring guarded by full/empty mbarriers
+//   warp 1      : MMA issuer (one elected lane): tcgen05.mma.cta_group::1.kind::tf32,
+//                 128 x BN x 8 per instruction, accumulator in TMEM
+//   warp 2      : TMEM allocator (2 x BN columns: double-buffered accumulator)
+//   warps 4..7  : epilogue: tcgen05.ld -> registers -> fused epilogue -> global
+//
+// Tiles are BM=128 rows x BN columns, BK=32 fp32 (= one 128-byte swizzle
+// atom for K-major operands).  K-major operands are loaded as one TMA box
+// {32 (K), rows}; MN-major operands as rows/32 boxes {32 (MN), 32 (K)}, each
+// a 4 KB canonical MN-major SW128 atom column.  See gemm.h for how the
+// forward / dgrad / wgrad products of the partitioned step map onto A and B.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "epilogue.cuh"
+#include "gemm_tc.h"
+#include "ptx.cuh"
+
+namespace ppb {
+
+namespace {
+
+constexpr int kBM = 128;
+constexpr int kBK = 32;
+constexpr int kThreads = 256;
+
+template <int BN>
+struct TcCfg {
+    static constexpr int kStageA = kBM * kBK * 4;  // bytes
+    static constexpr int kStageB = BN * kBK * 4;
+    static constexpr int kStageBytes = kStageA + kStageB;
+    static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
+    static constexpr int kTmemCols = 2 * BN;
+    // dynamic smem: 1 KB alignment slack + stages + barriers
+    static constexpr int kSmem = 1024 + kStages * kStageBytes + 256;
+};
+
+template <bool A_MN, bool B_MN, int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                   int M, int N, int K, const __grid_constant__ EpiParams epi) {
+    using C = TcCfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + C::kStages * C::kStageA;
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+    uint64_t* empty_bar = full_bar + C::kStages;
+    uint64_t* tfull_bar = empty_bar + C::kStages;   // [2]
+    uint64_t* tempty_bar = tfull_bar + 2;            // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+    const int warp = threadIdx.x / 32;
+    const int num_m = (M + kBM - 1) / kBM;
+    const int num_n = (N + BN - 1) / BN;
+    const int num_tiles = num_m * num_n;
+    const int nk = (K + kBK - 1) / kBK;
+
+    if (warp == 0 && elect_one()) {
+        tma_prefetch(&ta);
+        tma_prefetch(&tb);
+        for (int s = 0; s < C::kStages; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull_bar[i], 1);
+            mbar_init(&tempty_bar[i], 128);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, C::kTmemCols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer
+        if (elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                const int m0 = (tile % num_m) * kBM;
+                const int n0 = (tile / num_m) * BN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    const int k0 = kb * kBK;
+                    mbar_wait(&empty_bar[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes);
+                    uint8_t* a_dst = sA + stage * C::kStageA;
+                    uint8_t* b_dst = sB + stage * C::kStageB;
+                    if (A_MN) {
+#pragma unroll
+                        for (int i = 0; i < kBM / 32; ++i)
+                            tma_load_2d(a_dst + i * 4096, &ta, &full_bar[stage], m0 + 32 * i, k0);
+                    } else {
+                        tma_load_2d(a_dst, &ta, &full_bar[stage], k0, m0);
+                    }
+                    if (B_MN) {
+#pragma unroll
+                        for (int i = 0; i < BN / 32; ++i)
+                            tma_load_2d(b_dst + i * 4096, &tb, &full_bar[stage], n0 + 32 * i, k0);
+                    } else {
+                        tma_load_2d(b_dst, &tb, &full_bar[stage], k0, n0);
+                    }
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        constexpr uint32_t idesc = idesc_tf32(BN, A_MN, B_MN);
+        int stage = 0;
+        uint32_t phase = 0;
+        int local = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+            const int acc = local & 1;
+            const uint32_t acc_phase = (local >> 1) & 1;
+            mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + acc * BN;
+            for (int kb = 0; kb < nk; ++kb) {
+                mbar_wait(&full_bar[stage], phase);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t a_addr = smem_u32(sA + stage * C::kStageA);
+                    const uint32_t b_addr = smem_u32(sB + stage * C::kStageB);
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 8; ++kk) {
+                        // K-major (SW128): advance 32 B inside the 128 B swizzle
+                        // atom; 8-row groups 1 KB apart (SBO).
+                        // MN-major (SW128_BASE32B): advance 8 K rows (1 KB);
+                        // 4-row K groups 512 B apart (SBO), 32-wide MN atoms
+                        // 4 KB apart (LBO).
+                        const uint64_t ad = A_MN ? umma_desc<kLayoutSW128Base32>(a_addr + kk * 1024, 4096, 512)
+                                                 : umma_desc<kLayoutSW128>(a_addr + kk * 32, 16, 1024);
+                        const uint64_t bd = B_MN ? umma_desc<kLayoutSW128Base32>(b_addr + kk * 1024, 4096, 512)
+                                                 : umma_desc<kLayoutSW128>(b_addr + kk * 32, 16, 1024);
+                        mma_tf32(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                    }
+                    mma_commit(&empty_bar[stage]);
+                }
+                __syncwarp();
+                if (++stage == C::kStages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            if (elect_one()) mma_commit(&tfull_bar[acc]);
+            __syncwarp();
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------ epilogue
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int lane = threadIdx.x & 31;
+        int local = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+            const int m0 = (tile % num_m) * kBM;
+            const int n0 = (tile / num_m) * BN;
+            const int acc = local & 1;
+            const uint32_t acc_phase = (local >> 1) & 1;
+            mbar_wait(&tfull_bar[acc], acc_phase);
+            tc_fence_after();
+            const int m = m0 + q * 32 + lane;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, r);
+                tmem_ld_wait();
+                float v[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+                epilogue32(epi, m, n0 + c * 32, v);
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty_bar[acc]);
+        }
+    }
+
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, C::kTmemCols);
+    }
+}
+
+// ---------------------------------------------------------------- host side
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess) {
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+        }
+    });
+    return fn;
+}
+
+// Encode a 2-D fp32 map over a row-major (rows x cols, ld) matrix whose
+// innermost (contiguous) dimension is `cols`, box {32, box_rows}, SW128.
+bool encode_map(CUtensorMap* map, const float* ptr, int rows, int cols, long long ld,
+                int box_rows, bool mn_major, char* err, size_t errlen) {
+    auto enc = get_encode();
+    if (enc == nullptr) {
+        snprintf(err, errlen, "cuTensorMapEncodeTiled unavailable");
+        return false;
+    }
+    if ((reinterpret_cast<uintptr_t>(ptr) & 15u) != 0 || (ld * 4) % 16 != 0) {
+        snprintf(err, errlen, "TMA operand not 16-byte aligned (ptr=%p ld=%lld)", (const void*)ptr, ld);
+        return false;
+    }
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 4)};
+    cuuint32_t box[2] = {32u, static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t estr[2] = {1u, 1u};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        snprintf(err, errlen, "cuTensorMapEncodeTiled failed (%d) rows=%d cols=%d ld=%lld box=%d",
+                 static_cast<int>(r), rows, cols, ld, box_rows);
+        return false;
+    }
+    return true;
+}
+
+template <bool A_MN, bool B_MN, int BN>
+cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
+    using C = TcCfg<BN>;
+    auto k = tc_gemm_kernel<A_MN, B_MN, BN>;
+    static std::atomic<unsigned> attr_set{0};  // one bit per device ordinal
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned bit = 1u << (dev & 31);
+    if ((attr_set.load() & bit) == 0) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+        if (e != cudaSuccess) return e;
+        attr_set.fetch_or(bit);
+    }
+    k<<<p.grid, kThreads, C::kSmem, s>>>(p.ta, p.tb, p.M, p.N, p.K, p.epi);
+    return cudaGetLastError();
+}
+
+template <bool A_MN, bool B_MN>
+cudaError_t launch_bn(const TcGemmPlan& p, cudaStream_t s) {
+    switch (p.bn) {
+        case 64: return launch_t<A_MN, B_MN, 64>(p, s);
+        case 128: return launch_t<A_MN, B_MN, 128>(p, s);
+        default: return launch_t<A_MN, B_MN, 256>(p, s);
+    }
+}
+
+int sm_count() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+}  // namespace
+
+bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err, size_t errlen) {
+    TcGemmPlan p;
+    p.M = d.M;
+    p.N = d.N;
+    p.K = d.K;
+    p.a_mn = d.a.mn_major;
+    p.b_mn = d.b.mn_major;
+    p.epi = d.epi;
+    p.epi.M = d.M;
+    p.epi.N = d.N;
+    // Tile width: the widest BN that still gives every SM a tile, else 64.
+    const int sms = sm_count();
+    const int num_m = (d.M + kBM - 1) / kBM;
+    int bn = 256;
+    if (force_bn == 64 || force_bn == 128 || force_bn == 256) {
+        bn = force_bn;
+    } else {
+        while (bn > 64 && num_m * ((d.N + bn - 1) / bn) < sms) bn /= 2;
+    }
+    p.bn = bn;
+    const int tiles = num_m * ((d.N + bn - 1) / bn);
+    p.grid = tiles < sms ? tiles : sms;
+    // A: M extent x K.  K-major: rows=M, cols=K, box {32, 128}.  MN-major:
+    // stored K x M (rows=K, cols=M), box {32, 32}.
+    if (!encode_map(&p.ta, d.a.ptr, d.a.rows, d.a.cols, d.a.ld, d.a.mn_major ? 32 : kBM, d.a.mn_major, err, errlen))
+        return false;
+    if (!encode_map(&p.tb, d.b.ptr, d.b.rows, d.b.cols, d.b.ld, d.b.mn_major ? 32 : bn, d.b.mn_major, err, errlen))
+        return false;
+    *out = p;
+    return true;
+}
+
+cudaError_t tc_gemm_launch(const TcGemmPlan& p, cudaStream_t s) {
+    if (p.M <= 0 || p.N <= 0) return cudaSuccess;
+    if (p.a_mn) {
+        return p.b_mn ? launch_bn<true, true>(p, s) : launch_bn<true, false>(p, s);
+    }
+    return p.b_mn ? launch_bn<false, true>(p, s) : launch_bn<false, false>(p, s);
+}
+
+}  // namespace ppb
