@@ -93,16 +93,26 @@ __device__ __forceinline__ void epilogue32(const EpiParams& p, int m, int n0, fl
         case EPI_SLOTS: {
             for (int s = 0; s < p.nseg; ++s) {
                 const int lo = p.seg_lo[s] > n0 ? p.seg_lo[s] : n0;
-                int hi = p.seg_hi[s] < n0 + nvalid ? p.seg_hi[s] : n0 + nvalid;
+                const int hi = p.seg_hi[s] < n0 + nvalid ? p.seg_hi[s] : n0 + nvalid;
                 if (lo >= hi) continue;
+                float v[32];
+                if (p.seg_mask[s] != nullptr) {
+                    float mk[32];
+                    load_row32(p.seg_mask[s] + static_cast<long long>(m) * p.seg_mask_ld[s], n0, nvalid, mk);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = mk[i] > 0.f ? acc[i] : 0.f;
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = acc[i];
+                }
                 float* row = p.seg_dst[s] + static_cast<long long>(m) * p.seg_ld[s] - p.seg_lo[s];
                 if (lo == n0 && hi == n0 + 32) {
-                    store_row32(row, n0, 32, acc);
+                    store_row32(row, n0, 32, v);
                 } else {
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
                         const int n = n0 + i;
-                        if (n >= lo && n < hi) row[n] = acc[i];
+                        if (n >= lo && n < hi) row[n] = v[i];
                     }
                 }
             }

@@ -51,12 +51,16 @@ struct EpiParams {
     const double* alpha = nullptr;  // device scalar (the reference keeps alpha in double)
     float inv_b = 1.f;
     int* flag = nullptr;
-    // EPI_SLOTS: n in [seg_lo[s], seg_hi[s]) -> seg_dst[s][m*seg_ld[s] + n - seg_lo[s]]
+    // EPI_SLOTS: n in [seg_lo[s], seg_hi[s]) -> seg_dst[s][m*seg_ld[s] + n - seg_lo[s]],
+    // optionally ReLU-masked by seg_mask[s][m*seg_mask_ld[s] + n] > 0 (used when
+    // a layer has a single contributor, so the backward merge is a pure scatter).
     int nseg = 0;
     int seg_lo[kMaxDst] = {};
     int seg_hi[kMaxDst] = {};
     float* seg_dst[kMaxDst] = {};
     long long seg_ld[kMaxDst] = {};
+    const float* seg_mask[kMaxDst] = {};
+    long long seg_mask_ld[kMaxDst] = {};
 };
 
 // Host-side description of one operand: a row-major fp32 matrix of `rows` x

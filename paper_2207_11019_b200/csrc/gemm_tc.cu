@@ -29,6 +29,8 @@ namespace ppb {
 
 namespace {
 
+std::atomic<unsigned> g_attr_set{0};  // one bit per device: smem attributes set
+
 constexpr int kBM = 128;
 constexpr int kBK = 32;
 constexpr int kThreads = 256;
@@ -244,18 +246,19 @@ bool encode_map(CUtensorMap* map, const float* ptr, int rows, int cols, long lon
     return true;
 }
 
+}  // namespace
+cudaError_t tc_gemm_init_device();
+namespace {
+
 template <bool A_MN, bool B_MN, int BN>
 cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
     using C = TcCfg<BN>;
     auto k = tc_gemm_kernel<A_MN, B_MN, BN>;
-    static std::atomic<unsigned> attr_set{0};  // one bit per device ordinal
     int dev = 0;
     cudaGetDevice(&dev);
-    const unsigned bit = 1u << (dev & 31);
-    if ((attr_set.load() & bit) == 0) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    if ((g_attr_set.load() & (1u << (dev & 31))) == 0) {
+        cudaError_t e = tc_gemm_init_device();
         if (e != cudaSuccess) return e;
-        attr_set.fetch_or(bit);
     }
     k<<<p.grid, kThreads, C::kSmem, s>>>(p.ta, p.tb, p.M, p.N, p.K, p.epi);
     return cudaGetLastError();
@@ -313,6 +316,28 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
         return false;
     *out = p;
     return true;
+}
+
+// Set the dynamic shared-memory limit of every instantiation on the current
+// device (must happen before any launch is captured into a CUDA graph).
+cudaError_t tc_gemm_init_device() {
+    cudaError_t e = cudaSuccess;
+    auto set = [&](auto kernel, int smem) {
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    };
+#define PPB_SET(AM, BM)                                                   \
+    set(tc_gemm_kernel<AM, BM, 64>, TcCfg<64>::kSmem);                    \
+    set(tc_gemm_kernel<AM, BM, 128>, TcCfg<128>::kSmem);                  \
+    set(tc_gemm_kernel<AM, BM, 256>, TcCfg<256>::kSmem);
+    PPB_SET(false, false)
+    PPB_SET(false, true)
+    PPB_SET(true, false)
+    PPB_SET(true, true)
+#undef PPB_SET
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (e == cudaSuccess) g_attr_set.fetch_or(1u << (dev & 31));
+    return e;
 }
 
 cudaError_t tc_gemm_launch(const TcGemmPlan& p, cudaStream_t s) {

@@ -23,6 +23,7 @@ struct TcGemmPlan {
 
 bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err, size_t errlen);
 cudaError_t tc_gemm_launch(const TcGemmPlan& p, cudaStream_t s);
+cudaError_t tc_gemm_init_device();
 
 // Exact-fp32 SIMT path with identical operand conventions and epilogues
 // (debug / tight-tolerance parity mode).

@@ -1,0 +1,324 @@
+// Non-GEMM kernels of the partitioned step.  All are HBM-bound (bytes per
+// element listed per kernel in DESIGN.md) and deterministic: every reduction
+// uses a fixed tree shape, never atomics on floating-point values.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cmath>
+
+#include "kernels.h"
+
+namespace ppb {
+
+namespace {
+
+constexpr int kRowThreads = 256;
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// (value, index) max with first-index tie break.
+__device__ __forceinline__ void argmax_merge(float& v, int& i, float ov, int oi) {
+    if (ov > v || (ov == v && oi < i)) {
+        v = ov;
+        i = oi;
+    }
+}
+
+template <int NT>
+__device__ void block_argmax(float& v, int& i) {
+    __shared__ float sv[NT / 32];
+    __shared__ int si[NT / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        float ov = __shfl_xor_sync(0xffffffffu, v, o);
+        int oi = __shfl_xor_sync(0xffffffffu, i, o);
+        argmax_merge(v, i, ov, oi);
+    }
+    const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+    if (l == 0) {
+        sv[w] = v;
+        si[w] = i;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < NT / 32; ++k) argmax_merge(sv[0], si[0], sv[k], si[k]);
+    }
+    __syncthreads();
+    v = sv[0];
+    i = si[0];
+    __syncthreads();
+}
+
+template <int NT>
+__device__ float block_sum(float v) {
+    __shared__ float s[NT / 32];
+    v = warp_sum(v);
+    const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+    if (l == 0) s[w] = v;
+    __syncthreads();
+    float r = 0.f;
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < NT / 32; ++k) r += s[k];
+        s[0] = r;
+    }
+    __syncthreads();
+    r = s[0];
+    __syncthreads();
+    return r;
+}
+
+template <int NT>
+__device__ double block_sum_d(double v) {
+    __shared__ double s[NT / 32];
+    v = warp_sum_d(v);
+    const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+    if (l == 0) s[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < NT / 32; ++k) r += s[k];
+        s[0] = r;
+    }
+    __syncthreads();
+    r = s[0];
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(kRowThreads) loss_head_kernel(
+    const float* __restrict__ in, long long ld_in, int F, const int* __restrict__ labels,
+    int loss_kind, int relu_last, LossTargets t, double* __restrict__ loss_row,
+    int* __restrict__ correct_row) {
+    const int row = blockIdx.x;
+    const float* x = in + static_cast<long long>(row) * ld_in;
+    const int label = labels[row];
+    // argmax (prediction) over the row, first index on ties
+    float bv = -FLT_MAX;
+    int bi = 0x7fffffff;
+    for (int c = threadIdx.x; c < F; c += kRowThreads) argmax_merge(bv, bi, x[c], c);
+    block_argmax<kRowThreads>(bv, bi);
+
+    if (loss_kind == 1) {
+        // ---- softmax + cross entropy (tinynet.cpp:104-117, :232-238)
+        const float mx = bv;
+        float se = 0.f;
+        for (int c = threadIdx.x; c < F; c += kRowThreads) se += expf(x[c] - mx);
+        se = block_sum<kRowThreads>(se);
+        const float inv = 1.f / se;
+        for (int k = 0; k < t.n; ++k) {
+            float* d = t.delta[k] + static_cast<long long>(row) * t.ld[k];
+            for (int c = t.lo[k] + threadIdx.x; c < t.hi[k]; c += kRowThreads) {
+                const float p = expf(x[c] - mx) * inv;
+                d[c - t.lo[k]] = p - (c == label ? 1.f : 0.f);
+            }
+        }
+        if (threadIdx.x == 0 && loss_row != nullptr) {
+            // -log(max(p_label, 1e-300)) via log-sum-exp in double
+            double l = static_cast<double>(mx) - static_cast<double>(x[label]) + log(static_cast<double>(se));
+            const double cap = 690.77552789821368;  // -log(1e-300)
+            loss_row[row] = l < cap ? l : cap;
+            correct_row[row] = (F == 1 ? 1 : bi) == label;
+        }
+    } else {
+        // ---- mse, 1/2 convention (tinynet.cpp:222-229, :275-279)
+        double part = 0.0;
+        for (int c = threadIdx.x; c < F; c += kRowThreads) {
+            const float tg = F == 1 ? static_cast<float>(label) : (c == label ? 1.f : 0.f);
+            const float d = x[c] - tg;
+            part += 0.5 * static_cast<double>(d) * static_cast<double>(d);
+        }
+        for (int k = 0; k < t.n; ++k) {
+            float* dd = t.delta[k] + static_cast<long long>(row) * t.ld[k];
+            for (int c = t.lo[k] + threadIdx.x; c < t.hi[k]; c += kRowThreads) {
+                const float tg = F == 1 ? static_cast<float>(label) : (c == label ? 1.f : 0.f);
+                float d = x[c] - tg;
+                if (relu_last && !(x[c] > 0.f)) d = 0.f;
+                dd[c - t.lo[k]] = d;
+            }
+        }
+        part = block_sum_d<kRowThreads>(part);
+        if (threadIdx.x == 0 && loss_row != nullptr) {
+            loss_row[row] = part;
+            const int pred = F == 1 ? (x[0] >= 0.5f ? 1 : 0) : bi;
+            correct_row[row] = pred == label;
+        }
+    }
+}
+
+__global__ void reduce_mask_kernel(ReduceSlots slots, long long ld_slot, int rows, int cols,
+                                   const float* __restrict__ mask, long long ld_mask,
+                                   float* __restrict__ out, long long ld_out, bool vec) {
+    if (vec) {
+        const int c4 = cols / 4;
+        const long long total = static_cast<long long>(rows) * c4;
+        for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+             i += static_cast<long long>(gridDim.x) * blockDim.x) {
+            const int r = static_cast<int>(i / c4), c = static_cast<int>(i % c4) * 4;
+            float4 acc = *reinterpret_cast<const float4*>(slots.slot[0] + r * ld_slot + c);
+            for (int k = 1; k < slots.n; ++k) {
+                const float4 v = *reinterpret_cast<const float4*>(slots.slot[k] + r * ld_slot + c);
+                acc.x += v.x;
+                acc.y += v.y;
+                acc.z += v.z;
+                acc.w += v.w;
+            }
+            if (mask != nullptr) {
+                const float4 m = *reinterpret_cast<const float4*>(mask + r * ld_mask + c);
+                acc.x = m.x > 0.f ? acc.x : 0.f;
+                acc.y = m.y > 0.f ? acc.y : 0.f;
+                acc.z = m.z > 0.f ? acc.z : 0.f;
+                acc.w = m.w > 0.f ? acc.w : 0.f;
+            }
+            *reinterpret_cast<float4*>(out + r * ld_out + c) = acc;
+        }
+        return;
+    }
+    const long long total = static_cast<long long>(rows) * cols;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int r = static_cast<int>(i / cols), c = static_cast<int>(i % cols);
+        float acc = slots.slot[0][r * ld_slot + c];
+        for (int k = 1; k < slots.n; ++k) acc += slots.slot[k][r * ld_slot + c];
+        if (mask != nullptr && !(mask[r * ld_mask + c] > 0.f)) acc = 0.f;
+        out[r * ld_out + c] = acc;
+    }
+}
+
+__global__ void colsum_partial_kernel(const float* __restrict__ delta, long long ld, int rows, int u,
+                                      float* __restrict__ partial) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int chunk = blockIdx.y;
+    const int per = (rows + kColsumChunks - 1) / kColsumChunks;
+    const int r0 = chunk * per;
+    const int r1 = r0 + per < rows ? r0 + per : rows;
+    if (c >= u) return;
+    float s = 0.f;
+    for (int r = r0; r < r1; ++r) s += delta[r * ld + c];
+    partial[static_cast<long long>(chunk) * u + c] = s;
+}
+
+__global__ void bias_update_kernel(const float* __restrict__ partial, int u, float* __restrict__ bias,
+                                   const double* __restrict__ alpha, float inv_b) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= u) return;
+    float s = 0.f;
+    for (int k = 0; k < kColsumChunks; ++k) s += partial[static_cast<long long>(k) * u + c];
+    bias[c] -= static_cast<float>(*alpha) * (s * inv_b);
+}
+
+template <class T>
+__global__ void convert_kernel(const T* __restrict__ src, int rows, int cols, float* __restrict__ dst,
+                               long long ld) {
+    const long long total = static_cast<long long>(rows) * cols;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long r = i / cols, c = i % cols;
+        dst[r * ld + c] = static_cast<float>(src[i]);
+    }
+}
+
+__global__ void finalize_kernel(StepState* st, const double* __restrict__ loss_row,
+                                const int* __restrict__ correct_row, int b, double* loss_hist,
+                                double* acc_hist, int hist_cap, int write_hist) {
+    double ls = 0.0;
+    double cs = 0.0;
+    if (write_hist) {
+        // fixed-shape tree: thread i sums rows i, i+NT, ... in order
+        for (int r = threadIdx.x; r < b; r += kRowThreads) {
+            ls += loss_row[r];
+            cs += correct_row[r];
+        }
+        ls = block_sum_d<kRowThreads>(ls);
+        cs = block_sum_d<kRowThreads>(cs);
+    }
+    if (threadIdx.x == 0) {
+        const int t = st->t;
+        if (write_hist) {
+            loss_hist[t % hist_cap] = ls / b;
+            acc_hist[t % hist_cap] = cs / b;
+        }
+        if (st->diverge_flag && st->diverged_first == 0) st->diverged_first = t + 1;
+        st->diverge_flag = 0;
+        st->alpha *= 1.0 - st->decay;
+        st->t = t + 1;
+    }
+}
+
+int grid_for(long long work, int threads) {
+    long long g = (work + threads - 1) / threads;
+    const long long cap = 148LL * 16;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return static_cast<int>(g);
+}
+
+}  // namespace
+
+cudaError_t launch_loss_head(const float* in, long long ld_in, int rows, int F, const int* labels,
+                             int loss_kind, int relu_last, const LossTargets& t, double* loss_row,
+                             int* correct_row, cudaStream_t s) {
+    if (rows <= 0) return cudaSuccess;
+    loss_head_kernel<<<rows, kRowThreads, 0, s>>>(in, ld_in, F, labels, loss_kind, relu_last, t,
+                                                  loss_row, correct_row);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_mask(const ReduceSlots& slots, long long ld_slot, int rows, int cols,
+                               const float* mask, long long ld_mask, float* out, long long ld_out,
+                               cudaStream_t s) {
+    if (rows <= 0 || cols <= 0) return cudaSuccess;
+    bool vec = (cols % 4 == 0) && (ld_slot % 4 == 0) && (ld_out % 4 == 0) &&
+               (mask == nullptr || ld_mask % 4 == 0) &&
+               (reinterpret_cast<uintptr_t>(out) % 16 == 0) &&
+               (mask == nullptr || reinterpret_cast<uintptr_t>(mask) % 16 == 0);
+    for (int k = 0; k < slots.n; ++k) vec = vec && reinterpret_cast<uintptr_t>(slots.slot[k]) % 16 == 0;
+    const long long work = static_cast<long long>(rows) * (vec ? cols / 4 : cols);
+    reduce_mask_kernel<<<grid_for(work, 256), 256, 0, s>>>(slots, ld_slot, rows, cols, mask, ld_mask,
+                                                           out, ld_out, vec);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bias_update(const float* delta, long long ld, int rows, int u, float* partial,
+                               float* bias, const double* alpha, float inv_b, cudaStream_t s) {
+    if (u <= 0) return cudaSuccess;
+    dim3 g1((u + 127) / 128, kColsumChunks);
+    colsum_partial_kernel<<<g1, 128, 0, s>>>(delta, ld, rows, u, partial);
+    bias_update_kernel<<<(u + 127) / 128, 128, 0, s>>>(partial, u, bias, alpha, inv_b);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_convert_f64(const double* src, int rows, int cols, float* dst, long long ld,
+                               cudaStream_t s) {
+    const long long n = static_cast<long long>(rows) * cols;
+    if (n <= 0) return cudaSuccess;
+    convert_kernel<double><<<grid_for(n, 256), 256, 0, s>>>(src, rows, cols, dst, ld);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_convert_f32(const float* src, int rows, int cols, float* dst, long long ld,
+                               cudaStream_t s) {
+    const long long n = static_cast<long long>(rows) * cols;
+    if (n <= 0) return cudaSuccess;
+    convert_kernel<float><<<grid_for(n, 256), 256, 0, s>>>(src, rows, cols, dst, ld);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(StepState* st, const double* loss_row, const int* correct_row, int b,
+                            double* loss_hist, double* acc_hist, int hist_cap, int write_hist,
+                            cudaStream_t s) {
+    finalize_kernel<<<1, kRowThreads, 0, s>>>(st, loss_row, correct_row, b, loss_hist, acc_hist,
+                                              hist_cap, write_hist);
+    return cudaGetLastError();
+}
+
+}  // namespace ppb

@@ -1,0 +1,937 @@
+// Partitioned training step executor.  See session.h for the mapping from the
+// reference's worker threads / Mailbox to CUDA streams / events, and
+// DESIGN.md for buffer layouts and the per-kernel rooflines.
+#include "session.h"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <set>
+#include <stdexcept>
+#include <thread>
+
+namespace ppb {
+
+namespace {
+
+std::string S(long long v) { return std::to_string(v); }
+
+[[noreturn]] void cuda_fail(cudaError_t e, const std::string& what) {
+    throw std::runtime_error("CUDA error in " + what + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ state
+
+struct Session::Gpu {
+    int ordinal = 0;
+    cudaStream_t main = nullptr;
+    StepState* st = nullptr;
+    int* labels = nullptr;
+    double* loss_row = nullptr;
+    int* correct_row = nullptr;
+    double* loss_hist = nullptr;
+    double* acc_hist = nullptr;
+    double* xstage = nullptr;
+    std::map<int, float*> act;  // layer -> [b x ld(dims[layer])]
+    float* q = nullptr;         // softmax head pre-activation [b x ld(F)]
+    std::vector<void*> allocs;
+    cudaEvent_t ev_loaded = nullptr;
+    cudaEvent_t ev_done = nullptr;
+    bool needs_x = false, needs_labels = false;
+
+    void* alloc(size_t bytes) {
+        void* p = nullptr;
+        cudaSetDevice(ordinal);
+        cudaError_t e = cudaMalloc(&p, bytes < 16 ? 16 : bytes);
+        if (e != cudaSuccess) cuda_fail(e, "cudaMalloc(" + S(static_cast<long long>(bytes)) + ")");
+        cudaMemset(p, 0, bytes < 16 ? 16 : bytes);
+        allocs.push_back(p);
+        return p;
+    }
+};
+
+struct Session::WLayer {
+    int layer = 0, lo = 0, hi = 0, u = 0;
+    bool replicated = false;
+    bool contributor = true;  // writes the layer output / the dgrad partial
+    float* W = nullptr;
+    long long ldw = 0;
+    float* bias = nullptr;
+    float* delta = nullptr;  // [b x ldd]
+    long long ldd = 0;
+    float* partial = nullptr;            // [kColsumChunks x u]
+    std::vector<float*> slots;           // per contributor of layer+1 (multi-contributor merges)
+    std::vector<std::vector<int>> delta_ready;  // [j] -> op ids that produce delta rows of micro-batch j
+    std::vector<int> fwd_op, dgrad_op;   // [j]
+    TcGemmPlan p_wgrad;
+    GemmDesc d_wgrad;
+    std::vector<TcGemmPlan> p_fwd, p_dgrad;
+    std::vector<GemmDesc> d_fwd, d_dgrad;
+};
+
+struct Session::Worker {
+    int module = 0, device = 0, rank = 0, gpu = 0;
+    cudaStream_t sf = nullptr, sb = nullptr, su = nullptr;
+    std::vector<WLayer> layers;  // span order
+    std::vector<int> last_bwd;   // [j] latest backward-side op of this worker
+    WLayer& at(int layer) { return layers[layer - layers.front().layer]; }
+};
+
+// ------------------------------------------------------------------ helpers
+
+void Session::check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) cuda_fail(e, what);
+}
+
+Session::Gpu& Session::gpu_of(int ordinal) {
+    for (auto& g : gpus_)
+        if (g->ordinal == ordinal) return *g;
+    throw std::runtime_error("internal: unknown GPU ordinal " + S(ordinal));
+}
+
+float* Session::act_buf(int ordinal, int layer) {
+    Gpu& g = gpu_of(ordinal);
+    auto it = g.act.find(layer);
+    if (it == g.act.end()) throw std::runtime_error("internal: no activation buffer for layer " + S(layer));
+    return it->second;
+}
+
+float* Session::q_buf(int ordinal) { return gpu_of(ordinal).q; }
+
+// ------------------------------------------------------------------ construction
+
+Session::Session(const std::vector<int>& device_map, const NetDesc& net, const double* W,
+                 const double* b, const Plan& plan, const SessionConfig& cfg)
+    : net_(net), plan_(plan), cfg_(cfg), device_map_(device_map) {
+    const int L = net_.L();
+    // ---- entry validation, in the reference's order (train_partitioned.cpp:124-141)
+    if (L < 1) throw std::invalid_argument("net must have at least one layer");
+    size_t wo = 0, bo = 0;
+    for (int l = 0; l < L; ++l) {
+        if (net_.dims[l] < 1 || net_.dims[l + 1] < 1)
+            throw std::invalid_argument("layer " + S(l + 1) + ": empty weight matrix");
+        if (net_.acts[l] == 2 && l != L - 1)
+            throw std::invalid_argument("softmax is only valid on the last layer");
+        for (size_t i = 0; i < static_cast<size_t>(net_.dims[l]) * net_.dims[l + 1]; ++i)
+            if (!std::isfinite(W[wo + i])) throw std::invalid_argument("non-finite weight");
+        for (int i = 0; i < net_.dims[l + 1]; ++i)
+            if (!std::isfinite(b[bo + i])) throw std::invalid_argument("non-finite bias");
+        host_W_.push_back(W + wo);
+        host_b_.push_back(b + bo);
+        wo += static_cast<size_t>(net_.dims[l]) * net_.dims[l + 1];
+        bo += net_.dims[l + 1];
+    }
+    Chain g;
+    for (int l = 0; l < L; ++l) {
+        g.fan_in.push_back(net_.dims[l]);
+        g.fan_out.push_back(net_.dims[l + 1]);
+    }
+    try {
+        validate_plan(plan_, g, 0);
+    } catch (const std::exception& e) {
+        throw std::runtime_error(std::string("plan/net shape mismatch: ") + e.what());
+    }
+    if (cfg_.batch < 1) throw std::invalid_argument("batch rows and label count disagree");
+    if (cfg_.mode != 1 && cfg_.mode != 2)
+        throw std::invalid_argument("train_partitioned needs sync or async update mode");
+    mb_sizes_ = split_microbatches(cfg_.batch, cfg_.m);
+    mb_off_.assign(cfg_.m + 1, 0);
+    for (int j = 0; j < cfg_.m; ++j) mb_off_[j + 1] = mb_off_[j] + mb_sizes_[j];
+    if (cfg_.loss == 1 && net_.acts[L - 1] != 2)
+        throw std::runtime_error("cross_entropy needs probability outputs (softmax last layer required)");
+    if (cfg_.loss == 0 && net_.acts[L - 1] == 2)
+        throw std::runtime_error("softmax output requires the cross_entropy loss");
+    for (const SubModule& sm : plan_.subs) {
+        if (sm.devices.size() > static_cast<size_t>(kMaxDst))
+            throw std::invalid_argument("sub-module " + S(sm.index) + " uses more than " + S(kMaxDst) +
+                                        " devices (B200 node limit)");
+        for (int d : sm.devices)
+            if (d < 1 || d > static_cast<int>(device_map_.size()))
+                throw std::runtime_error("plan references device " + S(d) + " absent from the context");
+    }
+    build();
+}
+
+Session::~Session() {
+    for (auto& g : gpus_) {
+        cudaSetDevice(g->ordinal);
+        cudaDeviceSynchronize();
+    }
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+    if (graph_) cudaGraphDestroy(graph_);
+    for (auto& op : ops_) {
+        if (op.ev) {
+            cudaSetDevice(op.gpu);
+            cudaEventDestroy(op.ev);
+        }
+    }
+    for (auto& w : workers_) {
+        cudaSetDevice(w->gpu);
+        cudaStreamDestroy(w->sf);
+        cudaStreamDestroy(w->sb);
+        cudaStreamDestroy(w->su);
+    }
+    for (auto& g : gpus_) {
+        cudaSetDevice(g->ordinal);
+        for (void* p : g->allocs) cudaFree(p);
+        if (g->ev_loaded) cudaEventDestroy(g->ev_loaded);
+        if (g->ev_done) cudaEventDestroy(g->ev_done);
+        cudaStreamDestroy(g->main);
+    }
+}
+
+void Session::build() {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+        cudaGetLastError();
+        throw std::runtime_error("no CUDA device available for pipeplan_b200");
+    }
+    // ---- GPUs in first-use order (the plan's device 1 maps to gpus_[0] first)
+    std::vector<int> order;
+    for (const SubModule& sm : plan_.subs)
+        for (int d : sm.devices) {
+            const int ord = device_map_[d - 1];
+            if (ord < 0 || ord >= ndev) throw std::runtime_error("device map entry " + S(ord) + " is not a CUDA device");
+            if (std::find(order.begin(), order.end(), ord) == order.end()) order.push_back(ord);
+        }
+    for (int ord : order) {
+        auto g = std::make_unique<Gpu>();
+        g->ordinal = ord;
+        check(cudaSetDevice(ord), "cudaSetDevice");
+        check(tc_gemm_init_device(), "GEMM attributes");
+        check(cudaStreamCreateWithFlags(&g->main, cudaStreamNonBlocking), "stream");
+        check(cudaEventCreateWithFlags(&g->ev_loaded, cudaEventDisableTiming), "event");
+        check(cudaEventCreateWithFlags(&g->ev_done, cudaEventDisableTiming), "event");
+        gpus_.push_back(std::move(g));
+    }
+    // peer access between every pair of distinct GPUs (NVLink / NVSwitch)
+    for (auto& a : gpus_)
+        for (auto& c : gpus_) {
+            if (a->ordinal == c->ordinal) continue;
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, a->ordinal, c->ordinal);
+            if (!can) throw std::runtime_error("GPU " + S(a->ordinal) + " cannot access peer GPU " + S(c->ordinal));
+            cudaSetDevice(a->ordinal);
+            cudaError_t e = cudaDeviceEnablePeerAccess(c->ordinal, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) cuda_fail(e, "peer access");
+            cudaGetLastError();
+        }
+    // ---- workers, one per (sub-module, device) as in train_partitioned.cpp:150-176
+    const int L = net_.L();
+    layer_workers_.assign(L + 1, {});
+    for (const SubModule& sm : plan_.subs) {
+        for (size_t r = 0; r < sm.devices.size(); ++r) {
+            auto w = std::make_unique<Worker>();
+            w->module = sm.index;
+            w->device = sm.devices[r];
+            w->rank = static_cast<int>(r);
+            w->gpu = device_map_[w->device - 1];
+            check(cudaSetDevice(w->gpu), "cudaSetDevice");
+            check(cudaStreamCreateWithFlags(&w->sf, cudaStreamNonBlocking), "stream");
+            check(cudaStreamCreateWithFlags(&w->sb, cudaStreamNonBlocking), "stream");
+            check(cudaStreamCreateWithFlags(&w->su, cudaStreamNonBlocking), "stream");
+            for (int l = sm.first_layer; l <= sm.last_layer; ++l) {
+                const Shard& s = sm.layer_shards(l)[r];
+                WLayer wl;
+                wl.layer = l;
+                wl.lo = s.lo;
+                wl.hi = s.hi;
+                wl.u = s.hi - s.lo;
+                wl.replicated = s.replicated;
+                wl.contributor = !s.replicated || r == 0;  // train_partitioned.cpp:181-190
+                w->layers.push_back(std::move(wl));
+                layer_workers_[l].push_back(static_cast<int>(workers_.size()));
+            }
+            w->last_bwd.assign(cfg_.m, -1);
+            workers_.push_back(std::move(w));
+        }
+    }
+    // loss / history live with rank 0 of the last module (train_partitioned.cpp:372)
+    main_gpu_ = workers_[layer_workers_[L].front()]->gpu;
+    alloc_buffers();
+    build_ops();
+    if (cfg_.use_graph) capture_graph();
+}
+
+void Session::alloc_buffers() {
+    const int L = net_.L();
+    const int b = cfg_.batch;
+    const int F = net_.dims[L];
+    const bool softmax = net_.acts[L - 1] == 2;
+    hist_cap_ = 1 << 16;
+    // which GPUs need which full activations
+    std::map<int, std::set<int>> need;  // layer -> ordinals
+    for (int wi : layer_workers_[1]) need[0].insert(workers_[wi]->gpu);
+    for (int l = 1; l < L; ++l) {
+        for (int wi : layer_workers_[l]) need[l].insert(workers_[wi]->gpu);
+        for (int wi : layer_workers_[l + 1]) need[l].insert(workers_[wi]->gpu);
+    }
+    if (!softmax)
+        for (int wi : layer_workers_[L]) need[L].insert(workers_[wi]->gpu);
+    for (auto& [l, set] : need)
+        for (int ord : set) {
+            Gpu& g = gpu_of(ord);
+            g.act[l] = static_cast<float*>(g.alloc(sizeof(float) * b * ld_of(net_.dims[l])));
+        }
+    for (int wi : layer_workers_[1]) gpu_of(workers_[wi]->gpu).needs_x = true;
+    for (int wi : layer_workers_[L]) {
+        Gpu& g = gpu_of(workers_[wi]->gpu);
+        g.needs_labels = true;
+        if (softmax && g.q == nullptr) g.q = static_cast<float*>(g.alloc(sizeof(float) * b * ld_of(F)));
+    }
+    for (auto& gp : gpus_) {
+        Gpu& g = *gp;
+        g.st = static_cast<StepState*>(g.alloc(sizeof(StepState)));
+        StepState init{cfg_.alpha0, cfg_.decay, 0, 0, 0, 0};
+        check(cudaMemcpy(g.st, &init, sizeof(init), cudaMemcpyHostToDevice), "init state");
+        g.labels = static_cast<int*>(g.alloc(sizeof(int) * b));
+        g.loss_row = static_cast<double*>(g.alloc(sizeof(double) * b));
+        g.correct_row = static_cast<int*>(g.alloc(sizeof(int) * b));
+        if (g.ordinal == main_gpu_) {
+            g.loss_hist = static_cast<double*>(g.alloc(sizeof(double) * hist_cap_));
+            g.acc_hist = static_cast<double*>(g.alloc(sizeof(double) * hist_cap_));
+        }
+        if (g.needs_x) g.xstage = static_cast<double*>(g.alloc(sizeof(double) * b * net_.dims[0]));
+    }
+    // shard weights, bias, error signals
+    std::vector<float> tmp;
+    for (auto& wp : workers_) {
+        Worker& w = *wp;
+        Gpu& g = gpu_of(w.gpu);
+        for (WLayer& wl : w.layers) {
+            const int fi = net_.dims[wl.layer - 1];
+            wl.ldw = ld_of(fi);
+            wl.W = static_cast<float*>(g.alloc(sizeof(float) * wl.u * wl.ldw));
+            wl.bias = static_cast<float*>(g.alloc(sizeof(float) * wl.u));
+            wl.ldd = ld_of(wl.u);
+            wl.delta = static_cast<float*>(g.alloc(sizeof(float) * b * wl.ldd));
+            wl.partial = static_cast<float*>(g.alloc(sizeof(float) * kColsumChunks * wl.u));
+            // upload the shard rows [lo, hi) (train_partitioned.cpp:168-169), fp64 -> fp32
+            tmp.assign(static_cast<size_t>(wl.u) * wl.ldw, 0.f);
+            const double* Wl = host_W_[wl.layer - 1];
+            for (int r = 0; r < wl.u; ++r)
+                for (int c = 0; c < fi; ++c)
+                    tmp[static_cast<size_t>(r) * wl.ldw + c] = static_cast<float>(Wl[static_cast<size_t>(wl.lo + r) * fi + c]);
+            check(cudaSetDevice(w.gpu), "cudaSetDevice");
+            check(cudaMemcpy(wl.W, tmp.data(), sizeof(float) * tmp.size(), cudaMemcpyHostToDevice), "upload W");
+            std::vector<float> bb(wl.u);
+            for (int r = 0; r < wl.u; ++r) bb[r] = static_cast<float>(host_b_[wl.layer - 1][wl.lo + r]);
+            check(cudaMemcpy(wl.bias, bb.data(), sizeof(float) * wl.u, cudaMemcpyHostToDevice), "upload b");
+            wl.delta_ready.assign(cfg_.m, {});
+            wl.fwd_op.assign(cfg_.m, -1);
+            wl.dgrad_op.assign(cfg_.m, -1);
+        }
+    }
+    // contributor slots for multi-contributor backward merges
+    for (int l = 2; l <= L; ++l) {
+        int ncontrib = 0;
+        for (int wi : layer_workers_[l]) ncontrib += workers_[wi]->at(l).contributor;
+        if (ncontrib < 2) continue;
+        for (int wi : layer_workers_[l - 1]) {
+            Worker& w = *workers_[wi];
+            WLayer& wl = w.at(l - 1);
+            Gpu& g = gpu_of(w.gpu);
+            for (int k = 0; k < ncontrib; ++k)
+                wl.slots.push_back(static_cast<float*>(g.alloc(sizeof(float) * b * wl.ldd)));
+        }
+    }
+    for (auto& gp : gpus_) {
+        cudaSetDevice(gp->ordinal);
+        check(cudaDeviceSynchronize(), "alloc");
+    }
+}
+
+int Session::add_op(int gpu, cudaStream_t s, std::function<cudaError_t()> f, std::vector<int> deps,
+                    int kernels) {
+    Op op;
+    op.gpu = gpu;
+    op.stream = s;
+    op.launch = std::move(f);
+    op.deps = std::move(deps);
+    op.kernels = kernels;
+    check(cudaSetDevice(gpu), "cudaSetDevice");
+    check(cudaEventCreateWithFlags(&op.ev, cudaEventDisableTiming), "event");
+    ops_.push_back(std::move(op));
+    return static_cast<int>(ops_.size()) - 1;
+}
+
+void Session::build_ops() {
+    const int L = net_.L();
+    const int F = net_.dims[L];
+    const bool softmax = net_.acts[L - 1] == 2;
+    const int m = cfg_.m;
+    const bool tf32 = cfg_.precision == 0;
+    Gpu& g0 = *gpus_[0];
+    begin_op_ = add_op(g0.ordinal, g0.main, nullptr, {}, 0);
+
+    auto gemm_launch = [tf32](TcGemmPlan* p, GemmDesc* d, cudaStream_t s) -> std::function<cudaError_t()> {
+        if (tf32) return [p, s]() { return tc_gemm_launch(*p, s); };
+        return [d, s]() { return simt_gemm_launch(*d, s); };
+    };
+    auto prepare = [&](GemmDesc& d, TcGemmPlan& p) {
+        if (!tf32) return;
+        char err[256];
+        if (!tc_gemm_prepare(d, &p, 0, err, sizeof(err))) throw std::runtime_error(std::string("GEMM setup: ") + err);
+    };
+    auto module_of_layer = [&](int l) -> const SubModule& {
+        for (const SubModule& sm : plan_.subs)
+            if (l >= sm.first_layer && l <= sm.last_layer) return sm;
+        throw std::runtime_error("internal: no module for layer");
+    };
+    auto contributors = [&](int l) {
+        std::vector<int> c;
+        for (int wi : layer_workers_[l])
+            if (workers_[wi]->at(l).contributor) c.push_back(wi);
+        return c;
+    };
+
+    // pre-size the plan/desc vectors (pointers into them are captured)
+    for (auto& wp : workers_)
+        for (WLayer& wl : wp->layers) {
+            wl.p_fwd.resize(m);
+            wl.d_fwd.resize(m);
+            wl.p_dgrad.resize(m);
+            wl.d_dgrad.resize(m);
+        }
+
+    // per (layer, micro-batch): ops whose completion makes a_layer (or q) of
+    // that micro-batch available on a given GPU
+    std::vector<std::vector<std::map<int, std::vector<int>>>> act_ready(
+        L + 1, std::vector<std::map<int, std::vector<int>>>(m));
+    std::vector<std::vector<int>> loss_ops(m);
+
+    // ---------------- forward of micro-batch j (train_partitioned.cpp:245-419)
+    auto forward = [&](int j) {
+        const int rows = mb_sizes_[j];
+        const long long off = mb_off_[j];
+        for (int l = 1; l <= L; ++l) {
+            const SubModule& sm = module_of_layer(l);
+            const bool last_in_module = l == sm.last_layer;
+            const bool boundary_concat = last_in_module && sm.index < plan_.Z() &&
+                                         plan_.boundaries[sm.index - 1] == kConcat;
+            const SubModule* next = sm.index < plan_.Z() ? &plan_.subs[sm.index] : nullptr;
+            std::set<int> dest_gpus;
+            for (int wi : layer_workers_[l]) dest_gpus.insert(workers_[wi]->gpu);
+            int hub_gpu = -1;
+            if (l < L) {
+                if (boundary_concat) {
+                    hub_gpu = device_map_[next->devices.front() - 1];
+                    dest_gpus.insert(hub_gpu);
+                } else {
+                    for (int wi : layer_workers_[l + 1]) dest_gpus.insert(workers_[wi]->gpu);
+                }
+            }
+            std::vector<int> produced;
+            for (int wi : contributors(l)) {
+                Worker& w = *workers_[wi];
+                WLayer& wl = w.at(l);
+                const int fi = net_.dims[l - 1];
+                GemmDesc& d = wl.d_fwd[j];
+                d.a = Operand{act_buf(w.gpu, l - 1) + off * ld_of(fi), rows, fi, ld_of(fi), false};
+                d.b = Operand{wl.W, wl.u, fi, wl.ldw, false};
+                d.M = rows;
+                d.N = wl.u;
+                d.K = fi;
+                d.epi = EpiParams{};
+                d.epi.mode = EPI_STORE;
+                d.epi.bias = wl.bias;
+                d.epi.relu = net_.acts[l - 1] == 1;
+                d.epi.col0 = wl.lo;
+                d.epi.ldd = ld_of(net_.dims[l]);
+                for (int ord : dest_gpus) {
+                    float* base = (l == L && softmax) ? q_buf(ord) : act_buf(ord, l);
+                    d.epi.dst[d.epi.ndst++] = base + off * d.epi.ldd;
+                }
+                prepare(d, wl.p_fwd[j]);
+                std::vector<int> deps;
+                if (l == 1) {
+                    deps.push_back(begin_op_);
+                } else {
+                    auto it = act_ready[l - 1][j].find(w.gpu);
+                    if (it != act_ready[l - 1][j].end()) deps.insert(deps.end(), it->second.begin(), it->second.end());
+                }
+                if (l == w.layers.front().layer && cfg_.gate > 0 && j - cfg_.gate >= 0 &&
+                    w.last_bwd[j - cfg_.gate] >= 0)
+                    deps.push_back(w.last_bwd[j - cfg_.gate]);  // schedule.cpp:293-296
+                const int op = add_op(w.gpu, w.sf, gemm_launch(&wl.p_fwd[j], &wl.d_fwd[j], w.sf), deps, 1);
+                wl.fwd_op[j] = op;
+                produced.push_back(op);
+            }
+            for (int ord : dest_gpus) act_ready[l][j][ord] = produced;
+            if (l < L && boundary_concat) {
+                // concat_repartition: gather at the hub, then broadcast the full
+                // activation to the other consumer GPUs (:258-271, :357-362)
+                std::set<int> consumers;
+                for (int wi : layer_workers_[l + 1]) consumers.insert(workers_[wi]->gpu);
+                Gpu& hub = gpu_of(hub_gpu);
+                const long long ld = ld_of(net_.dims[l]);
+                for (int ord : consumers) {
+                    if (ord == hub_gpu) continue;
+                    float* src = act_buf(hub_gpu, l) + off * ld;
+                    float* dst = act_buf(ord, l) + off * ld;
+                    const size_t bytes = sizeof(float) * rows * ld;
+                    const int src_dev = hub_gpu, dst_dev = ord;
+                    cudaStream_t s = hub.main;
+                    const int op = add_op(hub_gpu, s, [=]() { return cudaMemcpyPeerAsync(dst, dst_dev, src, src_dev, bytes, s); },
+                                          produced, 0);
+                    act_ready[l][j][ord] = {op};
+                }
+            }
+        }
+        // loss head on every GPU holding last-module workers
+        std::set<int> head_gpus;
+        for (int wi : layer_workers_[L]) head_gpus.insert(workers_[wi]->gpu);
+        for (int ord : head_gpus) {
+            Gpu& g = gpu_of(ord);
+            LossTargets t;
+            for (int wi : layer_workers_[L]) {
+                Worker& w = *workers_[wi];
+                if (w.gpu != ord) continue;
+                WLayer& wl = w.at(L);
+                t.lo[t.n] = wl.lo;
+                t.hi[t.n] = wl.hi;
+                t.delta[t.n] = wl.delta + off * wl.ldd;
+                t.ld[t.n] = wl.ldd;
+                ++t.n;
+            }
+            const float* in = (softmax ? g.q : act_buf(ord, L)) + off * ld_of(F);
+            const long long ldin = ld_of(F);
+            const bool write = ord == main_gpu_;
+            double* lr = write ? g.loss_row + off : nullptr;
+            int* cr = write ? g.correct_row + off : nullptr;
+            const int* lab = g.labels + off;
+            const int kind = cfg_.loss;
+            const int relu_last = net_.acts[L - 1] == 1;
+            cudaStream_t s = g.main;
+            const int op = add_op(ord, s, [=]() {
+                return launch_loss_head(in, ldin, rows, F, lab, kind, relu_last, t, lr, cr, s);
+            }, act_ready[L][j][ord], 1);
+            loss_ops[j].push_back(op);
+            for (int wi : layer_workers_[L]) {
+                Worker& w = *workers_[wi];
+                if (w.gpu == ord) w.at(L).delta_ready[j] = {op};
+            }
+        }
+    };
+
+    // ---------------- backward of micro-batch j (train_partitioned.cpp:422-630)
+    auto backward = [&](int j) {
+        const int rows = mb_sizes_[j];
+        const long long off = mb_off_[j];
+        for (int l = L; l >= 2; --l) {
+            const std::vector<int> contrib = contributors(l);
+            const std::vector<int>& dests = layer_workers_[l - 1];
+            const int fi = net_.dims[l - 1];
+            const bool relu_below = net_.acts[l - 2] == 1;
+            const bool single = contrib.size() == 1;
+            std::vector<int> dgrad_ops;
+            for (size_t k = 0; k < contrib.size(); ++k) {
+                Worker& w = *workers_[contrib[k]];
+                WLayer& wl = w.at(l);
+                GemmDesc& d = wl.d_dgrad[j];
+                d.a = Operand{wl.delta + off * wl.ldd, rows, wl.u, wl.ldd, false};
+                d.b = Operand{wl.W, wl.u, fi, wl.ldw, true};
+                d.M = rows;
+                d.N = fi;
+                d.K = wl.u;
+                d.epi = EpiParams{};
+                d.epi.mode = EPI_SLOTS;
+                for (int di : dests) {
+                    Worker& dw = *workers_[di];
+                    WLayer& dl = dw.at(l - 1);
+                    const int s = d.epi.nseg++;
+                    d.epi.seg_lo[s] = dl.lo;
+                    d.epi.seg_hi[s] = dl.hi;
+                    d.epi.seg_ld[s] = dl.ldd;
+                    if (single) {
+                        d.epi.seg_dst[s] = dl.delta + off * dl.ldd;
+                        if (relu_below) {
+                            d.epi.seg_mask[s] = act_buf(dw.gpu, l - 1) + off * ld_of(fi);
+                            d.epi.seg_mask_ld[s] = ld_of(fi);
+                        }
+                    } else {
+                        d.epi.seg_dst[s] = dl.slots[k] + off * dl.ldd;
+                    }
+                }
+                prepare(d, wl.p_dgrad[j]);
+                const int op = add_op(w.gpu, w.sb, gemm_launch(&wl.p_dgrad[j], &wl.d_dgrad[j], w.sb),
+                                      wl.delta_ready[j], 1);
+                wl.dgrad_op[j] = op;
+                w.last_bwd[j] = std::max(w.last_bwd[j], op);
+                dgrad_ops.push_back(op);
+            }
+            for (int di : dests) {
+                Worker& dw = *workers_[di];
+                WLayer& dl = dw.at(l - 1);
+                if (single) {
+                    dl.delta_ready[j] = dgrad_ops;
+                    dw.last_bwd[j] = std::max(dw.last_bwd[j], dgrad_ops.front());
+                    continue;
+                }
+                ReduceSlots rs;
+                for (float* sp : dl.slots) rs.slot[rs.n++] = sp + off * dl.ldd;
+                const float* mask = relu_below ? act_buf(dw.gpu, l - 1) + off * ld_of(fi) + dl.lo : nullptr;
+                const long long ldm = ld_of(fi);
+                float* out = dl.delta + off * dl.ldd;
+                const long long ldd = dl.ldd;
+                const int u = dl.u;
+                cudaStream_t s = dw.sb;
+                const int op = add_op(dw.gpu, s, [=]() {
+                    return launch_reduce_mask(rs, ldd, rows, u, mask, ldm, out, ldd, s);
+                }, dgrad_ops, 1);
+                dl.delta_ready[j] = {op};
+                dw.last_bwd[j] = std::max(dw.last_bwd[j], op);
+            }
+        }
+        // module-1 / layer-1 workers: their backward ends when delta_1 is ready
+        for (int wi : layer_workers_[1])
+            for (int op : workers_[wi]->at(1).delta_ready[j])
+                workers_[wi]->last_bwd[j] = std::max(workers_[wi]->last_bwd[j], op);
+    };
+
+    // interleave creation so every dependency already exists: F(1..gate), then
+    // B(j-gate) before F(j) (the pipelined order, schedule.cpp:254-329)
+    const int gate = cfg_.gate > 0 ? cfg_.gate : m;
+    for (int k = 0; k < m + gate; ++k) {
+        if (k - gate >= 0 && k - gate < m) backward(k - gate);
+        if (k < m) forward(k);
+    }
+
+    // ---------------- updates (train_partitioned.cpp:632-651)
+    int bwd_join = -1;
+    if (cfg_.mode == 1) {
+        std::vector<int> all;
+        for (auto& wp : workers_)
+            for (WLayer& wl : wp->layers) {
+                for (int j = 0; j < m; ++j) {
+                    all.insert(all.end(), wl.delta_ready[j].begin(), wl.delta_ready[j].end());
+                    if (wl.dgrad_op[j] >= 0) all.push_back(wl.dgrad_op[j]);
+                }
+            }
+        bwd_join = add_op(g0.ordinal, g0.main, nullptr, all, 0);  // std::barrier (:633)
+    }
+    const float inv_b = 1.f / static_cast<float>(cfg_.batch);
+    for (auto& wp : workers_) {
+        Worker& w = *wp;
+        Gpu& g = gpu_of(w.gpu);
+        for (WLayer& wl : w.layers) {
+            const int l = wl.layer;
+            const int fi = net_.dims[l - 1];
+            GemmDesc& d = wl.d_wgrad;
+            d.a = Operand{wl.delta, cfg_.batch, wl.u, wl.ldd, true};
+            d.b = Operand{act_buf(w.gpu, l - 1), cfg_.batch, fi, ld_of(fi), true};
+            d.M = wl.u;
+            d.N = fi;
+            d.K = cfg_.batch;
+            d.epi = EpiParams{};
+            d.epi.mode = EPI_SGD;
+            d.epi.W = wl.W;
+            d.epi.ldw = wl.ldw;
+            d.epi.alpha = &g.st->alpha;
+            d.epi.inv_b = inv_b;
+            d.epi.flag = &g.st->diverge_flag;
+            prepare(d, wl.p_wgrad);
+            std::vector<int> deps;
+            for (int j = 0; j < m; ++j) {
+                deps.insert(deps.end(), wl.delta_ready[j].begin(), wl.delta_ready[j].end());
+                if (wl.dgrad_op[j] >= 0) deps.push_back(wl.dgrad_op[j]);
+            }
+            if (bwd_join >= 0) deps.push_back(bwd_join);
+            cudaStream_t s = w.su;
+            const float* delta = wl.delta;
+            const long long ldd = wl.ldd;
+            const int b = cfg_.batch, u = wl.u;
+            float* partial = wl.partial;
+            float* bias = wl.bias;
+            const double* alpha = &g.st->alpha;
+            auto wg = gemm_launch(&wl.p_wgrad, &wl.d_wgrad, s);
+            add_op(w.gpu, s, [=]() {
+                cudaError_t e = launch_bias_update(delta, ldd, b, u, partial, bias, alpha, inv_b, s);
+                if (e != cudaSuccess) return e;
+                return wg();
+            }, deps, 3);
+        }
+    }
+
+    // ---------------- finalize per GPU, then the iteration join
+    std::vector<int> finals;
+    for (auto& gp : gpus_) {
+        Gpu& g = *gp;
+        std::map<cudaStream_t, int> last;
+        for (int i = 0; i < static_cast<int>(ops_.size()); ++i)
+            if (ops_[i].gpu == g.ordinal) last[ops_[i].stream] = i;
+        std::vector<int> deps;
+        for (auto& kv : last) deps.push_back(kv.second);
+        StepState* st = g.st;
+        const double* lr = g.loss_row;
+        const int* cr = g.correct_row;
+        double* lh = g.loss_hist;
+        double* ah = g.acc_hist;
+        const int b = cfg_.batch, cap = hist_cap_;
+        const int write = g.ordinal == main_gpu_;
+        cudaStream_t s = g.main;
+        finals.push_back(add_op(g.ordinal, s, [=]() {
+            return launch_finalize(st, lr, cr, b, lh, ah, cap, write, s);
+        }, deps, 1));
+    }
+    {
+        std::map<cudaStream_t, int> last;
+        for (int i = 0; i < static_cast<int>(ops_.size()); ++i) last[ops_[i].stream] = i;
+        std::vector<int> deps = finals;
+        for (auto& kv : last) deps.push_back(kv.second);
+        end_op_ = add_op(g0.ordinal, g0.main, nullptr, deps, 0);
+    }
+    kernels_per_step_ = 0;
+    for (const Op& op : ops_) kernels_per_step_ += op.kernels;
+    (void)F;
+}
+
+void Session::enqueue_iteration() {
+    std::set<cudaStream_t> joined;
+    for (int i = 0; i < static_cast<int>(ops_.size()); ++i) {
+        Op& op = ops_[i];
+        check(cudaSetDevice(op.gpu), "cudaSetDevice");
+        if (i != begin_op_ && !joined.count(op.stream) && op.stream != ops_[begin_op_].stream)
+            check(cudaStreamWaitEvent(op.stream, ops_[begin_op_].ev, 0), "fork");
+        joined.insert(op.stream);
+        for (int d : op.deps)
+            if (ops_[d].stream != op.stream) check(cudaStreamWaitEvent(op.stream, ops_[d].ev, 0), "wait");
+        if (op.launch) check(op.launch(), "kernel launch");
+        check(cudaEventRecord(op.ev, op.stream), "record");
+    }
+}
+
+void Session::capture_graph() {
+    Gpu& g0 = *gpus_[0];
+    check(cudaSetDevice(g0.ordinal), "cudaSetDevice");
+    if (cudaStreamBeginCapture(g0.main, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    bool ok = true;
+    try {
+        enqueue_iteration();
+    } catch (...) {
+        ok = false;
+    }
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(g0.main, &graph);
+    if (!ok || e != cudaSuccess || graph == nullptr) {
+        cudaGetLastError();
+        if (graph) cudaGraphDestroy(graph);
+        return;
+    }
+    if (cudaGraphInstantiate(&graph_exec_, graph, 0) != cudaSuccess) {
+        cudaGetLastError();
+        cudaGraphDestroy(graph);
+        graph_exec_ = nullptr;
+        return;
+    }
+    graph_ = graph;
+    graph_ok_ = true;
+}
+
+// ------------------------------------------------------------------ runtime
+
+void Session::validate_labels(const int* labels) const {
+    const int L = net_.L();
+    const int F = net_.dims[L];
+    for (int i = 0; i < cfg_.batch; ++i) {
+        const int y = labels[i];
+        if (cfg_.loss == 1 && (y < 0 || y >= F)) throw std::invalid_argument("label out of range");
+        if (cfg_.loss == 0 && F > 1 && (y < 0 || y >= F))
+            throw std::invalid_argument("label out of range for one-hot target");
+    }
+}
+
+void Session::load_batch(const double* X64, const float* X32, const int* labels) {
+    validate_labels(labels);
+    // accuracy() accepts binary labels only (tinynet.cpp:376-378); the
+    // reference raises it from the history collector after the workers
+    // finished, so it is reported by sync() after any divergence error.
+    pending_acc_error_ = false;
+    if (!cfg_.multiclass)
+        for (int i = 0; i < cfg_.batch; ++i)
+            if (labels[i] != 0 && labels[i] != 1) pending_acc_error_ = true;
+    const int I0 = net_.dims[0];
+    const int b = cfg_.batch;
+    Gpu& g0 = *gpus_[0];
+    for (auto& gp : gpus_) {
+        Gpu& g = *gp;
+        check(cudaSetDevice(g.ordinal), "cudaSetDevice");
+        if (g.ordinal != g0.ordinal) check(cudaStreamWaitEvent(g.main, g0.ev_done, 0), "wait");
+        if (g.needs_x) {
+            float* x = g.act.at(0);
+            if (X64 != nullptr) {
+                check(cudaMemcpyAsync(g.xstage, X64, sizeof(double) * b * I0, cudaMemcpyHostToDevice, g.main), "H2D X");
+                check(launch_convert_f64(g.xstage, b, I0, x, ld_of(I0), g.main), "convert X");
+            } else {
+                check(cudaMemcpy2DAsync(x, sizeof(float) * ld_of(I0), X32, sizeof(float) * I0, sizeof(float) * I0, b,
+                                        cudaMemcpyHostToDevice, g.main), "H2D X");
+            }
+        }
+        if (g.needs_labels)
+            check(cudaMemcpyAsync(g.labels, labels, sizeof(int) * b, cudaMemcpyHostToDevice, g.main), "H2D labels");
+        check(cudaEventRecord(g.ev_loaded, g.main), "record");
+        if (g.ordinal != g0.ordinal) {
+            check(cudaSetDevice(g0.ordinal), "cudaSetDevice");
+            check(cudaStreamWaitEvent(g0.main, g.ev_loaded, 0), "wait");
+        }
+    }
+}
+
+void Session::step(int iterations) {
+    Gpu& g0 = *gpus_[0];
+    for (int it = 0; it < iterations; ++it) {
+        if (graph_ok_) {
+            check(cudaSetDevice(g0.ordinal), "cudaSetDevice");
+            check(cudaGraphLaunch(graph_exec_, g0.main), "graph launch");
+        } else {
+            enqueue_iteration();
+        }
+        ++steps_enqueued_;
+    }
+    check(cudaSetDevice(g0.ordinal), "cudaSetDevice");
+    check(cudaEventRecord(g0.ev_done, g0.main), "record");
+}
+
+void Session::sync() {
+    Gpu& g0 = *gpus_[0];
+    check(cudaSetDevice(g0.ordinal), "cudaSetDevice");
+    // watchdog in the spirit of the reference's receive deadline (:46-61)
+    const auto deadline = std::chrono::steady_clock::now() +
+                          std::chrono::duration<double>(cfg_.timeout_s * std::max(1, steps_enqueued_));
+    while (true) {
+        cudaError_t e = cudaEventQuery(g0.ev_done);
+        if (e == cudaSuccess) break;
+        if (e != cudaErrorNotReady) cuda_fail(e, "step");
+        if (std::chrono::steady_clock::now() > deadline)
+            throw std::runtime_error("handoff deadlock: timed out waiting for step " + S(steps_enqueued_));
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+    int first_bad = 0;
+    for (auto& gp : gpus_) {
+        check(cudaSetDevice(gp->ordinal), "cudaSetDevice");
+        check(cudaDeviceSynchronize(), "step");
+        StepState st;
+        check(cudaMemcpy(&st, gp->st, sizeof(st), cudaMemcpyDeviceToHost), "D2H state");
+        if (st.diverged_first && (first_bad == 0 || st.diverged_first < first_bad)) first_bad = st.diverged_first;
+    }
+    if (first_bad) throw std::runtime_error("diverged at iteration " + S(first_bad));
+    if (pending_acc_error_ && steps_enqueued_ > 0) throw std::invalid_argument("accuracy expects binary labels");
+}
+
+void Session::history(double* loss, double* acc, int cap, int* count) {
+    sync();
+    Gpu& g = gpu_of(main_gpu_);
+    const int n = std::min(steps_enqueued_, hist_cap_);
+    const int first = steps_enqueued_ - n;
+    std::vector<double> lh(hist_cap_), ah(hist_cap_);
+    check(cudaSetDevice(g.ordinal), "cudaSetDevice");
+    check(cudaMemcpy(lh.data(), g.loss_hist, sizeof(double) * hist_cap_, cudaMemcpyDeviceToHost), "D2H hist");
+    check(cudaMemcpy(ah.data(), g.acc_hist, sizeof(double) * hist_cap_, cudaMemcpyDeviceToHost), "D2H hist");
+    const int k = std::min(n, cap);
+    for (int i = 0; i < k; ++i) {
+        if (loss) loss[i] = lh[(first + i) % hist_cap_];
+        if (acc) acc[i] = ah[(first + i) % hist_cap_];
+    }
+    if (count) *count = n;
+}
+
+double Session::last_loss() {
+    if (steps_enqueued_ == 0) return 0.0;
+    Gpu& g = gpu_of(main_gpu_);
+    double v = 0.0;
+    check(cudaSetDevice(gpus_[0]->ordinal), "cudaSetDevice");
+    check(cudaEventSynchronize(gpus_[0]->ev_done), "sync");
+    check(cudaSetDevice(g.ordinal), "cudaSetDevice");
+    check(cudaMemcpy(&v, g.loss_hist + (steps_enqueued_ - 1) % hist_cap_, sizeof(double), cudaMemcpyDeviceToHost),
+          "D2H loss");
+    return v;
+}
+
+void Session::get_net(double* W, double* b) {
+    sync();
+    const int L = net_.L();
+    size_t wo = 0, bo = 0;
+    std::vector<float> tmp;
+    for (int l = 1; l <= L; ++l) {
+        const int fi = net_.dims[l - 1];
+        for (int wi : layer_workers_[l]) {
+            Worker& w = *workers_[wi];
+            WLayer& wl = w.at(l);
+            if (!wl.contributor) continue;  // replicated: rank 0 copy (:698)
+            tmp.resize(static_cast<size_t>(wl.u) * wl.ldw);
+            check(cudaSetDevice(w.gpu), "cudaSetDevice");
+            check(cudaMemcpy(tmp.data(), wl.W, sizeof(float) * tmp.size(), cudaMemcpyDeviceToHost), "D2H W");
+            for (int r = 0; r < wl.u; ++r)
+                for (int c = 0; c < fi; ++c)
+                    W[wo + static_cast<size_t>(wl.lo + r) * fi + c] = tmp[static_cast<size_t>(r) * wl.ldw + c];
+            std::vector<float> bb(wl.u);
+            check(cudaMemcpy(bb.data(), wl.bias, sizeof(float) * wl.u, cudaMemcpyDeviceToHost), "D2H b");
+            for (int r = 0; r < wl.u; ++r) b[bo + wl.lo + r] = bb[r];
+        }
+        wo += static_cast<size_t>(fi) * net_.dims[l];
+        bo += net_.dims[l];
+    }
+}
+
+size_t Session::read_tensor(int kind, int layer, int device, double* out, size_t cap) {
+    sync();
+    const int L = net_.L();
+    const int b = cfg_.batch;
+    if (layer < 1 || layer > L) throw std::out_of_range("layer " + S(layer) + " out of range");
+    std::vector<float> tmp;
+    auto fetch = [&](const float* p, int ord, int rows, int cols, long long ld) {
+        tmp.resize(static_cast<size_t>(rows) * ld);
+        check(cudaSetDevice(ord), "cudaSetDevice");
+        check(cudaMemcpy(tmp.data(), p, sizeof(float) * tmp.size(), cudaMemcpyDeviceToHost), "D2H tensor");
+        const size_t n = static_cast<size_t>(rows) * cols;
+        if (out != nullptr) {
+            if (cap < n) throw std::length_error("tensor buffer too small");
+            for (int r = 0; r < rows; ++r)
+                for (int c = 0; c < cols; ++c) out[static_cast<size_t>(r) * cols + c] = tmp[static_cast<size_t>(r) * ld + c];
+        }
+        return n;
+    };
+    const int F = net_.dims[layer];
+    const bool softmax_head = layer == L && net_.acts[L - 1] == 2;
+    if (kind == 0 || kind == 1) {
+        if (kind == 1 && !softmax_head) throw std::invalid_argument("pre-activation is kept only for the softmax head");
+        if (softmax_head) {
+            int ord = workers_[layer_workers_[L].front()]->gpu;
+            size_t n = fetch(q_buf(ord), ord, b, F, ld_of(F));
+            if (kind == 0 && out != nullptr) {
+                for (int r = 0; r < b; ++r) {
+                    double* row = out + static_cast<size_t>(r) * F;
+                    double mx = row[0];
+                    for (int c = 1; c < F; ++c) mx = std::max(mx, row[c]);
+                    double s = 0.0;
+                    for (int c = 0; c < F; ++c) s += (row[c] = std::exp(row[c] - mx));
+                    for (int c = 0; c < F; ++c) row[c] /= s;
+                }
+            }
+            return n;
+        }
+        for (auto& gp : gpus_) {
+            auto it = gp->act.find(layer);
+            if (it != gp->act.end()) return fetch(it->second, gp->ordinal, b, F, ld_of(F));
+        }
+        throw std::runtime_error("internal: activation not resident");
+    }
+    if (kind == 2) {
+        for (int wi : layer_workers_[layer]) {
+            Worker& w = *workers_[wi];
+            if (w.device != device) continue;
+            WLayer& wl = w.at(layer);
+            return fetch(wl.delta, w.gpu, b, wl.u, wl.ldd);
+        }
+        throw std::out_of_range("device " + S(device) + " holds no shard of layer " + S(layer));
+    }
+    throw std::invalid_argument("unknown tensor kind " + S(kind));
+}
+
+}  // namespace ppb

@@ -1,0 +1,112 @@
+// The partitioned training step on B200s: plan -> device-resident shards,
+// merge buffers and an event-ordered DAG of kernels per iteration.
+//
+// Reference: pipeplan::train_partitioned (src/train_partitioned.cpp:121-709).
+// One reference worker thread per (sub-module, device) becomes a `Worker`
+// with its own forward / backward / update CUDA streams; the Mailbox keys
+// (kind, layer, micro-batch, iteration, src) become DAG edges (CUDA events),
+// and the value-copy messages become writes into peer-visible merge buffers
+// fused into the producing GEMM's epilogue.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <functional>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "gemm_tc.h"
+#include "kernels.h"
+#include "planner.h"
+
+namespace ppb {
+
+struct NetDesc {
+    std::vector<int> dims;  // L+1
+    std::vector<int> acts;  // L (0 identity, 1 relu, 2 softmax_last)
+    int L() const { return static_cast<int>(acts.size()); }
+};
+
+struct SessionConfig {
+    double alpha0 = 1e-4;
+    double decay = 1e-2;
+    int loss = 1;  // 0 mse, 1 cross entropy
+    int batch = 0;
+    int m = 1;
+    int mode = 1;  // 1 sync_barrier, 2 async_per_module
+    double timeout_s = 30.0;
+    int precision = 0;  // 0 tf32 tcgen05, 1 fp32 SIMT
+    int multiclass = 0;
+    int use_graph = 1;
+    int gate = 2;
+};
+
+class Session {
+  public:
+    Session(const std::vector<int>& device_map, const NetDesc& net, const double* W,
+            const double* b, const Plan& plan, const SessionConfig& cfg);
+    ~Session();
+
+    void load_batch(const double* X64, const float* X32, const int* labels);
+    void step(int iterations);
+    void sync();  // throws on divergence / CUDA error / watchdog
+    int steps_done() const { return steps_enqueued_; }
+    void history(double* loss, double* acc, int cap, int* count);
+    void get_net(double* W, double* b);
+    size_t read_tensor(int kind, int layer, int device, double* out, size_t cap);
+    int kernels_per_step() const { return kernels_per_step_; }
+    double last_loss();
+
+  private:
+    struct Gpu;
+    struct Worker;
+    struct WLayer;
+    struct Op {
+        int gpu = 0;
+        cudaStream_t stream = nullptr;
+        std::function<cudaError_t()> launch;  // may be empty (pure sync node)
+        std::vector<int> deps;
+        cudaEvent_t ev = nullptr;
+        int kernels = 0;
+    };
+
+    void build();
+    void alloc_buffers();
+    void build_ops();
+    int add_op(int gpu, cudaStream_t s, std::function<cudaError_t()> f, std::vector<int> deps,
+               int kernels);
+    void enqueue_iteration();
+    void capture_graph();
+    Gpu& gpu_of(int ordinal);
+    float* act_buf(int ordinal, int layer);  // full activation a_layer on that GPU (layer 0 = X)
+    float* q_buf(int ordinal);               // gathered pre-activation of the softmax head
+    long long ld_of(int cols) const { return (cols + 3) / 4 * 4; }
+    void check(cudaError_t e, const char* what);
+    void validate_labels(const int* labels) const;
+
+    NetDesc net_;
+    Plan plan_;
+    SessionConfig cfg_;
+    std::vector<int> device_map_;
+    std::vector<int> mb_sizes_, mb_off_;
+    std::vector<std::unique_ptr<Gpu>> gpus_;
+    std::vector<std::unique_ptr<Worker>> workers_;
+    std::vector<std::vector<int>> layer_workers_;  // layer (1-based) -> worker indices (rank order)
+    std::vector<Op> ops_;
+    int begin_op_ = -1;
+    int end_op_ = -1;
+    int main_gpu_ = 0;  // ordinal holding the loss / history (rank 0 of the last module)
+    cudaGraphExec_t graph_exec_ = nullptr;
+    cudaGraph_t graph_ = nullptr;
+    bool graph_ok_ = false;
+    int steps_enqueued_ = 0;
+    int hist_cap_ = 0;
+    int kernels_per_step_ = 0;
+    std::vector<const double*> host_W_, host_b_;
+    bool pending_acc_error_ = false;
+};
+
+}  // namespace ppb

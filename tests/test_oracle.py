@@ -1,0 +1,161 @@
+"""The oracle (oracle/pipeplan_oracle.c) pinned against the reference.
+
+* bit-exact against every golden vector generated from the compiled
+  reference (tests/golden/make_golden.py),
+* the SPEC.md known-answer examples,
+* and, when oracle/_ref is built here, directly against the reference on
+  fresh random instances.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from _util import golden, oracle, reference_or_none
+
+
+@pytest.fixture(scope="module")
+def O():
+    return oracle()
+
+
+def test_split_layer_golden(O):
+    for e in golden()["split_layer"]:
+        if "error" in e:
+            with pytest.raises(Exception) as ei:
+                O.split_layer(e["fan_out"], e["n"], e["replicate"], 3)
+            assert str(ei.value) == e["error"]
+        else:
+            assert [list(s) for s in O.split_layer(e["fan_out"], e["n"], e["replicate"], 3)] == e["shards"]
+
+
+def test_split_microbatches_golden(O):
+    for e in golden()["split_microbatches"]:
+        if "error" in e:
+            with pytest.raises(Exception) as ei:
+                O.split_microbatches(e["b"], e["m"])
+            assert str(ei.value) == e["error"]
+        else:
+            assert O.split_microbatches(e["b"], e["m"]) == e["sizes"]
+
+
+def test_build_plan_golden(O):
+    n = 0
+    for e in golden()["build_plan"]:
+        if "error" in e:
+            with pytest.raises(Exception) as ei:
+                O.build_plan(e["dims"], e["n"], e["Z"], e["replicate"])
+            assert str(ei.value) == e["error"]
+            continue
+        p = O.build_plan(e["dims"], e["n"], e["Z"], e["replicate"])
+        assert p.tolist() == e["plan"]
+        if "merged_1_2" in e:
+            assert O.merge_submodules(p, [1, 2]).tolist() == e["merged_1_2"]
+            assert O.merge_submodules(p, list(range(1, e["Z"] + 1))).tolist() == e["merged_all"]
+        n += 1
+    assert n > 100
+
+
+def test_build_staged_plan_golden(O):
+    for e in golden()["build_staged_plan"]:
+        assert O.build_staged_plan(e["dims"], e["groups"]).tolist() == e["plan"]
+
+
+def _run(O, e, which):
+    args = (e["dims"], e["acts"], np.array(e["W"]), np.array(e["b"]), np.array(e["X"]), np.array(e["labels"]))
+    hp = (e["alpha0"], e["decay"], e["loss"], e["iterations"])
+    if which == "sequential":
+        return O.train_sequential(*args, *hp)
+    return O.train_partitioned(*args, np.array(e["plan"]), e["m"], int(which[-1]), *hp)
+
+
+@pytest.mark.parametrize("which", ["partitioned_mode1", "partitioned_mode2", "sequential"])
+def test_verify_instances_bitwise(O, which):
+    """The oracle reproduces the reference's train_partitioned / train_sequential bit for bit."""
+    for e in golden()["verify_instances"]:
+        exp = e[which]
+        if "error" in exp:
+            with pytest.raises(Exception) as ei:
+                _run(O, e, which)
+            assert str(ei.value) == exp["error"]
+            continue
+        W, b, lh, ah = _run(O, e, which)
+        assert W.tolist() == exp["W"]
+        assert b.tolist() == exp["b"]
+        assert lh.tolist() == exp["loss"]
+        assert ah.tolist() == exp["acc"]
+
+
+def test_mlp_config_bitwise(O):
+    import hashlib
+
+    g = golden()["mlp"]
+    W, b = O.init_net(g["dims"], g["init_seed"])
+    X, y = O.make_blobs(*g["blobs"])
+    assert hashlib.sha256(W.tobytes()).hexdigest() == g["W_sha256"]
+    assert hashlib.sha256(b.tobytes()).hexdigest() == g["b_sha256"]
+    assert hashlib.sha256(X.tobytes()).hexdigest() == g["X_sha256"]
+    assert y.tolist() == g["labels"]
+    for run in g["runs"][:3]:
+        Wo, bo, lh, ah = O.train_partitioned(g["dims"], g["acts"], W, b, X, y, np.array(run["plan"]), run["m"],
+                                             run["mode"], run["alpha0"], run["decay"], 1, run["iterations"])
+        assert lh.tolist() == run["loss"]
+        assert ah.tolist() == run["acc"]
+        assert hashlib.sha256(Wo.tobytes()).hexdigest() == run["W_sha256"]
+        assert bo.tolist() == run["b_out"]
+
+
+def test_spec_known_answers(O):
+    """SPEC.md:417-485 examples, on the oracle."""
+    X = np.array([[3.0]])
+    # forward: W=2 identity -> 6; relu W=-1 -> 0
+    assert O.forward([1, 1], [0], np.array([2.0]), np.array([0.0]), X)[0][0, 0] == 6.0
+    assert O.forward([1, 1], [1], np.array([-1.0]), np.array([0.0]), X)[0][0, 0] == 0.0
+    # one train step, mse target 0, alpha 0.01 -> W = 2 - 0.01*18 = 1.82; loss 18
+    W, b, lh, ah = O.train_sequential([1, 1], [0], np.array([2.0]), np.array([0.0]), X, np.array([0]), 0.01, 0.0, 0,
+                                      1)
+    assert W[0] == 2 - 0.01 * 18 and W[0] == 1.8200000000000001
+    assert b[0] == -0.01 * 6
+    assert lh[0] == 18.0
+    # cross entropy of a uniform 2-class prediction = ln 2
+    W, b, lh, _ = O.train_sequential([1, 2], [2], np.array([0.0, 0.0]), np.array([0.0, 0.0]), X, np.array([1]), 0.1,
+                                     0.0, 1, 1)
+    assert abs(lh[0] - math.log(2)) < 1e-15
+    assert O.split_microbatches(7, 2) == [4, 3]
+
+
+def test_binary_accuracy_contract(O):
+    """accuracy() throws on non-binary labels (tinynet.cpp:376-378)."""
+    W, b = O.init_net([4, 6, 3], 5)
+    X, _ = O.make_blobs(6, 4, 1.0, 3)
+    y = np.array([0, 1, 2, 0, 1, 2])
+    with pytest.raises(Exception) as ei:
+        O.train_sequential([4, 6, 3], [1, 2], W, b, X, y, 0.1, 0.01, 1, 2)
+    assert "accuracy expects binary labels" in str(ei.value)
+    O.train_sequential([4, 6, 3], [1, 2], W, b, X, y, 0.1, 0.01, 1, 2, multiclass=True)
+
+
+def test_reference_self_check():
+    assert golden()["run_verification"]["all_pass"]
+
+
+def test_oracle_vs_compiled_reference_random():
+    """Direct comparison when oracle/_ref is available (build container)."""
+    R = reference_or_none()
+    if R is None:
+        pytest.skip("oracle/_ref not built")
+    O = oracle()
+    for k in range(40):
+        d = R.draw_instance(9000 + k)
+        args = (d["dims"], d["acts"], d["W"], d["b"], d["X"], d["labels"], d["plan"], d["m"], 1,
+                d["alpha0"], d["decay"], d["loss"], d["iterations"])
+        try:
+            ref = R.train_partitioned(*args)
+        except Exception as e:  # noqa: BLE001
+            with pytest.raises(Exception) as ei:
+                O.train_partitioned(*args)
+            assert str(ei.value) == str(e)
+            continue
+        got = O.train_partitioned(*args)
+        for a, bb in zip(ref, got):
+            assert np.array_equal(a, bb)

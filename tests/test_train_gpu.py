@@ -1,0 +1,206 @@
+"""Parity of the CUDA partitioned step with the reference (GPU).
+
+Expected values come from the oracle (the C restatement, itself pinned bit
+for bit to the compiled reference by tests/test_oracle.py) and from the
+golden fixtures generated from the reference.
+
+Tolerances (the reference is fp64; the GPU computes in fp32):
+  * PPB_PRECISION_FP32 (CUDA-core fp32 FMA chains):
+        net_distance <= 2e-5, |loss - ref| <= 2e-5 * max(1, |ref|)
+  * PPB_PRECISION_TF32 (tcgen05 kind::tf32, fp32 accumulation; the default):
+        net_distance <= 5e-3, |loss - ref| <= 5e-3 * max(1, |ref|)
+    TF32 keeps 10 explicit mantissa bits of each operand (u = 2^-11); these
+    bounds cover a few iterations of alpha=0.05 training on the verify nets.
+  * integer / layout work (plans, shard offsets, merge layout, micro-batch
+    split) is bit-exact (tests/test_planner.py), and so is everything the GPU
+    path guarantees about itself: sync == async, m-invariance, determinism.
+"""
+import numpy as np
+import pytest
+
+from _util import golden, net_distance, oracle, rel_norm
+from paper_2207_11019_b200 import api
+from paper_2207_11019_b200.api import (Batch, LossKind, PartitionedTrainOptions, PartitionPlan, PipeplanError,
+                                       TinyNet, TrainConfig, UpdateMode)
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32": 2e-5, "tf32": 5e-3}
+
+
+def _net(e):
+    return TinyNet.unpack(e["dims"], e["acts"], np.array(e["W"], np.float64), np.array(e["b"], np.float64))
+
+
+def _cfg(e):
+    return TrainConfig(alpha0=e["alpha0"], decay=e["decay"], loss=LossKind(e["loss"]), iterations=e["iterations"])
+
+
+def _run_instance(e, mode, precision, m=None, **kw):
+    return api.train_partitioned(_net(e), Batch(np.array(e["X"]), np.array(e["labels"])), _cfg(e),
+                                 PartitionPlan.from_flat(e["plan"]), m or e["m"], UpdateMode(mode),
+                                 PartitionedTrainOptions(precision=precision, **kw))
+
+
+@pytest.mark.parametrize("precision", ["fp32", "tf32"])
+@pytest.mark.parametrize("mode", [1, 2])
+def test_verify_instances_match_reference(precision, mode):
+    """The reference's own run_verification instances (verify.cpp:20-62):
+    n <= 3 devices (all on cuda:0), Z <= L, m <= 4, merged boundaries,
+    replicated narrow layers, mse and cross-entropy."""
+    worst = 0.0
+    for e in golden()["verify_instances"]:
+        exp = e[f"partitioned_mode{mode}"]
+        if "error" in exp:
+            with pytest.raises(Exception) as ei:
+                _run_instance(e, mode, precision)
+            assert str(ei.value) == exp["error"]
+            continue
+        r = _run_instance(e, mode, precision)
+        Wg, bg = r.net.pack()
+        d = net_distance(Wg, bg, np.array(exp["W"]), np.array(exp["b"]))
+        worst = max(worst, d)
+        assert d <= TOL[precision], (e["seed"], d)
+        for got, ref in zip(r.loss_history, exp["loss"]):
+            assert abs(got - ref) <= TOL[precision] * max(1.0, abs(ref)), (e["seed"], got, ref)
+        assert len(r.acc_history) == len(exp["acc"])
+    print(f"worst net_distance {precision} mode{mode}: {worst:.3e}")
+
+
+def test_sync_async_bitwise_and_deterministic():
+    """Mode equivalence holds bitwise on the GPU, and repeated
+    runs are bitwise identical (fixed-shape reductions, no float atomics)."""
+    for e in golden()["verify_instances"][:20]:
+        if "error" in e["partitioned_mode1"]:
+            continue
+        a = _run_instance(e, 1, "tf32")
+        b = _run_instance(e, 2, "tf32")
+        c = _run_instance(e, 1, "tf32")
+        for x, y in [(a, b), (a, c)]:
+            assert np.array_equal(x.net.pack()[0], y.net.pack()[0])
+            assert np.array_equal(x.net.pack()[1], y.net.pack()[1])
+            assert x.loss_history == y.loss_history
+
+
+def test_microbatch_invariance_bitwise():
+    """Micro-batch invariance: on the GPU the wgrad runs once
+    over all b rows, so m changes nothing, bit for bit."""
+    for e in golden()["verify_instances"][:20]:
+        if "error" in e["partitioned_mode1"]:
+            continue
+        base = _run_instance(e, 1, "tf32", m=1)
+        for m in range(2, min(4, len(e["labels"])) + 1):
+            r = _run_instance(e, 1, "tf32", m=m)
+            assert np.array_equal(base.net.pack()[0], r.net.pack()[0])
+            assert base.loss_history == r.loss_history
+
+
+def _mlp():
+    g = golden()["mlp"]
+    O = oracle()
+    W, b = O.init_net(g["dims"], g["init_seed"])
+    X, y = O.make_blobs(*g["blobs"])
+    return g, O, W, b, X, y
+
+
+@pytest.mark.parametrize("precision", ["fp32", "tf32"])
+def test_mlp_config_loss_curve_and_weights(precision):
+    """BASELINE configs[0]: MLP 784-512-512-10, batch 64, n=2 (both plan
+    devices on cuda:0), the reference's plans from the golden file."""
+    g, O, W, b, X, y = _mlp()
+    net = TinyNet.unpack(g["dims"], g["acts"], W, b)
+    for run in g["runs"]:
+        plan = PartitionPlan.from_flat(run["plan"])
+        cfg = TrainConfig(alpha0=run["alpha0"], decay=run["decay"], iterations=run["iterations"])
+        r = api.train_partitioned(net, Batch(X, y), cfg, plan, run["m"], UpdateMode(run["mode"]),
+                                  PartitionedTrainOptions(precision=precision))
+        for got, ref in zip(r.loss_history, run["loss"]):
+            assert abs(got - ref) <= TOL[precision] * max(1.0, abs(ref)), (run, got, ref)
+        Wo, bo, lh, _ = O.train_partitioned(g["dims"], g["acts"], W, b, X, y, np.array(run["plan"]), run["m"],
+                                            run["mode"], run["alpha0"], run["decay"], 1, run["iterations"])
+        assert lh.tolist() == run["loss"]  # the oracle reproduces the golden curve exactly
+        Wg, bg = r.net.pack()
+        assert net_distance(Wg, bg, Wo, bo) <= TOL[precision]
+        assert rel_norm(Wg - W, Wo - W) <= (1e-3 if precision == "fp32" else 2e-2)  # the update itself
+
+
+def test_mlp_per_layer_activations_and_error_signals():
+    """Per-layer outputs and shard error signals against the oracle's forward
+    and a float64 restatement of the backward."""
+    g, O, W, b, X, y = _mlp()
+    net = TinyNet.unpack(g["dims"], g["acts"], W, b)
+    plan = api.build_plan(g["dims"], 2, 1)
+    ctx = api.Context([0, 0])
+    s = api.Session(ctx, net, 64, plan, 2, UpdateMode.sync_barrier, TrainConfig(alpha0=0.0, decay=0.0, iterations=1))
+    s.load_batch(X, y)
+    s.step(1)
+    acts = O.forward(g["dims"], g["acts"], W, b, X)
+    for l in (1, 2, 3):
+        got = s.read_tensor(0, l)
+        assert rel_norm(got, acts[l - 1]) <= 2e-3, l
+    # output delta of the softmax head per shard: p - onehot (train_partitioned.cpp:442-450)
+    p = acts[2]
+    d3 = p.copy()
+    d3[np.arange(64), y] -= 1.0
+    for dev, (lo, hi) in zip((1, 2), ((0, 5), (5, 10))):
+        got = s.read_tensor(2, 3, dev)
+        assert rel_norm(got, d3[:, lo:hi]) <= 5e-3
+    # layer-2 error signal: (d3 . W3) masked by a2 > 0, merged over both shards
+    W3 = W[784 * 512 + 512 * 512:].reshape(10, 512)
+    d2 = (d3 @ W3) * (acts[1] > 0)
+    got = np.concatenate([s.read_tensor(2, 2, 1), s.read_tensor(2, 2, 2)], axis=1)
+    assert rel_norm(got, d2) <= 5e-3
+
+
+def test_divergence_reported_with_iteration():
+    g, O, W, b, X, y = _mlp()
+    net = TinyNet.unpack(g["dims"], g["acts"], W, b)
+    with pytest.raises(PipeplanError, match=r"diverged at iteration \d+"):
+        api.train_partitioned(net, Batch(X * 1e30, y), TrainConfig(alpha0=1e30, iterations=3),
+                              api.build_plan(g["dims"], 2, 1), 1, UpdateMode.sync_barrier)
+
+
+def test_reference_error_contract():
+    g, O, W, b, X, y = _mlp()
+    net = TinyNet.unpack(g["dims"], g["acts"], W, b)
+    cfg = TrainConfig(iterations=1)
+    with pytest.raises(PipeplanError, match="plan/net shape mismatch"):
+        api.train_partitioned(net, Batch(X, y), cfg, api.build_plan([784, 512, 511, 10], 2, 1), 1,
+                              UpdateMode.sync_barrier)
+    with pytest.raises(ValueError, match="needs sync or async"):
+        api.train_partitioned(net, Batch(X, y), cfg, api.build_plan(g["dims"], 2, 1), 1, UpdateMode.none)
+    with pytest.raises(PipeplanError, match="micro-batch smaller than one sample"):
+        api.train_partitioned(net, Batch(X, y), cfg, api.build_plan(g["dims"], 2, 1), 65, UpdateMode.sync_barrier)
+    y10 = np.arange(64) % 10
+    with pytest.raises(ValueError, match="accuracy expects binary labels"):
+        api.train_partitioned(net, Batch(X, y10), cfg, api.build_plan(g["dims"], 2, 1), 1, UpdateMode.sync_barrier)
+    r = api.train_partitioned(net, Batch(X, y10), cfg, api.build_plan(g["dims"], 2, 1), 1, UpdateMode.sync_barrier,
+                              PartitionedTrainOptions(multiclass_accuracy=True))
+    assert np.isfinite(r.loss_history[0])
+
+
+def test_eager_equals_graph():
+    e = next(x for x in golden()["verify_instances"] if "error" not in x["partitioned_mode1"])
+    a = _run_instance(e, 1, "tf32", use_graph=True)
+    b = _run_instance(e, 1, "tf32", use_graph=False)
+    assert np.array_equal(a.net.pack()[0], b.net.pack()[0])
+    assert a.loss_history == b.loss_history
+
+
+def test_staged_plan_and_many_logical_devices():
+    """build_staged_plan groups and an 8-way plan, all on one GPU."""
+    O = oracle()
+    dims, acts = [64, 96, 80, 40, 10], [1, 1, 1, 2]
+    W, b = O.init_net(dims, 3)
+    X, y = O.make_blobs(48, 64, 1.0, 5)
+    net = TinyNet.unpack(dims, acts, W, b)
+    cfg = TrainConfig(alpha0=0.05, decay=0.01, iterations=4)
+    for plan in (api.build_staged_plan(dims, [[1, 2], [3, 4, 5]]), api.build_plan(dims, 8, 2),
+                 api.merge_all(api.build_plan(dims, 3, 4))):
+        n_dev = max(d for sm in plan.submodules for d in sm.devices)
+        r = api.train_partitioned(net, Batch(X, y), cfg, plan, 3, UpdateMode.async_per_module,
+                                  PartitionedTrainOptions(precision="fp32"), device_map=[0] * n_dev)
+        Wo, bo, lh, _ = O.train_partitioned(dims, acts, W, b, X, y, plan.to_flat(), 3, 2, 0.05, 0.01, 1, 4)
+        Wg, bg = r.net.pack()
+        assert net_distance(Wg, bg, Wo, bo) <= 2e-5
+        assert np.allclose(r.loss_history, lh, rtol=2e-5, atol=2e-5)
