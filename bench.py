@@ -1,0 +1,344 @@
+"""Benchmark of the partitioned fwd+bwd+update step (BASELINE.json metric:
+"train samples/sec (fwd+bwd+update) at 1/2/4/8 B200; % tensor-core roofline").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload wide_mlp|mlp784]
+                    [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  A "step" is one train_partitioned iteration
+(forward of every shard, merges, backward with the partial-gradient merge,
+SGD update) over one synthetic batch.
+
+* value      : samples/s with the batch resident in HBM, device time of the K
+               timed steps (CUDA events on the launching stream, the step's
+               join point; max over ranks).
+* e2e        : samples/s through the public C ABI (ppb_session_step_host) from
+               pinned host buffers: H2D of X and labels, the step, D2H of the
+               loss, every step, wall clock around K blocking calls.
+* roofline   : the dominant kernel (tcgen05 TF32 shard GEMM), algorithmic
+               FLOPs per launch / average launch time, both measured in this
+               run with CUDA events around every GEMM (ppb_session_profile).
+* cpu_baseline: the UNMODIFIED reference (oracle/_ref, compiled from
+               /root/reference) on a bounded sample, timed on this host.
+
+Multi-GPU: one process drives all N GPUs (the reference's own single-process
+architecture, one plan device per GPU, merges over NVLink peer memory); under
+torchrun every rank joins the barriers and rank 0 drives and reports.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # BASELINE.json configs[4]: the dense chain the reference itself executes,
+    # large enough to be tensor-core bound on one B200.
+    "wide_mlp": dict(dims=[8192] * 5, acts=[1, 1, 1, 2], batch=4096, name="Wide MLP 8192x4 layers, batch 4096"),
+    # BASELINE.json configs[0]: latency-bound (0.2 GFLOP/step); reported, not a roofline target.
+    "mlp784": dict(dims=[784, 512, 512, 10], acts=[1, 1, 2], batch=64, name="MLP 784-512-512-10, batch 64"),
+}
+
+
+def algorithmic_flops(dims, batch):
+    """fwd + wgrad + dgrad (no dgrad for layer 1), 2 FLOPs per MAC."""
+    f = 0.0
+    for l in range(1, len(dims)):
+        mac = dims[l - 1] * dims[l] * batch
+        f += 2 * mac * (3 if l > 1 else 2)
+    return f
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "MEASURED_PEAKS.json"
+    return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", ",".join(str(g) for g in self.gpus)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, ValueError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) < 9:
+                continue
+            for name, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        loaded = sorted(x for x in sm if x > 300) or sorted(sm)
+        return {"sm_mhz": loaded[len(loaded) // 2] if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+        return rank, world, dist
+    return 0, 1, None
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def max_over_ranks(dist, v):
+    if dist is None:
+        return v
+    import torch
+
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ----------------------------------------------------------------- reference arm
+
+def reference_bounded(workload, nthreads, target_s=12.0):
+    """Time the compiled reference's train_partitioned on a bounded sample of
+    the workload on this host: same dims, plan n = nthreads (the reference's
+    only parallelism is one std::thread per (module, device)), Z=1, m=1."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import REF_SO, Reference  # noqa: E402  (test / baseline infrastructure)
+
+    if not os.path.exists(REF_SO):
+        return None, f"{REF_SO} missing (build with make -C oracle ref)"
+    R = Reference()
+    w = WORKLOADS[workload]
+    dims, acts = w["dims"], w["acts"]
+    rng = np.random.default_rng(0)
+    W = np.concatenate([(rng.random(dims[l] * dims[l + 1]) - 0.5) / np.sqrt(dims[l]) for l in range(len(acts))])
+    b = np.concatenate([(rng.random(dims[l + 1]) - 0.5) / np.sqrt(dims[l]) for l in range(len(acts))])
+    n = max(1, min(nthreads, min(dims[1:])))
+    plan = R.build_plan(dims, n, 1)
+    # calibrate: a tiny probe, then size the sample for ~target_s of CPU work
+    per_sample_flops = algorithmic_flops(dims, 1)
+    probe_rows = 2
+    X = rng.standard_normal((probe_rows, dims[0]))
+    y = np.arange(probe_rows) % 2
+    t0 = time.perf_counter()
+    R.train_partitioned(dims, acts, W, b, X, y, plan, 1, 2, 1e-4, 1e-2, 1, 1, timeout_s=3600.0)
+    t_probe = time.perf_counter() - t0
+    rate = per_sample_flops * probe_rows / max(t_probe, 1e-6)
+    rows = int(max(2, min(w["batch"], target_s * rate / per_sample_flops)))
+    X = rng.standard_normal((rows, dims[0]))
+    y = np.arange(rows) % 2  # binary labels: the reference's accuracy() accepts only {0,1}
+    t0 = time.perf_counter()
+    R.train_partitioned(dims, acts, W, b, X, y, plan, 1, 2, 1e-4, 1e-2, 1, 1, timeout_s=3600.0)
+    dt = time.perf_counter() - t0
+    info = {"value": rows / dt, "unit": "samples/s", "cores": n + 1, "kind": "reference",
+            "sample": f"{w['name']}: {rows} samples x 1 iteration, plan n={n} Z=1 m=1 async "
+                      f"({dt:.1f} s; compiled reference oracle/_ref, fp64, {n} worker threads + main)",
+            "seconds": dt}
+    return info, None
+
+
+def run_reference(args, rank, world, dist):
+    if rank != 0:
+        barrier(dist)
+        return
+    nthreads = os.cpu_count() or 1
+    info, err = reference_bounded(args.workload, nthreads, target_s=min(20.0, 6.0 * max(1, args.steps)))
+    w = WORKLOADS[args.workload]
+    if info is None:
+        print(json.dumps({"impl": "reference", "unavailable": err}))
+        barrier(dist)
+        return
+    line = {"impl": "reference", "metric": "train samples/sec (fwd+bwd+update)", "value": info["value"],
+            "unit": "samples/s", "n_gpus": world, "steps": 1, "warmup": 0, "ms_per_step": 1000.0 * info["seconds"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "name": w["name"], "dims": w["dims"], "batch": w["batch"]},
+            "cpu_baseline": info, "e2e": {"value": info["value"], "unit": "samples/s", "h2d_bytes_per_step": 0,
+                                          "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    barrier(dist)
+
+
+# ----------------------------------------------------------------- our arm
+
+def run_ours(args, rank, world, dist):
+    import torch
+
+    from paper_2207_11019_b200 import api
+    from paper_2207_11019_b200.api import PartitionedTrainOptions, TinyNet, TrainConfig, UpdateMode
+
+    n = args.gpus
+    w = WORKLOADS[args.workload]
+    dims, acts, batch = w["dims"], w["acts"], w["batch"]
+    if rank != 0:
+        barrier(dist)  # setup
+        barrier(dist)  # before timing
+        barrier(dist)  # after timing
+        max_over_ranks(dist, 0.0)
+        return
+    rng = np.random.default_rng(1)
+    W = np.concatenate([(rng.random(dims[l] * dims[l + 1], dtype=np.float64) - 0.5) / np.sqrt(dims[l])
+                        for l in range(len(acts))])
+    b = np.concatenate([(rng.random(dims[l + 1]) - 0.5) / np.sqrt(dims[l]) for l in range(len(acts))])
+    net = TinyNet.unpack(dims, acts, W, b)
+    X = rng.standard_normal((batch, dims[0]), dtype=np.float32)
+    y = rng.integers(0, dims[-1], batch).astype(np.int32)
+    plan = api.build_plan(dims, n, 1)  # every layer over all n GPUs (build_plan, partition.cpp:110-121)
+    ctx = api.Context(list(range(n)))
+    cfg = TrainConfig(alpha0=1e-4, decay=1e-2, iterations=1)
+    opts = PartitionedTrainOptions(multiclass_accuracy=True, use_graph=True, pipeline_gate=2)
+    sess = api.Session(ctx, net, batch, plan, args.m, UpdateMode.async_per_module, cfg, opts)
+    sess.load_batch(X, y)
+    barrier(dist)
+    # warm-up
+    sess.step(args.warmup)
+    sess.sync()
+    # per-kernel device times (eager, CUDA events around each launch)
+    prof = sess.profile(1)
+    barrier(dist)
+    with ClockSampler(list(range(n))) as clk:
+        ms = sess.time_steps(args.steps)
+    barrier(dist)
+    ms = max_over_ranks(dist, ms)
+    lh, _ = sess.history()
+    if not np.all(np.isfinite(lh)):
+        raise RuntimeError("non-finite loss in benchmark run")
+    value = batch * args.steps / (ms / 1000.0)
+
+    # ---- end to end through the C ABI with pinned host buffers
+    Xp = torch.empty((batch, dims[0]), dtype=torch.float32, pin_memory=True)
+    Xp.numpy()[:] = X
+    yp = torch.empty(batch, dtype=torch.int32, pin_memory=True)
+    yp.numpy()[:] = y
+    Xn, yn = Xp.numpy(), yp.numpy()
+    e2e_steps = max(1, min(args.steps, 20))
+    sess.step_host(Xn, yn)  # warm
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        sess.step_host(Xn, yn)
+    e2e_s = time.perf_counter() - t0
+    e2e = {"value": batch * e2e_steps / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": int(Xn.nbytes + yn.nbytes),
+           "d2h_bytes_per_step": 8, "steps": e2e_steps}
+
+    # ---- roofline of the dominant kernel
+    peaks, peak_src = measured_peaks()
+    gemm_kinds = ("fwd_gemm", "dgrad_gemm", "wgrad_sgd_gemm")
+    g_ms = sum(prof[k]["ms"] for k in gemm_kinds if k in prof)
+    g_launch = sum(prof[k]["launches"] for k in gemm_kinds if k in prof)
+    g_flops = sum(prof[k]["flops"] for k in gemm_kinds if k in prof)
+    step_ms_eager = sum(v["ms"] for v in prof.values())
+    tf32_peak = peaks["bf16_tflops_sustained"] / 2.0  # TF32 dense rate is half of bf16 on B200
+    achieved = (g_flops / g_launch) / (g_ms / g_launch / 1000.0) / 1e12 if g_ms > 0 else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(args.workload)
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
+                "frac": achieved / tf32_peak, "traffic": traffic,
+                "kernel": "ppb::tc_gemm_kernel (tcgen05.mma kind::tf32, TMA SW128, fused epilogues)",
+                "flops_per_launch": g_flops / max(g_launch, 1), "avg_launch_ms": g_ms / max(g_launch, 1),
+                "launches_per_step": g_launch, "share_of_step": g_ms / step_ms_eager if step_ms_eager else None,
+                "peak_source": f"{peak_src}: bf16_tflops_sustained / 2 (TF32 = half the bf16 tensor rate)",
+                "peak_bf16_burst_measured": peaks.get("bf16_tflops"),
+                "frac_of_bf16_burst": achieved / peaks.get("bf16_tflops", 1612.0),
+                "step_tflops": algorithmic_flops(dims, batch) * args.steps / (ms / 1000.0) / 1e12 / n,
+                "per_kind_ms": {k: round(v["ms"], 4) for k, v in prof.items()}}
+
+    # ---- reference CPU baseline on a bounded sample (rank 0, N=1 only)
+    cpu = None
+    if n == 1 and not args.no_cpu_baseline:
+        cpu, err = reference_bounded(args.workload, os.cpu_count() or 1)
+        if cpu is None:
+            cpu = {"unavailable": err}
+        else:
+            cpu = {k: v for k, v in cpu.items() if k != "seconds"}
+
+    line = {"metric": "train samples/sec (fwd+bwd+update)", "value": value, "unit": "samples/s", "n_gpus": n,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak" if n == 1 else "strong", "vs_baseline": None, "dtype": "tf32",
+            "data": "synthetic (X ~ N(0,1), labels uniform over classes, weights U[-0.5,0.5]/sqrt(fan_in))",
+            "config": {"workload": args.workload, "name": w["name"], "dims": dims, "batch": batch, "global_batch": batch,
+                       "plan": f"build_plan n={n} Z=1, m={args.m}, async_per_module, CUDA graph",
+                       "parallelism": f"layer-wise partition over {n} GPU(s)",
+                       "l2": "inputs larger than L2 (weights 1 GiB + activations 0.5 GiB per step)"
+                       if args.workload == "wide_mlp" else "working set fits L2 (latency-bound config)"},
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
+            "gpu_launches": sess.kernels_per_step() * args.steps,
+            "loss_last": float(lh[-1]) if len(lh) else None}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="wide_mlp", choices=sorted(WORKLOADS))
+    ap.add_argument("--m", type=int, default=1, help="micro-batches per step")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank, world, dist = dist_setup()
+    if world > 1:
+        args.gpus = world
+    if args.impl == "reference":
+        run_reference(args, rank, world, dist)
+    else:
+        run_ours(args, rank, world, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -203,6 +203,18 @@ int ppb_session_read_tensor(ppb_session* s, int kind, int layer, int device, dou
 /* Launch statistics of one step (kernels per step as enqueued). */
 int ppb_session_kernels_per_step(ppb_session* s, int* out);
 
+/* Device time (CUDA events on the launching stream, ms) of `iterations`
+ * steps on the resident batch; blocking. */
+int ppb_session_time_steps(ppb_session* s, int iterations, float* ms_out);
+
+/* Per-op-kind device time: runs `iterations` eager steps with CUDA events
+ * around every kernel and accumulates, per kind (0 sync, 1 forward GEMM,
+ * 2 dgrad GEMM, 3 wgrad+SGD GEMM, 4 loss head, 5 backward merge, 6 bias
+ * update, 7 finalize, 8 peer copy), the milliseconds, launch count and
+ * algorithmic FLOPs.  Arrays hold `nkinds` entries. */
+int ppb_session_profile(ppb_session* s, int iterations, double* ms, int* count, double* flops,
+                        int nkinds);
+
 /* ------------------------------------------------------------------ diagnostics */
 
 /* One shard GEMM on device pointers (kernel unit tests): C = A.B^T with the

@@ -420,6 +420,29 @@ class Session:
         check(_lib.lib().ppb_session_read_tensor(self._h, kind, layer, device, _dp(out), n.value, C.byref(n)))
         return out.reshape(self.batch_size, -1)
 
+    def time_steps(self, iterations: int) -> float:
+        """Device milliseconds of `iterations` steps (CUDA events on the launching stream)."""
+        ms = C.c_float(0)
+        check(_lib.lib().ppb_session_time_steps(self._h, iterations, C.byref(ms)))
+        return ms.value
+
+    OP_KINDS = ("sync", "fwd_gemm", "dgrad_gemm", "wgrad_sgd_gemm", "loss_head", "bwd_merge", "bias_update",
+                "finalize", "peer_copy")
+
+    def profile(self, iterations: int = 1) -> dict:
+        """Per-op-kind device time / launches / FLOPs over `iterations` eager steps."""
+        k = len(self.OP_KINDS)
+        ms, cnt, fl = np.zeros(k), np.zeros(k, np.int32), np.zeros(k)
+        check(_lib.lib().ppb_session_profile(self._h, iterations, _dp(ms), _ip(cnt), _dp(fl), k))
+        return {name: {"ms": float(ms[i]), "launches": int(cnt[i]), "flops": float(fl[i])}
+                for i, name in enumerate(self.OP_KINDS) if cnt[i]}
+
+    def step_host(self, X: np.ndarray, labels: np.ndarray) -> float:
+        """End-to-end step from host buffers (H2D X/labels, step, D2H loss)."""
+        loss = C.c_double(0)
+        check(_lib.lib().ppb_session_step_host(self._h, X.ctypes.data_as(_f), _ip(labels), C.byref(loss)))
+        return loss.value
+
     def kernels_per_step(self) -> int:
         k = C.c_int(0)
         check(_lib.lib().ppb_session_kernels_per_step(self._h, C.byref(k)))

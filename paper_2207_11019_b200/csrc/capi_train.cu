@@ -140,6 +140,15 @@ extern "C" int ppb_session_read_tensor(ppb_session* s, int kind, int layer, int 
     });
 }
 
+extern "C" int ppb_session_time_steps(ppb_session* s, int iterations, float* ms_out) {
+    return ppb_guard([&] { *ms_out = s->s->time_steps(iterations); });
+}
+
+extern "C" int ppb_session_profile(ppb_session* s, int iterations, double* ms, int* count, double* flops,
+                                   int nkinds) {
+    return ppb_guard([&] { s->s->profile(iterations, ms, count, flops, nkinds); });
+}
+
 extern "C" int ppb_session_kernels_per_step(ppb_session* s, int* out) {
     return ppb_guard([&] { *out = s->s->kernels_per_step(); });
 }

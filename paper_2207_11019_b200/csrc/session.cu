@@ -345,8 +345,10 @@ void Session::alloc_buffers() {
 }
 
 int Session::add_op(int gpu, cudaStream_t s, std::function<cudaError_t()> f, std::vector<int> deps,
-                    int kernels) {
+                    int kernels, int kind, double flops) {
     Op op;
+    op.kind = kind;
+    op.flops = flops;
     op.gpu = gpu;
     op.stream = s;
     op.launch = std::move(f);
@@ -456,7 +458,8 @@ void Session::build_ops() {
                 if (l == w.layers.front().layer && cfg_.gate > 0 && j - cfg_.gate >= 0 &&
                     w.last_bwd[j - cfg_.gate] >= 0)
                     deps.push_back(w.last_bwd[j - cfg_.gate]);  // schedule.cpp:293-296
-                const int op = add_op(w.gpu, w.sf, gemm_launch(&wl.p_fwd[j], &wl.d_fwd[j], w.sf), deps, 1);
+                const int op = add_op(w.gpu, w.sf, gemm_launch(&wl.p_fwd[j], &wl.d_fwd[j], w.sf), deps, 1,
+                                      OP_FWD_GEMM, 2.0 * rows * wl.u * fi);
                 wl.fwd_op[j] = op;
                 produced.push_back(op);
             }
@@ -476,7 +479,7 @@ void Session::build_ops() {
                     const int src_dev = hub_gpu, dst_dev = ord;
                     cudaStream_t s = hub.main;
                     const int op = add_op(hub_gpu, s, [=]() { return cudaMemcpyPeerAsync(dst, dst_dev, src, src_dev, bytes, s); },
-                                          produced, 0);
+                                          produced, 0, OP_COPY);
                     act_ready[l][j][ord] = {op};
                 }
             }
@@ -508,7 +511,7 @@ void Session::build_ops() {
             cudaStream_t s = g.main;
             const int op = add_op(ord, s, [=]() {
                 return launch_loss_head(in, ldin, rows, F, lab, kind, relu_last, t, lr, cr, s);
-            }, act_ready[L][j][ord], 1);
+            }, act_ready[L][j][ord], 1, OP_LOSS);
             loss_ops[j].push_back(op);
             for (int wi : layer_workers_[L]) {
                 Worker& w = *workers_[wi];
@@ -558,7 +561,7 @@ void Session::build_ops() {
                 }
                 prepare(d, wl.p_dgrad[j]);
                 const int op = add_op(w.gpu, w.sb, gemm_launch(&wl.p_dgrad[j], &wl.d_dgrad[j], w.sb),
-                                      wl.delta_ready[j], 1);
+                                      wl.delta_ready[j], 1, OP_DGRAD_GEMM, 2.0 * rows * wl.u * fi);
                 wl.dgrad_op[j] = op;
                 w.last_bwd[j] = std::max(w.last_bwd[j], op);
                 dgrad_ops.push_back(op);
@@ -581,7 +584,7 @@ void Session::build_ops() {
                 cudaStream_t s = dw.sb;
                 const int op = add_op(dw.gpu, s, [=]() {
                     return launch_reduce_mask(rs, ldd, rows, u, mask, ldm, out, ldd, s);
-                }, dgrad_ops, 1);
+                }, dgrad_ops, 1, OP_REDUCE);
                 dl.delta_ready[j] = {op};
                 dw.last_bwd[j] = std::max(dw.last_bwd[j], op);
             }
@@ -647,12 +650,11 @@ void Session::build_ops() {
             float* partial = wl.partial;
             float* bias = wl.bias;
             const double* alpha = &g.st->alpha;
-            auto wg = gemm_launch(&wl.p_wgrad, &wl.d_wgrad, s);
-            add_op(w.gpu, s, [=]() {
-                cudaError_t e = launch_bias_update(delta, ldd, b, u, partial, bias, alpha, inv_b, s);
-                if (e != cudaSuccess) return e;
-                return wg();
-            }, deps, 3);
+            const int bop = add_op(w.gpu, s, [=]() {
+                return launch_bias_update(delta, ldd, b, u, partial, bias, alpha, inv_b, s);
+            }, deps, 2, OP_BIAS);
+            add_op(w.gpu, s, gemm_launch(&wl.p_wgrad, &wl.d_wgrad, s), {bop}, 1, OP_WGRAD_GEMM,
+                   2.0 * wl.u * fi * static_cast<double>(cfg_.batch));
         }
     }
 
@@ -675,7 +677,7 @@ void Session::build_ops() {
         cudaStream_t s = g.main;
         finals.push_back(add_op(g.ordinal, s, [=]() {
             return launch_finalize(st, lr, cr, b, lh, ah, cap, write, s);
-        }, deps, 1));
+        }, deps, 1, OP_FINALIZE));
     }
     {
         std::map<cudaStream_t, int> last;
@@ -701,6 +703,80 @@ void Session::enqueue_iteration() {
             if (ops_[d].stream != op.stream) check(cudaStreamWaitEvent(op.stream, ops_[d].ev, 0), "wait");
         if (op.launch) check(op.launch(), "kernel launch");
         check(cudaEventRecord(op.ev, op.stream), "record");
+    }
+}
+
+void Session::enqueue_iteration_timed(std::vector<cudaEvent_t>& t0, std::vector<cudaEvent_t>& t1) {
+    std::set<cudaStream_t> joined;
+    for (int i = 0; i < static_cast<int>(ops_.size()); ++i) {
+        Op& op = ops_[i];
+        check(cudaSetDevice(op.gpu), "cudaSetDevice");
+        if (i != begin_op_ && !joined.count(op.stream) && op.stream != ops_[begin_op_].stream)
+            check(cudaStreamWaitEvent(op.stream, ops_[begin_op_].ev, 0), "fork");
+        joined.insert(op.stream);
+        for (int d : op.deps)
+            if (ops_[d].stream != op.stream) check(cudaStreamWaitEvent(op.stream, ops_[d].ev, 0), "wait");
+        if (op.launch) {
+            check(cudaEventRecord(t0[i], op.stream), "record");
+            check(op.launch(), "kernel launch");
+            check(cudaEventRecord(t1[i], op.stream), "record");
+        }
+        check(cudaEventRecord(op.ev, op.stream), "record");
+    }
+}
+
+float Session::time_steps(int iterations) {
+    Gpu& g0 = *gpus_[0];
+    check(cudaSetDevice(g0.ordinal), "cudaSetDevice");
+    cudaEvent_t a, b;
+    check(cudaEventCreate(&a), "event");
+    check(cudaEventCreate(&b), "event");
+    check(cudaEventRecord(a, g0.main), "record");
+    step(iterations);
+    check(cudaSetDevice(g0.ordinal), "cudaSetDevice");
+    check(cudaEventRecord(b, g0.main), "record");
+    check(cudaEventSynchronize(b), "sync");
+    float ms = 0.f;
+    check(cudaEventElapsedTime(&ms, a, b), "elapsed");
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    sync();
+    return ms;
+}
+
+void Session::profile(int iterations, double* ms, int* count, double* flops, int nkinds) {
+    const int n = static_cast<int>(ops_.size());
+    std::vector<cudaEvent_t> t0(n, nullptr), t1(n, nullptr);
+    for (int i = 0; i < n; ++i) {
+        if (!ops_[i].launch) continue;
+        check(cudaSetDevice(ops_[i].gpu), "cudaSetDevice");
+        check(cudaEventCreate(&t0[i]), "event");
+        check(cudaEventCreate(&t1[i]), "event");
+    }
+    for (int k = 0; k < nkinds; ++k) {
+        ms[k] = 0;
+        count[k] = 0;
+        flops[k] = 0;
+    }
+    for (int it = 0; it < iterations; ++it) {
+        enqueue_iteration_timed(t0, t1);
+        ++steps_enqueued_;
+        Gpu& g0 = *gpus_[0];
+        check(cudaSetDevice(g0.ordinal), "cudaSetDevice");
+        check(cudaEventRecord(g0.ev_done, g0.main), "record");
+        sync();
+        for (int i = 0; i < n; ++i) {
+            if (!ops_[i].launch || ops_[i].kind >= nkinds) continue;
+            float e = 0.f;
+            check(cudaEventElapsedTime(&e, t0[i], t1[i]), "elapsed");
+            ms[ops_[i].kind] += e;
+            count[ops_[i].kind] += 1;
+            flops[ops_[i].kind] += ops_[i].flops;
+        }
+    }
+    for (int i = 0; i < n; ++i) {
+        if (t0[i]) cudaEventDestroy(t0[i]);
+        if (t1[i]) cudaEventDestroy(t1[i]);
     }
 }
 

@@ -30,6 +30,19 @@ struct NetDesc {
     int L() const { return static_cast<int>(acts.size()); }
 };
 
+enum OpKind : int {
+    OP_SYNC = 0,
+    OP_FWD_GEMM = 1,
+    OP_DGRAD_GEMM = 2,
+    OP_WGRAD_GEMM = 3,  // wgrad + fused SGD epilogue
+    OP_LOSS = 4,
+    OP_REDUCE = 5,
+    OP_BIAS = 6,
+    OP_FINALIZE = 7,
+    OP_COPY = 8,
+    OP_NKINDS = 9,
+};
+
 struct SessionConfig {
     double alpha0 = 1e-4;
     double decay = 1e-2;
@@ -58,6 +71,11 @@ class Session {
     void get_net(double* W, double* b);
     size_t read_tensor(int kind, int layer, int device, double* out, size_t cap);
     int kernels_per_step() const { return kernels_per_step_; }
+    // device time of `iterations` steps on the launching stream (CUDA events)
+    float time_steps(int iterations);
+    // one eager iteration per call with per-op CUDA events; accumulates the
+    // device time / launch count / algorithmic FLOPs per OpKind
+    void profile(int iterations, double* ms, int* count, double* flops, int nkinds);
     double last_loss();
 
   private:
@@ -65,6 +83,8 @@ class Session {
     struct Worker;
     struct WLayer;
     struct Op {
+        int kind = 0;       // OpKind
+        double flops = 0;   // algorithmic FLOPs of the op (GEMMs)
         int gpu = 0;
         cudaStream_t stream = nullptr;
         std::function<cudaError_t()> launch;  // may be empty (pure sync node)
@@ -77,7 +97,8 @@ class Session {
     void alloc_buffers();
     void build_ops();
     int add_op(int gpu, cudaStream_t s, std::function<cudaError_t()> f, std::vector<int> deps,
-               int kernels);
+               int kernels, int kind = 0, double flops = 0);
+    void enqueue_iteration_timed(std::vector<cudaEvent_t>& t0, std::vector<cudaEvent_t>& t1);
     void enqueue_iteration();
     void capture_graph();
     Gpu& gpu_of(int ordinal);
