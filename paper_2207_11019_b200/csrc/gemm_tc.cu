@@ -2,16 +2,23 @@
 //
 //   warp 0      : TMA producer (one elected lane), SWIZZLE_128B tiles into a
 //                 kStages-deep shared-memory ring guarded by full/empty mbarriers
-//   warp 1      : MMA issuer (one elected lane): tcgen05.mma.cta_group::1.kind::tf32,
-//                 128 x BN x 8 per instruction, accumulator in TMEM
+//   warp 1      : MMA issuer (one elected lane of the leader CTA):
+//                 tcgen05.mma.cta_group::{1,2}.kind::tf32, accumulator in TMEM
 //   warp 2      : TMEM allocator (2 x BN columns: double-buffered accumulator)
 //   warps 4..7  : epilogue: tcgen05.ld -> registers -> fused epilogue -> global
 //
-// Tiles are BM=128 rows x BN columns, BK=32 fp32 (= one 128-byte swizzle
-// atom for K-major operands).  K-major operands are loaded as one TMA box
-// {32 (K), rows}; MN-major operands as rows/32 boxes {32 (MN), 32 (K)}, each
-// a 4 KB canonical MN-major SW128 atom column.  See gemm.h for how the
-// forward / dgrad / wgrad products of the partitioned step map onto A and B.
+// CG = 1: one CTA computes a 128 x BN tile (UMMA M = 128).
+// CG = 2: a CTA pair (cluster of 2 on one TPC) computes a 256 x BN tile with
+//         UMMA M = 256: each CTA stages its own 128 rows of A and half of the
+//         BN rows of B, so each SM reads half the operand bytes per FLOP; the
+//         leader CTA issues the MMAs for both and its commits multicast to
+//         the pair's barriers.
+//
+// BK = 32 fp32 (one 128-byte swizzle atom for K-major operands).  K-major
+// operands are loaded as one TMA box {32 (K), rows}; MN-major operands as
+// rows/32 boxes {32 (MN), 32 (K)}, each a 4 KB SW128_BASE32B atom column.
+// See gemm.h for how the forward / dgrad / wgrad products of the partitioned
+// step map onto A and B.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -31,14 +38,15 @@ namespace {
 
 std::atomic<unsigned> g_attr_set{0};  // one bit per device: smem attributes set
 
-constexpr int kBM = 128;
+constexpr int kBM = 128;  // rows of A per CTA
 constexpr int kBK = 32;
 constexpr int kThreads = 256;
 
-template <int BN>
+template <int BN, int CG>
 struct TcCfg {
+    static constexpr int kBNc = BN / CG;  // rows of B staged per CTA
     static constexpr int kStageA = kBM * kBK * 4;  // bytes
-    static constexpr int kStageB = BN * kBK * 4;
+    static constexpr int kStageB = kBNc * kBK * 4;
     static constexpr int kStageBytes = kStageA + kStageB;
     static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
     static constexpr int kTmemCols = 2 * BN;
@@ -46,11 +54,11 @@ struct TcCfg {
     static constexpr int kSmem = 1024 + kStages * kStageBytes + 256;
 };
 
-template <bool A_MN, bool B_MN, int BN>
+template <bool A_MN, bool B_MN, int BN, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                    int M, int N, int K, const __grid_constant__ EpiParams epi) {
-    using C = TcCfg<BN>;
+    using C = TcCfg<BN, CG>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
@@ -63,10 +71,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
 
     const int warp = threadIdx.x / 32;
-    const int num_m = (M + kBM - 1) / kBM;
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+    const bool leader = rank == 0;
+    constexpr int TM = kBM * CG;  // tile rows
+    const int num_m = (M + TM - 1) / TM;
     const int num_n = (N + BN - 1) / BN;
     const int num_tiles = num_m * num_n;
     const int nk = (K + kBK - 1) / kBK;
+    const int unit = blockIdx.x / CG;  // cluster (or CTA) index
+    const int units = gridDim.x / CG;
 
     if (warp == 0 && elect_one()) {
         tma_prefetch(&ta);
@@ -77,13 +90,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull_bar[i], 1);
-            mbar_init(&tempty_bar[i], 128);
+            mbar_init(&tempty_bar[i], 4 * CG);  // one arrival per epilogue warp of the pair
         }
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc(tmem_slot, C::kTmemCols);
+    if (warp == 2) {
+        if (CG == 2) tmem_alloc_pair(tmem_slot, C::kTmemCols);
+        else tmem_alloc(tmem_slot, C::kTmemCols);
+    }
     tc_fence_before();
     __syncthreads();
+    if (CG == 2) cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -92,28 +109,48 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                const int m0 = (tile % num_m) * kBM;
-                const int n0 = (tile / num_m) * BN;
+            for (int tile = unit; tile < num_tiles; tile += units) {
+                const int m0 = (tile % num_m) * TM + static_cast<int>(rank) * kBM;
+                const int n0 = (tile / num_m) * BN + static_cast<int>(rank) * C::kBNc;
                 for (int kb = 0; kb < nk; ++kb) {
                     const int k0 = kb * kBK;
                     mbar_wait(&empty_bar[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes);
                     uint8_t* a_dst = sA + stage * C::kStageA;
                     uint8_t* b_dst = sB + stage * C::kStageB;
-                    if (A_MN) {
+                    if (CG == 1) {
+                        mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes);
+                        if (A_MN) {
 #pragma unroll
-                        for (int i = 0; i < kBM / 32; ++i)
-                            tma_load_2d(a_dst + i * 4096, &ta, &full_bar[stage], m0 + 32 * i, k0);
-                    } else {
-                        tma_load_2d(a_dst, &ta, &full_bar[stage], k0, m0);
-                    }
-                    if (B_MN) {
+                            for (int i = 0; i < kBM / 32; ++i)
+                                tma_load_2d(a_dst + i * 4096, &ta, &full_bar[stage], m0 + 32 * i, k0);
+                        } else {
+                            tma_load_2d(a_dst, &ta, &full_bar[stage], k0, m0);
+                        }
+                        if (B_MN) {
 #pragma unroll
-                        for (int i = 0; i < BN / 32; ++i)
-                            tma_load_2d(b_dst + i * 4096, &tb, &full_bar[stage], n0 + 32 * i, k0);
+                            for (int i = 0; i < C::kBNc / 32; ++i)
+                                tma_load_2d(b_dst + i * 4096, &tb, &full_bar[stage], n0 + 32 * i, k0);
+                        } else {
+                            tma_load_2d(b_dst, &tb, &full_bar[stage], k0, n0);
+                        }
                     } else {
-                        tma_load_2d(b_dst, &tb, &full_bar[stage], k0, n0);
+                        // both CTAs' bytes land on the leader's full barrier
+                        const uint32_t bar = mapa_shared(smem_u32(&full_bar[stage]), 0);
+                        if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * C::kStageBytes);
+                        if (A_MN) {
+#pragma unroll
+                            for (int i = 0; i < kBM / 32; ++i)
+                                tma_load_2d_pair(a_dst + i * 4096, &ta, bar, m0 + 32 * i, k0);
+                        } else {
+                            tma_load_2d_pair(a_dst, &ta, bar, k0, m0);
+                        }
+                        if (B_MN) {
+#pragma unroll
+                            for (int i = 0; i < C::kBNc / 32; ++i)
+                                tma_load_2d_pair(b_dst + i * 4096, &tb, bar, n0 + 32 * i, k0);
+                        } else {
+                            tma_load_2d_pair(b_dst, &tb, bar, k0, n0);
+                        }
                     }
                     if (++stage == C::kStages) {
                         stage = 0;
@@ -123,54 +160,62 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------ MMA issuer
-        constexpr uint32_t idesc = idesc_tf32(BN, A_MN, B_MN);
-        int stage = 0;
-        uint32_t phase = 0;
-        int local = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
-            const int acc = local & 1;
-            const uint32_t acc_phase = (local >> 1) & 1;
-            mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
-            tc_fence_after();
-            const uint32_t d_tmem = tmem_base + acc * BN;
-            for (int kb = 0; kb < nk; ++kb) {
-                mbar_wait(&full_bar[stage], phase);
+        // ------------------------------------------------ MMA issuer (leader CTA)
+        if (leader) {
+            constexpr uint32_t idesc = idesc_tf32(BN, A_MN, B_MN, TM);
+            int stage = 0;
+            uint32_t phase = 0;
+            int local = 0;
+            for (int tile = unit; tile < num_tiles; tile += units, ++local) {
+                const int acc = local & 1;
+                const uint32_t acc_phase = (local >> 1) & 1;
+                mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
                 tc_fence_after();
-                if (elect_one()) {
-                    const uint32_t a_addr = smem_u32(sA + stage * C::kStageA);
-                    const uint32_t b_addr = smem_u32(sB + stage * C::kStageB);
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&full_bar[stage], phase);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t a_addr = smem_u32(sA + stage * C::kStageA);
+                        const uint32_t b_addr = smem_u32(sB + stage * C::kStageB);
 #pragma unroll
-                    for (int kk = 0; kk < kBK / 8; ++kk) {
-                        // K-major (SW128): advance 32 B inside the 128 B swizzle
-                        // atom; 8-row groups 1 KB apart (SBO).
-                        // MN-major (SW128_BASE32B): advance 8 K rows (1 KB);
-                        // 4-row K groups 512 B apart (SBO), 32-wide MN atoms
-                        // 4 KB apart (LBO).
-                        const uint64_t ad = A_MN ? umma_desc<kLayoutSW128Base32>(a_addr + kk * 1024, 4096, 512)
-                                                 : umma_desc<kLayoutSW128>(a_addr + kk * 32, 16, 1024);
-                        const uint64_t bd = B_MN ? umma_desc<kLayoutSW128Base32>(b_addr + kk * 1024, 4096, 512)
-                                                 : umma_desc<kLayoutSW128>(b_addr + kk * 32, 16, 1024);
-                        mma_tf32(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                        for (int kk = 0; kk < kBK / 8; ++kk) {
+                            // K-major (SW128): advance 32 B inside the 128 B swizzle
+                            // atom; 8-row groups 1 KB apart (SBO).
+                            // MN-major (SW128_BASE32B): advance 8 K rows (1 KB);
+                            // 4-row K groups 512 B apart (SBO), 32-wide MN atoms
+                            // 4 KB apart (LBO).
+                            const uint64_t ad = A_MN ? umma_desc<kLayoutSW128Base32>(a_addr + kk * 1024, 4096, 512)
+                                                     : umma_desc<kLayoutSW128>(a_addr + kk * 32, 16, 1024);
+                            const uint64_t bd = B_MN ? umma_desc<kLayoutSW128Base32>(b_addr + kk * 1024, 4096, 512)
+                                                     : umma_desc<kLayoutSW128>(b_addr + kk * 32, 16, 1024);
+                            if (CG == 2) mma_tf32_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                            else mma_tf32(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                        }
+                        if (CG == 2) mma_commit_pair(&empty_bar[stage]);
+                        else mma_commit(&empty_bar[stage]);
                     }
-                    mma_commit(&empty_bar[stage]);
+                    __syncwarp();
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                if (elect_one()) {
+                    if (CG == 2) mma_commit_pair(&tfull_bar[acc]);
+                    else mma_commit(&tfull_bar[acc]);
                 }
                 __syncwarp();
-                if (++stage == C::kStages) {
-                    stage = 0;
-                    phase ^= 1;
-                }
             }
-            if (elect_one()) mma_commit(&tfull_bar[acc]);
-            __syncwarp();
         }
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         const int lane = threadIdx.x & 31;
+        const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty_bar[0]), 0) : 0;
         int local = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
-            const int m0 = (tile % num_m) * kBM;
+        for (int tile = unit; tile < num_tiles; tile += units, ++local) {
+            const int m0 = (tile % num_m) * TM + static_cast<int>(rank) * kBM;
             const int n0 = (tile / num_m) * BN;
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
@@ -188,14 +233,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 epilogue32(epi, m, n0 + c * 32, v);
             }
             tc_fence_before();
-            mbar_arrive(&tempty_bar[acc]);
+            __syncwarp();
+            if (lane == 0) {
+                if (CG == 2) mbar_arrive_cluster(tempty_leader + acc * sizeof(uint64_t));
+                else mbar_arrive(&tempty_bar[acc]);
+            }
         }
     }
 
+    tc_fence_before();
     __syncthreads();
+    if (CG == 2) cluster_sync();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, C::kTmemCols);
+        if (CG == 2) tmem_dealloc_pair(tmem_base, C::kTmemCols);
+        else tmem_dealloc(tmem_base, C::kTmemCols);
     }
 }
 
@@ -217,7 +269,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 // Encode a 2-D fp32 map over a row-major (rows x cols, ld) matrix whose
-// innermost (contiguous) dimension is `cols`, box {32, box_rows}, SW128.
+// innermost (contiguous) dimension is `cols`, box {32, box_rows}.
 bool encode_map(CUtensorMap* map, const float* ptr, int rows, int cols, long long ld,
                 int box_rows, bool mn_major, char* err, size_t errlen) {
     auto enc = get_encode();
@@ -246,30 +298,21 @@ bool encode_map(CUtensorMap* map, const float* ptr, int rows, int cols, long lon
     return true;
 }
 
-}  // namespace
-cudaError_t tc_gemm_init_device();
-namespace {
-
-template <bool A_MN, bool B_MN, int BN>
-cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
-    using C = TcCfg<BN>;
-    auto k = tc_gemm_kernel<A_MN, B_MN, BN>;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if ((g_attr_set.load() & (1u << (dev & 31))) == 0) {
-        cudaError_t e = tc_gemm_init_device();
-        if (e != cudaSuccess) return e;
-    }
-    k<<<p.grid, kThreads, C::kSmem, s>>>(p.ta, p.tb, p.M, p.N, p.K, p.epi);
-    return cudaGetLastError();
-}
+template <bool A_MN, bool B_MN, int BN, int CG>
+cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s);
 
 template <bool A_MN, bool B_MN>
 cudaError_t launch_bn(const TcGemmPlan& p, cudaStream_t s) {
+    if (p.cg == 2) {
+        switch (p.bn) {
+            case 128: return launch_t<A_MN, B_MN, 128, 2>(p, s);
+            default: return launch_t<A_MN, B_MN, 256, 2>(p, s);
+        }
+    }
     switch (p.bn) {
-        case 64: return launch_t<A_MN, B_MN, 64>(p, s);
-        case 128: return launch_t<A_MN, B_MN, 128>(p, s);
-        default: return launch_t<A_MN, B_MN, 256>(p, s);
+        case 64: return launch_t<A_MN, B_MN, 64, 1>(p, s);
+        case 128: return launch_t<A_MN, B_MN, 128, 1>(p, s);
+        default: return launch_t<A_MN, B_MN, 256, 1>(p, s);
     }
 }
 
@@ -286,6 +329,58 @@ int sm_count() {
 
 }  // namespace
 
+// Set the dynamic shared-memory limit of every instantiation on the current
+// device (must happen before any launch is captured into a CUDA graph).
+cudaError_t tc_gemm_init_device() {
+    cudaError_t e = cudaSuccess;
+    auto set = [&](auto kernel, int smem) {
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    };
+#define PPB_SET(AM, BM)                                                   \
+    set(tc_gemm_kernel<AM, BM, 64, 1>, TcCfg<64, 1>::kSmem);              \
+    set(tc_gemm_kernel<AM, BM, 128, 1>, TcCfg<128, 1>::kSmem);            \
+    set(tc_gemm_kernel<AM, BM, 256, 1>, TcCfg<256, 1>::kSmem);            \
+    set(tc_gemm_kernel<AM, BM, 128, 2>, TcCfg<128, 2>::kSmem);            \
+    set(tc_gemm_kernel<AM, BM, 256, 2>, TcCfg<256, 2>::kSmem);
+    PPB_SET(false, false)
+    PPB_SET(false, true)
+    PPB_SET(true, false)
+    PPB_SET(true, true)
+#undef PPB_SET
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (e == cudaSuccess) g_attr_set.fetch_or(1u << (dev & 31));
+    return e;
+}
+
+namespace {
+
+template <bool A_MN, bool B_MN, int BN, int CG>
+cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
+    using C = TcCfg<BN, CG>;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if ((g_attr_set.load() & (1u << (dev & 31))) == 0) {
+        cudaError_t e = tc_gemm_init_device();
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(p.grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<A_MN, B_MN, BN, CG>, p.ta, p.tb, p.M, p.N, p.K, p.epi);
+}
+
+}  // namespace
+
 bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err, size_t errlen) {
     TcGemmPlan p;
     p.M = d.M;
@@ -296,48 +391,45 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
     p.epi = d.epi;
     p.epi.M = d.M;
     p.epi.N = d.N;
-    // Tile width: the widest BN that still gives every SM a tile, else 64.
+    if (d.K < 1) {
+        snprintf(err, errlen, "GEMM with K=%d", d.K);
+        return false;
+    }
     const int sms = sm_count();
-    const int num_m = (d.M + kBM - 1) / kBM;
-    int bn = 256;
+    // force_bn: 0 = auto; 64/128/256 = 1-CTA tiles of that width;
+    // -128/-256 = CTA-pair tiles (256 x |bn|).
+    int bn = 256, cg = 1;
     if (force_bn == 64 || force_bn == 128 || force_bn == 256) {
         bn = force_bn;
+    } else if (force_bn == -128 || force_bn == -256) {
+        bn = -force_bn;
+        cg = 2;
     } else {
-        while (bn > 64 && num_m * ((d.N + bn - 1) / bn) < sms) bn /= 2;
+        // CTA pairs whenever the pair tiles still fill every SM pair;
+        // otherwise the widest 1-CTA tile that fills the SMs, down to 64.
+        const int pair_tiles = ((d.M + 255) / 256) * ((d.N + 255) / 256);
+        if (d.M > 128 && pair_tiles >= sms / 2) {
+            cg = 2;
+            bn = 256;
+        } else {
+            const int num_m = (d.M + kBM - 1) / kBM;
+            while (bn > 64 && num_m * ((d.N + bn - 1) / bn) < sms) bn /= 2;
+        }
     }
     p.bn = bn;
-    const int tiles = num_m * ((d.N + bn - 1) / bn);
-    p.grid = tiles < sms ? tiles : sms;
+    p.cg = cg;
+    const int tiles = ((d.M + kBM * cg - 1) / (kBM * cg)) * ((d.N + bn - 1) / bn);
+    const int units = sms / cg;
+    p.grid = (tiles < units ? tiles : units) * cg;
     // A: M extent x K.  K-major: rows=M, cols=K, box {32, 128}.  MN-major:
-    // stored K x M (rows=K, cols=M), box {32, 32}.
+    // stored K x M (rows=K, cols=M), box {32, 32}.  B rows per CTA = bn / cg.
     if (!encode_map(&p.ta, d.a.ptr, d.a.rows, d.a.cols, d.a.ld, d.a.mn_major ? 32 : kBM, d.a.mn_major, err, errlen))
         return false;
-    if (!encode_map(&p.tb, d.b.ptr, d.b.rows, d.b.cols, d.b.ld, d.b.mn_major ? 32 : bn, d.b.mn_major, err, errlen))
+    if (!encode_map(&p.tb, d.b.ptr, d.b.rows, d.b.cols, d.b.ld, d.b.mn_major ? 32 : bn / cg, d.b.mn_major, err,
+                    errlen))
         return false;
     *out = p;
     return true;
-}
-
-// Set the dynamic shared-memory limit of every instantiation on the current
-// device (must happen before any launch is captured into a CUDA graph).
-cudaError_t tc_gemm_init_device() {
-    cudaError_t e = cudaSuccess;
-    auto set = [&](auto kernel, int smem) {
-        if (e == cudaSuccess) e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    };
-#define PPB_SET(AM, BM)                                                   \
-    set(tc_gemm_kernel<AM, BM, 64>, TcCfg<64>::kSmem);                    \
-    set(tc_gemm_kernel<AM, BM, 128>, TcCfg<128>::kSmem);                  \
-    set(tc_gemm_kernel<AM, BM, 256>, TcCfg<256>::kSmem);
-    PPB_SET(false, false)
-    PPB_SET(false, true)
-    PPB_SET(true, false)
-    PPB_SET(true, true)
-#undef PPB_SET
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (e == cudaSuccess) g_attr_set.fetch_or(1u << (dev & 31));
-    return e;
 }
 
 cudaError_t tc_gemm_launch(const TcGemmPlan& p, cudaStream_t s) {

@@ -16,6 +16,7 @@ struct TcGemmPlan {
     CUtensorMap tb;
     int M = 0, N = 0, K = 0;
     int bn = 256;
+    int cg = 1;  // 1: single-CTA 128-row tiles, 2: CTA-pair 256-row tiles
     int grid = 1;
     bool a_mn = false, b_mn = false;
     EpiParams epi;

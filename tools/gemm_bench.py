@@ -46,7 +46,7 @@ def main():
         A = torch.randn(K, M, device="cuda") if a_mn else torch.randn(M, K, device="cuda")
         B = torch.randn(K, N, device="cuda") if b_mn else torch.randn(N, K, device="cuda")
         Cc = torch.empty(M, N, device="cuda")
-        for bn in (0, 128, 256):
+        for bn in (0, 256, -256, -128):
             def run():
                 rc = L.ppb_debug_gemm(C.c_void_p(A.data_ptr()), A.shape[0], A.shape[1], A.shape[1], a_mn,
                                       C.c_void_p(B.data_ptr()), B.shape[0], B.shape[1], B.shape[1], b_mn,
