@@ -226,6 +226,12 @@ int ppb_debug_gemm(const float* a, int a_rows, int a_cols, long long lda, int a_
                    const float* mask, long long ldm, const double* alpha, float inv_b, int* flag,
                    int precision, int force_bn, void* stream);
 
+/* Implicit-GEMM convolution product on device pointers (kernel unit tests):
+ * which = 0 forward, 1 dgrad, 2 wgrad; layouts in csrc/conv.h. */
+int ppb_debug_conv(int which, const float* x_pad, int N, int H, int W, int C, long long ldx, int pad, int ksz,
+                   const float* w, int u, const float* d_pad, long long ldd, float* out, long long ldo,
+                   int force_bn, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -90,6 +90,9 @@ _SIGS = {
                                  C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_longlong,
                                  C.c_void_p, C.c_int, C.c_void_p, C.c_longlong, C.c_void_p,
                                  C.c_float, C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    "ppb_debug_conv": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_longlong, C.c_int,
+                                 C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_longlong, C.c_void_p, C.c_longlong,
+                                 C.c_int, C.c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

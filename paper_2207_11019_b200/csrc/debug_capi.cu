@@ -54,3 +54,44 @@ extern "C" int ppb_debug_gemm(const float* a, int a_rows, int a_cols, long long 
     }
     return PPB_OK;
 }
+
+// Implicit-GEMM convolution products on device pointers (kernel unit tests):
+// which = 0 forward (out [N*Ho*Wo x ldo], cols u), 1 dgrad (out [N*H*W x ldo],
+// cols C), 2 wgrad (out [u x ldo], cols k*k*ck).  Layouts: csrc/conv.h.
+#include "conv.h"
+
+extern "C" int ppb_debug_conv(int which, const float* x_pad, int N, int H, int W, int C, long long ldx, int pad,
+                              int ksz, const float* w, int u, const float* d_pad, long long ldd, float* out,
+                              long long ldo, int force_bn, void* stream) {
+    ConvShape s;
+    s.N = N;
+    s.H = H;
+    s.W = W;
+    s.C = C;
+    s.ksz = ksz;
+    s.pad = pad;
+    s.u = u;
+    if (!conv_implicit_ok(s)) {
+        ppb_set_error("conv geometry does not tile into TMA boxes");
+        return PPB_ERR_INVALID_ARGUMENT;
+    }
+    GemmDesc d = which == 0 ? conv_fwd_desc(s, x_pad, ldx, w)
+                 : which == 1 ? conv_dgrad_desc(s, d_pad, ldd, w)
+                              : conv_wgrad_desc(s, d_pad, ldd, x_pad, ldx);
+    d.epi.mode = EPI_STORE;
+    d.epi.dst[0] = out;
+    d.epi.ndst = 1;
+    d.epi.ldd = ldo;
+    TcGemmPlan p;
+    char err[256];
+    if (!tc_gemm_prepare(d, &p, force_bn, err, sizeof(err))) {
+        ppb_set_error(err);
+        return PPB_ERR_CUDA;
+    }
+    cudaError_t e = tc_gemm_launch(p, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) {
+        ppb_set_error(cudaGetErrorString(e));
+        return PPB_ERR_CUDA;
+    }
+    return PPB_OK;
+}

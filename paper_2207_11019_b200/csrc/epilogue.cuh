@@ -61,8 +61,14 @@ __device__ __forceinline__ void epilogue32(const EpiParams& p, int m, int n0, fl
 #pragma unroll
                 for (int i = 0; i < 32; ++i) acc[i] = acc[i] > 0.f ? acc[i] : 0.f;
             }
+            long long row = m;
+            if (p.remap) {
+                const int img = m / p.r_howo, rem = m - img * p.r_howo;
+                const int h = rem / p.r_wo, w = rem - h * p.r_wo;
+                row = (static_cast<long long>(img) * p.r_hp + h + p.r_pad) * p.r_wp + w + p.r_pad;
+            }
             for (int d = 0; d < p.ndst; ++d) {
-                store_row32(p.dst[d] + static_cast<long long>(m) * p.ldd + p.col0, n0, nvalid, acc);
+                store_row32(p.dst[d] + row * p.ldd + p.col0, n0, nvalid, acc);
             }
             break;
         }

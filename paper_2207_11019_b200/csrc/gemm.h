@@ -41,6 +41,10 @@ struct EpiParams {
     int col0 = 0;
     const float* bias = nullptr;  // indexed by n, optional
     int relu = 0;
+    // EPI_STORE into a padded NHWC tensor: row m = output pixel (img, h, w) of
+    // an ho x wo grid lands at row ((img*hp + h + pad)*wp + w + pad).
+    int remap = 0;
+    int r_wo = 1, r_howo = 1, r_hp = 1, r_wp = 1, r_pad = 0;
     // EPI_MASK
     const float* mask = nullptr;
     long long ldm = 0;
@@ -66,12 +70,39 @@ struct EpiParams {
 // Host-side description of one operand: a row-major fp32 matrix of `rows` x
 // `cols` with leading dimension `ld` (elements).  For a K-major operand rows is
 // the M (or N) extent and cols is K; for an MN-major operand rows is K.
+//
+// Implicit-GEMM convolution operands (stride 1, k x k taps) address a padded
+// NHWC tensor [img][hp][wp][ch] (or a [u][k*k][ck] weight tensor) through a
+// rank-3/4 TMA map instead of a matrix:
+//   OP_CONV_ROWS  (A, K-major)  GEMM rows = output pixels; K = (tap, ch block):
+//                 box {32 ch, bw, bh, bn} of 128 pixels shifted by the tap
+//                 (forward: input x; dgrad: the padded error signal)
+//   OP_CONV_KPIX  (A or B, MN-major) K = output pixels (32 per box); MN = channel:
+//                 A: the error signal (wgrad); B: the input shifted by the tap of
+//                 the 32-column group (tap = col / ck, ch = col % ck)
+//   OP_WFLIP      (B, MN-major) dgrad weights: K = (tap, k block), N = input
+//                 channel, tap flipped (k*k-1-t), over a [u][k*k][ck] tensor
+enum OperandMode : int { OP_DENSE = 0, OP_CONV_ROWS = 1, OP_CONV_KPIX = 2, OP_WFLIP = 3 };
+
+struct ConvGeom {
+    int mode = OP_DENSE;
+    int wo = 1, howo = 1;    // output pixel grid (rows of the GEMM or its K)
+    int bw = 1, bh = 1, bn = 1;  // spatial box (bw*bh*bn = 128 for ROWS, 32 for KPIX)
+    int ksz = 1;             // kernel size (taps = ksz*ksz)
+    int cblocks = 1;         // 32-channel blocks per tap in the K loop (ROWS, WFLIP)
+    int ck = 32;             // per-tap channel pitch of the GEMM N index (KPIX B)
+    int off = 0;             // spatial offset into the padded tensor
+};
+
 struct Operand {
     const float* ptr = nullptr;
     int rows = 0;
     int cols = 0;
     long long ld = 0;
     bool mn_major = false;
+    ConvGeom geom;
+    // conv tensor extents (elements): [imgs][hp][wp][ch], ch pitch `ld`
+    int ch = 0, wp = 0, hp = 0, imgs = 0;
 };
 
 struct GemmDesc {

@@ -54,10 +54,67 @@ struct TcCfg {
     static constexpr int kSmem = 1024 + kStages * kStageBytes + 256;
 };
 
+// TMA loads of one operand for one pipeline stage: `rows` MN-rows starting at
+// mn0 (this CTA's slice) for K block kb.  CG = 2 signals the leader's barrier.
+template <int CG>
+struct Tma {
+    uint64_t* bar;
+    uint32_t bar_c;
+    __device__ __forceinline__ void d2(void* dst, const CUtensorMap* m, int a, int b) const {
+        if (CG == 2) tma_load_2d_pair(dst, m, bar_c, a, b);
+        else tma_load_2d(dst, m, bar, a, b);
+    }
+    __device__ __forceinline__ void d3(void* dst, const CUtensorMap* m, int a, int b, int c) const {
+        if (CG == 2) tma_load_3d_pair(dst, m, bar_c, a, b, c);
+        else tma_load_3d(dst, m, bar, a, b, c);
+    }
+    __device__ __forceinline__ void d4(void* dst, const CUtensorMap* m, int a, int b, int c, int d) const {
+        if (CG == 2) tma_load_4d_pair(dst, m, bar_c, a, b, c, d);
+        else tma_load_4d(dst, m, bar, a, b, c, d);
+    }
+};
+
+template <bool MN, int ROWS, int CG>
+__device__ __forceinline__ void load_operand(const Tma<CG>& t, const CUtensorMap* map, const ConvGeom& g,
+                                             uint8_t* dst, int mn0, int kb) {
+    const int k0 = kb * kBK;
+    if (g.mode == OP_DENSE) {
+        if (MN) {
+#pragma unroll
+            for (int i = 0; i < ROWS / 32; ++i) t.d2(dst + i * 4096, map, mn0 + 32 * i, k0);
+        } else {
+            t.d2(dst, map, k0, mn0);
+        }
+    } else if (g.mode == OP_CONV_ROWS) {
+        // 128 output pixels (rows) x 32 channels of tap t, channel block cb
+        const int tap = kb / g.cblocks, cb = kb - tap * g.cblocks;
+        const int r = tap / g.ksz, s = tap - r * g.ksz;
+        const int img = mn0 / g.howo, rem = mn0 - img * g.howo, h0 = rem / g.wo;
+        t.d4(dst, map, cb * 32, s + g.off, h0 + r + g.off, img);
+    } else if (g.mode == OP_CONV_KPIX) {
+        // 32 output pixels (K rows) x 32 channels per box; tap from the column
+        const int p0 = k0;
+        const int img = p0 / g.howo, rem = p0 - img * g.howo, h0 = rem / g.wo;
+#pragma unroll
+        for (int i = 0; i < ROWS / 32; ++i) {
+            const int col = mn0 + 32 * i;
+            const int tap = col / g.ck, c0 = col - tap * g.ck;
+            const int r = tap / g.ksz, s = tap - r * g.ksz;
+            t.d4(dst + i * 4096, map, c0, s + g.off, h0 + r + g.off, img);
+        }
+    } else {  // OP_WFLIP
+        const int tap = kb / g.cblocks, kblk = kb - tap * g.cblocks;
+        const int tf = g.ksz * g.ksz - 1 - tap;
+#pragma unroll
+        for (int i = 0; i < ROWS / 32; ++i) t.d3(dst + i * 4096, map, mn0 + 32 * i, tf, kblk * 32);
+    }
+}
+
 template <bool A_MN, bool B_MN, int BN, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
-                   int M, int N, int K, const __grid_constant__ EpiParams epi) {
+                   int M, int N, int K, const __grid_constant__ EpiParams epi,
+                   const __grid_constant__ ConvGeom ga, const __grid_constant__ ConvGeom gb) {
     using C = TcCfg<BN, CG>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -113,45 +170,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int m0 = (tile % num_m) * TM + static_cast<int>(rank) * kBM;
                 const int n0 = (tile / num_m) * BN + static_cast<int>(rank) * C::kBNc;
                 for (int kb = 0; kb < nk; ++kb) {
-                    const int k0 = kb * kBK;
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     uint8_t* a_dst = sA + stage * C::kStageA;
                     uint8_t* b_dst = sB + stage * C::kStageB;
+                    Tma<CG> t;
+                    t.bar = &full_bar[stage];
+                    t.bar_c = 0;
                     if (CG == 1) {
                         mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes);
-                        if (A_MN) {
-#pragma unroll
-                            for (int i = 0; i < kBM / 32; ++i)
-                                tma_load_2d(a_dst + i * 4096, &ta, &full_bar[stage], m0 + 32 * i, k0);
-                        } else {
-                            tma_load_2d(a_dst, &ta, &full_bar[stage], k0, m0);
-                        }
-                        if (B_MN) {
-#pragma unroll
-                            for (int i = 0; i < C::kBNc / 32; ++i)
-                                tma_load_2d(b_dst + i * 4096, &tb, &full_bar[stage], n0 + 32 * i, k0);
-                        } else {
-                            tma_load_2d(b_dst, &tb, &full_bar[stage], k0, n0);
-                        }
                     } else {
                         // both CTAs' bytes land on the leader's full barrier
-                        const uint32_t bar = mapa_shared(smem_u32(&full_bar[stage]), 0);
+                        t.bar_c = mapa_shared(smem_u32(&full_bar[stage]), 0);
                         if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * C::kStageBytes);
-                        if (A_MN) {
-#pragma unroll
-                            for (int i = 0; i < kBM / 32; ++i)
-                                tma_load_2d_pair(a_dst + i * 4096, &ta, bar, m0 + 32 * i, k0);
-                        } else {
-                            tma_load_2d_pair(a_dst, &ta, bar, k0, m0);
-                        }
-                        if (B_MN) {
-#pragma unroll
-                            for (int i = 0; i < C::kBNc / 32; ++i)
-                                tma_load_2d_pair(b_dst + i * 4096, &tb, bar, n0 + 32 * i, k0);
-                        } else {
-                            tma_load_2d_pair(b_dst, &tb, bar, k0, n0);
-                        }
                     }
+                    load_operand<A_MN, kBM, CG>(t, &ta, ga, a_dst, m0, kb);
+                    load_operand<B_MN, C::kBNc, CG>(t, &tb, gb, b_dst, n0, kb);
                     if (++stage == C::kStages) {
                         stage = 0;
                         phase ^= 1;
@@ -298,6 +331,59 @@ bool encode_map(CUtensorMap* map, const float* ptr, int rows, int cols, long lon
     return true;
 }
 
+// Rank-3/4 map for implicit-GEMM conv operands (see gemm.h): a padded NHWC
+// tensor {ch, wp, hp, imgs} (pitch ld) or a [u][taps][ck] weight tensor.
+bool encode_conv_map(CUtensorMap* map, const Operand& o, char* err, size_t errlen) {
+    auto enc = get_encode();
+    if (enc == nullptr) {
+        snprintf(err, errlen, "cuTensorMapEncodeTiled unavailable");
+        return false;
+    }
+    if ((reinterpret_cast<uintptr_t>(o.ptr) & 15u) != 0 || (o.ld * 4) % 16 != 0) {
+        snprintf(err, errlen, "TMA conv operand not 16-byte aligned (ld=%lld)", o.ld);
+        return false;
+    }
+    const ConvGeom& g = o.geom;
+    cuuint64_t dims[4];
+    cuuint64_t strides[3];
+    cuuint32_t box[4];
+    cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+    cuuint32_t rank;
+    if (g.mode == OP_WFLIP) {
+        rank = 3;
+        dims[0] = o.ch;
+        dims[1] = o.wp;
+        dims[2] = o.hp;
+        strides[0] = o.ld * 4;
+        strides[1] = static_cast<cuuint64_t>(o.wp) * o.ld * 4;
+        box[0] = 32;
+        box[1] = 1;
+        box[2] = 32;
+    } else {
+        rank = 4;
+        dims[0] = o.ch;
+        dims[1] = o.wp;
+        dims[2] = o.hp;
+        dims[3] = o.imgs;
+        strides[0] = o.ld * 4;
+        strides[1] = static_cast<cuuint64_t>(o.wp) * o.ld * 4;
+        strides[2] = static_cast<cuuint64_t>(o.hp) * o.wp * o.ld * 4;
+        box[0] = 32;
+        box[1] = g.bw;
+        box[2] = g.bh;
+        box[3] = g.bn;
+    }
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float*>(o.ptr), dims, strides, box,
+                     estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     o.mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        snprintf(err, errlen, "cuTensorMapEncodeTiled (conv, mode %d) failed (%d)", g.mode, static_cast<int>(r));
+        return false;
+    }
+    return true;
+}
+
 template <bool A_MN, bool B_MN, int BN, int CG>
 cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s);
 
@@ -376,7 +462,8 @@ cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<A_MN, B_MN, BN, CG>, p.ta, p.tb, p.M, p.N, p.K, p.epi);
+    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<A_MN, B_MN, BN, CG>, p.ta, p.tb, p.M, p.N, p.K, p.epi,
+                              p.ga, p.gb);
 }
 
 }  // namespace
@@ -423,11 +510,24 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
     p.grid = (tiles < units ? tiles : units) * cg;
     // A: M extent x K.  K-major: rows=M, cols=K, box {32, 128}.  MN-major:
     // stored K x M (rows=K, cols=M), box {32, 32}.  B rows per CTA = bn / cg.
-    if (!encode_map(&p.ta, d.a.ptr, d.a.rows, d.a.cols, d.a.ld, d.a.mn_major ? 32 : kBM, d.a.mn_major, err, errlen))
+    p.ga = d.a.geom;
+    p.gb = d.b.geom;
+    if (d.a.geom.mode != OP_DENSE) {
+        if (!encode_conv_map(&p.ta, d.a, err, errlen)) return false;
+    } else if (!encode_map(&p.ta, d.a.ptr, d.a.rows, d.a.cols, d.a.ld, d.a.mn_major ? 32 : kBM, d.a.mn_major, err,
+                           errlen)) {
         return false;
-    if (!encode_map(&p.tb, d.b.ptr, d.b.rows, d.b.cols, d.b.ld, d.b.mn_major ? 32 : bn / cg, d.b.mn_major, err,
-                    errlen))
+    }
+    if (d.b.geom.mode != OP_DENSE) {
+        if (d.b.geom.mode == OP_CONV_ROWS) {
+            snprintf(err, errlen, "conv pixel rows are only supported as operand A");
+            return false;
+        }
+        if (!encode_conv_map(&p.tb, d.b, err, errlen)) return false;
+    } else if (!encode_map(&p.tb, d.b.ptr, d.b.rows, d.b.cols, d.b.ld, d.b.mn_major ? 32 : bn / cg, d.b.mn_major,
+                           err, errlen)) {
         return false;
+    }
     *out = p;
     return true;
 }

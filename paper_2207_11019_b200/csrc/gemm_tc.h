@@ -20,6 +20,7 @@ struct TcGemmPlan {
     int grid = 1;
     bool a_mn = false, b_mn = false;
     EpiParams epi;
+    ConvGeom ga, gb;
 };
 
 bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err, size_t errlen);
