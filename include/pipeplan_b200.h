@@ -144,6 +144,27 @@ typedef struct {
     int reserved[8];
 } ppb_options;
 
+/* Layer description for nets with convolution layers (the BASELINE CNN
+ * configs; the reference itself is dense-only).  kind = PPB_LAYER_DENSE uses
+ * in_units/out_units (fan_in/fan_out) and act only.  kind = PPB_LAYER_CONV:
+ * stride-1 ksize x ksize convolution with zero padding `pad` over an input of
+ * height x width x in_units (NHWC), activation `act`, then a 2x2 max pool when
+ * pool = 2.  The plan shards out_units (channels).  Weights are
+ * [out_units][ksize][ksize][in_units] row-major, bias [out_units].  A dense
+ * layer after a conv reads the pooled output flattened in (c, h, w) order, so
+ * a channel shard is a contiguous feature range; images are passed as
+ * [batch][height][width][in_units]. */
+#define PPB_LAYER_DENSE 0
+#define PPB_LAYER_CONV 1
+typedef struct {
+    int kind;
+    int in_units;
+    int out_units;
+    int act;
+    int height, width;
+    int ksize, pad, pool;
+} ppb_layer;
+
 void ppb_default_options(ppb_options* o);
 void ppb_default_config(ppb_train_config* c);
 
@@ -172,6 +193,18 @@ int ppb_session_create(ppb_context* ctx, const int* dims, const int* acts, int L
                        const double* b, int batch, const int* plan, int plan_len, int m, int mode,
                        const ppb_train_config* cfg, const ppb_options* opts, ppb_session** out);
 void ppb_session_destroy(ppb_session* s);
+
+/* Same as ppb_session_create / ppb_train_partitioned for nets described by
+ * ppb_layer (dense and conv layers). */
+int ppb_session_create_layers(ppb_context* ctx, const ppb_layer* layers, int L, const double* W,
+                              const double* b, int batch, const int* plan, int plan_len, int m,
+                              int mode, const ppb_train_config* cfg, const ppb_options* opts,
+                              ppb_session** out);
+int ppb_train_partitioned_layers(ppb_context* ctx, const ppb_layer* layers, int L, const double* W,
+                                 const double* b, const double* X, const int* labels, int batch,
+                                 const int* plan, int plan_len, int m, int mode,
+                                 const ppb_train_config* cfg, const ppb_options* opts,
+                                 double* W_out, double* b_out, double* loss_hist, double* acc_hist);
 
 /* Upload a batch (host buffers; fp64 as in pipeplan::Batch, or fp32). */
 int ppb_session_load_batch(ppb_session* s, const double* X, const int* labels);

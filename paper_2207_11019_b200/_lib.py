@@ -48,6 +48,11 @@ class OptionsC(C.Structure):
     ]
 
 
+class LayerC(C.Structure):
+    _fields_ = [("kind", C.c_int), ("in_units", C.c_int), ("out_units", C.c_int), ("act", C.c_int),
+                ("height", C.c_int), ("width", C.c_int), ("ksize", C.c_int), ("pad", C.c_int), ("pool", C.c_int)]
+
+
 # name -> (restype, argtypes)
 _SIGS = {
     "ppb_last_error": (C.c_char_p, []),
@@ -73,6 +78,13 @@ _SIGS = {
                                      C.c_int, C.c_int, C.c_int, C.POINTER(TrainConfigC),
                                      C.POINTER(OptionsC), C.POINTER(C.c_void_p)]),
     "ppb_session_destroy": (None, [C.c_void_p]),
+    "ppb_session_create_layers": (C.c_int, [C.c_void_p, C.POINTER(LayerC), C.c_int, _f64p, _f64p, C.c_int, _i32p,
+                                            C.c_int, C.c_int, C.c_int, C.POINTER(TrainConfigC),
+                                            C.POINTER(OptionsC), C.POINTER(C.c_void_p)]),
+    "ppb_train_partitioned_layers": (C.c_int, [C.c_void_p, C.POINTER(LayerC), C.c_int, _f64p, _f64p, _f64p, _i32p,
+                                               C.c_int, _i32p, C.c_int, C.c_int, C.c_int,
+                                               C.POINTER(TrainConfigC), C.POINTER(OptionsC),
+                                               _f64p, _f64p, _f64p, _f64p]),
     "ppb_session_load_batch": (C.c_int, [C.c_void_p, _f64p, _i32p]),
     "ppb_session_load_batch_f32": (C.c_int, [C.c_void_p, _f32p, _i32p]),
     "ppb_session_step": (C.c_int, [C.c_void_p, C.c_int]),

@@ -23,7 +23,7 @@ from ._lib import PipeplanError, check
 
 __all__ = [
     "ActKind", "LossKind", "UpdateMode", "BoundaryKind", "LayerSpec", "ModelGraph", "Shard", "SubModule",
-    "PartitionPlan", "TinyLayer", "TinyNet", "Batch", "TrainConfig", "PartitionedTrainOptions", "TrainResult",
+    "PartitionPlan", "ConvSpec", "TinyLayer", "TinyNet", "Batch", "TrainConfig", "PartitionedTrainOptions", "TrainResult",
     "split_layer", "split_microbatches", "build_plan", "build_staged_plan", "build_plan_with_cuts",
     "merge_submodules", "merge_all", "validate_plan", "model_graph_of", "train_partitioned", "Context",
     "Session", "PipeplanError",
@@ -153,16 +153,59 @@ class PartitionPlan:  # partition.hpp:40-47
 
 
 @dataclass
+class ConvSpec:
+    """Convolution extension of a layer (BASELINE CNN configs; the reference is
+    dense-only): stride-1 ksize x ksize conv with zero padding over an input of
+    height x width x C_in (NHWC), then an optional 2x2 max pool (pool = 2)."""
+    height: int
+    width: int
+    ksize: int = 3
+    pad: int = 1
+    pool: int = 1
+
+    def out_hw(self):
+        ho = self.height + 2 * self.pad - self.ksize + 1
+        wo = self.width + 2 * self.pad - self.ksize + 1
+        return ho // self.pool, wo // self.pool
+
+
+@dataclass
 class TinyLayer:  # tinynet.hpp:41-48
-    weights: np.ndarray  # fan_out x fan_in, float64
-    bias: np.ndarray     # fan_out
+    weights: np.ndarray  # fan_out x fan_in (dense) | C_out x (ksize*ksize*C_in) (conv), float64
+    bias: np.ndarray     # fan_out | C_out
     act: ActKind = ActKind.identity
+    conv: Optional[ConvSpec] = None
 
     def fan_in(self) -> int:
         return self.weights.shape[1]
 
     def fan_out(self) -> int:
         return self.weights.shape[0]
+
+    def in_units(self) -> int:
+        return self.weights.shape[1] // (self.conv.ksize ** 2) if self.conv else self.weights.shape[1]
+
+    def out_features(self) -> int:
+        if self.conv is None:
+            return self.fan_out()
+        h, w = self.conv.out_hw()
+        return self.fan_out() * h * w
+
+    def fwd_flops(self) -> float:
+        if self.conv is None:
+            return 0.0  # default_costs (model.cpp:124-137) applies
+        c = self.conv
+        ho, wo = c.height + 2 * c.pad - c.ksize + 1, c.width + 2 * c.pad - c.ksize + 1
+        return 2.0 * self.weights.shape[0] * self.weights.shape[1] * ho * wo
+
+    def to_c(self) -> _lib.LayerC:
+        lc = _lib.LayerC()
+        lc.kind = 1 if self.conv else 0
+        lc.in_units, lc.out_units, lc.act = self.in_units(), self.fan_out(), int(self.act)
+        if self.conv:
+            lc.height, lc.width, lc.ksize, lc.pad, lc.pool = (self.conv.height, self.conv.width, self.conv.ksize,
+                                                              self.conv.pad, self.conv.pool)
+        return lc
 
 
 @dataclass
@@ -171,6 +214,15 @@ class TinyNet:  # tinynet.hpp:50-56
 
     def num_layers(self) -> int:
         return len(self.layers)
+
+    def has_conv(self) -> bool:
+        return any(l.conv is not None for l in self.layers)
+
+    def layers_c(self):
+        arr = (_lib.LayerC * len(self.layers))()
+        for i, l in enumerate(self.layers):
+            arr[i] = l.to_c()
+        return arr
 
     def dims(self) -> List[int]:
         return [self.layers[0].fan_in()] + [l.fan_out() for l in self.layers]
@@ -191,6 +243,17 @@ class TinyNet:  # tinynet.hpp:50-56
             layers.append(TinyLayer(W[wo: wo + fi * fo].reshape(fo, fi).copy(), b[bo: bo + fo].copy(), ActKind(acts[l])))
             wo += fi * fo
             bo += fo
+        return TinyNet(layers)
+
+    def replace_params(self, W, b) -> "TinyNet":
+        """Same architecture, parameters from packed arrays (pack() layout)."""
+        layers, wo, bo = [], 0, 0
+        for l in self.layers:
+            n = l.weights.size
+            layers.append(TinyLayer(W[wo: wo + n].reshape(l.weights.shape).copy(), b[bo: bo + l.bias.size].copy(),
+                                    l.act, l.conv))
+            wo += n
+            bo += l.bias.size
         return TinyNet(layers)
 
 
@@ -240,6 +303,8 @@ class TrainResult:  # tinynet.hpp:110-114
 # ---------------------------------------------------------------- planner
 
 def _chain(g):
+    if isinstance(g, TinyNet):
+        g = model_graph_of(g)
     if isinstance(g, ModelGraph):
         fi = np.asarray([l.fan_in for l in g.layers], np.int32)
         fo = np.asarray([l.fan_out for l in g.layers], np.int32)
@@ -250,8 +315,15 @@ def _chain(g):
 
 
 def model_graph_of(net: TinyNet) -> ModelGraph:
-    """tinynet.cpp:463-476 (default costs are applied by the planner)."""
-    return ModelGraph([LayerSpec(l + 1, layer.fan_in(), layer.fan_out()) for l, layer in enumerate(net.layers)])
+    """tinynet.cpp:463-476 (default costs are applied by the planner).  For
+    nets with conv layers the chain is over sharded units (channels) and the
+    conv layers carry their FLOPs explicitly."""
+    specs, prev = [], None
+    for l, layer in enumerate(net.layers):
+        fi = layer.in_units() if prev is None else prev
+        specs.append(LayerSpec(l + 1, fi, layer.fan_out(), layer.fwd_flops()))
+        prev = layer.fan_out()
+    return ModelGraph(specs)
 
 
 def split_layer(layer, devices, replicate_narrow: bool = False) -> List[Shard]:
@@ -364,6 +436,7 @@ class Session:
     def __init__(self, ctx: Context, net: TinyNet, batch_size: int, plan: PartitionPlan, m: int,
                  mode: UpdateMode, cfg: TrainConfig, opts: Optional[PartitionedTrainOptions] = None):
         opts = opts or PartitionedTrainOptions()
+        self._net = net
         self._dims = np.asarray(net.dims(), np.int32)
         self._acts = np.asarray(net.acts(), np.int32)
         W, b = net.pack()
@@ -371,9 +444,15 @@ class Session:
         h = C.c_void_p()
         self._cfg = _cfg_c(cfg)
         self._opts = opts.to_c()
-        check(_lib.lib().ppb_session_create(ctx._h, _ip(self._dims), _ip(self._acts), len(self._acts), _dp(W), _dp(b),
-                                            batch_size, _ip(flat), len(flat), m, int(mode), C.byref(self._cfg),
-                                            C.byref(self._opts), C.byref(h)))
+        if net.has_conv():
+            self._layers = net.layers_c()
+            check(_lib.lib().ppb_session_create_layers(ctx._h, self._layers, len(net.layers), _dp(W), _dp(b),
+                                                       batch_size, _ip(flat), len(flat), m, int(mode),
+                                                       C.byref(self._cfg), C.byref(self._opts), C.byref(h)))
+        else:
+            check(_lib.lib().ppb_session_create(ctx._h, _ip(self._dims), _ip(self._acts), len(self._acts), _dp(W),
+                                                _dp(b), batch_size, _ip(flat), len(flat), m, int(mode),
+                                                C.byref(self._cfg), C.byref(self._opts), C.byref(h)))
         self._h = h
         self._ctx = ctx
         self.batch_size = batch_size
@@ -411,7 +490,7 @@ class Session:
         W = np.zeros(self.nW)
         b = np.zeros(self.nb)
         check(_lib.lib().ppb_session_get_net(self._h, _dp(W), _dp(b)))
-        return TinyNet.unpack(list(self._dims), list(self._acts), W, b)
+        return self._net.replace_params(W, b)
 
     def read_tensor(self, kind: int, layer: int, device: int = 1) -> np.ndarray:
         n = C.c_size_t(0)
@@ -479,8 +558,13 @@ def train_partitioned(net: TinyNet, batch: Batch, cfg: TrainConfig, plan: Partit
     it = max(cfg.iterations, 1)
     lh, ah = np.zeros(it), np.zeros(it)
     cc, oc = _cfg_c(cfg), opts.to_c()
-    check(_lib.lib().ppb_train_partitioned(ctx._h, _ip(dims), _ip(acts), len(acts), _dp(W), _dp(b), _dp(X), _ip(y),
-                                           X.shape[0], _ip(flat), len(flat), m, int(mode), C.byref(cc), C.byref(oc),
-                                           _dp(Wo), _dp(bo), _dp(lh), _dp(ah)))
-    return TrainResult(TinyNet.unpack(list(dims), list(acts), Wo, bo), list(lh[: cfg.iterations]),
-                       list(ah[: cfg.iterations]))
+    if net.has_conv():
+        X = np.ascontiguousarray(X.reshape(X.shape[0], -1), np.float64)
+        check(_lib.lib().ppb_train_partitioned_layers(ctx._h, net.layers_c(), len(net.layers), _dp(W), _dp(b), _dp(X),
+                                                      _ip(y), X.shape[0], _ip(flat), len(flat), m, int(mode),
+                                                      C.byref(cc), C.byref(oc), _dp(Wo), _dp(bo), _dp(lh), _dp(ah)))
+    else:
+        check(_lib.lib().ppb_train_partitioned(ctx._h, _ip(dims), _ip(acts), len(acts), _dp(W), _dp(b), _dp(X),
+                                               _ip(y), X.shape[0], _ip(flat), len(flat), m, int(mode), C.byref(cc),
+                                               C.byref(oc), _dp(Wo), _dp(bo), _dp(lh), _dp(ah)))
+    return TrainResult(net.replace_params(Wo, bo), list(lh[: cfg.iterations]), list(ah[: cfg.iterations]))

@@ -1,0 +1,64 @@
+"""Network descriptions of the BASELINE.json configurations.
+
+Weights are random-initialised with the reference's rule, uniform
+[-0.5, 0.5] / sqrt(fan_in) (tinynet.cpp:176-196), fan_in = ksize^2 * C_in for
+conv layers; the RNG is numpy's (synthetic benchmark data,
+not the reference's libstdc++ stream — use the oracle's init_net for that).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .api import ActKind, ConvSpec, TinyLayer, TinyNet
+
+
+def _dense(rng, fi, fo, act):
+    s = 1.0 / np.sqrt(fi)
+    return TinyLayer((rng.random((fo, fi)) - 0.5) * s, (rng.random(fo) - 0.5) * s, ActKind(act))
+
+
+def _conv(rng, cin, cout, hw, k=3, pad=1, pool=1, act=1):
+    fan_in = k * k * cin
+    s = 1.0 / np.sqrt(fan_in)
+    return TinyLayer((rng.random((cout, fan_in)) - 0.5) * s, (rng.random(cout) - 0.5) * s, ActKind(act),
+                     ConvSpec(hw[0], hw[1], k, pad, pool))
+
+
+def dense_net(dims, acts, seed=1) -> TinyNet:
+    rng = np.random.default_rng(seed)
+    return TinyNet([_dense(rng, dims[l], dims[l + 1], acts[l]) for l in range(len(acts))])
+
+
+def mlp784(seed=1) -> TinyNet:
+    """BASELINE configs[0]: MLP 784-512-512-10."""
+    return dense_net([784, 512, 512, 10], [1, 1, 2], seed)
+
+
+def wide_mlp(seed=1) -> TinyNet:
+    """BASELINE configs[4]: 4 layers of 8192 -> 8192."""
+    return dense_net([8192] * 5, [1, 1, 1, 2], seed)
+
+
+VGG16 = [64, 64, "M", 128, 128, "M", 256, 256, 256, "M", 512, 512, 512, "M", 512, 512, 512, "M"]
+
+
+def vgg16_cifar(seed=1, classes=10, widths=VGG16, hw=32, cin=3) -> TinyNet:
+    """BASELINE configs[2]: VGG-16 on 32x32x3 (13 conv 3x3 + ReLU, 5 max pools,
+    classifier 512 -> classes)."""
+    rng = np.random.default_rng(seed)
+    layers, c, h = [], cin, hw
+    i = 0
+    while i < len(widths):
+        w = widths[i]
+        pool = 2 if i + 1 < len(widths) and widths[i + 1] == "M" else 1
+        layers.append(_conv(rng, c, w, (h, h), 3, 1, pool))
+        c = w
+        h //= pool
+        i += 2 if pool == 2 else 1
+    layers.append(_dense(rng, c * h * h, classes, 2))
+    return TinyNet(layers)
+
+
+def small_cnn(seed=1, hw=8, cin=3, widths=(16, "M", 32, "M"), classes=10) -> TinyNet:
+    """A scaled-down VGG-style net for parity tests."""
+    return vgg16_cifar(seed, classes, list(widths), hw, cin)

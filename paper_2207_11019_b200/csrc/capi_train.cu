@@ -99,6 +99,69 @@ extern "C" int ppb_session_create(ppb_context* ctx, const int* dims, const int* 
 
 extern "C" void ppb_session_destroy(ppb_session* s) { delete s; }
 
+extern "C" int ppb_session_create_layers(ppb_context* ctx, const ppb_layer* layers, int L, const double* W,
+                                         const double* b, int batch, const int* plan, int plan_len, int m,
+                                         int mode, const ppb_train_config* cfg, const ppb_options* opts,
+                                         ppb_session** out) {
+    return ppb_guard([&] {
+        if (ctx == nullptr || out == nullptr || layers == nullptr || L < 1)
+            throw std::invalid_argument("net must have at least one layer");
+        NetDesc net;
+        for (int l = 0; l < L; ++l) {
+            const ppb_layer& p = layers[l];
+            if (p.kind != PPB_LAYER_DENSE && p.kind != PPB_LAYER_CONV)
+                throw std::invalid_argument("unknown layer kind " + std::to_string(p.kind));
+            if (p.act < 0 || p.act > 2) throw std::invalid_argument("unknown activation kind " + std::to_string(p.act));
+            LayerInfo li;
+            li.kind = p.kind;
+            li.in_units = p.in_units;
+            li.out_units = p.out_units;
+            li.act = p.act;
+            if (p.kind == PPB_LAYER_CONV) {
+                li.H = p.height;
+                li.W = p.width;
+                li.ksz = p.ksize;
+                li.pad = p.pad;
+                li.pool = p.pool < 1 ? 1 : p.pool;
+            }
+            net.info.push_back(li);
+            net.acts.push_back(p.act);
+        }
+        net.dims.assign(L + 1, 0);
+        Plan pl;
+        try {
+            pl = plan_from_flat(plan, plan_len);
+        } catch (const std::exception& e) {
+            throw std::runtime_error(std::string("plan/net shape mismatch: ") + e.what());
+        }
+        auto s = std::make_unique<ppb_session>();
+        s->s = std::make_unique<Session>(ctx->device_map, net, W, b, pl, make_cfg(batch, m, mode, cfg, opts));
+        *out = s.release();
+    });
+}
+
+extern "C" int ppb_train_partitioned_layers(ppb_context* ctx, const ppb_layer* layers, int L, const double* W,
+                                            const double* b, const double* X, const int* labels, int batch,
+                                            const int* plan, int plan_len, int m, int mode,
+                                            const ppb_train_config* cfg, const ppb_options* opts, double* W_out,
+                                            double* b_out, double* loss_hist, double* acc_hist) {
+    ppb_session* s = nullptr;
+    int rc = ppb_session_create_layers(ctx, layers, L, W, b, batch, plan, plan_len, m, mode, cfg, opts, &s);
+    if (rc != PPB_OK) return rc;
+    std::unique_ptr<ppb_session> guard(s);
+    return ppb_guard([&] {
+        ppb_train_config dc;
+        ppb_default_config(&dc);
+        const int iters = cfg ? cfg->iterations : dc.iterations;
+        s->s->load_batch(X, nullptr, labels);
+        s->s->step(iters);
+        s->s->sync();
+        int count = 0;
+        s->s->history(loss_hist, acc_hist, iters, &count);
+        s->s->get_net(W_out, b_out);
+    });
+}
+
 extern "C" int ppb_session_load_batch(ppb_session* s, const double* X, const int* labels) {
     return ppb_guard([&] { s->s->load_batch(X, nullptr, labels); });
 }

@@ -195,10 +195,10 @@ __global__ void reduce_mask_kernel(ReduceSlots slots, long long ld_slot, int row
 }
 
 __global__ void colsum_partial_kernel(const float* __restrict__ delta, long long ld, int rows, int u,
-                                      float* __restrict__ partial) {
+                                      int chunks, float* __restrict__ partial) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     const int chunk = blockIdx.y;
-    const int per = (rows + kColsumChunks - 1) / kColsumChunks;
+    const int per = (rows + chunks - 1) / chunks;
     const int r0 = chunk * per;
     const int r1 = r0 + per < rows ? r0 + per : rows;
     if (c >= u) return;
@@ -207,13 +207,15 @@ __global__ void colsum_partial_kernel(const float* __restrict__ delta, long long
     partial[static_cast<long long>(chunk) * u + c] = s;
 }
 
-__global__ void bias_update_kernel(const float* __restrict__ partial, int u, float* __restrict__ bias,
-                                   const double* __restrict__ alpha, float inv_b) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= u) return;
+// one block per column: fixed-shape tree over the chunk partials
+__global__ void __launch_bounds__(kRowThreads) bias_update_kernel(const float* __restrict__ partial, int u,
+                                                                  int chunks, float* __restrict__ bias,
+                                                                  const double* __restrict__ alpha, float inv_b) {
+    const int c = blockIdx.x;
     float s = 0.f;
-    for (int k = 0; k < kColsumChunks; ++k) s += partial[static_cast<long long>(k) * u + c];
-    bias[c] -= static_cast<float>(*alpha) * (s * inv_b);
+    for (int k = threadIdx.x; k < chunks; k += kRowThreads) s += partial[static_cast<long long>(k) * u + c];
+    s = block_sum<kRowThreads>(s);
+    if (threadIdx.x == 0) bias[c] -= static_cast<float>(*alpha) * (s * inv_b);
 }
 
 template <class T>
@@ -254,6 +256,96 @@ __global__ void finalize_kernel(StepState* st, const double* __restrict__ loss_r
     }
 }
 
+template <class T>
+__global__ void pad_input_kernel(const T* __restrict__ src, int imgs, int H, int W, int C, float* __restrict__ dst,
+                                 int p, long long ld) {
+    const long long total = static_cast<long long>(imgs) * H * W * C;
+    const int hp = H + 2 * p, wp = W + 2 * p;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(i % C);
+        long long pix = i / C;
+        const int w = static_cast<int>(pix % W);
+        pix /= W;
+        const int h = static_cast<int>(pix % H);
+        const long long n = pix / H;
+        dst[((n * hp + h + p) * wp + w + p) * ld + c] = static_cast<float>(src[i]);
+    }
+}
+
+__global__ void pool_fwd_kernel(const float* __restrict__ U, long long ldu, int imgs, int Ho, int Wo, int uch,
+                                int pool, unsigned char* __restrict__ argmax, ActLayout out, PoolDsts dsts) {
+    const int Hq = Ho / pool, Wq = Wo / pool;
+    const long long total = static_cast<long long>(imgs) * Hq * Wq * uch;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(i % uch);
+        long long pp = i / uch;  // pooled pixel
+        const int x = static_cast<int>(pp % Wq);
+        const int y = static_cast<int>((pp / Wq) % Hq);
+        const long long n = pp / (static_cast<long long>(Wq) * Hq);
+        float v;
+        if (pool == 1) {
+            v = U[pp * ldu + c];
+        } else {
+            const long long base = (n * Ho + 2 * y) * Wo + 2 * x;
+            float best = U[base * ldu + c];
+            int arg = 0;
+            const float v1 = U[(base + 1) * ldu + c];
+            const float v2 = U[(base + Wo) * ldu + c];
+            const float v3 = U[(base + Wo + 1) * ldu + c];
+            if (v1 > best) { best = v1; arg = 1; }
+            if (v2 > best) { best = v2; arg = 2; }
+            if (v3 > best) { best = v3; arg = 3; }
+            v = best;
+            argmax[pp * uch + c] = static_cast<unsigned char>(arg);
+        }
+        long long o;
+        if (out.kind == 0) {
+            o = ((n * out.hp + y + out.pad) * out.wp + x + out.pad) * out.ld + out.col0 + c;
+        } else {
+            o = n * out.ld + static_cast<long long>(out.col0 + c) * Hq * Wq + static_cast<long long>(y) * Wq + x;
+        }
+        for (int d = 0; d < dsts.n; ++d) dsts.ptr[d][o] = v;
+    }
+}
+
+__global__ void conv_merge_kernel(ConvMerge m) {
+    const long long total = static_cast<long long>(m.imgs) * m.Ho * m.Wo * m.uch;
+    const int Hg = m.Ho / m.pool, Wg = m.Wo / m.pool;
+    const int hq = m.Ho + 2 * m.q, wq = m.Wo + 2 * m.q;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(i % m.uch);
+        long long pix = i / m.uch;
+        const int w = static_cast<int>(pix % m.Wo);
+        const int h = static_cast<int>((pix / m.Wo) % m.Ho);
+        const long long n = pix / (static_cast<long long>(m.Wo) * m.Ho);
+        float g = 0.f;
+        int y = h, x = w;
+        bool live = true;
+        if (m.pool == 2) {
+            y = h >> 1;
+            x = w >> 1;
+            live = y < Hg && x < Wg &&
+                   m.argmax[((n * Hg + y) * Wg + x) * m.uch + c] == static_cast<unsigned char>(((h & 1) << 1) | (w & 1));
+        }
+        if (live) {
+            const long long idx = m.slot_kind == 0 ? ((n * Hg + y) * Wg + x) * m.lds + c
+                                                   : n * m.lds + static_cast<long long>(c) * Hg * Wg + y * Wg + x;
+            g = m.slots.slot[0][idx];
+            for (int k = 1; k < m.slots.n; ++k) g += m.slots.slot[k][idx];
+        }
+        if (m.mask_kind == 1) {
+            if (!(m.U[pix * m.ldu + c] > 0.f)) g = 0.f;
+        } else if (m.mask_kind == 2) {
+            const ActLayout& a = m.act_layout;
+            if (!(m.act[((n * a.hp + h + a.pad) * a.wp + w + a.pad) * a.ld + a.col0 + c] > 0.f)) g = 0.f;
+        }
+        m.d_pad[((n * hq + h + m.q) * wq + w + m.q) * m.ldd + c] = g;
+    }
+}
+
 int grid_for(long long work, int threads) {
     long long g = (work + threads - 1) / threads;
     const long long cap = 148LL * 16;
@@ -291,9 +383,11 @@ cudaError_t launch_reduce_mask(const ReduceSlots& slots, long long ld_slot, int 
 cudaError_t launch_bias_update(const float* delta, long long ld, int rows, int u, float* partial,
                                float* bias, const double* alpha, float inv_b, cudaStream_t s) {
     if (u <= 0) return cudaSuccess;
-    dim3 g1((u + 127) / 128, kColsumChunks);
-    colsum_partial_kernel<<<g1, 128, 0, s>>>(delta, ld, rows, u, partial);
-    bias_update_kernel<<<(u + 127) / 128, 128, 0, s>>>(partial, u, bias, alpha, inv_b);
+    const int chunks = colsum_chunks(rows);
+    const int tpb = u >= 128 ? 128 : (u + 31) / 32 * 32;
+    dim3 g1((u + tpb - 1) / tpb, chunks);
+    colsum_partial_kernel<<<g1, tpb, 0, s>>>(delta, ld, rows, u, chunks, partial);
+    bias_update_kernel<<<u, kRowThreads, 0, s>>>(partial, u, chunks, bias, alpha, inv_b);
     return cudaGetLastError();
 }
 
@@ -310,6 +404,30 @@ cudaError_t launch_convert_f32(const float* src, int rows, int cols, float* dst,
     const long long n = static_cast<long long>(rows) * cols;
     if (n <= 0) return cudaSuccess;
     convert_kernel<float><<<grid_for(n, 256), 256, 0, s>>>(src, rows, cols, dst, ld);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pad_input(const double* src64, const float* src32, int imgs, int H, int W, int C, float* dst,
+                             int p, long long ld, cudaStream_t s) {
+    const long long n = static_cast<long long>(imgs) * H * W * C;
+    if (n <= 0) return cudaSuccess;
+    if (src64) pad_input_kernel<double><<<grid_for(n, 256), 256, 0, s>>>(src64, imgs, H, W, C, dst, p, ld);
+    else pad_input_kernel<float><<<grid_for(n, 256), 256, 0, s>>>(src32, imgs, H, W, C, dst, p, ld);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pool_fwd(const float* U, long long ldu, int imgs, int Ho, int Wo, int uch, int pool,
+                            unsigned char* argmax, const ActLayout& out, const PoolDsts& dsts, cudaStream_t s) {
+    const long long n = static_cast<long long>(imgs) * (Ho / pool) * (Wo / pool) * uch;
+    if (n <= 0) return cudaSuccess;
+    pool_fwd_kernel<<<grid_for(n, 256), 256, 0, s>>>(U, ldu, imgs, Ho, Wo, uch, pool, argmax, out, dsts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_conv_merge(const ConvMerge& m, cudaStream_t s) {
+    const long long n = static_cast<long long>(m.imgs) * m.Ho * m.Wo * m.uch;
+    if (n <= 0) return cudaSuccess;
+    conv_merge_kernel<<<grid_for(n, 256), 256, 0, s>>>(m);
     return cudaGetLastError();
 }
 

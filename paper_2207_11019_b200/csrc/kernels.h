@@ -42,8 +42,13 @@ cudaError_t launch_reduce_mask(const ReduceSlots& slots, long long ld_slot, int 
 
 // Bias gradient + update (train_partitioned.cpp:507-511 col_sums, :639-649):
 // db = column sums of delta (rows x u), bias -= alpha * (db / b).
-// Deterministic two-phase reduction; `partial` holds kColsumChunks x u floats.
-constexpr int kColsumChunks = 32;
+// Deterministic two-phase reduction over colsum_chunks(rows) row chunks;
+// `partial` holds colsum_chunks(rows) x u floats.
+constexpr int kColsumChunks = 1024;  // upper bound
+inline int colsum_chunks(long long rows) {
+    long long c = (rows + 127) / 128;
+    return static_cast<int>(c < 1 ? 1 : (c > kColsumChunks ? kColsumChunks : c));
+}
 cudaError_t launch_bias_update(const float* delta, long long ld, int rows, int u, float* partial,
                                float* bias, const double* alpha, float inv_b, cudaStream_t s);
 
@@ -52,6 +57,53 @@ cudaError_t launch_convert_f64(const double* src, int rows, int cols, float* dst
                                cudaStream_t s);
 cudaError_t launch_convert_f32(const float* src, int rows, int cols, float* dst, long long ld,
                                cudaStream_t s);
+
+// ---------------------------------------------------------------- conv layers
+// Input images: host NHWC rows [b x H*W*C] -> padded NHWC [b][H+2p][W+2p][ld].
+cudaError_t launch_pad_input(const double* src64, const float* src32, int imgs, int H, int W, int C, float* dst,
+                             int p, long long ld, cudaStream_t s);
+
+// Layout of a conv layer's output as its consumer reads it.
+struct ActLayout {
+    int kind = 0;        // 0 padded NHWC [img][hp][wp][ld] at channel col0 + c; 1 CHW-flatten rows [img][ld]
+    long long ld = 0;
+    int hp = 0, wp = 0, pad = 0;  // kind 0
+    int col0 = 0;                 // first channel (shard lo)
+};
+
+struct PoolDsts {
+    int n = 0;
+    float* ptr[kMaxTargets] = {};  // row 0 of this micro-batch in each destination
+};
+
+// Max-pool (pool = 2, window 2x2 stride 2, first max wins) or plain relayout
+// (pool = 1) of a shard's conv output u: [imgs*Ho*Wo x ldu] into the consumer
+// layout on every destination; argmax (0..3 per pooled element) for backward.
+cudaError_t launch_pool_fwd(const float* U, long long ldu, int imgs, int Ho, int Wo, int uch, int pool,
+                            unsigned char* argmax, const ActLayout& out, const PoolDsts& dsts, cudaStream_t s);
+
+// Backward merge into a conv layer's padded error signal d_pad
+// [img][Ho+2q][Wo+2q][ldd] (interior): G = sum of the contributor slots in
+// ascending device order (slot layout: 0 pixel-major [img*Hg*Wg x lds] over the
+// pooled grid, 1 CHW rows [img][lds]); routed through the pooling argmax;
+// masked by the ReLU of the layer's output (mask_kind 1: U rows, 2: the
+// padded consumer-layout activation, 0: none).
+struct ConvMerge {
+    ReduceSlots slots;
+    int slot_kind = 0;
+    long long lds = 0;
+    int imgs = 0, Ho = 0, Wo = 0, uch = 0, pool = 1;
+    const unsigned char* argmax = nullptr;
+    int mask_kind = 0;
+    const float* U = nullptr;
+    long long ldu = 0;
+    const float* act = nullptr;  // padded consumer layout, already offset to this micro-batch
+    ActLayout act_layout;
+    float* d_pad = nullptr;      // already offset to this micro-batch
+    int q = 0;
+    long long ldd = 0;
+};
+cudaError_t launch_conv_merge(const ConvMerge& m, cudaStream_t s);
 
 // Per-GPU step state, updated once per iteration by the finalize kernel.
 struct StepState {

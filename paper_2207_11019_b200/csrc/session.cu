@@ -3,6 +3,8 @@
 // DESIGN.md for buffer layouts and the per-kernel rooflines.
 #include "session.h"
 
+#include "conv.h"
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -63,7 +65,12 @@ struct Session::WLayer {
     float* delta = nullptr;  // [b x ldd]
     long long ldd = 0;
     float* partial = nullptr;            // [kColsumChunks x u]
-    std::vector<float*> slots;           // per contributor of layer+1 (multi-contributor merges)
+    std::vector<float*> slots;           // per contributor of layer+1 (backward merge inputs)
+    long long slot_ld = 0;               // row pitch of the slots
+    long long delta_img = 0;             // floats of delta per sample (conv: padded grid)
+    float* U = nullptr;                  // conv: pre-pool output of the shard [b*Ho*Wo x ldu]
+    long long ldu = 0;
+    unsigned char* argmax = nullptr;     // conv with pool: [b*Hq*Wq x u]
     std::vector<std::vector<int>> delta_ready;  // [j] -> op ids that produce delta rows of micro-batch j
     std::vector<int> fwd_op, dgrad_op;   // [j]
     TcGemmPlan p_wgrad;
@@ -109,25 +116,70 @@ Session::Session(const std::vector<int>& device_map, const NetDesc& net, const d
     const int L = net_.L();
     // ---- entry validation, in the reference's order (train_partitioned.cpp:124-141)
     if (L < 1) throw std::invalid_argument("net must have at least one layer");
-    size_t wo = 0, bo = 0;
+    if (net_.info.empty()) {
+        for (int l = 0; l < L; ++l) {
+            LayerInfo li;
+            li.in_units = net_.dims[l];
+            li.out_units = net_.dims[l + 1];
+            li.act = net_.acts[l];
+            net_.info.push_back(li);
+        }
+    }
+    if (static_cast<int>(net_.info.size()) != L) throw std::invalid_argument("layer description count mismatch");
+    net_.dims.assign(1, static_cast<int>(net_.info[0].in_features()));
     for (int l = 0; l < L; ++l) {
-        if (net_.dims[l] < 1 || net_.dims[l + 1] < 1)
+        const LayerInfo& li = net_.info[l];
+        net_.acts[l] = li.act;
+        net_.dims.push_back(static_cast<int>(li.out_features()));
+        if (li.in_units < 1 || li.out_units < 1)
             throw std::invalid_argument("layer " + S(l + 1) + ": empty weight matrix");
+        if (li.kind == 1) {
+            if (li.ksz < 1 || li.pad < 0 || (li.pool != 1 && li.pool != 2) || li.Ho() < 1 || li.Wo() < 1 ||
+                (li.pool == 2 && (li.Ho() % 2 || li.Wo() % 2)))
+                throw std::invalid_argument("layer " + S(l + 1) + ": invalid conv geometry");
+            ConvShape cs;
+            cs.N = 1;
+            cs.H = li.H;
+            cs.W = li.W;
+            cs.C = li.in_units;
+            cs.ksz = li.ksz;
+            cs.pad = li.pad;
+            cs.u = li.out_units;
+            if (!conv_implicit_ok(cs))
+                throw std::invalid_argument("layer " + S(l + 1) + ": conv grid does not tile into 128/32-pixel TMA boxes");
+            if (l == L - 1) throw std::invalid_argument("the last layer must be dense (classifier head)");
+            if (cfg_.precision == 1)
+                throw std::invalid_argument("fp32 precision mode supports dense layers only (conv runs on tcgen05)");
+            if (li.act == 2) throw std::invalid_argument("softmax is only valid on the last layer");
+        }
+        if (l > 0) {
+            const LayerInfo& pv = net_.info[l - 1];
+            if (li.kind == 1 && pv.kind == 0) throw std::invalid_argument("layer " + S(l + 1) + ": conv after dense");
+            if (li.kind == 1 && (li.in_units != pv.out_units || li.H != pv.Hq() || li.W != pv.Wq()))
+                throw std::invalid_argument("layers " + S(l) + "," + S(l + 1) + ": shape chain broken");
+            if (li.kind == 0 && li.in_units != pv.out_features())
+                throw std::invalid_argument("layers " + S(l) + "," + S(l + 1) + ": shape chain broken");
+        }
         if (net_.acts[l] == 2 && l != L - 1)
             throw std::invalid_argument("softmax is only valid on the last layer");
-        for (size_t i = 0; i < static_cast<size_t>(net_.dims[l]) * net_.dims[l + 1]; ++i)
+    }
+    size_t wo = 0, bo = 0;
+    for (int l = 0; l < L; ++l) {
+        const LayerInfo& li = net_.info[l];
+        const size_t nw = static_cast<size_t>(li.out_units) * li.host_wcols();
+        for (size_t i = 0; i < nw; ++i)
             if (!std::isfinite(W[wo + i])) throw std::invalid_argument("non-finite weight");
-        for (int i = 0; i < net_.dims[l + 1]; ++i)
+        for (int i = 0; i < li.out_units; ++i)
             if (!std::isfinite(b[bo + i])) throw std::invalid_argument("non-finite bias");
         host_W_.push_back(W + wo);
         host_b_.push_back(b + bo);
-        wo += static_cast<size_t>(net_.dims[l]) * net_.dims[l + 1];
-        bo += net_.dims[l + 1];
+        wo += nw;
+        bo += li.out_units;
     }
-    Chain g;
+    Chain g;  // the plan shards out_units (neurons or channels) of every layer
     for (int l = 0; l < L; ++l) {
-        g.fan_in.push_back(net_.dims[l]);
-        g.fan_out.push_back(net_.dims[l + 1]);
+        g.fan_in.push_back(l == 0 ? net_.info[0].in_units : net_.info[l - 1].out_units);
+        g.fan_out.push_back(net_.info[l].out_units);
     }
     try {
         validate_plan(plan_, g, 0);
@@ -256,12 +308,34 @@ void Session::build() {
     if (cfg_.use_graph) capture_graph();
 }
 
+long long Session::img_elems(int layer) const {
+    const ActLayout& a = lay_[layer];
+    return a.kind == 0 ? static_cast<long long>(a.hp) * a.wp * a.ld : a.ld;
+}
+
 void Session::alloc_buffers() {
     const int L = net_.L();
     const int b = cfg_.batch;
     const int F = net_.dims[L];
     const bool softmax = net_.acts[L - 1] == 2;
     hist_cap_ = 1 << 16;
+    // layout of a_l as layer l+1 reads it: padded NHWC for a conv consumer,
+    // dense rows (CHW flatten after a conv) for a dense consumer
+    lay_.assign(L + 1, ActLayout{});
+    for (int l = 0; l <= L; ++l) {
+        ActLayout& a = lay_[l];
+        if (l < L && net_.info[l].kind == 1) {
+            const LayerInfo& c = net_.info[l];
+            a.kind = 0;
+            a.pad = c.pad;
+            a.hp = c.H + 2 * c.pad;
+            a.wp = c.W + 2 * c.pad;
+            a.ld = ld_of(c.in_units);
+        } else {
+            a.kind = 1;
+            a.ld = ld_of(net_.dims[l]);
+        }
+    }
     // which GPUs need which full activations
     std::map<int, std::set<int>> need;  // layer -> ordinals
     for (int wi : layer_workers_[1]) need[0].insert(workers_[wi]->gpu);
@@ -274,7 +348,7 @@ void Session::alloc_buffers() {
     for (auto& [l, set] : need)
         for (int ord : set) {
             Gpu& g = gpu_of(ord);
-            g.act[l] = static_cast<float*>(g.alloc(sizeof(float) * b * ld_of(net_.dims[l])));
+            g.act[l] = static_cast<float*>(g.alloc(sizeof(float) * b * img_elems(l)));
         }
     for (int wi : layer_workers_[1]) gpu_of(workers_[wi]->gpu).needs_x = true;
     for (int wi : layer_workers_[L]) {
@@ -296,25 +370,48 @@ void Session::alloc_buffers() {
         }
         if (g.needs_x) g.xstage = static_cast<double*>(g.alloc(sizeof(double) * b * net_.dims[0]));
     }
-    // shard weights, bias, error signals
+    // shard weights, bias, error signals (+ conv pre-pool outputs / argmax)
     std::vector<float> tmp;
     for (auto& wp : workers_) {
         Worker& w = *wp;
         Gpu& g = gpu_of(w.gpu);
         for (WLayer& wl : w.layers) {
-            const int fi = net_.dims[wl.layer - 1];
-            wl.ldw = ld_of(fi);
+            const LayerInfo& li = net_.info[wl.layer - 1];
+            const int hc = li.host_wcols();
+            wl.ldw = li.kind ? li.dev_wcols() : ld_of(li.in_units);
             wl.W = static_cast<float*>(g.alloc(sizeof(float) * wl.u * wl.ldw));
             wl.bias = static_cast<float*>(g.alloc(sizeof(float) * wl.u));
             wl.ldd = ld_of(wl.u);
-            wl.delta = static_cast<float*>(g.alloc(sizeof(float) * b * wl.ldd));
-            wl.partial = static_cast<float*>(g.alloc(sizeof(float) * kColsumChunks * wl.u));
-            // upload the shard rows [lo, hi) (train_partitioned.cpp:168-169), fp64 -> fp32
+            if (li.kind == 1) {
+                const int q = li.ksz - 1 - li.pad;
+                wl.delta_img = static_cast<long long>(li.Ho() + 2 * q) * (li.Wo() + 2 * q) * wl.ldd;
+                const bool consumer_dense = wl.layer < L && net_.info[wl.layer].kind == 0;
+                if (li.pool == 2 || consumer_dense) {
+                    wl.ldu = ld_of(wl.u);
+                    wl.U = static_cast<float*>(g.alloc(sizeof(float) * b * li.Ho() * li.Wo() * wl.ldu));
+                }
+                if (li.pool == 2)
+                    wl.argmax = static_cast<unsigned char*>(g.alloc(static_cast<size_t>(b) * li.Hq() * li.Wq() * wl.u));
+            } else {
+                wl.delta_img = wl.ldd;
+            }
+            wl.delta = static_cast<float*>(g.alloc(sizeof(float) * b * wl.delta_img));
+            wl.partial = static_cast<float*>(g.alloc(sizeof(float) * kColsumChunks * wl.u));  // upper bound
+            // upload the shard rows [lo, hi) (train_partitioned.cpp:168-169), fp64 -> fp32;
+            // conv rows [k][k][C_in] go to the GEMM layout [k*k][ck] (zero-padded channels)
             tmp.assign(static_cast<size_t>(wl.u) * wl.ldw, 0.f);
             const double* Wl = host_W_[wl.layer - 1];
-            for (int r = 0; r < wl.u; ++r)
-                for (int c = 0; c < fi; ++c)
-                    tmp[static_cast<size_t>(r) * wl.ldw + c] = static_cast<float>(Wl[static_cast<size_t>(wl.lo + r) * fi + c]);
+            for (int r = 0; r < wl.u; ++r) {
+                const double* src = Wl + static_cast<size_t>(wl.lo + r) * hc;
+                float* dst = tmp.data() + static_cast<size_t>(r) * wl.ldw;
+                if (li.kind == 1) {
+                    for (int t = 0; t < li.ksz * li.ksz; ++t)
+                        for (int c = 0; c < li.in_units; ++c)
+                            dst[t * li.ck() + c] = static_cast<float>(src[t * li.in_units + c]);
+                } else {
+                    for (int c = 0; c < hc; ++c) dst[c] = static_cast<float>(src[c]);
+                }
+            }
             check(cudaSetDevice(w.gpu), "cudaSetDevice");
             check(cudaMemcpy(wl.W, tmp.data(), sizeof(float) * tmp.size(), cudaMemcpyHostToDevice), "upload W");
             std::vector<float> bb(wl.u);
@@ -325,17 +422,28 @@ void Session::alloc_buffers() {
             wl.dgrad_op.assign(cfg_.m, -1);
         }
     }
-    // contributor slots for multi-contributor backward merges
+    // contributor slots: multi-contributor dense merges, every conv merge
     for (int l = 2; l <= L; ++l) {
         int ncontrib = 0;
         for (int wi : layer_workers_[l]) ncontrib += workers_[wi]->at(l).contributor;
-        if (ncontrib < 2) continue;
+        const LayerInfo& dl = net_.info[l - 2];
+        const LayerInfo& cl = net_.info[l - 1];
+        if (dl.kind == 0 && ncontrib < 2) continue;
         for (int wi : layer_workers_[l - 1]) {
             Worker& w = *workers_[wi];
             WLayer& wl = w.at(l - 1);
             Gpu& g = gpu_of(w.gpu);
+            long long rows = b;
+            if (dl.kind == 0) {
+                wl.slot_ld = wl.ldd;
+            } else if (cl.kind == 1) {  // conv consumer: pixel-major over the pooled grid
+                wl.slot_ld = ld_of(wl.u);
+                rows = static_cast<long long>(b) * dl.Hq() * dl.Wq();
+            } else {  // dense consumer: CHW-flatten columns of this shard's channels
+                wl.slot_ld = ld_of(wl.u * dl.Hq() * dl.Wq());
+            }
             for (int k = 0; k < ncontrib; ++k)
-                wl.slots.push_back(static_cast<float*>(g.alloc(sizeof(float) * b * wl.ldd)));
+                wl.slots.push_back(static_cast<float*>(g.alloc(sizeof(float) * rows * wl.slot_ld)));
         }
     }
     for (auto& gp : gpus_) {
@@ -427,12 +535,75 @@ void Session::build_ops() {
                 }
             }
             std::vector<int> produced;
+            const LayerInfo& li = net_.info[l - 1];
             for (int wi : contributors(l)) {
                 Worker& w = *workers_[wi];
                 WLayer& wl = w.at(l);
                 const int fi = net_.dims[l - 1];
                 GemmDesc& d = wl.d_fwd[j];
-                d.a = Operand{act_buf(w.gpu, l - 1) + off * ld_of(fi), rows, fi, ld_of(fi), false};
+                std::vector<int> deps;
+                if (l == 1) {
+                    deps.push_back(begin_op_);
+                } else {
+                    auto it = act_ready[l - 1][j].find(w.gpu);
+                    if (it != act_ready[l - 1][j].end()) deps.insert(deps.end(), it->second.begin(), it->second.end());
+                }
+                if (l == w.layers.front().layer && cfg_.gate > 0 && j - cfg_.gate >= 0 &&
+                    w.last_bwd[j - cfg_.gate] >= 0)
+                    deps.push_back(w.last_bwd[j - cfg_.gate]);  // schedule.cpp:293-296
+                if (li.kind == 1) {
+                    // implicit-GEMM conv over the padded NHWC input of this micro-batch
+                    ConvShape cs;
+                    cs.N = rows;
+                    cs.H = li.H;
+                    cs.W = li.W;
+                    cs.C = li.in_units;
+                    cs.ksz = li.ksz;
+                    cs.pad = li.pad;
+                    cs.u = wl.u;
+                    d = conv_fwd_desc(cs, act_buf(w.gpu, l - 1) + off * img_elems(l - 1), lay_[l - 1].ld, wl.W);
+                    d.epi = EpiParams{};
+                    d.epi.mode = EPI_STORE;
+                    d.epi.bias = wl.bias;
+                    d.epi.relu = li.act == 1;
+                    const long long pix = static_cast<long long>(li.Ho()) * li.Wo();
+                    if (wl.U != nullptr) {  // pre-pool output, then pool / relayout
+                        d.epi.dst[d.epi.ndst++] = wl.U + off * pix * wl.ldu;
+                        d.epi.ldd = wl.ldu;
+                    } else {  // straight into every consumer GPU's padded NHWC input
+                        const ActLayout& a = lay_[l];
+                        d.epi.remap = 1;
+                        d.epi.r_wo = li.Wo();
+                        d.epi.r_howo = static_cast<int>(pix);
+                        d.epi.r_hp = a.hp;
+                        d.epi.r_wp = a.wp;
+                        d.epi.r_pad = a.pad;
+                        d.epi.ldd = a.ld;
+                        d.epi.col0 = wl.lo;
+                        for (int ord : dest_gpus) d.epi.dst[d.epi.ndst++] = act_buf(ord, l) + off * img_elems(l);
+                    }
+                    prepare(d, wl.p_fwd[j]);
+                    const double fl = 2.0 * rows * pix * wl.u * li.ksz * li.ksz * li.in_units;
+                    int op = add_op(w.gpu, w.sf, gemm_launch(&wl.p_fwd[j], &wl.d_fwd[j], w.sf), deps, 1, OP_FWD_GEMM, fl);
+                    if (wl.U != nullptr) {
+                        ActLayout out = lay_[l];
+                        out.col0 = wl.lo;
+                        PoolDsts pd;
+                        for (int ord : dest_gpus) pd.ptr[pd.n++] = act_buf(ord, l) + off * img_elems(l);
+                        const float* U = wl.U + off * pix * wl.ldu;
+                        const long long ldu = wl.ldu;
+                        unsigned char* am = wl.argmax ? wl.argmax + off * li.Hq() * li.Wq() * wl.u : nullptr;
+                        const int Ho = li.Ho(), Wo = li.Wo(), u = wl.u, pool = li.pool;
+                        cudaStream_t st = w.sf;
+                        op = add_op(w.gpu, st, [=]() {
+                            return launch_pool_fwd(U, ldu, rows, Ho, Wo, u, pool, am, out, pd, st);
+                        }, {op}, 1, OP_POOL);
+                    }
+                    wl.fwd_op[j] = op;
+                    produced.push_back(op);
+                    continue;
+                }
+                d.a = Operand{act_buf(w.gpu, l - 1) + off * img_elems(l - 1), rows, fi, lay_[l - 1].ld, false};
                 d.b = Operand{wl.W, wl.u, fi, wl.ldw, false};
                 d.M = rows;
                 d.N = wl.u;
@@ -448,16 +619,6 @@ void Session::build_ops() {
                     d.epi.dst[d.epi.ndst++] = base + off * d.epi.ldd;
                 }
                 prepare(d, wl.p_fwd[j]);
-                std::vector<int> deps;
-                if (l == 1) {
-                    deps.push_back(begin_op_);
-                } else {
-                    auto it = act_ready[l - 1][j].find(w.gpu);
-                    if (it != act_ready[l - 1][j].end()) deps.insert(deps.end(), it->second.begin(), it->second.end());
-                }
-                if (l == w.layers.front().layer && cfg_.gate > 0 && j - cfg_.gate >= 0 &&
-                    w.last_bwd[j - cfg_.gate] >= 0)
-                    deps.push_back(w.last_bwd[j - cfg_.gate]);  // schedule.cpp:293-296
                 const int op = add_op(w.gpu, w.sf, gemm_launch(&wl.p_fwd[j], &wl.d_fwd[j], w.sf), deps, 1,
                                       OP_FWD_GEMM, 2.0 * rows * wl.u * fi);
                 wl.fwd_op[j] = op;
@@ -470,7 +631,7 @@ void Session::build_ops() {
                 std::set<int> consumers;
                 for (int wi : layer_workers_[l + 1]) consumers.insert(workers_[wi]->gpu);
                 Gpu& hub = gpu_of(hub_gpu);
-                const long long ld = ld_of(net_.dims[l]);
+                const long long ld = img_elems(l);
                 for (int ord : consumers) {
                     if (ord == hub_gpu) continue;
                     float* src = act_buf(hub_gpu, l) + off * ld;
@@ -531,6 +692,97 @@ void Session::build_ops() {
             const bool relu_below = net_.acts[l - 2] == 1;
             const bool single = contrib.size() == 1;
             std::vector<int> dgrad_ops;
+            const LayerInfo& li = net_.info[l - 1];
+            const LayerInfo& lb = net_.info[l - 2];
+            if (lb.kind == 1) {
+                // destination is a conv layer: every contributor scatters its
+                // partial input gradient (conv: pixel-major over the pooled grid,
+                // dense: CHW-flatten columns) into per-destination slots; the
+                // destination sums them, routes through the pool argmax and
+                // masks by its ReLU into its padded error signal.
+                const int hw = lb.Hq() * lb.Wq();
+                for (size_t k = 0; k < contrib.size(); ++k) {
+                    Worker& w = *workers_[contrib[k]];
+                    WLayer& wl = w.at(l);
+                    GemmDesc& d = wl.d_dgrad[j];
+                    double fl;
+                    long long rows_per_img;
+                    if (li.kind == 1) {
+                        ConvShape cs;
+                        cs.N = rows;
+                        cs.H = li.H;
+                        cs.W = li.W;
+                        cs.C = li.in_units;
+                        cs.ksz = li.ksz;
+                        cs.pad = li.pad;
+                        cs.u = wl.u;
+                        d = conv_dgrad_desc(cs, wl.delta + off * wl.delta_img, wl.ldd, wl.W);
+                        fl = 2.0 * rows * li.H * li.W * li.in_units * li.ksz * li.ksz * wl.u;
+                        rows_per_img = static_cast<long long>(li.H) * li.W;
+                    } else {
+                        d.a = Operand{wl.delta + off * wl.ldd, rows, wl.u, wl.ldd, false};
+                        d.b = Operand{wl.W, wl.u, fi, wl.ldw, true};
+                        d.M = rows;
+                        d.N = fi;
+                        d.K = wl.u;
+                        fl = 2.0 * rows * wl.u * fi;
+                        rows_per_img = 1;
+                    }
+                    d.epi = EpiParams{};
+                    d.epi.mode = EPI_SLOTS;
+                    const int scale = li.kind == 1 ? 1 : hw;
+                    for (int di : dests) {
+                        WLayer& dl = workers_[di]->at(l - 1);
+                        const int sg = d.epi.nseg++;
+                        d.epi.seg_lo[sg] = dl.lo * scale;
+                        d.epi.seg_hi[sg] = dl.hi * scale;
+                        d.epi.seg_ld[sg] = dl.slot_ld;
+                        d.epi.seg_dst[sg] = dl.slots[k] + off * rows_per_img * dl.slot_ld;
+                    }
+                    prepare(d, wl.p_dgrad[j]);
+                    const int op = add_op(w.gpu, w.sb, gemm_launch(&wl.p_dgrad[j], &wl.d_dgrad[j], w.sb),
+                                          wl.delta_ready[j], 1, OP_DGRAD_GEMM, fl);
+                    wl.dgrad_op[j] = op;
+                    w.last_bwd[j] = std::max(w.last_bwd[j], op);
+                    dgrad_ops.push_back(op);
+                }
+                for (int di : dests) {
+                    Worker& dw = *workers_[di];
+                    WLayer& dl = dw.at(l - 1);
+                    ConvMerge cm;
+                    const long long rows_per_img = li.kind == 1 ? hw : 1;
+                    for (float* sp : dl.slots) cm.slots.slot[cm.slots.n++] = sp + off * rows_per_img * dl.slot_ld;
+                    cm.slot_kind = li.kind == 1 ? 0 : 1;
+                    cm.lds = dl.slot_ld;
+                    cm.imgs = rows;
+                    cm.Ho = lb.Ho();
+                    cm.Wo = lb.Wo();
+                    cm.uch = dl.u;
+                    cm.pool = lb.pool;
+                    cm.argmax = dl.argmax ? dl.argmax + off * hw * dl.u : nullptr;
+                    if (relu_below) {
+                        if (dl.U != nullptr) {
+                            cm.mask_kind = 1;
+                            cm.U = dl.U + off * lb.Ho() * lb.Wo() * dl.ldu;
+                            cm.ldu = dl.ldu;
+                        } else {
+                            cm.mask_kind = 2;
+                            cm.act = act_buf(dw.gpu, l - 1) + off * img_elems(l - 1);
+                            cm.act_layout = lay_[l - 1];
+                            cm.act_layout.col0 = dl.lo;
+                        }
+                    }
+                    cm.d_pad = dl.delta + off * dl.delta_img;
+                    cm.q = lb.ksz - 1 - lb.pad;
+                    cm.ldd = dl.ldd;
+                    cudaStream_t st = dw.sb;
+                    const int op = add_op(dw.gpu, st, [=]() { return launch_conv_merge(cm, st); }, dgrad_ops, 1,
+                                          OP_CONV_MERGE);
+                    dl.delta_ready[j] = {op};
+                    dw.last_bwd[j] = std::max(dw.last_bwd[j], op);
+                }
+                continue;
+            }
             for (size_t k = 0; k < contrib.size(); ++k) {
                 Worker& w = *workers_[contrib[k]];
                 WLayer& wl = w.at(l);
@@ -623,12 +875,30 @@ void Session::build_ops() {
         for (WLayer& wl : w.layers) {
             const int l = wl.layer;
             const int fi = net_.dims[l - 1];
+            const LayerInfo& li = net_.info[l - 1];
             GemmDesc& d = wl.d_wgrad;
-            d.a = Operand{wl.delta, cfg_.batch, wl.u, wl.ldd, true};
-            d.b = Operand{act_buf(w.gpu, l - 1), cfg_.batch, fi, ld_of(fi), true};
-            d.M = wl.u;
-            d.N = fi;
-            d.K = cfg_.batch;
+            double wfl;
+            long long bias_rows = cfg_.batch;
+            if (li.kind == 1) {
+                ConvShape cs;
+                cs.N = cfg_.batch;
+                cs.H = li.H;
+                cs.W = li.W;
+                cs.C = li.in_units;
+                cs.ksz = li.ksz;
+                cs.pad = li.pad;
+                cs.u = wl.u;
+                d = conv_wgrad_desc(cs, wl.delta, wl.ldd, act_buf(w.gpu, l - 1), lay_[l - 1].ld);
+                wfl = 2.0 * cfg_.batch * li.Ho() * li.Wo() * wl.u * li.ksz * li.ksz * li.in_units;
+                bias_rows = static_cast<long long>(cfg_.batch) * (wl.delta_img / wl.ldd);  // zero borders add nothing
+            } else {
+                d.a = Operand{wl.delta, cfg_.batch, wl.u, wl.ldd, true};
+                d.b = Operand{act_buf(w.gpu, l - 1), cfg_.batch, fi, lay_[l - 1].ld, true};
+                d.M = wl.u;
+                d.N = fi;
+                d.K = cfg_.batch;
+                wfl = 2.0 * wl.u * fi * static_cast<double>(cfg_.batch);
+            }
             d.epi = EpiParams{};
             d.epi.mode = EPI_SGD;
             d.epi.W = wl.W;
@@ -646,15 +916,14 @@ void Session::build_ops() {
             cudaStream_t s = w.su;
             const float* delta = wl.delta;
             const long long ldd = wl.ldd;
-            const int b = cfg_.batch, u = wl.u;
+            const int b = static_cast<int>(bias_rows), u = wl.u;
             float* partial = wl.partial;
             float* bias = wl.bias;
             const double* alpha = &g.st->alpha;
             const int bop = add_op(w.gpu, s, [=]() {
                 return launch_bias_update(delta, ldd, b, u, partial, bias, alpha, inv_b, s);
             }, deps, 2, OP_BIAS);
-            add_op(w.gpu, s, gemm_launch(&wl.p_wgrad, &wl.d_wgrad, s), {bop}, 1, OP_WGRAD_GEMM,
-                   2.0 * wl.u * fi * static_cast<double>(cfg_.batch));
+            add_op(w.gpu, s, gemm_launch(&wl.p_wgrad, &wl.d_wgrad, s), {bop}, 1, OP_WGRAD_GEMM, wfl);
         }
     }
 
@@ -839,7 +1108,21 @@ void Session::load_batch(const double* X64, const float* X32, const int* labels)
         Gpu& g = *gp;
         check(cudaSetDevice(g.ordinal), "cudaSetDevice");
         if (g.ordinal != g0.ordinal) check(cudaStreamWaitEvent(g.main, g0.ev_done, 0), "wait");
-        if (g.needs_x) {
+        if (g.needs_x && lay_[0].kind == 0) {
+            // conv input: host NHWC rows -> padded NHWC (zero border stays from allocation)
+            const LayerInfo& c = net_.info[0];
+            float* x = g.act.at(0);
+            const size_t n = static_cast<size_t>(b) * I0;
+            if (X64 != nullptr) {
+                check(cudaMemcpyAsync(g.xstage, X64, sizeof(double) * n, cudaMemcpyHostToDevice, g.main), "H2D X");
+                check(launch_pad_input(g.xstage, nullptr, b, c.H, c.W, c.in_units, x, c.pad, lay_[0].ld, g.main),
+                      "pad X");
+            } else {
+                float* st = reinterpret_cast<float*>(g.xstage);
+                check(cudaMemcpyAsync(st, X32, sizeof(float) * n, cudaMemcpyHostToDevice, g.main), "H2D X");
+                check(launch_pad_input(nullptr, st, b, c.H, c.W, c.in_units, x, c.pad, lay_[0].ld, g.main), "pad X");
+            }
+        } else if (g.needs_x) {
             float* x = g.act.at(0);
             if (X64 != nullptr) {
                 check(cudaMemcpyAsync(g.xstage, X64, sizeof(double) * b * I0, cudaMemcpyHostToDevice, g.main), "H2D X");
@@ -935,7 +1218,8 @@ void Session::get_net(double* W, double* b) {
     size_t wo = 0, bo = 0;
     std::vector<float> tmp;
     for (int l = 1; l <= L; ++l) {
-        const int fi = net_.dims[l - 1];
+        const LayerInfo& li = net_.info[l - 1];
+        const int hc = li.host_wcols();
         for (int wi : layer_workers_[l]) {
             Worker& w = *workers_[wi];
             WLayer& wl = w.at(l);
@@ -943,15 +1227,22 @@ void Session::get_net(double* W, double* b) {
             tmp.resize(static_cast<size_t>(wl.u) * wl.ldw);
             check(cudaSetDevice(w.gpu), "cudaSetDevice");
             check(cudaMemcpy(tmp.data(), wl.W, sizeof(float) * tmp.size(), cudaMemcpyDeviceToHost), "D2H W");
-            for (int r = 0; r < wl.u; ++r)
-                for (int c = 0; c < fi; ++c)
-                    W[wo + static_cast<size_t>(wl.lo + r) * fi + c] = tmp[static_cast<size_t>(r) * wl.ldw + c];
+            for (int r = 0; r < wl.u; ++r) {
+                double* dst = W + wo + static_cast<size_t>(wl.lo + r) * hc;
+                const float* src = tmp.data() + static_cast<size_t>(r) * wl.ldw;
+                if (li.kind == 1) {
+                    for (int t = 0; t < li.ksz * li.ksz; ++t)
+                        for (int c = 0; c < li.in_units; ++c) dst[t * li.in_units + c] = src[t * li.ck() + c];
+                } else {
+                    for (int c = 0; c < hc; ++c) dst[c] = src[c];
+                }
+            }
             std::vector<float> bb(wl.u);
             check(cudaMemcpy(bb.data(), wl.bias, sizeof(float) * wl.u, cudaMemcpyDeviceToHost), "D2H b");
             for (int r = 0; r < wl.u; ++r) b[bo + wl.lo + r] = bb[r];
         }
-        wo += static_cast<size_t>(fi) * net_.dims[l];
-        bo += net_.dims[l];
+        wo += static_cast<size_t>(hc) * li.out_units;
+        bo += li.out_units;
     }
 }
 
@@ -973,6 +1264,11 @@ size_t Session::read_tensor(int kind, int layer, int device, double* out, size_t
         }
         return n;
     };
+    auto raw = [&](const float* p, int ord, size_t nfloats) {
+        tmp.resize(nfloats);
+        check(cudaSetDevice(ord), "cudaSetDevice");
+        check(cudaMemcpy(tmp.data(), p, sizeof(float) * nfloats, cudaMemcpyDeviceToHost), "D2H tensor");
+    };
     const int F = net_.dims[layer];
     const bool softmax_head = layer == L && net_.acts[L - 1] == 2;
     if (kind == 0 || kind == 1) {
@@ -992,18 +1288,54 @@ size_t Session::read_tensor(int kind, int layer, int device, double* out, size_t
             }
             return n;
         }
+        const LayerInfo& li = net_.info[layer - 1];
         for (auto& gp : gpus_) {
             auto it = gp->act.find(layer);
-            if (it != gp->act.end()) return fetch(it->second, gp->ordinal, b, F, ld_of(F));
+            if (it == gp->act.end()) continue;
+            if (li.kind == 0) return fetch(it->second, gp->ordinal, b, F, ld_of(F));
+            // conv output, returned per sample in (h, w, c) order
+            const ActLayout& a = lay_[layer];
+            const int Hq = li.Hq(), Wq = li.Wq(), Cc = li.out_units;
+            const long long per = img_elems(layer);
+            raw(it->second, gp->ordinal, static_cast<size_t>(b) * per);
+            const size_t n = static_cast<size_t>(b) * Hq * Wq * Cc;
+            if (out != nullptr) {
+                if (cap < n) throw std::length_error("tensor buffer too small");
+                for (int i = 0; i < b; ++i)
+                    for (int y = 0; y < Hq; ++y)
+                        for (int x = 0; x < Wq; ++x)
+                            for (int c = 0; c < Cc; ++c) {
+                                const long long src = a.kind == 0
+                                    ? ((static_cast<long long>(i) * a.hp + y + a.pad) * a.wp + x + a.pad) * a.ld + c
+                                    : i * a.ld + (static_cast<long long>(c) * Hq + y) * Wq + x;
+                                out[((static_cast<size_t>(i) * Hq + y) * Wq + x) * Cc + c] = tmp[src];
+                            }
+            }
+            return n;
         }
         throw std::runtime_error("internal: activation not resident");
     }
     if (kind == 2) {
+        const LayerInfo& li = net_.info[layer - 1];
         for (int wi : layer_workers_[layer]) {
             Worker& w = *workers_[wi];
             if (w.device != device) continue;
             WLayer& wl = w.at(layer);
-            return fetch(wl.delta, w.gpu, b, wl.u, wl.ldd);
+            if (li.kind == 0) return fetch(wl.delta, w.gpu, b, wl.u, wl.ldd);
+            const int q = li.ksz - 1 - li.pad, Ho = li.Ho(), Wo = li.Wo();
+            const long long per = wl.delta_img;
+            raw(wl.delta, w.gpu, static_cast<size_t>(b) * per);
+            const size_t n = static_cast<size_t>(b) * Ho * Wo * wl.u;
+            if (out != nullptr) {
+                if (cap < n) throw std::length_error("tensor buffer too small");
+                for (int i = 0; i < b; ++i)
+                    for (int y = 0; y < Ho; ++y)
+                        for (int x = 0; x < Wo; ++x)
+                            for (int c = 0; c < wl.u; ++c)
+                                out[((static_cast<size_t>(i) * Ho + y) * Wo + x) * wl.u + c] =
+                                    tmp[i * per + ((static_cast<long long>(y + q)) * (Wo + 2 * q) + x + q) * wl.ldd + c];
+            }
+            return n;
         }
         throw std::out_of_range("device " + S(device) + " holds no shard of layer " + S(layer));
     }

@@ -24,9 +24,31 @@
 
 namespace ppb {
 
+// One parameterised layer.  Dense layers are the reference's TinyLayer
+// (tinynet.hpp:41-48); conv layers extend it (BASELINE.json CNN configs):
+// stride-1 k x k convolution with zero padding, activation, optional 2x2 max
+// pool, NHWC activations.  The sharded dimension (split_layer's fan_out) is
+// out_units: output neurons or output channels.
+struct LayerInfo {
+    int kind = 0;  // 0 dense, 1 conv
+    int in_units = 0, out_units = 0;
+    int act = 0;
+    int H = 1, W = 1, ksz = 1, pad = 0, pool = 1;  // conv: input grid, kernel, padding, pool factor (1|2)
+    int Ho() const { return H + 2 * pad - ksz + 1; }
+    int Wo() const { return W + 2 * pad - ksz + 1; }
+    int Hq() const { return Ho() / pool; }
+    int Wq() const { return Wo() / pool; }
+    long long in_features() const { return kind ? static_cast<long long>(in_units) * H * W : in_units; }
+    long long out_features() const { return kind ? static_cast<long long>(out_units) * Hq() * Wq() : out_units; }
+    int host_wcols() const { return kind ? ksz * ksz * in_units : in_units; }
+    int ck() const { return (in_units + 31) / 32 * 32; }
+    int dev_wcols() const { return kind ? ksz * ksz * ck() : in_units; }
+};
+
 struct NetDesc {
-    std::vector<int> dims;  // L+1
+    std::vector<int> dims;  // L+1 feature counts (dims[0] = input features)
     std::vector<int> acts;  // L (0 identity, 1 relu, 2 softmax_last)
+    std::vector<LayerInfo> info;  // L; filled from dims/acts for dense nets
     int L() const { return static_cast<int>(acts.size()); }
 };
 
@@ -40,7 +62,9 @@ enum OpKind : int {
     OP_BIAS = 6,
     OP_FINALIZE = 7,
     OP_COPY = 8,
-    OP_NKINDS = 9,
+    OP_POOL = 9,        // conv output -> pooled / relaid consumer layout
+    OP_CONV_MERGE = 10, // conv backward merge (slots, pool routing, ReLU mask)
+    OP_NKINDS = 11,
 };
 
 struct SessionConfig {
@@ -103,6 +127,7 @@ class Session {
     void capture_graph();
     Gpu& gpu_of(int ordinal);
     float* act_buf(int ordinal, int layer);  // full activation a_layer on that GPU (layer 0 = X)
+    long long img_elems(int layer) const;    // floats per sample of act layer `layer` (consumer layout)
     float* q_buf(int ordinal);               // gathered pre-activation of the softmax head
     long long ld_of(int cols) const { return (cols + 3) / 4 * 4; }
     void check(cudaError_t e, const char* what);
@@ -127,6 +152,7 @@ class Session {
     int hist_cap_ = 0;
     int kernels_per_step_ = 0;
     std::vector<const double*> host_W_, host_b_;
+    std::vector<ActLayout> lay_;  // [0..L]: layout of a_l as its consumer reads it
     bool pending_acc_error_ = false;
 };
 

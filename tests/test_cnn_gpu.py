@@ -1,0 +1,100 @@
+"""Partitioned training of nets with conv layers (BASELINE CNN configs) on the
+GPU against the float64 PyTorch restatement tests/cnn_oracle.py.
+
+Parity for conv is unpinned by the reference (it has no conv); the oracle
+follows the reference's partitioned-step semantics on the conv extension.
+Tolerance (TF32 operands, fp32 accumulation): net_distance <= 5e-3, loss
+|diff| <= 5e-3 * max(1, |ref|).
+"""
+import numpy as np
+import pytest
+
+import cnn_oracle
+from _util import net_distance, rel_norm
+from paper_2207_11019_b200 import api, configs
+from paper_2207_11019_b200.api import Batch, PartitionedTrainOptions, TrainConfig, UpdateMode
+
+pytestmark = pytest.mark.gpu
+
+TOL = 5e-3
+
+
+def data(net, b, classes, seed=0):
+    rng = np.random.default_rng(seed)
+    c = net.layers[0].conv
+    X = rng.standard_normal((b, c.height, c.width, net.layers[0].in_units()))
+    y = rng.integers(0, classes, b)
+    return X, y
+
+
+NETS = {
+    "pool_pool": lambda: configs.small_cnn(3, 8, 3, (16, "M", 32, "M")),
+    "nopool_pool": lambda: configs.small_cnn(4, 8, 3, (8, 16, "M")),
+    "relayout": lambda: configs.small_cnn(5, 4, 3, (8,)),
+    "deep": lambda: configs.small_cnn(6, 16, 5, (16, 16, "M", 32, "M", 48, "M", 64, "M")),
+}
+
+
+@pytest.mark.parametrize("name", sorted(NETS))
+@pytest.mark.parametrize("n,Z,m", [(1, 1, 1), (2, 1, 2), (2, 2, 1), (3, 1, 3)])
+def test_cnn_partitioned_matches_oracle(name, n, Z, m):
+    net = NETS[name]()
+    Z = min(Z, net.num_layers())
+    X, y = data(net, 24, 10)
+    cfg = TrainConfig(alpha0=0.05, decay=0.01, iterations=3)
+    plan = api.build_plan(net, n, Z, replicate_narrow=True)
+    r = api.train_partitioned(net, Batch(X, y), cfg, plan, m, UpdateMode.sync_barrier,
+                              PartitionedTrainOptions(multiclass_accuracy=True), device_map=[0] * n)
+    W0, b0 = net.pack()
+    Wr, br, lh, ah = cnn_oracle.train(net, X, y, 0.05, 0.01, 3, m)
+    Wg, bg = r.net.pack()
+    d = net_distance(Wg, bg, Wr, br)
+    assert d <= TOL, d
+    for got, ref in zip(r.loss_history, lh):
+        assert abs(got - ref) <= TOL * max(1.0, abs(ref)), (got, ref)
+    assert rel_norm(Wg - W0, Wr - W0) <= 3e-2  # the update itself
+    assert np.allclose(r.acc_history, ah, atol=2.0 / 24)
+
+
+def test_cnn_activations_and_error_signal():
+    net = NETS["pool_pool"]()
+    X, y = data(net, 16, 10, seed=3)
+    ctx = api.Context([0, 0])
+    plan = api.build_plan(net, 2, 1)
+    s = api.Session(ctx, net, 16, plan, 1, UpdateMode.sync_barrier, TrainConfig(alpha0=0.0, decay=0.0, iterations=1),
+                    PartitionedTrainOptions(multiclass_accuracy=True))
+    s.load_batch(X, y)
+    s.step(1)
+    ref = cnn_oracle.forward_acts(net, X.reshape(16, -1))
+    for l in (1, 2):
+        assert rel_norm(s.read_tensor(0, l), ref[l - 1]) <= 2e-3, l
+
+
+def test_cnn_sync_async_and_microbatch_bitwise():
+    net = NETS["deep"]()
+    X, y = data(net, 16, 10, seed=4)
+    cfg = TrainConfig(alpha0=0.05, decay=0.01, iterations=2)
+    plan = api.build_plan(net, 2, 2)
+    o = PartitionedTrainOptions(multiclass_accuracy=True)
+    a = api.train_partitioned(net, Batch(X, y), cfg, plan, 1, UpdateMode.sync_barrier, o, device_map=[0, 0])
+    b = api.train_partitioned(net, Batch(X, y), cfg, plan, 1, UpdateMode.async_per_module, o, device_map=[0, 0])
+    c = api.train_partitioned(net, Batch(X, y), cfg, plan, 4, UpdateMode.sync_barrier, o, device_map=[0, 0])
+    for r in (b, c):
+        assert np.array_equal(a.net.pack()[0], r.net.pack()[0])
+        assert a.loss_history == r.loss_history
+
+
+def test_vgg16_one_step_small_batch():
+    """Full VGG-16 (CIFAR) architecture, batch 8, n=2: one step vs the oracle."""
+    net = configs.vgg16_cifar(seed=7)
+    X, y = data(net, 8, 10, seed=5)
+    cfg = TrainConfig(alpha0=0.01, decay=0.0, iterations=1)
+    plan = api.build_plan(net, 2, 1)
+    r = api.train_partitioned(net, Batch(X, y), cfg, plan, 1, UpdateMode.async_per_module,
+                              PartitionedTrainOptions(multiclass_accuracy=True), device_map=[0, 0])
+    W0, _ = net.pack()
+    Wr, br, lh, _ = cnn_oracle.train(net, X, y, 0.01, 0.0, 1, 1)
+    Wg, bg = r.net.pack()
+    assert abs(r.loss_history[0] - lh[0]) <= TOL * max(1.0, lh[0])
+    assert net_distance(Wg, bg, Wr, br) <= TOL
+    assert rel_norm(Wg - W0, Wr - W0) <= 5e-2
