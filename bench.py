@@ -41,21 +41,35 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
+    # BASELINE.json configs[2]: the north-star target config (conv as implicit GEMM).
+    "vgg16": dict(net="vgg16", batch=512, classes=10, name="VGG-16 (CIFAR 32x32x3, 13 conv + 512->10), batch 512"),
     # BASELINE.json configs[4]: the dense chain the reference itself executes,
     # large enough to be tensor-core bound on one B200.
-    "wide_mlp": dict(dims=[8192] * 5, acts=[1, 1, 1, 2], batch=4096, name="Wide MLP 8192x4 layers, batch 4096"),
+    "wide_mlp": dict(net="wide_mlp", batch=4096, classes=8192, name="Wide MLP 8192x4 layers, batch 4096"),
     # BASELINE.json configs[0]: latency-bound (0.2 GFLOP/step); reported, not a roofline target.
-    "mlp784": dict(dims=[784, 512, 512, 10], acts=[1, 1, 2], batch=64, name="MLP 784-512-512-10, batch 64"),
+    "mlp784": dict(net="mlp784", batch=64, classes=10, name="MLP 784-512-512-10, batch 64"),
 }
 
 
-def algorithmic_flops(dims, batch):
+def build_net(workload, seed=1):
+    from paper_2207_11019_b200 import configs
+
+    return {"vgg16": configs.vgg16_cifar, "wide_mlp": configs.wide_mlp, "mlp784": configs.mlp784}[
+        WORKLOADS[workload]["net"]](seed=seed)
+
+
+def layer_macs(layer, batch):
+    if layer.conv is None:
+        return layer.fan_in() * layer.fan_out() * batch
+    c = layer.conv
+    ho = c.height + 2 * c.pad - c.ksize + 1
+    wo = c.width + 2 * c.pad - c.ksize + 1
+    return batch * ho * wo * layer.fan_out() * layer.fan_in()
+
+
+def algorithmic_flops(net, batch):
     """fwd + wgrad + dgrad (no dgrad for layer 1), 2 FLOPs per MAC."""
-    f = 0.0
-    for l in range(1, len(dims)):
-        mac = dims[l - 1] * dims[l] * batch
-        f += 2 * mac * (3 if l > 1 else 2)
-    return f
+    return sum(2.0 * layer_macs(l, batch) * (3 if i > 0 else 2) for i, l in enumerate(net.layers))
 
 
 def measured_peaks():
@@ -159,14 +173,13 @@ def reference_bounded(workload, nthreads, target_s=12.0):
         return None, f"{REF_SO} missing (build with make -C oracle ref)"
     R = Reference()
     w = WORKLOADS[workload]
-    dims, acts = w["dims"], w["acts"]
-    rng = np.random.default_rng(0)
-    W = np.concatenate([(rng.random(dims[l] * dims[l + 1]) - 0.5) / np.sqrt(dims[l]) for l in range(len(acts))])
-    b = np.concatenate([(rng.random(dims[l + 1]) - 0.5) / np.sqrt(dims[l]) for l in range(len(acts))])
+    net = build_net(workload, seed=0)
+    dims, acts = net.dims(), net.acts()
+    W, b = net.pack()
     n = max(1, min(nthreads, min(dims[1:])))
     plan = R.build_plan(dims, n, 1)
     # calibrate: a tiny probe, then size the sample for ~target_s of CPU work
-    per_sample_flops = algorithmic_flops(dims, 1)
+    per_sample_flops = algorithmic_flops(net, 1)
     probe_rows = 2
     X = rng.standard_normal((probe_rows, dims[0]))
     y = np.arange(probe_rows) % 2
@@ -187,12 +200,50 @@ def reference_bounded(workload, nthreads, target_s=12.0):
     return info, None
 
 
+def port_bounded(workload, nthreads, target_s=12.0):
+    """CPU baseline for the conv configs: the reference has no conv path, so the
+    oracle port (oracle/cnn_oracle.py, float64 PyTorch on the host cores)
+    runs a bounded sample of the same step."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import torch
+
+    import cnn_oracle  # noqa: E402  (baseline infrastructure)
+
+    torch.set_num_threads(nthreads)
+    w = WORKLOADS[workload]
+    net = build_net(workload, seed=0)
+    c = net.layers[0].conv
+    rng = np.random.default_rng(0)
+
+    def run(rows):
+        X = rng.standard_normal((rows, c.height * c.width * net.layers[0].in_units()))
+        y = rng.integers(0, w["classes"], rows)
+        t0 = time.perf_counter()
+        cnn_oracle.train(net, X, y, 1e-4, 1e-2, 1, 1)
+        return time.perf_counter() - t0
+
+    run(2)  # warm-up (thread pool, allocator)
+    t = run(4)
+    rows = int(max(2, min(w["batch"], 4 * target_s / max(t, 1e-3))))
+    dt = run(rows)
+    return {"value": rows / dt, "unit": "samples/s", "cores": nthreads, "kind": "port",
+            "sample": f"{w['name']}: {rows} samples x 1 iteration ({dt:.1f} s); the reference has no conv path, "
+                      f"so this is the fp64 PyTorch-CPU port oracle/cnn_oracle.py on {nthreads} threads",
+            "seconds": dt}, None
+
+
+def cpu_baseline_for(workload, nthreads, target_s=12.0):
+    if build_net(workload).has_conv():
+        return port_bounded(workload, nthreads, target_s)
+    return reference_bounded(workload, nthreads, target_s)
+
+
 def run_reference(args, rank, world, dist):
     if rank != 0:
         barrier(dist)
         return
     nthreads = os.cpu_count() or 1
-    info, err = reference_bounded(args.workload, nthreads, target_s=min(20.0, 6.0 * max(1, args.steps)))
+    info, err = cpu_baseline_for(args.workload, nthreads, target_s=min(20.0, 6.0 * max(1, args.steps)))
     w = WORKLOADS[args.workload]
     if info is None:
         print(json.dumps({"impl": "reference", "unavailable": err}))
@@ -201,7 +252,7 @@ def run_reference(args, rank, world, dist):
     line = {"impl": "reference", "metric": "train samples/sec (fwd+bwd+update)", "value": info["value"],
             "unit": "samples/s", "n_gpus": world, "steps": 1, "warmup": 0, "ms_per_step": 1000.0 * info["seconds"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.workload, "name": w["name"], "dims": w["dims"], "batch": w["batch"]},
+            "config": {"workload": args.workload, "name": w["name"], "batch": w["batch"]},
             "cpu_baseline": info, "e2e": {"value": info["value"], "unit": "samples/s", "h2d_bytes_per_step": 0,
                                           "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -218,7 +269,7 @@ def run_ours(args, rank, world, dist):
 
     n = args.gpus
     w = WORKLOADS[args.workload]
-    dims, acts, batch = w["dims"], w["acts"], w["batch"]
+    batch = w["batch"]
     if rank != 0:
         barrier(dist)  # setup
         barrier(dist)  # before timing
@@ -226,13 +277,13 @@ def run_ours(args, rank, world, dist):
         max_over_ranks(dist, 0.0)
         return
     rng = np.random.default_rng(1)
-    W = np.concatenate([(rng.random(dims[l] * dims[l + 1], dtype=np.float64) - 0.5) / np.sqrt(dims[l])
-                        for l in range(len(acts))])
-    b = np.concatenate([(rng.random(dims[l + 1]) - 0.5) / np.sqrt(dims[l]) for l in range(len(acts))])
-    net = TinyNet.unpack(dims, acts, W, b)
-    X = rng.standard_normal((batch, dims[0]), dtype=np.float32)
-    y = rng.integers(0, dims[-1], batch).astype(np.int32)
-    plan = api.build_plan(dims, n, 1)  # every layer over all n GPUs (build_plan, partition.cpp:110-121)
+    net = build_net(args.workload, seed=1)
+    dims = net.dims()
+    in_feat = net.layers[0].in_units() * (net.layers[0].conv.height * net.layers[0].conv.width
+                                          if net.layers[0].conv else 1)
+    X = rng.standard_normal((batch, in_feat), dtype=np.float32)
+    y = rng.integers(0, w["classes"], batch).astype(np.int32)
+    plan = api.build_plan(net, n, 1)  # every layer over all n GPUs (build_plan, partition.cpp:110-121)
     ctx = api.Context(list(range(n)))
     cfg = TrainConfig(alpha0=1e-4, decay=1e-2, iterations=1)
     opts = PartitionedTrainOptions(multiclass_accuracy=True, use_graph=True, pipeline_gate=2)
@@ -255,7 +306,7 @@ def run_ours(args, rank, world, dist):
     value = batch * args.steps / (ms / 1000.0)
 
     # ---- end to end through the C ABI with pinned host buffers
-    Xp = torch.empty((batch, dims[0]), dtype=torch.float32, pin_memory=True)
+    Xp = torch.empty((batch, in_feat), dtype=torch.float32, pin_memory=True)
     Xp.numpy()[:] = X
     yp = torch.empty(batch, dtype=torch.int32, pin_memory=True)
     yp.numpy()[:] = y
@@ -291,13 +342,14 @@ def run_ours(args, rank, world, dist):
                 "peak_source": f"{peak_src}: bf16_tflops (burst) / 2 (TF32 = half the bf16 tensor rate)",
                 "peak_bf16_burst_measured": peaks.get("bf16_tflops"),
                 "frac_of_bf16_burst": achieved / peaks.get("bf16_tflops", 1612.0),
-                "step_tflops": algorithmic_flops(dims, batch) * args.steps / (ms / 1000.0) / 1e12 / n,
+                "step_tflops": algorithmic_flops(net, batch) * args.steps / (ms / 1000.0) / 1e12 / n,
+                "step_frac": algorithmic_flops(net, batch) * args.steps / (ms / 1000.0) / 1e12 / n / tf32_peak,
                 "per_kind_ms": {k: round(v["ms"], 4) for k, v in prof.items()}}
 
     # ---- reference CPU baseline on a bounded sample (rank 0, N=1 only)
     cpu = None
     if n == 1 and not args.no_cpu_baseline:
-        cpu, err = reference_bounded(args.workload, os.cpu_count() or 1)
+        cpu, err = cpu_baseline_for(args.workload, os.cpu_count() or 1)
         if cpu is None:
             cpu = {"unavailable": err}
         else:
@@ -307,11 +359,13 @@ def run_ours(args, rank, world, dist):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak" if n == 1 else "strong", "vs_baseline": None, "dtype": "tf32",
             "data": "synthetic (X ~ N(0,1), labels uniform over classes, weights U[-0.5,0.5]/sqrt(fan_in))",
-            "config": {"workload": args.workload, "name": w["name"], "dims": dims, "batch": batch, "global_batch": batch,
+            "config": {"workload": args.workload, "name": w["name"], "batch": batch, "global_batch": batch,
+                       "gflop_per_step": algorithmic_flops(net, batch) / 1e9,
                        "plan": f"build_plan n={n} Z=1, m={args.m}, async_per_module, CUDA graph",
                        "parallelism": f"layer-wise partition over {n} GPU(s)",
-                       "l2": "inputs larger than L2 (weights 1 GiB + activations 0.5 GiB per step)"
-                       if args.workload == "wide_mlp" else "working set fits L2 (latency-bound config)"},
+                       "l2": {"wide_mlp": "inputs larger than L2 (weights 1 GiB + activations 0.5 GiB per step)",
+                              "vgg16": "inputs larger than L2 (activations + error signals ~1.5 GiB per step)"}.get(
+                           args.workload, "working set fits L2 (latency-bound config)")},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
             "gpu_launches": sess.kernels_per_step() * args.steps,
             "loss_last": float(lh[-1]) if len(lh) else None}

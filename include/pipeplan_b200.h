@@ -248,6 +248,12 @@ int ppb_session_time_steps(ppb_session* s, int iterations, float* ms_out);
 int ppb_session_profile(ppb_session* s, int iterations, double* ms, int* count, double* flops,
                         int nkinds);
 
+/* Per-op view of the last ppb_session_profile call: op kind, layer, GEMM
+ * tiling (bn | cta_group << 10 | split-K << 12), milliseconds, FLOPs.
+ * *count receives the number of ops (call with cap = 0 to size). */
+int ppb_session_profile_ops(ppb_session* s, int* kind, int* layer, int* info, double* ms, double* flops, int cap,
+                            int* count);
+
 /* ------------------------------------------------------------------ diagnostics */
 
 /* One shard GEMM on device pointers (kernel unit tests): C = A.B^T with the

@@ -506,7 +506,7 @@ class Session:
         return ms.value
 
     OP_KINDS = ("sync", "fwd_gemm", "dgrad_gemm", "wgrad_sgd_gemm", "loss_head", "bwd_merge", "bias_update",
-                "finalize", "peer_copy")
+                "finalize", "peer_copy", "pool_relayout", "conv_merge")
 
     def profile(self, iterations: int = 1) -> dict:
         """Per-op-kind device time / launches / FLOPs over `iterations` eager steps."""
@@ -515,6 +515,19 @@ class Session:
         check(_lib.lib().ppb_session_profile(self._h, iterations, _dp(ms), _ip(cnt), _dp(fl), k))
         return {name: {"ms": float(ms[i]), "launches": int(cnt[i]), "flops": float(fl[i])}
                 for i, name in enumerate(self.OP_KINDS) if cnt[i]}
+
+    def profile_ops(self) -> list:
+        """Per-op records of the last profile() call."""
+        n = C.c_int(0)
+        L = _lib.lib()
+        check(L.ppb_session_profile_ops(self._h, None, None, None, None, None, 0, C.byref(n)))
+        k, lay, inf = (np.zeros(max(n.value, 1), np.int32) for _ in range(3))
+        ms, fl = np.zeros(max(n.value, 1)), np.zeros(max(n.value, 1))
+        check(L.ppb_session_profile_ops(self._h, _ip(k), _ip(lay), _ip(inf), _dp(ms), _dp(fl), n.value, C.byref(n)))
+        return [{"kind": self.OP_KINDS[k[i]] if k[i] < len(self.OP_KINDS) else int(k[i]), "layer": int(lay[i]),
+                 "bn": int(inf[i] & 1023), "cg": int((inf[i] >> 10) & 3), "splits": int(inf[i] >> 12),
+                 "ms": float(ms[i]), "tflops": float(fl[i] / ms[i] / 1e9) if ms[i] > 0 else 0.0}
+                for i in range(n.value)]
 
     def step_host(self, X: np.ndarray, labels: np.ndarray) -> float:
         """End-to-end step from host buffers (H2D X/labels, step, D2H loss)."""

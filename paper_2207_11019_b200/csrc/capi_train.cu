@@ -212,6 +212,11 @@ extern "C" int ppb_session_profile(ppb_session* s, int iterations, double* ms, i
     return ppb_guard([&] { s->s->profile(iterations, ms, count, flops, nkinds); });
 }
 
+extern "C" int ppb_session_profile_ops(ppb_session* s, int* kind, int* layer, int* info, double* ms, double* flops,
+                                       int cap, int* count) {
+    return ppb_guard([&] { *count = s->s->profile_ops(kind, layer, info, ms, flops, cap); });
+}
+
 extern "C" int ppb_session_kernels_per_step(ppb_session* s, int* out) {
     return ppb_guard([&] { *out = s->s->kernels_per_step(); });
 }

@@ -10,6 +10,8 @@
 // wgrad   : dw[u x k*k*ck]   = sum_{pixel}  d_pad(pixel + q, k) x_pad(pixel shifted by tap, c)
 #pragma once
 
+#include <utility>
+
 #include "gemm.h"
 
 namespace ppb {
@@ -111,8 +113,10 @@ inline GemmDesc conv_dgrad_desc(const ConvShape& s, const float* d_pad, long lon
     return d;
 }
 
+// transposed = true computes dW^T (M = k*k*ck, N = u): better tile occupancy
+// when u < 128; pair it with EpiParams::sgd_t.
 inline GemmDesc conv_wgrad_desc(const ConvShape& s, const float* d_pad, long long ldd, const float* x_pad,
-                                long long ldx) {
+                                long long ldx, bool transposed = false) {
     GemmDesc d;
     const int q = s.q();
     d.a.ptr = d_pad;
@@ -142,6 +146,10 @@ inline GemmDesc conv_wgrad_desc(const ConvShape& s, const float* d_pad, long lon
     d.M = s.u;
     d.N = s.ksz * s.ksz * s.ck();
     d.K = s.N * s.Ho() * s.Wo();
+    if (transposed) {
+        std::swap(d.a, d.b);
+        std::swap(d.M, d.N);
+    }
     return d;
 }
 

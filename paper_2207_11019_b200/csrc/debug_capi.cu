@@ -10,6 +10,22 @@
 
 using namespace ppb;
 
+namespace {
+// split-K workspace for the diagnostic entry points (grown, never freed)
+float* debug_ws(size_t n) {
+    static float* p[32] = {};
+    static size_t cap[32] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cap[dev & 31] < n) {
+        if (p[dev & 31]) cudaFree(p[dev & 31]);
+        if (cudaMalloc(&p[dev & 31], n * sizeof(float)) != cudaSuccess) return nullptr;
+        cap[dev & 31] = n;
+    }
+    return p[dev & 31];
+}
+}  // namespace
+
 extern "C" int ppb_debug_gemm(const float* a, int a_rows, int a_cols, long long lda, int a_mn,
                               const float* b, int b_rows, int b_cols, long long ldb, int b_mn,
                               int M, int N, int K, int mode, float* c, long long ldc,
@@ -42,7 +58,7 @@ extern "C" int ppb_debug_gemm(const float* a, int a_rows, int a_cols, long long 
     } else {
         TcGemmPlan p;
         char err[256];
-        if (!tc_gemm_prepare(d, &p, force_bn, err, sizeof(err))) {
+        if (!tc_gemm_prepare(d, &p, force_bn, err, sizeof(err), force_bn == 0 ? WsAlloc(debug_ws) : WsAlloc())) {
             ppb_set_error(err);
             return PPB_ERR_CUDA;
         }
@@ -75,16 +91,33 @@ extern "C" int ppb_debug_conv(int which, const float* x_pad, int N, int H, int W
         ppb_set_error("conv geometry does not tile into TMA boxes");
         return PPB_ERR_INVALID_ARGUMENT;
     }
+    // which = 3: wgrad in the transposed orientation (dW^T), stored as SGD
+    // with alpha = 1 and inv_b = -1 onto out (zeroed by the caller) so that
+    // out[u][k*k*ck] receives dW.
     GemmDesc d = which == 0 ? conv_fwd_desc(s, x_pad, ldx, w)
                  : which == 1 ? conv_dgrad_desc(s, d_pad, ldd, w)
-                              : conv_wgrad_desc(s, d_pad, ldd, x_pad, ldx);
+                              : conv_wgrad_desc(s, d_pad, ldd, x_pad, ldx, which == 3);
     d.epi.mode = EPI_STORE;
     d.epi.dst[0] = out;
     d.epi.ndst = 1;
     d.epi.ldd = ldo;
+    static double* one = nullptr;
+    if (which == 3) {
+        if (one == nullptr) {
+            const double v = 1.0;
+            cudaMalloc(&one, sizeof(double));
+            cudaMemcpy(one, &v, sizeof(double), cudaMemcpyHostToDevice);
+        }
+        d.epi.mode = EPI_SGD;
+        d.epi.W = out;
+        d.epi.ldw = ldo;
+        d.epi.sgd_t = 1;
+        d.epi.alpha = one;
+        d.epi.inv_b = -1.f;
+    }
     TcGemmPlan p;
     char err[256];
-    if (!tc_gemm_prepare(d, &p, force_bn, err, sizeof(err))) {
+    if (!tc_gemm_prepare(d, &p, force_bn, err, sizeof(err), force_bn == 0 ? WsAlloc(debug_ws) : WsAlloc())) {
         ppb_set_error(err);
         return PPB_ERR_CUDA;
     }

@@ -81,19 +81,31 @@ __device__ __forceinline__ void epilogue32(const EpiParams& p, int m, int n0, fl
             break;
         }
         case EPI_SGD: {
-            float w[32];
-            float* row = p.W + static_cast<long long>(m) * p.ldw;
-            load_row32(row, n0, nvalid, w);
             const float alpha = static_cast<float>(*p.alpha);
             bool bad = false;
+            if (p.sgd_t) {  // C = dW^T: lanes hold consecutive m, so W[n][m] stores coalesce across the warp
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const float g = acc[i] * p.inv_b;
-                bad |= (i < nvalid) && !isfinite(g);
-                w[i] -= alpha * g;
+                for (int i = 0; i < 32; ++i) {
+                    if (i < nvalid) {
+                        const float g = acc[i] * p.inv_b;
+                        bad |= !isfinite(g);
+                        float* wp = p.W + static_cast<long long>(n0 + i) * p.ldw + m;
+                        *wp -= alpha * g;
+                    }
+                }
+            } else {
+                float w[32];
+                float* row = p.W + static_cast<long long>(m) * p.ldw;
+                load_row32(row, n0, nvalid, w);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const float g = acc[i] * p.inv_b;
+                    bad |= (i < nvalid) && !isfinite(g);
+                    w[i] -= alpha * g;
+                }
+                store_row32(row, n0, nvalid, w);
             }
             if (bad && p.flag != nullptr) atomicOr(p.flag, 1);
-            store_row32(row, n0, nvalid, w);
             break;
         }
         case EPI_SLOTS: {

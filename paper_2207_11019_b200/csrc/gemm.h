@@ -49,9 +49,10 @@ struct EpiParams {
     const float* mask = nullptr;
     long long ldm = 0;
     int mcol0 = 0;
-    // EPI_SGD
+    // EPI_SGD (sgd_t: the product is dW^T, so C(m, n) updates W[n][m])
     float* W = nullptr;
     long long ldw = 0;
+    int sgd_t = 0;
     const double* alpha = nullptr;  // device scalar (the reference keeps alpha in double)
     float inv_b = 1.f;
     int* flag = nullptr;
@@ -103,6 +104,17 @@ struct Operand {
     ConvGeom geom;
     // conv tensor extents (elements): [imgs][hp][wp][ch], ch pitch `ld`
     int ch = 0, wp = 0, hp = 0, imgs = 0;
+};
+
+// Split-K: the K loop is cut into `splits` ranges of `kps` 32-wide blocks; each
+// range's raw partial sums go to ws + split*stride (row pitch ld) and a
+// reduction kernel sums the splits in order before the real epilogue.
+struct SplitK {
+    int splits = 1;
+    int kps = 1 << 30;
+    float* ws = nullptr;
+    long long ld = 0;
+    long long stride = 0;
 };
 
 struct GemmDesc {

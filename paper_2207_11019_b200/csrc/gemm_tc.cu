@@ -114,7 +114,8 @@ template <bool A_MN, bool B_MN, int BN, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                    int M, int N, int K, const __grid_constant__ EpiParams epi,
-                   const __grid_constant__ ConvGeom ga, const __grid_constant__ ConvGeom gb) {
+                   const __grid_constant__ ConvGeom ga, const __grid_constant__ ConvGeom gb,
+                   const __grid_constant__ SplitK sk) {
     using C = TcCfg<BN, CG>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -133,7 +134,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int TM = kBM * CG;  // tile rows
     const int num_m = (M + TM - 1) / TM;
     const int num_n = (N + BN - 1) / BN;
-    const int num_tiles = num_m * num_n;
+    const int num_mn = num_m * num_n;
+    const int num_tiles = num_mn * sk.splits;  // split-K: tile = (split, n, m)
     const int nk = (K + kBK - 1) / kBK;
     const int unit = blockIdx.x / CG;  // cluster (or CTA) index
     const int units = gridDim.x / CG;
@@ -167,9 +169,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = unit; tile < num_tiles; tile += units) {
-                const int m0 = (tile % num_m) * TM + static_cast<int>(rank) * kBM;
-                const int n0 = (tile / num_m) * BN + static_cast<int>(rank) * C::kBNc;
-                for (int kb = 0; kb < nk; ++kb) {
+                const int mn = tile % num_mn, split = tile / num_mn;
+                const int m0 = (mn % num_m) * TM + static_cast<int>(rank) * kBM;
+                const int n0 = (mn / num_m) * BN + static_cast<int>(rank) * C::kBNc;
+                const int kb_end = min(nk, (split + 1) * sk.kps);
+                for (int kb = split * sk.kps; kb < kb_end; ++kb) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     uint8_t* a_dst = sA + stage * C::kStageA;
                     uint8_t* b_dst = sB + stage * C::kStageB;
@@ -205,7 +209,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
-                for (int kb = 0; kb < nk; ++kb) {
+                const int split = tile / num_mn;
+                const int kb0 = split * sk.kps, kb_end = min(nk, (split + 1) * sk.kps);
+                for (int kb = kb0; kb < kb_end; ++kb) {
                     mbar_wait(&full_bar[stage], phase);
                     tc_fence_after();
                     if (elect_one()) {
@@ -222,8 +228,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                      : umma_desc<kLayoutSW128>(a_addr + kk * 32, 16, 1024);
                             const uint64_t bd = B_MN ? umma_desc<kLayoutSW128Base32>(b_addr + kk * 1024, 4096, 512)
                                                      : umma_desc<kLayoutSW128>(b_addr + kk * 32, 16, 1024);
-                            if (CG == 2) mma_tf32_pair(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
-                            else mma_tf32(d_tmem, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+                            const uint32_t accum = (kb != kb0 || kk != 0) ? 1u : 0u;
+                            if (CG == 2) mma_tf32_pair(d_tmem, ad, bd, idesc, accum);
+                            else mma_tf32(d_tmem, ad, bd, idesc, accum);
                         }
                         if (CG == 2) mma_commit_pair(&empty_bar[stage]);
                         else mma_commit(&empty_bar[stage]);
@@ -248,8 +255,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty_bar[0]), 0) : 0;
         int local = 0;
         for (int tile = unit; tile < num_tiles; tile += units, ++local) {
-            const int m0 = (tile % num_m) * TM + static_cast<int>(rank) * kBM;
-            const int n0 = (tile / num_m) * BN;
+            const int mn = tile % num_mn, split = tile / num_mn;
+            const int m0 = (mn % num_m) * TM + static_cast<int>(rank) * kBM;
+            const int n0 = (mn / num_m) * BN;
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             mbar_wait(&tfull_bar[acc], acc_phase);
@@ -263,7 +271,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float v[32];
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-                epilogue32(epi, m, n0 + c * 32, v);
+                if (sk.splits > 1) {  // raw partial sums; splitk_epilogue_kernel reduces + applies the epilogue
+                    const int nn = n0 + c * 32;
+                    if (m < M && nn < N)
+                        store_row32(sk.ws + split * sk.stride + static_cast<long long>(m) * sk.ld, nn,
+                                    N - nn < 32 ? N - nn : 32, v);
+                } else {
+                    epilogue32(epi, m, n0 + c * 32, v);
+                }
             }
             tc_fence_before();
             __syncwarp();
@@ -282,6 +297,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (CG == 2) tmem_dealloc_pair(tmem_base, C::kTmemCols);
         else tmem_dealloc(tmem_base, C::kTmemCols);
     }
+}
+
+// Split-K reduction: C(m, n) = sum over splits in order (deterministic), then
+// the GEMM's real epilogue.  One thread per (row, 32-column chunk).
+__global__ void splitk_epilogue_kernel(const __grid_constant__ EpiParams epi, const __grid_constant__ SplitK sk,
+                                       int M, int N) {
+    const int chunks = (N + 31) / 32;
+    const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (idx >= static_cast<long long>(M) * chunks) return;
+    // consecutive threads take consecutive rows of one chunk (coalesced for sgd_t)
+    const int m = static_cast<int>(idx % M);
+    const int n0 = static_cast<int>(idx / M) * 32;
+    const int nvalid = N - n0 < 32 ? N - n0 : 32;
+    float acc[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+    for (int s = 0; s < sk.splits; ++s) {
+        float v[32];
+        load_row32(sk.ws + s * sk.stride + static_cast<long long>(m) * sk.ld, n0, nvalid, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] += v[i];
+    }
+    epilogue32(epi, m, n0, acc);
 }
 
 // ---------------------------------------------------------------- host side
@@ -462,13 +500,18 @@ cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, tc_gemm_kernel<A_MN, B_MN, BN, CG>, p.ta, p.tb, p.M, p.N, p.K, p.epi,
-                              p.ga, p.gb);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<A_MN, B_MN, BN, CG>, p.ta, p.tb, p.M, p.N, p.K, p.epi,
+                                       p.ga, p.gb, p.sk);
+    if (e != cudaSuccess || p.sk.splits <= 1) return e;
+    const long long threads = static_cast<long long>(p.M) * ((p.N + 31) / 32);
+    splitk_epilogue_kernel<<<static_cast<unsigned>((threads + 127) / 128), 128, 0, s>>>(p.epi, p.sk, p.M, p.N);
+    return cudaGetLastError();
 }
 
 }  // namespace
 
-bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err, size_t errlen) {
+bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err, size_t errlen,
+                     const WsAlloc& ws_alloc) {
     TcGemmPlan p;
     p.M = d.M;
     p.N = d.N;
@@ -483,6 +526,16 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
         return false;
     }
     const int sms = sm_count();
+    const int nk = (d.K + kBK - 1) / kBK;
+    const bool can_split = static_cast<bool>(ws_alloc) && nk >= 16;
+    // Split count that fills the SMs for a tile grid (>= 8 K blocks per split).
+    auto splits_for = [&](int tiles, int units) {
+        if (!can_split || tiles >= units) return 1;
+        int sp = units / tiles;
+        if (sp > nk / 8) sp = nk / 8;
+        if (sp > 64) sp = 64;
+        return sp < 1 ? 1 : sp;
+    };
     // force_bn: 0 = auto; 64/128/256 = 1-CTA tiles of that width;
     // -128/-256 = CTA-pair tiles (256 x |bn|).
     int bn = 256, cg = 1;
@@ -492,22 +545,57 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
         bn = -force_bn;
         cg = 2;
     } else {
-        // CTA pairs whenever the pair tiles still fill every SM pair;
-        // otherwise the widest 1-CTA tile that fills the SMs, down to 64.
-        const int pair_tiles = ((d.M + 255) / 256) * ((d.N + 255) / 256);
-        if (d.M > 128 && pair_tiles >= sms / 2) {
-            cg = 2;
-            bn = 256;
-        } else {
-            const int num_m = (d.M + kBM - 1) / kBM;
-            while (bn > 64 && num_m * ((d.N + bn - 1) / bn) < sms) bn /= 2;
+        // Score each tile shape by (relative MMA efficiency of the shape,
+        // measured on the wide-MLP GEMM) x (fraction of the tile that is
+        // real output) x (wave fill after split-K); keep the best.
+        struct Cand {
+            int cg, bn;
+            double eff;
+        };
+        const Cand cands[] = {{2, 256, 1.0}, {2, 128, 0.85}, {1, 256, 0.93}, {1, 128, 0.8}, {1, 64, 0.55}};
+        double best = -1;
+        for (const Cand& c : cands) {
+            if (c.cg == 2 && d.M <= 128) continue;
+            const int tm = kBM * c.cg;
+            const int num_m = (d.M + tm - 1) / tm, num_n = (d.N + c.bn - 1) / c.bn;
+            const int tiles = num_m * num_n, units = sms / c.cg;
+            const int work = tiles * splits_for(tiles, units);
+            const int waves = (work + units - 1) / units;
+            const double fill = static_cast<double>(work) / (static_cast<double>(waves) * units);
+            const double frac = static_cast<double>(d.M) / (num_m * tm) * static_cast<double>(d.N) / (num_n * c.bn);
+            const double score = c.eff * fill * frac;
+            if (score > best + 1e-9) {
+                best = score;
+                cg = c.cg;
+                bn = c.bn;
+            }
         }
     }
     p.bn = bn;
     p.cg = cg;
     const int tiles = ((d.M + kBM * cg - 1) / (kBM * cg)) * ((d.N + bn - 1) / bn);
     const int units = sms / cg;
-    p.grid = (tiles < units ? tiles : units) * cg;
+    // Split-K when the output tiles cannot fill the SMs (e.g. conv wgrad:
+    // small C_out x 9*C_in output, K = every pixel of the batch); partial
+    // sums are reduced in split order (deterministic).
+    {
+        int splits = splits_for(tiles, units);
+        if (splits >= 2) {
+            const int kps = (nk + splits - 1) / splits;
+            splits = (nk + kps - 1) / kps;
+            p.sk.splits = splits;
+            p.sk.kps = kps;
+            p.sk.ld = (d.N + 3) / 4 * 4;
+            p.sk.stride = p.sk.ld * d.M;
+            p.sk.ws = ws_alloc(static_cast<size_t>(p.sk.stride) * splits);
+            if (p.sk.ws == nullptr) {
+                snprintf(err, errlen, "split-K workspace allocation failed");
+                return false;
+            }
+        }
+    }
+    const int work = tiles * p.sk.splits;
+    p.grid = (work < units ? work : units) * cg;
     // A: M extent x K.  K-major: rows=M, cols=K, box {32, 128}.  MN-major:
     // stored K x M (rows=K, cols=M), box {32, 32}.  B rows per CTA = bn / cg.
     p.ga = d.a.geom;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstddef>
+#include <functional>
 
 #include "gemm.h"
 
@@ -21,9 +22,14 @@ struct TcGemmPlan {
     bool a_mn = false, b_mn = false;
     EpiParams epi;
     ConvGeom ga, gb;
+    SplitK sk;
 };
 
-bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err, size_t errlen);
+// ws_alloc (optional): allocates split-K workspace (floats) on the GEMM's
+// device; without it the GEMM never splits K.
+using WsAlloc = std::function<float*(size_t)>;
+bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err, size_t errlen,
+                     const WsAlloc& ws_alloc = nullptr);
 cudaError_t tc_gemm_launch(const TcGemmPlan& p, cudaStream_t s);
 cudaError_t tc_gemm_init_device();
 

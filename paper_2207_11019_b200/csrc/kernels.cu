@@ -273,76 +273,168 @@ __global__ void pad_input_kernel(const T* __restrict__ src, int imgs, int H, int
     }
 }
 
+// Threads own a fixed group of VEC channels for the whole grid-stride loop
+// (blockDim and the grid stride are multiples of the group count), which keeps
+// loads/stores vectorised along channels and lets conv_merge accumulate the
+// bias gradient of its channels in registers.
+template <int VEC>
 __global__ void pool_fwd_kernel(const float* __restrict__ U, long long ldu, int imgs, int Ho, int Wo, int uch,
                                 int pool, unsigned char* __restrict__ argmax, ActLayout out, PoolDsts dsts) {
     const int Hq = Ho / pool, Wq = Wo / pool;
-    const long long total = static_cast<long long>(imgs) * Hq * Wq * uch;
+    const int groups = uch / VEC;
+    const long long total = static_cast<long long>(imgs) * Hq * Wq * groups;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int c = static_cast<int>(i % uch);
-        long long pp = i / uch;  // pooled pixel
+        const int g = static_cast<int>(i % groups);
+        const long long pp = i / groups;  // pooled pixel
         const int x = static_cast<int>(pp % Wq);
-        const int y = static_cast<int>((pp / Wq) % Hq);
-        const long long n = pp / (static_cast<long long>(Wq) * Hq);
-        float v;
+        const long long t = pp / Wq;
+        const int y = static_cast<int>(t % Hq);
+        const long long n = t / Hq;
+        const int c0 = g * VEC;
+        float v[VEC];
+        unsigned char arg[VEC];
         if (pool == 1) {
-            v = U[pp * ldu + c];
+            if (VEC == 4) {
+                const float4 a = *reinterpret_cast<const float4*>(U + pp * ldu + c0);
+                v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+            } else {
+                v[0] = U[pp * ldu + c0];
+            }
         } else {
             const long long base = (n * Ho + 2 * y) * Wo + 2 * x;
-            float best = U[base * ldu + c];
-            int arg = 0;
-            const float v1 = U[(base + 1) * ldu + c];
-            const float v2 = U[(base + Wo) * ldu + c];
-            const float v3 = U[(base + Wo + 1) * ldu + c];
-            if (v1 > best) { best = v1; arg = 1; }
-            if (v2 > best) { best = v2; arg = 2; }
-            if (v3 > best) { best = v3; arg = 3; }
-            v = best;
-            argmax[pp * uch + c] = static_cast<unsigned char>(arg);
+            const long long offs[4] = {base, base + 1, base + Wo, base + Wo + 1};
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) {
+                v[k] = -INFINITY;
+                arg[k] = 0;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                float e[VEC];
+                if (VEC == 4) {
+                    const float4 a = *reinterpret_cast<const float4*>(U + offs[q] * ldu + c0);
+                    e[0] = a.x; e[1] = a.y; e[2] = a.z; e[3] = a.w;
+                } else {
+                    e[0] = U[offs[q] * ldu + c0];
+                }
+#pragma unroll
+                for (int k = 0; k < VEC; ++k)
+                    if (q == 0 || e[k] > v[k]) {  // first max wins
+                        v[k] = e[k];
+                        arg[k] = static_cast<unsigned char>(q);
+                    }
+            }
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) argmax[pp * uch + c0 + k] = arg[k];
         }
-        long long o;
         if (out.kind == 0) {
-            o = ((n * out.hp + y + out.pad) * out.wp + x + out.pad) * out.ld + out.col0 + c;
+            const long long o = ((n * out.hp + y + out.pad) * out.wp + x + out.pad) * out.ld + out.col0 + c0;
+            for (int d = 0; d < dsts.n; ++d) {
+                if (VEC == 4) *reinterpret_cast<float4*>(dsts.ptr[d] + o) = make_float4(v[0], v[1], v[2], v[3]);
+                else dsts.ptr[d][o] = v[0];
+            }
         } else {
-            o = n * out.ld + static_cast<long long>(out.col0 + c) * Hq * Wq + static_cast<long long>(y) * Wq + x;
+            for (int k = 0; k < VEC; ++k) {
+                const long long o = n * out.ld + static_cast<long long>(out.col0 + c0 + k) * Hq * Wq +
+                                    static_cast<long long>(y) * Wq + x;
+                for (int d = 0; d < dsts.n; ++d) dsts.ptr[d][o] = v[k];
+            }
         }
-        for (int d = 0; d < dsts.n; ++d) dsts.ptr[d][o] = v;
     }
 }
 
-__global__ void conv_merge_kernel(ConvMerge m) {
-    const long long total = static_cast<long long>(m.imgs) * m.Ho * m.Wo * m.uch;
+template <int VEC>
+__global__ void conv_merge_kernel(ConvMerge m, float* __restrict__ db_partial) {
+    const int groups = m.uch / VEC;
+    const long long total = static_cast<long long>(m.imgs) * m.Ho * m.Wo * groups;
     const int Hg = m.Ho / m.pool, Wg = m.Wo / m.pool;
     const int hq = m.Ho + 2 * m.q, wq = m.Wo + 2 * m.q;
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int c = static_cast<int>(i % m.uch);
-        long long pix = i / m.uch;
+    float db[VEC];
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) db[k] = 0.f;
+    const long long start = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    const int g = static_cast<int>(start % groups);  // constant: blockDim and the stride are multiples of groups
+    const int c0 = g * VEC;
+    for (long long i = start; i < total; i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long pix = i / groups;
         const int w = static_cast<int>(pix % m.Wo);
-        const int h = static_cast<int>((pix / m.Wo) % m.Ho);
-        const long long n = pix / (static_cast<long long>(m.Wo) * m.Ho);
-        float g = 0.f;
+        const long long t = pix / m.Wo;
+        const int h = static_cast<int>(t % m.Ho);
+        const long long n = t / m.Ho;
+        float gr[VEC];
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) gr[k] = 0.f;
         int y = h, x = w;
-        bool live = true;
+        bool in_grid = true;
         if (m.pool == 2) {
             y = h >> 1;
             x = w >> 1;
-            live = y < Hg && x < Wg &&
-                   m.argmax[((n * Hg + y) * Wg + x) * m.uch + c] == static_cast<unsigned char>(((h & 1) << 1) | (w & 1));
+            in_grid = y < Hg && x < Wg;
         }
-        if (live) {
-            const long long idx = m.slot_kind == 0 ? ((n * Hg + y) * Wg + x) * m.lds + c
-                                                   : n * m.lds + static_cast<long long>(c) * Hg * Wg + y * Wg + x;
-            g = m.slots.slot[0][idx];
-            for (int k = 1; k < m.slots.n; ++k) g += m.slots.slot[k][idx];
+        if (in_grid) {
+            const long long gp = (n * Hg + y) * Wg + x;
+            if (m.slot_kind == 0) {
+                const long long idx = gp * m.lds + c0;
+                for (int s = 0; s < m.slots.n; ++s) {
+                    if (VEC == 4) {
+                        const float4 a = *reinterpret_cast<const float4*>(m.slots.slot[s] + idx);
+                        gr[0] += a.x; gr[1] += a.y; gr[2] += a.z; gr[3] += a.w;
+                    } else {
+                        gr[0] += m.slots.slot[s][idx];
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < VEC; ++k) {
+                    const long long idx = n * m.lds + static_cast<long long>(c0 + k) * Hg * Wg + y * Wg + x;
+                    for (int s = 0; s < m.slots.n; ++s) gr[k] += m.slots.slot[s][idx];
+                }
+            }
+            if (m.pool == 2) {
+                const unsigned char want = static_cast<unsigned char>(((h & 1) << 1) | (w & 1));
+#pragma unroll
+                for (int k = 0; k < VEC; ++k)
+                    if (m.argmax[gp * m.uch + c0 + k] != want) gr[k] = 0.f;
+            }
         }
         if (m.mask_kind == 1) {
-            if (!(m.U[pix * m.ldu + c] > 0.f)) g = 0.f;
+            const float* up = m.U + pix * m.ldu + c0;
+#pragma unroll
+            for (int k = 0; k < VEC; ++k)
+                if (!(up[k] > 0.f)) gr[k] = 0.f;
         } else if (m.mask_kind == 2) {
             const ActLayout& a = m.act_layout;
-            if (!(m.act[((n * a.hp + h + a.pad) * a.wp + w + a.pad) * a.ld + a.col0 + c] > 0.f)) g = 0.f;
+            const float* ap = m.act + ((n * a.hp + h + a.pad) * a.wp + w + a.pad) * a.ld + a.col0 + c0;
+#pragma unroll
+            for (int k = 0; k < VEC; ++k)
+                if (!(ap[k] > 0.f)) gr[k] = 0.f;
         }
-        m.d_pad[((n * hq + h + m.q) * wq + w + m.q) * m.ldd + c] = g;
+        float* out = m.d_pad + ((n * hq + h + m.q) * wq + w + m.q) * m.ldd + c0;
+        if (VEC == 4) {
+            *reinterpret_cast<float4*>(out) = make_float4(gr[0], gr[1], gr[2], gr[3]);
+        } else {
+            out[0] = gr[0];
+        }
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) db[k] += gr[k];
+    }
+    // deterministic per-block channel partials: threads of the same channel
+    // group are threadIdx.x = g' + groups * j; sum them in j order
+    extern __shared__ float sh[];
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) sh[threadIdx.x * VEC + k] = db[k];
+    __syncthreads();
+    if (threadIdx.x < groups) {
+        float acc[VEC];
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) acc[k] = 0.f;
+        for (int t = threadIdx.x; t < static_cast<int>(blockDim.x); t += groups)
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) acc[k] += sh[t * VEC + k];
+#pragma unroll
+        for (int k = 0; k < VEC; ++k)
+            db_partial[static_cast<long long>(blockIdx.x) * m.uch + threadIdx.x * VEC + k] = acc[k];
     }
 }
 
@@ -416,18 +508,54 @@ cudaError_t launch_pad_input(const double* src64, const float* src32, int imgs, 
     return cudaGetLastError();
 }
 
+bool vec4_ok(long long a, long long b = 0, long long c = 0) { return a % 4 == 0 && b % 4 == 0 && c % 4 == 0; }
+
+int group_block(int groups) {
+    // a multiple of `groups` near 256 threads
+    int b = groups >= 256 ? groups : (256 / groups) * groups;
+    return b > 1024 ? groups : b;
+}
+
 cudaError_t launch_pool_fwd(const float* U, long long ldu, int imgs, int Ho, int Wo, int uch, int pool,
                             unsigned char* argmax, const ActLayout& out, const PoolDsts& dsts, cudaStream_t s) {
     const long long n = static_cast<long long>(imgs) * (Ho / pool) * (Wo / pool) * uch;
     if (n <= 0) return cudaSuccess;
-    pool_fwd_kernel<<<grid_for(n, 256), 256, 0, s>>>(U, ldu, imgs, Ho, Wo, uch, pool, argmax, out, dsts);
+    bool v4 = vec4_ok(uch, ldu) && (out.kind != 0 || vec4_ok(out.ld, out.col0)) &&
+              reinterpret_cast<uintptr_t>(U) % 16 == 0;
+    for (int d = 0; d < dsts.n; ++d) v4 = v4 && reinterpret_cast<uintptr_t>(dsts.ptr[d]) % 16 == 0;
+    if (v4) {
+        pool_fwd_kernel<4><<<grid_for(n / 4, 256), 256, 0, s>>>(U, ldu, imgs, Ho, Wo, uch, pool, argmax, out, dsts);
+    } else {
+        pool_fwd_kernel<1><<<grid_for(n, 256), 256, 0, s>>>(U, ldu, imgs, Ho, Wo, uch, pool, argmax, out, dsts);
+    }
     return cudaGetLastError();
 }
 
-cudaError_t launch_conv_merge(const ConvMerge& m, cudaStream_t s) {
+int conv_merge_blocks() { return 148 * 4; }
+
+cudaError_t launch_conv_merge(const ConvMerge& m, float* db_partial, cudaStream_t s) {
     const long long n = static_cast<long long>(m.imgs) * m.Ho * m.Wo * m.uch;
-    if (n <= 0) return cudaSuccess;
-    conv_merge_kernel<<<grid_for(n, 256), 256, 0, s>>>(m);
+    bool v4 = m.slot_kind == 0 && vec4_ok(m.uch, m.lds, m.ldd) && (m.mask_kind != 1 || vec4_ok(m.ldu)) &&
+              (m.mask_kind != 2 || vec4_ok(m.act_layout.ld, m.act_layout.col0)) &&
+              reinterpret_cast<uintptr_t>(m.d_pad) % 16 == 0;
+    for (int k = 0; k < m.slots.n; ++k) v4 = v4 && reinterpret_cast<uintptr_t>(m.slots.slot[k]) % 16 == 0;
+    const int vec = v4 ? 4 : 1;
+    const int groups = m.uch / vec;
+    const int block = group_block(groups);
+    const int grid = conv_merge_blocks();
+    const size_t shmem = sizeof(float) * block * vec;
+    if (n <= 0) {
+        return cudaMemsetAsync(db_partial, 0, sizeof(float) * grid * m.uch, s);
+    }
+    if (v4) conv_merge_kernel<4><<<grid, block, shmem, s>>>(m, db_partial);
+    else conv_merge_kernel<1><<<grid, block, shmem, s>>>(m, db_partial);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bias_from_partials(const float* partial, int chunks, int u, float* bias, const double* alpha,
+                                      float inv_b, cudaStream_t s) {
+    if (u <= 0) return cudaSuccess;
+    bias_update_kernel<<<u, kRowThreads, 0, s>>>(partial, u, chunks, bias, alpha, inv_b);
     return cudaGetLastError();
 }
 

@@ -103,7 +103,14 @@ struct ConvMerge {
     int q = 0;
     long long ldd = 0;
 };
-cudaError_t launch_conv_merge(const ConvMerge& m, cudaStream_t s);
+// Also writes the merge's bias-gradient partials db_partial[conv_merge_blocks()][uch]
+// (column sums of the produced error signal, deterministic per block).
+int conv_merge_blocks();
+cudaError_t launch_conv_merge(const ConvMerge& m, float* db_partial, cudaStream_t s);
+
+// bias -= alpha * (sum_k partial[k][c] / b) over `chunks` partial rows.
+cudaError_t launch_bias_from_partials(const float* partial, int chunks, int u, float* bias, const double* alpha,
+                                      float inv_b, cudaStream_t s);
 
 // Per-GPU step state, updated once per iteration by the finalize kernel.
 struct StepState {

@@ -396,7 +396,9 @@ void Session::alloc_buffers() {
                 wl.delta_img = wl.ldd;
             }
             wl.delta = static_cast<float*>(g.alloc(sizeof(float) * b * wl.delta_img));
-            wl.partial = static_cast<float*>(g.alloc(sizeof(float) * kColsumChunks * wl.u));  // upper bound
+            // bias-gradient partials: dense colsum chunks, or one row per (micro-batch, merge block) for conv
+            const long long prow = li.kind == 1 ? static_cast<long long>(cfg_.m) * conv_merge_blocks() : kColsumChunks;
+            wl.partial = static_cast<float*>(g.alloc(sizeof(float) * prow * wl.u));
             // upload the shard rows [lo, hi) (train_partitioned.cpp:168-169), fp64 -> fp32;
             // conv rows [k][k][C_in] go to the GEMM layout [k*k][ck] (zero-padded channels)
             tmp.assign(static_cast<size_t>(wl.u) * wl.ldw, 0.f);
@@ -457,6 +459,8 @@ int Session::add_op(int gpu, cudaStream_t s, std::function<cudaError_t()> f, std
     Op op;
     op.kind = kind;
     op.flops = flops;
+    op.layer = cur_layer_;
+    op.info = (kind == OP_FWD_GEMM || kind == OP_DGRAD_GEMM || kind == OP_WGRAD_GEMM) ? cur_info_ : 0;
     op.gpu = gpu;
     op.stream = s;
     op.launch = std::move(f);
@@ -481,10 +485,13 @@ void Session::build_ops() {
         if (tf32) return [p, s]() { return tc_gemm_launch(*p, s); };
         return [d, s]() { return simt_gemm_launch(*d, s); };
     };
-    auto prepare = [&](GemmDesc& d, TcGemmPlan& p) {
+    auto prepare = [&](GemmDesc& d, TcGemmPlan& p, int gpu) {
         if (!tf32) return;
         char err[256];
-        if (!tc_gemm_prepare(d, &p, 0, err, sizeof(err))) throw std::runtime_error(std::string("GEMM setup: ") + err);
+        Gpu* g = &gpu_of(gpu);
+        WsAlloc ws = [g](size_t n) { return static_cast<float*>(g->alloc(sizeof(float) * n)); };
+        if (!tc_gemm_prepare(d, &p, 0, err, sizeof(err), ws)) throw std::runtime_error(std::string("GEMM setup: ") + err);
+        cur_info_ = p.bn | (p.cg << 10) | (p.sk.splits << 12);
     };
     auto module_of_layer = [&](int l) -> const SubModule& {
         for (const SubModule& sm : plan_.subs)
@@ -518,6 +525,7 @@ void Session::build_ops() {
         const int rows = mb_sizes_[j];
         const long long off = mb_off_[j];
         for (int l = 1; l <= L; ++l) {
+            cur_layer_ = l;
             const SubModule& sm = module_of_layer(l);
             const bool last_in_module = l == sm.last_layer;
             const bool boundary_concat = last_in_module && sm.index < plan_.Z() &&
@@ -582,7 +590,7 @@ void Session::build_ops() {
                         d.epi.col0 = wl.lo;
                         for (int ord : dest_gpus) d.epi.dst[d.epi.ndst++] = act_buf(ord, l) + off * img_elems(l);
                     }
-                    prepare(d, wl.p_fwd[j]);
+                    prepare(d, wl.p_fwd[j], w.gpu);
                     const double fl = 2.0 * rows * pix * wl.u * li.ksz * li.ksz * li.in_units;
                     int op = add_op(w.gpu, w.sf, gemm_launch(&wl.p_fwd[j], &wl.d_fwd[j], w.sf), deps, 1, OP_FWD_GEMM, fl);
                     if (wl.U != nullptr) {
@@ -618,7 +626,7 @@ void Session::build_ops() {
                     float* base = (l == L && softmax) ? q_buf(ord) : act_buf(ord, l);
                     d.epi.dst[d.epi.ndst++] = base + off * d.epi.ldd;
                 }
-                prepare(d, wl.p_fwd[j]);
+                prepare(d, wl.p_fwd[j], w.gpu);
                 const int op = add_op(w.gpu, w.sf, gemm_launch(&wl.p_fwd[j], &wl.d_fwd[j], w.sf), deps, 1,
                                       OP_FWD_GEMM, 2.0 * rows * wl.u * fi);
                 wl.fwd_op[j] = op;
@@ -686,6 +694,7 @@ void Session::build_ops() {
         const int rows = mb_sizes_[j];
         const long long off = mb_off_[j];
         for (int l = L; l >= 2; --l) {
+            cur_layer_ = l;
             const std::vector<int> contrib = contributors(l);
             const std::vector<int>& dests = layer_workers_[l - 1];
             const int fi = net_.dims[l - 1];
@@ -739,7 +748,7 @@ void Session::build_ops() {
                         d.epi.seg_ld[sg] = dl.slot_ld;
                         d.epi.seg_dst[sg] = dl.slots[k] + off * rows_per_img * dl.slot_ld;
                     }
-                    prepare(d, wl.p_dgrad[j]);
+                    prepare(d, wl.p_dgrad[j], w.gpu);
                     const int op = add_op(w.gpu, w.sb, gemm_launch(&wl.p_dgrad[j], &wl.d_dgrad[j], w.sb),
                                           wl.delta_ready[j], 1, OP_DGRAD_GEMM, fl);
                     wl.dgrad_op[j] = op;
@@ -776,7 +785,8 @@ void Session::build_ops() {
                     cm.q = lb.ksz - 1 - lb.pad;
                     cm.ldd = dl.ldd;
                     cudaStream_t st = dw.sb;
-                    const int op = add_op(dw.gpu, st, [=]() { return launch_conv_merge(cm, st); }, dgrad_ops, 1,
+                    float* dbp = dl.partial + static_cast<long long>(j) * conv_merge_blocks() * dl.u;
+                    const int op = add_op(dw.gpu, st, [=]() { return launch_conv_merge(cm, dbp, st); }, dgrad_ops, 1,
                                           OP_CONV_MERGE);
                     dl.delta_ready[j] = {op};
                     dw.last_bwd[j] = std::max(dw.last_bwd[j], op);
@@ -811,7 +821,7 @@ void Session::build_ops() {
                         d.epi.seg_dst[s] = dl.slots[k] + off * dl.ldd;
                     }
                 }
-                prepare(d, wl.p_dgrad[j]);
+                prepare(d, wl.p_dgrad[j], w.gpu);
                 const int op = add_op(w.gpu, w.sb, gemm_launch(&wl.p_dgrad[j], &wl.d_dgrad[j], w.sb),
                                       wl.delta_ready[j], 1, OP_DGRAD_GEMM, 2.0 * rows * wl.u * fi);
                 wl.dgrad_op[j] = op;
@@ -874,6 +884,7 @@ void Session::build_ops() {
         Gpu& g = gpu_of(w.gpu);
         for (WLayer& wl : w.layers) {
             const int l = wl.layer;
+            cur_layer_ = l;
             const int fi = net_.dims[l - 1];
             const LayerInfo& li = net_.info[l - 1];
             GemmDesc& d = wl.d_wgrad;
@@ -888,7 +899,7 @@ void Session::build_ops() {
                 cs.ksz = li.ksz;
                 cs.pad = li.pad;
                 cs.u = wl.u;
-                d = conv_wgrad_desc(cs, wl.delta, wl.ldd, act_buf(w.gpu, l - 1), lay_[l - 1].ld);
+                d = conv_wgrad_desc(cs, wl.delta, wl.ldd, act_buf(w.gpu, l - 1), lay_[l - 1].ld, wl.u < 128);
                 wfl = 2.0 * cfg_.batch * li.Ho() * li.Wo() * wl.u * li.ksz * li.ksz * li.in_units;
                 bias_rows = static_cast<long long>(cfg_.batch) * (wl.delta_img / wl.ldd);  // zero borders add nothing
             } else {
@@ -897,16 +908,22 @@ void Session::build_ops() {
                 d.M = wl.u;
                 d.N = fi;
                 d.K = cfg_.batch;
+                if (wl.u < 128 && fi > wl.u) {  // dW^T: the wide side fills the 128-row tiles
+                    std::swap(d.a, d.b);
+                    std::swap(d.M, d.N);
+                }
                 wfl = 2.0 * wl.u * fi * static_cast<double>(cfg_.batch);
             }
+            const bool wt = d.M != wl.u;
             d.epi = EpiParams{};
             d.epi.mode = EPI_SGD;
             d.epi.W = wl.W;
             d.epi.ldw = wl.ldw;
+            d.epi.sgd_t = wt ? 1 : 0;
             d.epi.alpha = &g.st->alpha;
             d.epi.inv_b = inv_b;
             d.epi.flag = &g.st->diverge_flag;
-            prepare(d, wl.p_wgrad);
+            prepare(d, wl.p_wgrad, w.gpu);
             std::vector<int> deps;
             for (int j = 0; j < m; ++j) {
                 deps.insert(deps.end(), wl.delta_ready[j].begin(), wl.delta_ready[j].end());
@@ -920,9 +937,12 @@ void Session::build_ops() {
             float* partial = wl.partial;
             float* bias = wl.bias;
             const double* alpha = &g.st->alpha;
+            const bool from_merge = li.kind == 1;  // conv: db partials came with the merges
+            const int chunks = cfg_.m * conv_merge_blocks();
             const int bop = add_op(w.gpu, s, [=]() {
+                if (from_merge) return launch_bias_from_partials(partial, chunks, u, bias, alpha, inv_b, s);
                 return launch_bias_update(delta, ldd, b, u, partial, bias, alpha, inv_b, s);
-            }, deps, 2, OP_BIAS);
+            }, deps, from_merge ? 1 : 2, OP_BIAS);
             add_op(w.gpu, s, gemm_launch(&wl.p_wgrad, &wl.d_wgrad, s), {bop}, 1, OP_WGRAD_GEMM, wfl);
         }
     }
@@ -1027,6 +1047,7 @@ void Session::profile(int iterations, double* ms, int* count, double* flops, int
         count[k] = 0;
         flops[k] = 0;
     }
+    last_op_ms_.assign(n, 0.0);
     for (int it = 0; it < iterations; ++it) {
         enqueue_iteration_timed(t0, t1);
         ++steps_enqueued_;
@@ -1038,6 +1059,7 @@ void Session::profile(int iterations, double* ms, int* count, double* flops, int
             if (!ops_[i].launch || ops_[i].kind >= nkinds) continue;
             float e = 0.f;
             check(cudaEventElapsedTime(&e, t0[i], t1[i]), "elapsed");
+            last_op_ms_[i] += e;
             ms[ops_[i].kind] += e;
             count[ops_[i].kind] += 1;
             flops[ops_[i].kind] += ops_[i].flops;
@@ -1047,6 +1069,22 @@ void Session::profile(int iterations, double* ms, int* count, double* flops, int
         if (t0[i]) cudaEventDestroy(t0[i]);
         if (t1[i]) cudaEventDestroy(t1[i]);
     }
+}
+
+int Session::profile_ops(int* kind, int* layer, int* info, double* ms, double* flops, int cap) {
+    int k = 0;
+    for (int i = 0; i < static_cast<int>(ops_.size()) && i < static_cast<int>(last_op_ms_.size()); ++i) {
+        if (!ops_[i].launch) continue;
+        if (k < cap) {
+            kind[k] = ops_[i].kind;
+            layer[k] = ops_[i].layer;
+            info[k] = ops_[i].info;
+            ms[k] = last_op_ms_[i];
+            flops[k] = ops_[i].flops;
+        }
+        ++k;
+    }
+    return k;
 }
 
 void Session::capture_graph() {

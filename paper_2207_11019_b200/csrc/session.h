@@ -100,6 +100,8 @@ class Session {
     // one eager iteration per call with per-op CUDA events; accumulates the
     // device time / launch count / algorithmic FLOPs per OpKind
     void profile(int iterations, double* ms, int* count, double* flops, int nkinds);
+    // per-op device times of the last profile() call
+    int profile_ops(int* kind, int* layer, int* info, double* ms, double* flops, int cap);
     double last_loss();
 
   private:
@@ -108,6 +110,8 @@ class Session {
     struct WLayer;
     struct Op {
         int kind = 0;       // OpKind
+        int layer = 0;      // layer the op belongs to (0: none)
+        int info = 0;       // GEMM ops: bn | cg << 10 | splits << 12
         double flops = 0;   // algorithmic FLOPs of the op (GEMMs)
         int gpu = 0;
         cudaStream_t stream = nullptr;
@@ -154,6 +158,8 @@ class Session {
     std::vector<const double*> host_W_, host_b_;
     std::vector<ActLayout> lay_;  // [0..L]: layout of a_l as its consumer reads it
     bool pending_acc_error_ = false;
+    int cur_layer_ = 0, cur_info_ = 0;
+    std::vector<double> last_op_ms_;
 };
 
 }  // namespace ppb

@@ -1,5 +1,5 @@
 """Partitioned training of nets with conv layers (BASELINE CNN configs) on the
-GPU against the float64 PyTorch restatement tests/cnn_oracle.py.
+GPU against the float64 PyTorch restatement oracle/cnn_oracle.py.
 
 Parity for conv is unpinned by the reference (it has no conv); the oracle
 follows the reference's partitioned-step semantics on the conv extension.
@@ -9,8 +9,8 @@ Tolerance (TF32 operands, fp32 accumulation): net_distance <= 5e-3, loss
 import numpy as np
 import pytest
 
-import cnn_oracle
-from _util import net_distance, rel_norm
+from _util import net_distance, rel_norm  # noqa: I001  (puts oracle/ on sys.path)
+import cnn_oracle  # oracle/cnn_oracle.py (test infrastructure)
 from paper_2207_11019_b200 import api, configs
 from paper_2207_11019_b200.api import Batch, PartitionedTrainOptions, TrainConfig, UpdateMode
 

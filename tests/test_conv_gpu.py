@@ -97,3 +97,17 @@ def test_conv_wgrad(shape, bn):
     got = out.reshape(u, k * k, ck)
     assert rel(got[:, :, :Cin].double(), ref) < 2e-3
     assert torch.count_nonzero(got[:, :, Cin:]) == 0
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_conv_wgrad_transposed_splitk(shape):
+    """dW^T orientation (M = k*k*ck, N = u) with split-K and the transposed SGD
+    epilogue writing W[u][tap][c] (the session uses it for u < 128)."""
+    N, H, W, Cin, u, k, p = shape
+    x, wt, dy, x_pad, w, d_pad, ldx, ldd, ck, Ho, Wo = _setup(*shape, seed=3)
+    out = torch.zeros(u, k * k * ck, device="cuda")
+    _call(3, N, H, W, Cin, ldx, p, k, x_pad, w, u, d_pad, ldd, out, k * k * ck, 0)
+    ref = torch.nn.grad.conv2d_weight(x.permute(0, 3, 1, 2), (u, Cin, k, k), dy.permute(0, 3, 1, 2), padding=p)
+    ref = ref.permute(0, 2, 3, 1).reshape(u, k * k, Cin)
+    got = out.reshape(u, k * k, ck)
+    assert rel(got[:, :, :Cin].double(), ref) < 2e-3

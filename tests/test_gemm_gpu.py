@@ -138,3 +138,11 @@ def test_gemm_mask_and_sgd_epilogues(precision):
 def test_tc_gemm_large():
     ef, et, _ = _run(2048, 4096, 4096, False, False, seed=3)
     assert ef < 2e-3 and et < 1e-4, (ef, et)
+
+
+@pytest.mark.parametrize("shape", [(64, 96, 65536), (200, 130, 20000), (8, 300, 4096)])
+@pytest.mark.parametrize("majors", MAJORS)
+def test_tc_gemm_splitk(shape, majors):
+    """Few output tiles, long K: the K loop is split and reduced in order."""
+    ef, et, _ = _run(*shape, *majors)
+    assert ef < 2e-3 and et < 1e-4, (ef, et)
