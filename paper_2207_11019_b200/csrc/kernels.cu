@@ -257,6 +257,27 @@ __global__ void finalize_kernel(StepState* st, const double* __restrict__ loss_r
 }
 
 template <class T>
+__global__ void im2col_kernel(const T* __restrict__ src, int imgs, int H, int W, int C, int k, int p,
+                              float* __restrict__ dst, long long ld) {
+    const int Ho = H + 2 * p - k + 1, Wo = W + 2 * p - k + 1;
+    const int kc = k * k * C;
+    const long long total = static_cast<long long>(imgs) * Ho * Wo * kc;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int col = static_cast<int>(i % kc);
+        const long long pix = i / kc;
+        const int c = col % C, tap = col / C, r = tap / k, s = tap % k;
+        const int wo = static_cast<int>(pix % Wo);
+        const int ho = static_cast<int>((pix / Wo) % Ho);
+        const long long n = pix / (static_cast<long long>(Wo) * Ho);
+        const int hi = ho + r - p, wi = wo + s - p;
+        float v = 0.f;
+        if (hi >= 0 && hi < H && wi >= 0 && wi < W) v = static_cast<float>(src[((n * H + hi) * W + wi) * C + c]);
+        dst[pix * ld + col] = v;
+    }
+}
+
+template <class T>
 __global__ void pad_input_kernel(const T* __restrict__ src, int imgs, int H, int W, int C, float* __restrict__ dst,
                                  int p, long long ld) {
     const long long total = static_cast<long long>(imgs) * H * W * C;
@@ -277,18 +298,18 @@ __global__ void pad_input_kernel(const T* __restrict__ src, int imgs, int H, int
 // (blockDim and the grid stride are multiples of the group count), which keeps
 // loads/stores vectorised along channels and lets conv_merge accumulate the
 // bias gradient of its channels in registers.
-template <int VEC>
+template <int VEC, class IDX>
 __global__ void pool_fwd_kernel(const float* __restrict__ U, long long ldu, int imgs, int Ho, int Wo, int uch,
                                 int pool, unsigned char* __restrict__ argmax, ActLayout out, PoolDsts dsts) {
     const int Hq = Ho / pool, Wq = Wo / pool;
-    const int groups = uch / VEC;
-    const long long total = static_cast<long long>(imgs) * Hq * Wq * groups;
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const IDX groups = uch / VEC;
+    const IDX total = static_cast<IDX>(imgs) * Hq * Wq * groups;
+    for (IDX i = blockIdx.x * static_cast<IDX>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<IDX>(gridDim.x) * blockDim.x) {
         const int g = static_cast<int>(i % groups);
-        const long long pp = i / groups;  // pooled pixel
+        const IDX pp = i / groups;  // pooled pixel
         const int x = static_cast<int>(pp % Wq);
-        const long long t = pp / Wq;
+        const IDX t = pp / Wq;
         const int y = static_cast<int>(t % Hq);
         const long long n = t / Hq;
         const int c0 = g * VEC;
@@ -296,14 +317,15 @@ __global__ void pool_fwd_kernel(const float* __restrict__ U, long long ldu, int 
         unsigned char arg[VEC];
         if (pool == 1) {
             if (VEC == 4) {
-                const float4 a = *reinterpret_cast<const float4*>(U + pp * ldu + c0);
+                const float4 a = *reinterpret_cast<const float4*>(U + static_cast<long long>(pp) * ldu + c0);
                 v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
             } else {
-                v[0] = U[pp * ldu + c0];
+                v[0] = U[static_cast<long long>(pp) * ldu + c0];
             }
         } else {
             const long long base = (n * Ho + 2 * y) * Wo + 2 * x;
             const long long offs[4] = {base, base + 1, base + Wo, base + Wo + 1};
+            static_assert(sizeof(IDX) >= 4, "index type");
 #pragma unroll
             for (int k = 0; k < VEC; ++k) {
                 v[k] = -INFINITY;
@@ -326,7 +348,7 @@ __global__ void pool_fwd_kernel(const float* __restrict__ U, long long ldu, int 
                     }
             }
 #pragma unroll
-            for (int k = 0; k < VEC; ++k) argmax[pp * uch + c0 + k] = arg[k];
+            for (int k = 0; k < VEC; ++k) argmax[static_cast<long long>(pp) * uch + c0 + k] = arg[k];
         }
         if (out.kind == 0) {
             const long long o = ((n * out.hp + y + out.pad) * out.wp + x + out.pad) * out.ld + out.col0 + c0;
@@ -344,22 +366,22 @@ __global__ void pool_fwd_kernel(const float* __restrict__ U, long long ldu, int 
     }
 }
 
-template <int VEC>
+template <int VEC, class IDX>
 __global__ void conv_merge_kernel(ConvMerge m, float* __restrict__ db_partial) {
     const int groups = m.uch / VEC;
-    const long long total = static_cast<long long>(m.imgs) * m.Ho * m.Wo * groups;
+    const IDX total = static_cast<IDX>(m.imgs) * m.Ho * m.Wo * groups;
     const int Hg = m.Ho / m.pool, Wg = m.Wo / m.pool;
     const int hq = m.Ho + 2 * m.q, wq = m.Wo + 2 * m.q;
     float db[VEC];
 #pragma unroll
     for (int k = 0; k < VEC; ++k) db[k] = 0.f;
-    const long long start = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    const IDX start = blockIdx.x * static_cast<IDX>(blockDim.x) + threadIdx.x;
     const int g = static_cast<int>(start % groups);  // constant: blockDim and the stride are multiples of groups
     const int c0 = g * VEC;
-    for (long long i = start; i < total; i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const long long pix = i / groups;
+    for (IDX i = start; i < total; i += static_cast<IDX>(gridDim.x) * blockDim.x) {
+        const IDX pix = i / groups;
         const int w = static_cast<int>(pix % m.Wo);
-        const long long t = pix / m.Wo;
+        const IDX t = pix / m.Wo;
         const int h = static_cast<int>(t % m.Ho);
         const long long n = t / m.Ho;
         float gr[VEC];
@@ -399,7 +421,7 @@ __global__ void conv_merge_kernel(ConvMerge m, float* __restrict__ db_partial) {
             }
         }
         if (m.mask_kind == 1) {
-            const float* up = m.U + pix * m.ldu + c0;
+            const float* up = m.U + static_cast<long long>(pix) * m.ldu + c0;
 #pragma unroll
             for (int k = 0; k < VEC; ++k)
                 if (!(up[k] > 0.f)) gr[k] = 0.f;
@@ -499,6 +521,15 @@ cudaError_t launch_convert_f32(const float* src, int rows, int cols, float* dst,
     return cudaGetLastError();
 }
 
+cudaError_t launch_im2col_input(const double* src64, const float* src32, int imgs, int H, int W, int C, int k,
+                                int p, float* dst, long long ld, cudaStream_t s) {
+    const long long n = static_cast<long long>(imgs) * (H + 2 * p - k + 1) * (W + 2 * p - k + 1) * k * k * C;
+    if (n <= 0) return cudaSuccess;
+    if (src64) im2col_kernel<double><<<grid_for(n, 256), 256, 0, s>>>(src64, imgs, H, W, C, k, p, dst, ld);
+    else im2col_kernel<float><<<grid_for(n, 256), 256, 0, s>>>(src32, imgs, H, W, C, k, p, dst, ld);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pad_input(const double* src64, const float* src32, int imgs, int H, int W, int C, float* dst,
                              int p, long long ld, cudaStream_t s) {
     const long long n = static_cast<long long>(imgs) * H * W * C;
@@ -523,10 +554,13 @@ cudaError_t launch_pool_fwd(const float* U, long long ldu, int imgs, int Ho, int
     bool v4 = vec4_ok(uch, ldu) && (out.kind != 0 || vec4_ok(out.ld, out.col0)) &&
               reinterpret_cast<uintptr_t>(U) % 16 == 0;
     for (int d = 0; d < dsts.n; ++d) v4 = v4 && reinterpret_cast<uintptr_t>(dsts.ptr[d]) % 16 == 0;
+    const bool i32 = n < (1LL << 31);
     if (v4) {
-        pool_fwd_kernel<4><<<grid_for(n / 4, 256), 256, 0, s>>>(U, ldu, imgs, Ho, Wo, uch, pool, argmax, out, dsts);
+        if (i32) pool_fwd_kernel<4, unsigned><<<grid_for(n / 4, 256), 256, 0, s>>>(U, ldu, imgs, Ho, Wo, uch, pool, argmax, out, dsts);
+        else pool_fwd_kernel<4, long long><<<grid_for(n / 4, 256), 256, 0, s>>>(U, ldu, imgs, Ho, Wo, uch, pool, argmax, out, dsts);
     } else {
-        pool_fwd_kernel<1><<<grid_for(n, 256), 256, 0, s>>>(U, ldu, imgs, Ho, Wo, uch, pool, argmax, out, dsts);
+        if (i32) pool_fwd_kernel<1, unsigned><<<grid_for(n, 256), 256, 0, s>>>(U, ldu, imgs, Ho, Wo, uch, pool, argmax, out, dsts);
+        else pool_fwd_kernel<1, long long><<<grid_for(n, 256), 256, 0, s>>>(U, ldu, imgs, Ho, Wo, uch, pool, argmax, out, dsts);
     }
     return cudaGetLastError();
 }
@@ -547,8 +581,14 @@ cudaError_t launch_conv_merge(const ConvMerge& m, float* db_partial, cudaStream_
     if (n <= 0) {
         return cudaMemsetAsync(db_partial, 0, sizeof(float) * grid * m.uch, s);
     }
-    if (v4) conv_merge_kernel<4><<<grid, block, shmem, s>>>(m, db_partial);
-    else conv_merge_kernel<1><<<grid, block, shmem, s>>>(m, db_partial);
+    const bool i32 = n < (1LL << 31);
+    if (v4) {
+        if (i32) conv_merge_kernel<4, unsigned><<<grid, block, shmem, s>>>(m, db_partial);
+        else conv_merge_kernel<4, long long><<<grid, block, shmem, s>>>(m, db_partial);
+    } else {
+        if (i32) conv_merge_kernel<1, unsigned><<<grid, block, shmem, s>>>(m, db_partial);
+        else conv_merge_kernel<1, long long><<<grid, block, shmem, s>>>(m, db_partial);
+    }
     return cudaGetLastError();
 }
 

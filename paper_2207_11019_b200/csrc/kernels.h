@@ -63,6 +63,11 @@ cudaError_t launch_convert_f32(const float* src, int rows, int cols, float* dst,
 cudaError_t launch_pad_input(const double* src64, const float* src32, int imgs, int H, int W, int C, float* dst,
                              int p, long long ld, cudaStream_t s);
 
+// First conv layer with few input channels: im2col rows
+// dst[(n*Ho + h)*Wo + w][(r*k + s)*C + c] = x[n][h+r-p][w+s-p][c] (0 outside), pitch ld.
+cudaError_t launch_im2col_input(const double* src64, const float* src32, int imgs, int H, int W, int C, int k,
+                                int p, float* dst, long long ld, cudaStream_t s);
+
 // Layout of a conv layer's output as its consumer reads it.
 struct ActLayout {
     int kind = 0;        // 0 padded NHWC [img][hp][wp][ld] at channel col0 + c; 1 CHW-flatten rows [img][ld]

@@ -163,6 +163,9 @@ Session::Session(const std::vector<int>& device_map, const NetDesc& net, const d
         if (net_.acts[l] == 2 && l != L - 1)
             throw std::invalid_argument("softmax is only valid on the last layer");
     }
+    // few input channels on the first conv: im2col rows (K = k*k*C) instead of
+    // 32-channel-padded implicit GEMM taps (K = k*k*32)
+    if (net_.info[0].kind == 1 && net_.info[0].in_units < 16) net_.info[0].im2col = true;
     size_t wo = 0, bo = 0;
     for (int l = 0; l < L; ++l) {
         const LayerInfo& li = net_.info[l];
@@ -310,7 +313,7 @@ void Session::build() {
 
 long long Session::img_elems(int layer) const {
     const ActLayout& a = lay_[layer];
-    return a.kind == 0 ? static_cast<long long>(a.hp) * a.wp * a.ld : a.ld;
+    return a.kind == 1 ? a.ld : static_cast<long long>(a.hp) * a.wp * a.ld;
 }
 
 void Session::alloc_buffers() {
@@ -324,7 +327,13 @@ void Session::alloc_buffers() {
     lay_.assign(L + 1, ActLayout{});
     for (int l = 0; l <= L; ++l) {
         ActLayout& a = lay_[l];
-        if (l < L && net_.info[l].kind == 1) {
+        if (l == 0 && net_.info[0].im2col) {
+            const LayerInfo& c = net_.info[0];
+            a.kind = 2;  // im2col rows [pixel][k*k*C]
+            a.hp = c.Ho() * c.Wo();
+            a.wp = 1;
+            a.ld = ld_of(c.ksz * c.ksz * c.in_units);
+        } else if (l < L && net_.info[l].kind == 1) {
             const LayerInfo& c = net_.info[l];
             a.kind = 0;
             a.pad = c.pad;
@@ -406,7 +415,7 @@ void Session::alloc_buffers() {
             for (int r = 0; r < wl.u; ++r) {
                 const double* src = Wl + static_cast<size_t>(wl.lo + r) * hc;
                 float* dst = tmp.data() + static_cast<size_t>(r) * wl.ldw;
-                if (li.kind == 1) {
+                if (li.kind == 1 && !li.im2col) {
                     for (int t = 0; t < li.ksz * li.ksz; ++t)
                         for (int c = 0; c < li.in_units; ++c)
                             dst[t * li.ck() + c] = static_cast<float>(src[t * li.in_units + c]);
@@ -569,7 +578,18 @@ void Session::build_ops() {
                     cs.ksz = li.ksz;
                     cs.pad = li.pad;
                     cs.u = wl.u;
-                    d = conv_fwd_desc(cs, act_buf(w.gpu, l - 1) + off * img_elems(l - 1), lay_[l - 1].ld, wl.W);
+                    if (li.im2col) {  // dense GEMM over the im2col rows
+                        const int kc = li.ksz * li.ksz * li.in_units;
+                        const int prow = rows * li.Ho() * li.Wo();
+                        d = GemmDesc{};
+                        d.a = Operand{act_buf(w.gpu, l - 1) + off * img_elems(l - 1), prow, kc, lay_[l - 1].ld, false};
+                        d.b = Operand{wl.W, wl.u, kc, wl.ldw, false};
+                        d.M = prow;
+                        d.N = wl.u;
+                        d.K = kc;
+                    } else {
+                        d = conv_fwd_desc(cs, act_buf(w.gpu, l - 1) + off * img_elems(l - 1), lay_[l - 1].ld, wl.W);
+                    }
                     d.epi = EpiParams{};
                     d.epi.mode = EPI_STORE;
                     d.epi.bias = wl.bias;
@@ -899,7 +919,14 @@ void Session::build_ops() {
                 cs.ksz = li.ksz;
                 cs.pad = li.pad;
                 cs.u = wl.u;
-                d = conv_wgrad_desc(cs, wl.delta, wl.ldd, act_buf(w.gpu, l - 1), lay_[l - 1].ld, wl.u < 128);
+                if (li.im2col) {  // B = im2col rows (pixel-major, MN = k*k*C)
+                    d = conv_wgrad_desc(cs, wl.delta, wl.ldd, act_buf(w.gpu, l - 1), lay_[l - 1].ld, false);
+                    const int kc = li.ksz * li.ksz * li.in_units;
+                    d.b = Operand{act_buf(w.gpu, l - 1), cfg_.batch * li.Ho() * li.Wo(), kc, lay_[l - 1].ld, true};
+                    d.N = kc;
+                } else {
+                    d = conv_wgrad_desc(cs, wl.delta, wl.ldd, act_buf(w.gpu, l - 1), lay_[l - 1].ld, wl.u < 128);
+                }
                 wfl = 2.0 * cfg_.batch * li.Ho() * li.Wo() * wl.u * li.ksz * li.ksz * li.in_units;
                 bias_rows = static_cast<long long>(cfg_.batch) * (wl.delta_img / wl.ldd);  // zero borders add nothing
             } else {
@@ -1146,7 +1173,21 @@ void Session::load_batch(const double* X64, const float* X32, const int* labels)
         Gpu& g = *gp;
         check(cudaSetDevice(g.ordinal), "cudaSetDevice");
         if (g.ordinal != g0.ordinal) check(cudaStreamWaitEvent(g.main, g0.ev_done, 0), "wait");
-        if (g.needs_x && lay_[0].kind == 0) {
+        if (g.needs_x && lay_[0].kind == 2) {
+            const LayerInfo& c = net_.info[0];
+            float* x = g.act.at(0);
+            const size_t n = static_cast<size_t>(b) * I0;
+            if (X64 != nullptr) {
+                check(cudaMemcpyAsync(g.xstage, X64, sizeof(double) * n, cudaMemcpyHostToDevice, g.main), "H2D X");
+                check(launch_im2col_input(g.xstage, nullptr, b, c.H, c.W, c.in_units, c.ksz, c.pad, x, lay_[0].ld,
+                                          g.main), "im2col X");
+            } else {
+                float* st = reinterpret_cast<float*>(g.xstage);
+                check(cudaMemcpyAsync(st, X32, sizeof(float) * n, cudaMemcpyHostToDevice, g.main), "H2D X");
+                check(launch_im2col_input(nullptr, st, b, c.H, c.W, c.in_units, c.ksz, c.pad, x, lay_[0].ld, g.main),
+                      "im2col X");
+            }
+        } else if (g.needs_x && lay_[0].kind == 0) {
             // conv input: host NHWC rows -> padded NHWC (zero border stays from allocation)
             const LayerInfo& c = net_.info[0];
             float* x = g.act.at(0);
@@ -1268,7 +1309,7 @@ void Session::get_net(double* W, double* b) {
             for (int r = 0; r < wl.u; ++r) {
                 double* dst = W + wo + static_cast<size_t>(wl.lo + r) * hc;
                 const float* src = tmp.data() + static_cast<size_t>(r) * wl.ldw;
-                if (li.kind == 1) {
+                if (li.kind == 1 && !li.im2col) {
                     for (int t = 0; t < li.ksz * li.ksz; ++t)
                         for (int c = 0; c < li.in_units; ++c) dst[t * li.in_units + c] = src[t * li.ck() + c];
                 } else {

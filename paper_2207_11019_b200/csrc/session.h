@@ -34,6 +34,7 @@ struct LayerInfo {
     int in_units = 0, out_units = 0;
     int act = 0;
     int H = 1, W = 1, ksz = 1, pad = 0, pool = 1;  // conv: input grid, kernel, padding, pool factor (1|2)
+    bool im2col = false;  // first layer with few input channels: explicit im2col rows, dense GEMMs
     int Ho() const { return H + 2 * pad - ksz + 1; }
     int Wo() const { return W + 2 * pad - ksz + 1; }
     int Hq() const { return Ho() / pool; }
@@ -42,7 +43,10 @@ struct LayerInfo {
     long long out_features() const { return kind ? static_cast<long long>(out_units) * Hq() * Wq() : out_units; }
     int host_wcols() const { return kind ? ksz * ksz * in_units : in_units; }
     int ck() const { return (in_units + 31) / 32 * 32; }
-    int dev_wcols() const { return kind ? ksz * ksz * ck() : in_units; }
+    int dev_wcols() const {
+        if (!kind) return in_units;
+        return im2col ? (ksz * ksz * in_units + 3) / 4 * 4 : ksz * ksz * ck();
+    }
 };
 
 struct NetDesc {
