@@ -141,4 +141,52 @@ __device__ __forceinline__ void epilogue32(const EpiParams& p, int m, int n0, fl
     }
 }
 
+// Row offset (elements) of output row m in the EPI_STORE destination.
+__device__ __forceinline__ long long epi_store_row(const EpiParams& p, int m) {
+    if (!p.remap) return static_cast<long long>(m) * p.ldd;
+    const int img = m / p.r_howo, rem = m - img * p.r_howo;
+    const int h = rem / p.r_wo, w = rem - h * p.r_wo;
+    return ((static_cast<long long>(img) * p.r_hp + h + p.r_pad) * p.r_wp + w + p.r_pad) * p.ldd;
+}
+
+// Element-wise form of the epilogue for the coalesced (row-wise) path: lanes
+// of a warp hold consecutive columns n of one row m.  `row_off` is
+// epi_store_row(p, m) (EPI_STORE only).  Not used for sgd_t (its natural
+// coalescing is along m) or split-K partials (handled by the caller).
+__device__ __forceinline__ void epilogue1(const EpiParams& p, int m, int n, float v, long long row_off) {
+    if (m >= p.M || n >= p.N) return;
+    switch (p.mode) {
+        case EPI_STORE: {
+            if (p.bias != nullptr) v += __ldg(p.bias + n);
+            if (p.relu) v = v > 0.f ? v : 0.f;
+            for (int d = 0; d < p.ndst; ++d) p.dst[d][row_off + p.col0 + n] = v;
+            break;
+        }
+        case EPI_MASK: {
+            const float mk = p.mask[static_cast<long long>(m) * p.ldm + p.mcol0 + n];
+            p.dst[0][static_cast<long long>(m) * p.ldd + p.col0 + n] = mk > 0.f ? v : 0.f;
+            break;
+        }
+        case EPI_SGD: {
+            const float g = v * p.inv_b;
+            if (!isfinite(g) && p.flag != nullptr) atomicOr(p.flag, 1);
+            float* wp = p.W + static_cast<long long>(m) * p.ldw + n;
+            *wp -= static_cast<float>(*p.alpha) * g;
+            break;
+        }
+        case EPI_SLOTS: {
+            for (int s = 0; s < p.nseg; ++s) {
+                if (n < p.seg_lo[s] || n >= p.seg_hi[s]) continue;
+                float o = v;
+                if (p.seg_mask[s] != nullptr && !(p.seg_mask[s][static_cast<long long>(m) * p.seg_mask_ld[s] + n] > 0.f))
+                    o = 0.f;
+                p.seg_dst[s][static_cast<long long>(m) * p.seg_ld[s] + n - p.seg_lo[s]] = o;
+            }
+            break;
+        }
+        default:
+            break;
+    }
+}
+
 }  // namespace ppb

@@ -25,6 +25,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -271,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float v[32];
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-                if (sk.splits > 1) {  // raw partial sums; splitk_epilogue_kernel reduces + applies the epilogue
+                if (sk.splits > 1) {  // raw partial sums for splitk_epilogue_kernel
                     const int nn = n0 + c * 32;
                     if (m < M && nn < N)
                         store_row32(sk.ws + split * sk.stride + static_cast<long long>(m) * sk.ld, nn,
@@ -303,23 +304,26 @@ __global__ void __launch_bounds__(kThreads, 1)
 // the GEMM's real epilogue.  One thread per (row, 32-column chunk).
 __global__ void splitk_epilogue_kernel(const __grid_constant__ EpiParams epi, const __grid_constant__ SplitK sk,
                                        int M, int N) {
-    const int chunks = (N + 31) / 32;
     const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-    if (idx >= static_cast<long long>(M) * chunks) return;
-    // consecutive threads take consecutive rows of one chunk (coalesced for sgd_t)
-    const int m = static_cast<int>(idx % M);
-    const int n0 = static_cast<int>(idx / M) * 32;
-    const int nvalid = N - n0 < 32 ? N - n0 : 32;
-    float acc[32];
-#pragma unroll
-    for (int i = 0; i < 32; ++i) acc[i] = 0.f;
-    for (int s = 0; s < sk.splits; ++s) {
-        float v[32];
-        load_row32(sk.ws + s * sk.stride + static_cast<long long>(m) * sk.ld, n0, nvalid, v);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) acc[i] += v[i];
+    if (idx >= static_cast<long long>(M) * N) return;
+    int m, n;
+    if (epi.mode == EPI_SGD && epi.sgd_t) {  // coalesce along m (W[n][m])
+        m = static_cast<int>(idx % M);
+        n = static_cast<int>(idx / M);
+    } else {  // coalesce along n
+        n = static_cast<int>(idx % N);
+        m = static_cast<int>(idx / N);
     }
-    epilogue32(epi, m, n0, acc);
+    float acc = 0.f;
+    const long long off = static_cast<long long>(m) * sk.ld + n;
+    for (int s = 0; s < sk.splits; ++s) acc += sk.ws[s * sk.stride + off];
+    if (epi.mode == EPI_SGD && epi.sgd_t) {
+        const float g = acc * epi.inv_b;
+        if (!isfinite(g) && epi.flag != nullptr) atomicOr(epi.flag, 1);
+        epi.W[static_cast<long long>(n) * epi.ldw + m] -= static_cast<float>(*epi.alpha) * g;
+        return;
+    }
+    epilogue1(epi, m, n, acc, epi.mode == EPI_STORE ? epi_store_row(epi, m) : 0);
 }
 
 // ---------------------------------------------------------------- host side
@@ -503,8 +507,8 @@ cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
     cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<A_MN, B_MN, BN, CG>, p.ta, p.tb, p.M, p.N, p.K, p.epi,
                                        p.ga, p.gb, p.sk);
     if (e != cudaSuccess || p.sk.splits <= 1) return e;
-    const long long threads = static_cast<long long>(p.M) * ((p.N + 31) / 32);
-    splitk_epilogue_kernel<<<static_cast<unsigned>((threads + 127) / 128), 128, 0, s>>>(p.epi, p.sk, p.M, p.N);
+    const long long threads = static_cast<long long>(p.M) * p.N;
+    splitk_epilogue_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(p.epi, p.sk, p.M, p.N);
     return cudaGetLastError();
 }
 
