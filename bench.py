@@ -1,7 +1,7 @@
 """Benchmark of the partitioned fwd+bwd+update step (BASELINE.json metric:
 "train samples/sec (fwd+bwd+update) at 1/2/4/8 B200; % tensor-core roofline").
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload wide_mlp|mlp784]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload vgg16|wide_mlp|mlp784]
                     [--impl ours|reference]
 
 Prints ONE JSON line (rank 0).  A "step" is one train_partitioned iteration
@@ -377,7 +377,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="wide_mlp", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="vgg16", choices=sorted(WORKLOADS))
     ap.add_argument("--m", type=int, default=1, help="micro-batches per step")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -565,7 +565,7 @@ cudaError_t launch_pool_fwd(const float* U, long long ldu, int imgs, int Ho, int
     return cudaGetLastError();
 }
 
-int conv_merge_blocks() { return 148 * 4; }
+int conv_merge_blocks() { return 148 * 16; }
 
 cudaError_t launch_conv_merge(const ConvMerge& m, float* db_partial, cudaStream_t s) {
     const long long n = static_cast<long long>(m.imgs) * m.Ho * m.Wo * m.uch;
