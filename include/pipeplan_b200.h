@@ -114,6 +114,17 @@ int ppb_merge_submodules(int* plan, int plan_len, const int* group, int group_le
 /* merge_all (src/partition.cpp:177-182), in place. */
 int ppb_merge_all(int* plan, int plan_len);
 
+/* serialize_plan (src/partition.cpp:303-331): the reference's plan JSON,
+ * byte-identical to its nlohmann::json dump(2).  provenance: entries joined
+ * by '\n' (may be NULL).  *out_len = text length (call with cap = 0 to size;
+ * cap must exceed the length for the terminating NUL). */
+int ppb_serialize_plan(const int* plan, int plan_len, const char* provenance, char* out, size_t cap,
+                       size_t* out_len);
+
+/* parse_plan (src/partition.cpp:333-384) -> flat plan; provenance entries are
+ * returned '\n'-joined in `provenance` when non-NULL. */
+int ppb_parse_plan(const char* text, int* out, int cap, int* out_len, char* provenance, size_t prov_cap);
+
 /* validate_plan (src/partition.cpp:232-294) against a dense chain. */
 int ppb_validate_plan(const int* plan, int plan_len, const int* fan_in, const int* fan_out, int L,
                       int num_cluster_devices /* 0 = no cluster check */);

@@ -358,6 +358,30 @@ class Reference(_Base):
                     plan=plan[: plen.value].copy(), W=W[:nw].copy(), b=b[: sum(d[1:])].copy(),
                     X=X[: batch.value * d[0]].reshape(batch.value, d[0]).copy(), labels=y[: batch.value].copy())
 
+    def serialize_plan(self, plan, provenance=()):
+        p = np.ascontiguousarray(plan, np.int32)
+        n = C.c_size_t(0)
+        err = C.create_string_buffer(512)
+        prov = "\n".join(provenance).encode()
+        f = self._fn("serialize_plan")
+        rc = f(_ip(p), len(p), prov, None, 0, C.byref(n), err, 512)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        buf = C.create_string_buffer(n.value + 1)
+        rc = f(_ip(p), len(p), prov, buf, n.value + 1, C.byref(n), err, 512)
+        return buf.value.decode()
+
+    def parse_plan(self, text):
+        n = C.c_int(0)
+        err = C.create_string_buffer(512)
+        f = self._fn("parse_plan")
+        rc = f(text.encode(), None, 0, C.byref(n), err, 512)
+        if rc:
+            raise OracleError(rc, err.value.decode())
+        out = np.zeros(n.value, np.int32)
+        f(text.encode(), _ip(out), n.value, C.byref(n), err, 512)
+        return out
+
     def run_verification(self, seeds=100):
         buf = C.create_string_buffer(8192)
         ok = self._fn("run_verification")(seeds, buf, 8192)

@@ -296,6 +296,32 @@ int ref_train_partitioned(const int* dims, const int* acts, int L, const double*
     });
 }
 
+// serialize_plan (src/partition.cpp:303-331); provenance = '\n'-joined entries.
+int ref_serialize_plan(const int* plan, int len, const char* provenance, char* out, size_t cap, size_t* out_len,
+                       char* err, size_t errlen) {
+    return run(err, errlen, [&] {
+        PartitionPlan p = unflatten(plan, len);
+        if (provenance && *provenance) {
+            std::string s(provenance), item;
+            size_t a = 0;
+            while (true) {
+                size_t b = s.find('\n', a);
+                p.provenance.push_back(s.substr(a, b == std::string::npos ? std::string::npos : b - a));
+                if (b == std::string::npos) break;
+                a = b + 1;
+            }
+        }
+        const std::string t = serialize_plan(p);
+        *out_len = t.size();
+        if (out && cap > t.size()) std::memcpy(out, t.c_str(), t.size() + 1);
+    });
+}
+
+// parse_plan (src/partition.cpp:333-384) -> flat plan.
+int ref_parse_plan(const char* text, int* out, int cap, int* out_len, char* err, size_t errlen) {
+    return run(err, errlen, [&] { emit(flatten(parse_plan(text)), out, cap, out_len); });
+}
+
 // run_verification (src/verify.cpp:104-247): 1 if every property passed.
 int ref_run_verification(int seeds, char* report, size_t len) {
     VerifyOptions o;

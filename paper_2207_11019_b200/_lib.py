@@ -66,6 +66,8 @@ _SIGS = {
     "ppb_merge_submodules": (C.c_int, [_i32p, C.c_int, _i32p, C.c_int]),
     "ppb_merge_all": (C.c_int, [_i32p, C.c_int]),
     "ppb_validate_plan": (C.c_int, [_i32p, C.c_int, _i32p, _i32p, C.c_int, C.c_int]),
+    "ppb_serialize_plan": (C.c_int, [_i32p, C.c_int, C.c_char_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
+    "ppb_parse_plan": (C.c_int, [C.c_char_p, _i32p, C.c_int, _i32p, C.c_char_p, C.c_size_t]),
     "ppb_default_options": (None, [C.POINTER(OptionsC)]),
     "ppb_default_config": (None, [C.POINTER(TrainConfigC)]),
     "ppb_context_create": (C.c_int, [_i32p, C.c_int, C.POINTER(C.c_void_p)]),

@@ -25,7 +25,7 @@ __all__ = [
     "ActKind", "LossKind", "UpdateMode", "BoundaryKind", "LayerSpec", "ModelGraph", "Shard", "SubModule",
     "PartitionPlan", "ConvSpec", "TinyLayer", "TinyNet", "Batch", "TrainConfig", "PartitionedTrainOptions", "TrainResult",
     "split_layer", "split_microbatches", "build_plan", "build_staged_plan", "build_plan_with_cuts",
-    "merge_submodules", "merge_all", "validate_plan", "model_graph_of", "train_partitioned", "Context",
+    "merge_submodules", "merge_all", "validate_plan", "serialize_plan", "parse_plan", "model_graph_of", "train_partitioned", "Context",
     "Session", "PipeplanError",
 ]
 
@@ -397,6 +397,31 @@ def merge_all(p: PartitionPlan) -> PartitionPlan:
     if p.num_submodules() < 2:
         return p
     return merge_submodules(p, list(range(1, p.num_submodules() + 1)))
+
+
+def serialize_plan(p: PartitionPlan) -> str:
+    """partition.cpp:303-331 (byte-identical JSON)."""
+    flat = p.to_flat()
+    prov = "\n".join(p.provenance).encode()
+    n = C.c_size_t(0)
+    L = _lib.lib()
+    check(L.ppb_serialize_plan(_ip(flat), len(flat), prov, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    check(L.ppb_serialize_plan(_ip(flat), len(flat), prov, buf, n.value + 1, C.byref(n)))
+    return buf.value.decode()
+
+
+def parse_plan(text: str) -> PartitionPlan:
+    """partition.cpp:333-384."""
+    L = _lib.lib()
+    n = C.c_int(0)
+    check(L.ppb_parse_plan(text.encode(), None, 0, C.byref(n), None, 0))
+    out = np.zeros(n.value, np.int32)
+    prov = C.create_string_buffer(len(text) + 1)
+    check(L.ppb_parse_plan(text.encode(), _ip(out), n.value, C.byref(n), prov, len(text) + 1))
+    p = PartitionPlan.from_flat(out)
+    p.provenance = [x for x in prov.value.decode().split("\n") if x] if prov.value else []
+    return p
 
 
 def validate_plan(p: PartitionPlan, g, cluster_devices: int = 0) -> None:

@@ -96,6 +96,44 @@ extern "C" int ppb_merge_all(int* plan, int plan_len) {
     return ppb_guard([&] { emit(merge_all(plan_from_flat(plan, plan_len)), plan, plan_len, nullptr); });
 }
 
+extern "C" int ppb_serialize_plan(const int* plan, int plan_len, const char* provenance, char* out, size_t cap,
+                                  size_t* out_len) {
+    return ppb_guard([&] {
+        std::vector<std::string> prov;
+        if (provenance != nullptr && *provenance) {
+            std::string s(provenance);
+            size_t a = 0;
+            while (true) {
+                const size_t b = s.find('\n', a);
+                prov.push_back(s.substr(a, b == std::string::npos ? std::string::npos : b - a));
+                if (b == std::string::npos) break;
+                a = b + 1;
+            }
+        }
+        const std::string t = serialize_plan(plan_from_flat(plan, plan_len), prov);
+        if (out_len) *out_len = t.size();
+        if (out != nullptr && cap > 0) {
+            if (cap <= t.size()) throw std::length_error("plan text buffer too small");
+            std::memcpy(out, t.c_str(), t.size() + 1);
+        }
+    });
+}
+
+extern "C" int ppb_parse_plan(const char* text, int* out, int cap, int* out_len, char* provenance, size_t prov_cap) {
+    return ppb_guard([&] {
+        if (text == nullptr) throw std::invalid_argument("null plan text");
+        std::vector<std::string> prov;
+        const Plan p = parse_plan(text, &prov);
+        emit(p, out, cap, out_len);
+        if (provenance != nullptr && prov_cap > 0) {
+            std::string joined;
+            for (size_t i = 0; i < prov.size(); ++i) joined += (i ? "\n" : "") + prov[i];
+            if (prov_cap <= joined.size()) throw std::length_error("provenance buffer too small");
+            std::memcpy(provenance, joined.c_str(), joined.size() + 1);
+        }
+    });
+}
+
 extern "C" int ppb_validate_plan(const int* plan, int plan_len, const int* fan_in,
                                  const int* fan_out, int L, int num_cluster_devices) {
     return ppb_guard([&] {

@@ -9,7 +9,10 @@
 //   split_microbatches  src/schedule.cpp:46-55
 #include "planner.h"
 
+#include <algorithm>
+#include <cctype>
 #include <cmath>
+#include <cstdio>
 #include <stdexcept>
 
 namespace ppb {
@@ -216,6 +219,283 @@ void validate_plan(const Plan& p, const Chain& g, int cluster_devices) {
     if (expect != g.L() + 1)
         throw std::runtime_error("plan does not cover all layers (ends at " + S(expect - 1) + " of " +
                                  S(g.L()) + ")");
+}
+
+// ------------------------------------------------------------------ JSON I/O
+
+namespace {
+
+std::string jstr(const std::string& v) {
+    std::string o = "\"";
+    for (char c : v) {
+        switch (c) {
+            case '"': o += "\\\""; break;
+            case '\\': o += "\\\\"; break;
+            case '\n': o += "\\n"; break;
+            case '\t': o += "\\t"; break;
+            case '\r': o += "\\r"; break;
+            default:
+                if (static_cast<unsigned char>(c) < 0x20) {
+                    char buf[8];
+                    snprintf(buf, sizeof(buf), "\\u%04x", c);
+                    o += buf;
+                } else {
+                    o += c;
+                }
+        }
+    }
+    return o + "\"";
+}
+
+std::string ind(int d) { return std::string(2 * d, ' '); }
+
+std::string int_array(const std::vector<int>& v) {
+    std::string o = "[";
+    for (size_t i = 0; i < v.size(); ++i) o += (i ? "," : "") + S(v[i]);
+    return o + "]";
+}
+
+std::string str_array(const std::vector<std::string>& v, int d) {
+    if (v.empty()) return "[]";
+    std::string o = "[\n";
+    for (size_t i = 0; i < v.size(); ++i) o += ind(d + 1) + jstr(v[i]) + (i + 1 < v.size() ? ",\n" : "\n");
+    return o + ind(d) + "]";
+}
+
+// Minimal JSON reader for plan documents (objects, arrays, numbers, strings,
+// booleans, null).
+struct JVal {
+    enum Kind { kNull, kBool, kNum, kStr, kArr, kObj } kind = kNull;
+    double num = 0;
+    bool b = false;
+    std::string str;
+    std::vector<JVal> arr;
+    std::vector<std::pair<std::string, JVal>> obj;
+    const JVal* find(const std::string& k) const {
+        for (const auto& kv : obj)
+            if (kv.first == k) return &kv.second;
+        return nullptr;
+    }
+    const JVal& at(const std::string& k) const {
+        const JVal* v = find(k);
+        if (!v) throw std::runtime_error("[json.exception.out_of_range.403] key '" + k + "' not found");
+        return *v;
+    }
+    const JVal& at(size_t i) const {
+        if (kind != kArr || i >= arr.size())
+            throw std::runtime_error("[json.exception.out_of_range.401] array index " + S(static_cast<long long>(i)) +
+                                     " is out of range");
+        return arr[i];
+    }
+    int as_int() const {
+        if (kind != kNum) throw std::runtime_error("[json.exception.type_error.302] type must be number");
+        return static_cast<int>(num);
+    }
+    const std::string& as_str() const {
+        if (kind != kStr) throw std::runtime_error("[json.exception.type_error.302] type must be string");
+        return str;
+    }
+};
+
+struct JParser {
+    const std::string& t;
+    size_t i = 0;
+    explicit JParser(const std::string& s) : t(s) {}
+    [[noreturn]] void fail(const std::string& what) {
+        throw std::runtime_error("plan parse error: " + what + " at offset " + S(static_cast<long long>(i)));
+    }
+    void ws() {
+        while (i < t.size() && (t[i] == ' ' || t[i] == '\n' || t[i] == '\t' || t[i] == '\r')) ++i;
+    }
+    JVal value() {
+        ws();
+        if (i >= t.size()) fail("unexpected end of input");
+        JVal v;
+        const char c = t[i];
+        if (c == '{') {
+            v.kind = JVal::kObj;
+            ++i;
+            ws();
+            if (i < t.size() && t[i] == '}') {
+                ++i;
+                return v;
+            }
+            while (true) {
+                ws();
+                JVal k = value();
+                if (k.kind != JVal::kStr) fail("object key must be a string");
+                ws();
+                if (i >= t.size() || t[i] != ':') fail("expected ':'");
+                ++i;
+                v.obj.emplace_back(k.str, value());
+                ws();
+                if (i < t.size() && t[i] == ',') {
+                    ++i;
+                    continue;
+                }
+                if (i < t.size() && t[i] == '}') {
+                    ++i;
+                    return v;
+                }
+                fail("expected ',' or '}'");
+            }
+        }
+        if (c == '[') {
+            v.kind = JVal::kArr;
+            ++i;
+            ws();
+            if (i < t.size() && t[i] == ']') {
+                ++i;
+                return v;
+            }
+            while (true) {
+                v.arr.push_back(value());
+                ws();
+                if (i < t.size() && t[i] == ',') {
+                    ++i;
+                    continue;
+                }
+                if (i < t.size() && t[i] == ']') {
+                    ++i;
+                    return v;
+                }
+                fail("expected ',' or ']'");
+            }
+        }
+        if (c == '"') {
+            v.kind = JVal::kStr;
+            ++i;
+            while (i < t.size() && t[i] != '"') {
+                if (t[i] == '\\' && i + 1 < t.size()) {
+                    const char e = t[i + 1];
+                    v.str += e == 'n' ? '\n' : e == 't' ? '\t' : e == 'r' ? '\r' : e;
+                    i += 2;
+                } else {
+                    v.str += t[i++];
+                }
+            }
+            if (i >= t.size()) fail("unterminated string");
+            ++i;
+            return v;
+        }
+        if (t.compare(i, 4, "true") == 0) {
+            v.kind = JVal::kBool;
+            v.b = true;
+            i += 4;
+            return v;
+        }
+        if (t.compare(i, 5, "false") == 0) {
+            v.kind = JVal::kBool;
+            i += 5;
+            return v;
+        }
+        if (t.compare(i, 4, "null") == 0) {
+            i += 4;
+            return v;
+        }
+        size_t end = i;
+        while (end < t.size() && (isdigit(static_cast<unsigned char>(t[end])) || t[end] == '-' || t[end] == '+' ||
+                                  t[end] == '.' || t[end] == 'e' || t[end] == 'E'))
+            ++end;
+        if (end == i) fail("syntax error");
+        v.kind = JVal::kNum;
+        v.num = std::stod(t.substr(i, end - i));
+        i = end;
+        return v;
+    }
+};
+
+}  // namespace
+
+std::string serialize_plan(const Plan& p, const std::vector<std::string>& provenance) {
+    std::vector<std::string> bounds;
+    for (int b : p.boundaries) bounds.push_back(b == kConcat ? "concat" : "direct");
+    std::string o = "{\n";
+    o += ind(1) + "\"boundaries\": " + str_array(bounds, 1) + ",\n";
+    o += ind(1) + "\"n\": " + S(p.n) + ",\n";
+    o += ind(1) + "\"provenance\": " + str_array(provenance, 1) + ",\n";
+    o += ind(1) + "\"schema\": 1,\n";
+    o += ind(1) + "\"submodules\": ";
+    if (p.subs.empty()) {
+        o += "[]\n";
+    } else {
+        o += "[\n";
+        for (size_t j = 0; j < p.subs.size(); ++j) {
+            const SubModule& sm = p.subs[j];
+            o += ind(2) + "{\n";
+            o += ind(3) + "\"devices\": " + int_array(sm.devices) + ",\n";
+            std::vector<const Shard*> all;
+            for (const auto& row : sm.shards)
+                for (const Shard& s : row) all.push_back(&s);
+            o += ind(3) + "\"shards\": ";
+            if (all.empty()) {
+                o += "[]";
+            } else {
+                o += "[\n";
+                for (size_t k = 0; k < all.size(); ++k) {
+                    const Shard& s = *all[k];
+                    o += ind(4) + "{\n";
+                    o += ind(5) + "\"device\": " + S(s.device_id) + ",\n";
+                    o += ind(5) + "\"layer\": " + S(s.layer_id) + ",\n";
+                    o += ind(5) + "\"range\": " + int_array({s.lo, s.hi});
+                    o += s.replicated ? ",\n" + ind(5) + "\"replicated\": true\n" : "\n";
+                    o += ind(4) + "}" + (k + 1 < all.size() ? ",\n" : "\n");
+                }
+                o += ind(3) + "]";
+            }
+            o += ",\n" + ind(3) + "\"span\": " + int_array({sm.first_layer, sm.last_layer}) + "\n";
+            o += ind(2) + "}" + (j + 1 < p.subs.size() ? ",\n" : "\n");
+        }
+        o += ind(1) + "]\n";
+    }
+    return o + "}\n";
+}
+
+Plan parse_plan(const std::string& text, std::vector<std::string>* provenance) {
+    JParser jp(text);
+    const JVal doc = jp.value();
+    jp.ws();
+    if (jp.i != text.size()) jp.fail("trailing characters");
+    Plan p;
+    p.n = doc.at("n").as_int();
+    int index = 1;
+    const JVal& subs = doc.at("submodules");
+    for (const JVal& jm : subs.arr) {
+        SubModule sm;
+        sm.index = index++;
+        sm.first_layer = jm.at("span").at(0).as_int();
+        sm.last_layer = jm.at("span").at(1).as_int();
+        if (const JVal* d = jm.find("devices"))
+            for (const JVal& x : d->arr) sm.devices.push_back(x.as_int());
+        sm.shards.assign(std::max(0, sm.last_layer - sm.first_layer + 1), {});
+        for (const JVal& js : jm.at("shards").arr) {
+            Shard s;
+            s.layer_id = js.at("layer").as_int();
+            s.device_id = js.at("device").as_int();
+            s.lo = js.at("range").at(0).as_int();
+            s.hi = js.at("range").at(1).as_int();
+            const JVal* r = js.find("replicated");
+            s.replicated = r != nullptr && r->kind == JVal::kBool && r->b;
+            if (s.layer_id < sm.first_layer || s.layer_id > sm.last_layer)
+                throw std::runtime_error("plan shard layer " + S(s.layer_id) + " outside its sub-module span");
+            sm.shards[s.layer_id - sm.first_layer].push_back(s);
+        }
+        if (sm.devices.empty() && !sm.shards.empty())
+            for (const Shard& s : sm.shards.front()) sm.devices.push_back(s.device_id);
+        p.subs.push_back(std::move(sm));
+    }
+    for (const JVal& jb : doc.at("boundaries").arr) {
+        const std::string& b = jb.as_str();
+        if (b == "concat") p.boundaries.push_back(kConcat);
+        else if (b == "direct") p.boundaries.push_back(kDirect);
+        else throw std::runtime_error("unknown boundary kind \"" + b + "\"");
+    }
+    if (provenance) {
+        provenance->clear();
+        if (const JVal* pv = doc.find("provenance"))
+            for (const JVal& x : pv->arr) provenance->push_back(x.as_str());
+    }
+    return p;
 }
 
 Plan plan_from_flat(const int* f, int len) {

@@ -58,6 +58,11 @@ Plan merge_all(const Plan& p);
 void validate_chain(const Chain& g);
 void validate_plan(const Plan& p, const Chain& g, int cluster_devices);
 
+// Plan documents (src/partition.cpp:303-384): the reference's JSON schema,
+// serialised byte-for-byte like its nlohmann::json dump(2).
+std::string serialize_plan(const Plan& p, const std::vector<std::string>& provenance);
+Plan parse_plan(const std::string& text, std::vector<std::string>* provenance);
+
 Plan plan_from_flat(const int* flat, int len);
 std::vector<int> plan_to_flat(const Plan& p);
 

@@ -77,6 +77,20 @@ def main():
         staged.append({"dims": dims, "groups": groups, **({"plan": res["ok"].tolist()} if "ok" in res else res)})
     g["build_staged_plan"] = staged
 
+    # plan JSON I/O (partition.cpp:303-384): byte-exact serialisations + parse cases
+    js = []
+    for e in plans[:: 7]:
+        if "plan" not in e:
+            continue
+        prov = ["merge[1..2]"] if e["Z"] >= 2 else []
+        src = e["merged_1_2"] if e["Z"] >= 2 else e["plan"]
+        js.append({"plan": src, "provenance": prov, "json": r.serialize_plan(np.array(src), prov)})
+    g["serialize_plan"] = js
+    bad = ['{"n": 2, "submodules": [{"span": [1, 1], "shards": [{"layer": 2, "device": 1, "range": [0, 4]}]}], "boundaries": []}',
+           '{"n": 1, "submodules": [{"span": [1, 1], "devices": [1], "shards": [{"layer": 1, "device": 1, "range": [0, 4]}]}], "boundaries": ["sideways"]}',
+           '{"n": 1, "submodules": [{"span": [1, 2], "shards": [{"layer": 1, "device": 1, "range": [0, 4]}, {"layer": 2, "device": 1, "range": [0, 3], "replicated": true}]}], "boundaries": []}']
+    g["parse_plan"] = [{"text": t, **({"plan": v["ok"].tolist()} if "ok" in (v := call(r.parse_plan, t)) else v)} for t in bad]
+
     # verify instances (verify.cpp:20-62) with the reference's own outputs
     inst = []
     for k in range(60):

@@ -9,7 +9,7 @@ import pytest
 
 from _util import golden, oracle
 from paper_2207_11019_b200 import api
-from paper_2207_11019_b200.api import BoundaryKind, LayerSpec, ModelGraph, PipeplanError
+from paper_2207_11019_b200.api import BoundaryKind, LayerSpec, ModelGraph, PipeplanError  # noqa: F401
 
 
 def test_split_layer_golden():
@@ -149,3 +149,28 @@ def test_planner_matches_oracle_random():
             assert str(ei.value) == str(e)
             continue
         assert api.build_plan(dims, n, Z, rep).to_flat().tolist() == ref
+
+
+def test_serialize_plan_byte_identical_to_reference():
+    """partition.cpp:303-331: the same JSON text the reference writes."""
+    for e in golden()["serialize_plan"]:
+        p = api.PartitionPlan.from_flat(e["plan"], e["provenance"])
+        assert api.serialize_plan(p) == e["json"]
+
+
+def test_parse_plan_round_trip_and_errors():
+    for e in golden()["serialize_plan"]:
+        p = api.parse_plan(e["json"])
+        assert p.to_flat().tolist() == e["plan"]
+        assert p.provenance == e["provenance"]
+    for e in golden()["parse_plan"]:
+        if "error" in e:
+            with pytest.raises(PipeplanError) as ei:
+                api.parse_plan(e["text"])
+            assert str(ei.value) == e["error"]
+        else:
+            assert api.parse_plan(e["text"]).to_flat().tolist() == e["plan"]
+    with pytest.raises(PipeplanError, match="plan parse error"):
+        api.parse_plan("{not json")
+    with pytest.raises(PipeplanError, match="key 'n' not found"):
+        api.parse_plan('{"submodules": [], "boundaries": []}')

@@ -1,5 +1,5 @@
 #!/bin/bash
-# One GPU session: tests, smoke, bench lines, ncu launch list + one full capture.
+# One GPU session: tests, smoke, bench lines, ncu launch list + a full capture.
 # Usage (under gpurun): bash tools/gpu_round.sh <tag> [tests|notests]
 set -u
 TAG=${1:-r01}
@@ -9,9 +9,13 @@ if [ "${2:-tests}" = "tests" ]; then
   timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/${TAG}_pytest_gpu.txt 2>&1; echo "pytest rc=$?"
   tail -3 gpurun_out/${TAG}_pytest_gpu.txt
 fi
-timeout 300 python __graft_entry__.py smoke > gpurun_out/${TAG}_smoke.txt 2>&1; echo "smoke rc=$?"; tail -2 gpurun_out/${TAG}_smoke.txt
-timeout 600 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench rc=$?"; cat gpurun_out/${TAG}_bench.json; tail -5 gpurun_out/${TAG}_bench.err
-timeout 300 python bench.py --workload mlp784 --steps 50 > gpurun_out/${TAG}_bench_mlp784.json 2>&1; echo "bench784 rc=$?"; tail -c 1500 gpurun_out/${TAG}_bench_mlp784.json
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_ncu_launch_stdout.txt 2>&1; echo "ncu list rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 12 -c 3 -o gpurun_out/${TAG}_gemm python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_ncu_full_stdout.txt 2>&1; echo "ncu full rc=$?"
-ls -la gpurun_out | tail -20
+timeout 300 python __graft_entry__.py smoke > gpurun_out/${TAG}_smoke.txt 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/${TAG}_smoke.txt
+for W in vgg16 wide_mlp mlp784; do
+  timeout 600 python bench.py --workload $W > gpurun_out/${TAG}_bench_${W}.json 2> gpurun_out/${TAG}_bench_${W}.err; echo "bench $W rc=$?"
+  timeout 600 python bench.py --workload $W --impl reference > gpurun_out/${TAG}_ref_${W}.json 2>&1; echo "ref $W rc=$?"
+done
+timeout 300 python tools/profile_ops.py vgg16 > gpurun_out/${TAG}_ops_vgg16.jsonl 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_ncu_launch_stdout.txt 2>&1; echo "ncu list rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 5 -c 4 -o gpurun_out/${TAG}_gemm python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_ncu_full_stdout.txt 2>&1; echo "ncu full rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 12 -c 2 -o gpurun_out/${TAG}_gemm_wide python bench.py --workload wide_mlp --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_ncu_full_wide_stdout.txt 2>&1; echo "ncu full wide rc=$?"
+ls gpurun_out | grep ${TAG}
