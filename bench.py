@@ -176,6 +176,7 @@ def reference_bounded(workload, nthreads, target_s=12.0):
     net = build_net(workload, seed=0)
     dims, acts = net.dims(), net.acts()
     W, b = net.pack()
+    rng = np.random.default_rng(0)
     n = max(1, min(nthreads, min(dims[1:])))
     plan = R.build_plan(dims, n, 1)
     # calibrate: a tiny probe, then size the sample for ~target_s of CPU work
