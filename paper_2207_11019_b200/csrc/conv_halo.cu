@@ -1,0 +1,417 @@
+// Halo-reuse implicit-GEMM 3x3 convolution for sm_100a (tcgen05, TF32).
+//
+// The rank-4 implicit GEMM in gemm_tc.cu stages a fresh 128-pixel x 32-channel
+// A box for every one of the 9 taps, so A crosses L2 -> SM nine times.  On the
+// narrow layers (C_out <= 128, large spatial grids) that traffic, not the
+// tensor core, sets the speed: ~42 B/clk/SM of TMA service against a 128 x 64
+// x 32 MMA block that needs ~130 clk.
+//
+// Here the GEMM rows are positions of the PADDED grid [imgs][hp][wp] (the
+// rows at pad positions are computed and dropped by the epilogue, ~13% extra
+// MMA work at 32x32, ~27% at 16x16).  In that space tap (r, s) is a constant
+// row shift r*wp + s, so one TMA box of 128 + 2*(wp+1) consecutive rows (the
+// "halo") per 32-channel block serves all 9 taps: the MMA issuer points the
+// SW128 K-major A descriptor at halo row r*wp + s (rows are 128 B apart, the
+// swizzle phase follows the absolute smem address exactly as the TMA wrote it).
+// A traffic drops ~6x; B (weights) streams through its own ring.
+//
+//   warp 0      TMA producer: halo ring (3 x 32 KB) + B ring
+//   warp 1      MMA issuer (leader CTA; CG = 2 -> M = 256 over a CTA pair)
+//   warp 2      TMEM allocator (2 x BN accumulator columns)
+//   warps 4..7  epilogue: padded position -> output pixel (or skip) -> the
+//               shared epilogue32 (bias/ReLU/remap/slots/mask)
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+
+#include "epilogue.cuh"
+#include "gemm_tc.h"
+#include "ptx.cuh"
+#include "tc_common.cuh"
+
+namespace ppb {
+
+namespace {
+
+std::atomic<unsigned> g_halo_attr{0};
+
+constexpr int kHaloThreads = 256;
+constexpr int kHaloMaxRows = 256;  // TMA box limit
+constexpr int kHaloStageBytes = kHaloMaxRows * 128;
+constexpr int kHaloStages = 3;
+
+template <int BN, int CG>
+struct HaloCfg {
+    static constexpr int kBNc = BN / CG;
+    static constexpr int kStageB = kBNc * kBK * 4;
+    static constexpr int kBudget = 200 * 1024 - kHaloStages * kHaloStageBytes;
+    static constexpr int kBStages = kBudget / kStageB > 12 ? 12 : kBudget / kStageB;
+    static constexpr int kTmemCols = 2 * BN;
+    static constexpr int kSmem = 1024 + kHaloStages * kHaloStageBytes + kBStages * kStageB + 512;
+};
+
+template <bool B_MN, int BN, int CG>
+__global__ void __launch_bounds__(kHaloThreads, 1)
+    halo_conv_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int N,
+                     const __grid_constant__ HaloGeom hg, const __grid_constant__ EpiParams epi,
+                     const __grid_constant__ ConvGeom gb) {
+    using C = HaloCfg<BN, CG>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* sH = smem;
+    uint8_t* sB = smem + kHaloStages * kHaloStageBytes;
+    uint64_t* hfull = reinterpret_cast<uint64_t*>(sB + C::kBStages * C::kStageB);
+    uint64_t* hempty = hfull + kHaloStages;
+    uint64_t* bfull = hempty + kHaloStages;
+    uint64_t* bempty = bfull + C::kBStages;
+    uint64_t* tfull = bempty + C::kBStages;  // [2]
+    uint64_t* tempty = tfull + 2;            // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x / 32;
+    const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+    const bool leader = rank == 0;
+    constexpr int TM = kBM * CG;
+    const int num_m = static_cast<int>((hg.Mp + TM - 1) / TM);
+    const int num_n = (N + BN - 1) / BN;
+    const int num_tiles = num_m * num_n;
+    const int unit = blockIdx.x / CG;
+    const int units = gridDim.x / CG;
+    const int cblocks = hg.cblocks;
+    const uint32_t halo_bytes = static_cast<uint32_t>(hg.rows) * 128u;
+
+    if (warp == 0 && elect_one()) {
+        tma_prefetch(&ta);
+        tma_prefetch(&tb);
+        for (int s = 0; s < kHaloStages; ++s) {
+            mbar_init(&hfull[s], 1);
+            mbar_init(&hempty[s], 1);
+        }
+        for (int s = 0; s < C::kBStages; ++s) {
+            mbar_init(&bfull[s], 1);
+            mbar_init(&bempty[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 4 * CG);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) {
+        if (CG == 2) tmem_alloc_pair(tmem_slot, C::kTmemCols);
+        else tmem_alloc(tmem_slot, C::kTmemCols);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (CG == 2) cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer
+        if (elect_one()) {
+            int hs = 0, bs = 0;
+            uint32_t hph = 0, bph = 0;
+            for (int tile = unit; tile < num_tiles; tile += units) {
+                const long long p0 = static_cast<long long>(tile % num_m) * TM + static_cast<long long>(rank) * kBM;
+                const int n0 = (tile / num_m) * BN + static_cast<int>(rank) * C::kBNc;
+                for (int cb = 0; cb < cblocks; ++cb) {
+                    mbar_wait(&hempty[hs], hph ^ 1);
+                    Tma<CG> th;
+                    th.bar = &hfull[hs];
+                    th.bar_c = 0;
+                    if (CG == 1) {
+                        mbar_arrive_expect_tx(&hfull[hs], halo_bytes);
+                    } else {
+                        th.bar_c = mapa_shared(smem_u32(&hfull[hs]), 0);
+                        if (leader) mbar_arrive_expect_tx(&hfull[hs], 2 * halo_bytes);
+                    }
+                    // rows [p0 - wp - 1, p0 + 128 + wp + 1): out-of-range rows are zero-filled
+                    th.d2(sH + hs * kHaloStageBytes, &ta, cb * 32, static_cast<int>(p0 - hg.wp - 1));
+                    if (++hs == kHaloStages) {
+                        hs = 0;
+                        hph ^= 1;
+                    }
+                    for (int tap = 0; tap < 9; ++tap) {
+                        mbar_wait(&bempty[bs], bph ^ 1);
+                        Tma<CG> t;
+                        t.bar = &bfull[bs];
+                        t.bar_c = 0;
+                        if (CG == 1) {
+                            mbar_arrive_expect_tx(&bfull[bs], C::kStageB);
+                        } else {
+                            t.bar_c = mapa_shared(smem_u32(&bfull[bs]), 0);
+                            if (leader) mbar_arrive_expect_tx(&bfull[bs], 2 * C::kStageB);
+                        }
+                        load_operand<B_MN, C::kBNc, CG>(t, &tb, gb, sB + bs * C::kStageB, n0, tap * cblocks + cb);
+                        if (++bs == C::kBStages) {
+                            bs = 0;
+                            bph ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer (leader CTA)
+        if (leader) {
+            constexpr uint32_t idesc = idesc_tf32(BN, false, B_MN, TM);
+            int hs = 0, bs = 0;
+            uint32_t hph = 0, bph = 0;
+            int local = 0;
+            for (int tile = unit; tile < num_tiles; tile += units, ++local) {
+                const int acc = local & 1;
+                const uint32_t acc_phase = (local >> 1) & 1;
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int cb = 0; cb < cblocks; ++cb) {
+                    mbar_wait(&hfull[hs], hph);
+                    const uint32_t h_addr = smem_u32(sH + hs * kHaloStageBytes);
+                    for (int tap = 0; tap < 9; ++tap) {
+                        const int r = tap / 3, s = tap - 3 * (tap / 3);
+                        mbar_wait(&bfull[bs], bph);
+                        tc_fence_after();
+                        if (elect_one()) {
+                            const uint32_t a_addr = h_addr + static_cast<uint32_t>(r * hg.wp + s) * 128u;
+                            const uint32_t b_addr = smem_u32(sB + bs * C::kStageB);
+#pragma unroll
+                            for (int kk = 0; kk < kBK / 8; ++kk) {
+                                const uint64_t ad = umma_desc<kLayoutSW128>(a_addr + kk * 32, 16, 1024);
+                                const uint64_t bd = B_MN ? umma_desc<kLayoutSW128Base32>(b_addr + kk * 1024, 4096, 512)
+                                                         : umma_desc<kLayoutSW128>(b_addr + kk * 32, 16, 1024);
+                                const uint32_t accum = (cb != 0 || tap != 0 || kk != 0) ? 1u : 0u;
+                                if (CG == 2) mma_tf32_pair(d_tmem, ad, bd, idesc, accum);
+                                else mma_tf32(d_tmem, ad, bd, idesc, accum);
+                            }
+                            if (CG == 2) mma_commit_pair(&bempty[bs]);
+                            else mma_commit(&bempty[bs]);
+                        }
+                        __syncwarp();
+                        if (++bs == C::kBStages) {
+                            bs = 0;
+                            bph ^= 1;
+                        }
+                    }
+                    if (elect_one()) {
+                        if (CG == 2) mma_commit_pair(&hempty[hs]);
+                        else mma_commit(&hempty[hs]);
+                    }
+                    __syncwarp();
+                    if (++hs == kHaloStages) {
+                        hs = 0;
+                        hph ^= 1;
+                    }
+                }
+                if (elect_one()) {
+                    if (CG == 2) mma_commit_pair(&tfull[acc]);
+                    else mma_commit(&tfull[acc]);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------ epilogue
+        const int q = warp & 3;
+        const int lane = threadIdx.x & 31;
+        const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
+        const int hpwp = hg.hp * hg.wp;
+        int local = 0;
+        for (int tile = unit; tile < num_tiles; tile += units, ++local) {
+            const long long p0 = static_cast<long long>(tile % num_m) * TM + static_cast<long long>(rank) * kBM;
+            const int n0 = (tile / num_m) * BN;
+            const int acc = local & 1;
+            const uint32_t acc_phase = (local >> 1) & 1;
+            // padded position -> output pixel, -1 on the pad ring / past the end
+            const long long pos = p0 + q * 32 + lane;
+            int m = -1;
+            if (pos < hg.Mp) {
+                const int img = static_cast<int>(pos / hpwp);
+                const int rem = static_cast<int>(pos - static_cast<long long>(img) * hpwp);
+                const int hh = rem / hg.wp, ww = rem - hh * hg.wp;
+                if (hh >= 1 && hh <= hg.ho && ww >= 1 && ww <= hg.wo) m = (img * hg.ho + hh - 1) * hg.wo + ww - 1;
+            }
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t rr[32];
+                tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, rr);
+                tmem_ld_wait();
+                if (m >= 0) {
+                    float v[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(rr[i]);
+                    epilogue32(epi, m, n0 + c * 32, v);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (CG == 2) mbar_arrive_cluster(tempty_leader + acc * sizeof(uint64_t));
+                else mbar_arrive(&tempty[acc]);
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (CG == 2) cluster_sync();
+    if (warp == 2) {
+        tc_fence_after();
+        if (CG == 2) tmem_dealloc_pair(tmem_base, C::kTmemCols);
+        else tmem_dealloc(tmem_base, C::kTmemCols);
+    }
+}
+
+template <bool B_MN, int BN, int CG>
+cudaError_t launch_halo_t(const TcGemmPlan& p, cudaStream_t s) {
+    using C = HaloCfg<BN, CG>;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if ((g_halo_attr.load() & (1u << (dev & 31))) == 0) {
+        cudaError_t e = halo_conv_init_device();
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(p.grid);
+    cfg.blockDim = dim3(kHaloThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, halo_conv_kernel<B_MN, BN, CG>, p.ta, p.tb, p.N, p.hg, p.epi, p.gb);
+}
+
+template <bool B_MN>
+cudaError_t launch_halo_bn(const TcGemmPlan& p, cudaStream_t s) {
+    if (p.cg == 2) {
+        switch (p.bn) {
+            case 64: return launch_halo_t<B_MN, 64, 2>(p, s);
+            case 128: return launch_halo_t<B_MN, 128, 2>(p, s);
+            default: return launch_halo_t<B_MN, 256, 2>(p, s);
+        }
+    }
+    switch (p.bn) {
+        case 64: return launch_halo_t<B_MN, 64, 1>(p, s);
+        case 128: return launch_halo_t<B_MN, 128, 1>(p, s);
+        default: return launch_halo_t<B_MN, 256, 1>(p, s);
+    }
+}
+
+}  // namespace
+
+cudaError_t halo_conv_init_device() {
+    cudaError_t e = cudaSuccess;
+    auto set = [&](auto kernel, int smem) {
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    };
+#define PPB_HSET(BM)                                                     \
+    set(halo_conv_kernel<BM, 64, 1>, HaloCfg<64, 1>::kSmem);             \
+    set(halo_conv_kernel<BM, 128, 1>, HaloCfg<128, 1>::kSmem);           \
+    set(halo_conv_kernel<BM, 256, 1>, HaloCfg<256, 1>::kSmem);           \
+    set(halo_conv_kernel<BM, 64, 2>, HaloCfg<64, 2>::kSmem);             \
+    set(halo_conv_kernel<BM, 128, 2>, HaloCfg<128, 2>::kSmem);           \
+    set(halo_conv_kernel<BM, 256, 2>, HaloCfg<256, 2>::kSmem);
+    PPB_HSET(false)
+    PPB_HSET(true)
+#undef PPB_HSET
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (e == cudaSuccess) g_halo_attr.fetch_or(1u << (dev & 31));
+    return e;
+}
+
+// A conv forward / dgrad descriptor (conv.h) whose A operand is a 3x3 implicit
+// conv over a padded grid with a one-pixel ring, whose output grid equals the
+// padded grid's interior, and where the padded-space overhead is modest.
+bool halo_conv_eligible(const GemmDesc& d) {
+    const ConvGeom& g = d.a.geom;
+    if (g.mode != OP_CONV_ROWS || d.a.mn_major || g.ksz != 3 || g.off != 0) return false;
+    if (d.b.geom.mode != OP_DENSE && d.b.geom.mode != OP_WFLIP) return false;
+    const int wo = g.wo, ho = g.howo / g.wo;
+    if (d.a.wp != wo + 2 || d.a.hp != ho + 2) return false;
+    if (d.a.wp + 1 > (kHaloMaxRows - kBM) / 2) return false;
+    if (static_cast<long long>(d.a.imgs) * d.a.hp * d.a.wp >= (1LL << 31)) return false;
+    if (d.M != d.a.imgs * ho * wo || d.K != 9 * g.cblocks * 32) return false;
+    const double waste = static_cast<double>(d.a.hp) * d.a.wp / (static_cast<double>(ho) * wo);
+    return waste <= 1.3;
+}
+
+// force: 0 = automatic tile choice; 1000 + bn = 1-CTA tiles of width bn;
+// 2000 + bn = CTA-pair tiles (256 x bn).
+bool halo_conv_prepare(const GemmDesc& d, TcGemmPlan* out, int force, char* err, size_t errlen) {
+    if (!halo_conv_eligible(d)) {
+        snprintf(err, errlen, "conv descriptor not eligible for the halo kernel");
+        return false;
+    }
+    TcGemmPlan p;
+    p.halo = 1;
+    p.M = d.M;
+    p.N = d.N;
+    p.K = d.K;
+    p.a_mn = false;
+    p.b_mn = d.b.mn_major;
+    p.epi = d.epi;
+    p.epi.M = d.M;
+    p.epi.N = d.N;
+    p.ga = d.a.geom;
+    p.gb = d.b.geom;
+    HaloGeom& hg = p.hg;
+    hg.wp = d.a.wp;
+    hg.hp = d.a.hp;
+    hg.wo = d.a.geom.wo;
+    hg.ho = d.a.geom.howo / d.a.geom.wo;
+    hg.cblocks = d.a.geom.cblocks;
+    hg.rows = kBM + 2 * (hg.wp + 1);
+    hg.Mp = static_cast<long long>(d.a.imgs) * hg.hp * hg.wp;
+    int bn, cg;
+    if (force >= 2000) {
+        cg = 2;
+        bn = force - 2000;
+    } else if (force >= 1000) {
+        cg = 1;
+        bn = force - 1000;
+    } else {
+        // pairs halve the per-SM B bytes; pick the narrowest width covering N
+        // (or 256-wide column tiles)
+        cg = hg.Mp > 2 * kBM ? 2 : 1;
+        bn = d.N <= 64 ? 64 : (d.N <= 128 ? 128 : 256);
+    }
+    if (bn != 64 && bn != 128 && bn != 256) {
+        snprintf(err, errlen, "halo conv: unsupported tile width %d", bn);
+        return false;
+    }
+    p.bn = bn;
+    p.cg = cg;
+    const int tm = kBM * cg;
+    const long long tiles = ((hg.Mp + tm - 1) / tm) * ((d.N + bn - 1) / bn);
+    const int units = sm_count() / cg;
+    p.grid = static_cast<int>(tiles < units ? tiles : units) * cg;
+    // A: the padded tensor as a 2-D [Mp rows][ch] matrix, box {32 ch, halo rows}
+    if (!encode_map(&p.ta, d.a.ptr, static_cast<int>(hg.Mp), d.a.ch, d.a.ld, hg.rows, false, err, errlen))
+        return false;
+    if (d.b.geom.mode != OP_DENSE) {
+        if (!encode_conv_map(&p.tb, d.b, err, errlen)) return false;
+    } else if (!encode_map(&p.tb, d.b.ptr, d.b.rows, d.b.cols, d.b.ld, d.b.mn_major ? 32 : bn / cg, d.b.mn_major, err,
+                           errlen)) {
+        return false;
+    }
+    *out = p;
+    return true;
+}
+
+cudaError_t halo_conv_launch(const TcGemmPlan& p, cudaStream_t s) {
+    if (p.M <= 0 || p.N <= 0) return cudaSuccess;
+    return p.b_mn ? launch_halo_bn<true>(p, s) : launch_halo_bn<false>(p, s);
+}
+
+}  // namespace ppb

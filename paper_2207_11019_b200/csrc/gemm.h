@@ -117,6 +117,18 @@ struct SplitK {
     long long stride = 0;
 };
 
+// Padded-position geometry of the halo conv kernel (conv_halo.cu): GEMM row
+// p = position in the [imgs][hp][wp] padded grid of the operand A tensor; the
+// output pixel (h, w) sits at padded position (h + 1, w + 1); taps (r, s) read
+// position p + (r - 1) * wp + (s - 1).
+struct HaloGeom {
+    int wp = 0, hp = 0;   // padded grid (ho + 2, wo + 2)
+    int ho = 0, wo = 0;   // output grid
+    int cblocks = 1;      // 32-channel blocks of A
+    int rows = 0;         // halo rows staged per CTA: 128 + 2 * (wp + 1)
+    long long Mp = 0;     // imgs * hp * wp
+};
+
 struct GemmDesc {
     Operand a, b;
     int M = 0, N = 0, K = 0;

@@ -32,6 +32,7 @@
 #include "epilogue.cuh"
 #include "gemm_tc.h"
 #include "ptx.cuh"
+#include "tc_common.cuh"
 
 namespace ppb {
 
@@ -39,8 +40,6 @@ namespace {
 
 std::atomic<unsigned> g_attr_set{0};  // one bit per device: smem attributes set
 
-constexpr int kBM = 128;  // rows of A per CTA
-constexpr int kBK = 32;
 constexpr int kThreads = 256;
 
 template <int BN, int CG>
@@ -54,62 +53,6 @@ struct TcCfg {
     // dynamic smem: 1 KB alignment slack + stages + barriers
     static constexpr int kSmem = 1024 + kStages * kStageBytes + 256;
 };
-
-// TMA loads of one operand for one pipeline stage: `rows` MN-rows starting at
-// mn0 (this CTA's slice) for K block kb.  CG = 2 signals the leader's barrier.
-template <int CG>
-struct Tma {
-    uint64_t* bar;
-    uint32_t bar_c;
-    __device__ __forceinline__ void d2(void* dst, const CUtensorMap* m, int a, int b) const {
-        if (CG == 2) tma_load_2d_pair(dst, m, bar_c, a, b);
-        else tma_load_2d(dst, m, bar, a, b);
-    }
-    __device__ __forceinline__ void d3(void* dst, const CUtensorMap* m, int a, int b, int c) const {
-        if (CG == 2) tma_load_3d_pair(dst, m, bar_c, a, b, c);
-        else tma_load_3d(dst, m, bar, a, b, c);
-    }
-    __device__ __forceinline__ void d4(void* dst, const CUtensorMap* m, int a, int b, int c, int d) const {
-        if (CG == 2) tma_load_4d_pair(dst, m, bar_c, a, b, c, d);
-        else tma_load_4d(dst, m, bar, a, b, c, d);
-    }
-};
-
-template <bool MN, int ROWS, int CG>
-__device__ __forceinline__ void load_operand(const Tma<CG>& t, const CUtensorMap* map, const ConvGeom& g,
-                                             uint8_t* dst, int mn0, int kb) {
-    const int k0 = kb * kBK;
-    if (g.mode == OP_DENSE) {
-        if (MN) {
-#pragma unroll
-            for (int i = 0; i < ROWS / 32; ++i) t.d2(dst + i * 4096, map, mn0 + 32 * i, k0);
-        } else {
-            t.d2(dst, map, k0, mn0);
-        }
-    } else if (g.mode == OP_CONV_ROWS) {
-        // 128 output pixels (rows) x 32 channels of tap t, channel block cb
-        const int tap = kb / g.cblocks, cb = kb - tap * g.cblocks;
-        const int r = tap / g.ksz, s = tap - r * g.ksz;
-        const int img = mn0 / g.howo, rem = mn0 - img * g.howo, h0 = rem / g.wo;
-        t.d4(dst, map, cb * 32, s + g.off, h0 + r + g.off, img);
-    } else if (g.mode == OP_CONV_KPIX) {
-        // 32 output pixels (K rows) x 32 channels per box; tap from the column
-        const int p0 = k0;
-        const int img = p0 / g.howo, rem = p0 - img * g.howo, h0 = rem / g.wo;
-#pragma unroll
-        for (int i = 0; i < ROWS / 32; ++i) {
-            const int col = mn0 + 32 * i;
-            const int tap = col / g.ck, c0 = col - tap * g.ck;
-            const int r = tap / g.ksz, s = tap - r * g.ksz;
-            t.d4(dst + i * 4096, map, c0, s + g.off, h0 + r + g.off, img);
-        }
-    } else {  // OP_WFLIP
-        const int tap = kb / g.cblocks, kblk = kb - tap * g.cblocks;
-        const int tf = g.ksz * g.ksz - 1 - tap;
-#pragma unroll
-        for (int i = 0; i < ROWS / 32; ++i) t.d3(dst + i * 4096, map, mn0 + 32 * i, tf, kblk * 32);
-    }
-}
 
 template <bool A_MN, bool B_MN, int BN, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -328,6 +271,8 @@ __global__ void splitk_epilogue_kernel(const __grid_constant__ EpiParams epi, co
 
 // ---------------------------------------------------------------- host side
 
+}  // namespace
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
@@ -426,6 +371,8 @@ bool encode_conv_map(CUtensorMap* map, const Operand& o, char* err, size_t errle
     return true;
 }
 
+namespace {
+
 template <bool A_MN, bool B_MN, int BN, int CG>
 cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s);
 
@@ -444,6 +391,8 @@ cudaError_t launch_bn(const TcGemmPlan& p, cudaStream_t s) {
     }
 }
 
+}  // namespace
+
 int sm_count() {
     static int n = 0;
     if (n == 0) {
@@ -454,8 +403,6 @@ int sm_count() {
     }
     return n;
 }
-
-}  // namespace
 
 // Set the dynamic shared-memory limit of every instantiation on the current
 // device (must happen before any launch is captured into a CUDA graph).
@@ -475,6 +422,7 @@ cudaError_t tc_gemm_init_device() {
     PPB_SET(true, false)
     PPB_SET(true, true)
 #undef PPB_SET
+    if (e == cudaSuccess) e = halo_conv_init_device();
     int dev = 0;
     cudaGetDevice(&dev);
     if (e == cudaSuccess) g_attr_set.fetch_or(1u << (dev & 31));
@@ -516,6 +464,17 @@ cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
 
 bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err, size_t errlen,
                      const WsAlloc& ws_alloc) {
+    // 3x3 convs over large padded grids: the halo-reuse kernel (conv_halo.cu)
+    static const bool no_halo = [] {
+        const char* e = getenv("PPB_NO_HALO");
+        return e != nullptr && *e != '\0' && *e != '0';
+    }();
+    if ((force_bn >= 1000 || (force_bn == 0 && !no_halo)) && halo_conv_eligible(d))
+        return halo_conv_prepare(d, out, force_bn, err, errlen);
+    if (force_bn >= 1000) {
+        snprintf(err, errlen, "halo conv tile forced on an ineligible GEMM");
+        return false;
+    }
     TcGemmPlan p;
     p.M = d.M;
     p.N = d.N;
@@ -626,6 +585,7 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
 
 cudaError_t tc_gemm_launch(const TcGemmPlan& p, cudaStream_t s) {
     if (p.M <= 0 || p.N <= 0) return cudaSuccess;
+    if (p.halo) return halo_conv_launch(p, s);
     if (p.a_mn) {
         return p.b_mn ? launch_bn<true, true>(p, s) : launch_bn<true, false>(p, s);
     }

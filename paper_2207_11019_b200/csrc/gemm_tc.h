@@ -23,6 +23,8 @@ struct TcGemmPlan {
     EpiParams epi;
     ConvGeom ga, gb;
     SplitK sk;
+    int halo = 0;  // 1: conv_halo.cu kernel (hg describes the padded grid)
+    HaloGeom hg;
 };
 
 // ws_alloc (optional): allocates split-K workspace (floats) on the GEMM's
@@ -32,6 +34,19 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
                      const WsAlloc& ws_alloc = nullptr);
 cudaError_t tc_gemm_launch(const TcGemmPlan& p, cudaStream_t s);
 cudaError_t tc_gemm_init_device();
+
+// Halo-reuse implicit conv (conv_halo.cu): a 3x3 stride-1 conv over a padded
+// NHWC grid computed in padded-position space; see halo_conv_prepare.
+bool halo_conv_eligible(const GemmDesc& d);
+bool halo_conv_prepare(const GemmDesc& d, TcGemmPlan* p, int force, char* err, size_t errlen);
+cudaError_t halo_conv_launch(const TcGemmPlan& p, cudaStream_t s);
+cudaError_t halo_conv_init_device();
+
+// host helpers shared by the tcgen05 kernels (gemm_tc.cu)
+bool encode_map(CUtensorMap* map, const float* ptr, int rows, int cols, long long ld, int box_rows, bool mn_major,
+                char* err, size_t errlen);
+bool encode_conv_map(CUtensorMap* map, const Operand& o, char* err, size_t errlen);
+int sm_count();
 
 // Exact-fp32 SIMT path with identical operand conventions and epilogues
 // (debug / tight-tolerance parity mode).

@@ -460,6 +460,93 @@ __global__ void conv_merge_kernel(ConvMerge m, float* __restrict__ db_partial) {
     }
 }
 
+// Vectorised conv_merge (slot_kind 0, VEC 4): one image row (n, h) per block
+// iteration, thread = (pixel column w, channel group g) with g fixed for the
+// thread.  Index math is per row; the U pixels a thread owns in a row are
+// loaded first (slot, argmax, mask) and then combined, so each thread keeps
+// ~3U independent loads in flight instead of a dependent chain per element.
+template <int U>
+__global__ void conv_merge_rows_kernel(ConvMerge m, float* __restrict__ db_partial) {
+    const int groups = m.uch >> 2;
+    const int g = threadIdx.x % groups;
+    const int c0 = g * 4;
+    const int wstep = blockDim.x / groups;
+    const int w0 = threadIdx.x / groups;
+    const int Hg = m.Ho / m.pool, Wg = m.Wo / m.pool;
+    const int hq = m.Ho + 2 * m.q, wq = m.Wo + 2 * m.q;
+    const int rows = m.imgs * m.Ho;
+    const ActLayout& a = m.act_layout;
+    float4 db = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+        const int n = r / m.Ho, h = r - n * m.Ho;
+        const int y = m.pool == 2 ? h >> 1 : h;
+        const bool row_in = y < Hg;
+        const long long grow = (static_cast<long long>(n) * Hg + y) * Wg;
+        const float* arow = m.mask_kind == 2
+                                ? m.act + ((static_cast<long long>(n) * a.hp + h + a.pad) * a.wp + a.pad) * a.ld + a.col0 + c0
+                                : nullptr;
+        const float* urow = m.mask_kind == 1 ? m.U + static_cast<long long>(r) * m.Wo * m.ldu + c0 : nullptr;
+        float* orow = m.d_pad + ((static_cast<long long>(n) * hq + h + m.q) * wq + m.q) * m.ldd + c0;
+        for (int wb = w0; wb < m.Wo; wb += U * wstep) {
+            float4 gr[U];
+            uint32_t am[U];
+            float4 mk[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int w = wb + u * wstep;
+                gr[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                am[u] = 0;
+                mk[u] = make_float4(1.f, 1.f, 1.f, 1.f);
+                if (w >= m.Wo) continue;
+                const int x = m.pool == 2 ? w >> 1 : w;
+                if (row_in && x < Wg) {
+                    const long long gp = grow + x;
+                    for (int s = 0; s < m.slots.n; ++s) {
+                        const float4 v = __ldg(reinterpret_cast<const float4*>(m.slots.slot[s] + gp * m.lds + c0));
+                        gr[u].x += v.x; gr[u].y += v.y; gr[u].z += v.z; gr[u].w += v.w;
+                    }
+                    if (m.pool == 2) am[u] = __ldg(reinterpret_cast<const uint32_t*>(m.argmax + gp * m.uch + c0));
+                } else {
+                    am[u] = 0xffffffffu;  // outside the pooled grid: no gradient
+                }
+                if (m.mask_kind == 2) mk[u] = __ldg(reinterpret_cast<const float4*>(arow + static_cast<long long>(w) * a.ld));
+                else if (m.mask_kind == 1) mk[u] = __ldg(reinterpret_cast<const float4*>(urow + static_cast<long long>(w) * m.ldu));
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int w = wb + u * wstep;
+                if (w >= m.Wo) continue;
+                float4 v = gr[u];
+                if (m.pool == 2) {  // outside the pooled grid gr is 0 already
+                    const uint32_t want = static_cast<uint32_t>(((h & 1) << 1) | (w & 1));
+                    const uint32_t b = am[u];
+                    if ((b & 0xffu) != want) v.x = 0.f;
+                    if (((b >> 8) & 0xffu) != want) v.y = 0.f;
+                    if (((b >> 16) & 0xffu) != want) v.z = 0.f;
+                    if ((b >> 24) != want) v.w = 0.f;
+                }
+                if (!(mk[u].x > 0.f)) v.x = 0.f;
+                if (!(mk[u].y > 0.f)) v.y = 0.f;
+                if (!(mk[u].z > 0.f)) v.z = 0.f;
+                if (!(mk[u].w > 0.f)) v.w = 0.f;
+                *reinterpret_cast<float4*>(orow + static_cast<long long>(w) * m.ldd) = v;
+                db.x += v.x; db.y += v.y; db.z += v.z; db.w += v.w;
+            }
+        }
+    }
+    extern __shared__ float sh[];
+    reinterpret_cast<float4*>(sh)[threadIdx.x] = db;
+    __syncthreads();
+    if (threadIdx.x < groups) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int t = threadIdx.x; t < static_cast<int>(blockDim.x); t += groups) {
+            const float4 v = reinterpret_cast<const float4*>(sh)[t];
+            acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        *reinterpret_cast<float4*>(db_partial + static_cast<long long>(blockIdx.x) * m.uch + c0) = acc;
+    }
+}
+
 int grid_for(long long work, int threads) {
     long long g = (work + threads - 1) / threads;
     const long long cap = 148LL * 16;
@@ -582,7 +669,9 @@ cudaError_t launch_conv_merge(const ConvMerge& m, float* db_partial, cudaStream_
         return cudaMemsetAsync(db_partial, 0, sizeof(float) * grid * m.uch, s);
     }
     const bool i32 = n < (1LL << 31);
-    if (v4) {
+    if (v4 && (m.pool == 1 || m.pool == 2)) {
+        conv_merge_rows_kernel<2><<<grid, block, shmem, s>>>(m, db_partial);
+    } else if (v4) {
         if (i32) conv_merge_kernel<4, unsigned><<<grid, block, shmem, s>>>(m, db_partial);
         else conv_merge_kernel<4, long long><<<grid, block, shmem, s>>>(m, db_partial);
     } else {

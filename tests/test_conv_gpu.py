@@ -111,3 +111,39 @@ def test_conv_wgrad_transposed_splitk(shape):
     ref = ref.permute(0, 2, 3, 1).reshape(u, k * k, Cin)
     got = out.reshape(u, k * k, ck)
     assert rel(got[:, :, :Cin].double(), ref) < 2e-3
+
+
+# Halo-reuse kernel (csrc/conv_halo.cu): padded-position GEMM rows, one halo
+# box per 32-channel block shared by the 9 taps.  force = 1000 + bn (1-CTA) or
+# 2000 + bn (CTA pair).
+HALO_SHAPES = [
+    (4, 32, 32, 64, 64, 3, 1),
+    (8, 16, 16, 64, 128, 3, 1),
+    (3, 16, 32, 96, 80, 3, 1),
+    (2, 32, 32, 3, 64, 3, 1),
+    (5, 16, 16, 128, 256, 3, 1),
+]
+HALO_TILES = [1064, 1128, 1256, 2064, 2128, 2256]
+
+
+@pytest.mark.parametrize("shape", HALO_SHAPES)
+@pytest.mark.parametrize("bn", HALO_TILES)
+def test_conv_forward_halo(shape, bn):
+    test_conv_forward(shape, bn)
+
+
+@pytest.mark.parametrize("shape", HALO_SHAPES)
+@pytest.mark.parametrize("bn", HALO_TILES)
+def test_conv_dgrad_halo(shape, bn):
+    test_conv_dgrad(shape, bn)
+
+
+def test_halo_ineligible_is_refused():
+    """A 4x4 grid (2.25x padded-space overhead) is not routed to the halo
+    kernel; forcing it reports an error instead of computing."""
+    shape = (32, 4, 4, 256, 256, 3, 1)
+    x, wt, dy, x_pad, w, d_pad, ldx, ldd, ck, Ho, Wo = _setup(*shape)
+    N, H, W, Cin, u, k, p = shape
+    out = torch.zeros(N * Ho * Wo, r4(u), device="cuda")
+    with pytest.raises(Exception):
+        _call(0, N, H, W, Cin, ldx, p, k, x_pad, w, u, d_pad, ldd, out, r4(u), 1128)
