@@ -550,7 +550,8 @@ class Session:
         ms, fl = np.zeros(max(n.value, 1)), np.zeros(max(n.value, 1))
         check(L.ppb_session_profile_ops(self._h, _ip(k), _ip(lay), _ip(inf), _dp(ms), _dp(fl), n.value, C.byref(n)))
         return [{"kind": self.OP_KINDS[k[i]] if k[i] < len(self.OP_KINDS) else int(k[i]), "layer": int(lay[i]),
-                 "bn": int(inf[i] & 1023), "cg": int((inf[i] >> 10) & 3), "splits": int(inf[i] >> 12),
+                 "bn": int(inf[i] & 1023), "cg": int((inf[i] >> 10) & 3),
+                 "splits": int((inf[i] >> 12) & 4095), "halo": int((inf[i] >> 24) & 1),
                  "ms": float(ms[i]), "tflops": float(fl[i] / ms[i] / 1e9) if ms[i] > 0 else 0.0}
                 for i in range(n.value)]
 

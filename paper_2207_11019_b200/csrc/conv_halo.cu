@@ -13,9 +13,12 @@
 // "halo") per 32-channel block serves all 9 taps: the MMA issuer points the
 // SW128 K-major A descriptor at halo row r*wp + s (rows are 128 B apart, the
 // swizzle phase follows the absolute smem address exactly as the TMA wrote it).
-// A traffic drops ~6x; B (weights) streams through its own ring.
+// A traffic drops ~6x.  B (the weights) is then the larger stream: when the
+// CTA's whole B column slice (BN/CG rows x 9*C) fits beside two halo stages it
+// is loaded ONCE per CTA and stays resident (VGG conv2 / conv3 and their dgrads);
+// otherwise it streams through its own ring.
 //
-//   warp 0      TMA producer: halo ring (3 x 32 KB) + B ring
+//   warp 0      TMA producer: halo ring (2-4 stages) + resident B / B ring
 //   warp 1      MMA issuer (leader CTA; CG = 2 -> M = 256 over a CTA pair)
 //   warp 2      TMEM allocator (2 x BN accumulator columns)
 //   warps 4..7  epilogue: padded position -> output pixel (or skip) -> the
@@ -25,6 +28,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 
 #include "epilogue.cuh"
 #include "gemm_tc.h"
@@ -39,17 +43,14 @@ std::atomic<unsigned> g_halo_attr{0};
 
 constexpr int kHaloThreads = 256;
 constexpr int kHaloMaxRows = 256;  // TMA box limit
-constexpr int kHaloStageBytes = kHaloMaxRows * 128;
-constexpr int kHaloStages = 3;
+constexpr int kHaloSmemMax = 227 * 1024;
+constexpr int kHaloReserve = 1024 + 1024;  // alignment slack + barriers
 
 template <int BN, int CG>
 struct HaloCfg {
     static constexpr int kBNc = BN / CG;
     static constexpr int kStageB = kBNc * kBK * 4;
-    static constexpr int kBudget = 200 * 1024 - kHaloStages * kHaloStageBytes;
-    static constexpr int kBStages = kBudget / kStageB > 12 ? 12 : kBudget / kStageB;
     static constexpr int kTmemCols = 2 * BN;
-    static constexpr int kSmem = 1024 + kHaloStages * kHaloStageBytes + kBStages * kStageB + 512;
 };
 
 template <bool B_MN, int BN, int CG>
@@ -61,13 +62,15 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
+    const int kHaloStages = hg.hstages, kHaloStageBytes = hg.hstage_bytes;
+    const int kBStages = hg.bstages;  // resident: one slot per K block, loaded once
     uint8_t* sH = smem;
     uint8_t* sB = smem + kHaloStages * kHaloStageBytes;
-    uint64_t* hfull = reinterpret_cast<uint64_t*>(sB + C::kBStages * C::kStageB);
+    uint64_t* hfull = reinterpret_cast<uint64_t*>(sB + kBStages * C::kStageB);
     uint64_t* hempty = hfull + kHaloStages;
     uint64_t* bfull = hempty + kHaloStages;
-    uint64_t* bempty = bfull + C::kBStages;
-    uint64_t* tfull = bempty + C::kBStages;  // [2]
+    uint64_t* bempty = bfull + kBStages;
+    uint64_t* tfull = bempty + kBStages;  // [2]
     uint64_t* tempty = tfull + 2;            // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -90,7 +93,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             mbar_init(&hfull[s], 1);
             mbar_init(&hempty[s], 1);
         }
-        for (int s = 0; s < C::kBStages; ++s) {
+        for (int s = 0; s < kBStages; ++s) {
             mbar_init(&bfull[s], 1);
             mbar_init(&bempty[s], 1);
         }
@@ -115,6 +118,23 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         if (elect_one()) {
             int hs = 0, bs = 0;
             uint32_t hph = 0, bph = 0;
+            if (hg.resident) {
+                // the whole B slice of this CTA (one column tile): every K block,
+                // one barrier per block so the first MMAs start early
+                const int n0 = static_cast<int>(rank) * C::kBNc;
+                for (int kb = 0; kb < 9 * cblocks; ++kb) {
+                    Tma<CG> t;
+                    t.bar = &bfull[kb];
+                    t.bar_c = 0;
+                    if (CG == 1) {
+                        mbar_arrive_expect_tx(&bfull[kb], C::kStageB);
+                    } else {
+                        t.bar_c = mapa_shared(smem_u32(&bfull[kb]), 0);
+                        if (leader) mbar_arrive_expect_tx(&bfull[kb], 2 * C::kStageB);
+                    }
+                    load_operand<B_MN, C::kBNc, CG>(t, &tb, gb, sB + kb * C::kStageB, n0, kb);
+                }
+            }
             for (int tile = unit; tile < num_tiles; tile += units) {
                 const long long p0 = static_cast<long long>(tile % num_m) * TM + static_cast<long long>(rank) * kBM;
                 const int n0 = (tile / num_m) * BN + static_cast<int>(rank) * C::kBNc;
@@ -135,6 +155,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                         hs = 0;
                         hph ^= 1;
                     }
+                    if (hg.resident) continue;
                     for (int tap = 0; tap < 9; ++tap) {
                         mbar_wait(&bempty[bs], bph ^ 1);
                         Tma<CG> t;
@@ -147,7 +168,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                             if (leader) mbar_arrive_expect_tx(&bfull[bs], 2 * C::kStageB);
                         }
                         load_operand<B_MN, C::kBNc, CG>(t, &tb, gb, sB + bs * C::kStageB, n0, tap * cblocks + cb);
-                        if (++bs == C::kBStages) {
+                        if (++bs == kBStages) {
                             bs = 0;
                             bph ^= 1;
                         }
@@ -169,15 +190,22 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
                 for (int cb = 0; cb < cblocks; ++cb) {
-                    mbar_wait(&hfull[hs], hph);
+                    if (!(hg.dbg & 4) || local == 0) mbar_wait(&hfull[hs], hph);
                     const uint32_t h_addr = smem_u32(sH + hs * kHaloStageBytes);
                     for (int tap = 0; tap < 9; ++tap) {
                         const int r = tap / 3, s = tap - 3 * (tap / 3);
-                        mbar_wait(&bfull[bs], bph);
+                        const int kb = tap * cblocks + cb;
+                        if (hg.resident) {
+                            if (local == 0) mbar_wait(&bfull[kb], 0);
+                        } else {
+                            mbar_wait(&bfull[bs], bph);
+                        }
                         tc_fence_after();
                         if (elect_one()) {
-                            const uint32_t a_addr = h_addr + static_cast<uint32_t>(r * hg.wp + s) * 128u;
-                            const uint32_t b_addr = smem_u32(sB + bs * C::kStageB);
+                            int roff = r * hg.wp + s;
+                            if (hg.dbg & 1) roff &= ~7;  // timing probe only (wrong results)
+                            const uint32_t a_addr = h_addr + static_cast<uint32_t>(roff) * 128u;
+                            const uint32_t b_addr = smem_u32(sB + (hg.resident ? kb : bs) * C::kStageB);
 #pragma unroll
                             for (int kk = 0; kk < kBK / 8; ++kk) {
                                 const uint64_t ad = umma_desc<kLayoutSW128>(a_addr + kk * 32, 16, 1024);
@@ -187,11 +215,13 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                                 if (CG == 2) mma_tf32_pair(d_tmem, ad, bd, idesc, accum);
                                 else mma_tf32(d_tmem, ad, bd, idesc, accum);
                             }
-                            if (CG == 2) mma_commit_pair(&bempty[bs]);
-                            else mma_commit(&bempty[bs]);
+                            if (!hg.resident) {
+                                if (CG == 2) mma_commit_pair(&bempty[bs]);
+                                else mma_commit(&bempty[bs]);
+                            }
                         }
                         __syncwarp();
-                        if (++bs == C::kBStages) {
+                        if (!hg.resident && ++bs == kBStages) {
                             bs = 0;
                             bph ^= 1;
                         }
@@ -241,7 +271,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 uint32_t rr[32];
                 tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, rr);
                 tmem_ld_wait();
-                if (m >= 0) {
+                if (m >= 0 && !(hg.dbg & 2)) {
                     float v[32];
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(rr[i]);
@@ -269,7 +299,6 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
 
 template <bool B_MN, int BN, int CG>
 cudaError_t launch_halo_t(const TcGemmPlan& p, cudaStream_t s) {
-    using C = HaloCfg<BN, CG>;
     int dev = 0;
     cudaGetDevice(&dev);
     if ((g_halo_attr.load() & (1u << (dev & 31))) == 0) {
@@ -279,7 +308,7 @@ cudaError_t launch_halo_t(const TcGemmPlan& p, cudaStream_t s) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.grid);
     cfg.blockDim = dim3(kHaloThreads);
-    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.dynamicSmemBytes = p.hg.smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -315,12 +344,12 @@ cudaError_t halo_conv_init_device() {
         if (e == cudaSuccess) e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     };
 #define PPB_HSET(BM)                                                     \
-    set(halo_conv_kernel<BM, 64, 1>, HaloCfg<64, 1>::kSmem);             \
-    set(halo_conv_kernel<BM, 128, 1>, HaloCfg<128, 1>::kSmem);           \
-    set(halo_conv_kernel<BM, 256, 1>, HaloCfg<256, 1>::kSmem);           \
-    set(halo_conv_kernel<BM, 64, 2>, HaloCfg<64, 2>::kSmem);             \
-    set(halo_conv_kernel<BM, 128, 2>, HaloCfg<128, 2>::kSmem);           \
-    set(halo_conv_kernel<BM, 256, 2>, HaloCfg<256, 2>::kSmem);
+    set(halo_conv_kernel<BM, 64, 1>, kHaloSmemMax);             \
+    set(halo_conv_kernel<BM, 128, 1>, kHaloSmemMax);           \
+    set(halo_conv_kernel<BM, 256, 1>, kHaloSmemMax);           \
+    set(halo_conv_kernel<BM, 64, 2>, kHaloSmemMax);             \
+    set(halo_conv_kernel<BM, 128, 2>, kHaloSmemMax);           \
+    set(halo_conv_kernel<BM, 256, 2>, kHaloSmemMax);
     PPB_HSET(false)
     PPB_HSET(true)
 #undef PPB_HSET
@@ -373,6 +402,7 @@ bool halo_conv_prepare(const GemmDesc& d, TcGemmPlan* out, int force, char* err,
     hg.cblocks = d.a.geom.cblocks;
     hg.rows = kBM + 2 * (hg.wp + 1);
     hg.Mp = static_cast<long long>(d.a.imgs) * hg.hp * hg.wp;
+    if (const char* e = getenv("PPB_HALO_DBG")) hg.dbg = atoi(e);  // timing probes only
     int bn, cg;
     if (force >= 2000) {
         cg = 2;
@@ -392,6 +422,35 @@ bool halo_conv_prepare(const GemmDesc& d, TcGemmPlan* out, int force, char* err,
     }
     p.bn = bn;
     p.cg = cg;
+    // shared-memory plan: halo ring + either the whole B column slice resident
+    // (one column tile, fits next to >= 2 halo stages) or a streaming B ring
+    {
+        const int stage_b = bn / cg * kBK * 4;
+        const int nkb = 9 * hg.cblocks;
+        hg.hstage_bytes = (hg.rows * 128 + 1023) / 1024 * 1024;
+        const int avail = kHaloSmemMax - kHaloReserve;
+        const bool one_col = d.N <= bn;
+        if (one_col && nkb * stage_b + 2 * hg.hstage_bytes <= avail && !getenv("PPB_HALO_STREAM_B")) {
+            hg.resident = 1;
+            hg.bstages = nkb;
+            hg.hstages = (avail - nkb * stage_b) / hg.hstage_bytes;
+            if (hg.hstages > 4) hg.hstages = 4;
+        } else {
+            hg.resident = 0;
+            hg.hstages = 3;
+            hg.bstages = (200 * 1024 - 3 * hg.hstage_bytes) / stage_b;
+            if (hg.bstages > 12) hg.bstages = 12;
+            if (hg.bstages < 2) {
+                snprintf(err, errlen, "halo conv: shared memory too small for tile width %d", bn);
+                return false;
+            }
+        }
+        hg.smem = 1024 + hg.hstages * hg.hstage_bytes + hg.bstages * stage_b + 1024;
+        if (2 * (hg.hstages + hg.bstages + 2) * 8 + 8 > 1024) {
+            snprintf(err, errlen, "halo conv: too many pipeline barriers");
+            return false;
+        }
+    }
     const int tm = kBM * cg;
     const long long tiles = ((hg.Mp + tm - 1) / tm) * ((d.N + bn - 1) / bn);
     const int units = sm_count() / cg;

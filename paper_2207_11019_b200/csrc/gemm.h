@@ -127,6 +127,12 @@ struct HaloGeom {
     int cblocks = 1;      // 32-channel blocks of A
     int rows = 0;         // halo rows staged per CTA: 128 + 2 * (wp + 1)
     long long Mp = 0;     // imgs * hp * wp
+    // shared-memory plan (set by halo_conv_prepare)
+    int hstages = 3, hstage_bytes = 0;  // halo ring
+    int bstages = 0;                    // B ring slots (resident: one per K block)
+    int resident = 0;                   // B column slice loaded once per CTA
+    int smem = 0;                       // dynamic shared memory bytes
+    int dbg = 0;  // timing probes (wrong results): 1 align taps, 2 no epilogue stores, 4 no halo waits
 };
 
 struct GemmDesc {

@@ -207,15 +207,26 @@ __global__ void colsum_partial_kernel(const float* __restrict__ delta, long long
     partial[static_cast<long long>(chunk) * u + c] = s;
 }
 
-// one block per column: fixed-shape tree over the chunk partials
-__global__ void __launch_bounds__(kRowThreads) bias_update_kernel(const float* __restrict__ partial, int u,
-                                                                  int chunks, float* __restrict__ bias,
-                                                                  const double* __restrict__ alpha, float inv_b) {
-    const int c = blockIdx.x;
+// bias[c] -= alpha * (sum_k partial[k][c]) * inv_b, one block per 32 columns:
+// lane = column (coalesced rows of `partial`), threadIdx.y strides the chunks
+// in ascending order, then a fixed-order sum over threadIdx.y (deterministic).
+__global__ void __launch_bounds__(1024) bias_update_cols_kernel(const float* __restrict__ partial, int u, int chunks,
+                                                                float* __restrict__ bias,
+                                                                const double* __restrict__ alpha, float inv_b) {
+    __shared__ float sh[32][33];
+    const int c = blockIdx.x * 32 + threadIdx.x;
     float s = 0.f;
-    for (int k = threadIdx.x; k < chunks; k += kRowThreads) s += partial[static_cast<long long>(k) * u + c];
-    s = block_sum<kRowThreads>(s);
-    if (threadIdx.x == 0) bias[c] -= static_cast<float>(*alpha) * (s * inv_b);
+    if (c < u) {
+#pragma unroll 4
+        for (int k = threadIdx.y; k < chunks; k += 32) s += __ldg(partial + static_cast<long long>(k) * u + c);
+    }
+    sh[threadIdx.y][threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.y == 0 && c < u) {
+        float t = 0.f;
+        for (int j = 0; j < 32; ++j) t += sh[j][threadIdx.x];
+        bias[c] -= static_cast<float>(*alpha) * (t * inv_b);
+    }
 }
 
 template <class T>
@@ -588,7 +599,7 @@ cudaError_t launch_bias_update(const float* delta, long long ld, int rows, int u
     const int tpb = u >= 128 ? 128 : (u + 31) / 32 * 32;
     dim3 g1((u + tpb - 1) / tpb, chunks);
     colsum_partial_kernel<<<g1, tpb, 0, s>>>(delta, ld, rows, u, chunks, partial);
-    bias_update_kernel<<<u, kRowThreads, 0, s>>>(partial, u, chunks, bias, alpha, inv_b);
+    bias_update_cols_kernel<<<(u + 31) / 32, dim3(32, 32), 0, s>>>(partial, u, chunks, bias, alpha, inv_b);
     return cudaGetLastError();
 }
 
@@ -652,7 +663,7 @@ cudaError_t launch_pool_fwd(const float* U, long long ldu, int imgs, int Ho, int
     return cudaGetLastError();
 }
 
-int conv_merge_blocks() { return 148 * 16; }
+int conv_merge_blocks() { return 148 * 4; }
 
 cudaError_t launch_conv_merge(const ConvMerge& m, float* db_partial, cudaStream_t s) {
     const long long n = static_cast<long long>(m.imgs) * m.Ho * m.Wo * m.uch;
@@ -684,7 +695,7 @@ cudaError_t launch_conv_merge(const ConvMerge& m, float* db_partial, cudaStream_
 cudaError_t launch_bias_from_partials(const float* partial, int chunks, int u, float* bias, const double* alpha,
                                       float inv_b, cudaStream_t s) {
     if (u <= 0) return cudaSuccess;
-    bias_update_kernel<<<u, kRowThreads, 0, s>>>(partial, u, chunks, bias, alpha, inv_b);
+    bias_update_cols_kernel<<<(u + 31) / 32, dim3(32, 32), 0, s>>>(partial, u, chunks, bias, alpha, inv_b);
     return cudaGetLastError();
 }
 

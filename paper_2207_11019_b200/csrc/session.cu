@@ -500,7 +500,7 @@ void Session::build_ops() {
         Gpu* g = &gpu_of(gpu);
         WsAlloc ws = [g](size_t n) { return static_cast<float*>(g->alloc(sizeof(float) * n)); };
         if (!tc_gemm_prepare(d, &p, 0, err, sizeof(err), ws)) throw std::runtime_error(std::string("GEMM setup: ") + err);
-        cur_info_ = p.bn | (p.cg << 10) | (p.sk.splits << 12);
+        cur_info_ = p.bn | (p.cg << 10) | (p.sk.splits << 12) | (p.halo << 24);
     };
     auto module_of_layer = [&](int l) -> const SubModule& {
         for (const SubModule& sm : plan_.subs)
