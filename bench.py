@@ -337,7 +337,7 @@ def run_ours(args, rank, world, dist):
             traffic = json.load(f).get(args.workload)
     roofline = {"bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
                 "frac": achieved / tf32_peak, "traffic": traffic,
-                "kernel": "ppb::tc_gemm_kernel (tcgen05.mma kind::tf32, TMA SW128, fused epilogues)",
+                "kernel": "ppb::tc_gemm_kernel + ppb::halo_conv_kernel (all shard GEMMs: tcgen05.mma kind::tf32, TMA SW128, fused epilogues)",
                 "flops_per_launch": g_flops / max(g_launch, 1), "avg_launch_ms": g_ms / max(g_launch, 1),
                 "launches_per_step": g_launch, "share_of_step": g_ms / step_ms_eager if step_ms_eager else None,
                 "peak_source": f"{peak_src}: bf16_tflops (burst) / 2 (TF32 = half the bf16 tensor rate)",

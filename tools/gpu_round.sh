@@ -16,6 +16,6 @@ for W in vgg16 wide_mlp mlp784; do
 done
 timeout 300 python tools/profile_ops.py vgg16 > gpurun_out/${TAG}_ops_vgg16.jsonl 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_ncu_launch_stdout.txt 2>&1; echo "ncu list rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 5 -c 4 -o gpurun_out/${TAG}_gemm python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_ncu_full_stdout.txt 2>&1; echo "ncu full rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tc_gemm|halo_conv" -s 0 -c 6 -o gpurun_out/${TAG}_gemm python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_ncu_full_stdout.txt 2>&1; echo "ncu full rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 12 -c 2 -o gpurun_out/${TAG}_gemm_wide python bench.py --workload wide_mlp --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_ncu_full_wide_stdout.txt 2>&1; echo "ncu full wide rc=$?"
 ls gpurun_out | grep ${TAG}
