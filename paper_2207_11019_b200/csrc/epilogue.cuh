@@ -136,6 +136,46 @@ __device__ __forceinline__ void epilogue32(const EpiParams& p, int m, int n0, fl
             }
             break;
         }
+        case EPI_MERGE: {
+            const int hw = p.mg_hg * p.mg_wg;
+            const int img = m / hw, rem = m - img * hw, y = rem / p.mg_wg, x = rem - y * p.mg_wg;
+            uint32_t code[8] = {};
+            if (p.mg_pool == 2) {
+                const unsigned char* ap = p.mg_argmax + static_cast<long long>(m) * p.mg_uch + n0;
+                if ((p.mg_uch & 3) == 0 && nvalid == 32) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) code[i] = __ldg(reinterpret_cast<const uint32_t*>(ap) + i);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        code[i] = 0;
+#pragma unroll
+                        for (int b = 0; b < 4; ++b)
+                            if (4 * i + b < nvalid) code[i] |= static_cast<uint32_t>(__ldg(ap + 4 * i + b)) << (8 * b);
+                    }
+                }
+            }
+            const int npos = p.mg_pool * p.mg_pool;
+            for (int q = 0; q < npos; ++q) {
+                const int h = y * p.mg_pool + (q >> 1), w = x * p.mg_pool + (q & 1);
+                float v[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const bool hit = p.mg_pool == 1 || ((code[i >> 2] >> (8 * (i & 3))) & 0xffu) == static_cast<uint32_t>(q);
+                    v[i] = hit ? acc[i] : 0.f;
+                }
+                if (p.mg_mask != nullptr) {
+                    float mk[32];
+                    const long long mrow = (static_cast<long long>(img) * p.mg_mhp + h + p.mg_mpad) * p.mg_mwp + w + p.mg_mpad;
+                    load_row32(p.mg_mask + mrow * p.mg_mld + p.mg_mcol0, n0, nvalid, mk);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = mk[i] > 0.f ? v[i] : 0.f;
+                }
+                const long long drow = (static_cast<long long>(img) * p.mg_dhp + h + p.mg_dpad) * p.mg_dwp + w + p.mg_dpad;
+                store_row32(p.mg_d + drow * p.mg_dld, n0, nvalid, v);
+            }
+            break;
+        }
         default:
             break;
     }
@@ -181,6 +221,23 @@ __device__ __forceinline__ void epilogue1(const EpiParams& p, int m, int n, floa
                 if (p.seg_mask[s] != nullptr && !(p.seg_mask[s][static_cast<long long>(m) * p.seg_mask_ld[s] + n] > 0.f))
                     o = 0.f;
                 p.seg_dst[s][static_cast<long long>(m) * p.seg_ld[s] + n - p.seg_lo[s]] = o;
+            }
+            break;
+        }
+        case EPI_MERGE: {
+            const int hw = p.mg_hg * p.mg_wg;
+            const int img = m / hw, rem = m - img * hw, y = rem / p.mg_wg, x = rem - y * p.mg_wg;
+            const int code = p.mg_pool == 2 ? p.mg_argmax[static_cast<long long>(m) * p.mg_uch + n] : 0;
+            const int npos = p.mg_pool * p.mg_pool;
+            for (int q = 0; q < npos; ++q) {
+                const int h = y * p.mg_pool + (q >> 1), w = x * p.mg_pool + (q & 1);
+                float o = (p.mg_pool == 1 || code == q) ? v : 0.f;
+                if (p.mg_mask != nullptr) {
+                    const long long mrow = (static_cast<long long>(img) * p.mg_mhp + h + p.mg_mpad) * p.mg_mwp + w + p.mg_mpad;
+                    if (!(p.mg_mask[mrow * p.mg_mld + p.mg_mcol0 + n] > 0.f)) o = 0.f;
+                }
+                const long long drow = (static_cast<long long>(img) * p.mg_dhp + h + p.mg_dpad) * p.mg_dwp + w + p.mg_dpad;
+                p.mg_d[drow * p.mg_dld + n] = o;
             }
             break;
         }

@@ -27,6 +27,7 @@ enum EpiMode : int {
     EPI_MASK = 1,   // out = acc * (mask[m][mcol0+n] > 0) stored to dst[0]
     EPI_SGD = 2,    // W[m][n] -= alpha * (acc * inv_b); non-finite acc -> *flag = 1
     EPI_SLOTS = 3,  // column segment s of acc stored to seg_dst[s] (backward scatter)
+    EPI_MERGE = 4,  // single-contributor conv backward merge (pool argmax + ReLU mask -> padded error)
 };
 
 constexpr int kMaxDst = 8;
@@ -66,6 +67,21 @@ struct EpiParams {
     long long seg_ld[kMaxDst] = {};
     const float* seg_mask[kMaxDst] = {};
     long long seg_mask_ld[kMaxDst] = {};
+    // EPI_MERGE (kernels.h ConvMerge with one contributor, fused): row m = pixel
+    // (img, y, x) of the pooled grid mg_hg x mg_wg, column n = channel.  Each
+    // pre-pool position (y*pool + dy, x*pool + dx) whose argmax code (dy*2 + dx)
+    // matches receives acc (others 0), masked by mask > 0, stored into the
+    // padded error signal d.  Positions outside the pooled grid are never
+    // written (they stay zero).
+    int mg_pool = 1, mg_hg = 1, mg_wg = 1;
+    const unsigned char* mg_argmax = nullptr;  // [m][mg_uch]
+    int mg_uch = 0;
+    const float* mg_mask = nullptr;            // [img][mhp][mwp][mld] + mcol0 (ReLU of the layer below)
+    long long mg_mld = 0;
+    int mg_mhp = 1, mg_mwp = 1, mg_mpad = 0, mg_mcol0 = 0;
+    float* mg_d = nullptr;                     // [img][dhp][dwp][dld]
+    long long mg_dld = 0;
+    int mg_dhp = 1, mg_dwp = 1, mg_dpad = 0;
 };
 
 // Host-side description of one operand: a row-major fp32 matrix of `rows` x

@@ -71,6 +71,7 @@ struct Session::WLayer {
     float* U = nullptr;                  // conv: pre-pool output of the shard [b*Ho*Wo x ldu]
     long long ldu = 0;
     unsigned char* argmax = nullptr;     // conv with pool: [b*Hq*Wq x u]
+    bool merge_fused = false;            // conv: delta written by the dgrad epilogue (EPI_MERGE)
     std::vector<std::vector<int>> delta_ready;  // [j] -> op ids that produce delta rows of micro-batch j
     std::vector<int> fwd_op, dgrad_op;   // [j]
     TcGemmPlan p_wgrad;
@@ -113,6 +114,7 @@ float* Session::q_buf(int ordinal) { return gpu_of(ordinal).q; }
 Session::Session(const std::vector<int>& device_map, const NetDesc& net, const double* W,
                  const double* b, const Plan& plan, const SessionConfig& cfg)
     : net_(net), plan_(plan), cfg_(cfg), device_map_(device_map) {
+    if (const char* e = getenv("PPB_NO_FUSED_MERGE")) fuse_merge_ = !(*e != '\0' && *e != '0');
     const int L = net_.L();
     // ---- entry validation, in the reference's order (train_partitioned.cpp:124-141)
     if (L < 1) throw std::invalid_argument("net must have at least one layer");
@@ -406,7 +408,8 @@ void Session::alloc_buffers() {
             }
             wl.delta = static_cast<float*>(g.alloc(sizeof(float) * b * wl.delta_img));
             // bias-gradient partials: dense colsum chunks, or one row per (micro-batch, merge block) for conv
-            const long long prow = li.kind == 1 ? static_cast<long long>(cfg_.m) * conv_merge_blocks() : kColsumChunks;
+            const long long prow = li.kind == 1 ? std::max<long long>(static_cast<long long>(cfg_.m) * conv_merge_blocks(), kColsumChunks)
+                                                : kColsumChunks;
             wl.partial = static_cast<float*>(g.alloc(sizeof(float) * prow * wl.u));
             // upload the shard rows [lo, hi) (train_partitioned.cpp:168-169), fp64 -> fp32;
             // conv rows [k][k][C_in] go to the GEMM layout [k*k][ck] (zero-padded channels)
@@ -730,6 +733,63 @@ void Session::build_ops() {
                 // destination sums them, routes through the pool argmax and
                 // masks by its ReLU into its padded error signal.
                 const int hw = lb.Hq() * lb.Wq();
+                if (li.kind == 1 && contrib.size() == 1 && dests.size() == 1 && fuse_merge_) {
+                    // one contributor, one destination: the merge (pool routing,
+                    // ReLU mask, padded store) runs in the dgrad epilogue
+                    Worker& w = *workers_[contrib[0]];
+                    WLayer& wl = w.at(l);
+                    Worker& dw = *workers_[dests[0]];
+                    WLayer& dl = dw.at(l - 1);
+                    GemmDesc& d = wl.d_dgrad[j];
+                    ConvShape cs;
+                    cs.N = rows;
+                    cs.H = li.H;
+                    cs.W = li.W;
+                    cs.C = li.in_units;
+                    cs.ksz = li.ksz;
+                    cs.pad = li.pad;
+                    cs.u = wl.u;
+                    d = conv_dgrad_desc(cs, wl.delta + off * wl.delta_img, wl.ldd, wl.W);
+                    d.epi = EpiParams{};
+                    d.epi.mode = EPI_MERGE;
+                    d.epi.mg_pool = lb.pool;
+                    d.epi.mg_hg = lb.Hq();
+                    d.epi.mg_wg = lb.Wq();
+                    d.epi.mg_argmax = dl.argmax ? dl.argmax + off * hw * dl.u : nullptr;
+                    d.epi.mg_uch = dl.u;
+                    if (relu_below) {
+                        if (dl.U != nullptr) {
+                            d.epi.mg_mask = dl.U + off * lb.Ho() * lb.Wo() * dl.ldu;
+                            d.epi.mg_mld = dl.ldu;
+                            d.epi.mg_mhp = lb.Ho();
+                            d.epi.mg_mwp = lb.Wo();
+                        } else {
+                            const ActLayout& a = lay_[l - 1];
+                            d.epi.mg_mask = act_buf(dw.gpu, l - 1) + off * img_elems(l - 1);
+                            d.epi.mg_mld = a.ld;
+                            d.epi.mg_mhp = a.hp;
+                            d.epi.mg_mwp = a.wp;
+                            d.epi.mg_mpad = a.pad;
+                            d.epi.mg_mcol0 = dl.lo;
+                        }
+                    }
+                    const int q = lb.ksz - 1 - lb.pad;
+                    d.epi.mg_d = dl.delta + off * dl.delta_img;
+                    d.epi.mg_dld = dl.ldd;
+                    d.epi.mg_dhp = lb.Ho() + 2 * q;
+                    d.epi.mg_dwp = lb.Wo() + 2 * q;
+                    d.epi.mg_dpad = q;
+                    prepare(d, wl.p_dgrad[j], w.gpu);
+                    const double fl = 2.0 * rows * li.H * li.W * li.in_units * li.ksz * li.ksz * wl.u;
+                    const int op = add_op(w.gpu, w.sb, gemm_launch(&wl.p_dgrad[j], &wl.d_dgrad[j], w.sb),
+                                          wl.delta_ready[j], 1, OP_DGRAD_GEMM, fl);
+                    wl.dgrad_op[j] = op;
+                    w.last_bwd[j] = std::max(w.last_bwd[j], op);
+                    dl.merge_fused = true;
+                    dl.delta_ready[j] = {op};
+                    dw.last_bwd[j] = std::max(dw.last_bwd[j], op);
+                    continue;
+                }
                 for (size_t k = 0; k < contrib.size(); ++k) {
                     Worker& w = *workers_[contrib[k]];
                     WLayer& wl = w.at(l);
@@ -964,7 +1024,7 @@ void Session::build_ops() {
             float* partial = wl.partial;
             float* bias = wl.bias;
             const double* alpha = &g.st->alpha;
-            const bool from_merge = li.kind == 1;  // conv: db partials came with the merges
+            const bool from_merge = li.kind == 1 && !wl.merge_fused;  // conv: db partials came with the merges
             const int chunks = cfg_.m * conv_merge_blocks();
             const int bop = add_op(w.gpu, s, [=]() {
                 if (from_merge) return launch_bias_from_partials(partial, chunks, u, bias, alpha, inv_b, s);

@@ -152,6 +152,7 @@ class Session {
     std::vector<Op> ops_;
     int begin_op_ = -1;
     int end_op_ = -1;
+    bool fuse_merge_ = true;  // single-contributor conv merges in the dgrad epilogue (PPB_NO_FUSED_MERGE=1 disables)
     int main_gpu_ = 0;  // ordinal holding the loss / history (rank 0 of the last module)
     cudaGraphExec_t graph_exec_ = nullptr;
     cudaGraph_t graph_ = nullptr;

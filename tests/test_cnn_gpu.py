@@ -98,3 +98,40 @@ def test_vgg16_one_step_small_batch():
     assert abs(r.loss_history[0] - lh[0]) <= TOL * max(1.0, lh[0])
     assert net_distance(Wg, bg, Wr, br) <= TOL
     assert rel_norm(Wg - W0, Wr - W0) <= 5e-2
+
+
+def test_vgg16_one_step_n1_halo_fused_merge():
+    """n = 1: the 32x32 / 16x16 convs run on the halo kernel and every backward
+    merge is fused into the dgrad epilogue (EPI_MERGE)."""
+    net = configs.vgg16_cifar(seed=11)
+    X, y = data(net, 6, 10, seed=6)
+    cfg = TrainConfig(alpha0=0.01, decay=0.0, iterations=2)
+    plan = api.build_plan(net, 1, 1)
+    r = api.train_partitioned(net, Batch(X, y), cfg, plan, 2, UpdateMode.async_per_module,
+                              PartitionedTrainOptions(multiclass_accuracy=True), device_map=[0])
+    W0, _ = net.pack()
+    Wr, br, lh, _ = cnn_oracle.train(net, X, y, 0.01, 0.0, 2, 2)
+    Wg, bg = r.net.pack()
+    for got, ref in zip(r.loss_history, lh):
+        assert abs(got - ref) <= TOL * max(1.0, abs(ref)), (got, ref)
+    assert net_distance(Wg, bg, Wr, br) <= TOL
+    assert rel_norm(Wg - W0, Wr - W0) <= 5e-2
+
+
+@pytest.mark.parametrize("name", ["pool_pool", "nopool_pool", "deep"])
+def test_fused_merge_matches_unfused(name, monkeypatch):
+    """The fused single-contributor merge produces the same error signals as
+    the slot + conv_merge path (only the bias-gradient summation tree differs)."""
+    net = NETS[name]()
+    X, y = data(net, 12, 10, seed=8)
+    cfg = TrainConfig(alpha0=0.05, decay=0.01, iterations=2)
+    plan = api.build_plan(net, 1, 1)
+    o = PartitionedTrainOptions(multiclass_accuracy=True)
+    a = api.train_partitioned(net, Batch(X, y), cfg, plan, 2, UpdateMode.sync_barrier, o, device_map=[0])
+    monkeypatch.setenv("PPB_NO_FUSED_MERGE", "1")
+    b = api.train_partitioned(net, Batch(X, y), cfg, plan, 2, UpdateMode.sync_barrier, o, device_map=[0])
+    Wa, ba = a.net.pack()
+    Wb, bb = b.net.pack()
+    assert net_distance(Wa, ba, Wb, bb) <= 1e-5
+    for p, q in zip(a.loss_history, b.loss_history):
+        assert abs(p - q) <= 1e-5 * max(1.0, abs(q))
