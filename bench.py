@@ -83,55 +83,64 @@ def measured_peaks():
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """Samples SM clocks and clock-event (throttle) reasons during the timed
+    region through NVML every ~2 ms (the timed region of a short run is tens
+    of ms, far below nvidia-smi's sampling period)."""
 
-    def __init__(self, gpus):
+    def __init__(self, gpus, period_s=0.002):
         self.gpus = gpus
-        self.rows = []
-        self.proc = None
+        self.period = period_s
+        self.rows = []  # (sm_mhz, max_mhz, reason bits)
+        self.stop = threading.Event()
+        self.t = None
+
+    def _handles(self, nv):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [v.strip() for v in vis.split(",") if v.strip()] if vis else []
+        hs = []
+        for g in self.gpus:
+            idx = int(ids[g]) if g < len(ids) and ids[g].isdigit() else g
+            hs.append(nv.nvmlDeviceGetHandleByIndex(idx))
+        return hs
+
+    def _loop(self, nv, hs):
+        while not self.stop.is_set():
+            for h in hs:
+                try:
+                    self.rows.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                      nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM),
+                                      nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)))
+                except Exception:  # noqa: BLE001
+                    pass
+            self.stop.wait(self.period)
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-lms", "200", "-i", ",".join(str(g) for g in self.gpus)],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+
+            nv.nvmlInit()
+            hs = self._handles(nv)
+            self.t = threading.Thread(target=self._loop, args=(nv, hs), daemon=True)
             self.t.start()
-        except (OSError, ValueError):
-            self.proc = None
+        except Exception:  # noqa: BLE001
+            self.t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
-
     def __exit__(self, *a):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self.stop.set()
+        if self.t is not None:
             self.t.join(timeout=2)
 
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            if len(r) < 9:
-                continue
-            for name, v in zip(names, r[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(name)
-        loaded = sorted(x for x in sm if x > 300) or sorted(sm)
-        return {"sm_mhz": loaded[len(loaded) // 2] if loaded else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons), "samples": len(self.rows)}
+        bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+        reasons = sorted({k for _, _, r in self.rows for k, b in bits.items() if r & b})
+        sm = sorted(r[0] for r in self.rows)
+        loaded = [x for x in sm if x > 300] or sm
+        return {"sm_mhz": loaded[len(loaded) // 2], "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": reasons, "samples": len(self.rows), "source": "NVML, 2 ms period, timed region"}
 
 
 def dist_setup():

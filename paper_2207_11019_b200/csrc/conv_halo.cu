@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     uint64_t* tfull = bempty + kBStages;  // [2]
     uint64_t* tempty = tfull + 2;            // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    float* db_s = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(hfull) + 1024);  // [4][ldb] (EPI_MERGE db)
 
     const int warp = threadIdx.x / 32;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
@@ -249,6 +250,11 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         const int lane = threadIdx.x & 31;
         const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
         const int hpwp = hg.hp * hg.wp;
+        const bool db = epi.db_partial != nullptr;
+        const int ldb = (N + 31) & ~31;
+        float* db_row = db_s + q * ldb;
+        if (db)
+            for (int i = lane; i < ldb; i += 32) db_row[i] = 0.f;
         int local = 0;
         for (int tile = unit; tile < num_tiles; tile += units, ++local) {
             const long long p0 = static_cast<long long>(tile % num_m) * TM + static_cast<long long>(rank) * kBM;
@@ -271,12 +277,11 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 uint32_t rr[32];
                 tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, rr);
                 tmem_ld_wait();
-                if (m >= 0 && !(hg.dbg & 2)) {
-                    float v[32];
+                float v[32];
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(rr[i]);
-                    epilogue32(epi, m, n0 + c * 32, v);
-                }
+                for (int i = 0; i < 32; ++i) v[i] = m >= 0 ? __uint_as_float(rr[i]) : 0.f;
+                if (m >= 0 && !(hg.dbg & 2)) epilogue32(epi, m, n0 + c * 32, v);
+                if (db && n0 + c * 32 < N) db_accumulate(db_row, n0 + c * 32, N, v, lane);
             }
             tc_fence_before();
             __syncwarp();
@@ -284,6 +289,11 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 if (CG == 2) mbar_arrive_cluster(tempty_leader + acc * sizeof(uint64_t));
                 else mbar_arrive(&tempty[acc]);
             }
+        }
+        if (db) {
+            __syncwarp();
+            float* out = epi.db_partial + (static_cast<long long>(blockIdx.x) * 4 + q) * N;
+            for (int i = lane; i < N; i += 32) out[i] = db_row[i];
         }
     }
 
@@ -446,6 +456,16 @@ bool halo_conv_prepare(const GemmDesc& d, TcGemmPlan* out, int force, char* err,
             }
         }
         hg.smem = 1024 + hg.hstages * hg.hstage_bytes + hg.bstages * stage_b + 1024;
+        if (p.epi.db_partial != nullptr) {  // EPI_MERGE bias partials after the barrier block
+            const int need = 4 * ((d.N + 31) / 32 * 32) * 4;
+            while (hg.smem + need > kHaloSmemMax && ((hg.resident && hg.hstages > 2) || (!hg.resident && hg.bstages > 2))) {
+                if (hg.resident) --hg.hstages;
+                else --hg.bstages;
+                hg.smem = 1024 + hg.hstages * hg.hstage_bytes + hg.bstages * stage_b + 1024;
+            }
+            if (hg.smem + need <= kHaloSmemMax) hg.smem += need;
+            else p.epi.db_partial = nullptr;
+        }
         if (2 * (hg.hstages + hg.bstages + 2) * 8 + 8 > 1024) {
             snprintf(err, errlen, "halo conv: too many pipeline barriers");
             return false;

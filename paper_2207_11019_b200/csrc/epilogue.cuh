@@ -155,6 +155,15 @@ __device__ __forceinline__ void epilogue32(const EpiParams& p, int m, int n0, fl
                     }
                 }
             }
+            // ReLU mask: the pooled activation (y, x) is the window max = U at the
+            // argmax position, so one row of it masks every routed value
+            if (p.mg_mask != nullptr) {
+                float mk[32];
+                const long long mrow = (static_cast<long long>(img) * p.mg_mhp + y + p.mg_mpad) * p.mg_mwp + x + p.mg_mpad;
+                load_row32(p.mg_mask + mrow * p.mg_mld + p.mg_mcol0, n0, nvalid, mk);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) acc[i] = mk[i] > 0.f ? acc[i] : 0.f;
+            }
             const int npos = p.mg_pool * p.mg_pool;
             for (int q = 0; q < npos; ++q) {
                 const int h = y * p.mg_pool + (q >> 1), w = x * p.mg_pool + (q & 1);
@@ -164,13 +173,6 @@ __device__ __forceinline__ void epilogue32(const EpiParams& p, int m, int n0, fl
                     const bool hit = p.mg_pool == 1 || ((code[i >> 2] >> (8 * (i & 3))) & 0xffu) == static_cast<uint32_t>(q);
                     v[i] = hit ? acc[i] : 0.f;
                 }
-                if (p.mg_mask != nullptr) {
-                    float mk[32];
-                    const long long mrow = (static_cast<long long>(img) * p.mg_mhp + h + p.mg_mpad) * p.mg_mwp + w + p.mg_mpad;
-                    load_row32(p.mg_mask + mrow * p.mg_mld + p.mg_mcol0, n0, nvalid, mk);
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) v[i] = mk[i] > 0.f ? v[i] : 0.f;
-                }
                 const long long drow = (static_cast<long long>(img) * p.mg_dhp + h + p.mg_dpad) * p.mg_dwp + w + p.mg_dpad;
                 store_row32(p.mg_d + drow * p.mg_dld, n0, nvalid, v);
             }
@@ -179,6 +181,23 @@ __device__ __forceinline__ void epilogue32(const EpiParams& p, int m, int n0, fl
         default:
             break;
     }
+}
+
+// Column sums of a warp's 32 x 32 block (row = lane): butterfly transpose-
+// reduce, lane L ends with the sum of column L over the 32 rows (fixed order,
+// deterministic), added into db_row[n0 + L] (shared memory, this warp only).
+__device__ __forceinline__ void db_accumulate(float* db_row, int n0, int N, float (&v)[32], int lane) {
+#pragma unroll
+    for (int k = 16; k >= 1; k >>= 1) {
+        const bool upper = (lane & k) != 0;
+#pragma unroll
+        for (int i = 0; i < k; ++i) {
+            const float send = upper ? v[i] : v[i + k];
+            const float keep = upper ? v[i + k] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, k);
+        }
+    }
+    if (n0 + lane < N) db_row[n0 + lane] += v[0];
 }
 
 // Row offset (elements) of output row m in the EPI_STORE destination.
@@ -228,16 +247,15 @@ __device__ __forceinline__ void epilogue1(const EpiParams& p, int m, int n, floa
             const int hw = p.mg_hg * p.mg_wg;
             const int img = m / hw, rem = m - img * hw, y = rem / p.mg_wg, x = rem - y * p.mg_wg;
             const int code = p.mg_pool == 2 ? p.mg_argmax[static_cast<long long>(m) * p.mg_uch + n] : 0;
+            if (p.mg_mask != nullptr) {
+                const long long mrow = (static_cast<long long>(img) * p.mg_mhp + y + p.mg_mpad) * p.mg_mwp + x + p.mg_mpad;
+                if (!(p.mg_mask[mrow * p.mg_mld + p.mg_mcol0 + n] > 0.f)) v = 0.f;
+            }
             const int npos = p.mg_pool * p.mg_pool;
             for (int q = 0; q < npos; ++q) {
                 const int h = y * p.mg_pool + (q >> 1), w = x * p.mg_pool + (q & 1);
-                float o = (p.mg_pool == 1 || code == q) ? v : 0.f;
-                if (p.mg_mask != nullptr) {
-                    const long long mrow = (static_cast<long long>(img) * p.mg_mhp + h + p.mg_mpad) * p.mg_mwp + w + p.mg_mpad;
-                    if (!(p.mg_mask[mrow * p.mg_mld + p.mg_mcol0 + n] > 0.f)) o = 0.f;
-                }
                 const long long drow = (static_cast<long long>(img) * p.mg_dhp + h + p.mg_dpad) * p.mg_dwp + w + p.mg_dpad;
-                p.mg_d[drow * p.mg_dld + n] = o;
+                p.mg_d[drow * p.mg_dld + n] = (p.mg_pool == 1 || code == q) ? v : 0.f;
             }
             break;
         }

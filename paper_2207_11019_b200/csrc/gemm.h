@@ -70,18 +70,26 @@ struct EpiParams {
     // EPI_MERGE (kernels.h ConvMerge with one contributor, fused): row m = pixel
     // (img, y, x) of the pooled grid mg_hg x mg_wg, column n = channel.  Each
     // pre-pool position (y*pool + dy, x*pool + dx) whose argmax code (dy*2 + dx)
-    // matches receives acc (others 0), masked by mask > 0, stored into the
-    // padded error signal d.  Positions outside the pooled grid are never
-    // written (they stay zero).
+    // matches receives acc (others 0), stored into the padded error signal d.
+    // The ReLU mask is read at the POOLED pixel (y, x) of the layer's output
+    // activation: the pooled value is the window max, i.e. U at the argmax, so
+    // mask(U[argmax] > 0) == mask(pooled > 0).  Positions outside the pooled
+    // grid are never written (they stay zero).
     int mg_pool = 1, mg_hg = 1, mg_wg = 1;
     const unsigned char* mg_argmax = nullptr;  // [m][mg_uch]
     int mg_uch = 0;
-    const float* mg_mask = nullptr;            // [img][mhp][mwp][mld] + mcol0 (ReLU of the layer below)
+    const float* mg_mask = nullptr;            // pooled activation [img][mhp][mwp][mld] + mcol0
     long long mg_mld = 0;
     int mg_mhp = 1, mg_mwp = 1, mg_mpad = 0, mg_mcol0 = 0;
     float* mg_d = nullptr;                     // [img][dhp][dwp][dld]
     long long mg_dld = 0;
     int mg_dhp = 1, mg_dwp = 1, mg_dpad = 0;
+    // EPI_MERGE, optional: column sums of the routed (masked) values, i.e. the
+    // bias gradient of the layer below, one row per (CTA, epilogue warp):
+    // db_partial[(blockIdx.x * 4 + warp) * N + n], accumulated in shared memory
+    // over the CTA's tiles in order (deterministic).  tcgen05 kernels without
+    // split-K only; tc_gemm_prepare clears it otherwise.
+    float* db_partial = nullptr;
 };
 
 // Host-side description of one operand: a row-major fp32 matrix of `rows` x

@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tfull_bar = empty_bar + C::kStages;   // [2]
     uint64_t* tempty_bar = tfull_bar + 2;            // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+    float* db_s = reinterpret_cast<float*>(smem + C::kStages * C::kStageBytes + 256);  // [4][ldb] (EPI_MERGE db)
 
     const int warp = threadIdx.x / 32;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
@@ -197,6 +198,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         const int lane = threadIdx.x & 31;
         const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty_bar[0]), 0) : 0;
+        const bool db = epi.db_partial != nullptr;
+        const int ldb = (N + 31) & ~31;
+        float* db_row = db_s + q * ldb;
+        if (db)
+            for (int i = lane; i < ldb; i += 32) db_row[i] = 0.f;
         int local = 0;
         for (int tile = unit; tile < num_tiles; tile += units, ++local) {
             const int mn = tile % num_mn, split = tile / num_mn;
@@ -222,6 +228,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     N - nn < 32 ? N - nn : 32, v);
                 } else {
                     epilogue32(epi, m, n0 + c * 32, v);
+                    if (db && n0 + c * 32 < N) {
+                        if (m >= M) {
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+                        }
+                        db_accumulate(db_row, n0 + c * 32, N, v, lane);
+                    }
                 }
             }
             tc_fence_before();
@@ -230,6 +243,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (CG == 2) mbar_arrive_cluster(tempty_leader + acc * sizeof(uint64_t));
                 else mbar_arrive(&tempty_bar[acc]);
             }
+        }
+        if (db) {
+            __syncwarp();
+            float* out = epi.db_partial + (static_cast<long long>(blockIdx.x) * 4 + q) * N;
+            for (int i = lane; i < N; i += 32) out[i] = db_row[i];
         }
     }
 
@@ -257,9 +275,18 @@ __global__ void splitk_epilogue_kernel(const __grid_constant__ EpiParams epi, co
         n = static_cast<int>(idx % N);
         m = static_cast<int>(idx / N);
     }
+    // splits summed in order 0, 1, 2, ... (deterministic); the loads of a group
+    // of 8 are issued before the adds so they overlap
     float acc = 0.f;
     const long long off = static_cast<long long>(m) * sk.ld + n;
-    for (int s = 0; s < sk.splits; ++s) acc += sk.ws[s * sk.stride + off];
+    for (int s0 = 0; s0 < sk.splits; s0 += 8) {
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = s0 + i < sk.splits ? __ldg(sk.ws + (s0 + i) * sk.stride + off) : 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (s0 + i < sk.splits) acc += v[i];
+    }
     if (epi.mode == EPI_SGD && epi.sgd_t) {
         const float g = acc * epi.inv_b;
         if (!isfinite(g) && epi.flag != nullptr) atomicOr(epi.flag, 1);
@@ -411,12 +438,13 @@ cudaError_t tc_gemm_init_device() {
     auto set = [&](auto kernel, int smem) {
         if (e == cudaSuccess) e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     };
+    constexpr int kCap = 227 * 1024;  // launches add the EPI_MERGE db region to TcCfg::kSmem
 #define PPB_SET(AM, BM)                                                   \
-    set(tc_gemm_kernel<AM, BM, 64, 1>, TcCfg<64, 1>::kSmem);              \
-    set(tc_gemm_kernel<AM, BM, 128, 1>, TcCfg<128, 1>::kSmem);            \
-    set(tc_gemm_kernel<AM, BM, 256, 1>, TcCfg<256, 1>::kSmem);            \
-    set(tc_gemm_kernel<AM, BM, 128, 2>, TcCfg<128, 2>::kSmem);            \
-    set(tc_gemm_kernel<AM, BM, 256, 2>, TcCfg<256, 2>::kSmem);
+    set(tc_gemm_kernel<AM, BM, 64, 1>, kCap);                             \
+    set(tc_gemm_kernel<AM, BM, 128, 1>, kCap);                            \
+    set(tc_gemm_kernel<AM, BM, 256, 1>, kCap);                            \
+    set(tc_gemm_kernel<AM, BM, 128, 2>, kCap);                            \
+    set(tc_gemm_kernel<AM, BM, 256, 2>, kCap);
     PPB_SET(false, false)
     PPB_SET(false, true)
     PPB_SET(true, false)
@@ -443,7 +471,7 @@ cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.grid);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.dynamicSmemBytes = C::kSmem + p.db_smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -496,7 +524,7 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
         if (!can_split || tiles >= units) return 1;
         int sp = units / tiles;
         if (sp > nk / 8) sp = nk / 8;
-        if (sp > 64) sp = 64;
+        if (sp > sms) sp = sms;
         return sp < 1 ? 1 : sp;
     };
     // force_bn: 0 = auto; 64/128/256 = 1-CTA tiles of that width;
@@ -559,6 +587,14 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
     }
     const int work = tiles * p.sk.splits;
     p.grid = (work < units ? work : units) * cg;
+    if (p.epi.db_partial != nullptr) {  // in-epilogue bias partials: single-pass (no split-K) only
+        const int need = 4 * ((d.N + 31) / 32 * 32) * 4;
+        const int base = bn == 64 ? TcCfg<64, 1>::kSmem
+                         : cg == 2 ? (bn == 128 ? TcCfg<128, 2>::kSmem : TcCfg<256, 2>::kSmem)
+                                   : (bn == 128 ? TcCfg<128, 1>::kSmem : TcCfg<256, 1>::kSmem);
+        if (p.sk.splits > 1 || base + need > 227 * 1024) p.epi.db_partial = nullptr;
+        else p.db_smem = need;
+    }
     // A: M extent x K.  K-major: rows=M, cols=K, box {32, 128}.  MN-major:
     // stored K x M (rows=K, cols=M), box {32, 32}.  B rows per CTA = bn / cg.
     p.ga = d.a.geom;

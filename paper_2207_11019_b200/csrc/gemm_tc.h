@@ -24,6 +24,7 @@ struct TcGemmPlan {
     ConvGeom ga, gb;
     SplitK sk;
     int halo = 0;  // 1: conv_halo.cu kernel (hg describes the padded grid)
+    int db_smem = 0;  // extra dynamic smem of the EPI_MERGE db accumulator
     HaloGeom hg;
 };
 

@@ -194,17 +194,63 @@ __global__ void reduce_mask_kernel(ReduceSlots slots, long long ld_slot, int row
     }
 }
 
-__global__ void colsum_partial_kernel(const float* __restrict__ delta, long long ld, int rows, int u,
-                                      int chunks, float* __restrict__ partial) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    const int chunk = blockIdx.y;
-    const int per = (rows + chunks - 1) / chunks;
-    const int r0 = chunk * per;
-    const int r1 = r0 + per < rows ? r0 + per : rows;
-    if (c >= u) return;
-    float s = 0.f;
-    for (int r = r0; r < r1; ++r) s += delta[r * ld + c];
-    partial[static_cast<long long>(chunk) * u + c] = s;
+// Column sums of delta [rows x u] (pitch ld) into partial[blockIdx.x][u]:
+// block b owns rows [b*per, (b+1)*per); thread = (channel group g of VEC
+// channels, row lane j) with g fixed for the thread (blockDim % groups == 0),
+// rows j, j+lanes, ... summed in ascending order, 4 loads in flight; then a
+// fixed-order sum over the row lanes (deterministic).
+template <int VEC>
+__global__ void colsum_rows_kernel(const float* __restrict__ delta, long long ld, long long rows, int u,
+                                   float* __restrict__ partial) {
+    const int groups = u / VEC;
+    const int gpb = groups < 256 ? groups : 256;  // channel groups per block (blockIdx.y: group block)
+    const int g = blockIdx.y * gpb + threadIdx.x % gpb, j = threadIdx.x / gpb;
+    const int lanes = blockDim.x / gpb;
+    const bool live = g < groups;
+    const long long per = (rows + gridDim.x - 1) / gridDim.x;
+    const long long r0 = blockIdx.x * per;
+    const long long r1 = r0 + per < rows ? r0 + per : rows;
+    const float* base = delta + g * VEC;
+    float acc[VEC];
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) acc[k] = 0.f;
+    long long r = live ? r0 + j : r1;
+    for (; r + 3LL * lanes < r1; r += 4LL * lanes) {
+        float v[4][VEC];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float* p = base + (r + q * lanes) * ld;
+            if (VEC == 4) {
+                const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+                v[q][0] = t.x; v[q][1] = t.y; v[q][2] = t.z; v[q][3] = t.w;
+            } else {
+                v[q][0] = __ldg(p);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) acc[k] += v[q][k];
+    }
+    for (; r < r1; r += lanes) {
+        const float* p = base + r * ld;
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) acc[k] += __ldg(p + k);
+    }
+    extern __shared__ float sh[];
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) sh[threadIdx.x * VEC + k] = acc[k];
+    __syncthreads();
+    if (threadIdx.x < gpb && live) {
+        float t[VEC];
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) t[k] = 0.f;
+        for (int q = threadIdx.x; q < static_cast<int>(blockDim.x); q += gpb)
+#pragma unroll
+            for (int k = 0; k < VEC; ++k) t[k] += sh[q * VEC + k];
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) partial[static_cast<long long>(blockIdx.x) * u + g * VEC + k] = t[k];
+    }
 }
 
 // bias[c] -= alpha * (sum_k partial[k][c]) * inv_b, one block per 32 columns:
@@ -592,13 +638,18 @@ cudaError_t launch_reduce_mask(const ReduceSlots& slots, long long ld_slot, int 
     return cudaGetLastError();
 }
 
-cudaError_t launch_bias_update(const float* delta, long long ld, int rows, int u, float* partial,
+cudaError_t launch_bias_update(const float* delta, long long ld, long long rows, int u, float* partial,
                                float* bias, const double* alpha, float inv_b, cudaStream_t s) {
     if (u <= 0) return cudaSuccess;
     const int chunks = colsum_chunks(rows);
-    const int tpb = u >= 128 ? 128 : (u + 31) / 32 * 32;
-    dim3 g1((u + tpb - 1) / tpb, chunks);
-    colsum_partial_kernel<<<g1, tpb, 0, s>>>(delta, ld, rows, u, chunks, partial);
+    const bool v4 = u % 4 == 0 && ld % 4 == 0 && reinterpret_cast<uintptr_t>(delta) % 16 == 0;
+    const int groups = v4 ? u / 4 : u;
+    const int gpb = groups < 256 ? groups : 256;
+    const int block = (256 / gpb) * gpb;
+    const dim3 grid(chunks, (groups + gpb - 1) / gpb);
+    const size_t shmem = sizeof(float) * block * (v4 ? 4 : 1);
+    if (v4) colsum_rows_kernel<4><<<grid, block, shmem, s>>>(delta, ld, rows, u, partial);
+    else colsum_rows_kernel<1><<<grid, block, shmem, s>>>(delta, ld, rows, u, partial);
     bias_update_cols_kernel<<<(u + 31) / 32, dim3(32, 32), 0, s>>>(partial, u, chunks, bias, alpha, inv_b);
     return cudaGetLastError();
 }

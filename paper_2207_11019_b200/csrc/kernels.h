@@ -46,10 +46,11 @@ cudaError_t launch_reduce_mask(const ReduceSlots& slots, long long ld_slot, int 
 // `partial` holds colsum_chunks(rows) x u floats.
 constexpr int kColsumChunks = 1024;  // upper bound
 inline int colsum_chunks(long long rows) {
-    long long c = (rows + 127) / 128;
-    return static_cast<int>(c < 1 ? 1 : (c > kColsumChunks ? kColsumChunks : c));
+    // one block per >= 64 rows, at most 4 blocks per SM
+    long long c = (rows + 63) / 64;
+    return static_cast<int>(c < 1 ? 1 : (c > 148 * 4 ? 148 * 4 : c));
 }
-cudaError_t launch_bias_update(const float* delta, long long ld, int rows, int u, float* partial,
+cudaError_t launch_bias_update(const float* delta, long long ld, long long rows, int u, float* partial,
                                float* bias, const double* alpha, float inv_b, cudaStream_t s);
 
 // fp64 (host layout, dense) -> fp32 padded rows.

@@ -72,6 +72,7 @@ struct Session::WLayer {
     long long ldu = 0;
     unsigned char* argmax = nullptr;     // conv with pool: [b*Hq*Wq x u]
     bool merge_fused = false;            // conv: delta written by the dgrad epilogue (EPI_MERGE)
+    bool db_colsum = false;              // fused merge without in-epilogue bias partials: column-sum pass
     std::vector<std::vector<int>> delta_ready;  // [j] -> op ids that produce delta rows of micro-batch j
     std::vector<int> fwd_op, dgrad_op;   // [j]
     TcGemmPlan p_wgrad;
@@ -757,21 +758,14 @@ void Session::build_ops() {
                     d.epi.mg_wg = lb.Wq();
                     d.epi.mg_argmax = dl.argmax ? dl.argmax + off * hw * dl.u : nullptr;
                     d.epi.mg_uch = dl.u;
-                    if (relu_below) {
-                        if (dl.U != nullptr) {
-                            d.epi.mg_mask = dl.U + off * lb.Ho() * lb.Wo() * dl.ldu;
-                            d.epi.mg_mld = dl.ldu;
-                            d.epi.mg_mhp = lb.Ho();
-                            d.epi.mg_mwp = lb.Wo();
-                        } else {
-                            const ActLayout& a = lay_[l - 1];
-                            d.epi.mg_mask = act_buf(dw.gpu, l - 1) + off * img_elems(l - 1);
-                            d.epi.mg_mld = a.ld;
-                            d.epi.mg_mhp = a.hp;
-                            d.epi.mg_mwp = a.wp;
-                            d.epi.mg_mpad = a.pad;
-                            d.epi.mg_mcol0 = dl.lo;
-                        }
+                    if (relu_below) {  // mask at the pooled pixel of the layer's output (consumer layout)
+                        const ActLayout& a = lay_[l - 1];
+                        d.epi.mg_mask = act_buf(dw.gpu, l - 1) + off * img_elems(l - 1);
+                        d.epi.mg_mld = a.ld;
+                        d.epi.mg_mhp = a.hp;
+                        d.epi.mg_mwp = a.wp;
+                        d.epi.mg_mpad = a.pad;
+                        d.epi.mg_mcol0 = dl.lo;
                     }
                     const int q = lb.ksz - 1 - lb.pad;
                     d.epi.mg_d = dl.delta + off * dl.delta_img;
@@ -779,7 +773,11 @@ void Session::build_ops() {
                     d.epi.mg_dhp = lb.Ho() + 2 * q;
                     d.epi.mg_dwp = lb.Wo() + 2 * q;
                     d.epi.mg_dpad = q;
+                    // bias-gradient partials of the layer below, same [j][merge block][u]
+                    // layout the unfused conv_merge writes
+                    d.epi.db_partial = dl.partial + static_cast<long long>(j) * conv_merge_blocks() * dl.u;
                     prepare(d, wl.p_dgrad[j], w.gpu);
+                    if (!tf32 || wl.p_dgrad[j].epi.db_partial == nullptr) dl.db_colsum = true;
                     const double fl = 2.0 * rows * li.H * li.W * li.in_units * li.ksz * li.ksz * wl.u;
                     const int op = add_op(w.gpu, w.sb, gemm_launch(&wl.p_dgrad[j], &wl.d_dgrad[j], w.sb),
                                           wl.delta_ready[j], 1, OP_DGRAD_GEMM, fl);
@@ -1024,7 +1022,8 @@ void Session::build_ops() {
             float* partial = wl.partial;
             float* bias = wl.bias;
             const double* alpha = &g.st->alpha;
-            const bool from_merge = li.kind == 1 && !wl.merge_fused;  // conv: db partials came with the merges
+            // conv: db partials came with the merges (conv_merge or the EPI_MERGE epilogue)
+            const bool from_merge = li.kind == 1 && !wl.db_colsum;
             const int chunks = cfg_.m * conv_merge_blocks();
             const int bop = add_op(w.gpu, s, [=]() {
                 if (from_merge) return launch_bias_from_partials(partial, chunks, u, bias, alpha, inv_b, s);
