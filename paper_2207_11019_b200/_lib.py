@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpipeplan_b200.so")
+LIB_PATH = os.environ.get("PPB_LIB_PATH") or os.path.join(_HERE, "libpipeplan_b200.so")  # override: A/B experiments
 
 PPB_OK = 0
 PPB_ERR_INVALID_ARGUMENT = 1
@@ -108,6 +108,7 @@ _SIGS = {
     "ppb_debug_conv": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_longlong, C.c_int,
                                  C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_longlong, C.c_void_p, C.c_longlong,
                                  C.c_int, C.c_void_p]),
+    "ppb_debug_tma_bw": (C.c_int, [C.c_void_p] + [C.c_int] * 8 + [C.c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -39,6 +39,9 @@ inline bool conv_box(int ho, int wo, int pixels, ConvGeom& g) {
     }
     g.wo = wo;
     g.howo = hw;
+    g.ho = ho;
+    g.krows = hw >= 32 && 32 % wo == 0 ? 32 / wo : 1;
+    g.kimgs = hw < 32 && 32 % hw == 0 ? 32 / hw : 1;
     return true;
 }
 

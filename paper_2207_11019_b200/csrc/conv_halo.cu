@@ -18,7 +18,8 @@
 // is loaded ONCE per CTA and stays resident (VGG conv2 / conv3 and their dgrads);
 // otherwise it streams through its own ring.
 //
-//   warp 0      TMA producer: halo ring (2-4 stages) + resident B / B ring
+//   warp 0      TMA producer: halo ring (2-4 stages)
+//   warp 3      TMA producer: resident B slice (once) or the B ring
 //   warp 1      MMA issuer (leader CTA; CG = 2 -> M = 256 over a CTA pair)
 //   warp 2      TMEM allocator (2 x BN accumulator columns)
 //   warps 4..7  epilogue: padded position -> output pixel (or skip) -> the
@@ -115,30 +116,12 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ------------------------------------------------ TMA producer
+        // ------------------------------------------------ TMA producer: halo boxes
         if (elect_one()) {
-            int hs = 0, bs = 0;
-            uint32_t hph = 0, bph = 0;
-            if (hg.resident) {
-                // the whole B slice of this CTA (one column tile): every K block,
-                // one barrier per block so the first MMAs start early
-                const int n0 = static_cast<int>(rank) * C::kBNc;
-                for (int kb = 0; kb < 9 * cblocks; ++kb) {
-                    Tma<CG> t;
-                    t.bar = &bfull[kb];
-                    t.bar_c = 0;
-                    if (CG == 1) {
-                        mbar_arrive_expect_tx(&bfull[kb], C::kStageB);
-                    } else {
-                        t.bar_c = mapa_shared(smem_u32(&bfull[kb]), 0);
-                        if (leader) mbar_arrive_expect_tx(&bfull[kb], 2 * C::kStageB);
-                    }
-                    load_operand<B_MN, C::kBNc, CG>(t, &tb, gb, sB + kb * C::kStageB, n0, kb);
-                }
-            }
+            int hs = 0;
+            uint32_t hph = 0;
             for (int tile = unit; tile < num_tiles; tile += units) {
                 const long long p0 = static_cast<long long>(tile % num_m) * TM + static_cast<long long>(rank) * kBM;
-                const int n0 = (tile / num_m) * BN + static_cast<int>(rank) * C::kBNc;
                 for (int cb = 0; cb < cblocks; ++cb) {
                     mbar_wait(&hempty[hs], hph ^ 1);
                     Tma<CG> th;
@@ -156,22 +139,41 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                         hs = 0;
                         hph ^= 1;
                     }
-                    if (hg.resident) continue;
-                    for (int tap = 0; tap < 9; ++tap) {
-                        mbar_wait(&bempty[bs], bph ^ 1);
-                        Tma<CG> t;
-                        t.bar = &bfull[bs];
-                        t.bar_c = 0;
-                        if (CG == 1) {
-                            mbar_arrive_expect_tx(&bfull[bs], C::kStageB);
-                        } else {
-                            t.bar_c = mapa_shared(smem_u32(&bfull[bs]), 0);
-                            if (leader) mbar_arrive_expect_tx(&bfull[bs], 2 * C::kStageB);
-                        }
-                        load_operand<B_MN, C::kBNc, CG>(t, &tb, gb, sB + bs * C::kStageB, n0, tap * cblocks + cb);
-                        if (++bs == kBStages) {
-                            bs = 0;
-                            bph ^= 1;
+                }
+            }
+        }
+    } else if (warp == 3) {
+        // ------------------------------------------------ TMA producer: B (weights)
+        if (elect_one()) {
+            auto issue = [&](int slot, int n0, int kb) {
+                Tma<CG> t;
+                t.bar = &bfull[slot];
+                t.bar_c = 0;
+                if (CG == 1) {
+                    mbar_arrive_expect_tx(&bfull[slot], C::kStageB);
+                } else {
+                    t.bar_c = mapa_shared(smem_u32(&bfull[slot]), 0);
+                    if (leader) mbar_arrive_expect_tx(&bfull[slot], 2 * C::kStageB);
+                }
+                load_operand<B_MN, C::kBNc, CG>(t, &tb, gb, sB + slot * C::kStageB, n0, kb);
+            };
+            if (hg.resident) {
+                // the whole B slice of this CTA (one column tile), once: every K
+                // block on its own barrier so the first MMAs start early
+                for (int kb = 0; kb < 9 * cblocks; ++kb) issue(kb, static_cast<int>(rank) * C::kBNc, kb);
+            } else {
+                int bs = 0;
+                uint32_t bph = 0;
+                for (int tile = unit; tile < num_tiles; tile += units) {
+                    const int n0 = (tile / num_m) * BN + static_cast<int>(rank) * C::kBNc;
+                    for (int cb = 0; cb < cblocks; ++cb) {
+                        for (int tap = 0; tap < 9; ++tap) {
+                            mbar_wait(&bempty[bs], bph ^ 1);
+                            issue(bs, n0, tap * cblocks + cb);
+                            if (++bs == kBStages) {
+                                bs = 0;
+                                bph ^= 1;
+                            }
                         }
                     }
                 }

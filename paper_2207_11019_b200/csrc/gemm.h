@@ -117,6 +117,8 @@ struct ConvGeom {
     int cblocks = 1;         // 32-channel blocks per tap in the K loop (ROWS, WFLIP)
     int ck = 32;             // per-tap channel pitch of the GEMM N index (KPIX B)
     int off = 0;             // spatial offset into the padded tensor
+    int ho = 1;              // output grid rows (howo / wo)
+    int krows = 1, kimgs = 1;  // KPIX: rows (howo >= 32) or images (howo < 32) per 32-pixel K block
 };
 
 struct Operand {
@@ -139,6 +141,7 @@ struct SplitK {
     float* ws = nullptr;
     long long ld = 0;
     long long stride = 0;
+    int trans = 0;  // workspace stored [n][m] (EPI_SGD with sgd_t)
 };
 
 // Padded-position geometry of the halo conv kernel (conv_halo.cu): GEMM row

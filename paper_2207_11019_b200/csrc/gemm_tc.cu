@@ -1,7 +1,8 @@
 // Persistent, warp-specialised tcgen05 TF32 GEMM for sm_100a.
 //
-//   warp 0      : TMA producer (one elected lane), SWIZZLE_128B tiles into a
-//                 kStages-deep shared-memory ring guarded by full/empty mbarriers
+//   warps 0, 3  : TMA producers (one elected lane each: A, B), SWIZZLE_128B tiles
+//                 into a kStages-deep shared-memory ring guarded by full/empty
+//                 mbarriers (full: one arrival per producer)
 //   warp 1      : MMA issuer (one elected lane of the leader CTA):
 //                 tcgen05.mma.cta_group::{1,2}.kind::tf32, accumulator in TMEM
 //   warp 2      : TMEM allocator (2 x BN columns: double-buffered accumulator)
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch(&ta);
         tma_prefetch(&tb);
         for (int s = 0; s < C::kStages; ++s) {
-            mbar_init(&full_bar[s], 1);
+            mbar_init(&full_bar[s], 2);  // the A and the B producer each arrive (with their tx bytes)
             mbar_init(&empty_bar[s], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -108,38 +109,50 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp == 0) {
-        // ------------------------------------------------ TMA producer
-        if (elect_one()) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int tile = unit; tile < num_tiles; tile += units) {
-                const int mn = tile % num_mn, split = tile / num_mn;
-                const int m0 = (mn % num_m) * TM + static_cast<int>(rank) * kBM;
-                const int n0 = (mn / num_m) * BN + static_cast<int>(rank) * C::kBNc;
-                const int kb_end = min(nk, (split + 1) * sk.kps);
-                for (int kb = split * sk.kps; kb < kb_end; ++kb) {
-                    mbar_wait(&empty_bar[stage], phase ^ 1);
-                    uint8_t* a_dst = sA + stage * C::kStageA;
-                    uint8_t* b_dst = sB + stage * C::kStageB;
-                    Tma<CG> t;
-                    t.bar = &full_bar[stage];
-                    t.bar_c = 0;
-                    if (CG == 1) {
-                        mbar_arrive_expect_tx(&full_bar[stage], C::kStageBytes);
-                    } else {
-                        // both CTAs' bytes land on the leader's full barrier
-                        t.bar_c = mapa_shared(smem_u32(&full_bar[stage]), 0);
-                        if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * C::kStageBytes);
-                    }
-                    load_operand<A_MN, kBM, CG>(t, &ta, ga, a_dst, m0, kb);
-                    load_operand<B_MN, C::kBNc, CG>(t, &tb, gb, b_dst, n0, kb);
-                    if (++stage == C::kStages) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+    // ------------------------------------------------ TMA producers: warp 0 stages A, warp 3 stages B
+    // (two single-thread issue streams: one thread's per-K-block bookkeeping
+    // was on the critical path of the N = 256 pair tiles)
+    auto produce = [&](auto& cur, const CUtensorMap* map, const ConvGeom& g, uint8_t* base, int stage_bytes,
+                       bool is_a) {
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int tile = unit; tile < num_tiles; tile += units) {
+            const int mn = tile % num_mn, split = tile / num_mn;
+            const int o = is_a ? (mn % num_m) * TM + static_cast<int>(rank) * kBM
+                               : (mn / num_m) * BN + static_cast<int>(rank) * C::kBNc;
+            const int kb0 = split * sk.kps;
+            const int kb_end = min(nk, (split + 1) * sk.kps);
+            cur.init(g, o, kb0);
+            for (int kb = kb0; kb < kb_end; ++kb) {
+                mbar_wait(&empty_bar[stage], phase ^ 1);
+                Tma<CG> t;
+                t.bar = &full_bar[stage];
+                t.bar_c = 0;
+                if (CG == 1) {
+                    mbar_arrive_expect_tx(&full_bar[stage], stage_bytes);
+                } else {
+                    // both CTAs' bytes land on the leader's full barrier
+                    t.bar_c = mapa_shared(smem_u32(&full_bar[stage]), 0);
+                    if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * stage_bytes);
+                }
+                cur.load(t, map, g, base + stage * stage_bytes, o);
+                cur.advance(g);
+                if (++stage == C::kStages) {
+                    stage = 0;
+                    phase ^= 1;
                 }
             }
+        }
+    };
+    if (warp == 0) {
+        if (elect_one()) {
+            OperandCursor<A_MN, kBM, CG> ca;
+            produce(ca, &ta, ga, sA, C::kStageA, true);
+        }
+    } else if (warp == 3) {
+        if (elect_one()) {
+            OperandCursor<B_MN, C::kBNc, CG> cb;
+            produce(cb, &tb, gb, sB, C::kStageB, false);
         }
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer (leader CTA)
@@ -223,9 +236,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
                 if (sk.splits > 1) {  // raw partial sums for splitk_epilogue_kernel
                     const int nn = n0 + c * 32;
-                    if (m < M && nn < N)
+                    if (sk.trans) {  // [n][m]: for each column the warp's lanes write consecutive m
+                        float* col = sk.ws + split * sk.stride + m;
+                        if (m < M) {
+#pragma unroll
+                            for (int i = 0; i < 32; ++i)
+                                if (nn + i < N) col[static_cast<long long>(nn + i) * sk.ld] = v[i];
+                        }
+                    } else if (m < M && nn < N) {
                         store_row32(sk.ws + split * sk.stride + static_cast<long long>(m) * sk.ld, nn,
                                     N - nn < 32 ? N - nn : 32, v);
+                    }
                 } else {
                     epilogue32(epi, m, n0 + c * 32, v);
                     if (db && n0 + c * 32 < N) {
@@ -261,39 +282,63 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-// Split-K reduction: C(m, n) = sum over splits in order (deterministic), then
-// the GEMM's real epilogue.  One thread per (row, 32-column chunk).
-__global__ void splitk_epilogue_kernel(const __grid_constant__ EpiParams epi, const __grid_constant__ SplitK sk,
-                                       int M, int N) {
-    const long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-    if (idx >= static_cast<long long>(M) * N) return;
-    int m, n;
-    if (epi.mode == EPI_SGD && epi.sgd_t) {  // coalesce along m (W[n][m])
-        m = static_cast<int>(idx % M);
-        n = static_cast<int>(idx / M);
-    } else {  // coalesce along n
-        n = static_cast<int>(idx % N);
-        m = static_cast<int>(idx / N);
-    }
-    // splits summed in order 0, 1, 2, ... (deterministic); the loads of a group
-    // of 8 are issued before the adds so they overlap
-    float acc = 0.f;
-    const long long off = static_cast<long long>(m) * sk.ld + n;
-    for (int s0 = 0; s0 < sk.splits; s0 += 8) {
-        float v[8];
+// Split-K reduction: C(m, n) = sum over splits in order 0, 1, 2, ...
+// (deterministic), then the GEMM's real epilogue.  The workspace is [m][n]
+// (pitch sk.ld), or [n][m] when sk.trans (the dW^T SGD epilogue, whose W[n][m]
+// writes coalesce along m).  Thread = 4 consecutive workspace columns of one
+// workspace row; 32-bit index math; float4 loads.
+__global__ void __launch_bounds__(256) splitk_epilogue_kernel(const __grid_constant__ EpiParams epi,
+                                                              const __grid_constant__ SplitK sk, int M, int N) {
+    const int R = sk.trans ? N : M;
+    const int Cc = sk.trans ? M : N;
+    const int c4 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (c4 >= Cc) return;
+    const int nc = Cc - c4 < 4 ? Cc - c4 : 4;
+    const bool vec = nc == 4 && (sk.ld & 3) == 0;
+    const float alpha = epi.mode == EPI_SGD ? static_cast<float>(*epi.alpha) : 0.f;
+    for (int r = blockIdx.y; r < R; r += gridDim.y) {
+        const long long off = static_cast<long long>(r) * sk.ld + c4;
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int s0 = 0; s0 < sk.splits; s0 += 4) {
+            float v[4][4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = s0 + i < sk.splits ? __ldg(sk.ws + (s0 + i) * sk.stride + off) : 0.f;
+            for (int i = 0; i < 4; ++i) {
+                const float* src = sk.ws + static_cast<long long>(s0 + i) * sk.stride + off;
+                if (s0 + i >= sk.splits) {
+                    v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0.f;
+                } else if (vec) {
+                    const float4 t = __ldg(reinterpret_cast<const float4*>(src));
+                    v[i][0] = t.x; v[i][1] = t.y; v[i][2] = t.z; v[i][3] = t.w;
+                } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-            if (s0 + i < sk.splits) acc += v[i];
+                    for (int j = 0; j < 4; ++j) v[i][j] = j < nc ? __ldg(src + j) : 0.f;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (s0 + i < sk.splits)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[j] += v[i][j];
+        }
+        if (sk.trans) {  // EPI_SGD on dW^T: row r = n, columns = m
+            float* w = epi.W + static_cast<long long>(r) * epi.ldw + c4;
+            bool bad = false;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (j < nc) {
+                    const float g = acc[j] * epi.inv_b;
+                    bad |= !isfinite(g);
+                    w[j] -= alpha * g;
+                }
+            }
+            if (bad && epi.flag != nullptr) atomicOr(epi.flag, 1);
+            continue;
+        }
+        const long long row_off = epi.mode == EPI_STORE ? epi_store_row(epi, r) : 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (j < nc) epilogue1(epi, r, c4 + j, acc[j], row_off);
     }
-    if (epi.mode == EPI_SGD && epi.sgd_t) {
-        const float g = acc * epi.inv_b;
-        if (!isfinite(g) && epi.flag != nullptr) atomicOr(epi.flag, 1);
-        epi.W[static_cast<long long>(n) * epi.ldw + m] -= static_cast<float>(*epi.alpha) * g;
-        return;
-    }
-    epilogue1(epi, m, n, acc, epi.mode == EPI_STORE ? epi_store_row(epi, m) : 0);
 }
 
 // ---------------------------------------------------------------- host side
@@ -483,8 +528,9 @@ cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
     cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<A_MN, B_MN, BN, CG>, p.ta, p.tb, p.M, p.N, p.K, p.epi,
                                        p.ga, p.gb, p.sk);
     if (e != cudaSuccess || p.sk.splits <= 1) return e;
-    const long long threads = static_cast<long long>(p.M) * p.N;
-    splitk_epilogue_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(p.epi, p.sk, p.M, p.N);
+    const int R = p.sk.trans ? p.N : p.M, Cc = p.sk.trans ? p.M : p.N;
+    const dim3 grid((Cc + 1023) / 1024, R < 65535 ? R : 65535);
+    splitk_epilogue_kernel<<<grid, 256, 0, s>>>(p.epi, p.sk, p.M, p.N);
     return cudaGetLastError();
 }
 
@@ -576,8 +622,9 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
             splits = (nk + kps - 1) / kps;
             p.sk.splits = splits;
             p.sk.kps = kps;
-            p.sk.ld = (d.N + 3) / 4 * 4;
-            p.sk.stride = p.sk.ld * d.M;
+            p.sk.trans = d.epi.mode == EPI_SGD && d.epi.sgd_t ? 1 : 0;
+            p.sk.ld = p.sk.trans ? (d.M + 3) / 4 * 4 : (d.N + 3) / 4 * 4;
+            p.sk.stride = p.sk.ld * (p.sk.trans ? d.N : d.M);
             p.sk.ws = ws_alloc(static_cast<size_t>(p.sk.stride) * splits);
             if (p.sk.ws == nullptr) {
                 snprintf(err, errlen, "split-K workspace allocation failed");
