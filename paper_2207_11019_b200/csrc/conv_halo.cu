@@ -42,7 +42,7 @@ namespace {
 
 std::atomic<unsigned> g_halo_attr{0};
 
-constexpr int kHaloThreads = 256;
+constexpr int kHaloThreads = 128 + 32 * kEpiWarps;
 constexpr int kHaloMaxRows = 256;  // TMA box limit
 constexpr int kHaloSmemMax = 227 * 1024;
 constexpr int kHaloReserve = 1024 + 1024;  // alignment slack + barriers
@@ -58,7 +58,7 @@ template <bool B_MN, int BN, int CG>
 __global__ void __launch_bounds__(kHaloThreads, 1)
     halo_conv_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int N,
                      const __grid_constant__ HaloGeom hg, const __grid_constant__ EpiParams epi,
-                     const __grid_constant__ ConvGeom gb) {
+                     const __grid_constant__ ConvGeom gb, const __grid_constant__ TmaStore ts) {
     using C = HaloCfg<BN, CG>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -75,6 +75,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     uint64_t* tempty = tfull + 2;            // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     float* db_s = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(hfull) + 1024);  // [4][ldb] (EPI_MERGE db)
+    uint8_t* stg = reinterpret_cast<uint8_t*>(hfull) + ts.stage_off;                    // TMA-store staging
 
     const int warp = threadIdx.x / 32;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
@@ -101,7 +102,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 4 * CG);
+            mbar_init(&tempty[i], kEpiWarps * CG);
         }
         fence_mbar_init();
     }
@@ -248,15 +249,19 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         }
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue
-        const int q = warp & 3;
+        const int q = warp & 3;              // TMEM lane quarter this warp may access
+        const int half = (warp - 4) >> 2;    // 0 / 1: even / odd 32-column chunks
         const int lane = threadIdx.x & 31;
         const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
         const int hpwp = hg.hp * hg.wp;
         const bool db = epi.db_partial != nullptr;
         const int ldb = (N + 31) & ~31;
         float* db_row = db_s + q * ldb;
-        if (db)
-            for (int i = lane; i < ldb; i += 32) db_row[i] = 0.f;
+        if (db) {
+            if (half == 0)
+                for (int i = lane; i < ldb; i += 32) db_row[i] = 0.f;
+            epi_bar_sync();
+        }
         int local = 0;
         for (int tile = unit; tile < num_tiles; tile += units, ++local) {
             const long long p0 = static_cast<long long>(tile % num_m) * TM + static_cast<long long>(rank) * kBM;
@@ -275,14 +280,24 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = half; c < BN / 32; c += 2) {
                 uint32_t rr[32];
                 tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, rr);
                 tmem_ld_wait();
                 float v[32];
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = m >= 0 ? __uint_as_float(rr[i]) : 0.f;
-                if (m >= 0 && !(hg.dbg & 2)) epilogue32(epi, m, n0 + c * 32, v);
+                if (ts.n) {  // pad-ring rows store zeros (the destination's own ring)
+                    epi_values32(epi, m, n0 + c * 32, v, lane);
+                    if (m < 0) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+                    }
+                    if (!(hg.dbg & 2))
+                        tma_store_chunk(ts, stg + (warp - 4) * 4096, lane, v, static_cast<int>(p0) + q * 32, n0 + c * 32);
+                } else if (m >= 0 && !(hg.dbg & 2)) {
+                    epilogue32(epi, m, n0 + c * 32, v);
+                }
                 if (db && n0 + c * 32 < N) db_accumulate(db_row, n0 + c * 32, N, v, lane);
             }
             tc_fence_before();
@@ -292,11 +307,14 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 else mbar_arrive(&tempty[acc]);
             }
         }
-        if (db) {
-            __syncwarp();
-            float* out = epi.db_partial + (static_cast<long long>(blockIdx.x) * 4 + q) * N;
-            for (int i = lane; i < N; i += 32) out[i] = db_row[i];
+        if (db) {  // both warps of the quarter accumulated into db_row (disjoint columns)
+            epi_bar_sync();
+            if (half == 0) {
+                float* out = epi.db_partial + (static_cast<long long>(blockIdx.x) * 4 + q) * N;
+                for (int i = lane; i < N; i += 32) out[i] = db_row[i];
+            }
         }
+        if (ts.n && lane == 0) bulk_wait<0>();
     }
 
     tc_fence_before();
@@ -329,7 +347,7 @@ cudaError_t launch_halo_t(const TcGemmPlan& p, cudaStream_t s) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, halo_conv_kernel<B_MN, BN, CG>, p.ta, p.tb, p.N, p.hg, p.epi, p.gb);
+    return cudaLaunchKernelEx(&cfg, halo_conv_kernel<B_MN, BN, CG>, p.ta, p.tb, p.N, p.hg, p.epi, p.gb, p.ts);
 }
 
 template <bool B_MN>
@@ -435,12 +453,20 @@ bool halo_conv_prepare(const GemmDesc& d, TcGemmPlan* out, int force, char* err,
     p.bn = bn;
     p.cg = cg;
     // shared-memory plan: halo ring + either the whole B column slice resident
-    // (one column tile, fits next to >= 2 halo stages) or a streaming B ring
+    // (one column tile, fits next to >= 2 halo stages) or a streaming B ring;
+    // after the barrier block: the EPI_MERGE db rows, then the TMA-store staging
     {
         const int stage_b = bn / cg * kBK * 4;
         const int nkb = 9 * hg.cblocks;
         hg.hstage_bytes = (hg.rows * 128 + 1023) / 1024 * 1024;
-        const int avail = kHaloSmemMax - kHaloReserve;
+        const int db_need = p.epi.db_partial != nullptr ? 4 * ((d.N + 31) / 32 * 32) * 4 : 0;
+        const bool tma = tma_store_setup(p.epi, d.M, d.N, &hg, &p.ts);
+        int extra = db_need;
+        if (tma) {
+            p.ts.stage_off = 1024 + (db_need + 1023) / 1024 * 1024;
+            extra = p.ts.stage_off - 1024 + kEpiStageBytes;
+        }
+        const int avail = kHaloSmemMax - kHaloReserve - extra;
         const bool one_col = d.N <= bn;
         if (one_col && nkb * stage_b + 2 * hg.hstage_bytes <= avail && !getenv("PPB_HALO_STREAM_B")) {
             hg.resident = 1;
@@ -450,24 +476,14 @@ bool halo_conv_prepare(const GemmDesc& d, TcGemmPlan* out, int force, char* err,
         } else {
             hg.resident = 0;
             hg.hstages = 3;
-            hg.bstages = (200 * 1024 - 3 * hg.hstage_bytes) / stage_b;
+            hg.bstages = (avail - 3 * hg.hstage_bytes) / stage_b;
             if (hg.bstages > 12) hg.bstages = 12;
             if (hg.bstages < 2) {
                 snprintf(err, errlen, "halo conv: shared memory too small for tile width %d", bn);
                 return false;
             }
         }
-        hg.smem = 1024 + hg.hstages * hg.hstage_bytes + hg.bstages * stage_b + 1024;
-        if (p.epi.db_partial != nullptr) {  // EPI_MERGE bias partials after the barrier block
-            const int need = 4 * ((d.N + 31) / 32 * 32) * 4;
-            while (hg.smem + need > kHaloSmemMax && ((hg.resident && hg.hstages > 2) || (!hg.resident && hg.bstages > 2))) {
-                if (hg.resident) --hg.hstages;
-                else --hg.bstages;
-                hg.smem = 1024 + hg.hstages * hg.hstage_bytes + hg.bstages * stage_b + 1024;
-            }
-            if (hg.smem + need <= kHaloSmemMax) hg.smem += need;
-            else p.epi.db_partial = nullptr;
-        }
+        hg.smem = 1024 + hg.hstages * hg.hstage_bytes + hg.bstages * stage_b + 1024 + extra;
         if (2 * (hg.hstages + hg.bstages + 2) * 8 + 8 > 1024) {
             snprintf(err, errlen, "halo conv: too many pipeline barriers");
             return false;

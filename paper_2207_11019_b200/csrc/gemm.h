@@ -90,6 +90,9 @@ struct EpiParams {
     // over the CTA's tiles in order (deterministic).  tcgen05 kernels without
     // split-K only; tc_gemm_prepare clears it otherwise.
     float* db_partial = nullptr;
+    // timing probes only (wrong results): 2 = skip the epilogue's global stores,
+    // 4 = skip the epilogue, 8 = skip the MMAs
+    int dbg = 0;
 };
 
 // Host-side description of one operand: a row-major fp32 matrix of `rows` x

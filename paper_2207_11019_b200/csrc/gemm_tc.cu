@@ -41,7 +41,7 @@ namespace {
 
 std::atomic<unsigned> g_attr_set{0};  // one bit per device: smem attributes set
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 128 + 32 * kEpiWarps;  // 4 control warps + epilogue warps
 
 template <int BN, int CG>
 struct TcCfg {
@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                    int M, int N, int K, const __grid_constant__ EpiParams epi,
                    const __grid_constant__ ConvGeom ga, const __grid_constant__ ConvGeom gb,
-                   const __grid_constant__ SplitK sk) {
+                   const __grid_constant__ SplitK sk, const __grid_constant__ TmaStore ts) {
     using C = TcCfg<BN, CG>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tempty_bar = tfull_bar + 2;            // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
     float* db_s = reinterpret_cast<float*>(smem + C::kStages * C::kStageBytes + 256);  // [4][ldb] (EPI_MERGE db)
+    uint8_t* stg = smem + C::kStages * C::kStageBytes + ts.stage_off;                  // TMA-store staging
 
     const int warp = threadIdx.x / 32;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull_bar[i], 1);
-            mbar_init(&tempty_bar[i], 4 * CG);  // one arrival per epilogue warp of the pair
+            mbar_init(&tempty_bar[i], kEpiWarps * CG);  // one arrival per epilogue warp of the pair
         }
         fence_mbar_init();
     }
@@ -187,6 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const uint64_t bd = B_MN ? umma_desc<kLayoutSW128Base32>(b_addr + kk * 1024, 4096, 512)
                                                      : umma_desc<kLayoutSW128>(b_addr + kk * 32, 16, 1024);
                             const uint32_t accum = (kb != kb0 || kk != 0) ? 1u : 0u;
+                            if (epi.dbg & 8) continue;  // timing probe: no MMAs
                             if (CG == 2) mma_tf32_pair(d_tmem, ad, bd, idesc, accum);
                             else mma_tf32(d_tmem, ad, bd, idesc, accum);
                         }
@@ -208,14 +210,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue
-        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int q = warp & 3;              // TMEM lane quarter this warp may access
+        const int half = (warp - 4) >> 2;    // 0 / 1: even / odd 32-column chunks  // TMEM lane quarter this warp may access
         const int lane = threadIdx.x & 31;
         const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty_bar[0]), 0) : 0;
         const bool db = epi.db_partial != nullptr;
         const int ldb = (N + 31) & ~31;
         float* db_row = db_s + q * ldb;
-        if (db)
-            for (int i = lane; i < ldb; i += 32) db_row[i] = 0.f;
+        if (db) {
+            if (half == 0)
+                for (int i = lane; i < ldb; i += 32) db_row[i] = 0.f;
+            epi_bar_sync();
+        }
         int local = 0;
         for (int tile = unit; tile < num_tiles; tile += units, ++local) {
             const int mn = tile % num_mn, split = tile / num_mn;
@@ -227,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const int m = m0 + q * 32 + lane;
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = half; c < ((epi.dbg & 4) ? 0 : BN / 32); c += 2) {  // dbg 4: timing probe, no epilogue
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, r);
                 tmem_ld_wait();
@@ -248,7 +254,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     N - nn < 32 ? N - nn : 32, v);
                     }
                 } else {
-                    epilogue32(epi, m, n0 + c * 32, v);
+                    if (ts.n) {
+                        epi_values32(epi, m, n0 + c * 32, v, lane);
+                        if (!(epi.dbg & 2)) tma_store_chunk(ts, stg + (warp - 4) * 4096, lane, v, m0 + q * 32, n0 + c * 32);
+                    } else if (!(epi.dbg & 2)) {
+                        epilogue32(epi, m, n0 + c * 32, v);
+                    }
                     if (db && n0 + c * 32 < N) {
                         if (m >= M) {
 #pragma unroll
@@ -265,11 +276,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 else mbar_arrive(&tempty_bar[acc]);
             }
         }
-        if (db) {
-            __syncwarp();
-            float* out = epi.db_partial + (static_cast<long long>(blockIdx.x) * 4 + q) * N;
-            for (int i = lane; i < N; i += 32) out[i] = db_row[i];
+        if (db) {  // both warps of the quarter accumulated into db_row (disjoint columns)
+            epi_bar_sync();
+            if (half == 0) {
+                float* out = epi.db_partial + (static_cast<long long>(blockIdx.x) * 4 + q) * N;
+                for (int i = lane; i < N; i += 32) out[i] = db_row[i];
+            }
         }
+        if (ts.n && lane == 0) bulk_wait<0>();
     }
 
     tc_fence_before();
@@ -443,6 +457,120 @@ bool encode_conv_map(CUtensorMap* map, const Operand& o, char* err, size_t errle
     return true;
 }
 
+// ---------------------------------------------------------------- TMA-store epilogue setup
+
+bool tma_store_setup(const EpiParams& e, int M, int N, const HaloGeom* hg, TmaStore* ts) {
+    ts->n = 0;
+    static const bool off = [] {
+        const char* v = getenv("PPB_NO_TMA_STORE");
+        return v != nullptr && *v != '\0' && *v != '0';
+    }();
+    auto enc = get_encode();
+    if (off || enc == nullptr || N < 32 || M <= 0) return false;
+    float* ptrs[kMaxDst];
+    int nd = 0;
+    long long ld = 0;
+    int col0 = 0;
+    bool padded = false;
+    int hp = 1, wp = 1, pad = 0, wo = 1, ho = 1;
+    switch (e.mode) {
+        case EPI_STORE:
+            for (int d = 0; d < e.ndst; ++d) ptrs[nd++] = e.dst[d];
+            ld = e.ldd;
+            col0 = e.col0;
+            if (e.remap) {
+                padded = true;
+                hp = e.r_hp, wp = e.r_wp, pad = e.r_pad, wo = e.r_wo, ho = e.r_howo / e.r_wo;
+            }
+            break;
+        case EPI_MERGE:
+            if (e.mg_pool != 1 || N % 32 != 0) return false;
+            if (e.mg_mask != nullptr && (e.mg_mld % 4 != 0 || e.mg_mcol0 % 4 != 0 ||
+                                         (reinterpret_cast<uintptr_t>(e.mg_mask) & 15u) != 0))
+                return false;
+            ptrs[nd++] = e.mg_d;
+            ld = e.mg_dld;
+            padded = true;
+            hp = e.mg_dhp, wp = e.mg_dwp, pad = e.mg_dpad, wo = e.mg_wg, ho = e.mg_hg;
+            break;
+        case EPI_MASK:
+            if (N % 32 != 0 || e.ldm % 4 != 0 || e.mcol0 % 4 != 0 || (reinterpret_cast<uintptr_t>(e.mask) & 15u) != 0)
+                return false;
+            ptrs[nd++] = e.dst[0];
+            ld = e.ldd;
+            col0 = e.col0;
+            break;
+        default:
+            return false;
+    }
+    if (nd == 0 || ld % 4 != 0 || col0 % 4 != 0) return false;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    for (int d = 0; d < nd; ++d) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, ptrs[d]) != cudaSuccess || a.type != cudaMemoryTypeDevice || a.device != dev) {
+            cudaGetLastError();
+            return false;  // peer destinations keep the register path
+        }
+        if ((reinterpret_cast<uintptr_t>(ptrs[d] + col0) & 15u) != 0) return false;
+    }
+    cuuint64_t dims[4];
+    cuuint64_t strides[3];
+    cuuint32_t box[4] = {32u, 32u, 1u, 1u};
+    cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+    cuuint32_t rank = 2;
+    long long base_off = col0;
+    if (hg != nullptr) {
+        // halo rows are padded positions: identity when the destination has the same grid
+        if (!padded || hp != hg->hp || wp != hg->wp || pad != 1 || ho != hg->ho || wo != hg->wo) return false;
+        dims[0] = static_cast<cuuint64_t>(N);
+        dims[1] = static_cast<cuuint64_t>(hg->Mp);
+        strides[0] = static_cast<cuuint64_t>(ld) * 4;
+    } else if (!padded) {
+        dims[0] = static_cast<cuuint64_t>(N);
+        dims[1] = static_cast<cuuint64_t>(M);
+        strides[0] = static_cast<cuuint64_t>(ld) * 4;
+    } else {
+        const int pix = wo * ho;
+        if (pix <= 0 || M % pix != 0) return false;
+        rank = 4;
+        if (wo >= 32) {
+            if (wo % 32 != 0) return false;
+            box[1] = 32;
+        } else if (32 % wo != 0) {
+            return false;
+        } else if (pix >= 32) {
+            if (pix % 32 != 0) return false;
+            box[1] = wo;
+            box[2] = 32 / wo;
+        } else {
+            if (32 % pix != 0) return false;
+            box[1] = wo;
+            box[2] = ho;
+            box[3] = 32 / pix;
+        }
+        dims[0] = static_cast<cuuint64_t>(N);
+        dims[1] = static_cast<cuuint64_t>(wo);
+        dims[2] = static_cast<cuuint64_t>(ho);
+        dims[3] = static_cast<cuuint64_t>(M / pix);
+        strides[0] = static_cast<cuuint64_t>(ld) * 4;
+        strides[1] = static_cast<cuuint64_t>(wp) * ld * 4;
+        strides[2] = static_cast<cuuint64_t>(hp) * wp * ld * 4;
+        base_off += (static_cast<long long>(pad) * wp + pad) * ld;
+        ts->wo = wo;
+        ts->pix = pix;
+    }
+    ts->rank = static_cast<int>(rank);
+    for (int d = 0; d < nd; ++d) {
+        CUresult r = enc(&ts->map[d], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, ptrs[d] + base_off, dims, strides, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return false;
+    }
+    ts->n = nd;
+    return true;
+}
+
 namespace {
 
 template <bool A_MN, bool B_MN, int BN, int CG>
@@ -526,7 +654,7 @@ cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<A_MN, B_MN, BN, CG>, p.ta, p.tb, p.M, p.N, p.K, p.epi,
-                                       p.ga, p.gb, p.sk);
+                                       p.ga, p.gb, p.sk, p.ts);
     if (e != cudaSuccess || p.sk.splits <= 1) return e;
     const int R = p.sk.trans ? p.N : p.M, Cc = p.sk.trans ? p.M : p.N;
     const dim3 grid((Cc + 1023) / 1024, R < 65535 ? R : 65535);
@@ -558,6 +686,7 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
     p.epi = d.epi;
     p.epi.M = d.M;
     p.epi.N = d.N;
+    if (const char* e = getenv("PPB_GEMM_DBG")) p.epi.dbg = atoi(e);  // timing probes only
     if (d.K < 1) {
         snprintf(err, errlen, "GEMM with K=%d", d.K);
         return false;
@@ -641,6 +770,20 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
                                    : (bn == 128 ? TcCfg<128, 1>::kSmem : TcCfg<256, 1>::kSmem);
         if (p.sk.splits > 1 || base + need > 227 * 1024) p.epi.db_partial = nullptr;
         else p.db_smem = need;
+    }
+    if (p.sk.splits == 1 && tma_store_setup(p.epi, d.M, d.N, nullptr, &p.ts)) {
+        const int base = bn == 64 ? TcCfg<64, 1>::kSmem
+                         : cg == 2 ? (bn == 128 ? TcCfg<128, 2>::kSmem : TcCfg<256, 2>::kSmem)
+                                   : (bn == 128 ? TcCfg<128, 1>::kSmem : TcCfg<256, 1>::kSmem);
+        // staging after the barrier block and the db rows, 1 KB aligned (SW128 boxes)
+        const int off = 1024 + (p.db_smem + 1023) / 1024 * 1024;
+        const int extra = off + kEpiStageBytes - 256;
+        if (base + extra <= 227 * 1024) {
+            p.ts.stage_off = off;
+            p.db_smem = extra;
+        } else {
+            p.ts.n = 0;
+        }
     }
     // A: M extent x K.  K-major: rows=M, cols=K, box {32, 128}.  MN-major:
     // stored K x M (rows=K, cols=M), box {32, 32}.  B rows per CTA = bn / cg.

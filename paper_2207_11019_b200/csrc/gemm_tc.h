@@ -7,6 +7,7 @@
 #include <functional>
 
 #include "gemm.h"
+#include "tma_epi.cuh"
 
 namespace ppb {
 
@@ -26,6 +27,7 @@ struct TcGemmPlan {
     int halo = 0;  // 1: conv_halo.cu kernel (hg describes the padded grid)
     int db_smem = 0;  // extra dynamic smem of the EPI_MERGE db accumulator
     HaloGeom hg;
+    TmaStore ts;  // TMA-store epilogue (ts.n == 0: register epilogue)
 };
 
 // ws_alloc (optional): allocates split-K workspace (floats) on the GEMM's

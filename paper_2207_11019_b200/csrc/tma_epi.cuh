@@ -1,0 +1,122 @@
+// TMA-store epilogue shared by the tcgen05 kernels (gemm_tc.cu, conv_halo.cu).
+//
+// The register epilogue stores each accumulator row from its own thread: a
+// warp's st.global.v4 touches 32 different rows (16 B each), so a 128 x 256
+// tile leaves an SM at a few B/clk and, on single-wave GEMMs, the store tail
+// is fully exposed (measured: 18 us of an 85 us 32768 x 256 x 2304 conv GEMM).
+// Here each epilogue warp finishes its 32 x 32 chunk in registers (bias,
+// ReLU, mask), writes it into a SWIZZLE_128B staging box in shared memory
+// (conflict-free: lane = row, 16 B chunk j at j ^ (row & 7)) and one lane
+// issues a bulk tensor store per destination; two staging buffers per warp
+// let the next chunk's tcgen05.ld overlap the previous store.
+//
+// Row geometries (TmaStore::rank):
+//   2: GEMM row r -> destination row r (plain matrices; the halo kernel's
+//      padded-position rows when the destination has the same padded grid)
+//   4: GEMM row r = output pixel (img, h, w) of an ho x wo grid -> padded NHWC
+//      [img][h + pad][w + pad] (the map's base already points at the interior)
+#pragma once
+
+#include <cuda.h>
+
+#include <cstdint>
+
+#include "gemm.h"
+#include "ptx.cuh"
+
+namespace ppb {
+
+constexpr int kEpiWarps = 8;                     // two warps per TMEM lane quarter (alternate column chunks)
+constexpr int kEpiStageBytes = kEpiWarps * 4096;  // one 32 rows x 128 B staging box per epilogue warp
+
+struct TmaStore {
+    CUtensorMap map[kMaxDst];
+    int n = 0;     // destinations; 0 = register epilogue
+    int rank = 2;  // 2 or 4 (see above)
+    int wo = 1, pix = 1;
+    int stage_off = 0;  // staging offset (bytes) past the kernel's barrier block
+};
+
+// Host: encode the destination maps for an epilogue, or leave ts->n = 0 (the
+// register epilogue) when the mode / geometry / alignment does not qualify.
+// hg != nullptr: the halo kernel (rows are padded positions of hg's grid).
+bool tma_store_setup(const EpiParams& e, int M, int N, const HaloGeom* hg, TmaStore* ts);
+
+// Named barrier over the epilogue warps only (id 1).
+__device__ __forceinline__ void epi_bar_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+}
+
+// Registers -> swizzled staging box -> bulk tensor store(s).  All 32 lanes
+// call it; lane 0 owns the bulk async-group state.  The warp's next chunk
+// (tcgen05.ld, transform) overlaps the store's smem read.
+__device__ __forceinline__ void tma_store_chunk(const TmaStore& ts, uint8_t* buf, int lane, const float (&v)[32],
+                                                int r0, int n) {
+    if (lane == 0) bulk_wait_read<0>();  // the previous store has read the box
+    __syncwarp();
+    const uint32_t row = smem_u32(buf) + lane * 128;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        st_shared_v4(row + ((j ^ (lane & 7)) << 4), v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+        if (ts.rank == 2) {
+            for (int d = 0; d < ts.n; ++d) tma_store_2d(&ts.map[d], buf, n, r0);
+        } else {
+            const int img = r0 / ts.pix, rem = r0 - img * ts.pix;
+            const int h = rem / ts.wo, w = rem - h * ts.wo;
+            for (int d = 0; d < ts.n; ++d) tma_store_4d(&ts.map[d], buf, n, w, h, img);
+        }
+        bulk_commit();
+    }
+}
+
+// The epilogue's value transform without its stores (the TMA path stores).
+// EPI_STORE: bias + ReLU.  EPI_MERGE with pool 1 / EPI_MASK: ReLU mask.
+// Warp-uniform call (all lanes, any m): the bias row is loaded once per warp
+// (lane L holds bias[n0 + L]) and broadcast with shuffles.
+__device__ __forceinline__ void epi_values32(const EpiParams& p, int m, int n0, float (&acc)[32], int lane) {
+    if (n0 >= p.N) return;
+    if (p.mode == EPI_STORE) {
+        if (p.bias != nullptr) {
+            const float bl = n0 + lane < p.N ? __ldg(p.bias + n0 + lane) : 0.f;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc[i] += __shfl_sync(0xffffffffu, bl, i);
+        }
+        if (m < 0 || m >= p.M) return;
+        if (p.relu) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc[i] = acc[i] > 0.f ? acc[i] : 0.f;
+        }
+    } else if (m < 0 || m >= p.M) {
+        return;
+    } else if (p.mode == EPI_MERGE) {
+        if (p.mg_mask != nullptr) {
+            const int hw = p.mg_hg * p.mg_wg;
+            const int img = m / hw, rem = m - img * hw, y = rem / p.mg_wg, x = rem - y * p.mg_wg;
+            const long long mrow = (static_cast<long long>(img) * p.mg_mhp + y + p.mg_mpad) * p.mg_mwp + x + p.mg_mpad;
+            const float* mp = p.mg_mask + mrow * p.mg_mld + p.mg_mcol0 + n0;
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+                const float4 t = __ldg(reinterpret_cast<const float4*>(mp + i));
+                acc[i] = t.x > 0.f ? acc[i] : 0.f;
+                acc[i + 1] = t.y > 0.f ? acc[i + 1] : 0.f;
+                acc[i + 2] = t.z > 0.f ? acc[i + 2] : 0.f;
+                acc[i + 3] = t.w > 0.f ? acc[i + 3] : 0.f;
+            }
+        }
+    } else if (p.mode == EPI_MASK) {
+        const float* mp = p.mask + static_cast<long long>(m) * p.ldm + p.mcol0 + n0;
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+            const float4 t = __ldg(reinterpret_cast<const float4*>(mp + i));
+            acc[i] = t.x > 0.f ? acc[i] : 0.f;
+            acc[i + 1] = t.y > 0.f ? acc[i + 1] : 0.f;
+            acc[i + 2] = t.z > 0.f ? acc[i + 2] : 0.f;
+            acc[i + 3] = t.w > 0.f ? acc[i + 3] : 0.f;
+        }
+    }
+}
+
+}  // namespace ppb
