@@ -242,7 +242,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
                 if (sk.splits > 1) {  // raw partial sums for splitk_epilogue_kernel
                     const int nn = n0 + c * 32;
-                    if (sk.trans) {  // [n][m]: for each column the warp's lanes write consecutive m
+                    if (ts.n) {
+                        if (!(epi.dbg & 2)) tma_store_partial(ts, stg + (warp - 4) * 4096, lane, v, m0 + q * 32, nn, split);
+                    } else if (sk.trans) {  // [n][m]: for each column the warp's lanes write consecutive m
                         float* col = sk.ws + split * sk.stride + m;
                         if (m < M) {
 #pragma unroll
@@ -296,63 +298,83 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-// Split-K reduction: C(m, n) = sum over splits in order 0, 1, 2, ...
-// (deterministic), then the GEMM's real epilogue.  The workspace is [m][n]
+// Split-K reduction + the GEMM's real epilogue.  The workspace is [m][n]
 // (pitch sk.ld), or [n][m] when sk.trans (the dW^T SGD epilogue, whose W[n][m]
-// writes coalesce along m).  Thread = 4 consecutive workspace columns of one
-// workspace row; 32-bit index math; float4 loads.
-__global__ void __launch_bounds__(256) splitk_epilogue_kernel(const __grid_constant__ EpiParams epi,
-                                                              const __grid_constant__ SplitK sk, int M, int N) {
+// writes coalesce along m).  Work item = one workspace row x 4 consecutive
+// columns.  PHASES = 1: a thread sums every split of its item in order.
+// PHASES = 8 (many splits, e.g. the 148-way wgrad of VGG conv1): phase y sums
+// splits y, y+8, ... in order, then phase 0 adds the 8 phase sums in order
+// (a fixed tree: deterministic).
+template <int PHASES>
+__global__ void __launch_bounds__(256) splitk_epilogue_kernel(
+    const __grid_constant__ EpiParams epi, const __grid_constant__ SplitK sk, int M, int N) {
+    constexpr int kItems = 256 / PHASES;
+    __shared__ float4 part[PHASES][kItems];
     const int R = sk.trans ? N : M;
     const int Cc = sk.trans ? M : N;
-    const int c4 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
-    if (c4 >= Cc) return;
+    const int cq = (Cc + 3) / 4;
+    const long long item = static_cast<long long>(blockIdx.x) * kItems + threadIdx.x;
+    const bool live = item < static_cast<long long>(R) * cq;
+    const int r = live ? static_cast<int>(item / cq) : 0;
+    const int c4 = live ? static_cast<int>(item - static_cast<long long>(r) * cq) * 4 : 0;
     const int nc = Cc - c4 < 4 ? Cc - c4 : 4;
     const bool vec = nc == 4 && (sk.ld & 3) == 0;
-    const float alpha = epi.mode == EPI_SGD ? static_cast<float>(*epi.alpha) : 0.f;
-    for (int r = blockIdx.y; r < R; r += gridDim.y) {
-        const long long off = static_cast<long long>(r) * sk.ld + c4;
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int s0 = 0; s0 < sk.splits; s0 += 4) {
-            float v[4][4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const float* src = sk.ws + static_cast<long long>(s0 + i) * sk.stride + off;
-                if (s0 + i >= sk.splits) {
-                    v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0.f;
-                } else if (vec) {
-                    const float4 t = __ldg(reinterpret_cast<const float4*>(src));
-                    v[i][0] = t.x; v[i][1] = t.y; v[i][2] = t.z; v[i][3] = t.w;
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) v[i][j] = j < nc ? __ldg(src + j) : 0.f;
-                }
+    const long long off = static_cast<long long>(r) * sk.ld + c4;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (live) {
+#pragma unroll 4
+        for (int sp = threadIdx.y; sp < sk.splits; sp += PHASES) {
+            const float* src = sk.ws + static_cast<long long>(sp) * sk.stride + off;
+            float4 t;
+            if (vec) {
+                t = __ldcg(reinterpret_cast<const float4*>(src));
+            } else {
+                t.x = __ldcg(src);
+                t.y = nc > 1 ? __ldcg(src + 1) : 0.f;
+                t.z = nc > 2 ? __ldcg(src + 2) : 0.f;
+                t.w = nc > 3 ? __ldcg(src + 3) : 0.f;
             }
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-                if (s0 + i < sk.splits)
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) acc[j] += v[i][j];
+            acc.x += t.x;
+            acc.y += t.y;
+            acc.z += t.z;
+            acc.w += t.w;
         }
-        if (sk.trans) {  // EPI_SGD on dW^T: row r = n, columns = m
-            float* w = epi.W + static_cast<long long>(r) * epi.ldw + c4;
-            bool bad = false;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (j < nc) {
-                    const float g = acc[j] * epi.inv_b;
-                    bad |= !isfinite(g);
-                    w[j] -= alpha * g;
-                }
-            }
-            if (bad && epi.flag != nullptr) atomicOr(epi.flag, 1);
-            continue;
-        }
-        const long long row_off = epi.mode == EPI_STORE ? epi_store_row(epi, r) : 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (j < nc) epilogue1(epi, r, c4 + j, acc[j], row_off);
     }
+    float a[4] = {acc.x, acc.y, acc.z, acc.w};
+    if (PHASES > 1) {
+        part[threadIdx.y][threadIdx.x] = acc;
+        __syncthreads();
+        if (threadIdx.y != 0) return;
+        a[0] = a[1] = a[2] = a[3] = 0.f;
+#pragma unroll
+        for (int y = 0; y < PHASES; ++y) {
+            const float4 t = part[y][threadIdx.x];
+            a[0] += t.x;
+            a[1] += t.y;
+            a[2] += t.z;
+            a[3] += t.w;
+        }
+    }
+    if (!live) return;
+    if (sk.trans) {  // EPI_SGD on dW^T: row r = n, columns = m
+        const float alpha = static_cast<float>(*epi.alpha);
+        float* w = epi.W + static_cast<long long>(r) * epi.ldw + c4;
+        bool bad = false;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (j < nc) {
+                const float g = a[j] * epi.inv_b;
+                bad |= !isfinite(g);
+                w[j] -= alpha * g;
+            }
+        }
+        if (bad && epi.flag != nullptr) atomicOr(epi.flag, 1);
+        return;
+    }
+    const long long row_off = epi.mode == EPI_STORE ? epi_store_row(epi, r) : 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (j < nc) epilogue1(epi, r, c4 + j, a[j], row_off);
 }
 
 // ---------------------------------------------------------------- host side
@@ -571,6 +593,33 @@ bool tma_store_setup(const EpiParams& e, int M, int N, const HaloGeom* hg, TmaSt
     return true;
 }
 
+bool tma_store_setup_splitk(const SplitK& sk, int M, int N, TmaStore* ts) {
+    ts->n = 0;
+    static const bool off = [] {
+        const char* v = getenv("PPB_NO_TMA_STORE");
+        return v != nullptr && *v != '\0' && *v != '0';
+    }();
+    auto enc = get_encode();
+    static const bool off_sk = getenv("PPB_NO_TMA_SPLITK") != nullptr;
+    if (off || off_sk || enc == nullptr || sk.splits < 2 || sk.ws == nullptr) return false;
+    const int inner = sk.trans ? M : N, outer = sk.trans ? N : M;
+    if (inner < 32 || sk.ld % 4 != 0 || sk.stride % 4 != 0 || (reinterpret_cast<uintptr_t>(sk.ws) & 15u) != 0)
+        return false;
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer),
+                          static_cast<cuuint64_t>(sk.splits)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(sk.ld) * 4, static_cast<cuuint64_t>(sk.stride) * 4};
+    cuuint32_t box[3] = {32u, 32u, 1u};
+    cuuint32_t estr[3] = {1u, 1u, 1u};
+    if (enc(&ts->map[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, sk.ws, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    ts->rank = 3;
+    ts->tr = sk.trans;
+    ts->n = 1;
+    return true;
+}
+
 namespace {
 
 template <bool A_MN, bool B_MN, int BN, int CG>
@@ -656,9 +705,13 @@ cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
     cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<A_MN, B_MN, BN, CG>, p.ta, p.tb, p.M, p.N, p.K, p.epi,
                                        p.ga, p.gb, p.sk, p.ts);
     if (e != cudaSuccess || p.sk.splits <= 1) return e;
-    const int R = p.sk.trans ? p.N : p.M, Cc = p.sk.trans ? p.M : p.N;
-    const dim3 grid((Cc + 1023) / 1024, R < 65535 ? R : 65535);
-    splitk_epilogue_kernel<<<grid, 256, 0, s>>>(p.epi, p.sk, p.M, p.N);
+    const long long R = p.sk.trans ? p.N : p.M, Cc = p.sk.trans ? p.M : p.N;
+    const long long items = R * ((Cc + 3) / 4);
+    if (p.sk.splits >= 16)
+        splitk_epilogue_kernel<8><<<static_cast<unsigned>((items + 31) / 32), dim3(32, 8), 0, s>>>(p.epi, p.sk, p.M, p.N);
+    else
+        splitk_epilogue_kernel<1><<<static_cast<unsigned>((items + 255) / 256), dim3(256, 1), 0, s>>>(p.epi, p.sk, p.M,
+                                                                                                     p.N);
     return cudaGetLastError();
 }
 
@@ -771,7 +824,8 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
         if (p.sk.splits > 1 || base + need > 227 * 1024) p.epi.db_partial = nullptr;
         else p.db_smem = need;
     }
-    if (p.sk.splits == 1 && tma_store_setup(p.epi, d.M, d.N, nullptr, &p.ts)) {
+    if (p.sk.splits == 1 ? tma_store_setup(p.epi, d.M, d.N, nullptr, &p.ts)
+                         : tma_store_setup_splitk(p.sk, d.M, d.N, &p.ts)) {
         const int base = bn == 64 ? TcCfg<64, 1>::kSmem
                          : cg == 2 ? (bn == 128 ? TcCfg<128, 2>::kSmem : TcCfg<256, 2>::kSmem)
                                    : (bn == 128 ? TcCfg<128, 1>::kSmem : TcCfg<256, 1>::kSmem);

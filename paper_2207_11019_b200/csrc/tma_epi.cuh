@@ -35,7 +35,12 @@ struct TmaStore {
     int rank = 2;  // 2 or 4 (see above)
     int wo = 1, pix = 1;
     int stage_off = 0;  // staging offset (bytes) past the kernel's barrier block
+    int tr = 0;         // rank 3 (split-K workspace [split][rows][ld]): 1 = [n][m] (dW^T)
 };
+
+// Host: split-K partial sums through the same staging path: a rank-3 map over
+// the workspace ([split][M][ld], or [split][N][ld] transposed).
+bool tma_store_setup_splitk(const SplitK& sk, int M, int N, TmaStore* ts);
 
 // Host: encode the destination maps for an epilogue, or leave ts->n = 0 (the
 // register epilogue) when the mode / geometry / alignment does not qualify.
@@ -45,6 +50,32 @@ bool tma_store_setup(const EpiParams& e, int M, int N, const HaloGeom* hg, TmaSt
 // Named barrier over the epilogue warps only (id 1).
 __device__ __forceinline__ void epi_bar_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+}
+
+// Split-K partial chunk: C(r0 + lane, n .. n + 31) of split `split` into the
+// workspace (transposed boxes for the [n][m] layout).
+__device__ __forceinline__ void tma_store_partial(const TmaStore& ts, uint8_t* buf, int lane, const float (&v)[32],
+                                                  int r0, int n, int split) {
+    if (lane == 0) bulk_wait_read<0>();
+    __syncwarp();
+    const uint32_t base = smem_u32(buf);
+    if (ts.tr) {  // box row = column n + i, 32 consecutive m across the lanes
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            st_shared_f32(base + i * 128 + ((((lane >> 2) ^ (i & 7)) << 4) | ((lane & 3) << 2)), v[i]);
+    } else {
+        const uint32_t row = base + lane * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            st_shared_v4(row + ((j ^ (lane & 7)) << 4), v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+        if (ts.tr) tma_store_3d(&ts.map[0], buf, r0, n, split);
+        else tma_store_3d(&ts.map[0], buf, n, r0, split);
+        bulk_commit();
+    }
 }
 
 // Registers -> swizzled staging box -> bulk tensor store(s).  All 32 lanes
