@@ -14,10 +14,22 @@ __device__ __forceinline__ bool aligned16(const void* p) {
     return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
 }
 
+__device__ __forceinline__ void st_global_v8(float* p, float a, float b, float c, float d, float e, float f, float g,
+                                             float h) {
+    asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(a), "f"(b), "f"(c),
+                 "f"(d), "f"(e), "f"(f), "f"(g), "f"(h)
+                 : "memory");
+}
+
 __device__ __forceinline__ void store_row32(float* row, int n0, int nvalid, const float (&v)[32]) {
     // row points at column 0 of the destination row; n0 is a multiple of 32.
     float* p = row + n0;
-    if (nvalid >= 32 && aligned16(p)) {
+    if (nvalid >= 32 && (reinterpret_cast<uintptr_t>(p) & 31u) == 0) {
+        // 256-bit stores: each lane writes whole 32 B sectors
+#pragma unroll
+        for (int i = 0; i < 32; i += 8)
+            st_global_v8(p + i, v[i], v[i + 1], v[i + 2], v[i + 3], v[i + 4], v[i + 5], v[i + 6], v[i + 7]);
+    } else if (nvalid >= 32 && aligned16(p)) {
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
             *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);

@@ -145,6 +145,11 @@ struct SplitK {
     long long ld = 0;
     long long stride = 0;
     int trans = 0;  // workspace stored [n][m] (EPI_SGD with sgd_t)
+    // optional bias job folded into the reduction launch (wgrad + SGD only):
+    // bias[c] -= alpha * inv_b * sum_k bpart[k][c], k in [0, bchunks), c < bu
+    const float* bpart = nullptr;
+    float* bias = nullptr;
+    int bchunks = 0, bu = 0;
 };
 
 // Padded-position geometry of the halo conv kernel (conv_halo.cu): GEMM row

@@ -310,6 +310,28 @@ __global__ void __launch_bounds__(256) splitk_epilogue_kernel(
     const __grid_constant__ EpiParams epi, const __grid_constant__ SplitK sk, int M, int N) {
     constexpr int kItems = 256 / PHASES;
     __shared__ float4 part[PHASES][kItems];
+    const int bblocks = sk.bias != nullptr ? (sk.bu + 31) / 32 : 0;
+    if (static_cast<int>(blockIdx.x) >= static_cast<int>(gridDim.x) - bblocks) {
+        // bias job: column = t % 32, phase y = t / 32 sums chunks y, y+8, ...
+        // in order; phase sums added in order 0..7 (deterministic)
+        __shared__ float bsh[8][33];
+        const int t = threadIdx.y * blockDim.x + threadIdx.x;
+        const int col = (blockIdx.x - (gridDim.x - bblocks)) * 32 + (t & 31), y = t >> 5;
+        float acc = 0.f;
+        if (col < sk.bu) {
+#pragma unroll 4
+            for (int k = y; k < sk.bchunks; k += 8) acc += __ldcg(sk.bpart + static_cast<long long>(k) * sk.bu + col);
+        }
+        bsh[y][t & 31] = acc;
+        __syncthreads();
+        if (y == 0 && col < sk.bu) {
+            float g = 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) g += bsh[j][t & 31];
+            sk.bias[col] -= static_cast<float>(*epi.alpha) * (g * epi.inv_b);
+        }
+        return;
+    }
     const int R = sk.trans ? N : M;
     const int Cc = sk.trans ? M : N;
     const int cq = (Cc + 3) / 4;
@@ -707,11 +729,13 @@ cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
     if (e != cudaSuccess || p.sk.splits <= 1) return e;
     const long long R = p.sk.trans ? p.N : p.M, Cc = p.sk.trans ? p.M : p.N;
     const long long items = R * ((Cc + 3) / 4);
+    const unsigned bblocks = p.sk.bias != nullptr ? static_cast<unsigned>((p.sk.bu + 31) / 32) : 0u;
     if (p.sk.splits >= 16)
-        splitk_epilogue_kernel<8><<<static_cast<unsigned>((items + 31) / 32), dim3(32, 8), 0, s>>>(p.epi, p.sk, p.M, p.N);
+        splitk_epilogue_kernel<8><<<static_cast<unsigned>((items + 31) / 32) + bblocks, dim3(32, 8), 0, s>>>(
+            p.epi, p.sk, p.M, p.N);
     else
-        splitk_epilogue_kernel<1><<<static_cast<unsigned>((items + 255) / 256), dim3(256, 1), 0, s>>>(p.epi, p.sk, p.M,
-                                                                                                     p.N);
+        splitk_epilogue_kernel<1><<<static_cast<unsigned>((items + 255) / 256) + bblocks, dim3(256, 1), 0, s>>>(
+            p.epi, p.sk, p.M, p.N);
     return cudaGetLastError();
 }
 

@@ -469,6 +469,16 @@ void Session::alloc_buffers() {
 
 int Session::add_op(int gpu, cudaStream_t s, std::function<cudaError_t()> f, std::vector<int> deps,
                     int kernels, int kind, double flops) {
+    // timing probes only (wrong results): PPB_PROBE_SKIP = bitmask of op kinds
+    // whose launches are dropped from the step (dependencies are kept)
+    static const unsigned skip = [] {
+        const char* e = getenv("PPB_PROBE_SKIP");
+        return e != nullptr ? static_cast<unsigned>(strtoul(e, nullptr, 0)) : 0u;
+    }();
+    if (kind > 0 && (skip >> kind) & 1u) {
+        f = nullptr;
+        kernels = 0;
+    }
     Op op;
     op.kind = kind;
     op.flops = flops;
@@ -498,6 +508,8 @@ void Session::build_ops() {
         if (tf32) return [p, s]() { return tc_gemm_launch(*p, s); };
         return [d, s]() { return simt_gemm_launch(*d, s); };
     };
+    // kernels per GEMM launch (the split-K reduction is a second kernel)
+    auto nk = [tf32](const TcGemmPlan& p) { return tf32 && p.sk.splits > 1 ? 2 : 1; };
     auto prepare = [&](GemmDesc& d, TcGemmPlan& p, int gpu) {
         if (!tf32) return;
         char err[256];
@@ -616,7 +628,7 @@ void Session::build_ops() {
                     }
                     prepare(d, wl.p_fwd[j], w.gpu);
                     const double fl = 2.0 * rows * pix * wl.u * li.ksz * li.ksz * li.in_units;
-                    int op = add_op(w.gpu, w.sf, gemm_launch(&wl.p_fwd[j], &wl.d_fwd[j], w.sf), deps, 1, OP_FWD_GEMM, fl);
+                    int op = add_op(w.gpu, w.sf, gemm_launch(&wl.p_fwd[j], &wl.d_fwd[j], w.sf), deps, nk(wl.p_fwd[j]), OP_FWD_GEMM, fl);
                     if (wl.U != nullptr) {
                         ActLayout out = lay_[l];
                         out.col0 = wl.lo;
@@ -651,7 +663,7 @@ void Session::build_ops() {
                     d.epi.dst[d.epi.ndst++] = base + off * d.epi.ldd;
                 }
                 prepare(d, wl.p_fwd[j], w.gpu);
-                const int op = add_op(w.gpu, w.sf, gemm_launch(&wl.p_fwd[j], &wl.d_fwd[j], w.sf), deps, 1,
+                const int op = add_op(w.gpu, w.sf, gemm_launch(&wl.p_fwd[j], &wl.d_fwd[j], w.sf), deps, nk(wl.p_fwd[j]),
                                       OP_FWD_GEMM, 2.0 * rows * wl.u * fi);
                 wl.fwd_op[j] = op;
                 produced.push_back(op);
@@ -780,7 +792,7 @@ void Session::build_ops() {
                     if (!tf32 || wl.p_dgrad[j].epi.db_partial == nullptr) dl.db_colsum = true;
                     const double fl = 2.0 * rows * li.H * li.W * li.in_units * li.ksz * li.ksz * wl.u;
                     const int op = add_op(w.gpu, w.sb, gemm_launch(&wl.p_dgrad[j], &wl.d_dgrad[j], w.sb),
-                                          wl.delta_ready[j], 1, OP_DGRAD_GEMM, fl);
+                                          wl.delta_ready[j], nk(wl.p_dgrad[j]), OP_DGRAD_GEMM, fl);
                     wl.dgrad_op[j] = op;
                     w.last_bwd[j] = std::max(w.last_bwd[j], op);
                     dl.merge_fused = true;
@@ -828,7 +840,7 @@ void Session::build_ops() {
                     }
                     prepare(d, wl.p_dgrad[j], w.gpu);
                     const int op = add_op(w.gpu, w.sb, gemm_launch(&wl.p_dgrad[j], &wl.d_dgrad[j], w.sb),
-                                          wl.delta_ready[j], 1, OP_DGRAD_GEMM, fl);
+                                          wl.delta_ready[j], nk(wl.p_dgrad[j]), OP_DGRAD_GEMM, fl);
                     wl.dgrad_op[j] = op;
                     w.last_bwd[j] = std::max(w.last_bwd[j], op);
                     dgrad_ops.push_back(op);
@@ -901,7 +913,7 @@ void Session::build_ops() {
                 }
                 prepare(d, wl.p_dgrad[j], w.gpu);
                 const int op = add_op(w.gpu, w.sb, gemm_launch(&wl.p_dgrad[j], &wl.d_dgrad[j], w.sb),
-                                      wl.delta_ready[j], 1, OP_DGRAD_GEMM, 2.0 * rows * wl.u * fi);
+                                      wl.delta_ready[j], nk(wl.p_dgrad[j]), OP_DGRAD_GEMM, 2.0 * rows * wl.u * fi);
                 wl.dgrad_op[j] = op;
                 w.last_bwd[j] = std::max(w.last_bwd[j], op);
                 dgrad_ops.push_back(op);
@@ -1025,11 +1037,21 @@ void Session::build_ops() {
             // conv: db partials came with the merges (conv_merge or the EPI_MERGE epilogue)
             const bool from_merge = li.kind == 1 && !wl.db_colsum;
             const int chunks = cfg_.m * conv_merge_blocks();
+            const int splits = tf32 ? wl.p_wgrad.sk.splits : 1;
+            if (from_merge && splits > 1) {
+                // the bias update rides in the wgrad's split-K reduction launch
+                wl.p_wgrad.sk.bpart = partial;
+                wl.p_wgrad.sk.bias = bias;
+                wl.p_wgrad.sk.bchunks = chunks;
+                wl.p_wgrad.sk.bu = u;
+                add_op(w.gpu, s, gemm_launch(&wl.p_wgrad, &wl.d_wgrad, s), deps, 2, OP_WGRAD_GEMM, wfl);
+                continue;
+            }
             const int bop = add_op(w.gpu, s, [=]() {
                 if (from_merge) return launch_bias_from_partials(partial, chunks, u, bias, alpha, inv_b, s);
                 return launch_bias_update(delta, ldd, b, u, partial, bias, alpha, inv_b, s);
             }, deps, from_merge ? 1 : 2, OP_BIAS);
-            add_op(w.gpu, s, gemm_launch(&wl.p_wgrad, &wl.d_wgrad, s), {bop}, 1, OP_WGRAD_GEMM, wfl);
+            add_op(w.gpu, s, gemm_launch(&wl.p_wgrad, &wl.d_wgrad, s), {bop}, splits > 1 ? 2 : 1, OP_WGRAD_GEMM, wfl);
         }
     }
 
