@@ -222,8 +222,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int i = lane; i < ldb; i += 32) db_row[i] = 0.f;
             epi_bar_sync();
         }
+        // >= 2 tiles per CTA: the two warp groups take alternate tiles (two
+        // tiles' epilogues in flight, each on its own TMEM accumulator);
+        // otherwise they split the tile's column chunks
+        const bool by_tile = num_tiles >= 2 * units;
+        const int c_first = by_tile ? 0 : half, c_step = by_tile ? 1 : 2;
         int local = 0;
         for (int tile = unit; tile < num_tiles; tile += units, ++local) {
+            if (by_tile && (local & 1) != half) continue;
             const int mn = tile % num_mn, split = tile / num_mn;
             const int m0 = (mn % num_m) * TM + static_cast<int>(rank) * kBM;
             const int n0 = (mn / num_m) * BN;
@@ -233,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const int m = m0 + q * 32 + lane;
 #pragma unroll 1
-            for (int c = half; c < ((epi.dbg & 4) ? 0 : BN / 32); c += 2) {  // dbg 4: timing probe, no epilogue
+            for (int c = c_first; c < ((epi.dbg & 4) ? 0 : BN / 32); c += c_step) {  // dbg 4: timing probe, no epilogue
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, r);
                 tmem_ld_wait();
@@ -274,8 +280,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                if (CG == 2) mbar_arrive_cluster(tempty_leader + acc * sizeof(uint64_t));
-                else mbar_arrive(&tempty_bar[acc]);
+                const uint32_t cnt = by_tile ? 2u : 1u;  // by_tile: 4 warps stand for all 8
+                if (CG == 2) mbar_arrive_cluster_n(tempty_leader + acc * sizeof(uint64_t), cnt);
+                else mbar_arrive_n(&tempty_bar[acc], cnt);
             }
         }
         if (db) {  // both warps of the quarter accumulated into db_row (disjoint columns)

@@ -335,7 +335,7 @@ void Session::alloc_buffers() {
             a.kind = 2;  // im2col rows [pixel][k*k*C]
             a.hp = c.Ho() * c.Wo();
             a.wp = 1;
-            a.ld = ld_of(c.ksz * c.ksz * c.in_units);
+            a.ld = (c.ksz * c.ksz * c.in_units + 31) / 32 * 32;  // 128 B rows: whole-line TMA fetches
         } else if (l < L && net_.info[l].kind == 1) {
             const LayerInfo& c = net_.info[l];
             a.kind = 0;
