@@ -62,3 +62,16 @@ def vgg16_cifar(seed=1, classes=10, widths=VGG16, hw=32, cin=3) -> TinyNet:
 def small_cnn(seed=1, hw=8, cin=3, widths=(16, "M", 32, "M"), classes=10) -> TinyNet:
     """A scaled-down VGG-style net for parity tests."""
     return vgg16_cifar(seed, classes, list(widths), hw, cin)
+
+
+def lenet5(seed=1, classes=10, hw=28, cin=1) -> TinyNet:
+    """BASELINE configs[1]: LeNet-5-style CNN on 28x28x1: C1 5x5x6 (pad 2, the
+    original's 32x32 input) + ReLU + 2x2 max-pool -> 14x14x6, C3 5x5x16
+    (valid) + ReLU + pool -> 5x5x16, F5 400 -> 120, F6 120 -> 84, output
+    84 -> classes (softmax).  The 28x28 / 10x10 grids do not tile into
+    128-pixel TMA boxes, so both convs run on the generic im2col path."""
+    rng = np.random.default_rng(seed)
+    layers = [_conv(rng, cin, 6, (hw, hw), 5, 2, 2), _conv(rng, 6, 16, (hw // 2, hw // 2), 5, 0, 2)]
+    s = (hw // 2 - 4) // 2
+    layers += [_dense(rng, 16 * s * s, 120, 1), _dense(rng, 120, 84, 1), _dense(rng, 84, classes, 2)]
+    return TinyNet(layers)

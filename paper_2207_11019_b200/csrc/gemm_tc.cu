@@ -555,6 +555,12 @@ bool tma_store_setup(const EpiParams& e, int M, int N, const HaloGeom* hg, TmaSt
             return false;
     }
     if (nd == 0 || ld % 4 != 0 || col0 % 4 != 0) return false;
+    // Shards of one layer store disjoint column ranges of the same rows
+    // concurrently; a bulk tensor store that shares a 32 B sector with another
+    // writer's range corrupts it (measured: LeNet 120 -> 60/60 shards), so the
+    // TMA path needs sector-aligned ranges unless this GEMM owns whole rows.
+    const bool whole_rows = col0 == 0 && (N + 3) / 4 * 4 == ld;
+    if (!whole_rows && (col0 % 8 != 0 || N % 8 != 0 || ld % 8 != 0)) return false;
     int dev = 0;
     cudaGetDevice(&dev);
     for (int d = 0; d < nd; ++d) {

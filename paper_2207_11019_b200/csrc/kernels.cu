@@ -334,6 +334,59 @@ __global__ void im2col_kernel(const T* __restrict__ src, int imgs, int H, int W,
     }
 }
 
+// Generic conv path (grids the TMA boxes cannot tile, e.g. LeNet's 28x28 /
+// 10x10): explicit im2col rows of a padded NHWC activation.  Column
+// (tap, c) of output pixel (img, y, x) = x_pad[img][y + r][x + s][c] (the
+// tensor's own zero ring is the conv padding); columns >= k*k*C are zero.
+__global__ void im2col_act_kernel(const float* __restrict__ x, int imgs, int hp, int wp, long long ldx, int C, int k,
+                                  int Ho, int Wo, float* __restrict__ dst, long long ldc) {
+    const int kc = k * k * C;
+    const long long total = static_cast<long long>(imgs) * Ho * Wo * ldc;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int col = static_cast<int>(i % ldc);
+        const long long pix = i / ldc;
+        float v = 0.f;
+        if (col < kc) {
+            const int c = col % C, tap = col / C, r = tap / k, s = tap % k;
+            const int wo = static_cast<int>(pix % Wo);
+            const int ho = static_cast<int>((pix / Wo) % Ho);
+            const long long n = pix / (static_cast<long long>(Wo) * Ho);
+            v = x[((n * hp + ho + r) * wp + wo + s) * ldx + c];
+        }
+        dst[i] = v;
+    }
+}
+
+// col2im of the partial input gradient: g(img, y, x, c) for the input grid
+// H x W = sum over taps (r, s) ascending of dcols[(img, y + p - r, x + p - s)]
+// [(r*k + s)*C + c] over valid output positions (fixed order: deterministic).
+// Channels [c0, c0 + nc) go to dst[(img*H + y)*W + x][c - c0] (a merge slot).
+__global__ void col2im_kernel(const float* __restrict__ dcols, long long ldk, int imgs, int H, int W, int C, int k,
+                              int p, int Ho, int Wo, int c0, int nc, float* __restrict__ dst, long long ldo) {
+    const long long total = static_cast<long long>(imgs) * H * W * nc;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int cc = static_cast<int>(i % nc);
+        const long long pix = i / nc;
+        const int x = static_cast<int>(pix % W);
+        const int y = static_cast<int>((pix / W) % H);
+        const long long n = pix / (static_cast<long long>(W) * H);
+        const int c = c0 + cc;
+        float g = 0.f;
+        for (int r = 0; r < k; ++r) {
+            const int oy = y + p - r;
+            if (oy < 0 || oy >= Ho) continue;
+            for (int s = 0; s < k; ++s) {
+                const int ox = x + p - s;
+                if (ox < 0 || ox >= Wo) continue;
+                g += dcols[((n * Ho + oy) * Wo + ox) * ldk + (r * k + s) * C + c];
+            }
+        }
+        dst[pix * ldo + cc] = g;
+    }
+}
+
 template <class T>
 __global__ void pad_input_kernel(const T* __restrict__ src, int imgs, int H, int W, int C, float* __restrict__ dst,
                                  int p, long long ld) {
@@ -676,6 +729,23 @@ cudaError_t launch_im2col_input(const double* src64, const float* src32, int img
     if (n <= 0) return cudaSuccess;
     if (src64) im2col_kernel<double><<<grid_for(n, 256), 256, 0, s>>>(src64, imgs, H, W, C, k, p, dst, ld);
     else im2col_kernel<float><<<grid_for(n, 256), 256, 0, s>>>(src32, imgs, H, W, C, k, p, dst, ld);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_im2col_act(const float* x, int imgs, int hp, int wp, long long ldx, int C, int k, int Ho, int Wo,
+                              float* dst, long long ldc, cudaStream_t s) {
+    const long long n = static_cast<long long>(imgs) * Ho * Wo * ldc;
+    if (n <= 0) return cudaSuccess;
+    im2col_act_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, imgs, hp, wp, ldx, C, k, Ho, Wo, dst, ldc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_col2im(const float* dcols, long long ldk, int imgs, int H, int W, int C, int k, int p, int c0,
+                          int nc, float* dst, long long ldo, cudaStream_t s) {
+    const long long n = static_cast<long long>(imgs) * H * W * nc;
+    if (n <= 0) return cudaSuccess;
+    const int Ho = H + 2 * p - k + 1, Wo = W + 2 * p - k + 1;
+    col2im_kernel<<<grid_for(n, 256), 256, 0, s>>>(dcols, ldk, imgs, H, W, C, k, p, Ho, Wo, c0, nc, dst, ldo);
     return cudaGetLastError();
 }
 

@@ -69,6 +69,14 @@ cudaError_t launch_pad_input(const double* src64, const float* src32, int imgs, 
 cudaError_t launch_im2col_input(const double* src64, const float* src32, int imgs, int H, int W, int C, int k,
                                 int p, float* dst, long long ld, cudaStream_t s);
 
+// Generic conv path: im2col rows of a padded NHWC activation (columns
+// (tap, c), zero beyond k*k*C) and the col2im of a partial input gradient into
+// a merge slot (channels [c0, c0 + nc)).  See kernels.cu.
+cudaError_t launch_im2col_act(const float* x, int imgs, int hp, int wp, long long ldx, int C, int k, int Ho, int Wo,
+                              float* dst, long long ldc, cudaStream_t s);
+cudaError_t launch_col2im(const float* dcols, long long ldk, int imgs, int H, int W, int C, int k, int p, int c0,
+                          int nc, float* dst, long long ldo, cudaStream_t s);
+
 // Layout of a conv layer's output as its consumer reads it.
 struct ActLayout {
     int kind = 0;        // 0 padded NHWC [img][hp][wp][ld] at channel col0 + c; 1 CHW-flatten rows [img][ld]

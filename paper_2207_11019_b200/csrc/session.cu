@@ -71,6 +71,10 @@ struct Session::WLayer {
     float* U = nullptr;                  // conv: pre-pool output of the shard [b*Ho*Wo x ldu]
     long long ldu = 0;
     unsigned char* argmax = nullptr;     // conv with pool: [b*Hq*Wq x u]
+    float* cols = nullptr;               // generic conv: im2col rows of the input [b*Ho*Wo x ldc]
+    long long ldc = 0;
+    float* dcols = nullptr;              // generic conv: dgrad partial in column space [b*Ho*Wo x ldk]
+    long long ldk = 0;
     bool merge_fused = false;            // conv: delta written by the dgrad epilogue (EPI_MERGE)
     bool db_colsum = false;              // fused merge without in-epilogue bias partials: column-sum pass
     std::vector<std::vector<int>> delta_ready;  // [j] -> op ids that produce delta rows of micro-batch j
@@ -131,7 +135,7 @@ Session::Session(const std::vector<int>& device_map, const NetDesc& net, const d
     if (static_cast<int>(net_.info.size()) != L) throw std::invalid_argument("layer description count mismatch");
     net_.dims.assign(1, static_cast<int>(net_.info[0].in_features()));
     for (int l = 0; l < L; ++l) {
-        const LayerInfo& li = net_.info[l];
+        LayerInfo& li = net_.info[l];
         net_.acts[l] = li.act;
         net_.dims.push_back(static_cast<int>(li.out_features()));
         if (li.in_units < 1 || li.out_units < 1)
@@ -148,8 +152,13 @@ Session::Session(const std::vector<int>& device_map, const NetDesc& net, const d
             cs.ksz = li.ksz;
             cs.pad = li.pad;
             cs.u = li.out_units;
-            if (!conv_implicit_ok(cs))
-                throw std::invalid_argument("layer " + S(l + 1) + ": conv grid does not tile into 128/32-pixel TMA boxes");
+            if (!conv_implicit_ok(cs)) {
+                // generic path: explicit im2col rows + dense GEMMs (layer 1: the
+                // staged im2col of X), unpadded error signal
+                if (l == 0) li.im2col = true;
+                else li.generic = true;
+                li.dense_delta = true;
+            }
             if (l == L - 1) throw std::invalid_argument("the last layer must be dense (classifier head)");
             if (cfg_.precision == 1)
                 throw std::invalid_argument("fp32 precision mode supports dense layers only (conv runs on tcgen05)");
@@ -395,7 +404,7 @@ void Session::alloc_buffers() {
             wl.bias = static_cast<float*>(g.alloc(sizeof(float) * wl.u));
             wl.ldd = ld_of(wl.u);
             if (li.kind == 1) {
-                const int q = li.ksz - 1 - li.pad;
+                const int q = li.dq();
                 wl.delta_img = static_cast<long long>(li.Ho() + 2 * q) * (li.Wo() + 2 * q) * wl.ldd;
                 const bool consumer_dense = wl.layer < L && net_.info[wl.layer].kind == 0;
                 if (li.pool == 2 || consumer_dense) {
@@ -404,6 +413,14 @@ void Session::alloc_buffers() {
                 }
                 if (li.pool == 2)
                     wl.argmax = static_cast<unsigned char*>(g.alloc(static_cast<size_t>(b) * li.Hq() * li.Wq() * wl.u));
+                if (li.generic) {
+                    const long long pix = static_cast<long long>(b) * li.Ho() * li.Wo();
+                    const int kc = li.ksz * li.ksz * li.in_units;
+                    wl.ldc = (kc + 31) / 32 * 32;
+                    wl.ldk = ld_of(kc);
+                    wl.cols = static_cast<float*>(g.alloc(sizeof(float) * pix * wl.ldc));
+                    wl.dcols = static_cast<float*>(g.alloc(sizeof(float) * pix * wl.ldk));
+                }
             } else {
                 wl.delta_img = wl.ldd;
             }
@@ -419,7 +436,7 @@ void Session::alloc_buffers() {
             for (int r = 0; r < wl.u; ++r) {
                 const double* src = Wl + static_cast<size_t>(wl.lo + r) * hc;
                 float* dst = tmp.data() + static_cast<size_t>(r) * wl.ldw;
-                if (li.kind == 1 && !li.im2col) {
+                if (li.kind == 1 && !li.im2col && !li.generic) {
                     for (int t = 0; t < li.ksz * li.ksz; ++t)
                         for (int c = 0; c < li.in_units; ++c)
                             dst[t * li.ck() + c] = static_cast<float>(src[t * li.in_units + c]);
@@ -594,7 +611,25 @@ void Session::build_ops() {
                     cs.ksz = li.ksz;
                     cs.pad = li.pad;
                     cs.u = wl.u;
-                    if (li.im2col) {  // dense GEMM over the im2col rows
+                    if (li.generic) {  // per-step im2col rows of the padded input, then a dense GEMM
+                        const ActLayout& a = lay_[l - 1];
+                        const float* x = act_buf(w.gpu, l - 1) + off * img_elems(l - 1);
+                        float* cols = wl.cols + off * li.Ho() * li.Wo() * wl.ldc;
+                        const int hp = a.hp, wp = a.wp, C = li.in_units, k = li.ksz, Ho = li.Ho(), Wo = li.Wo();
+                        const long long ldx = a.ld, ldc = wl.ldc;
+                        cudaStream_t st = w.sf;
+                        const int iop = add_op(w.gpu, st, [=]() {
+                            return launch_im2col_act(x, rows, hp, wp, ldx, C, k, Ho, Wo, cols, ldc, st);
+                        }, deps, 1, OP_POOL);
+                        deps = {iop};
+                        const int kc = k * k * C;
+                        d = GemmDesc{};
+                        d.a = Operand{cols, rows * Ho * Wo, kc, ldc, false};
+                        d.b = Operand{wl.W, wl.u, kc, wl.ldw, false};
+                        d.M = rows * Ho * Wo;
+                        d.N = wl.u;
+                        d.K = kc;
+                    } else if (li.im2col) {  // dense GEMM over the im2col rows
                         const int kc = li.ksz * li.ksz * li.in_units;
                         const int prow = rows * li.Ho() * li.Wo();
                         d = GemmDesc{};
@@ -746,7 +781,7 @@ void Session::build_ops() {
                 // destination sums them, routes through the pool argmax and
                 // masks by its ReLU into its padded error signal.
                 const int hw = lb.Hq() * lb.Wq();
-                if (li.kind == 1 && contrib.size() == 1 && dests.size() == 1 && fuse_merge_) {
+                if (li.kind == 1 && !li.generic && contrib.size() == 1 && dests.size() == 1 && fuse_merge_) {
                     // one contributor, one destination: the merge (pool routing,
                     // ReLU mask, padded store) runs in the dgrad epilogue
                     Worker& w = *workers_[contrib[0]];
@@ -779,7 +814,7 @@ void Session::build_ops() {
                         d.epi.mg_mpad = a.pad;
                         d.epi.mg_mcol0 = dl.lo;
                     }
-                    const int q = lb.ksz - 1 - lb.pad;
+                    const int q = lb.dq();
                     d.epi.mg_d = dl.delta + off * dl.delta_img;
                     d.epi.mg_dld = dl.ldd;
                     d.epi.mg_dhp = lb.Ho() + 2 * q;
@@ -806,6 +841,43 @@ void Session::build_ops() {
                     GemmDesc& d = wl.d_dgrad[j];
                     double fl;
                     long long rows_per_img;
+                    if (li.kind == 1 && li.generic) {
+                        // dcols = delta . W (column space), then col2im into each
+                        // destination's slot (its channel slice)
+                        const int kc = li.ksz * li.ksz * li.in_units;
+                        const long long pix = static_cast<long long>(li.Ho()) * li.Wo();
+                        d = GemmDesc{};
+                        d.a = Operand{wl.delta + off * wl.delta_img, static_cast<int>(rows * pix), wl.u, wl.ldd, false};
+                        d.b = Operand{wl.W, wl.u, kc, wl.ldw, true};
+                        d.M = static_cast<int>(rows * pix);
+                        d.N = kc;
+                        d.K = wl.u;
+                        d.epi = EpiParams{};
+                        d.epi.mode = EPI_STORE;
+                        d.epi.dst[d.epi.ndst++] = wl.dcols + off * pix * wl.ldk;
+                        d.epi.ldd = wl.ldk;
+                        prepare(d, wl.p_dgrad[j], w.gpu);
+                        fl = 2.0 * rows * li.H * li.W * li.in_units * li.ksz * li.ksz * wl.u;
+                        int op = add_op(w.gpu, w.sb, gemm_launch(&wl.p_dgrad[j], &wl.d_dgrad[j], w.sb), wl.delta_ready[j],
+                                        nk(wl.p_dgrad[j]), OP_DGRAD_GEMM, fl);
+                        wl.dgrad_op[j] = op;
+                        const float* dc = wl.dcols + off * pix * wl.ldk;
+                        const long long ldk = wl.ldk;
+                        const int H = li.H, W = li.W, C = li.in_units, ks = li.ksz, pd = li.pad;
+                        for (int di : dests) {
+                            WLayer& dl = workers_[di]->at(l - 1);
+                            float* dst = dl.slots[k] + off * H * W * dl.slot_ld;
+                            const long long ldo = dl.slot_ld;
+                            const int c0 = dl.lo, nc = dl.u;
+                            cudaStream_t st = w.sb;
+                            op = add_op(w.gpu, st, [=]() {
+                                return launch_col2im(dc, ldk, rows, H, W, C, ks, pd, c0, nc, dst, ldo, st);
+                            }, {op}, 1, OP_CONV_MERGE);
+                        }
+                        w.last_bwd[j] = std::max(w.last_bwd[j], op);
+                        dgrad_ops.push_back(op);
+                        continue;
+                    }
                     if (li.kind == 1) {
                         ConvShape cs;
                         cs.N = rows;
@@ -872,7 +944,7 @@ void Session::build_ops() {
                         }
                     }
                     cm.d_pad = dl.delta + off * dl.delta_img;
-                    cm.q = lb.ksz - 1 - lb.pad;
+                    cm.q = lb.dq();
                     cm.ldd = dl.ldd;
                     cudaStream_t st = dw.sb;
                     float* dbp = dl.partial + static_cast<long long>(j) * conv_merge_blocks() * dl.u;
@@ -989,7 +1061,22 @@ void Session::build_ops() {
                 cs.ksz = li.ksz;
                 cs.pad = li.pad;
                 cs.u = wl.u;
-                if (li.im2col) {  // B = im2col rows (pixel-major, MN = k*k*C)
+                if (li.dense_delta) {  // dense wgrad: K = output pixels, unpadded error signal x im2col rows
+                    const int kc = li.ksz * li.ksz * li.in_units;
+                    const int pix = cfg_.batch * li.Ho() * li.Wo();
+                    const float* colsp = li.generic ? wl.cols : act_buf(w.gpu, l - 1);
+                    const long long ldc = li.generic ? wl.ldc : lay_[l - 1].ld;
+                    d = GemmDesc{};
+                    d.a = Operand{wl.delta, pix, wl.u, wl.ldd, true};
+                    d.b = Operand{colsp, pix, kc, ldc, true};
+                    d.M = wl.u;
+                    d.N = kc;
+                    d.K = pix;
+                    if (wl.u < 128 && kc > wl.u) {  // dW^T: the wide side fills the 128-row tiles
+                        std::swap(d.a, d.b);
+                        std::swap(d.M, d.N);
+                    }
+                } else if (li.im2col) {  // B = im2col rows (pixel-major, MN = k*k*C)
                     d = conv_wgrad_desc(cs, wl.delta, wl.ldd, act_buf(w.gpu, l - 1), lay_[l - 1].ld, false);
                     const int kc = li.ksz * li.ksz * li.in_units;
                     d.b = Operand{act_buf(w.gpu, l - 1), cfg_.batch * li.Ho() * li.Wo(), kc, lay_[l - 1].ld, true};
@@ -1390,7 +1477,7 @@ void Session::get_net(double* W, double* b) {
             for (int r = 0; r < wl.u; ++r) {
                 double* dst = W + wo + static_cast<size_t>(wl.lo + r) * hc;
                 const float* src = tmp.data() + static_cast<size_t>(r) * wl.ldw;
-                if (li.kind == 1 && !li.im2col) {
+                if (li.kind == 1 && !li.im2col && !li.generic) {
                     for (int t = 0; t < li.ksz * li.ksz; ++t)
                         for (int c = 0; c < li.in_units; ++c) dst[t * li.in_units + c] = src[t * li.ck() + c];
                 } else {
@@ -1482,7 +1569,7 @@ size_t Session::read_tensor(int kind, int layer, int device, double* out, size_t
             if (w.device != device) continue;
             WLayer& wl = w.at(layer);
             if (li.kind == 0) return fetch(wl.delta, w.gpu, b, wl.u, wl.ldd);
-            const int q = li.ksz - 1 - li.pad, Ho = li.Ho(), Wo = li.Wo();
+            const int q = li.dq(), Ho = li.Ho(), Wo = li.Wo();
             const long long per = wl.delta_img;
             raw(wl.delta, w.gpu, static_cast<size_t>(b) * per);
             const size_t n = static_cast<size_t>(b) * Ho * Wo * wl.u;

@@ -35,6 +35,11 @@ struct LayerInfo {
     int act = 0;
     int H = 1, W = 1, ksz = 1, pad = 0, pool = 1;  // conv: input grid, kernel, padding, pool factor (1|2)
     bool im2col = false;  // first layer with few input channels: explicit im2col rows, dense GEMMs
+    // generic conv (grids the 128/32-pixel TMA boxes cannot tile): per-step
+    // im2col rows of the padded input, dense GEMMs, col2im of the dgrad partial
+    bool generic = false;
+    bool dense_delta = false;  // error signal stored unpadded [pixel][ldd] (dense wgrad operand)
+    int dq() const { return dense_delta ? 0 : ksz - 1 - pad; }  // zero ring of the stored error signal
     int Ho() const { return H + 2 * pad - ksz + 1; }
     int Wo() const { return W + 2 * pad - ksz + 1; }
     int Hq() const { return Ho() / pool; }
@@ -45,7 +50,7 @@ struct LayerInfo {
     int ck() const { return (in_units + 31) / 32 * 32; }
     int dev_wcols() const {
         if (!kind) return in_units;
-        return im2col ? (ksz * ksz * in_units + 3) / 4 * 4 : ksz * ksz * ck();
+        return im2col || generic ? (ksz * ksz * in_units + 3) / 4 * 4 : ksz * ksz * ck();
     }
 };
 
