@@ -254,6 +254,15 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         const int lane = threadIdx.x & 31;
         const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0;
         const int hpwp = hg.hp * hg.wp;
+        uint64_t* mbar = epi_mask_bar(stg, warp - 4);
+        uint32_t mphase = 0;
+        if (ts.n && ts.mask) {
+            if (lane == 0) {
+                mbar_init(mbar, 1);
+                fence_mbar_init();
+            }
+            __syncwarp();
+        }
         const bool db = epi.db_partial != nullptr;
         const int ldb = (N + 31) & ~31;
         float* db_row = db_s + q * ldb;
@@ -287,7 +296,10 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 float v[32];
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = m >= 0 ? __uint_as_float(rr[i]) : 0.f;
-                if (ts.n) {  // pad-ring rows store zeros (the destination's own ring)
+                if (ts.n && ts.mask) {  // the mask is zero on the ring
+                    tma_store_chunk_masked(ts, stg + (warp - 4) * 4096, mbar, mphase, lane, v,
+                                           static_cast<int>(p0) + q * 32, n0 + c * 32);
+                } else if (ts.n) {  // pad-ring rows store zeros (the destination's own ring)
                     epi_values32(epi, m, n0 + c * 32, v, lane);
                     if (m < 0) {
 #pragma unroll

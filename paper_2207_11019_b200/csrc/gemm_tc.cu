@@ -51,8 +51,6 @@ struct TcCfg {
     static constexpr int kStageBytes = kStageA + kStageB;
     static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
     static constexpr int kTmemCols = 2 * BN;
-    // dynamic smem: 1 KB alignment slack + stages + barriers
-    static constexpr int kSmem = 1024 + kStages * kStageBytes + 256;
 };
 
 template <bool A_MN, bool B_MN, int BN, int CG>
@@ -60,20 +58,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                    int M, int N, int K, const __grid_constant__ EpiParams epi,
                    const __grid_constant__ ConvGeom ga, const __grid_constant__ ConvGeom gb,
-                   const __grid_constant__ SplitK sk, const __grid_constant__ TmaStore ts) {
+                   const __grid_constant__ SplitK sk, const __grid_constant__ TmaStore ts, int nst) {
     using C = TcCfg<BN, CG>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
     uint8_t* sA = smem;
-    uint8_t* sB = smem + C::kStages * C::kStageA;
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
-    uint64_t* empty_bar = full_bar + C::kStages;
-    uint64_t* tfull_bar = empty_bar + C::kStages;   // [2]
+    uint8_t* sB = smem + nst * C::kStageA;  // nst <= C::kStages ring stages (host: smem budget)
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + nst * C::kStageBytes);
+    uint64_t* empty_bar = full_bar + nst;
+    uint64_t* tfull_bar = empty_bar + nst;   // [2]
     uint64_t* tempty_bar = tfull_bar + 2;            // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-    float* db_s = reinterpret_cast<float*>(smem + C::kStages * C::kStageBytes + 256);  // [4][ldb] (EPI_MERGE db)
-    uint8_t* stg = smem + C::kStages * C::kStageBytes + ts.stage_off;                  // TMA-store staging
+    float* db_s = reinterpret_cast<float*>(smem + nst * C::kStageBytes + 256);  // [4][ldb] (EPI_MERGE db)
+    uint8_t* stg = smem + nst * C::kStageBytes + ts.stage_off;                  // TMA-store staging
 
     const int warp = threadIdx.x / 32;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
@@ -90,7 +88,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 && elect_one()) {
         tma_prefetch(&ta);
         tma_prefetch(&tb);
-        for (int s = 0; s < C::kStages; ++s) {
+        for (int s = 0; s < nst; ++s) {
             mbar_init(&full_bar[s], 2);  // the A and the B producer each arrive (with their tx bytes)
             mbar_init(&empty_bar[s], 1);
         }
@@ -138,7 +136,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 cur.load(t, map, g, base + stage * stage_bytes, o);
                 cur.advance(g);
-                if (++stage == C::kStages) {
+                if (++stage == nst) {
                     stage = 0;
                     phase ^= 1;
                 }
@@ -196,7 +194,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         else mma_commit(&empty_bar[stage]);
                     }
                     __syncwarp();
-                    if (++stage == C::kStages) {
+                    if (++stage == nst) {
                         stage = 0;
                         phase ^= 1;
                     }
@@ -225,6 +223,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         // >= 2 tiles per CTA: the two warp groups take alternate tiles (two
         // tiles' epilogues in flight, each on its own TMEM accumulator);
         // otherwise they split the tile's column chunks
+        uint64_t* mbar = epi_mask_bar(stg, warp - 4);
+        uint32_t mphase = 0;
+        if (ts.n && ts.mask) {
+            if (lane == 0) {
+                mbar_init(mbar, 1);
+                fence_mbar_init();
+            }
+            __syncwarp();
+        }
         const bool by_tile = num_tiles >= 2 * units;
         const int c_first = by_tile ? 0 : half, c_step = by_tile ? 1 : 2;
         int local = 0;
@@ -262,7 +269,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     N - nn < 32 ? N - nn : 32, v);
                     }
                 } else {
-                    if (ts.n) {
+                    if (ts.n && ts.mask) {
+                        tma_store_chunk_masked(ts, stg + (warp - 4) * 4096, mbar, mphase, lane, v, m0 + q * 32,
+                                               n0 + c * 32);
+                    } else if (ts.n) {
                         epi_values32(epi, m, n0 + c * 32, v, lane);
                         if (!(epi.dbg & 2)) tma_store_chunk(ts, stg + (warp - 4) * 4096, lane, v, m0 + q * 32, n0 + c * 32);
                     } else if (!(epi.dbg & 2)) {
@@ -617,6 +627,33 @@ bool tma_store_setup(const EpiParams& e, int M, int N, const HaloGeom* hg, TmaSt
         ts->wo = wo;
         ts->pix = pix;
     }
+    // mask map (EPI_MERGE pool 1 / EPI_MASK): the activation at the same rows / columns
+    const float* mptr = nullptr;
+    long long mld = 0;
+    if (e.mode == EPI_MERGE && e.mg_mask != nullptr) {
+        mptr = e.mg_mask + e.mg_mcol0;
+        mld = e.mg_mld;
+        if (hg != nullptr ? (e.mg_mhp != hg->hp || e.mg_mwp != hg->wp || e.mg_mpad != 1)
+                          : (e.mg_mhp != hp || e.mg_mwp != wp || e.mg_mpad != pad))
+            return false;
+    } else if (e.mode == EPI_MASK) {
+        mptr = e.mask + e.mcol0;
+        mld = e.ldm;
+    }
+    ts->mask = 0;
+    static const bool no_mask = getenv("PPB_NO_TMA_MASK") != nullptr;
+    if (mptr != nullptr && no_mask) return false;
+    if (mptr != nullptr) {
+        if ((reinterpret_cast<uintptr_t>(mptr) & 15u) != 0 || mld % 4 != 0) return false;
+        cuuint64_t mstr[3] = {static_cast<cuuint64_t>(mld) * 4, static_cast<cuuint64_t>(wp) * mld * 4,
+                              static_cast<cuuint64_t>(hp) * wp * mld * 4};
+        const long long moff = rank == 4 ? (static_cast<long long>(pad) * wp + pad) * mld : 0;
+        if (enc(&ts->mmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float*>(mptr) + moff, dims, mstr, box,
+                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+        ts->mask = 1;
+    }
     ts->rank = static_cast<int>(rank);
     for (int d = 0; d < nd; ++d) {
         CUresult r = enc(&ts->map[d], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, ptrs[d] + base_off, dims, strides, box,
@@ -728,7 +765,7 @@ cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.grid);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = C::kSmem + p.db_smem;
+    cfg.dynamicSmemBytes = 1024 + p.stages * C::kStageBytes + 256 + p.db_smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -738,7 +775,7 @@ cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<A_MN, B_MN, BN, CG>, p.ta, p.tb, p.M, p.N, p.K, p.epi,
-                                       p.ga, p.gb, p.sk, p.ts);
+                                       p.ga, p.gb, p.sk, p.ts, p.stages);
     if (e != cudaSuccess || p.sk.splits <= 1) return e;
     const long long R = p.sk.trans ? p.N : p.M, Cc = p.sk.trans ? p.M : p.N;
     const long long items = R * ((Cc + 3) / 4);
@@ -853,27 +890,35 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
     }
     const int work = tiles * p.sk.splits;
     p.grid = (work < units ? work : units) * cg;
+    // shared memory: stage ring + barrier block, then the EPI_MERGE db rows,
+    // then the TMA-store staging; the ring gives up stages (down to 4) to fit
+    const int stage_bytes = bn == 64 ? TcCfg<64, 1>::kStageBytes
+                            : cg == 2 ? (bn == 128 ? TcCfg<128, 2>::kStageBytes : TcCfg<256, 2>::kStageBytes)
+                                      : (bn == 128 ? TcCfg<128, 1>::kStageBytes : TcCfg<256, 1>::kStageBytes);
+    const int def_stages = bn == 64 ? TcCfg<64, 1>::kStages
+                           : cg == 2 ? (bn == 128 ? TcCfg<128, 2>::kStages : TcCfg<256, 2>::kStages)
+                                     : (bn == 128 ? TcCfg<128, 1>::kStages : TcCfg<256, 1>::kStages);
+    constexpr int kCapSmem = 227 * 1024;
+    auto ring = [&](int st) { return 1024 + st * stage_bytes + 256; };
+    p.stages = def_stages;
     if (p.epi.db_partial != nullptr) {  // in-epilogue bias partials: single-pass (no split-K) only
         const int need = 4 * ((d.N + 31) / 32 * 32) * 4;
-        const int base = bn == 64 ? TcCfg<64, 1>::kSmem
-                         : cg == 2 ? (bn == 128 ? TcCfg<128, 2>::kSmem : TcCfg<256, 2>::kSmem)
-                                   : (bn == 128 ? TcCfg<128, 1>::kSmem : TcCfg<256, 1>::kSmem);
-        if (p.sk.splits > 1 || base + need > 227 * 1024) p.epi.db_partial = nullptr;
+        if (p.sk.splits > 1 || ring(p.stages) + need > kCapSmem) p.epi.db_partial = nullptr;
         else p.db_smem = need;
     }
     if (p.sk.splits == 1 ? tma_store_setup(p.epi, d.M, d.N, nullptr, &p.ts)
                          : tma_store_setup_splitk(p.sk, d.M, d.N, &p.ts)) {
-        const int base = bn == 64 ? TcCfg<64, 1>::kSmem
-                         : cg == 2 ? (bn == 128 ? TcCfg<128, 2>::kSmem : TcCfg<256, 2>::kSmem)
-                                   : (bn == 128 ? TcCfg<128, 1>::kSmem : TcCfg<256, 1>::kSmem);
         // staging after the barrier block and the db rows, 1 KB aligned (SW128 boxes)
         const int off = 1024 + (p.db_smem + 1023) / 1024 * 1024;
         const int extra = off + kEpiStageBytes - 256;
-        if (base + extra <= 227 * 1024) {
+        int st = p.stages;
+        while (ring(st) + extra > kCapSmem && st > 4) --st;
+        if (ring(st) + extra <= kCapSmem) {
+            p.stages = st;
             p.ts.stage_off = off;
             p.db_smem = extra;
         } else {
-            p.ts.n = 0;
+            p.ts = TmaStore{};
         }
     }
     // A: M extent x K.  K-major: rows=M, cols=K, box {32, 128}.  MN-major:

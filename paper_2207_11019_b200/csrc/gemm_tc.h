@@ -25,7 +25,8 @@ struct TcGemmPlan {
     ConvGeom ga, gb;
     SplitK sk;
     int halo = 0;  // 1: conv_halo.cu kernel (hg describes the padded grid)
-    int db_smem = 0;  // extra dynamic smem of the EPI_MERGE db accumulator
+    int db_smem = 0;  // extra dynamic smem past the ring: EPI_MERGE db rows + TMA-store staging
+    int stages = 0;   // tc_gemm ring stages (<= TcCfg::kStages)
     HaloGeom hg;
     TmaStore ts;  // TMA-store epilogue (ts.n == 0: register epilogue)
 };

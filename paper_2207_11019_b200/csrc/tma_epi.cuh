@@ -27,7 +27,7 @@
 namespace ppb {
 
 constexpr int kEpiWarps = 8;                     // two warps per TMEM lane quarter (alternate column chunks)
-constexpr int kEpiStageBytes = kEpiWarps * 4096;  // one 32 rows x 128 B staging box per epilogue warp
+constexpr int kEpiStageBytes = kEpiWarps * 4096 + 128;  // one 32 rows x 128 B staging box per epilogue warp + mbarriers
 
 struct TmaStore {
     CUtensorMap map[kMaxDst];
@@ -36,6 +36,11 @@ struct TmaStore {
     int wo = 1, pix = 1;
     int stage_off = 0;  // staging offset (bytes) past the kernel's barrier block
     int tr = 0;         // rank 3 (split-K workspace [split][rows][ld]): 1 = [n][m] (dW^T)
+    // ReLU mask of EPI_MERGE (pool 1) / EPI_MASK, same box geometry as the
+    // store: TMA-loaded into the staging box (one mbarrier per epilogue warp
+    // after the staging boxes), then applied from shared memory
+    int mask = 0;
+    CUtensorMap mmap;
 };
 
 // Host: split-K partial sums through the same staging path: a rank-3 map over
@@ -74,6 +79,55 @@ __device__ __forceinline__ void tma_store_partial(const TmaStore& ts, uint8_t* b
     if (lane == 0) {
         if (ts.tr) tma_store_3d(&ts.map[0], buf, r0, n, split);
         else tma_store_3d(&ts.map[0], buf, n, r0, split);
+        bulk_commit();
+    }
+}
+
+__device__ __forceinline__ uint64_t* epi_mask_bar(uint8_t* stage_base, int ewarp) {
+    return reinterpret_cast<uint64_t*>(stage_base + kEpiWarps * 4096) + ewarp;
+}
+
+// Masked variant: the chunk's ReLU-mask box (the layer's activation at the
+// same rows / columns) is TMA-loaded into the staging box, each lane masks
+// its row from shared memory (conflict-free, same swizzle), writes the
+// result back in place and lane 0 stores it.  v is masked in place (db).
+__device__ __forceinline__ void tma_store_chunk_masked(const TmaStore& ts, uint8_t* buf, uint64_t* bar,
+                                                       uint32_t& phase, int lane, float (&v)[32], int r0, int n) {
+    if (lane == 0) {
+        bulk_wait_read<0>();  // the previous store has read the box
+        mbar_arrive_expect_tx(bar, 4096);
+        if (ts.rank == 2) {
+            tma_load_2d(buf, &ts.mmap, bar, n, r0);
+        } else {
+            const int img = r0 / ts.pix, rem = r0 - img * ts.pix;
+            const int h = rem / ts.wo, w = rem - h * ts.wo;
+            tma_load_4d(buf, &ts.mmap, bar, n, w, h, img);
+        }
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    const uint32_t row = smem_u32(buf) + lane * 128;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t a = row + ((j ^ (lane & 7)) << 4);
+        float m0, m1, m2, m3;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(m0), "=f"(m1), "=f"(m2), "=f"(m3) : "r"(a));
+        v[4 * j] = m0 > 0.f ? v[4 * j] : 0.f;
+        v[4 * j + 1] = m1 > 0.f ? v[4 * j + 1] : 0.f;
+        v[4 * j + 2] = m2 > 0.f ? v[4 * j + 2] : 0.f;
+        v[4 * j + 3] = m3 > 0.f ? v[4 * j + 3] : 0.f;
+        st_shared_v4(a, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+        if (ts.rank == 2) {
+            for (int d = 0; d < ts.n; ++d) tma_store_2d(&ts.map[d], buf, n, r0);
+        } else {
+            const int img = r0 / ts.pix, rem = r0 - img * ts.pix;
+            const int h = rem / ts.wo, w = rem - h * ts.wo;
+            for (int d = 0; d < ts.n; ++d) tma_store_4d(&ts.map[d], buf, n, w, h, img);
+        }
         bulk_commit();
     }
 }
