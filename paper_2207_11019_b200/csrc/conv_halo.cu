@@ -115,6 +115,10 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     if (CG == 2) cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // prologue done (barriers, TMEM, tensor-map prefetch): wait for the
+    // stream predecessor's results, then let the successor start launching
+    griddep_wait();
+    griddep_launch_dependents();
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer: halo boxes
@@ -352,13 +356,15 @@ cudaError_t launch_halo_t(const TcGemmPlan& p, cudaStream_t s) {
     cfg.blockDim = dim3(kHaloThreads);
     cfg.dynamicSmemBytes = p.hg.smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, halo_conv_kernel<B_MN, BN, CG>, p.ta, p.tb, p.N, p.hg, p.epi, p.gb, p.ts);
 }
 

@@ -107,6 +107,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (CG == 2) cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // prologue done (barriers, TMEM, tensor-map prefetch): wait for the
+    // stream predecessor's results, then let the successor start launching
+    griddep_wait();
+    griddep_launch_dependents();
 
     // ------------------------------------------------ TMA producers: warp 0 stages A, warp 3 stages B
     // (two single-thread issue streams: one thread's per-K-block bookkeeping
@@ -327,6 +331,7 @@ __global__ void __launch_bounds__(256) splitk_epilogue_kernel(
     const __grid_constant__ EpiParams epi, const __grid_constant__ SplitK sk, int M, int N) {
     constexpr int kItems = 256 / PHASES;
     __shared__ float4 part[PHASES][kItems];
+    griddep_wait();  // launched programmatically after its GEMM
     const int bblocks = sk.bias != nullptr ? (sk.bu + 31) / 32 : 0;
     if (static_cast<int>(blockIdx.x) >= static_cast<int>(gridDim.x) - bblocks) {
         // bias job: column = t % 32, phase y = t / 32 sums chunks y, y+8, ...
@@ -714,6 +719,14 @@ cudaError_t launch_bn(const TcGemmPlan& p, cudaStream_t s) {
 
 }  // namespace
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("PPB_NO_PDL");
+        return !(e != nullptr && *e != '\0' && *e != '0');
+    }();
+    return on;
+}
+
 int sm_count() {
     static int n = 0;
     if (n == 0) {
@@ -767,25 +780,38 @@ cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = 1024 + p.stages * C::kStageBytes + 256 + p.db_smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<A_MN, B_MN, BN, CG>, p.ta, p.tb, p.M, p.N, p.K, p.epi,
                                        p.ga, p.gb, p.sk, p.ts, p.stages);
     if (e != cudaSuccess || p.sk.splits <= 1) return e;
     const long long R = p.sk.trans ? p.N : p.M, Cc = p.sk.trans ? p.M : p.N;
     const long long items = R * ((Cc + 3) / 4);
     const unsigned bblocks = p.sk.bias != nullptr ? static_cast<unsigned>((p.sk.bu + 31) / 32) : 0u;
-    if (p.sk.splits >= 16)
-        splitk_epilogue_kernel<8><<<static_cast<unsigned>((items + 31) / 32) + bblocks, dim3(32, 8), 0, s>>>(
-            p.epi, p.sk, p.M, p.N);
-    else
-        splitk_epilogue_kernel<1><<<static_cast<unsigned>((items + 255) / 256) + bblocks, dim3(256, 1), 0, s>>>(
-            p.epi, p.sk, p.M, p.N);
+    cudaLaunchConfig_t rc{};
+    rc.stream = s;
+    cudaLaunchAttribute ra[1];
+    ra[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    ra[0].val.programmaticStreamSerializationAllowed = 1;
+    rc.attrs = ra;
+    rc.numAttrs = pdl_enabled() ? 1 : 0;
+    if (p.sk.splits >= 16) {
+        rc.gridDim = dim3(static_cast<unsigned>((items + 31) / 32) + bblocks);
+        rc.blockDim = dim3(32, 8);
+        e = cudaLaunchKernelEx(&rc, splitk_epilogue_kernel<8>, p.epi, p.sk, p.M, p.N);
+    } else {
+        rc.gridDim = dim3(static_cast<unsigned>((items + 255) / 256) + bblocks);
+        rc.blockDim = dim3(256, 1);
+        e = cudaLaunchKernelEx(&rc, splitk_epilogue_kernel<1>, p.epi, p.sk, p.M, p.N);
+    }
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

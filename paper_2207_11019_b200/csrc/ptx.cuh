@@ -323,4 +323,14 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, float a, float b, fl
                  : "memory");
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// The kernel may be launched before its stream predecessor finishes (launch
+// attribute programmaticStreamSerialization); everything before griddep_wait()
+// must not touch memory the predecessor writes.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+bool pdl_enabled();  // host: PPB_NO_PDL unset
+
 }  // namespace ppb
