@@ -65,6 +65,21 @@ __device__ __forceinline__ void epilogue32(const EpiParams& p, int m, int n0, fl
     const int nvalid = p.N - n0 < 32 ? p.N - n0 : 32;
     switch (p.mode) {
         case EPI_STORE: {
+            if (p.seg_w > 0) {  // dense conv: chunk n0 lies in segment n0 / seg_w
+                const int sp = n0 / p.seg_w, sc = n0 - sp * p.seg_w;
+                if (p.bias != nullptr) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) acc[i] += __ldg(p.bias + sc + i);
+                }
+                if (p.relu) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) acc[i] = acc[i] > 0.f ? acc[i] : 0.f;
+                }
+                for (int d = 0; d < p.ndst; ++d)
+                    store_row32(p.dst[d] + static_cast<long long>(m) * p.ldd + sp * p.seg_pitch + p.col0 + sc, 0, 32,
+                                acc);
+                break;
+            }
             if (p.bias != nullptr) {
 #pragma unroll
                 for (int i = 0; i < 32; ++i) acc[i] += (i < nvalid) ? __ldg(p.bias + n0 + i) : 0.f;
@@ -228,9 +243,16 @@ __device__ __forceinline__ void epilogue1(const EpiParams& p, int m, int n, floa
     if (m >= p.M || n >= p.N) return;
     switch (p.mode) {
         case EPI_STORE: {
-            if (p.bias != nullptr) v += __ldg(p.bias + n);
+            long long col = p.col0 + n;
+            int bn = n;
+            if (p.seg_w > 0) {
+                const int sp = n / p.seg_w;
+                bn = n - sp * p.seg_w;
+                col = sp * p.seg_pitch + p.col0 + bn;
+            }
+            if (p.bias != nullptr) v += __ldg(p.bias + bn);
             if (p.relu) v = v > 0.f ? v : 0.f;
-            for (int d = 0; d < p.ndst; ++d) p.dst[d][row_off + p.col0 + n] = v;
+            for (int d = 0; d < p.ndst; ++d) p.dst[d][row_off + col] = v;
             break;
         }
         case EPI_MASK: {

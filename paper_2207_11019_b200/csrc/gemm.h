@@ -46,6 +46,11 @@ struct EpiParams {
     // an ho x wo grid lands at row ((img*hp + h + pad)*wp + w + pad).
     int remap = 0;
     int r_wo = 1, r_howo = 1, r_hp = 1, r_wp = 1, r_pad = 0;
+    // EPI_STORE, segmented columns (dense conv: GEMM column n = (p, c) with
+    // p = n / seg_w, c = n % seg_w): C(m, n) -> dst[m*ldd + p*seg_pitch + col0 + c],
+    // bias indexed by c.  seg_w is a multiple of 32 (a chunk never straddles).
+    int seg_w = 0;
+    long long seg_pitch = 0;
     // EPI_MASK
     const float* mask = nullptr;
     long long ldm = 0;

@@ -575,7 +575,7 @@ bool tma_store_setup(const EpiParams& e, int M, int N, const HaloGeom* hg, TmaSt
     // writer's range corrupts it (measured: LeNet 120 -> 60/60 shards), so the
     // TMA path needs sector-aligned ranges unless this GEMM owns whole rows.
     const bool whole_rows = col0 == 0 && (N + 3) / 4 * 4 == ld;
-    if (!whole_rows && (col0 % 8 != 0 || N % 8 != 0 || ld % 8 != 0)) return false;
+    if (!whole_rows && e.seg_w == 0 && (col0 % 8 != 0 || N % 8 != 0 || ld % 8 != 0)) return false;
     int dev = 0;
     cudaGetDevice(&dev);
     for (int d = 0; d < nd; ++d) {
@@ -592,7 +592,21 @@ bool tma_store_setup(const EpiParams& e, int M, int N, const HaloGeom* hg, TmaSt
     cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
     cuuint32_t rank = 2;
     long long base_off = col0;
-    if (hg != nullptr) {
+    ts->segw = 0;
+    if (e.mode == EPI_STORE && e.seg_w > 0) {  // dense conv: {c, p, row}, box {32, 1, 32}
+        if (hg != nullptr || padded || e.seg_w % 32 != 0 || N % e.seg_w != 0 || e.seg_pitch % 8 != 0 || col0 % 8 != 0 ||
+            ld % 8 != 0)
+            return false;
+        rank = 3;
+        dims[0] = static_cast<cuuint64_t>(e.seg_w);
+        dims[1] = static_cast<cuuint64_t>(N / e.seg_w);
+        dims[2] = static_cast<cuuint64_t>(M);
+        strides[0] = static_cast<cuuint64_t>(e.seg_pitch) * 4;
+        strides[1] = static_cast<cuuint64_t>(ld) * 4;
+        box[1] = 1;
+        box[2] = 32;
+        ts->segw = e.seg_w;
+    } else if (hg != nullptr) {
         // halo rows are padded positions: identity when the destination has the same grid
         if (!padded || hp != hg->hp || wp != hg->wp || pad != 1 || ho != hg->ho || wo != hg->wo) return false;
         dims[0] = static_cast<cuuint64_t>(N);

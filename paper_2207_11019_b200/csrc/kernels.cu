@@ -387,6 +387,144 @@ __global__ void col2im_kernel(const float* __restrict__ dcols, long long ldk, in
     }
 }
 
+// Small-grid conv as a dense layer ("dense conv", e.g. VGG's 2x2 layers):
+// with P = Ho*Wo output and Q = H*W input positions, the conv is
+//   out[n][(p, co)] = sum_{(q, ci)} in[n][(q, ci)] * Wx[(p, co)][(q, ci)]
+//   Wx[(p, co)][(q, ci)] = W[co][tap(p, q)][ci],  tap = (qy - py + pad, qx - px + pad)
+// (zero when the tap falls outside the kernel).  W stays the parameter
+// ([u][k*k][ck], the implicit-GEMM layout); Wx is re-expanded after every
+// update.  The wgrad GEMM yields dWx; the fold sums dWx over the (p, q) pairs
+// of each tap in ascending (p, q) order (deterministic), applies SGD to W and
+// rewrites Wx.  Thread = one (co, ci) pair.
+__device__ __forceinline__ int dc_tap(const DenseConvGeom& g, int p, int q) {
+    const int py = p / g.Wo, px = p - py * g.Wo, qy = q / g.W, qx = q - qy * g.W;
+    const int r = qy - py + g.pad, s = qx - px + g.pad;
+    return (r >= 0 && r < g.k && s >= 0 && s < g.k) ? r * g.k + s : -1;
+}
+
+__global__ void dense_conv_expand_kernel(DenseConvGeom g, const float* __restrict__ W, float* __restrict__ Wx) {
+    const int P = g.Ho * g.Wo, Q = g.H * g.W;
+    const long long total = static_cast<long long>(g.u) * g.C;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int co = static_cast<int>(i / g.C), ci = static_cast<int>(i % g.C);
+        for (int p = 0; p < P; ++p)
+            for (int q = 0; q < Q; ++q) {
+                const int t = dc_tap(g, p, q);
+                Wx[static_cast<long long>(p * g.u + co) * g.ldx + q * g.C + ci] =
+                    t >= 0 ? W[co * g.ldw + t * g.ck + ci] : 0.f;
+            }
+    }
+}
+
+// 3x3 / pad 1 on a 2x2 grid (VGG conv11-13), fully unrolled: 16 (p, q)
+// pairs onto 9 taps, summed in ascending (p, q) order.  Extra blocks past the
+// (co, ci) range apply the bias update from the merge's partial rows (lane =
+// column, 8 phases over the chunks, fixed-order sum).
+__global__ void __launch_bounds__(256) dense_conv_update_2x2_kernel(
+    DenseConvGeom g, const float* __restrict__ dWx, float* __restrict__ W, float* __restrict__ Wx,
+    const double* __restrict__ alpha, float inv_b, int* flag, const float* __restrict__ bpart, int bchunks,
+    float* __restrict__ bias) {
+    const float a = static_cast<float>(*alpha);
+    const long long total = static_cast<long long>(g.u) * g.C;
+    const int main_blocks = static_cast<int>((total + 255) / 256);
+    if (static_cast<int>(blockIdx.x) >= main_blocks) {
+        __shared__ float bsh[8][33];
+        const int t = threadIdx.x, col = (blockIdx.x - main_blocks) * 32 + (t & 31), y = t >> 5;
+        float acc = 0.f;
+        if (col < g.u)
+            for (int k = y; k < bchunks; k += 8) acc += bpart[static_cast<long long>(k) * g.u + col];
+        bsh[y][t & 31] = acc;
+        __syncthreads();
+        if (y == 0 && col < g.u) {
+            float s = 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) s += bsh[j][t & 31];
+            bias[col] -= a * (s * inv_b);
+        }
+        return;
+    }
+    const long long i = blockIdx.x * 256LL + threadIdx.x;
+    if (i >= total) return;
+    const int co = static_cast<int>(i / g.C), ci = static_cast<int>(i % g.C);
+    float v[4][4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[p][q] = dWx[static_cast<long long>(p * g.u + co) * g.ldx + q * g.C + ci];
+    float gs[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) gs[t] = 0.f;
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) gs[((q >> 1) - (p >> 1) + 1) * 3 + ((q & 1) - (p & 1) + 1)] += v[p][q];
+    bool bad = false;
+    float wn[9];
+    float* wr = W + co * g.ldw + ci;
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+        const float gr = gs[t] * inv_b;
+        bad |= !isfinite(gr);
+        wn[t] = wr[t * g.ck] - a * gr;
+        wr[t * g.ck] = wn[t];
+    }
+    if (bad && flag != nullptr) atomicOr(flag, 1);
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            Wx[static_cast<long long>(p * g.u + co) * g.ldx + q * g.C + ci] =
+                wn[((q >> 1) - (p >> 1) + 1) * 3 + ((q & 1) - (p & 1) + 1)];
+}
+
+__global__ void dense_conv_fold_sgd_kernel(DenseConvGeom g, const float* __restrict__ dWx, float* __restrict__ W,
+                                           float* __restrict__ Wx, const double* __restrict__ alpha, float inv_b,
+                                           int* flag) {
+    const int P = g.Ho * g.Wo, Q = g.H * g.W;
+    const float a = static_cast<float>(*alpha);
+    const long long total = static_cast<long long>(g.u) * g.C;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int co = static_cast<int>(i / g.C), ci = static_cast<int>(i % g.C);
+        float gsum[25];
+#pragma unroll
+        for (int t = 0; t < 25; ++t) gsum[t] = 0.f;
+        for (int p = 0; p < P; ++p)
+            for (int q = 0; q < Q; ++q) {
+                const int t = dc_tap(g, p, q);
+                if (t < 0) continue;
+                const float v = dWx[static_cast<long long>(p * g.u + co) * g.ldx + q * g.C + ci];
+#pragma unroll
+                for (int tt = 0; tt < 25; ++tt)
+                    if (tt == t) gsum[tt] += v;
+            }
+        bool bad = false;
+        float wn[25];
+#pragma unroll
+        for (int t = 0; t < 25; ++t) {
+            wn[t] = 0.f;
+            if (t < g.k * g.k) {
+                const float gr = gsum[t] * inv_b;
+                bad |= !isfinite(gr);
+                float* w = W + co * g.ldw + t * g.ck + ci;
+                wn[t] = *w - a * gr;
+                *w = wn[t];
+            }
+        }
+        if (bad && flag != nullptr) atomicOr(flag, 1);
+        for (int p = 0; p < P; ++p)
+            for (int q = 0; q < Q; ++q) {
+                const int t = dc_tap(g, p, q);
+                float v = 0.f;
+#pragma unroll
+                for (int tt = 0; tt < 25; ++tt)
+                    if (tt == t) v = wn[tt];
+                Wx[static_cast<long long>(p * g.u + co) * g.ldx + q * g.C + ci] = v;
+            }
+    }
+}
+
 template <class T>
 __global__ void pad_input_kernel(const T* __restrict__ src, int imgs, int H, int W, int C, float* __restrict__ dst,
                                  int p, long long ld) {
@@ -746,6 +884,31 @@ cudaError_t launch_col2im(const float* dcols, long long ldk, int imgs, int H, in
     if (n <= 0) return cudaSuccess;
     const int Ho = H + 2 * p - k + 1, Wo = W + 2 * p - k + 1;
     col2im_kernel<<<grid_for(n, 256), 256, 0, s>>>(dcols, ldk, imgs, H, W, C, k, p, Ho, Wo, c0, nc, dst, ldo);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dense_conv_expand(const DenseConvGeom& g, const float* W, float* Wx, cudaStream_t s) {
+    const long long n = static_cast<long long>(g.u) * g.C;
+    if (n <= 0) return cudaSuccess;
+    dense_conv_expand_kernel<<<grid_for(n, 256), 256, 0, s>>>(g, W, Wx);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dense_conv_fold_sgd(const DenseConvGeom& g, const float* dWx, float* W, float* Wx,
+                                       const double* alpha, float inv_b, int* flag, cudaStream_t s,
+                                       const float* bpart, int bchunks, float* bias) {
+    const long long n = static_cast<long long>(g.u) * g.C;
+    if (n <= 0) return cudaSuccess;
+    if (g.k == 3 && g.pad == 1 && g.H == 2 && g.W == 2 && g.Ho == 2 && g.Wo == 2) {
+        const unsigned blocks = static_cast<unsigned>((n + 255) / 256) + (bias != nullptr ? (g.u + 31) / 32 : 0);
+        dense_conv_update_2x2_kernel<<<blocks, 256, 0, s>>>(g, dWx, W, Wx, alpha, inv_b, flag, bpart, bchunks, bias);
+        return cudaGetLastError();
+    }
+    if (bias != nullptr) {
+        cudaError_t e = launch_bias_from_partials(bpart, bchunks, g.u, bias, alpha, inv_b, s);
+        if (e != cudaSuccess) return e;
+    }
+    dense_conv_fold_sgd_kernel<<<grid_for(n, 256), 256, 0, s>>>(g, dWx, W, Wx, alpha, inv_b, flag);
     return cudaGetLastError();
 }
 

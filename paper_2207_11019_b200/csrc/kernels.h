@@ -77,6 +77,21 @@ cudaError_t launch_im2col_act(const float* x, int imgs, int hp, int wp, long lon
 cudaError_t launch_col2im(const float* dcols, long long ldk, int imgs, int H, int W, int C, int k, int p, int c0,
                           int nc, float* dst, long long ldo, cudaStream_t s);
 
+// Small-grid conv as a dense layer (kernels.cu: DenseConvGeom): expansion of
+// W into Wx, and the fold of dWx + SGD on W + re-expansion.
+struct DenseConvGeom {  // see kernels.cu
+    int u = 0, C = 0, k = 3, pad = 1, H = 2, W = 2, Ho = 2, Wo = 2;
+    long long ldw = 0;   // W row pitch (k*k*ck)
+    int ck = 32;
+    long long ldx = 0;   // Wx / dWx row pitch (>= Q*C)
+};
+
+cudaError_t launch_dense_conv_expand(const DenseConvGeom& g, const float* W, float* Wx, cudaStream_t s);
+// bpart / bchunks / bias (optional): the layer's bias update from merge partials, same launch
+cudaError_t launch_dense_conv_fold_sgd(const DenseConvGeom& g, const float* dWx, float* W, float* Wx,
+                                       const double* alpha, float inv_b, int* flag, cudaStream_t s,
+                                       const float* bpart = nullptr, int bchunks = 0, float* bias = nullptr);
+
 // Layout of a conv layer's output as its consumer reads it.
 struct ActLayout {
     int kind = 0;        // 0 padded NHWC [img][hp][wp][ld] at channel col0 + c; 1 CHW-flatten rows [img][ld]

@@ -74,7 +74,11 @@ struct Session::WLayer {
     float* cols = nullptr;               // generic conv: im2col rows of the input [b*Ho*Wo x ldc]
     long long ldc = 0;
     float* dcols = nullptr;              // generic conv: dgrad partial in column space [b*Ho*Wo x ldk]
-    long long ldk = 0;
+    long long ldk = 0;                   // (dense conv: input-gradient rows [b][H*W*C])
+    float* Wx = nullptr;                 // dense conv: expanded weight [Ho*Wo*u x ldwx]
+    float* dWx = nullptr;                // dense conv: its gradient
+    long long ldwx = 0;
+    DenseConvGeom dcg;
     bool merge_fused = false;            // conv: delta written by the dgrad epilogue (EPI_MERGE)
     bool db_colsum = false;              // fused merge without in-epilogue bias partials: column-sum pass
     std::vector<std::vector<int>> delta_ready;  // [j] -> op ids that produce delta rows of micro-batch j
@@ -334,6 +338,27 @@ void Session::alloc_buffers() {
     const int F = net_.dims[L];
     const bool softmax = net_.acts[L - 1] == 2;
     hist_cap_ = 1 << 16;
+    // dense conv for small grids (fewer MACs than the 3x3 implicit GEMM): every
+    // shard width a multiple of 32 (segmented epilogue chunks), C % 4 == 0
+    // (unpadded input rows are the K dimension); its output must feed a pool /
+    // dense consumer or another dense-conv layer.  Decided from the top down.
+    {
+        static const bool off = getenv("PPB_NO_DENSE_CONV") != nullptr;
+        for (int i = L - 1; i >= 1 && !off; --i) {
+            LayerInfo& li = net_.info[i];
+            if (li.kind != 1 || li.generic || li.im2col || li.H * li.W > 4 || li.in_units % 4 != 0 ||
+                li.ksz * li.ksz > 25 || cfg_.precision != 0)
+                continue;
+            bool ok = true;
+            for (int wi : layer_workers_[i + 1]) ok = ok && workers_[wi]->at(i + 1).u % 32 == 0;
+            const LayerInfo* nx = i + 1 < L ? &net_.info[i + 1] : nullptr;
+            if (li.pool == 1 && nx != nullptr && nx->kind == 1 && !nx->dense_conv) ok = false;
+            if (ok) {
+                li.dense_conv = true;
+                li.dense_delta = true;
+            }
+        }
+    }
     // layout of a_l as layer l+1 reads it: padded NHWC for a conv consumer,
     // dense rows (CHW flatten after a conv) for a dense consumer
     lay_.assign(L + 1, ActLayout{});
@@ -348,9 +373,9 @@ void Session::alloc_buffers() {
         } else if (l < L && net_.info[l].kind == 1) {
             const LayerInfo& c = net_.info[l];
             a.kind = 0;
-            a.pad = c.pad;
-            a.hp = c.H + 2 * c.pad;
-            a.wp = c.W + 2 * c.pad;
+            a.pad = c.dense_conv ? 0 : c.pad;  // dense conv reads unpadded rows [img][(q, c)]
+            a.hp = c.H + 2 * a.pad;
+            a.wp = c.W + 2 * a.pad;
             a.ld = ld_of(c.in_units);
         } else {
             a.kind = 1;
@@ -413,6 +438,25 @@ void Session::alloc_buffers() {
                 }
                 if (li.pool == 2)
                     wl.argmax = static_cast<unsigned char*>(g.alloc(static_cast<size_t>(b) * li.Hq() * li.Wq() * wl.u));
+                if (li.dense_conv) {
+                    const int P = li.Ho() * li.Wo(), Q = li.H * li.W;
+                    wl.ldwx = static_cast<long long>(Q) * li.in_units;
+                    wl.Wx = static_cast<float*>(g.alloc(sizeof(float) * P * wl.u * wl.ldwx));
+                    wl.dWx = static_cast<float*>(g.alloc(sizeof(float) * P * wl.u * wl.ldwx));
+                    wl.ldk = wl.ldwx;
+                    wl.dcols = static_cast<float*>(g.alloc(sizeof(float) * b * wl.ldk));
+                    DenseConvGeom& dg = wl.dcg;
+                    dg.u = wl.u;
+                    dg.C = li.in_units;
+                    dg.k = li.ksz;
+                    dg.pad = li.pad;
+                    dg.H = li.H;
+                    dg.W = li.W;
+                    dg.Ho = li.Ho();
+                    dg.Wo = li.Wo();
+                    dg.ck = li.ck();
+                    dg.ldx = wl.ldwx;
+                }
                 if (li.generic) {
                     const long long pix = static_cast<long long>(b) * li.Ho() * li.Wo();
                     const int kc = li.ksz * li.ksz * li.in_units;
@@ -446,6 +490,11 @@ void Session::alloc_buffers() {
             }
             check(cudaSetDevice(w.gpu), "cudaSetDevice");
             check(cudaMemcpy(wl.W, tmp.data(), sizeof(float) * tmp.size(), cudaMemcpyHostToDevice), "upload W");
+            if (li.dense_conv) {
+                wl.dcg.ldw = wl.ldw;
+                check(launch_dense_conv_expand(wl.dcg, wl.W, wl.Wx, nullptr), "expand Wx");
+                check(cudaDeviceSynchronize(), "expand Wx");
+            }
             std::vector<float> bb(wl.u);
             for (int r = 0; r < wl.u; ++r) bb[r] = static_cast<float>(host_b_[wl.layer - 1][wl.lo + r]);
             check(cudaMemcpy(wl.bias, bb.data(), sizeof(float) * wl.u, cudaMemcpyHostToDevice), "upload b");
@@ -611,7 +660,16 @@ void Session::build_ops() {
                     cs.ksz = li.ksz;
                     cs.pad = li.pad;
                     cs.u = wl.u;
-                    if (li.generic) {  // per-step im2col rows of the padded input, then a dense GEMM
+                    if (li.dense_conv) {  // dense layer over all positions with the expanded weight
+                        const int P = li.Ho() * li.Wo(), Q = li.H * li.W;
+                        d = GemmDesc{};
+                        d.a = Operand{act_buf(w.gpu, l - 1) + off * img_elems(l - 1), rows, Q * li.in_units,
+                                      img_elems(l - 1), false};
+                        d.b = Operand{wl.Wx, P * wl.u, Q * li.in_units, wl.ldwx, false};
+                        d.M = rows;
+                        d.N = P * wl.u;
+                        d.K = Q * li.in_units;
+                    } else if (li.generic) {  // per-step im2col rows of the padded input, then a dense GEMM
                         const ActLayout& a = lay_[l - 1];
                         const float* x = act_buf(w.gpu, l - 1) + off * img_elems(l - 1);
                         float* cols = wl.cols + off * li.Ho() * li.Wo() * wl.ldc;
@@ -661,8 +719,22 @@ void Session::build_ops() {
                         d.epi.col0 = wl.lo;
                         for (int ord : dest_gpus) d.epi.dst[d.epi.ndst++] = act_buf(ord, l) + off * img_elems(l);
                     }
+                    if (li.dense_conv) {  // segmented columns (p, c): unpadded per-pixel rows of the destination
+                        d.epi.remap = 0;
+                        d.epi.seg_w = wl.u;
+                        if (wl.U != nullptr) {
+                            d.epi.seg_pitch = wl.ldu;
+                            d.epi.ldd = pix * wl.ldu;
+                            d.epi.col0 = 0;
+                        } else {
+                            d.epi.seg_pitch = lay_[l].ld;
+                            d.epi.ldd = img_elems(l);
+                            d.epi.col0 = wl.lo;
+                        }
+                    }
                     prepare(d, wl.p_fwd[j], w.gpu);
-                    const double fl = 2.0 * rows * pix * wl.u * li.ksz * li.ksz * li.in_units;
+                    const double fl = li.dense_conv ? 2.0 * rows * pix * wl.u * li.H * li.W * li.in_units  // executed
+                                                    : 2.0 * rows * pix * wl.u * li.ksz * li.ksz * li.in_units;
                     int op = add_op(w.gpu, w.sf, gemm_launch(&wl.p_fwd[j], &wl.d_fwd[j], w.sf), deps, nk(wl.p_fwd[j]), OP_FWD_GEMM, fl);
                     if (wl.U != nullptr) {
                         ActLayout out = lay_[l];
@@ -781,7 +853,8 @@ void Session::build_ops() {
                 // destination sums them, routes through the pool argmax and
                 // masks by its ReLU into its padded error signal.
                 const int hw = lb.Hq() * lb.Wq();
-                if (li.kind == 1 && !li.generic && contrib.size() == 1 && dests.size() == 1 && fuse_merge_) {
+                if (li.kind == 1 && !li.generic && !li.dense_conv && contrib.size() == 1 && dests.size() == 1 &&
+                    fuse_merge_) {
                     // one contributor, one destination: the merge (pool routing,
                     // ReLU mask, padded store) runs in the dgrad epilogue
                     Worker& w = *workers_[contrib[0]];
@@ -841,30 +914,55 @@ void Session::build_ops() {
                     GemmDesc& d = wl.d_dgrad[j];
                     double fl;
                     long long rows_per_img;
-                    if (li.kind == 1 && li.generic) {
-                        // dcols = delta . W (column space), then col2im into each
-                        // destination's slot (its channel slice)
+                    if (li.kind == 1 && (li.generic || li.dense_conv)) {
+                        // generic: dcols = delta . W (column space), then col2im into each
+                        // destination's slot (its channel slice).  Dense conv: the
+                        // input-gradient rows [img][(q, c)] = delta . Wx, then a k = 1
+                        // col2im (channel-slice copy) into the slots.
                         const int kc = li.ksz * li.ksz * li.in_units;
                         const long long pix = static_cast<long long>(li.Ho()) * li.Wo();
+                        const int Q = li.H * li.W;
                         d = GemmDesc{};
-                        d.a = Operand{wl.delta + off * wl.delta_img, static_cast<int>(rows * pix), wl.u, wl.ldd, false};
-                        d.b = Operand{wl.W, wl.u, kc, wl.ldw, true};
-                        d.M = static_cast<int>(rows * pix);
-                        d.N = kc;
-                        d.K = wl.u;
+                        if (li.dense_conv) {
+                            d.a = Operand{wl.delta + off * wl.delta_img, rows, static_cast<int>(pix) * wl.u, wl.delta_img,
+                                          false};
+                            d.b = Operand{wl.Wx, static_cast<int>(pix) * wl.u, Q * li.in_units, wl.ldwx, true};
+                            d.M = rows;
+                            d.N = Q * li.in_units;
+                            d.K = static_cast<int>(pix) * wl.u;
+                        } else {
+                            d.a = Operand{wl.delta + off * wl.delta_img, static_cast<int>(rows * pix), wl.u, wl.ldd, false};
+                            d.b = Operand{wl.W, wl.u, kc, wl.ldw, true};
+                            d.M = static_cast<int>(rows * pix);
+                            d.N = kc;
+                            d.K = wl.u;
+                        }
                         d.epi = EpiParams{};
                         d.epi.mode = EPI_STORE;
-                        d.epi.dst[d.epi.ndst++] = wl.dcols + off * pix * wl.ldk;
-                        d.epi.ldd = wl.ldk;
+                        const long long drows = li.dense_conv ? 1 : pix;  // dcols rows per image
+                        // dense conv, one destination owning every input channel with
+                        // slot pitch C: the gradient rows [img][(q, c)] ARE its slot
+                        WLayer& d0 = workers_[dests[0]]->at(l - 1);
+                        const bool direct = li.dense_conv && dests.size() == 1 && d0.u == li.in_units &&
+                                            d0.slot_ld == li.in_units;
+                        if (direct) {
+                            d.epi.dst[d.epi.ndst++] = d0.slots[k] + off * Q * d0.slot_ld;
+                            d.epi.ldd = static_cast<long long>(Q) * d0.slot_ld;
+                        } else {
+                            d.epi.dst[d.epi.ndst++] = wl.dcols + off * drows * wl.ldk;
+                            d.epi.ldd = wl.ldk;
+                        }
                         prepare(d, wl.p_dgrad[j], w.gpu);
-                        fl = 2.0 * rows * li.H * li.W * li.in_units * li.ksz * li.ksz * wl.u;
+                        fl = li.dense_conv ? 2.0 * rows * pix * wl.u * Q * li.in_units
+                                           : 2.0 * rows * li.H * li.W * li.in_units * li.ksz * li.ksz * wl.u;
                         int op = add_op(w.gpu, w.sb, gemm_launch(&wl.p_dgrad[j], &wl.d_dgrad[j], w.sb), wl.delta_ready[j],
                                         nk(wl.p_dgrad[j]), OP_DGRAD_GEMM, fl);
                         wl.dgrad_op[j] = op;
-                        const float* dc = wl.dcols + off * pix * wl.ldk;
-                        const long long ldk = wl.ldk;
-                        const int H = li.H, W = li.W, C = li.in_units, ks = li.ksz, pd = li.pad;
-                        for (int di : dests) {
+                        const float* dc = wl.dcols + off * drows * wl.ldk;
+                        const bool dcv = li.dense_conv;
+                        const long long ldk = dcv ? li.in_units : wl.ldk;  // dense conv: pixel-major [img*Q][C]
+                        const int H = li.H, W = li.W, C = li.in_units, ks = dcv ? 1 : li.ksz, pd = dcv ? 0 : li.pad;
+                        for (int di : direct ? std::vector<int>{} : dests) {
                             WLayer& dl = workers_[di]->at(l - 1);
                             float* dst = dl.slots[k] + off * H * W * dl.slot_ld;
                             const long long ldo = dl.slot_ld;
@@ -1061,7 +1159,15 @@ void Session::build_ops() {
                 cs.ksz = li.ksz;
                 cs.pad = li.pad;
                 cs.u = wl.u;
-                if (li.dense_delta) {  // dense wgrad: K = output pixels, unpadded error signal x im2col rows
+                if (li.dense_conv) {  // dWx = delta^T . a over the batch (K = images); folded below
+                    const int P = li.Ho() * li.Wo(), Q = li.H * li.W;
+                    d = GemmDesc{};
+                    d.a = Operand{wl.delta, cfg_.batch, P * wl.u, wl.delta_img, true};
+                    d.b = Operand{act_buf(w.gpu, l - 1), cfg_.batch, Q * li.in_units, img_elems(l - 1), true};
+                    d.M = P * wl.u;
+                    d.N = Q * li.in_units;
+                    d.K = cfg_.batch;
+                } else if (li.dense_delta) {  // dense wgrad: K = output pixels, unpadded error signal x im2col rows
                     const int kc = li.ksz * li.ksz * li.in_units;
                     const int pix = cfg_.batch * li.Ho() * li.Wo();
                     const float* colsp = li.generic ? wl.cols : act_buf(w.gpu, l - 1);
@@ -1084,7 +1190,8 @@ void Session::build_ops() {
                 } else {
                     d = conv_wgrad_desc(cs, wl.delta, wl.ldd, act_buf(w.gpu, l - 1), lay_[l - 1].ld, wl.u < 128);
                 }
-                wfl = 2.0 * cfg_.batch * li.Ho() * li.Wo() * wl.u * li.ksz * li.ksz * li.in_units;
+                wfl = li.dense_conv ? 2.0 * cfg_.batch * li.Ho() * li.Wo() * wl.u * li.H * li.W * li.in_units  // executed
+                                    : 2.0 * cfg_.batch * li.Ho() * li.Wo() * wl.u * li.ksz * li.ksz * li.in_units;
                 bias_rows = static_cast<long long>(cfg_.batch) * (wl.delta_img / wl.ldd);  // zero borders add nothing
             } else {
                 d.a = Operand{wl.delta, cfg_.batch, wl.u, wl.ldd, true};
@@ -1107,6 +1214,12 @@ void Session::build_ops() {
             d.epi.alpha = &g.st->alpha;
             d.epi.inv_b = inv_b;
             d.epi.flag = &g.st->diverge_flag;
+            if (li.dense_conv) {  // plain dWx; the fold kernel applies SGD to W and re-expands Wx
+                d.epi = EpiParams{};
+                d.epi.mode = EPI_STORE;
+                d.epi.dst[d.epi.ndst++] = wl.dWx;
+                d.epi.ldd = wl.ldwx;
+            }
             prepare(d, wl.p_wgrad, w.gpu);
             std::vector<int> deps;
             for (int j = 0; j < m; ++j) {
@@ -1125,6 +1238,28 @@ void Session::build_ops() {
             const bool from_merge = li.kind == 1 && !wl.db_colsum;
             const int chunks = cfg_.m * conv_merge_blocks();
             const int splits = tf32 ? wl.p_wgrad.sk.splits : 1;
+            if (li.dense_conv) {
+                // dWx GEMM, then one launch: fold + SGD on W + re-expand Wx (+ the
+                // bias update from the merge partials)
+                std::vector<int> gdeps = deps;
+                if (!from_merge)
+                    gdeps = {add_op(w.gpu, s, [=]() {
+                        return launch_bias_update(delta, ldd, b, u, partial, bias, alpha, inv_b, s);
+                    }, deps, 2, OP_BIAS)};
+                const int gop = add_op(w.gpu, s, gemm_launch(&wl.p_wgrad, &wl.d_wgrad, s), gdeps, nk(wl.p_wgrad),
+                                       OP_WGRAD_GEMM, wfl);
+                const DenseConvGeom dg = wl.dcg;
+                const float* dWx = wl.dWx;
+                float* Wp = wl.W;
+                float* Wx = wl.Wx;
+                int* flag = &g.st->diverge_flag;
+                const float* bp = from_merge ? partial : nullptr;
+                float* bb = from_merge ? bias : nullptr;
+                add_op(w.gpu, s, [=]() {
+                    return launch_dense_conv_fold_sgd(dg, dWx, Wp, Wx, alpha, inv_b, flag, s, bp, chunks, bb);
+                }, {gop}, 1, OP_BIAS);
+                continue;
+            }
             if (from_merge && splits > 1) {
                 // the bias update rides in the wgrad's split-K reduction launch
                 wl.p_wgrad.sk.bpart = partial;

@@ -39,6 +39,10 @@ struct LayerInfo {
     // im2col rows of the padded input, dense GEMMs, col2im of the dgrad partial
     bool generic = false;
     bool dense_delta = false;  // error signal stored unpadded [pixel][ldd] (dense wgrad operand)
+    // small grid (H*W <= 4, e.g. VGG's 2x2 layers): the conv as a dense layer
+    // over all positions with an expanded weight Wx (kernels.cu DenseConvGeom);
+    // input and output stored unpadded NHWC
+    bool dense_conv = false;
     int dq() const { return dense_delta ? 0 : ksz - 1 - pad; }  // zero ring of the stored error signal
     int Ho() const { return H + 2 * pad - ksz + 1; }
     int Wo() const { return W + 2 * pad - ksz + 1; }

@@ -36,6 +36,7 @@ struct TmaStore {
     int wo = 1, pix = 1;
     int stage_off = 0;  // staging offset (bytes) past the kernel's barrier block
     int tr = 0;         // rank 3 (split-K workspace [split][rows][ld]): 1 = [n][m] (dW^T)
+    int segw = 0;       // rank 3 segmented columns (dense conv): box at (n % segw, n / segw, row)
     // ReLU mask of EPI_MERGE (pool 1) / EPI_MASK, same box geometry as the
     // store: TMA-loaded into the staging box (one mbarrier per epilogue warp
     // after the staging boxes), then applied from shared memory
@@ -146,7 +147,9 @@ __device__ __forceinline__ void tma_store_chunk(const TmaStore& ts, uint8_t* buf
     fence_proxy_async();
     __syncwarp();
     if (lane == 0) {
-        if (ts.rank == 2) {
+        if (ts.segw) {
+            for (int d = 0; d < ts.n; ++d) tma_store_3d(&ts.map[d], buf, n % ts.segw, n / ts.segw, r0);
+        } else if (ts.rank == 2) {
             for (int d = 0; d < ts.n; ++d) tma_store_2d(&ts.map[d], buf, n, r0);
         } else {
             const int img = r0 / ts.pix, rem = r0 - img * ts.pix;
@@ -165,7 +168,8 @@ __device__ __forceinline__ void epi_values32(const EpiParams& p, int m, int n0, 
     if (n0 >= p.N) return;
     if (p.mode == EPI_STORE) {
         if (p.bias != nullptr) {
-            const float bl = n0 + lane < p.N ? __ldg(p.bias + n0 + lane) : 0.f;
+            const int bi = p.seg_w > 0 ? (n0 + lane) % p.seg_w : n0 + lane;
+            const float bl = n0 + lane < p.N ? __ldg(p.bias + bi) : 0.f;
 #pragma unroll
             for (int i = 0; i < 32; ++i) acc[i] += __shfl_sync(0xffffffffu, bl, i);
         }
