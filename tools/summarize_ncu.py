@@ -54,10 +54,12 @@ def to_bytes(s):
 
 def main():
     tag, workload = sys.argv[1], sys.argv[2]
+    rep = sys.argv[3] if len(sys.argv) > 3 else "gemm"  # gpurun_out/<tag>_<rep>.ncu-rep
+    out_name = f"{tag}_ncu.md" if rep == "gemm" else f"{tag}_{rep}_ncu.md"
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     md = [f"# ncu summary {tag} ({workload})", ""]
     lpath = os.path.join(ROOT, "gpurun_out", f"{tag}_launches.csv")
-    if os.path.exists(lpath):
+    if os.path.exists(lpath) and rep == "gemm":
         agg = launches(lpath)
         tot = sum(v[1] for v in agg.values())
         md += ["## Launch list (`ncu --metrics gpu__time_duration.sum --clock-control none`, "
@@ -66,7 +68,7 @@ def main():
         for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
             md.append(f"| `{k}` | {n} | {t:.0f} | {t / tot:.1%} |")
         md.append("")
-    fpath = os.path.join(ROOT, "gpurun_out", f"{tag}_gemm.ncu-rep")
+    fpath = os.path.join(ROOT, "gpurun_out", f"{tag}_{rep}.ncu-rep")
     if os.path.exists(fpath):
         res = full(fpath)
         md += ["## `--set full` capture of the dominant kernel", ""]
@@ -79,9 +81,9 @@ def main():
         tpath = os.path.join(ROOT, "profiles", "gemm_traffic.json")
         d = json.load(open(tpath)) if os.path.exists(tpath) else {}
         d[workload] = sum(tr) / len(tr)
-        d[f"{workload}_source"] = f"profiles/{tag}_ncu.md (dram__bytes_read.sum + dram__bytes_write.sum per launch)"
+        d[f"{workload}_source"] = f"profiles/{out_name} (dram__bytes_read.sum + dram__bytes_write.sum per launch)"
         json.dump(d, open(tpath, "w"), indent=1)
-    open(os.path.join(ROOT, "profiles", f"{tag}_ncu.md"), "w").write("\n".join(md) + "\n")
+    open(os.path.join(ROOT, "profiles", out_name), "w").write("\n".join(md) + "\n")
     print("\n".join(md))
 
 
