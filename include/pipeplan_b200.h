@@ -265,6 +265,11 @@ int ppb_session_profile(ppb_session* s, int iterations, double* ms, int* count, 
 int ppb_session_profile_ops(ppb_session* s, int* kind, int* layer, int* info, double* ms, double* flops, int cap,
                             int* count);
 
+/* Timeline of the last ppb_session_profile iteration (same op order as
+ * ppb_session_profile_ops): start of each op in ms from the first op on its
+ * device, and a per-session stream index (eager launch order, not a graph). */
+int ppb_session_profile_starts(ppb_session* s, double* start_ms, int* stream_id, int cap, int* count);
+
 /* ------------------------------------------------------------------ diagnostics */
 
 /* One shard GEMM on device pointers (kernel unit tests): C = A.B^T with the

@@ -555,6 +555,18 @@ class Session:
                  "ms": float(ms[i]), "tflops": float(fl[i] / ms[i] / 1e9) if ms[i] > 0 else 0.0}
                 for i in range(n.value)]
 
+    def profile_timeline(self) -> list:
+        """profile_ops() records with the op's start (ms from the first op) and stream index."""
+        ops = self.profile_ops()
+        n = C.c_int(0)
+        L = _lib.lib()
+        st, sid = np.zeros(max(len(ops), 1)), np.zeros(max(len(ops), 1), np.int32)
+        check(L.ppb_session_profile_starts(self._h, _dp(st), _ip(sid), len(ops), C.byref(n)))
+        for i, o in enumerate(ops):
+            o["start"] = float(st[i])
+            o["stream"] = int(sid[i])
+        return ops
+
     def step_host(self, X: np.ndarray, labels: np.ndarray) -> float:
         """End-to-end step from host buffers (H2D X/labels, step, D2H loss)."""
         loss = C.c_double(0)

@@ -212,6 +212,10 @@ extern "C" int ppb_session_profile(ppb_session* s, int iterations, double* ms, i
     return ppb_guard([&] { s->s->profile(iterations, ms, count, flops, nkinds); });
 }
 
+extern "C" int ppb_session_profile_starts(ppb_session* s, double* start_ms, int* stream_id, int cap, int* count) {
+    return ppb_guard([&] { *count = s->s->profile_starts(start_ms, stream_id, cap); });
+}
+
 extern "C" int ppb_session_profile_ops(ppb_session* s, int* kind, int* layer, int* info, double* ms, double* flops,
                                        int cap, int* count) {
     return ppb_guard([&] { *count = s->s->profile_ops(kind, layer, info, ms, flops, cap); });

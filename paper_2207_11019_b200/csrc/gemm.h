@@ -155,6 +155,12 @@ struct SplitK {
     const float* bpart = nullptr;
     float* bias = nullptr;
     int bchunks = 0, bu = 0;
+    // in-kernel reduction (few splits): each epilogue warp publishes its
+    // partial chunks with a per-(tile, CTA, warp slot) counter; the last of
+    // the `splits` arrivals sums the splits in order 0..splits-1 and runs the
+    // real epilogue (no reduction kernel; counters re-armed to 0)
+    int fixup = 0;
+    int* counters = nullptr;
 };
 
 // Padded-position geometry of the halo conv kernel (conv_halo.cu): GEMM row

@@ -298,6 +298,59 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (CG == 2) mbar_arrive_cluster_n(tempty_leader + acc * sizeof(uint64_t), cnt);
                 else mbar_arrive_n(&tempty_bar[acc], cnt);
             }
+            if (sk.splits > 1 && sk.fixup && !(epi.dbg & 6)) {
+                // publish this warp's partial chunks; the last writer of the slot reduces
+                if (ts.n && lane == 0) bulk_wait<0>();
+                fence_proxy_async_global();
+                __threadfence();
+                __syncwarp();
+                const int slot = by_tile ? q : q * 2 + half;
+                int* ctr = sk.counters + (static_cast<long long>(mn) * CG + rank) * 8 + slot;
+                int old = 0;
+                if (lane == 0) old = atomicAdd(ctr, 1);
+                old = __shfl_sync(0xffffffffu, old, 0);
+                if (old == sk.splits - 1) {
+                    __threadfence();
+#pragma unroll 1
+                    for (int c = c_first; c < BN / 32; c += c_step) {
+                        const int nn = n0 + c * 32;
+                        if (nn >= N) break;
+                        const int nv = N - nn < 32 ? N - nn : 32;
+                        float v[32];
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+                        if (m < M) {
+#pragma unroll 1
+                            for (int sp = 0; sp < sk.splits; ++sp) {
+                                if (sk.trans) {
+                                    const float* col = sk.ws + sp * sk.stride + m;
+#pragma unroll
+                                    for (int i = 0; i < 32; ++i)
+                                        if (i < nv) v[i] += __ldcg(col + static_cast<long long>(nn + i) * sk.ld);
+                                } else {
+                                    const float* row = sk.ws + sp * sk.stride + static_cast<long long>(m) * sk.ld + nn;
+                                    if (nv == 32 && (sk.ld & 3) == 0) {
+#pragma unroll
+                                        for (int i = 0; i < 32; i += 4) {
+                                            const float4 t = __ldcg(reinterpret_cast<const float4*>(row + i));
+                                            v[i] += t.x;
+                                            v[i + 1] += t.y;
+                                            v[i + 2] += t.z;
+                                            v[i + 3] += t.w;
+                                        }
+                                    } else {
+#pragma unroll
+                                        for (int i = 0; i < 32; ++i)
+                                            if (i < nv) v[i] += __ldcg(row + i);
+                                    }
+                                }
+                            }
+                        }
+                        epilogue32(epi, m, nn, v);
+                    }
+                    if (lane == 0) *ctr = 0;  // re-armed for the next launch
+                }
+            }
         }
         if (db) {  // both warps of the quarter accumulated into db_row (disjoint columns)
             epi_bar_sync();
@@ -805,7 +858,7 @@ cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<A_MN, B_MN, BN, CG>, p.ta, p.tb, p.M, p.N, p.K, p.epi,
                                        p.ga, p.gb, p.sk, p.ts, p.stages);
-    if (e != cudaSuccess || p.sk.splits <= 1) return e;
+    if (e != cudaSuccess || p.sk.splits <= 1 || p.sk.fixup) return e;
     const long long R = p.sk.trans ? p.N : p.M, Cc = p.sk.trans ? p.M : p.N;
     const long long items = R * ((Cc + 3) / 4);
     const unsigned bblocks = p.sk.bias != nullptr ? static_cast<unsigned>((p.sk.bu + 31) / 32) : 0u;
@@ -925,6 +978,18 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
             if (p.sk.ws == nullptr) {
                 snprintf(err, errlen, "split-K workspace allocation failed");
                 return false;
+            }
+            // in-kernel fixup: measured slower than the reduction kernel (the
+            // last warp's serial row-per-thread reads sit on the tile's tail:
+            // VGG step 2.54 -> 3.07 ms), so opt-in only
+            static const bool fixup_on = getenv("PPB_SPLITK_FIXUP") != nullptr;
+            if (splits <= 8 && fixup_on) {
+                const size_t nctr = static_cast<size_t>(tiles) * cg * 8;
+                float* c = ws_alloc(nctr);
+                if (c != nullptr && cudaMemset(c, 0, nctr * sizeof(int)) == cudaSuccess) {
+                    p.sk.counters = reinterpret_cast<int*>(c);
+                    p.sk.fixup = 1;
+                }
             }
         }
     }

@@ -81,6 +81,7 @@ struct Session::WLayer {
     DenseConvGeom dcg;
     bool merge_fused = false;            // conv: delta written by the dgrad epilogue (EPI_MERGE)
     bool db_colsum = false;              // fused merge without in-epilogue bias partials: column-sum pass
+    int db_q = 1;                        // bias partial rows per merge block (dense-conv dgrad: one per position)
     std::vector<std::vector<int>> delta_ready;  // [j] -> op ids that produce delta rows of micro-batch j
     std::vector<int> fwd_op, dgrad_op;   // [j]
     TcGemmPlan p_wgrad;
@@ -470,8 +471,10 @@ void Session::alloc_buffers() {
             }
             wl.delta = static_cast<float*>(g.alloc(sizeof(float) * b * wl.delta_img));
             // bias-gradient partials: dense colsum chunks, or one row per (micro-batch, merge block) for conv
-            const long long prow = li.kind == 1 ? std::max<long long>(static_cast<long long>(cfg_.m) * conv_merge_blocks(), kColsumChunks)
-                                                : kColsumChunks;
+            const long long prow =
+                li.kind == 1 ? std::max<long long>(static_cast<long long>(cfg_.m) * conv_merge_blocks() * li.Ho() * li.Wo(),
+                                                   kColsumChunks)
+                             : kColsumChunks;
             wl.partial = static_cast<float*>(g.alloc(sizeof(float) * prow * wl.u));
             // upload the shard rows [lo, hi) (train_partitioned.cpp:168-169), fp64 -> fp32;
             // conv rows [k][k][C_in] go to the GEMM layout [k*k][ck] (zero-padded channels)
@@ -575,7 +578,7 @@ void Session::build_ops() {
         return [d, s]() { return simt_gemm_launch(*d, s); };
     };
     // kernels per GEMM launch (the split-K reduction is a second kernel)
-    auto nk = [tf32](const TcGemmPlan& p) { return tf32 && p.sk.splits > 1 ? 2 : 1; };
+    auto nk = [tf32](const TcGemmPlan& p) { return tf32 && p.sk.splits > 1 && !p.sk.fixup ? 2 : 1; };
     auto prepare = [&](GemmDesc& d, TcGemmPlan& p, int gpu) {
         if (!tf32) return;
         char err[256];
@@ -908,6 +911,7 @@ void Session::build_ops() {
                     dw.last_bwd[j] = std::max(dw.last_bwd[j], op);
                     continue;
                 }
+                bool fused_dc = false;  // dense-conv dgrad performed the whole merge
                 for (size_t k = 0; k < contrib.size(); ++k) {
                     Worker& w = *workers_[contrib[k]];
                     WLayer& wl = w.at(l);
@@ -945,6 +949,35 @@ void Session::build_ops() {
                         WLayer& d0 = workers_[dests[0]]->at(l - 1);
                         const bool direct = li.dense_conv && dests.size() == 1 && d0.u == li.in_units &&
                                             d0.slot_ld == li.in_units;
+                        // dense conv over an unpooled dense-layout layer below, one
+                        // contributor: the whole merge (ReLU mask + bias partials, one
+                        // partial row per (CTA, warp, position)) runs in the epilogue
+                        const bool fused = direct && contrib.size() == 1 && fuse_merge_ && lb.pool == 1 &&
+                                           lb.dq() == 0 && d0.ldd == li.in_units && tf32;
+                        if (fused) {
+                            Worker& dw = *workers_[dests[0]];
+                            d.epi.mode = relu_below ? EPI_MASK : EPI_STORE;
+                            d.epi.dst[d.epi.ndst++] = d0.delta + off * d0.delta_img;
+                            d.epi.ldd = d0.delta_img;
+                            if (relu_below) {
+                                d.epi.mask = act_buf(dw.gpu, l - 1) + off * img_elems(l - 1);
+                                d.epi.ldm = img_elems(l - 1);
+                            }
+                            d.epi.db_partial = d0.partial + static_cast<long long>(j) * conv_merge_blocks() * Q * d0.u;
+                            prepare(d, wl.p_dgrad[j], w.gpu);
+                            if (wl.p_dgrad[j].epi.db_partial == nullptr) d0.db_colsum = true;
+                            d0.db_q = Q;
+                            const double fl2 = 2.0 * rows * pix * wl.u * Q * li.in_units;
+                            const int op = add_op(w.gpu, w.sb, gemm_launch(&wl.p_dgrad[j], &wl.d_dgrad[j], w.sb),
+                                                  wl.delta_ready[j], nk(wl.p_dgrad[j]), OP_DGRAD_GEMM, fl2);
+                            wl.dgrad_op[j] = op;
+                            w.last_bwd[j] = std::max(w.last_bwd[j], op);
+                            d0.merge_fused = true;
+                            d0.delta_ready[j] = {op};
+                            dw.last_bwd[j] = std::max(dw.last_bwd[j], op);
+                            fused_dc = true;
+                            break;
+                        }
                         if (direct) {
                             d.epi.dst[d.epi.ndst++] = d0.slots[k] + off * Q * d0.slot_ld;
                             d.epi.ldd = static_cast<long long>(Q) * d0.slot_ld;
@@ -1015,6 +1048,7 @@ void Session::build_ops() {
                     w.last_bwd[j] = std::max(w.last_bwd[j], op);
                     dgrad_ops.push_back(op);
                 }
+                if (fused_dc) continue;
                 for (int di : dests) {
                     Worker& dw = *workers_[di];
                     WLayer& dl = dw.at(l - 1);
@@ -1236,7 +1270,7 @@ void Session::build_ops() {
             const double* alpha = &g.st->alpha;
             // conv: db partials came with the merges (conv_merge or the EPI_MERGE epilogue)
             const bool from_merge = li.kind == 1 && !wl.db_colsum;
-            const int chunks = cfg_.m * conv_merge_blocks();
+            const int chunks = cfg_.m * conv_merge_blocks() * wl.db_q;
             const int splits = tf32 ? wl.p_wgrad.sk.splits : 1;
             if (li.dense_conv) {
                 // dWx GEMM, then one launch: fold + SGD on W + re-expand Wx (+ the
@@ -1260,7 +1294,7 @@ void Session::build_ops() {
                 }, {gop}, 1, OP_BIAS);
                 continue;
             }
-            if (from_merge && splits > 1) {
+            if (from_merge && splits > 1 && !wl.p_wgrad.sk.fixup) {
                 // the bias update rides in the wgrad's split-K reduction launch
                 wl.p_wgrad.sk.bpart = partial;
                 wl.p_wgrad.sk.bias = bias;
@@ -1273,7 +1307,7 @@ void Session::build_ops() {
                 if (from_merge) return launch_bias_from_partials(partial, chunks, u, bias, alpha, inv_b, s);
                 return launch_bias_update(delta, ldd, b, u, partial, bias, alpha, inv_b, s);
             }, deps, from_merge ? 1 : 2, OP_BIAS);
-            add_op(w.gpu, s, gemm_launch(&wl.p_wgrad, &wl.d_wgrad, s), {bop}, splits > 1 ? 2 : 1, OP_WGRAD_GEMM, wfl);
+            add_op(w.gpu, s, gemm_launch(&wl.p_wgrad, &wl.d_wgrad, s), {bop}, nk(wl.p_wgrad), OP_WGRAD_GEMM, wfl);
         }
     }
 
@@ -1378,6 +1412,7 @@ void Session::profile(int iterations, double* ms, int* count, double* flops, int
         flops[k] = 0;
     }
     last_op_ms_.assign(n, 0.0);
+    last_op_start_.assign(n, 0.0);
     for (int it = 0; it < iterations; ++it) {
         enqueue_iteration_timed(t0, t1);
         ++steps_enqueued_;
@@ -1390,6 +1425,12 @@ void Session::profile(int iterations, double* ms, int* count, double* flops, int
             float e = 0.f;
             check(cudaEventElapsedTime(&e, t0[i], t1[i]), "elapsed");
             last_op_ms_[i] += e;
+            int first = -1;
+            for (int f = 0; f < n && first < 0; ++f)
+                if (ops_[f].launch && ops_[f].gpu == ops_[i].gpu) first = f;
+            float st = 0.f;
+            if (first >= 0) check(cudaEventElapsedTime(&st, t0[first], t0[i]), "elapsed");
+            last_op_start_[i] = st;
             ms[ops_[i].kind] += e;
             count[ops_[i].kind] += 1;
             flops[ops_[i].kind] += ops_[i].flops;
@@ -1411,6 +1452,24 @@ int Session::profile_ops(int* kind, int* layer, int* info, double* ms, double* f
             info[k] = ops_[i].info;
             ms[k] = last_op_ms_[i];
             flops[k] = ops_[i].flops;
+        }
+        ++k;
+    }
+    return k;
+}
+
+int Session::profile_starts(double* start_ms, int* stream_id, int cap) {
+    std::map<cudaStream_t, int> ids;
+    int k = 0;
+    for (int i = 0; i < static_cast<int>(ops_.size()) && i < static_cast<int>(last_op_start_.size()); ++i) {
+        if (!ops_[i].launch) continue;
+        if (!ids.count(ops_[i].stream)) {
+            const int id = static_cast<int>(ids.size());
+            ids[ops_[i].stream] = id;
+        }
+        if (k < cap) {
+            start_ms[k] = last_op_start_[i];
+            stream_id[k] = ids[ops_[i].stream];
         }
         ++k;
     }

@@ -115,6 +115,7 @@ class Session {
     void profile(int iterations, double* ms, int* count, double* flops, int nkinds);
     // per-op device times of the last profile() call
     int profile_ops(int* kind, int* layer, int* info, double* ms, double* flops, int cap);
+    int profile_starts(double* start_ms, int* stream_id, int cap);
     double last_loss();
 
   private:
@@ -174,6 +175,7 @@ class Session {
     bool pending_acc_error_ = false;
     int cur_layer_ = 0, cur_info_ = 0;
     std::vector<double> last_op_ms_;
+    std::vector<double> last_op_start_;  // ms from the first timed op (same device), last profile iteration
 };
 
 }  // namespace ppb

@@ -44,6 +44,12 @@ def run(which, N, H, W, Cin, u, dbg="0", reps=20, bn=0):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "wgrad":
+        for shp in ((512, 8, 8, 128, 256), (512, 4, 4, 256, 512), (512, 8, 8, 256, 256), (512, 4, 4, 512, 512),
+                    (512, 16, 16, 128, 128), (512, 16, 16, 64, 128)):
+            for which in (2, 3):
+                run(which, *shp)
+        sys.exit(0)
     for shp in ((512, 8, 8, 256, 256), (512, 4, 4, 512, 512), (512, 2, 2, 512, 512), (512, 8, 8, 128, 256)):
         for which in (0, 1, 3):
             for dbg in ("0", "2"):
