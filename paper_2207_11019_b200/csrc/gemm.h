@@ -161,6 +161,7 @@ struct SplitK {
     // real epilogue (no reduction kernel; counters re-armed to 0)
     int fixup = 0;
     int* counters = nullptr;
+    int deferred = 0;  // reduction carried by the next GEMM's SideJob (no kernel here)
 };
 
 // Padded-position geometry of the halo conv kernel (conv_halo.cu): GEMM row
@@ -179,6 +180,20 @@ struct HaloGeom {
     int resident = 0;                   // B column slice loaded once per CTA
     int smem = 0;                       // dynamic shared memory bytes
     int dbg = 0;  // timing probes (wrong results): 1 align taps, 2 no epilogue stores, 4 no halo waits
+};
+
+// A split-K reduction carried by the NEXT GEMM on the stream ("side job"):
+// the wgrad + SGD of one layer has no reader before the next step's forward,
+// so its reduction (and bias update) runs in the following wgrad GEMM's
+// epilogue warps while that GEMM's mainloop occupies the tensor cores,
+// instead of as a separate kernel.  Same split order as the reduction kernel
+// (sequential 0..splits-1); the bias job sums chunks in 8 lane phases and a
+// fixed butterfly.
+struct SideJob {
+    int on = 0;
+    int M = 0, N = 0;
+    SplitK sk;
+    EpiParams epi;
 };
 
 struct GemmDesc {

@@ -53,12 +53,89 @@ struct TcCfg {
     static constexpr int kTmemCols = 2 * BN;
 };
 
+// One split-K work item (row r, columns c4..c4+3 of the workspace): sum the
+// splits in order 0..splits-1, then the GEMM's epilogue (SGD on dW^T / dW).
+__device__ __forceinline__ void splitk_item_seq(const EpiParams& epi, const SplitK& sk, int M, int N, long long item) {
+    const int R = sk.trans ? N : M;
+    const int Cc = sk.trans ? M : N;
+    const int cq = (Cc + 3) / 4;
+    if (item >= static_cast<long long>(R) * cq) return;
+    const int r = static_cast<int>(item / cq);
+    const int c4 = static_cast<int>(item - static_cast<long long>(r) * cq) * 4;
+    const int nc = Cc - c4 < 4 ? Cc - c4 : 4;
+    const bool vec = nc == 4 && (sk.ld & 3) == 0;
+    const long long off = static_cast<long long>(r) * sk.ld + c4;
+    float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+    for (int sp = 0; sp < sk.splits; ++sp) {
+        const float* src = sk.ws + static_cast<long long>(sp) * sk.stride + off;
+        if (vec) {
+            const float4 t = __ldcg(reinterpret_cast<const float4*>(src));
+            a[0] += t.x;
+            a[1] += t.y;
+            a[2] += t.z;
+            a[3] += t.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (j < nc) a[j] += __ldcg(src + j);
+        }
+    }
+    if (sk.trans) {
+        const float alpha = static_cast<float>(*epi.alpha);
+        float* w = epi.W + static_cast<long long>(r) * epi.ldw + c4;
+        bool bad = false;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (j < nc) {
+                const float g = a[j] * epi.inv_b;
+                bad |= !isfinite(g);
+                w[j] -= alpha * g;
+            }
+        }
+        if (bad && epi.flag != nullptr) atomicOr(epi.flag, 1);
+        return;
+    }
+    const long long row_off = epi.mode == EPI_STORE ? epi_store_row(epi, r) : 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (j < nc) epilogue1(epi, r, c4 + j, a[j], row_off);
+}
+
+// The side job over every epilogue thread of the grid (gt = global epilogue
+// thread index, nt = their count).  Bias job first: warp-group of 32 lanes =
+// 4 columns x 8 phases (phase p sums chunks p, p+8, ... in order), butterfly
+// over the phases (fixed tree), lane with phase 0 updates the column.
+__device__ __forceinline__ void run_side_job(const SideJob& sj, long long gt, long long nt, int lane) {
+    const SplitK& sk = sj.sk;
+    if (sk.bias != nullptr) {
+        const long long gw = gt >> 5, nw = nt >> 5;
+        const int groups = (sk.bu + 3) / 4;
+        for (long long grp = gw; grp < groups; grp += nw) {
+            const int col = static_cast<int>(grp) * 4 + (lane >> 3), ph = lane & 7;
+            float acc = 0.f;
+            if (col < sk.bu) {
+#pragma unroll 4
+                for (int k = ph; k < sk.bchunks; k += 8) acc += __ldcg(sk.bpart + static_cast<long long>(k) * sk.bu + col);
+            }
+            acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+            acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+            acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+            if (ph == 0 && col < sk.bu) sk.bias[col] -= static_cast<float>(*sj.epi.alpha) * (acc * sj.epi.inv_b);
+        }
+    }
+    const long long R = sk.trans ? sj.N : sj.M, Cc = sk.trans ? sj.M : sj.N;
+    const long long items = R * ((Cc + 3) / 4);
+    for (long long it = gt; it < items; it += nt) splitk_item_seq(sj.epi, sk, sj.M, sj.N, it);
+}
+
 template <bool A_MN, bool B_MN, int BN, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                    int M, int N, int K, const __grid_constant__ EpiParams epi,
                    const __grid_constant__ ConvGeom ga, const __grid_constant__ ConvGeom gb,
-                   const __grid_constant__ SplitK sk, const __grid_constant__ TmaStore ts, int nst) {
+                   const __grid_constant__ SplitK sk, const __grid_constant__ TmaStore ts, int nst,
+                   const __grid_constant__ SideJob sj) {
     using C = TcCfg<BN, CG>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -236,6 +313,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             __syncwarp();
         }
+        if (sj.on)  // a previous GEMM's split-K reduction, under this GEMM's mainloop
+            run_side_job(sj, static_cast<long long>(blockIdx.x) * (kEpiWarps * 32) + (threadIdx.x - 128),
+                         static_cast<long long>(gridDim.x) * (kEpiWarps * 32), lane);
         const bool by_tile = num_tiles >= 2 * units;
         const int c_first = by_tile ? 0 : half, c_step = by_tile ? 1 : 2;
         int local = 0;
@@ -857,8 +937,9 @@ cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<A_MN, B_MN, BN, CG>, p.ta, p.tb, p.M, p.N, p.K, p.epi,
-                                       p.ga, p.gb, p.sk, p.ts, p.stages);
-    if (e != cudaSuccess || p.sk.splits <= 1 || p.sk.fixup) return e;
+                                       p.ga, p.gb, p.sk, p.ts, p.stages, p.sj);
+    static const bool probe_no_reduce = getenv("PPB_PROBE_NO_REDUCE") != nullptr;  // timing probe (wrong results)
+    if (e != cudaSuccess || p.sk.splits <= 1 || p.sk.fixup || p.sk.deferred || probe_no_reduce) return e;
     const long long R = p.sk.trans ? p.N : p.M, Cc = p.sk.trans ? p.M : p.N;
     const long long items = R * ((Cc + 3) / 4);
     const unsigned bblocks = p.sk.bias != nullptr ? static_cast<unsigned>((p.sk.bu + 31) / 32) : 0u;

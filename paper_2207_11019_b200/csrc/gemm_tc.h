@@ -29,6 +29,7 @@ struct TcGemmPlan {
     int stages = 0;   // tc_gemm ring stages (<= TcCfg::kStages)
     HaloGeom hg;
     TmaStore ts;  // TMA-store epilogue (ts.n == 0: register epilogue)
+    SideJob sj;   // a previous GEMM's deferred split-K reduction
 };
 
 // ws_alloc (optional): allocates split-K workspace (floats) on the GEMM's

@@ -1173,10 +1173,32 @@ void Session::build_ops() {
         bwd_join = add_op(g0.ordinal, g0.main, nullptr, all, 0);  // std::barrier (:633)
     }
     const float inv_b = 1.f / static_cast<float>(cfg_.batch);
+    static const bool no_side = getenv("PPB_NO_SIDE_JOB") != nullptr;
     for (auto& wp : workers_) {
         Worker& w = *wp;
         Gpu& g = gpu_of(w.gpu);
-        for (WLayer& wl : w.layers) {
+        // wgrads in backward order (top layer first: each can start as soon as
+        // its delta exists); a split-K wgrad's reduction + SGD is carried by the
+        // next wgrad GEMM on the stream (SideJob) instead of its own kernel
+        TcGemmPlan* prev_plan = nullptr;
+        int prev_op = -1;
+        auto link_side = [&](TcGemmPlan* p, int op, bool carrier_ok) {
+            if (!tf32) return;
+            if (prev_plan != nullptr && carrier_ok && !no_side && p->halo == 0 && prev_plan->sk.splits > 1 &&
+                prev_plan->sk.splits < 16 && !prev_plan->sk.fixup && !prev_plan->sk.deferred) {
+                p->sj.on = 1;
+                p->sj.M = prev_plan->M;
+                p->sj.N = prev_plan->N;
+                p->sj.sk = prev_plan->sk;
+                p->sj.epi = prev_plan->epi;
+                prev_plan->sk.deferred = 1;
+                ops_[prev_op].kernels -= 1;
+            }
+            prev_plan = p;
+            prev_op = op;
+        };
+        for (auto wit = w.layers.rbegin(); wit != w.layers.rend(); ++wit) {
+            WLayer& wl = *wit;
             const int l = wl.layer;
             cur_layer_ = l;
             const int fi = net_.dims[l - 1];
@@ -1282,6 +1304,7 @@ void Session::build_ops() {
                     }, deps, 2, OP_BIAS)};
                 const int gop = add_op(w.gpu, s, gemm_launch(&wl.p_wgrad, &wl.d_wgrad, s), gdeps, nk(wl.p_wgrad),
                                        OP_WGRAD_GEMM, wfl);
+                link_side(&wl.p_wgrad, gop, true);
                 const DenseConvGeom dg = wl.dcg;
                 const float* dWx = wl.dWx;
                 float* Wp = wl.W;
@@ -1300,14 +1323,17 @@ void Session::build_ops() {
                 wl.p_wgrad.sk.bias = bias;
                 wl.p_wgrad.sk.bchunks = chunks;
                 wl.p_wgrad.sk.bu = u;
-                add_op(w.gpu, s, gemm_launch(&wl.p_wgrad, &wl.d_wgrad, s), deps, 2, OP_WGRAD_GEMM, wfl);
+                const int gop = add_op(w.gpu, s, gemm_launch(&wl.p_wgrad, &wl.d_wgrad, s), deps, 2, OP_WGRAD_GEMM, wfl);
+                link_side(&wl.p_wgrad, gop, true);
                 continue;
             }
             const int bop = add_op(w.gpu, s, [=]() {
                 if (from_merge) return launch_bias_from_partials(partial, chunks, u, bias, alpha, inv_b, s);
                 return launch_bias_update(delta, ldd, b, u, partial, bias, alpha, inv_b, s);
             }, deps, from_merge ? 1 : 2, OP_BIAS);
-            add_op(w.gpu, s, gemm_launch(&wl.p_wgrad, &wl.d_wgrad, s), {bop}, nk(wl.p_wgrad), OP_WGRAD_GEMM, wfl);
+            const int gop = add_op(w.gpu, s, gemm_launch(&wl.p_wgrad, &wl.d_wgrad, s), {bop}, nk(wl.p_wgrad),
+                                   OP_WGRAD_GEMM, wfl);
+            link_side(&wl.p_wgrad, gop, true);
         }
     }
 
