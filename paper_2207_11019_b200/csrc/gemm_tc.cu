@@ -66,20 +66,29 @@ __device__ __forceinline__ void splitk_item_seq(const EpiParams& epi, const Spli
     const bool vec = nc == 4 && (sk.ld & 3) == 0;
     const long long off = static_cast<long long>(r) * sk.ld + c4;
     float a[4] = {0.f, 0.f, 0.f, 0.f};
+    // association of splitk_epilogue_kernel: sequential for < 16 splits;
+    // otherwise 8 phase sums (splits p, p+8, ...) added in phase order
+    const int nph = sk.splits >= 16 ? 8 : 1;
+#pragma unroll 1
+    for (int ph = 0; ph < nph; ++ph) {
+        float b[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 4
-    for (int sp = 0; sp < sk.splits; ++sp) {
-        const float* src = sk.ws + static_cast<long long>(sp) * sk.stride + off;
-        if (vec) {
-            const float4 t = __ldcg(reinterpret_cast<const float4*>(src));
-            a[0] += t.x;
-            a[1] += t.y;
-            a[2] += t.z;
-            a[3] += t.w;
-        } else {
+        for (int sp = ph; sp < sk.splits; sp += nph) {
+            const float* src = sk.ws + static_cast<long long>(sp) * sk.stride + off;
+            if (vec) {
+                const float4 t = __ldcg(reinterpret_cast<const float4*>(src));
+                b[0] += t.x;
+                b[1] += t.y;
+                b[2] += t.z;
+                b[3] += t.w;
+            } else {
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (j < nc) a[j] += __ldcg(src + j);
+                for (int j = 0; j < 4; ++j)
+                    if (j < nc) b[j] += __ldcg(src + j);
+            }
         }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) a[j] += b[j];
     }
     if (sk.trans) {
         const float alpha = static_cast<float>(*epi.alpha);

@@ -302,9 +302,15 @@ void Session::build() {
             w->rank = static_cast<int>(r);
             w->gpu = device_map_[w->device - 1];
             check(cudaSetDevice(w->gpu), "cudaSetDevice");
-            check(cudaStreamCreateWithFlags(&w->sf, cudaStreamNonBlocking), "stream");
-            check(cudaStreamCreateWithFlags(&w->sb, cudaStreamNonBlocking), "stream");
-            check(cudaStreamCreateWithFlags(&w->su, cudaStreamNonBlocking), "stream");
+            // the forward / input-gradient chain is the critical path: its streams get
+            // the highest priority, the weight-gradient stream (fills the gaps) the lowest
+            int prio_lo = 0, prio_hi = 0;
+            cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+            static const bool no_prio = getenv("PPB_NO_PRIO") != nullptr;
+            if (no_prio) prio_lo = prio_hi = 0;
+            check(cudaStreamCreateWithPriority(&w->sf, cudaStreamNonBlocking, prio_hi), "stream");
+            check(cudaStreamCreateWithPriority(&w->sb, cudaStreamNonBlocking, prio_hi), "stream");
+            check(cudaStreamCreateWithPriority(&w->su, cudaStreamNonBlocking, prio_lo), "stream");
             for (int l = sm.first_layer; l <= sm.last_layer; ++l) {
                 const Shard& s = sm.layer_shards(l)[r];
                 WLayer wl;
@@ -1185,7 +1191,7 @@ void Session::build_ops() {
         auto link_side = [&](TcGemmPlan* p, int op, bool carrier_ok) {
             if (!tf32) return;
             if (prev_plan != nullptr && carrier_ok && !no_side && p->halo == 0 && prev_plan->sk.splits > 1 &&
-                prev_plan->sk.splits < 16 && !prev_plan->sk.fixup && !prev_plan->sk.deferred) {
+                !prev_plan->sk.fixup && !prev_plan->sk.deferred) {
                 p->sj.on = 1;
                 p->sj.M = prev_plan->M;
                 p->sj.N = prev_plan->N;
