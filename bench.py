@@ -14,9 +14,13 @@ SGD update) over one synthetic batch.
 * e2e        : samples/s through the public C ABI (ppb_session_step_host) from
                pinned host buffers: H2D of X and labels, the step, D2H of the
                loss, every step, wall clock around K blocking calls.
-* roofline   : the dominant kernel (tcgen05 TF32 shard GEMM), algorithmic
-               FLOPs per launch / average launch time, both measured in this
-               run with CUDA events around every GEMM (ppb_session_profile).
+* roofline   : the dominant kernel family (tcgen05 TF32 shard GEMMs + halo
+               conv), FLOPs per launch / average launch time, measured in this
+               run with CUDA events around every GEMM of one eager step whose
+               ops are serialised (ppb_session_profile: the graph overlaps the
+               wgrad stream with the forward / dgrad chain, and events cannot
+               split concurrent kernels).  Dense-conv GEMMs count the FLOPs
+               they execute; step_tflops uses the algorithmic 9-tap count.
 * cpu_baseline: the UNMODIFIED reference (oracle/_ref, compiled from
                /root/reference) on a bounded sample, timed on this host.
 
@@ -385,7 +389,7 @@ def run_ours(args, rank, world, dist):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="vgg16", choices=sorted(WORKLOADS))
     ap.add_argument("--m", type=int, default=1, help="micro-batches per step")

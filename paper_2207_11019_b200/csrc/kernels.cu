@@ -912,6 +912,21 @@ cudaError_t launch_dense_conv_fold_sgd(const DenseConvGeom& g, const float* dWx,
     return cudaGetLastError();
 }
 
+// Keeps a stream busy for ~`ns` nanoseconds (profiling: the ops that follow
+// are already enqueued when it finishes, so their start events carry no
+// host-launch latency).
+__global__ void spin_kernel(long long ns) {
+    const long long t0 = clock64();
+    const long long cycles = ns * 2;  // >= ns at <= 2 GHz
+    while (clock64() - t0 < cycles) {
+    }
+}
+
+cudaError_t launch_spin(long long ns, cudaStream_t s) {
+    spin_kernel<<<1, 32, 0, s>>>(ns);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pad_input(const double* src64, const float* src32, int imgs, int H, int W, int C, float* dst,
                              int p, long long ld, cudaStream_t s) {
     const long long n = static_cast<long long>(imgs) * H * W * C;

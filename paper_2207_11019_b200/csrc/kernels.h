@@ -92,6 +92,8 @@ cudaError_t launch_dense_conv_fold_sgd(const DenseConvGeom& g, const float* dWx,
                                        const double* alpha, float inv_b, int* flag, cudaStream_t s,
                                        const float* bpart = nullptr, int bchunks = 0, float* bias = nullptr);
 
+cudaError_t launch_spin(long long ns, cudaStream_t s);  // profiling helper
+
 // Layout of a conv layer's output as its consumer reads it.
 struct ActLayout {
     int kind = 0;        // 0 padded NHWC [img][hp][wp][ld] at channel col0 + c; 1 CHW-flatten rows [img][ld]

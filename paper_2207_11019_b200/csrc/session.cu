@@ -1402,9 +1402,14 @@ void Session::enqueue_iteration_timed(std::vector<cudaEvent_t>& t0, std::vector<
         for (int d : op.deps)
             if (ops_[d].stream != op.stream) check(cudaStreamWaitEvent(op.stream, ops_[d].ev, 0), "wait");
         if (op.launch) {
+            check(launch_spin(30000, op.stream), "spin");  // absorbs the launch latency of what follows
             check(cudaEventRecord(t0[i], op.stream), "record");
             check(op.launch(), "kernel launch");
             check(cudaEventRecord(t1[i], op.stream), "record");
+            // serialised: every op runs alone, so its CUDA-event duration is the
+            // kernel's own time (the graph overlaps streams; events cannot
+            // separate concurrent kernels)
+            check(cudaEventSynchronize(t1[i]), "serialise");
         }
         check(cudaEventRecord(op.ev, op.stream), "record");
     }

@@ -19,3 +19,10 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tc_gemm|halo_conv" -s 0 -c 6 -o gpurun_out/${TAG}_gemm python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_ncu_full_stdout.txt 2>&1; echo "ncu full rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:tc_gemm -s 12 -c 2 -o gpurun_out/${TAG}_gemm_wide python bench.py --workload wide_mlp --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_ncu_full_wide_stdout.txt 2>&1; echo "ncu full wide rc=$?"
 ls gpurun_out | grep ${TAG}
+# summaries on the box (the merged gpurun_out/ is capped at 64 MiB): keep the
+# VGG capture for source-level reading, drop the wide-MLP one after summarising
+python tools/summarize_ncu.py ${TAG} vgg16 > /dev/null 2>&1
+python tools/summarize_ncu.py ${TAG} wide_mlp gemm_wide > /dev/null 2>&1
+cp profiles/${TAG}_ncu.md profiles/${TAG}_gemm_wide_ncu.md profiles/gemm_traffic.json gpurun_out/ 2>/dev/null
+rm -f gpurun_out/${TAG}_gemm_wide.ncu-rep
+du -sh gpurun_out
