@@ -116,9 +116,9 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     // prologue done (barriers, TMEM, tensor-map prefetch): wait for the
-    // stream predecessor's results, then let the successor start launching
+    // stream predecessor's results (the successor is released after the last
+    // MMA is issued, so its waiting CTAs do not squat on SMs other streams use)
     griddep_wait();
-    griddep_launch_dependents();
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer: halo boxes
@@ -147,6 +147,8 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 }
             }
         }
+        __syncwarp();
+        griddep_launch_dependents();  // every halo load issued: release the stream successor
     } else if (warp == 3) {
         // ------------------------------------------------ TMA producer: B (weights)
         if (elect_one()) {

@@ -7,8 +7,28 @@
 #include <cmath>
 
 #include "kernels.h"
+#include "ptx.cuh"
 
 namespace ppb {
+
+namespace {
+// Programmatic dependent launch for the step's small kernels (each calls
+// griddep_wait() before touching its predecessor's results).
+template <typename... P, typename... A>
+cudaError_t pdl_launch(void (*k)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
+}
+}  // namespace
 
 namespace {
 
@@ -99,6 +119,7 @@ __global__ void __launch_bounds__(kRowThreads) loss_head_kernel(
     const float* __restrict__ in, long long ld_in, int F, const int* __restrict__ labels,
     int loss_kind, int relu_last, LossTargets t, double* __restrict__ loss_row,
     int* __restrict__ correct_row) {
+    griddep_wait();  // programmatic launch: the predecessor's results are visible after this
     const int row = blockIdx.x;
     const float* x = in + static_cast<long long>(row) * ld_in;
     const int label = labels[row];
@@ -158,6 +179,7 @@ __global__ void __launch_bounds__(kRowThreads) loss_head_kernel(
 __global__ void reduce_mask_kernel(ReduceSlots slots, long long ld_slot, int rows, int cols,
                                    const float* __restrict__ mask, long long ld_mask,
                                    float* __restrict__ out, long long ld_out, bool vec) {
+    griddep_wait();  // programmatic launch: the predecessor's results are visible after this
     if (vec) {
         const int c4 = cols / 4;
         const long long total = static_cast<long long>(rows) * c4;
@@ -202,6 +224,7 @@ __global__ void reduce_mask_kernel(ReduceSlots slots, long long ld_slot, int row
 template <int VEC>
 __global__ void colsum_rows_kernel(const float* __restrict__ delta, long long ld, long long rows, int u,
                                    float* __restrict__ partial) {
+    griddep_wait();  // programmatic launch: the predecessor's results are visible after this
     const int groups = u / VEC;
     const int gpb = groups < 256 ? groups : 256;  // channel groups per block (blockIdx.y: group block)
     const int g = blockIdx.y * gpb + threadIdx.x % gpb, j = threadIdx.x / gpb;
@@ -259,6 +282,7 @@ __global__ void colsum_rows_kernel(const float* __restrict__ delta, long long ld
 __global__ void __launch_bounds__(1024) bias_update_cols_kernel(const float* __restrict__ partial, int u, int chunks,
                                                                 float* __restrict__ bias,
                                                                 const double* __restrict__ alpha, float inv_b) {
+    griddep_wait();  // programmatic launch: the predecessor's results are visible after this
     __shared__ float sh[32][33];
     const int c = blockIdx.x * 32 + threadIdx.x;
     float s = 0.f;
@@ -289,6 +313,7 @@ __global__ void convert_kernel(const T* __restrict__ src, int rows, int cols, fl
 __global__ void finalize_kernel(StepState* st, const double* __restrict__ loss_row,
                                 const int* __restrict__ correct_row, int b, double* loss_hist,
                                 double* acc_hist, int hist_cap, int write_hist) {
+    griddep_wait();  // programmatic launch: the predecessor's results are visible after this
     double ls = 0.0;
     double cs = 0.0;
     if (write_hist) {
@@ -340,6 +365,7 @@ __global__ void im2col_kernel(const T* __restrict__ src, int imgs, int H, int W,
 // tensor's own zero ring is the conv padding); columns >= k*k*C are zero.
 __global__ void im2col_act_kernel(const float* __restrict__ x, int imgs, int hp, int wp, long long ldx, int C, int k,
                                   int Ho, int Wo, float* __restrict__ dst, long long ldc) {
+    griddep_wait();  // programmatic launch: the predecessor's results are visible after this
     const int kc = k * k * C;
     const long long total = static_cast<long long>(imgs) * Ho * Wo * ldc;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
@@ -364,6 +390,7 @@ __global__ void im2col_act_kernel(const float* __restrict__ x, int imgs, int hp,
 // Channels [c0, c0 + nc) go to dst[(img*H + y)*W + x][c - c0] (a merge slot).
 __global__ void col2im_kernel(const float* __restrict__ dcols, long long ldk, int imgs, int H, int W, int C, int k,
                               int p, int Ho, int Wo, int c0, int nc, float* __restrict__ dst, long long ldo) {
+    griddep_wait();  // programmatic launch: the predecessor's results are visible after this
     const long long total = static_cast<long long>(imgs) * H * W * nc;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -425,6 +452,7 @@ __global__ void __launch_bounds__(256) dense_conv_update_2x2_kernel(
     DenseConvGeom g, const float* __restrict__ dWx, float* __restrict__ W, float* __restrict__ Wx,
     const double* __restrict__ alpha, float inv_b, int* flag, const float* __restrict__ bpart, int bchunks,
     float* __restrict__ bias) {
+    griddep_wait();  // programmatic launch: the predecessor's results are visible after this
     const float a = static_cast<float>(*alpha);
     const long long total = static_cast<long long>(g.u) * g.C;
     const int main_blocks = static_cast<int>((total + 255) / 256);
@@ -481,6 +509,7 @@ __global__ void __launch_bounds__(256) dense_conv_update_2x2_kernel(
 __global__ void dense_conv_fold_sgd_kernel(DenseConvGeom g, const float* __restrict__ dWx, float* __restrict__ W,
                                            float* __restrict__ Wx, const double* __restrict__ alpha, float inv_b,
                                            int* flag) {
+    griddep_wait();  // programmatic launch: the predecessor's results are visible after this
     const int P = g.Ho * g.Wo, Q = g.H * g.W;
     const float a = static_cast<float>(*alpha);
     const long long total = static_cast<long long>(g.u) * g.C;
@@ -549,6 +578,7 @@ __global__ void pad_input_kernel(const T* __restrict__ src, int imgs, int H, int
 template <int VEC, class IDX>
 __global__ void pool_fwd_kernel(const float* __restrict__ U, long long ldu, int imgs, int Ho, int Wo, int uch,
                                 int pool, unsigned char* __restrict__ argmax, ActLayout out, PoolDsts dsts) {
+    griddep_wait();  // programmatic launch: the predecessor's results are visible after this
     const int Hq = Ho / pool, Wq = Wo / pool;
     const IDX groups = uch / VEC;
     const IDX total = static_cast<IDX>(imgs) * Hq * Wq * groups;
@@ -616,6 +646,7 @@ __global__ void pool_fwd_kernel(const float* __restrict__ U, long long ldu, int 
 
 template <int VEC, class IDX>
 __global__ void conv_merge_kernel(ConvMerge m, float* __restrict__ db_partial) {
+    griddep_wait();  // programmatic launch: the predecessor's results are visible after this
     const int groups = m.uch / VEC;
     const IDX total = static_cast<IDX>(m.imgs) * m.Ho * m.Wo * groups;
     const int Hg = m.Ho / m.pool, Wg = m.Wo / m.pool;
@@ -715,6 +746,7 @@ __global__ void conv_merge_kernel(ConvMerge m, float* __restrict__ db_partial) {
 // ~3U independent loads in flight instead of a dependent chain per element.
 template <int U>
 __global__ void conv_merge_rows_kernel(ConvMerge m, float* __restrict__ db_partial) {
+    griddep_wait();  // programmatic launch: the predecessor's results are visible after this
     const int groups = m.uch >> 2;
     const int g = threadIdx.x % groups;
     const int c0 = g * 4;
@@ -809,7 +841,7 @@ cudaError_t launch_loss_head(const float* in, long long ld_in, int rows, int F, 
                              int loss_kind, int relu_last, const LossTargets& t, double* loss_row,
                              int* correct_row, cudaStream_t s) {
     if (rows <= 0) return cudaSuccess;
-    loss_head_kernel<<<rows, kRowThreads, 0, s>>>(in, ld_in, F, labels, loss_kind, relu_last, t,
+    pdl_launch(loss_head_kernel, dim3(rows), dim3(kRowThreads), 0, s, in, ld_in, F, labels, loss_kind, relu_last, t,
                                                   loss_row, correct_row);
     return cudaGetLastError();
 }
@@ -824,7 +856,7 @@ cudaError_t launch_reduce_mask(const ReduceSlots& slots, long long ld_slot, int 
                (mask == nullptr || reinterpret_cast<uintptr_t>(mask) % 16 == 0);
     for (int k = 0; k < slots.n; ++k) vec = vec && reinterpret_cast<uintptr_t>(slots.slot[k]) % 16 == 0;
     const long long work = static_cast<long long>(rows) * (vec ? cols / 4 : cols);
-    reduce_mask_kernel<<<grid_for(work, 256), 256, 0, s>>>(slots, ld_slot, rows, cols, mask, ld_mask,
+    pdl_launch(reduce_mask_kernel, dim3(grid_for(work, 256)), dim3(256), 0, s, slots, ld_slot, rows, cols, mask, ld_mask,
                                                            out, ld_out, vec);
     return cudaGetLastError();
 }
@@ -839,9 +871,9 @@ cudaError_t launch_bias_update(const float* delta, long long ld, long long rows,
     const int block = (256 / gpb) * gpb;
     const dim3 grid(chunks, (groups + gpb - 1) / gpb);
     const size_t shmem = sizeof(float) * block * (v4 ? 4 : 1);
-    if (v4) colsum_rows_kernel<4><<<grid, block, shmem, s>>>(delta, ld, rows, u, partial);
-    else colsum_rows_kernel<1><<<grid, block, shmem, s>>>(delta, ld, rows, u, partial);
-    bias_update_cols_kernel<<<(u + 31) / 32, dim3(32, 32), 0, s>>>(partial, u, chunks, bias, alpha, inv_b);
+    if (v4) pdl_launch(colsum_rows_kernel<4>, dim3(grid), dim3(block), shmem, s, delta, ld, rows, u, partial);
+    else pdl_launch(colsum_rows_kernel<1>, dim3(grid), dim3(block), shmem, s, delta, ld, rows, u, partial);
+    pdl_launch(bias_update_cols_kernel, dim3((u + 31) / 32), dim3(dim3(32, 32)), 0, s, partial, u, chunks, bias, alpha, inv_b);
     return cudaGetLastError();
 }
 
@@ -874,7 +906,7 @@ cudaError_t launch_im2col_act(const float* x, int imgs, int hp, int wp, long lon
                               float* dst, long long ldc, cudaStream_t s) {
     const long long n = static_cast<long long>(imgs) * Ho * Wo * ldc;
     if (n <= 0) return cudaSuccess;
-    im2col_act_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, imgs, hp, wp, ldx, C, k, Ho, Wo, dst, ldc);
+    pdl_launch(im2col_act_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, x, imgs, hp, wp, ldx, C, k, Ho, Wo, dst, ldc);
     return cudaGetLastError();
 }
 
@@ -883,7 +915,7 @@ cudaError_t launch_col2im(const float* dcols, long long ldk, int imgs, int H, in
     const long long n = static_cast<long long>(imgs) * H * W * nc;
     if (n <= 0) return cudaSuccess;
     const int Ho = H + 2 * p - k + 1, Wo = W + 2 * p - k + 1;
-    col2im_kernel<<<grid_for(n, 256), 256, 0, s>>>(dcols, ldk, imgs, H, W, C, k, p, Ho, Wo, c0, nc, dst, ldo);
+    pdl_launch(col2im_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, dcols, ldk, imgs, H, W, C, k, p, Ho, Wo, c0, nc, dst, ldo);
     return cudaGetLastError();
 }
 
@@ -901,14 +933,14 @@ cudaError_t launch_dense_conv_fold_sgd(const DenseConvGeom& g, const float* dWx,
     if (n <= 0) return cudaSuccess;
     if (g.k == 3 && g.pad == 1 && g.H == 2 && g.W == 2 && g.Ho == 2 && g.Wo == 2) {
         const unsigned blocks = static_cast<unsigned>((n + 255) / 256) + (bias != nullptr ? (g.u + 31) / 32 : 0);
-        dense_conv_update_2x2_kernel<<<blocks, 256, 0, s>>>(g, dWx, W, Wx, alpha, inv_b, flag, bpart, bchunks, bias);
+        pdl_launch(dense_conv_update_2x2_kernel, dim3(blocks), dim3(256), 0, s, g, dWx, W, Wx, alpha, inv_b, flag, bpart, bchunks, bias);
         return cudaGetLastError();
     }
     if (bias != nullptr) {
         cudaError_t e = launch_bias_from_partials(bpart, bchunks, g.u, bias, alpha, inv_b, s);
         if (e != cudaSuccess) return e;
     }
-    dense_conv_fold_sgd_kernel<<<grid_for(n, 256), 256, 0, s>>>(g, dWx, W, Wx, alpha, inv_b, flag);
+    pdl_launch(dense_conv_fold_sgd_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, g, dWx, W, Wx, alpha, inv_b, flag);
     return cudaGetLastError();
 }
 
@@ -953,11 +985,11 @@ cudaError_t launch_pool_fwd(const float* U, long long ldu, int imgs, int Ho, int
     for (int d = 0; d < dsts.n; ++d) v4 = v4 && reinterpret_cast<uintptr_t>(dsts.ptr[d]) % 16 == 0;
     const bool i32 = n < (1LL << 31);
     if (v4) {
-        if (i32) pool_fwd_kernel<4, unsigned><<<grid_for(n / 4, 256), 256, 0, s>>>(U, ldu, imgs, Ho, Wo, uch, pool, argmax, out, dsts);
-        else pool_fwd_kernel<4, long long><<<grid_for(n / 4, 256), 256, 0, s>>>(U, ldu, imgs, Ho, Wo, uch, pool, argmax, out, dsts);
+        if (i32) pdl_launch(pool_fwd_kernel<4, unsigned>, dim3(grid_for(n / 4, 256)), dim3(256), 0, s, U, ldu, imgs, Ho, Wo, uch, pool, argmax, out, dsts);
+        else pdl_launch(pool_fwd_kernel<4, long long>, dim3(grid_for(n / 4, 256)), dim3(256), 0, s, U, ldu, imgs, Ho, Wo, uch, pool, argmax, out, dsts);
     } else {
-        if (i32) pool_fwd_kernel<1, unsigned><<<grid_for(n, 256), 256, 0, s>>>(U, ldu, imgs, Ho, Wo, uch, pool, argmax, out, dsts);
-        else pool_fwd_kernel<1, long long><<<grid_for(n, 256), 256, 0, s>>>(U, ldu, imgs, Ho, Wo, uch, pool, argmax, out, dsts);
+        if (i32) pdl_launch(pool_fwd_kernel<1, unsigned>, dim3(grid_for(n, 256)), dim3(256), 0, s, U, ldu, imgs, Ho, Wo, uch, pool, argmax, out, dsts);
+        else pdl_launch(pool_fwd_kernel<1, long long>, dim3(grid_for(n, 256)), dim3(256), 0, s, U, ldu, imgs, Ho, Wo, uch, pool, argmax, out, dsts);
     }
     return cudaGetLastError();
 }
@@ -980,13 +1012,13 @@ cudaError_t launch_conv_merge(const ConvMerge& m, float* db_partial, cudaStream_
     }
     const bool i32 = n < (1LL << 31);
     if (v4 && (m.pool == 1 || m.pool == 2)) {
-        conv_merge_rows_kernel<2><<<grid, block, shmem, s>>>(m, db_partial);
+        pdl_launch(conv_merge_rows_kernel<2>, dim3(grid), dim3(block), shmem, s, m, db_partial);
     } else if (v4) {
-        if (i32) conv_merge_kernel<4, unsigned><<<grid, block, shmem, s>>>(m, db_partial);
-        else conv_merge_kernel<4, long long><<<grid, block, shmem, s>>>(m, db_partial);
+        if (i32) pdl_launch(conv_merge_kernel<4, unsigned>, dim3(grid), dim3(block), shmem, s, m, db_partial);
+        else pdl_launch(conv_merge_kernel<4, long long>, dim3(grid), dim3(block), shmem, s, m, db_partial);
     } else {
-        if (i32) conv_merge_kernel<1, unsigned><<<grid, block, shmem, s>>>(m, db_partial);
-        else conv_merge_kernel<1, long long><<<grid, block, shmem, s>>>(m, db_partial);
+        if (i32) pdl_launch(conv_merge_kernel<1, unsigned>, dim3(grid), dim3(block), shmem, s, m, db_partial);
+        else pdl_launch(conv_merge_kernel<1, long long>, dim3(grid), dim3(block), shmem, s, m, db_partial);
     }
     return cudaGetLastError();
 }
@@ -994,14 +1026,14 @@ cudaError_t launch_conv_merge(const ConvMerge& m, float* db_partial, cudaStream_
 cudaError_t launch_bias_from_partials(const float* partial, int chunks, int u, float* bias, const double* alpha,
                                       float inv_b, cudaStream_t s) {
     if (u <= 0) return cudaSuccess;
-    bias_update_cols_kernel<<<(u + 31) / 32, dim3(32, 32), 0, s>>>(partial, u, chunks, bias, alpha, inv_b);
+    pdl_launch(bias_update_cols_kernel, dim3((u + 31) / 32), dim3(dim3(32, 32)), 0, s, partial, u, chunks, bias, alpha, inv_b);
     return cudaGetLastError();
 }
 
 cudaError_t launch_finalize(StepState* st, const double* loss_row, const int* correct_row, int b,
                             double* loss_hist, double* acc_hist, int hist_cap, int write_hist,
                             cudaStream_t s) {
-    finalize_kernel<<<1, kRowThreads, 0, s>>>(st, loss_row, correct_row, b, loss_hist, acc_hist,
+    pdl_launch(finalize_kernel, dim3(1), dim3(kRowThreads), 0, s, st, loss_row, correct_row, b, loss_hist, acc_hist,
                                               hist_cap, write_hist);
     return cudaGetLastError();
 }
