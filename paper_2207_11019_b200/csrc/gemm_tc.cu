@@ -1045,8 +1045,15 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
             const int waves = (work + units - 1) / units;
             const double fill = static_cast<double>(work) / (static_cast<double>(waves) * units);
             const double frac = static_cast<double>(d.M) / (num_m * tm) * static_cast<double>(d.N) / (num_n * c.bn);
-            const double score = c.eff * fill * frac;
-            if (score > best + 1e-9) {
+            // estimated time: MMA at the shape's efficiency, plus the split-K
+            // reduction pass (partials re-read from L2 + the epilogue's write +
+            // a launch) unless it is a wgrad+SGD, whose reduction rides in the
+            // next GEMM's mainloop (SideJob)
+            const int sp = work / tiles;
+            double t = 2.0 * d.M * d.N * d.K / (806e12 * c.eff * fill * frac);
+            if (sp > 1 && d.epi.mode != EPI_SGD) t += (sp + 1.0) * d.M * d.N * 4.0 / 8e12 + 3e-6;
+            const double score = 1.0 / t;
+            if (score > best * (1.0 + 1e-9)) {
                 best = score;
                 cg = c.cg;
                 bn = c.bn;
