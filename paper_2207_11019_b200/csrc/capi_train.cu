@@ -176,9 +176,7 @@ extern "C" int ppb_session_step(ppb_session* s, int iterations) {
 
 extern "C" int ppb_session_step_host(ppb_session* s, const float* X, const int* labels, double* loss_out) {
     return ppb_guard([&] {
-        s->s->load_batch(nullptr, X, labels);
-        s->s->step(1);
-        const double v = s->s->last_loss();
+        const double v = s->s->step_host(X, labels);
         if (loss_out) *loss_out = v;
     });
 }

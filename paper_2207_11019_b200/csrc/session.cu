@@ -228,6 +228,7 @@ Session::Session(const std::vector<int>& device_map, const NetDesc& net, const d
 }
 
 Session::~Session() {
+    if (loss_pinned_ != nullptr) cudaFreeHost(loss_pinned_);
     for (auto& g : gpus_) {
         cudaSetDevice(g->ordinal);
         cudaDeviceSynchronize();
@@ -1676,6 +1677,20 @@ void Session::history(double* loss, double* acc, int cap, int* count) {
         if (acc) acc[i] = ah[(first + i) % hist_cap_];
     }
     if (count) *count = n;
+}
+
+double Session::step_host(const float* X, const int* labels) {
+    load_batch(nullptr, X, labels);
+    step(1);
+    Gpu& g = gpu_of(main_gpu_);
+    if (loss_pinned_ == nullptr) check(cudaMallocHost(&loss_pinned_, sizeof(double)), "pinned loss");
+    check(cudaSetDevice(g.ordinal), "cudaSetDevice");
+    if (g.ordinal != gpus_[0]->ordinal) check(cudaStreamWaitEvent(g.main, gpus_[0]->ev_done, 0), "wait");
+    check(cudaMemcpyAsync(loss_pinned_, g.loss_hist + (steps_enqueued_ - 1) % hist_cap_, sizeof(double),
+                          cudaMemcpyDeviceToHost, g.main),
+          "D2H loss");
+    check(cudaStreamSynchronize(g.main), "sync");
+    return *loss_pinned_;
 }
 
 double Session::last_loss() {

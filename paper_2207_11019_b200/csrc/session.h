@@ -117,6 +117,7 @@ class Session {
     int profile_ops(int* kind, int* layer, int* info, double* ms, double* flops, int cap);
     int profile_starts(double* start_ms, int* stream_id, int cap);
     double last_loss();
+    double step_host(const float* X, const int* labels);  // load + one step + loss, one stream sync
 
   private:
     struct Gpu;
@@ -175,6 +176,7 @@ class Session {
     bool pending_acc_error_ = false;
     int cur_layer_ = 0, cur_info_ = 0;
     std::vector<double> last_op_ms_;
+    double* loss_pinned_ = nullptr;  // pinned host slot for step_host's loss read-back
     std::vector<double> last_op_start_;  // ms from the first timed op (same device), last profile iteration
 };
 
