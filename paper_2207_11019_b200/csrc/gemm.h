@@ -191,9 +191,16 @@ struct HaloGeom {
 // fixed butterfly.
 struct SideJob {
     int on = 0;
+    int kind = 0;  // 0: split-K reduction (sk, epi, M, N); 1: dense-conv 2x2 weight update
     int M = 0, N = 0;
-    SplitK sk;
-    EpiParams epi;
+    SplitK sk;     // kind 1: only the bias job fields (bpart, bias, bchunks, bu)
+    EpiParams epi; // kind 1: alpha, inv_b, flag
+    // kind 1 (kernels.h DenseConvGeom for 3x3 / pad 1 / 2x2): dWx -> W, Wx
+    const float* dWx = nullptr;
+    float* Wm = nullptr;
+    float* Wx = nullptr;
+    int dc_u = 0, dc_C = 0, dc_ck = 0;
+    long long dc_ldw = 0, dc_ldx = 0;
 };
 
 struct GemmDesc {

@@ -30,6 +30,7 @@
 #include <cstring>
 #include <mutex>
 
+#include "dense_conv.cuh"
 #include "epilogue.cuh"
 #include "gemm_tc.h"
 #include "ptx.cuh"
@@ -132,6 +133,19 @@ __device__ __forceinline__ void run_side_job(const SideJob& sj, long long gt, lo
             acc += __shfl_xor_sync(0xffffffffu, acc, 4);
             if (ph == 0 && col < sk.bu) sk.bias[col] -= static_cast<float>(*sj.epi.alpha) * (acc * sj.epi.inv_b);
         }
+    }
+    if (sj.kind == 1) {  // dense-conv fold + SGD + re-expansion, one (co, ci) pair per item
+        DenseConvGeom g;
+        g.u = sj.dc_u;
+        g.C = sj.dc_C;
+        g.ck = sj.dc_ck;
+        g.ldw = sj.dc_ldw;
+        g.ldx = sj.dc_ldx;
+        const float a = static_cast<float>(*sj.epi.alpha);
+        const long long items = static_cast<long long>(g.u) * g.C;
+        for (long long it = gt; it < items; it += nt)
+            dense_conv_update_2x2_item(g, sj.dWx, sj.Wm, sj.Wx, a, sj.epi.inv_b, sj.epi.flag, it);
+        return;
     }
     const long long R = sk.trans ? sj.N : sj.M, Cc = sk.trans ? sj.M : sj.N;
     const long long items = R * ((Cc + 3) / 4);

@@ -8,6 +8,7 @@
 
 #include "kernels.h"
 #include "ptx.cuh"
+#include "dense_conv.cuh"
 
 namespace ppb {
 
@@ -460,8 +461,10 @@ __global__ void __launch_bounds__(256) dense_conv_update_2x2_kernel(
         __shared__ float bsh[8][33];
         const int t = threadIdx.x, col = (blockIdx.x - main_blocks) * 32 + (t & 31), y = t >> 5;
         float acc = 0.f;
-        if (col < g.u)
+        if (col < g.u) {
+#pragma unroll 8
             for (int k = y; k < bchunks; k += 8) acc += bpart[static_cast<long long>(k) * g.u + col];
+        }
         bsh[y][t & 31] = acc;
         __syncthreads();
         if (y == 0 && col < g.u) {
@@ -474,36 +477,7 @@ __global__ void __launch_bounds__(256) dense_conv_update_2x2_kernel(
     }
     const long long i = blockIdx.x * 256LL + threadIdx.x;
     if (i >= total) return;
-    const int co = static_cast<int>(i / g.C), ci = static_cast<int>(i % g.C);
-    float v[4][4];
-#pragma unroll
-    for (int p = 0; p < 4; ++p)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) v[p][q] = dWx[static_cast<long long>(p * g.u + co) * g.ldx + q * g.C + ci];
-    float gs[9];
-#pragma unroll
-    for (int t = 0; t < 9; ++t) gs[t] = 0.f;
-#pragma unroll
-    for (int p = 0; p < 4; ++p)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) gs[((q >> 1) - (p >> 1) + 1) * 3 + ((q & 1) - (p & 1) + 1)] += v[p][q];
-    bool bad = false;
-    float wn[9];
-    float* wr = W + co * g.ldw + ci;
-#pragma unroll
-    for (int t = 0; t < 9; ++t) {
-        const float gr = gs[t] * inv_b;
-        bad |= !isfinite(gr);
-        wn[t] = wr[t * g.ck] - a * gr;
-        wr[t * g.ck] = wn[t];
-    }
-    if (bad && flag != nullptr) atomicOr(flag, 1);
-#pragma unroll
-    for (int p = 0; p < 4; ++p)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            Wx[static_cast<long long>(p * g.u + co) * g.ldx + q * g.C + ci] =
-                wn[((q >> 1) - (p >> 1) + 1) * 3 + ((q & 1) - (p & 1) + 1)];
+    dense_conv_update_2x2_item(g, dWx, W, Wx, a, inv_b, flag, i);
 }
 
 __global__ void dense_conv_fold_sgd_kernel(DenseConvGeom g, const float* __restrict__ dWx, float* __restrict__ W,

@@ -4,6 +4,7 @@
 #include "session.h"
 
 #include "conv.h"
+#include "dense_conv.cuh"
 
 #include <algorithm>
 #include <chrono>
@@ -80,6 +81,7 @@ struct Session::WLayer {
     long long ldwx = 0;
     DenseConvGeom dcg;
     bool merge_fused = false;            // conv: delta written by the dgrad epilogue (EPI_MERGE)
+    bool fold_deferred = false;          // dense conv: weight update carried by the next wgrad GEMM
     bool db_colsum = false;              // fused merge without in-epilogue bias partials: column-sum pass
     int db_q = 1;                        // bias partial rows per merge block (dense-conv dgrad: one per position)
     std::vector<std::vector<int>> delta_ready;  // [j] -> op ids that produce delta rows of micro-batch j
@@ -1187,12 +1189,24 @@ void Session::build_ops() {
         // wgrads in backward order (top layer first: each can start as soon as
         // its delta exists); a split-K wgrad's reduction + SGD is carried by the
         // next wgrad GEMM on the stream (SideJob) instead of its own kernel
+        // pending side job: the previous split-K wgrad's reduction, or the
+        // previous dense-conv layer's weight update (its op is then a no-op)
         TcGemmPlan* prev_plan = nullptr;
         int prev_op = -1;
+        SideJob pend_fold;
+        bool* pend_flag = nullptr;
+        int pend_fold_op = -1;
         auto link_side = [&](TcGemmPlan* p, int op, bool carrier_ok) {
             if (!tf32) return;
-            if (prev_plan != nullptr && carrier_ok && !no_side && p->halo == 0 && prev_plan->sk.splits > 1 &&
-                !prev_plan->sk.fixup && !prev_plan->sk.deferred) {
+            const bool can = carrier_ok && !no_side && p->halo == 0;
+            if (pend_flag != nullptr) {
+                if (can) {
+                    p->sj = pend_fold;
+                    *pend_flag = true;
+                    ops_[pend_fold_op].kernels -= 1;
+                }
+            } else if (prev_plan != nullptr && can && prev_plan->sk.splits > 1 && !prev_plan->sk.fixup &&
+                       !prev_plan->sk.deferred) {
                 p->sj.on = 1;
                 p->sj.M = prev_plan->M;
                 p->sj.N = prev_plan->N;
@@ -1201,6 +1215,7 @@ void Session::build_ops() {
                 prev_plan->sk.deferred = 1;
                 ops_[prev_op].kernels -= 1;
             }
+            pend_flag = nullptr;
             prev_plan = p;
             prev_op = op;
         };
@@ -1319,9 +1334,38 @@ void Session::build_ops() {
                 int* flag = &g.st->diverge_flag;
                 const float* bp = from_merge ? partial : nullptr;
                 float* bb = from_merge ? bias : nullptr;
-                add_op(w.gpu, s, [=]() {
+                bool* deferred = &wl.fold_deferred;
+                const int fop = add_op(w.gpu, s, [=]() {
+                    if (*deferred) return cudaSuccess;  // carried by the next wgrad GEMM (SideJob)
                     return launch_dense_conv_fold_sgd(dg, dWx, Wp, Wx, alpha, inv_b, flag, s, bp, chunks, bb);
                 }, {gop}, 1, OP_BIAS);
+                // carrying the update in the next wgrad GEMM measured slower (2.287
+                // vs 2.281 ms: its 51 MB of traffic slows that GEMM's mainloop more
+                // than the low-priority kernel costs), so it is opt-in
+                static const bool fold_side = getenv("PPB_FOLD_SIDE") != nullptr;
+                if (tf32 && dense_conv_is_2x2(dg) && fold_side) {  // offer the update to the next wgrad GEMM
+                    SideJob& f = pend_fold;
+                    f = SideJob{};
+                    f.on = 1;
+                    f.kind = 1;
+                    f.dWx = dWx;
+                    f.Wm = Wp;
+                    f.Wx = Wx;
+                    f.dc_u = dg.u;
+                    f.dc_C = dg.C;
+                    f.dc_ck = dg.ck;
+                    f.dc_ldw = dg.ldw;
+                    f.dc_ldx = dg.ldx;
+                    f.epi.alpha = alpha;
+                    f.epi.inv_b = inv_b;
+                    f.epi.flag = flag;
+                    f.sk.bpart = bp;
+                    f.sk.bias = bb;
+                    f.sk.bchunks = chunks;
+                    f.sk.bu = u;
+                    pend_flag = deferred;
+                    pend_fold_op = fop;
+                }
                 continue;
             }
             if (from_merge && splits > 1 && !wl.p_wgrad.sk.fixup) {
