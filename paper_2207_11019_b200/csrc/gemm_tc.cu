@@ -378,7 +378,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     N - nn < 32 ? N - nn : 32, v);
                     }
                 } else {
-                    if (ts.n && ts.mask) {
+                    if (ts.n && ts.pool2) {
+                        uint8_t* buf = stg + (warp - 4) * 4096;
+                        if (ts.mask) tma_mask_chunk(ts, buf, mbar, mphase, lane, v, m0 + q * 32, n0 + c * 32);
+                        uint32_t code[8];
+                        const unsigned char* ap =
+                            epi.mg_argmax + static_cast<long long>(m < M ? m : 0) * epi.mg_uch + n0 + c * 32;
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) code[i] = m < M ? __ldg(reinterpret_cast<const uint32_t*>(ap) + i) : 0u;
+                        tma_merge_pool2_chunk(ts, buf, lane, v, code, m0 + q * 32, n0 + c * 32);
+                    } else if (ts.n && ts.mask) {
                         tma_store_chunk_masked(ts, stg + (warp - 4) * 4096, mbar, mphase, lane, v, m0 + q * 32,
                                                n0 + c * 32);
                     } else if (ts.n) {
@@ -683,14 +692,89 @@ bool encode_conv_map(CUtensorMap* map, const Operand& o, char* err, size_t errle
 
 // ---------------------------------------------------------------- TMA-store epilogue setup
 
+// EPI_MERGE through a 2x2 pool (tc kernel rows = pooled pixels): the
+// error-signal map traverses the full grid with element stride 2 in w and h,
+// so the box of 32 pooled pixels' quadrant q lands on positions
+// (2y + dy, 2x + dx); the mask map covers the pooled activation.
+static bool tma_store_setup_pool2(const EpiParams& e, int M, int N, TmaStore* ts) {
+    auto enc = get_encode();
+    static const bool off = getenv("PPB_NO_TMA_POOL2") != nullptr;
+    if (off || enc == nullptr || N % 32 != 0 || M <= 0 || e.mg_dld % 4 != 0 || e.mg_uch % 4 != 0 ||
+        (reinterpret_cast<uintptr_t>(e.mg_argmax) & 3u) != 0)
+        return false;
+    const int wo = e.mg_wg, ho = e.mg_hg, pix = wo * ho;
+    if (pix <= 0 || M % pix != 0 || 2 * wo > 256 || 2 * ho > 256) return false;
+    cuuint32_t box[4] = {32u, 32u, 1u, 1u};
+    if (wo >= 32) {
+        if (wo % 32 != 0) return false;
+    } else if (32 % wo != 0) {
+        return false;
+    } else if (pix >= 32) {
+        if (pix % 32 != 0) return false;
+        box[1] = wo;
+        box[2] = 32 / wo;
+    } else {
+        if (32 % pix != 0) return false;
+        box[1] = wo;
+        box[2] = ho;
+        box[3] = 32 / pix;
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, e.mg_d) != cudaSuccess || a.type != cudaMemoryTypeDevice || a.device != dev) {
+        cudaGetLastError();
+        return false;
+    }
+    if ((reinterpret_cast<uintptr_t>(e.mg_d) & 15u) != 0) return false;
+    const long long ld = e.mg_dld;
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(2 * wo), static_cast<cuuint64_t>(2 * ho),
+                          static_cast<cuuint64_t>(M / pix)};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(ld) * 4, static_cast<cuuint64_t>(e.mg_dwp) * ld * 4,
+                             static_cast<cuuint64_t>(e.mg_dhp) * e.mg_dwp * ld * 4};
+    cuuint32_t sbox[4] = {32u, 2 * box[1], 2 * box[2], box[3]};
+    cuuint32_t sestr[4] = {1u, 2u, 2u, 1u};
+    float* base = e.mg_d + (static_cast<long long>(e.mg_dpad) * e.mg_dwp + e.mg_dpad) * ld;
+    if (enc(&ts->map[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, base, dims, strides, sbox, sestr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    ts->mask = 0;
+    if (e.mg_mask != nullptr) {
+        const float* mptr = e.mg_mask + e.mg_mcol0;
+        const long long mld = e.mg_mld;
+        if ((reinterpret_cast<uintptr_t>(mptr) & 15u) != 0 || mld % 4 != 0) return false;
+        cuuint64_t mdims[4] = {static_cast<cuuint64_t>(N), static_cast<cuuint64_t>(wo), static_cast<cuuint64_t>(ho),
+                               static_cast<cuuint64_t>(M / pix)};
+        cuuint64_t mstr[3] = {static_cast<cuuint64_t>(mld) * 4, static_cast<cuuint64_t>(e.mg_mwp) * mld * 4,
+                              static_cast<cuuint64_t>(e.mg_mhp) * e.mg_mwp * mld * 4};
+        cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+        const float* mbase = mptr + (static_cast<long long>(e.mg_mpad) * e.mg_mwp + e.mg_mpad) * mld;
+        if (enc(&ts->mmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(mbase), mdims, mstr, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+        ts->mask = 1;
+    }
+    ts->rank = 4;
+    ts->wo = wo;
+    ts->pix = pix;
+    ts->segw = 0;
+    ts->pool2 = 1;
+    ts->n = 1;
+    return true;
+}
+
 bool tma_store_setup(const EpiParams& e, int M, int N, const HaloGeom* hg, TmaStore* ts) {
     ts->n = 0;
+    ts->pool2 = 0;
     static const bool off = [] {
         const char* v = getenv("PPB_NO_TMA_STORE");
         return v != nullptr && *v != '\0' && *v != '0';
     }();
     auto enc = get_encode();
     if (off || enc == nullptr || N < 32 || M <= 0) return false;
+    if (e.mode == EPI_MERGE && e.mg_pool == 2) return hg == nullptr && tma_store_setup_pool2(e, M, N, ts);
     float* ptrs[kMaxDst];
     int nd = 0;
     long long ld = 0;

@@ -37,6 +37,7 @@ struct TmaStore {
     int stage_off = 0;  // staging offset (bytes) past the kernel's barrier block
     int tr = 0;         // rank 3 (split-K workspace [split][rows][ld]): 1 = [n][m] (dW^T)
     int segw = 0;       // rank 3 segmented columns (dense conv): box at (n % segw, n / segw, row)
+    int pool2 = 0;      // EPI_MERGE through a 2x2 pool: 4 quadrant stores with a stride-2 map
     // ReLU mask of EPI_MERGE (pool 1) / EPI_MASK, same box geometry as the
     // store: TMA-loaded into the staging box (one mbarrier per epilogue warp
     // after the staging boxes), then applied from shared memory
@@ -130,6 +131,66 @@ __device__ __forceinline__ void tma_store_chunk_masked(const TmaStore& ts, uint8
             for (int d = 0; d < ts.n; ++d) tma_store_4d(&ts.map[d], buf, n, w, h, img);
         }
         bulk_commit();
+    }
+}
+
+// ReLU mask of the chunk (TMA-loaded box) applied in registers, no store.
+__device__ __forceinline__ void tma_mask_chunk(const TmaStore& ts, uint8_t* buf, uint64_t* bar, uint32_t& phase,
+                                               int lane, float (&v)[32], int r0, int n) {
+    if (lane == 0) {
+        bulk_wait_read<0>();
+        mbar_arrive_expect_tx(bar, 4096);
+        const int img = r0 / ts.pix, rem = r0 - img * ts.pix;
+        const int h = rem / ts.wo, w = rem - h * ts.wo;
+        tma_load_4d(buf, &ts.mmap, bar, n, w, h, img);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    const uint32_t row = smem_u32(buf) + lane * 128;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        float m0, m1, m2, m3;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(m0), "=f"(m1), "=f"(m2), "=f"(m3)
+                     : "r"(row + ((j ^ (lane & 7)) << 4)));
+        v[4 * j] = m0 > 0.f ? v[4 * j] : 0.f;
+        v[4 * j + 1] = m1 > 0.f ? v[4 * j + 1] : 0.f;
+        v[4 * j + 2] = m2 > 0.f ? v[4 * j + 2] : 0.f;
+        v[4 * j + 3] = m3 > 0.f ? v[4 * j + 3] : 0.f;
+    }
+    __syncwarp();
+}
+
+// Backward merge through a 2x2 max-pool: row r0 + lane = pooled pixel, its 32
+// channels route to the argmax position of their window (code byte q =
+// dy*2 + dx, zeros elsewhere).  Quadrant q of the 32 pooled pixels is one box
+// of a stride-2 tensor map over the error signal's interior, so the four
+// quadrants are four bulk stores (staged one after the other).
+__device__ __forceinline__ void tma_merge_pool2_chunk(const TmaStore& ts, uint8_t* buf, int lane, const float (&v)[32],
+                                                      const uint32_t (&code)[8], int r0, int n) {
+    const int img = r0 / ts.pix, rem = r0 - img * ts.pix;
+    const int h = rem / ts.wo, w = rem - h * ts.wo;
+    const uint32_t row = smem_u32(buf) + lane * 128;
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q) {
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float o[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = 4 * j + k;
+                o[k] = ((code[i >> 2] >> (8 * (i & 3))) & 0xffu) == static_cast<uint32_t>(q) ? v[i] : 0.f;
+            }
+            st_shared_v4(row + ((j ^ (lane & 7)) << 4), o[0], o[1], o[2], o[3]);
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_4d(&ts.map[0], buf, n, 2 * w + (q & 1), 2 * h + (q >> 1), img);
+            bulk_commit();
+        }
     }
 }
 
