@@ -1119,6 +1119,7 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
     // force_bn: 0 = auto; 64/128/256 = 1-CTA tiles of that width;
     // -128/-256 = CTA-pair tiles (256 x |bn|).
     int bn = 256, cg = 1;
+    int best_sp = -1;  // split count chosen with the tile shape (-1: splits_for)
     if (force_bn == 64 || force_bn == 128 || force_bn == 256) {
         bn = force_bn;
     } else if (force_bn == -128 || force_bn == -256) {
@@ -1139,22 +1140,25 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
             const int tm = kBM * c.cg;
             const int num_m = (d.M + tm - 1) / tm, num_n = (d.N + c.bn - 1) / c.bn;
             const int tiles = num_m * num_n, units = sms / c.cg;
-            const int work = tiles * splits_for(tiles, units);
-            const int waves = (work + units - 1) / units;
-            const double fill = static_cast<double>(work) / (static_cast<double>(waves) * units);
             const double frac = static_cast<double>(d.M) / (num_m * tm) * static_cast<double>(d.N) / (num_n * c.bn);
-            // estimated time: MMA at the shape's efficiency, plus the split-K
-            // reduction pass (partials re-read from L2 + the epilogue's write +
-            // a launch) unless it is a wgrad+SGD, whose reduction rides in the
-            // next GEMM's mainloop (SideJob)
-            const int sp = work / tiles;
-            double t = 2.0 * d.M * d.N * d.K / (806e12 * c.eff * fill * frac);
-            if (sp > 1 && d.epi.mode != EPI_SGD) t += (sp + 1.0) * d.M * d.N * 4.0 / 8e12 + 3e-6;
-            const double score = 1.0 / t;
-            if (score > best * (1.0 + 1e-9)) {
-                best = score;
-                cg = c.cg;
-                bn = c.bn;
+            // with and without split-K
+            for (int sp : {1, splits_for(tiles, units)}) {
+                const int work = tiles * sp;
+                const int waves = (work + units - 1) / units;
+                const double fill = static_cast<double>(work) / (static_cast<double>(waves) * units);
+                // estimated time: MMA at the shape's efficiency, plus the split-K
+                // reduction pass (partials re-read from L2 + the epilogue's write +
+                // a launch) unless it is a wgrad+SGD, whose reduction rides in the
+                // next GEMM's mainloop (SideJob)
+                double t = 2.0 * d.M * d.N * d.K / (806e12 * c.eff * fill * frac);
+                if (sp > 1 && d.epi.mode != EPI_SGD) t += (sp + 1.0) * d.M * d.N * 4.0 / 8e12 + 3e-6;
+                const double score = 1.0 / t;
+                if (score > best * (1.0 + 1e-9)) {
+                    best = score;
+                    cg = c.cg;
+                    bn = c.bn;
+                    best_sp = sp;
+                }
             }
         }
     }
@@ -1166,7 +1170,7 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
     // small C_out x 9*C_in output, K = every pixel of the batch); partial
     // sums are reduced in split order (deterministic).
     {
-        int splits = splits_for(tiles, units);
+        int splits = best_sp > 0 ? best_sp : splits_for(tiles, units);
         if (splits >= 2) {
             const int kps = (nk + splits - 1) / splits;
             splits = (nk + kps - 1) / kps;
