@@ -69,7 +69,7 @@ __device__ __forceinline__ void splitk_item_seq(const EpiParams& epi, const Spli
     float a[4] = {0.f, 0.f, 0.f, 0.f};
     // association of splitk_epilogue_kernel: sequential for < 16 splits;
     // otherwise 8 phase sums (splits p, p+8, ...) added in phase order
-    const int nph = sk.splits >= 16 ? 8 : 1;
+    const int nph = sk.splits >= 64 ? 32 : sk.splits >= 16 ? 8 : 1;
 #pragma unroll 1
     for (int ph = 0; ph < nph; ++ph) {
         float b[4] = {0.f, 0.f, 0.f, 0.f};
@@ -1063,7 +1063,11 @@ cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
     ra[0].val.programmaticStreamSerializationAllowed = 1;
     rc.attrs = ra;
     rc.numAttrs = pdl_enabled() ? 1 : 0;
-    if (p.sk.splits >= 16) {
+    if (p.sk.splits >= 64) {  // e.g. conv1's 148-way wgrad: 8 items x 32 phases per block
+        rc.gridDim = dim3(static_cast<unsigned>((items + 7) / 8) + bblocks);
+        rc.blockDim = dim3(8, 32);
+        e = cudaLaunchKernelEx(&rc, splitk_epilogue_kernel<32>, p.epi, p.sk, p.M, p.N);
+    } else if (p.sk.splits >= 16) {
         rc.gridDim = dim3(static_cast<unsigned>((items + 31) / 32) + bblocks);
         rc.blockDim = dim3(32, 8);
         e = cudaLaunchKernelEx(&rc, splitk_epilogue_kernel<8>, p.epi, p.sk, p.M, p.N);

@@ -456,26 +456,22 @@ __global__ void __launch_bounds__(256) dense_conv_update_2x2_kernel(
     griddep_wait();  // programmatic launch: the predecessor's results are visible after this
     const float a = static_cast<float>(*alpha);
     const long long total = static_cast<long long>(g.u) * g.C;
-    const int main_blocks = static_cast<int>((total + 255) / 256);
-    if (static_cast<int>(blockIdx.x) >= main_blocks) {
-        __shared__ float bsh[8][33];
-        const int t = threadIdx.x, col = (blockIdx.x - main_blocks) * 32 + (t & 31), y = t >> 5;
+    // bias blocks first (they start with the grid): warp = column, lane =
+    // phase over the chunks (k = lane, lane + 32, ...), fixed butterfly
+    const int bblocks = bias != nullptr ? (g.u + 7) / 8 : 0;
+    if (static_cast<int>(blockIdx.x) < bblocks) {
+        const int col = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
         float acc = 0.f;
         if (col < g.u) {
 #pragma unroll 8
-            for (int k = y; k < bchunks; k += 8) acc += bpart[static_cast<long long>(k) * g.u + col];
+            for (int k = lane; k < bchunks; k += 32) acc += bpart[static_cast<long long>(k) * g.u + col];
         }
-        bsh[y][t & 31] = acc;
-        __syncthreads();
-        if (y == 0 && col < g.u) {
-            float s = 0.f;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) s += bsh[j][t & 31];
-            bias[col] -= a * (s * inv_b);
-        }
+        for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0 && col < g.u) bias[col] -= a * (acc * inv_b);
         return;
     }
-    const long long i = blockIdx.x * 256LL + threadIdx.x;
+    const long long i = (blockIdx.x - bblocks) * 256LL + threadIdx.x;
     if (i >= total) return;
     dense_conv_update_2x2_item(g, dWx, W, Wx, a, inv_b, flag, i);
 }
@@ -906,7 +902,7 @@ cudaError_t launch_dense_conv_fold_sgd(const DenseConvGeom& g, const float* dWx,
     const long long n = static_cast<long long>(g.u) * g.C;
     if (n <= 0) return cudaSuccess;
     if (g.k == 3 && g.pad == 1 && g.H == 2 && g.W == 2 && g.Ho == 2 && g.Wo == 2) {
-        const unsigned blocks = static_cast<unsigned>((n + 255) / 256) + (bias != nullptr ? (g.u + 31) / 32 : 0);
+        const unsigned blocks = static_cast<unsigned>((n + 255) / 256) + (bias != nullptr ? (g.u + 7) / 8 : 0);
         pdl_launch(dense_conv_update_2x2_kernel, dim3(blocks), dim3(256), 0, s, g, dWx, W, Wx, alpha, inv_b, flag, bpart, bchunks, bias);
         return cudaGetLastError();
     }
