@@ -1,7 +1,7 @@
 """Benchmark of the partitioned fwd+bwd+update step (BASELINE.json metric:
 "train samples/sec (fwd+bwd+update) at 1/2/4/8 B200; % tensor-core roofline").
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload vgg16|wide_mlp|mlp784]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload vgg16|wide_mlp|mlp784|lenet5]
                     [--impl ours|reference]
 
 Prints ONE JSON line (rank 0).  A "step" is one train_partitioned iteration
@@ -52,14 +52,16 @@ WORKLOADS = {
     "wide_mlp": dict(net="wide_mlp", batch=4096, classes=8192, name="Wide MLP 8192x4 layers, batch 4096"),
     # BASELINE.json configs[0]: latency-bound (0.2 GFLOP/step); reported, not a roofline target.
     "mlp784": dict(net="mlp784", batch=64, classes=10, name="MLP 784-512-512-10, batch 64"),
+    # BASELINE.json configs[1]: LeNet-5 on 28x28x1 (generic im2col conv path; latency-bound).
+    "lenet5": dict(net="lenet5", batch=256, classes=10, name="LeNet-5 (28x28x1, 5x5 convs), batch 256"),
 }
 
 
 def build_net(workload, seed=1):
     from paper_2207_11019_b200 import configs
 
-    return {"vgg16": configs.vgg16_cifar, "wide_mlp": configs.wide_mlp, "mlp784": configs.mlp784}[
-        WORKLOADS[workload]["net"]](seed=seed)
+    return {"vgg16": configs.vgg16_cifar, "wide_mlp": configs.wide_mlp, "mlp784": configs.mlp784,
+            "lenet5": configs.lenet5}[WORKLOADS[workload]["net"]](seed=seed)
 
 
 def layer_macs(layer, batch):
