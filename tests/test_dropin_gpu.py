@@ -33,3 +33,21 @@ def test_reference_verification_suite_on_gpu(precision, tol):
     assert rep["oracle-equivalence-sync"]["max_err"] <= tol
     for name in ("microbatch-invariance", "gradient-correctness", "shard-reassembly"):
         assert rep[name]["pass"], rep[name]
+
+
+def test_calibrated_optimize_plan_on_gpu(tmp_path):
+    """The reference's optimize_plan priced with per-layer seconds measured on
+    the B200 (dropin/optimize_main.cpp): a valid plan whose objective is no
+    worse than the default build_plan, and a calibrated model document."""
+    exe = os.path.join(ROOT, "dropin", "_build", "optimize_b200")
+    if not os.path.exists(exe):
+        pytest.skip("dropin/_build/optimize_b200 not built (needs the reference sources)")
+    model = tmp_path / "model.json"
+    out = subprocess.run([exe, "784,512,512,10", "2", "2", "64", str(model)], capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr
+    last = json.loads(out.stdout.strip().splitlines()[-1])
+    assert 0 < last["optimized_objective_s"] <= last["baseline_build_plan_Z1_objective_s"] * (1 + 1e-12)
+    assert last["measured_step_fwd_s"] > 0 and last["measured_step_bwd_s"] > 0
+    g = json.loads(model.read_text())
+    assert len(g["layers"]) == 3 and all(l["fwd_flops"] > 0 and l["bwd_flops"] > 0 for l in g["layers"])
