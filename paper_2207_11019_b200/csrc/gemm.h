@@ -192,6 +192,7 @@ struct HaloGeom {
 struct SideJob {
     int on = 0;
     int kind = 0;  // 0: split-K reduction (sk, epi, M, N); 1: dense-conv 2x2 weight update
+    int scalar = 0;  // reduction items one at a time (A/B probe)
     int M = 0, N = 0;
     SplitK sk;     // kind 1: only the bias job fields (bpart, bias, bchunks, bu)
     EpiParams epi; // kind 1: alpha, inv_b, flag

@@ -148,8 +148,78 @@ __device__ __forceinline__ void run_side_job(const SideJob& sj, long long gt, lo
         return;
     }
     const long long R = sk.trans ? sj.N : sj.M, Cc = sk.trans ? sj.M : sj.N;
-    const long long items = R * ((Cc + 3) / 4);
-    for (long long it = gt; it < items; it += nt) splitk_item_seq(sj.epi, sk, sj.M, sj.N, it);
+    const int cq = static_cast<int>((Cc + 3) / 4);
+    const long long items = R * cq;
+    // 4 items per thread per pass (independent load chains: each thread owns
+    // ~items / nt of them, so one-at-a-time would be latency-bound); full
+    // float4 items only, the ragged ones go through splitk_item_seq
+    const int nph = sk.splits >= 64 ? 32 : sk.splits >= 16 ? 8 : 1;
+    const bool vec_ok = (sk.ld & 3) == 0 && (Cc & 3) == 0 && !sj.scalar;
+    long long it = gt;
+    if (vec_ok) {
+        for (; it + 3 * nt < items; it += 4 * nt) {
+            float4 a[4];
+            long long off[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const long long t = it + i * nt;
+                const long long r = t / cq;
+                off[i] = r * sk.ld + (t - r * cq) * 4;
+                a[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll 1
+            for (int ph = 0; ph < nph; ++ph) {
+                float4 b[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) b[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 2
+                for (int sp = ph; sp < sk.splits; sp += nph) {
+                    const float* base = sk.ws + static_cast<long long>(sp) * sk.stride;
+                    float4 t[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) t[i] = __ldcg(reinterpret_cast<const float4*>(base + off[i]));
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        b[i].x += t[i].x;
+                        b[i].y += t[i].y;
+                        b[i].z += t[i].z;
+                        b[i].w += t[i].w;
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    a[i].x += b[i].x;
+                    a[i].y += b[i].y;
+                    a[i].z += b[i].z;
+                    a[i].w += b[i].w;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const long long t = it + i * nt;
+                const int r = static_cast<int>(t / cq);
+                const int c4 = static_cast<int>(t - static_cast<long long>(r) * cq) * 4;
+                const float av[4] = {a[i].x, a[i].y, a[i].z, a[i].w};
+                if (sk.trans) {
+                    const float alpha = static_cast<float>(*sj.epi.alpha);
+                    float* w = sj.epi.W + static_cast<long long>(r) * sj.epi.ldw + c4;
+                    bool bad = false;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const float g = av[j] * sj.epi.inv_b;
+                        bad |= !isfinite(g);
+                        w[j] -= alpha * g;
+                    }
+                    if (bad && sj.epi.flag != nullptr) atomicOr(sj.epi.flag, 1);
+                } else {
+                    const long long row_off = sj.epi.mode == EPI_STORE ? epi_store_row(sj.epi, r) : 0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) epilogue1(sj.epi, r, c4 + j, av[j], row_off);
+                }
+            }
+        }
+    }
+    for (; it < items; it += nt) splitk_item_seq(sj.epi, sk, sj.M, sj.N, it);
 }
 
 template <bool A_MN, bool B_MN, int BN, int CG>

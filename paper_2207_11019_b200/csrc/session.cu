@@ -1208,6 +1208,8 @@ void Session::build_ops() {
             } else if (prev_plan != nullptr && can && prev_plan->sk.splits > 1 && !prev_plan->sk.fixup &&
                        !prev_plan->sk.deferred) {
                 p->sj.on = 1;
+                static const bool side_scalar = getenv("PPB_SIDE_SCALAR") != nullptr;
+                p->sj.scalar = side_scalar ? 1 : 0;
                 p->sj.M = prev_plan->M;
                 p->sj.N = prev_plan->N;
                 p->sj.sk = prev_plan->sk;
