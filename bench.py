@@ -300,7 +300,15 @@ def run_ours(args, rank, world, dist):
     X = rng.standard_normal((batch, in_feat), dtype=np.float32)
     y = rng.integers(0, w["classes"], batch).astype(np.int32)
     plan = api.build_plan(net, n, 1)  # every layer over all n GPUs (build_plan, partition.cpp:110-121)
-    ctx = api.Context(list(range(n)))
+    # PPB_BENCH_PLAN_DEVICES=k (testing): a k-device plan with every plan device
+    # on cuda:0 (exercises the multi-device step on a one-GPU box)
+    plan_devs = int(os.environ.get("PPB_BENCH_PLAN_DEVICES", "0"))
+    if plan_devs > 1 and n == 1:
+        n = plan_devs
+        plan = api.build_plan(net, n, 1)
+        ctx = api.Context([0] * n)
+    else:
+        ctx = api.Context(list(range(n)))
     cfg = TrainConfig(alpha0=1e-4, decay=1e-2, iterations=1)
     opts = PartitionedTrainOptions(multiclass_accuracy=True, use_graph=True, pipeline_gate=2)
     sess = api.Session(ctx, net, batch, plan, args.m, UpdateMode.async_per_module, cfg, opts)
