@@ -227,6 +227,52 @@ __device__ __forceinline__ void db_accumulate(float* db_row, int n0, int N, floa
     if (n0 + lane < N) db_row[n0 + lane] += v[0];
 }
 
+// Fused 2x2 max-pool of a 32 x 32 chunk (EpiParams pl_*): all lanes call it
+// with their row's final values (after bias / ReLU); window partners are
+// lanes +1, +wo, +wo+1 of the same warp.
+__device__ __forceinline__ void epi_pool32(const EpiParams& p, int m, int n0, const float (&v)[32], int lane) {
+    const int wo = p.pl_wo, howo = p.pl_wo * p.pl_ho;
+    const int img = m / howo, rem = m - img * howo, h = rem / wo, w = rem - h * wo;
+    const bool leader = m < p.M && (h & 1) == 0 && (w & 1) == 0;
+    float out[32];
+    uint32_t code[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        const float e1 = __shfl_down_sync(0xffffffffu, v[i], 1);
+        const float e2 = __shfl_down_sync(0xffffffffu, v[i], wo);
+        const float e3 = __shfl_down_sync(0xffffffffu, v[i], wo + 1);
+        float b = v[i];
+        uint32_t q = 0;
+        if (e1 > b) { b = e1; q = 1; }
+        if (e2 > b) { b = e2; q = 2; }
+        if (e3 > b) { b = e3; q = 3; }
+        out[i] = b;
+        code[i >> 2] |= q << (8 * (i & 3));
+    }
+    if (!leader || n0 >= p.N) return;
+    const int nvalid = p.N - n0 < 32 ? p.N - n0 : 32;
+    const int Hq = p.pl_ho / 2, Wq = wo / 2, y = h / 2, x = w / 2;
+    const long long pp = (static_cast<long long>(img) * Hq + y) * Wq + x;
+    unsigned char* ap = p.pl_arg + pp * p.pl_uch + n0;
+    if (nvalid == 32 && (p.pl_uch & 3) == 0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) reinterpret_cast<uint32_t*>(ap)[i] = code[i];
+    } else {
+        for (int i = 0; i < nvalid; ++i) ap[i] = static_cast<unsigned char>((code[i >> 2] >> (8 * (i & 3))) & 0xffu);
+    }
+    if (p.pl_kind == 0) {
+        const long long o = ((static_cast<long long>(img) * p.pl_hp + y + p.pl_pad) * p.pl_wp + x + p.pl_pad) * p.pl_ld +
+                            p.pl_col0;
+        for (int d = 0; d < p.pl_ndst; ++d) store_row32(p.pl_dst[d] + o, n0, nvalid, out);
+    } else {
+        for (int i = 0; i < nvalid; ++i) {
+            const long long o = static_cast<long long>(img) * p.pl_ld +
+                                static_cast<long long>(p.pl_col0 + n0 + i) * Hq * Wq + static_cast<long long>(y) * Wq + x;
+            for (int d = 0; d < p.pl_ndst; ++d) p.pl_dst[d][o] = out[i];
+        }
+    }
+}
+
 // Row offset (elements) of output row m in the EPI_STORE destination.
 __device__ __forceinline__ long long epi_store_row(const EpiParams& p, int m) {
     if (!p.remap) return static_cast<long long>(m) * p.ldd;

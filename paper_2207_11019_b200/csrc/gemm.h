@@ -46,6 +46,22 @@ struct EpiParams {
     // an ho x wo grid lands at row ((img*hp + h + pad)*wp + w + pad).
     int remap = 0;
     int r_wo = 1, r_howo = 1, r_hp = 1, r_wp = 1, r_pad = 0;
+    // EPI_STORE + fused 2x2 max-pool (tc kernel; rows = pixels of a
+    // pl_ho x pl_wo grid with pl_wo <= 16, so each warp's 32 rows hold whole
+    // windows): the window's top-left lane writes the pooled value (first max
+    // wins in order (0,0),(0,1),(1,0),(1,1)) to pl_dst[d] in the consumer
+    // layout (pl_kind 0: padded NHWC pl_hp x pl_wp, pad pl_pad, pitch pl_ld;
+    // 1: CHW-flatten rows of pitch pl_ld) at channel pl_col0 + n, and the
+    // window code to pl_arg[pooled pixel * pl_uch + n]
+    int pl_on = 0;
+    int pl_wo = 1, pl_ho = 1;
+    float* pl_dst[kMaxDst] = {};
+    int pl_ndst = 0;
+    int pl_kind = 0;
+    long long pl_ld = 0;
+    int pl_hp = 1, pl_wp = 1, pl_pad = 0, pl_col0 = 0;
+    unsigned char* pl_arg = nullptr;
+    int pl_uch = 0;
     // EPI_STORE, segmented columns (dense conv: GEMM column n = (p, c) with
     // p = n / seg_w, c = n % seg_w): C(m, n) -> dst[m*ldd + p*seg_pitch + col0 + c],
     // bias indexed by c.  seg_w is a multiple of 32 (a chunk never straddles).

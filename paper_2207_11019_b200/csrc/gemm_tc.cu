@@ -463,8 +463,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     } else if (ts.n) {
                         epi_values32(epi, m, n0 + c * 32, v, lane);
                         if (!(epi.dbg & 2)) tma_store_chunk(ts, stg + (warp - 4) * 4096, lane, v, m0 + q * 32, n0 + c * 32);
+                        if (epi.pl_on) epi_pool32(epi, m, n0 + c * 32, v, lane);
                     } else if (!(epi.dbg & 2)) {
                         epilogue32(epi, m, n0 + c * 32, v);
+                        if (epi.pl_on) epi_pool32(epi, m, n0 + c * 32, v, lane);
                     }
                     if (db && n0 + c * 32 < N) {
                         if (m >= M) {

@@ -744,11 +744,37 @@ void Session::build_ops() {
                             d.epi.col0 = wl.lo;
                         }
                     }
+                    // 2x2 max-pool fused into the epilogue when each warp's 32 rows hold
+                    // whole windows (grid width <= 16); the GEMM must end up unsplit and
+                    // on the tc kernel, else the pool kernel runs as before
+                    static const bool no_pool_fuse = getenv("PPB_NO_POOL_FUSE") != nullptr;
+                    const int Wo1 = li.Wo(), Ho1 = li.Ho();
+                    if (tf32 && !no_pool_fuse && li.pool == 2 && wl.U != nullptr && !li.dense_conv && wl.argmax &&
+                        Wo1 >= 2 && 32 % (2 * Wo1) == 0 && Ho1 % 2 == 0 && (pix % 32 == 0 || 32 % pix == 0)) {
+                        const ActLayout& a = lay_[l];
+                        d.epi.pl_on = 1;
+                        d.epi.pl_wo = Wo1;
+                        d.epi.pl_ho = Ho1;
+                        for (int ord : dest_gpus) d.epi.pl_dst[d.epi.pl_ndst++] = act_buf(ord, l) + off * img_elems(l);
+                        d.epi.pl_kind = a.kind == 1 ? 1 : 0;
+                        d.epi.pl_ld = a.ld;
+                        d.epi.pl_hp = a.hp;
+                        d.epi.pl_wp = a.wp;
+                        d.epi.pl_pad = a.pad;
+                        d.epi.pl_col0 = wl.lo;
+                        d.epi.pl_arg = wl.argmax + off * li.Hq() * li.Wq() * wl.u;
+                        d.epi.pl_uch = wl.u;
+                    }
                     prepare(d, wl.p_fwd[j], w.gpu);
+                    bool pool_fused = false;
+                    if (d.epi.pl_on) {
+                        pool_fused = wl.p_fwd[j].halo == 0 && wl.p_fwd[j].sk.splits == 1;
+                        if (!pool_fused) wl.p_fwd[j].epi.pl_on = 0;
+                    }
                     const double fl = li.dense_conv ? 2.0 * rows * pix * wl.u * li.H * li.W * li.in_units  // executed
                                                     : 2.0 * rows * pix * wl.u * li.ksz * li.ksz * li.in_units;
                     int op = add_op(w.gpu, w.sf, gemm_launch(&wl.p_fwd[j], &wl.d_fwd[j], w.sf), deps, nk(wl.p_fwd[j]), OP_FWD_GEMM, fl);
-                    if (wl.U != nullptr) {
+                    if (wl.U != nullptr && !pool_fused) {
                         ActLayout out = lay_[l];
                         out.col0 = wl.lo;
                         PoolDsts pd;
