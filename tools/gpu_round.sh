@@ -25,4 +25,5 @@ python tools/summarize_ncu.py ${TAG} vgg16 > /dev/null 2>&1
 python tools/summarize_ncu.py ${TAG} wide_mlp gemm_wide > /dev/null 2>&1
 cp profiles/${TAG}_ncu.md profiles/${TAG}_gemm_wide_ncu.md profiles/gemm_traffic.json gpurun_out/ 2>/dev/null
 rm -f gpurun_out/${TAG}_gemm_wide.ncu-rep
+[ "${KEEP_REP:-0}" = "1" ] || rm -f gpurun_out/${TAG}_gemm.ncu-rep
 du -sh gpurun_out
