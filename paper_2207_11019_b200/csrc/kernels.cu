@@ -524,6 +524,43 @@ __global__ void dense_conv_fold_sgd_kernel(DenseConvGeom g, const float* __restr
     }
 }
 
+// im2col of the fp32 input for K = k*k*C <= 32 (VGG conv1 27, LeNet C1 25):
+// thread = output pixel, its 32-column row (zeros past K) assembled in
+// registers and written as eight float4 (128 B rows: whole-line stores).
+__global__ void __launch_bounds__(256) im2col_row32_kernel(const float* __restrict__ src, int imgs, int H, int W,
+                                                           int C, int k, int p, float* __restrict__ dst,
+                                                           long long ld) {
+    const int Ho = H + 2 * p - k + 1, Wo = W + 2 * p - k + 1;
+    const long long npix = static_cast<long long>(imgs) * Ho * Wo;
+    const long long pix = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (pix >= npix) return;
+    const int wo = static_cast<int>(pix % Wo);
+    const long long t = pix / Wo;
+    const int ho = static_cast<int>(t % Ho);
+    const long long n = t / Ho;
+    float r[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) r[i] = 0.f;
+    int col = 0;
+    for (int rr = 0; rr < k; ++rr) {
+        const int hi = ho + rr - p;
+        for (int ss = 0; ss < k; ++ss) {
+            const int wi = wo + ss - p;
+            const bool in = hi >= 0 && hi < H && wi >= 0 && wi < W;
+            const float* sp = src + ((n * H + hi) * W + wi) * C;
+            for (int c = 0; c < C; ++c, ++col) {
+                const float v = in ? __ldg(sp + c) : 0.f;
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (i == col) r[i] = v;
+            }
+        }
+    }
+    float4* d = reinterpret_cast<float4*>(dst + pix * ld);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) d[i] = make_float4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+}
+
 template <class T>
 __global__ void pad_input_kernel(const T* __restrict__ src, int imgs, int H, int W, int C, float* __restrict__ dst,
                                  int p, long long ld) {
@@ -867,6 +904,12 @@ cudaError_t launch_im2col_input(const double* src64, const float* src32, int img
                                 int p, float* dst, long long ld, cudaStream_t s) {
     const long long n = static_cast<long long>(imgs) * (H + 2 * p - k + 1) * (W + 2 * p - k + 1) * k * k * C;
     if (n <= 0) return cudaSuccess;
+    const long long npix = n / (static_cast<long long>(k) * k * C);
+    if (src32 != nullptr && k * k * C <= 32 && ld == 32 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+        im2col_row32_kernel<<<static_cast<unsigned>((npix + 255) / 256), 256, 0, s>>>(src32, imgs, H, W, C, k, p, dst,
+                                                                                      ld);
+        return cudaGetLastError();
+    }
     if (src64) im2col_kernel<double><<<grid_for(n, 256), 256, 0, s>>>(src64, imgs, H, W, C, k, p, dst, ld);
     else im2col_kernel<float><<<grid_for(n, 256), 256, 0, s>>>(src32, imgs, H, W, C, k, p, dst, ld);
     return cudaGetLastError();
