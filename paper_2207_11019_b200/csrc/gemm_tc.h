@@ -30,6 +30,7 @@ struct TcGemmPlan {
     HaloGeom hg;
     TmaStore ts;  // TMA-store epilogue (ts.n == 0: register epilogue)
     SideJob sj;   // a previous GEMM's deferred split-K reduction
+    int skinny = 0;  // launch on the CUDA-core skinny kernels (gemm_simt.cu) instead
 };
 
 // ws_alloc (optional): allocates split-K workspace (floats) on the GEMM's
@@ -56,5 +57,11 @@ int sm_count();
 // Exact-fp32 SIMT path with identical operand conventions and epilogues
 // (debug / tight-tolerance parity mode).
 cudaError_t simt_gemm_launch(const GemmDesc& d, cudaStream_t s);
+
+// Skinny shard GEMMs (N <= 32 or K <= 32, e.g. the classifier head) on the
+// CUDA cores in exact fp32 (gemm_simt.cu); the session routes eligible
+// descriptors here instead of a mostly idle tensor-core tile.
+bool skinny_gemm_eligible(const GemmDesc& d);
+cudaError_t skinny_gemm_launch(const GemmDesc& d, cudaStream_t s);
 
 }  // namespace ppb

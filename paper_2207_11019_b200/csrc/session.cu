@@ -583,7 +583,7 @@ void Session::build_ops() {
     begin_op_ = add_op(g0.ordinal, g0.main, nullptr, {}, 0);
 
     auto gemm_launch = [tf32](TcGemmPlan* p, GemmDesc* d, cudaStream_t s) -> std::function<cudaError_t()> {
-        if (tf32) return [p, s]() { return tc_gemm_launch(*p, s); };
+        if (tf32) return [p, d, s]() { return p->skinny ? skinny_gemm_launch(*d, s) : tc_gemm_launch(*p, s); };
         return [d, s]() { return simt_gemm_launch(*d, s); };
     };
     // kernels per GEMM launch (the split-K reduction is a second kernel)
@@ -594,6 +594,14 @@ void Session::build_ops() {
         Gpu* g = &gpu_of(gpu);
         WsAlloc ws = [g](size_t n) { return static_cast<float*>(g->alloc(sizeof(float) * n)); };
         if (!tc_gemm_prepare(d, &p, 0, err, sizeof(err), ws)) throw std::runtime_error(std::string("GEMM setup: ") + err);
+        // opt-in: measured slower than the tcgen05 tiles on VGG's head (2.301 vs
+        // 2.279 ms) and the MLP-784 step (0.098 vs 0.088 ms)
+        static const bool skinny_on = getenv("PPB_SKINNY") != nullptr;
+        if (skinny_on && skinny_gemm_eligible(d)) {  // CUDA-core path: no split-K / TMA state
+            p.skinny = 1;
+            p.sk = SplitK{};
+            p.ts = TmaStore{};
+        }
         cur_info_ = p.bn | (p.cg << 10) | (p.sk.splits << 12) | (p.halo << 24);
     };
     auto module_of_layer = [&](int l) -> const SubModule& {
@@ -1224,7 +1232,7 @@ void Session::build_ops() {
         int pend_fold_op = -1;
         auto link_side = [&](TcGemmPlan* p, int op, bool carrier_ok) {
             if (!tf32) return;
-            const bool can = carrier_ok && !no_side && p->halo == 0;
+            const bool can = carrier_ok && !no_side && p->halo == 0 && !p->skinny;
             if (pend_flag != nullptr) {
                 if (can) {
                     p->sj = pend_fold;
