@@ -78,6 +78,27 @@ def algorithmic_flops(net, batch):
     return sum(2.0 * layer_macs(l, batch) * (3 if i > 0 else 2) for i, l in enumerate(net.layers))
 
 
+def by_tile_width(ops, peak):
+    """GEMM launches grouped by output-tile width: the TF32 smem-operand rate
+    caps N = 64 / 128 tiles at ~41 % / ~67 % of peak, N = 256
+    tiles are not capped."""
+    out = {}
+    for o in ops:
+        if "gemm" not in str(o["kind"]) or o["ms"] <= 0:
+            continue
+        key = f"bn{o['bn']}"
+        g = out.setdefault(key, {"ms": 0.0, "tflop": 0.0, "launches": 0})
+        g["ms"] += o["ms"]
+        g["tflop"] += o["tflops"] * o["ms"] / 1e3  # tflops * s
+        g["launches"] += 1
+    for g in out.values():
+        g["achieved_tflops"] = g["tflop"] / (g["ms"] / 1e3) if g["ms"] > 0 else 0.0
+        g["frac"] = g["achieved_tflops"] / peak
+        g["ms"] = round(g["ms"], 4)
+        del g["tflop"]
+    return out
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -319,6 +340,7 @@ def run_ours(args, rank, world, dist):
     sess.sync()
     # per-kernel device times (eager, CUDA events around each launch)
     prof = sess.profile(1)
+    prof_ops = sess.profile_ops()
     barrier(dist)
     with ClockSampler(list(range(n))) as clk:
         ms = sess.time_steps(args.steps)
@@ -368,7 +390,8 @@ def run_ours(args, rank, world, dist):
                 "frac_of_bf16_burst": achieved / peaks.get("bf16_tflops", 1612.0),
                 "step_tflops": algorithmic_flops(net, batch) * args.steps / (ms / 1000.0) / 1e12 / n,
                 "step_frac": algorithmic_flops(net, batch) * args.steps / (ms / 1000.0) / 1e12 / n / tf32_peak,
-                "per_kind_ms": {k: round(v["ms"], 4) for k, v in prof.items()}}
+                "per_kind_ms": {k: round(v["ms"], 4) for k, v in prof.items()},
+                "by_tile_width": by_tile_width(prof_ops, tf32_peak)}
 
     # ---- reference CPU baseline on a bounded sample (rank 0, N=1 only)
     cpu = None
