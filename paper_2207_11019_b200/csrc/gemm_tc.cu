@@ -1209,6 +1209,9 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
             int cg, bn;
             double eff;
         };
+        // (an operand-bound table {1, .69, .69, .52, .35} measured slower on the
+        // VGG step, 2.30 vs 2.27 ms: the split-K reduction it then prefers
+        // costs more than the model charges)
         const Cand cands[] = {{2, 256, 1.0}, {2, 128, 0.85}, {1, 256, 0.93}, {1, 128, 0.8}, {1, 64, 0.55}};
         double best = -1;
         for (const Cand& c : cands) {
