@@ -273,6 +273,64 @@ __device__ __forceinline__ void epi_pool32(const EpiParams& p, int m, int n0, co
     }
 }
 
+// Same pool, reading the window partners' rows from the chunk's SWIZZLE_128B
+// staging box (row r, 16 B chunk j at j ^ (r & 7)) instead of 96 shuffles:
+// only the window leaders load (3 x 8 float4).  The caller has just written
+// the box (TMA-store path) and syncs the warp before it is overwritten.
+__device__ __forceinline__ void epi_pool32_smem(const EpiParams& p, int m, int n0, const float (&v)[32], int lane,
+                                                uint32_t box) {
+    const int wo = p.pl_wo, howo = p.pl_wo * p.pl_ho;
+    const int img = m / howo, rem = m - img * howo, h = rem / wo, w = rem - h * wo;
+    const bool leader = m < p.M && (h & 1) == 0 && (w & 1) == 0 && n0 < p.N;
+    if (!leader) return;
+    float out[32];
+    uint32_t code[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int i = 0; i < 32; ++i) out[i] = v[i];
+    const int rows[3] = {lane + 1, lane + wo, lane + wo + 1};
+#pragma unroll
+    for (int qq = 0; qq < 3; ++qq) {
+        const int r = rows[qq];
+        const uint32_t q = static_cast<uint32_t>(qq + 1);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float e[4];
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(e[0]), "=f"(e[1]), "=f"(e[2]), "=f"(e[3])
+                         : "r"(box + r * 128 + ((j ^ (r & 7)) << 4)));
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int i = 4 * j + k;
+                if (e[k] > out[i]) {
+                    out[i] = e[k];
+                    code[i >> 2] = (code[i >> 2] & ~(0xffu << (8 * (i & 3)))) | (q << (8 * (i & 3)));
+                }
+            }
+        }
+    }
+    const int nvalid = p.N - n0 < 32 ? p.N - n0 : 32;
+    const int Hq = p.pl_ho / 2, Wq = wo / 2, y = h / 2, x = w / 2;
+    const long long pp = (static_cast<long long>(img) * Hq + y) * Wq + x;
+    unsigned char* ap = p.pl_arg + pp * p.pl_uch + n0;
+    if (nvalid == 32 && (p.pl_uch & 3) == 0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) reinterpret_cast<uint32_t*>(ap)[i] = code[i];
+    } else {
+        for (int i = 0; i < nvalid; ++i) ap[i] = static_cast<unsigned char>((code[i >> 2] >> (8 * (i & 3))) & 0xffu);
+    }
+    if (p.pl_kind == 0) {
+        const long long o = ((static_cast<long long>(img) * p.pl_hp + y + p.pl_pad) * p.pl_wp + x + p.pl_pad) * p.pl_ld +
+                            p.pl_col0;
+        for (int d = 0; d < p.pl_ndst; ++d) store_row32(p.pl_dst[d] + o, n0, nvalid, out);
+    } else {
+        for (int i = 0; i < nvalid; ++i) {
+            const long long o = static_cast<long long>(img) * p.pl_ld +
+                                static_cast<long long>(p.pl_col0 + n0 + i) * Hq * Wq + static_cast<long long>(y) * Wq + x;
+            for (int d = 0; d < p.pl_ndst; ++d) p.pl_dst[d][o] = out[i];
+        }
+    }
+}
+
 // Row offset (elements) of output row m in the EPI_STORE destination.
 __device__ __forceinline__ long long epi_store_row(const EpiParams& p, int m) {
     if (!p.remap) return static_cast<long long>(m) * p.ldd;

@@ -463,7 +463,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     } else if (ts.n) {
                         epi_values32(epi, m, n0 + c * 32, v, lane);
                         if (!(epi.dbg & 2)) tma_store_chunk(ts, stg + (warp - 4) * 4096, lane, v, m0 + q * 32, n0 + c * 32);
-                        if (epi.pl_on) epi_pool32(epi, m, n0 + c * 32, v, lane);
+                        if (epi.pl_on == 2) {  // window partners from the staging box just written
+                            __syncwarp();
+                            epi_pool32_smem(epi, m, n0 + c * 32, v, lane, smem_u32(stg + (warp - 4) * 4096));
+                            __syncwarp();
+                        } else if (epi.pl_on) {
+                            epi_pool32(epi, m, n0 + c * 32, v, lane);
+                        }
                     } else if (!(epi.dbg & 2)) {
                         epilogue32(epi, m, n0 + c * 32, v);
                         if (epi.pl_on) epi_pool32(epi, m, n0 + c * 32, v, lane);

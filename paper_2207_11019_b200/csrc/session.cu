@@ -760,7 +760,8 @@ void Session::build_ops() {
                     if (tf32 && !no_pool_fuse && li.pool == 2 && wl.U != nullptr && !li.dense_conv && wl.argmax &&
                         Wo1 >= 2 && 32 % (2 * Wo1) == 0 && Ho1 % 2 == 0 && (pix % 32 == 0 || 32 % pix == 0)) {
                         const ActLayout& a = lay_[l];
-                        d.epi.pl_on = 1;
+                        static const bool pool_smem = getenv("PPB_POOL_SMEM") != nullptr;
+                        d.epi.pl_on = pool_smem ? 2 : 1;
                         d.epi.pl_wo = Wo1;
                         d.epi.pl_ho = Ho1;
                         for (int ord : dest_gpus) d.epi.pl_dst[d.epi.pl_ndst++] = act_buf(ord, l) + off * img_elems(l);
