@@ -1099,7 +1099,9 @@ void Session::build_ops() {
                     ConvMerge cm;
                     const long long rows_per_img = li.kind == 1 ? hw : 1;
                     for (float* sp : dl.slots) cm.slots.slot[cm.slots.n++] = sp + off * rows_per_img * dl.slot_ld;
-                    cm.slot_kind = li.kind == 1 ? 0 : 1;
+                    // a dense consumer's CHW-flatten slot over a 1 x 1 pooled grid is
+                    // the pixel-major layout (vectorised merge kernel)
+                    cm.slot_kind = (li.kind == 1 || lb.Hq() * lb.Wq() == 1) ? 0 : 1;
                     cm.lds = dl.slot_ld;
                     cm.imgs = rows;
                     cm.Ho = lb.Ho();
