@@ -425,6 +425,20 @@ bool halo_conv_eligible(const GemmDesc& d) {
     return waste <= 1.3;
 }
 
+// Automatic choice between the halo kernel and the rank-4 implicit GEMM for an
+// eligible descriptor, measured with the TMA-store epilogues (VGG,
+// profile_ops): a pooled backward merge needs the stride-2 quadrant boxes the
+// padded-position tiles cannot form (conv3 dgrad 107.6 vs 91.1 us), and
+// MN-major (flipped-weight) B at N >= 128 streams B beside the halo (conv4
+// dgrad 113.7 vs 97.3 us).  Step 2.270 -> 2.244 ms.
+bool halo_conv_preferred(const GemmDesc& d) {
+    static const bool always = getenv("PPB_HALO_ALWAYS") != nullptr;
+    if (always) return true;
+    if (d.epi.mode == EPI_MERGE && d.epi.mg_pool == 2) return false;
+    if (d.b.mn_major && d.N >= 128) return false;
+    return true;
+}
+
 // force: 0 = automatic tile choice; 1000 + bn = 1-CTA tiles of width bn;
 // 2000 + bn = CTA-pair tiles (256 x bn).
 bool halo_conv_prepare(const GemmDesc& d, TcGemmPlan* out, int force, char* err, size_t errlen) {

@@ -1167,7 +1167,7 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
         const char* e = getenv("PPB_NO_HALO");
         return e != nullptr && *e != '\0' && *e != '0';
     }();
-    if ((force_bn >= 1000 || (force_bn == 0 && !no_halo)) && halo_conv_eligible(d))
+    if ((force_bn >= 1000 || (force_bn == 0 && !no_halo && halo_conv_preferred(d))) && halo_conv_eligible(d))
         return halo_conv_prepare(d, out, force_bn, err, errlen);
     if (force_bn >= 1000) {
         snprintf(err, errlen, "halo conv tile forced on an ineligible GEMM");

@@ -44,6 +44,7 @@ cudaError_t tc_gemm_init_device();
 // Halo-reuse implicit conv (conv_halo.cu): a 3x3 stride-1 conv over a padded
 // NHWC grid computed in padded-position space; see halo_conv_prepare.
 bool halo_conv_eligible(const GemmDesc& d);
+bool halo_conv_preferred(const GemmDesc& d);  // automatic choice among eligible descriptors
 bool halo_conv_prepare(const GemmDesc& d, TcGemmPlan* p, int force, char* err, size_t errlen);
 cudaError_t halo_conv_launch(const TcGemmPlan& p, cudaStream_t s);
 cudaError_t halo_conv_init_device();
