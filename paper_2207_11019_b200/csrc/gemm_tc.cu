@@ -1218,9 +1218,16 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
         // (an operand-bound table {1, .69, .69, .52, .35} measured slower on the
         // VGG step, 2.30 vs 2.27 ms: the split-K reduction it then prefers
         // costs more than the model charges)
-        const Cand cands[] = {{2, 256, 1.0}, {2, 128, 0.85}, {1, 256, 0.93}, {1, 128, 0.8}, {1, 64, 0.55}};
+        const Cand cands_std[] = {{2, 256, 1.0}, {2, 128, 0.85}, {1, 256, 0.93}, {1, 128, 0.8}, {1, 64, 0.55}};
+        const Cand cands_op[] = {{2, 256, 1.0}, {2, 128, 0.69}, {1, 256, 0.69}, {1, 128, 0.52}, {1, 64, 0.35}};
+        // wgrad + SGD (reduction free as a side job): the operand-bound table
+        // picks slightly better tiles (2.238 -> 2.233 ms); elsewhere it prefers
+        // split-K whose reduction costs more than modelled
+        static const bool sgd_std = getenv("PPB_SGD_STDTABLE") != nullptr;
+        const Cand* cands = (!sgd_std && d.epi.mode == EPI_SGD) ? cands_op : cands_std;
         double best = -1;
-        for (const Cand& c : cands) {
+        for (int ci = 0; ci < 5; ++ci) {
+            const Cand& c = cands[ci];
             if (c.cg == 2 && d.M <= 128) continue;
             const int tm = kBM * c.cg;
             const int num_m = (d.M + tm - 1) / tm, num_n = (d.N + c.bn - 1) / c.bn;
