@@ -60,8 +60,24 @@ WORKLOADS = {
 def build_net(workload, seed=1):
     from paper_2207_11019_b200 import configs
 
+    kw = {"init": "kaiming"} if workload in ("vgg16", "lenet5") else {}
     return {"vgg16": configs.vgg16_cifar, "wide_mlp": configs.wide_mlp, "mlp784": configs.mlp784,
-            "lenet5": configs.lenet5}[WORKLOADS[workload]["net"]](seed=seed)
+            "lenet5": configs.lenet5}[WORKLOADS[workload]["net"]](seed=seed, **kw)
+
+
+def synthetic_batch(workload, seed=1):
+    """The benchmark's network and batch (also what tests/test_bench_parity_gpu.py
+    checks against the oracle): weights U[-0.5,0.5]/sqrt(fan_in) from
+    numpy's default_rng(seed), X ~ N(0,1) float32, labels uniform over the
+    classes."""
+    w = WORKLOADS[workload]
+    rng = np.random.default_rng(seed)
+    net = build_net(workload, seed=seed)
+    l0 = net.layers[0]
+    in_feat = l0.in_units() * (l0.conv.height * l0.conv.width if l0.conv else 1)
+    X = rng.standard_normal((w["batch"], in_feat), dtype=np.float32)
+    y = rng.integers(0, w["classes"], w["batch"]).astype(np.int32)
+    return net, X, y
 
 
 def layer_macs(layer, batch):
@@ -313,13 +329,8 @@ def run_ours(args, rank, world, dist):
         barrier(dist)  # after timing
         max_over_ranks(dist, 0.0)
         return
-    rng = np.random.default_rng(1)
-    net = build_net(args.workload, seed=1)
-    dims = net.dims()
-    in_feat = net.layers[0].in_units() * (net.layers[0].conv.height * net.layers[0].conv.width
-                                          if net.layers[0].conv else 1)
-    X = rng.standard_normal((batch, in_feat), dtype=np.float32)
-    y = rng.integers(0, w["classes"], batch).astype(np.int32)
+    net, X, y = synthetic_batch(args.workload, seed=1)
+    in_feat = X.shape[1]
     plan = api.build_plan(net, n, 1)  # every layer over all n GPUs (build_plan, partition.cpp:110-121)
     # PPB_BENCH_PLAN_DEVICES=k (testing): a k-device plan with every plan device
     # on cuda:0 (exercises the multi-device step on a one-GPU box)
@@ -409,7 +420,9 @@ def run_ours(args, rank, world, dist):
     line = {"metric": "train samples/sec (fwd+bwd+update)", "value": value, "unit": "samples/s", "n_gpus": n,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak" if n == 1 else "strong", "vs_baseline": None, "dtype": "tf32",
-            "data": "synthetic (X ~ N(0,1), labels uniform over classes, weights U[-0.5,0.5]/sqrt(fan_in))",
+            "data": "synthetic (X ~ N(0,1), labels uniform over classes, weights "
+                    + ("U[-sqrt(6/fan_in), sqrt(6/fan_in)] (kaiming)" if args.workload in ("vgg16", "lenet5")
+                       else "U[-0.5,0.5]/sqrt(fan_in) (the reference's init rule)") + ")",
             "config": {"workload": args.workload, "name": w["name"], "batch": batch, "global_batch": batch,
                        "gflop_per_step": algorithmic_flops(net, batch) / 1e9,
                        "plan": f"build_plan n={n} Z=1, m={args.m}, async_per_module, CUDA graph",

@@ -4,6 +4,14 @@ Weights are random-initialised with the reference's rule, uniform
 [-0.5, 0.5] / sqrt(fan_in) (tinynet.cpp:176-196), fan_in = ksize^2 * C_in for
 conv layers; the RNG is numpy's (synthetic benchmark data,
 not the reference's libstdc++ stream — use the oracle's init_net for that).
+
+`init="kaiming"` draws conv / hidden weights from U[-sqrt(6/fan_in),
++sqrt(6/fan_in)] instead (variance 2/fan_in, the ReLU-preserving scale).  The
+reference rule has variance 1/(12 fan_in), so every ReLU layer shrinks the
+signal variance ~24x: through VGG-16's 13 convs the conv1 gradient ends up
+~1e-15 of its weights, below fp32 resolution (the reference trains 2-4 layer
+MLPs, where this does not matter).  The benchmarked CNNs use kaiming so the
+parity checks at the bench configuration compare real updates of every layer.
 """
 from __future__ import annotations
 
@@ -12,16 +20,21 @@ import numpy as np
 from .api import ActKind, ConvSpec, TinyLayer, TinyNet
 
 
-def _dense(rng, fi, fo, act):
+def _scale(fan_in, init):
+    # width of the uniform distribution around 0
+    return 1.0 / np.sqrt(fan_in) if init == "reference" else 2.0 * np.sqrt(6.0 / fan_in)
+
+
+def _dense(rng, fi, fo, act, init="reference"):
     s = 1.0 / np.sqrt(fi)
-    return TinyLayer((rng.random((fo, fi)) - 0.5) * s, (rng.random(fo) - 0.5) * s, ActKind(act))
+    return TinyLayer((rng.random((fo, fi)) - 0.5) * _scale(fi, init), (rng.random(fo) - 0.5) * s, ActKind(act))
 
 
-def _conv(rng, cin, cout, hw, k=3, pad=1, pool=1, act=1):
+def _conv(rng, cin, cout, hw, k=3, pad=1, pool=1, act=1, init="reference"):
     fan_in = k * k * cin
     s = 1.0 / np.sqrt(fan_in)
-    return TinyLayer((rng.random((cout, fan_in)) - 0.5) * s, (rng.random(cout) - 0.5) * s, ActKind(act),
-                     ConvSpec(hw[0], hw[1], k, pad, pool))
+    return TinyLayer((rng.random((cout, fan_in)) - 0.5) * _scale(fan_in, init), (rng.random(cout) - 0.5) * s,
+                     ActKind(act), ConvSpec(hw[0], hw[1], k, pad, pool))
 
 
 def dense_net(dims, acts, seed=1) -> TinyNet:
@@ -42,7 +55,7 @@ def wide_mlp(seed=1) -> TinyNet:
 VGG16 = [64, 64, "M", 128, 128, "M", 256, 256, 256, "M", 512, 512, 512, "M", 512, 512, 512, "M"]
 
 
-def vgg16_cifar(seed=1, classes=10, widths=VGG16, hw=32, cin=3) -> TinyNet:
+def vgg16_cifar(seed=1, classes=10, widths=VGG16, hw=32, cin=3, init="reference") -> TinyNet:
     """BASELINE configs[2]: VGG-16 on 32x32x3 (13 conv 3x3 + ReLU, 5 max pools,
     classifier 512 -> classes)."""
     rng = np.random.default_rng(seed)
@@ -51,7 +64,7 @@ def vgg16_cifar(seed=1, classes=10, widths=VGG16, hw=32, cin=3) -> TinyNet:
     while i < len(widths):
         w = widths[i]
         pool = 2 if i + 1 < len(widths) and widths[i + 1] == "M" else 1
-        layers.append(_conv(rng, c, w, (h, h), 3, 1, pool))
+        layers.append(_conv(rng, c, w, (h, h), 3, 1, pool, init=init))
         c = w
         h //= pool
         i += 2 if pool == 2 else 1
@@ -64,14 +77,14 @@ def small_cnn(seed=1, hw=8, cin=3, widths=(16, "M", 32, "M"), classes=10) -> Tin
     return vgg16_cifar(seed, classes, list(widths), hw, cin)
 
 
-def lenet5(seed=1, classes=10, hw=28, cin=1) -> TinyNet:
+def lenet5(seed=1, classes=10, hw=28, cin=1, init="reference") -> TinyNet:
     """BASELINE configs[1]: LeNet-5-style CNN on 28x28x1: C1 5x5x6 (pad 2, the
     original's 32x32 input) + ReLU + 2x2 max-pool -> 14x14x6, C3 5x5x16
     (valid) + ReLU + pool -> 5x5x16, F5 400 -> 120, F6 120 -> 84, output
     84 -> classes (softmax).  The 28x28 / 10x10 grids do not tile into
     128-pixel TMA boxes, so both convs run on the generic im2col path."""
     rng = np.random.default_rng(seed)
-    layers = [_conv(rng, cin, 6, (hw, hw), 5, 2, 2), _conv(rng, 6, 16, (hw // 2, hw // 2), 5, 0, 2)]
+    layers = [_conv(rng, cin, 6, (hw, hw), 5, 2, 2, init=init), _conv(rng, 6, 16, (hw // 2, hw // 2), 5, 0, 2, init=init)]
     s = (hw // 2 - 4) // 2
-    layers += [_dense(rng, 16 * s * s, 120, 1), _dense(rng, 120, 84, 1), _dense(rng, 84, classes, 2)]
+    layers += [_dense(rng, 16 * s * s, 120, 1, init), _dense(rng, 120, 84, 1, init), _dense(rng, 84, classes, 2)]
     return TinyNet(layers)
