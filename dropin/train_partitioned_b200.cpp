@@ -53,6 +53,10 @@ TrainResult train_partitioned(const TinyNet& net, const Batch& batch, const Trai
     validate_net(net);  // the reference's own entry checks (train_partitioned.cpp:124)
     if (batch.size() != static_cast<int>(batch.labels.size()))
         throw std::invalid_argument("batch rows and label count disagree");
+    // the ABI takes a bare pointer to rows x input_dim doubles: a narrower X
+    // would be read past its end (the reference throws in matmul_nt,
+    // tinynet.cpp:25, called from the shard forward)
+    if (batch.X.cols != net.input_dim()) throw std::invalid_argument("matmul_nt: inner dimensions disagree");
     std::vector<int> dims{net.input_dim()}, acts;
     std::vector<double> W, b;
     for (const TinyLayer& l : net.layers) {
@@ -65,7 +69,13 @@ TrainResult train_partitioned(const TinyNet& net, const Batch& batch, const Trai
     int ndev = plan.n;
     for (const SubModule& sm : plan.submodules)
         for (int d : sm.devices) ndev = d > ndev ? d : ndev;
+    // default: plan device k+1 on CUDA ordinal k, one plan device per visible
+    // GPU (round-robin when the plan has more devices than the box has GPUs);
+    // PPB_DEVICES=o1,o2,... overrides
+    int ngpu = 0;
+    if (ppb_device_count(&ngpu) != PPB_OK || ngpu < 1) ngpu = 1;
     std::vector<int> map(ndev > 0 ? ndev : 1, 0);
+    for (size_t k = 0; k < map.size(); ++k) map[k] = static_cast<int>(k % static_cast<size_t>(ngpu));
     if (const char* env = std::getenv("PPB_DEVICES")) {
         std::stringstream ss(env);
         std::string tok;

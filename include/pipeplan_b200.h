@@ -287,12 +287,6 @@ int ppb_debug_conv(int which, const float* x_pad, int N, int H, int W, int C, lo
                    const float* w, int u, const float* d_pad, long long ldd, float* out, long long ldo,
                    int force_bn, void* stream);
 
-/* TMA load throughput probe (csrc/tma_probe.cu): `ctas` CTAs each stream
- * `iters` stages of `boxes` boxes {32 fp32, box_rows} of a rows x cols matrix
- * into shared memory (mn_major selects the SW128_ATOM_32B swizzle). */
-int ppb_debug_tma_bw(const float* src, int rows, int cols, int box_rows, int mn_major, int boxes, int stages,
-                     int iters, int ctas, void* stream);
-
 #ifdef __cplusplus
 }
 #endif

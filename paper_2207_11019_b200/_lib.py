@@ -109,7 +109,6 @@ _SIGS = {
     "ppb_debug_conv": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_longlong, C.c_int,
                                  C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_longlong, C.c_void_p, C.c_longlong,
                                  C.c_int, C.c_void_p]),
-    "ppb_debug_tma_bw": (C.c_int, [C.c_void_p] + [C.c_int] * 8 + [C.c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -319,9 +319,15 @@ def model_graph_of(net: TinyNet) -> ModelGraph:
     nets with conv layers the chain is over sharded units (channels) and the
     conv layers carry their FLOPs explicitly."""
     specs, prev = [], None
+    conv = net.has_conv()
     for l, layer in enumerate(net.layers):
         fi = layer.in_units() if prev is None else prev
-        specs.append(LayerSpec(l + 1, fi, layer.fan_out(), layer.fwd_flops()))
+        fl = layer.fwd_flops()
+        if conv and layer.conv is None:
+            # a dense layer over a flattened conv output: its real fan_in is
+            # C*H*W, not the C units the chain shards, so price it explicitly
+            fl = 2.0 * layer.fan_in() * layer.fan_out()
+        specs.append(LayerSpec(l + 1, fi, layer.fan_out(), fl))
         prev = layer.fan_out()
     return ModelGraph(specs)
 
@@ -482,19 +488,37 @@ class Session:
         self._ctx = ctx
         self.batch_size = batch_size
         self.nW, self.nb = W.size, b.size
+        self.in_features = _input_features(net)
 
     def __del__(self):
         if getattr(self, "_h", None):
             _lib.lib().ppb_session_destroy(self._h)
             self._h = None
 
+    def _host_batch(self, X, labels, dtype):
+        """The C ABI takes bare pointers: check shapes here (the reference
+        throws on a width mismatch in matmul_nt, tinynet.cpp:24-35, and on a
+        row / label count mismatch, train_partitioned.cpp:132) and hand it
+        contiguous buffers of the exact element types."""
+        X = np.asarray(X)
+        y = np.ascontiguousarray(labels, np.int32).reshape(-1)
+        rows = X.shape[0] if X.ndim else 0
+        width = int(np.prod(X.shape[1:])) if X.ndim >= 2 else (0 if X.ndim == 0 else 1)
+        if rows != self.batch_size:
+            raise ValueError(f"batch has {rows} rows, session was created for {self.batch_size}")
+        if y.shape[0] != rows:
+            raise ValueError("batch rows and label count disagree")
+        if width != self.in_features:
+            raise ValueError(f"matmul_nt: inner dimensions disagree (X has {width} columns, "
+                             f"the network takes {self.in_features})")
+        return np.ascontiguousarray(X.reshape(rows, width), dtype), y
+
     def load_batch(self, X, labels):
-        y = np.ascontiguousarray(labels, np.int32)
-        if X.dtype == np.float32:
-            Xc = np.ascontiguousarray(X)
+        if np.asarray(X).dtype == np.float32:
+            Xc, y = self._host_batch(X, labels, np.float32)
             check(_lib.lib().ppb_session_load_batch_f32(self._h, Xc.ctypes.data_as(_f), _ip(y)))
         else:
-            Xc = np.ascontiguousarray(X, np.float64)
+            Xc, y = self._host_batch(X, labels, np.float64)
             check(_lib.lib().ppb_session_load_batch(self._h, _dp(Xc), _ip(y)))
 
     def step(self, iterations: int = 1):
@@ -570,7 +594,8 @@ class Session:
     def step_host(self, X: np.ndarray, labels: np.ndarray) -> float:
         """End-to-end step from host buffers (H2D X/labels, step, D2H loss)."""
         loss = C.c_double(0)
-        check(_lib.lib().ppb_session_step_host(self._h, X.ctypes.data_as(_f), _ip(labels), C.byref(loss)))
+        Xc, y = self._host_batch(X, labels, np.float32)  # no copy when already float32 / int32 contiguous
+        check(_lib.lib().ppb_session_step_host(self._h, Xc.ctypes.data_as(_f), _ip(y), C.byref(loss)))
         return loss.value
 
     def kernels_per_step(self) -> int:
@@ -580,6 +605,25 @@ class Session:
 
 
 _default_ctx = {}
+
+
+def _input_features(net: TinyNet) -> int:
+    l0 = net.layers[0]
+    return l0.in_units() * (l0.conv.height * l0.conv.width if l0.conv else 1)
+
+
+def device_count() -> int:
+    n = C.c_int(0)
+    check(_lib.lib().ppb_device_count(C.byref(n)))
+    return n.value
+
+
+def default_device_map(n_dev: int) -> List[int]:
+    """Plan device k+1 -> CUDA ordinal k, one plan device per visible GPU; a
+    plan with more devices than visible GPUs wraps round-robin (several plan
+    devices then share a GPU, which is how multi-device plans run on one)."""
+    g = max(1, device_count())
+    return [k % g for k in range(n_dev)]
 
 
 def _context_for(devices):
@@ -593,10 +637,11 @@ def train_partitioned(net: TinyNet, batch: Batch, cfg: TrainConfig, plan: Partit
                       mode: UpdateMode, opts: Optional[PartitionedTrainOptions] = None,
                       device_map: Optional[Sequence[int]] = None) -> TrainResult:
     """train_partitioned.cpp:121-709 on B200s.  `device_map[k]` is the CUDA
-    ordinal of plan device k+1 (default: all plan devices on cuda:0)."""
+    ordinal of plan device k+1 (default: default_device_map, one plan device
+    per visible GPU)."""
     opts = opts or PartitionedTrainOptions()
     n_dev = max([d for sm in plan.submodules for d in sm.devices] + [plan.n, 1])
-    ctx = _context_for(device_map if device_map is not None else [0] * n_dev)
+    ctx = _context_for(device_map if device_map is not None else default_device_map(n_dev))
     dims = np.asarray(net.dims(), np.int32)
     acts = np.asarray(net.acts(), np.int32)
     W, b = net.pack()
@@ -604,6 +649,9 @@ def train_partitioned(net: TinyNet, batch: Batch, cfg: TrainConfig, plan: Partit
     y = np.ascontiguousarray(batch.labels, np.int32)
     if X.shape[0] != y.shape[0]:
         raise ValueError("batch rows and label count disagree")
+    if int(np.prod(X.shape[1:])) != _input_features(net):
+        raise ValueError(f"matmul_nt: inner dimensions disagree (X has {int(np.prod(X.shape[1:]))} columns, "
+                         f"the network takes {_input_features(net)})")
     flat = plan.to_flat()
     Wo, bo = np.zeros_like(W), np.zeros_like(b)
     it = max(cfg.iterations, 1)

@@ -31,6 +31,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "dev_knobs.h"
 #include "epilogue.cuh"
 #include "gemm_tc.h"
 #include "ptx.cuh"
@@ -470,7 +471,7 @@ bool halo_conv_prepare(const GemmDesc& d, TcGemmPlan* out, int force, char* err,
     hg.cblocks = d.a.geom.cblocks;
     hg.rows = kBM + 2 * (hg.wp + 1);
     hg.Mp = static_cast<long long>(d.a.imgs) * hg.hp * hg.wp;
-    if (const char* e = getenv("PPB_HALO_DBG")) hg.dbg = atoi(e);  // timing probes only
+    hg.dbg = static_cast<int>(dev_knob_uint("PPB_HALO_DBG"));  // timing probes only
     int bn, cg;
     if (force >= 2000) {
         cg = 2;

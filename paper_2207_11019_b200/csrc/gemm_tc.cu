@@ -30,6 +30,7 @@
 #include <cstring>
 #include <mutex>
 
+#include "dev_knobs.h"
 #include "dense_conv.cuh"
 #include "epilogue.cuh"
 #include "gemm_tc.h"
@@ -1058,11 +1059,7 @@ cudaError_t launch_bn(const TcGemmPlan& p, cudaStream_t s) {
 // CTAs on SMs the other stream could use (measured 2.305 ms without, 2.312 ms
 // with the late trigger, 2.340 ms with an early trigger).
 bool pdl_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("PPB_PDL");
-        return e != nullptr && *e != '\0' && *e != '0';
-    }();
-    return on;
+    return dev_knob("PPB_PDL");
 }
 
 int sm_count() {
@@ -1129,7 +1126,7 @@ cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<A_MN, B_MN, BN, CG>, p.ta, p.tb, p.M, p.N, p.K, p.epi,
                                        p.ga, p.gb, p.sk, p.ts, p.stages, p.sj);
-    static const bool probe_no_reduce = getenv("PPB_PROBE_NO_REDUCE") != nullptr;  // timing probe (wrong results)
+    const bool probe_no_reduce = dev_knob("PPB_PROBE_NO_REDUCE");  // timing probe (wrong results)
     if (e != cudaSuccess || p.sk.splits <= 1 || p.sk.fixup || p.sk.deferred || probe_no_reduce) return e;
     const long long R = p.sk.trans ? p.N : p.M, Cc = p.sk.trans ? p.M : p.N;
     const long long items = R * ((Cc + 3) / 4);
@@ -1182,7 +1179,7 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
     p.epi = d.epi;
     p.epi.M = d.M;
     p.epi.N = d.N;
-    if (const char* e = getenv("PPB_GEMM_DBG")) p.epi.dbg = atoi(e);  // timing probes only
+    p.epi.dbg = static_cast<int>(dev_knob_uint("PPB_GEMM_DBG"));  // timing probes only
     if (d.K < 1) {
         snprintf(err, errlen, "GEMM with K=%d", d.K);
         return false;
@@ -1279,7 +1276,7 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
             // in-kernel fixup: measured slower than the reduction kernel (the
             // last warp's serial row-per-thread reads sit on the tile's tail:
             // VGG step 2.54 -> 3.07 ms), so opt-in only
-            static const bool fixup_on = getenv("PPB_SPLITK_FIXUP") != nullptr;
+            const bool fixup_on = dev_knob("PPB_SPLITK_FIXUP");
             if (splits <= 8 && fixup_on) {
                 const size_t nctr = static_cast<size_t>(tiles) * cg * 8;
                 float* c = ws_alloc(nctr);

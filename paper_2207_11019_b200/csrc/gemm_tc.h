@@ -30,7 +30,6 @@ struct TcGemmPlan {
     HaloGeom hg;
     TmaStore ts;  // TMA-store epilogue (ts.n == 0: register epilogue)
     SideJob sj;   // a previous GEMM's deferred split-K reduction
-    int skinny = 0;  // launch on the CUDA-core skinny kernels (gemm_simt.cu) instead
 };
 
 // ws_alloc (optional): allocates split-K workspace (floats) on the GEMM's
@@ -59,10 +58,5 @@ int sm_count();
 // (debug / tight-tolerance parity mode).
 cudaError_t simt_gemm_launch(const GemmDesc& d, cudaStream_t s);
 
-// Skinny shard GEMMs (N <= 32 or K <= 32, e.g. the classifier head) on the
-// CUDA cores in exact fp32 (gemm_simt.cu); the session routes eligible
-// descriptors here instead of a mostly idle tensor-core tile.
-bool skinny_gemm_eligible(const GemmDesc& d);
-cudaError_t skinny_gemm_launch(const GemmDesc& d, cudaStream_t s);
 
 }  // namespace ppb

@@ -1,6 +1,7 @@
 // Partitioned training step executor.  See session.h for the mapping from the
 // reference's worker threads / Mailbox to CUDA streams / events, and
 // DESIGN.md for buffer layouts and the per-kernel rooflines.
+#include "dev_knobs.h"
 #include "session.h"
 
 #include "conv.h"
@@ -549,10 +550,7 @@ int Session::add_op(int gpu, cudaStream_t s, std::function<cudaError_t()> f, std
                     int kernels, int kind, double flops) {
     // timing probes only (wrong results): PPB_PROBE_SKIP = bitmask of op kinds
     // whose launches are dropped from the step (dependencies are kept)
-    static const unsigned skip = [] {
-        const char* e = getenv("PPB_PROBE_SKIP");
-        return e != nullptr ? static_cast<unsigned>(strtoul(e, nullptr, 0)) : 0u;
-    }();
+    const unsigned skip = dev_knob_uint("PPB_PROBE_SKIP");
     if (kind > 0 && (skip >> kind) & 1u) {
         f = nullptr;
         kernels = 0;
@@ -583,7 +581,7 @@ void Session::build_ops() {
     begin_op_ = add_op(g0.ordinal, g0.main, nullptr, {}, 0);
 
     auto gemm_launch = [tf32](TcGemmPlan* p, GemmDesc* d, cudaStream_t s) -> std::function<cudaError_t()> {
-        if (tf32) return [p, d, s]() { return p->skinny ? skinny_gemm_launch(*d, s) : tc_gemm_launch(*p, s); };
+        if (tf32) return [p, d, s]() { return tc_gemm_launch(*p, s); };
         return [d, s]() { return simt_gemm_launch(*d, s); };
     };
     // kernels per GEMM launch (the split-K reduction is a second kernel)
@@ -594,14 +592,6 @@ void Session::build_ops() {
         Gpu* g = &gpu_of(gpu);
         WsAlloc ws = [g](size_t n) { return static_cast<float*>(g->alloc(sizeof(float) * n)); };
         if (!tc_gemm_prepare(d, &p, 0, err, sizeof(err), ws)) throw std::runtime_error(std::string("GEMM setup: ") + err);
-        // opt-in: measured slower than the tcgen05 tiles on VGG's head (2.301 vs
-        // 2.279 ms) and the MLP-784 step (0.098 vs 0.088 ms)
-        static const bool skinny_on = getenv("PPB_SKINNY") != nullptr;
-        if (skinny_on && skinny_gemm_eligible(d)) {  // CUDA-core path: no split-K / TMA state
-            p.skinny = 1;
-            p.sk = SplitK{};
-            p.ts = TmaStore{};
-        }
         cur_info_ = p.bn | (p.cg << 10) | (p.sk.splits << 12) | (p.halo << 24);
     };
     auto module_of_layer = [&](int l) -> const SubModule& {
@@ -760,7 +750,7 @@ void Session::build_ops() {
                     if (tf32 && !no_pool_fuse && li.pool == 2 && wl.U != nullptr && !li.dense_conv && wl.argmax &&
                         Wo1 >= 2 && 32 % (2 * Wo1) == 0 && Ho1 % 2 == 0 && (pix % 32 == 0 || 32 % pix == 0)) {
                         const ActLayout& a = lay_[l];
-                        static const bool pool_smem = getenv("PPB_POOL_SMEM") != nullptr;
+                        const bool pool_smem = dev_knob("PPB_POOL_SMEM");
                         d.epi.pl_on = pool_smem ? 2 : 1;
                         d.epi.pl_wo = Wo1;
                         d.epi.pl_ho = Ho1;
@@ -1235,7 +1225,7 @@ void Session::build_ops() {
         int pend_fold_op = -1;
         auto link_side = [&](TcGemmPlan* p, int op, bool carrier_ok) {
             if (!tf32) return;
-            const bool can = carrier_ok && !no_side && p->halo == 0 && !p->skinny;
+            const bool can = carrier_ok && !no_side && p->halo == 0;
             if (pend_flag != nullptr) {
                 if (can) {
                     p->sj = pend_fold;
@@ -1381,7 +1371,7 @@ void Session::build_ops() {
                 // carrying the update in the next wgrad GEMM measured slower (2.287
                 // vs 2.281 ms: its 51 MB of traffic slows that GEMM's mainloop more
                 // than the low-priority kernel costs), so it is opt-in
-                static const bool fold_side = getenv("PPB_FOLD_SIDE") != nullptr;
+                const bool fold_side = dev_knob("PPB_FOLD_SIDE");
                 if (tf32 && dense_conv_is_2x2(dg) && fold_side) {  // offer the update to the next wgrad GEMM
                     SideJob& f = pend_fold;
                     f = SideJob{};
