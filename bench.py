@@ -123,6 +123,37 @@ def measured_peaks():
     return {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
 
 
+def tf32_peak_live(reps=10):
+    """Dense TF32 tensor-core peak measured on THIS box in this run, the way
+    MEASURED_PEAKS.json measures bf16: cuBLAS (torch.matmul, TF32 allowed)
+    8192^3 fp32, 2*N^3 FLOPs, best of `reps` launches (burst), CUDA events.
+    tools/tf32_peak.py also records the sustained figure (profiles/)."""
+    import torch
+
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        N = 8192
+        a = torch.randn(N, N, device="cuda", dtype=torch.float32)
+        b = torch.randn(N, N, device="cuda", dtype=torch.float32)
+        c = torch.empty(N, N, device="cuda", dtype=torch.float32)
+        for _ in range(3):
+            torch.matmul(a, b, out=c)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        best = 1e9
+        for _ in range(reps):
+            s.record()
+            torch.matmul(a, b, out=c)
+            e.record()
+            e.synchronize()
+            best = min(best, s.elapsed_time(e))
+        del a, b, c
+        torch.cuda.empty_cache()
+        return 2.0 * N ** 3 / best / 1e9
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -332,18 +363,38 @@ def run_ours(args, rank, world, dist):
     net, X, y = synthetic_batch(args.workload, seed=1)
     in_feat = X.shape[1]
     plan = api.build_plan(net, n, 1)  # every layer over all n GPUs (build_plan, partition.cpp:110-121)
+    m = args.m
+    # plan chooser (plan_search.py): priced with the calibration measured on a
+    # B200 (profiles/calib_<workload>.json); --plan all keeps build_plan(n, 1)
+    choice, scaling = None, None
+    from paper_2207_11019_b200 import plan_search
+
+    cpath = plan_search.default_calibration_path(args.workload)
+    if os.path.exists(cpath):
+        cal = plan_search.Calibration.load(cpath)
+        try:
+            scaling = plan_search.predicted_scaling(net, cal)
+            if n > 1 and args.plan == "auto":
+                best, _ = plan_search.choose_plan(net, n, cal)
+                plan, m = best.plan, best.m
+                choice = best.describe()
+        except (KeyError, ValueError) as e:  # calibration does not cover this n
+            scaling = {"error": str(e)}
     # PPB_BENCH_PLAN_DEVICES=k (testing): a k-device plan with every plan device
     # on cuda:0 (exercises the multi-device step on a one-GPU box)
     plan_devs = int(os.environ.get("PPB_BENCH_PLAN_DEVICES", "0"))
     if plan_devs > 1 and n == 1:
-        n = plan_devs
-        plan = api.build_plan(net, n, 1)
-        ctx = api.Context([0] * n)
+        plan = api.build_plan(net, plan_devs, 1)
+        ctx = api.Context([0] * plan_devs)
     else:
+        plan_devs = n
+        if api.device_count() < n:
+            raise RuntimeError(f"bench.py --gpus {n}: rank 0 drives every plan device but sees only "
+                               f"{api.device_count()} GPU(s)")
         ctx = api.Context(list(range(n)))
     cfg = TrainConfig(alpha0=1e-4, decay=1e-2, iterations=1)
     opts = PartitionedTrainOptions(multiclass_accuracy=True, use_graph=True, pipeline_gate=2)
-    sess = api.Session(ctx, net, batch, plan, args.m, UpdateMode.async_per_module, cfg, opts)
+    sess = api.Session(ctx, net, batch, plan, m, UpdateMode.async_per_module, cfg, opts)
     sess.load_batch(X, y)
     barrier(dist)
     # warm-up
@@ -384,7 +435,8 @@ def run_ours(args, rank, world, dist):
     g_launch = sum(prof[k]["launches"] for k in gemm_kinds if k in prof)
     g_flops = sum(prof[k]["flops"] for k in gemm_kinds if k in prof)
     step_ms_eager = sum(v["ms"] for v in prof.values())
-    tf32_peak = peaks["bf16_tflops"] / 2.0  # TF32 dense rate is half of bf16 on B200 (burst: timed region < 1 s)
+    tf32_live = tf32_peak_live()
+    tf32_peak = tf32_live
     achieved = (g_flops / g_launch) / (g_ms / g_launch / 1000.0) / 1e12 if g_ms > 0 else 0.0
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "gemm_traffic.json")
@@ -396,15 +448,20 @@ def run_ours(args, rank, world, dist):
                 "kernel": "ppb::tc_gemm_kernel + ppb::halo_conv_kernel (all shard GEMMs: tcgen05.mma kind::tf32, TMA SW128, fused epilogues)",
                 "flops_per_launch": g_flops / max(g_launch, 1), "avg_launch_ms": g_ms / max(g_launch, 1),
                 "launches_per_step": g_launch, "share_of_step": g_ms / step_ms_eager if step_ms_eager else None,
-                "peak_source": f"{peak_src}: bf16_tflops (burst) / 2 (TF32 = half the bf16 tensor rate)",
+                "peak_source": "measured in this run: cuBLAS TF32 (torch.matmul fp32, allow_tf32) 8192^3, "
+                               "best of 10 launches (burst), CUDA events (bench.tf32_peak_live)",
                 "peak_bf16_burst_measured": peaks.get("bf16_tflops"),
-                "frac_of_bf16_burst": achieved / peaks.get("bf16_tflops", 1612.0),
+                "peak_tf32_as_half_bf16": peaks["bf16_tflops"] / 2.0,
+                "frac_of_half_bf16": achieved / (peaks["bf16_tflops"] / 2.0),
+                "half_bf16_source": peak_src,
                 # the profiling guide's nominal dense TF32 (B200_PROFILING.md): the
                 # bf16/2 figure above is measured at power-limited clocks, and the
                 # wide-MLP GEMM slightly exceeds it in short bursts at 1965 MHz
                 "frac_of_nominal_tf32_1100": achieved / 1100.0,
                 "step_tflops": algorithmic_flops(net, batch) * args.steps / (ms / 1000.0) / 1e12 / n,
                 "step_frac": algorithmic_flops(net, batch) * args.steps / (ms / 1000.0) / 1e12 / n / tf32_peak,
+                "step_frac_of_half_bf16": algorithmic_flops(net, batch) * args.steps / (ms / 1000.0) / 1e12 / n
+                                          / (peaks["bf16_tflops"] / 2.0),
                 "per_kind_ms": {k: round(v["ms"], 4) for k, v in prof.items()},
                 "by_tile_width": by_tile_width(prof_ops, tf32_peak)}
 
@@ -418,6 +475,7 @@ def run_ours(args, rank, world, dist):
             cpu = {k: v for k, v in cpu.items() if k != "seconds"}
 
     line = {"metric": "train samples/sec (fwd+bwd+update)", "value": value, "unit": "samples/s", "n_gpus": n,
+            "plan_devices": plan_devs,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak" if n == 1 else "strong", "vs_baseline": None, "dtype": "tf32",
             "data": "synthetic (X ~ N(0,1), labels uniform over classes, weights "
@@ -425,13 +483,16 @@ def run_ours(args, rank, world, dist):
                        else "U[-0.5,0.5]/sqrt(fan_in) (the reference's init rule)") + ")",
             "config": {"workload": args.workload, "name": w["name"], "batch": batch, "global_batch": batch,
                        "gflop_per_step": algorithmic_flops(net, batch) / 1e9,
-                       "plan": f"build_plan n={n} Z=1, m={args.m}, async_per_module, CUDA graph",
-                       "parallelism": f"layer-wise partition over {n} GPU(s)",
+                       "plan": (f"plan_search choice: {choice}" if choice else
+                                f"build_plan n={plan_devs} Z=1, m={m}") + ", async_per_module, CUDA graph",
+                       "parallelism": f"layer-wise partition over {n} GPU(s)" + (
+                           f" ({plan_devs} plan devices sharing cuda:0)" if plan_devs != n else ""),
                        "l2": {"wide_mlp": "inputs larger than L2 (weights 1 GiB + activations 0.5 GiB per step)",
                               "vgg16": "inputs larger than L2 (activations + error signals ~1.5 GiB per step)"}.get(
                            args.workload, "working set fits L2 (latency-bound config)")},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
             "gpu_launches": sess.kernels_per_step() * args.steps,
+            "predicted_scaling": scaling,
             "loss_last": float(lh[-1]) if len(lh) else None}
     print(json.dumps(line))
 
@@ -439,10 +500,12 @@ def run_ours(args, rank, world, dist):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="vgg16", choices=sorted(WORKLOADS))
     ap.add_argument("--m", type=int, default=1, help="micro-batches per step")
+    ap.add_argument("--plan", default="auto", choices=["auto", "all"],
+                    help="N>1: plan_search choice (auto) or every layer over all N GPUs (all)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

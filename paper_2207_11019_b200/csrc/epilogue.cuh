@@ -273,6 +273,46 @@ __device__ __forceinline__ void epi_pool32(const EpiParams& p, int m, int n0, co
     }
 }
 
+// 2x2 max-pool across a warp pair (pl_on == 3, grid width 32): `top` / `bot`
+// are the SWIZZLE_128B staging boxes of the warps holding image rows 2y and
+// 2y+1 (row r of a box = pixel x = r, 16 B chunk j at j ^ (r & 7)); mtop is
+// the top row's first pixel.  Warp `sub` of the pair pools windows
+// x = 8*sub .. 8*sub+7; lane = channel, so every pooled pixel is one 128 B
+// store per destination and one 32 B argmax store.  Window order and
+// tie-breaking as pool_fwd_kernel / epi_pool32: first max wins in
+// (0,0), (0,1), (1,0), (1,1).
+__device__ __forceinline__ void epi_pool_pair(const EpiParams& p, int mtop, int n0, int lane, uint32_t top,
+                                              uint32_t bot, int sub) {
+    const int n = n0 + lane;
+    if (n >= p.N) return;
+    const int wo = p.pl_wo, howo = wo * p.pl_ho;
+    const int img = mtop / howo, h = (mtop - img * howo) / wo;
+    const int Hq = p.pl_ho >> 1, Wq = wo >> 1, y = h >> 1;
+    const uint32_t j = static_cast<uint32_t>(lane) >> 2, kofs = (static_cast<uint32_t>(lane) & 3u) << 2;
+    const long long prow = (static_cast<long long>(img) * Hq + y) * Wq;
+    const long long obase = (static_cast<long long>(img) * p.pl_hp + y + p.pl_pad) * p.pl_wp + p.pl_pad;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int x = sub * 8 + i;
+        const uint32_t r0 = 2u * x, r1 = r0 + 1u;
+        const uint32_t o0 = r0 * 128u + ((j ^ (r0 & 7u)) << 4) + kofs;
+        const uint32_t o1 = r1 * 128u + ((j ^ (r1 & 7u)) << 4) + kofs;
+        float e0, e1, e2, e3;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(e0) : "r"(top + o0));
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(e1) : "r"(top + o1));
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(e2) : "r"(bot + o0));
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(e3) : "r"(bot + o1));
+        float best = e0;
+        unsigned char code = 0;
+        if (e1 > best) { best = e1; code = 1; }
+        if (e2 > best) { best = e2; code = 2; }
+        if (e3 > best) { best = e3; code = 3; }
+        p.pl_arg[(prow + x) * p.pl_uch + n] = code;
+        const long long o = (obase + x) * p.pl_ld + p.pl_col0 + n;
+        for (int d = 0; d < p.pl_ndst; ++d) p.pl_dst[d][o] = best;
+    }
+}
+
 // Same pool, reading the window partners' rows from the chunk's SWIZZLE_128B
 // staging box (row r, 16 B chunk j at j ^ (r & 7)) instead of 96 shuffles:
 // only the window leaders load (3 x 8 float4).  The caller has just written

@@ -52,7 +52,12 @@ struct EpiParams {
     // wins in order (0,0),(0,1),(1,0),(1,1)) to pl_dst[d] in the consumer
     // layout (pl_kind 0: padded NHWC pl_hp x pl_wp, pad pl_pad, pitch pl_ld;
     // 1: CHW-flatten rows of pitch pl_ld) at channel pl_col0 + n, and the
-    // window code to pl_arg[pooled pixel * pl_uch + n]
+    // window code to pl_arg[pooled pixel * pl_uch + n].
+    // pl_on == 3 (grid width 32, TMA-store staging, 128-row tiles of 4 image
+    // rows): the windows span the warp pair (q, q^1) holding rows 2y, 2y+1;
+    // both stage their chunk in shared memory, meet at a pair barrier and pool
+    // from the two boxes (epi_pool_pair).  The pre-pool rows are then not
+    // stored at all (nothing else reads them).
     int pl_on = 0;
     int pl_wo = 1, pl_ho = 1;
     float* pl_dst[kMaxDst] = {};

@@ -414,6 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                          static_cast<long long>(gridDim.x) * (kEpiWarps * 32), lane);
         const bool by_tile = num_tiles >= 2 * units;
         const int c_first = by_tile ? 0 : half, c_step = by_tile ? 1 : 2;
+        int bsel = 0;  // staging box of the next store (alternates when ts.dbuf)
         int local = 0;
         for (int tile = unit; tile < num_tiles; tile += units, ++local) {
             if (by_tile && (local & 1) != half) continue;
@@ -436,7 +437,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (sk.splits > 1) {  // raw partial sums for splitk_epilogue_kernel
                     const int nn = n0 + c * 32;
                     if (ts.n) {
-                        if (!(epi.dbg & 2)) tma_store_partial(ts, stg + (warp - 4) * 4096, lane, v, m0 + q * 32, nn, split);
+                        if (!(epi.dbg & 2)) tma_store_partial(ts, epi_box(stg, warp - 4, bsel), lane, v, m0 + q * 32, nn, split);
+                        bsel ^= ts.dbuf;
                     } else if (sk.trans) {  // [n][m]: for each column the warp's lanes write consecutive m
                         float* col = sk.ws + split * sk.stride + m;
                         if (m < M) {
@@ -461,9 +463,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                     } else if (ts.n && ts.mask) {
                         tma_store_chunk_masked(ts, stg + (warp - 4) * 4096, mbar, mphase, lane, v, m0 + q * 32,
                                                n0 + c * 32);
+                    } else if (ts.n && epi.pl_on == 3) {
+                        // 2x2 pool across the warp pair holding image rows 2y, 2y+1
+                        // (pre-pool rows are not stored: nothing reads them)
+                        epi_values32(epi, m, n0 + c * 32, v, lane);
+                        stage_chunk(stg + (warp - 4) * 4096, lane, v);
+                        pair_bar_sync(warp - 4);
+                        const int pw = (warp - 4) & ~1;
+                        epi_pool_pair(epi, m0 + (q & ~1) * 32, n0 + c * 32, lane, smem_u32(stg + pw * 4096),
+                                      smem_u32(stg + (pw + 1) * 4096), q & 1);
+                        pair_bar_sync(warp - 4);
                     } else if (ts.n) {
                         epi_values32(epi, m, n0 + c * 32, v, lane);
-                        if (!(epi.dbg & 2)) tma_store_chunk(ts, stg + (warp - 4) * 4096, lane, v, m0 + q * 32, n0 + c * 32);
+                        if (!(epi.dbg & 2)) tma_store_chunk(ts, epi_box(stg, warp - 4, bsel), lane, v, m0 + q * 32, n0 + c * 32);
+                        bsel ^= ts.dbuf;
                         if (epi.pl_on == 2) {  // window partners from the staging box just written
                             __syncwarp();
                             epi_pool32_smem(epi, m, n0 + c * 32, v, lane, smem_u32(stg + (warp - 4) * 4096));
@@ -1041,6 +1054,7 @@ template <bool A_MN, bool B_MN>
 cudaError_t launch_bn(const TcGemmPlan& p, cudaStream_t s) {
     if (p.cg == 2) {
         switch (p.bn) {
+            case 64: return launch_t<A_MN, B_MN, 64, 2>(p, s);
             case 128: return launch_t<A_MN, B_MN, 128, 2>(p, s);
             default: return launch_t<A_MN, B_MN, 256, 2>(p, s);
         }
@@ -1085,6 +1099,7 @@ cudaError_t tc_gemm_init_device() {
     set(tc_gemm_kernel<AM, BM, 64, 1>, kCap);                             \
     set(tc_gemm_kernel<AM, BM, 128, 1>, kCap);                            \
     set(tc_gemm_kernel<AM, BM, 256, 1>, kCap);                            \
+    set(tc_gemm_kernel<AM, BM, 64, 2>, kCap);                             \
     set(tc_gemm_kernel<AM, BM, 128, 2>, kCap);                            \
     set(tc_gemm_kernel<AM, BM, 256, 2>, kCap);
     PPB_SET(false, false)
@@ -1201,7 +1216,7 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
     int best_sp = -1;  // split count chosen with the tile shape (-1: splits_for)
     if (force_bn == 64 || force_bn == 128 || force_bn == 256) {
         bn = force_bn;
-    } else if (force_bn == -128 || force_bn == -256) {
+    } else if (force_bn == -64 || force_bn == -128 || force_bn == -256) {
         bn = -force_bn;
         cg = 2;
     } else {
@@ -1215,16 +1230,24 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
         // (an operand-bound table {1, .69, .69, .52, .35} measured slower on the
         // VGG step, 2.30 vs 2.27 ms: the split-K reduction it then prefers
         // costs more than the model charges)
-        const Cand cands_std[] = {{2, 256, 1.0}, {2, 128, 0.85}, {1, 256, 0.93}, {1, 128, 0.8}, {1, 64, 0.55}};
-        const Cand cands_op[] = {{2, 256, 1.0}, {2, 128, 0.69}, {1, 256, 0.69}, {1, 128, 0.52}, {1, 64, 0.35}};
+        // CTA-pair 64-wide tiles: each SM reads its 128 A rows and HALF of B
+        // from shared memory (the pair exchanges B), 5 instead of 6 KB per
+        // 128 x 64 x 8 MMA, so the narrow layers' operand-rate cap
+        // rises by ~1.2x
+        const Cand cands_std[] = {{2, 256, 1.0}, {2, 128, 0.85}, {1, 256, 0.93}, {1, 128, 0.8}, {2, 64, 0.62},
+                                  {1, 64, 0.55}};
+        const Cand cands_op[] = {{2, 256, 1.0}, {2, 128, 0.69}, {1, 256, 0.69}, {1, 128, 0.52}, {2, 64, 0.42},
+                                 {1, 64, 0.35}};
         // wgrad + SGD (reduction free as a side job): the operand-bound table
         // picks slightly better tiles (2.238 -> 2.233 ms); elsewhere it prefers
         // split-K whose reduction costs more than modelled
         static const bool sgd_std = getenv("PPB_SGD_STDTABLE") != nullptr;
         const Cand* cands = (!sgd_std && d.epi.mode == EPI_SGD) ? cands_op : cands_std;
         double best = -1;
-        for (int ci = 0; ci < 5; ++ci) {
+        static const bool no_pair64 = getenv("PPB_NO_PAIR64") != nullptr;  // A/B switch
+        for (int ci = 0; ci < 6; ++ci) {
             const Cand& c = cands[ci];
+            if (no_pair64 && c.cg == 2 && c.bn == 64) continue;
             if (c.cg == 2 && d.M <= 128) continue;
             const int tm = kBM * c.cg;
             const int num_m = (d.M + tm - 1) / tm, num_n = (d.N + c.bn - 1) / c.bn;
@@ -1291,12 +1314,14 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
     p.grid = (work < units ? work : units) * cg;
     // shared memory: stage ring + barrier block, then the EPI_MERGE db rows,
     // then the TMA-store staging; the ring gives up stages (down to 4) to fit
-    const int stage_bytes = bn == 64 ? TcCfg<64, 1>::kStageBytes
-                            : cg == 2 ? (bn == 128 ? TcCfg<128, 2>::kStageBytes : TcCfg<256, 2>::kStageBytes)
-                                      : (bn == 128 ? TcCfg<128, 1>::kStageBytes : TcCfg<256, 1>::kStageBytes);
-    const int def_stages = bn == 64 ? TcCfg<64, 1>::kStages
-                           : cg == 2 ? (bn == 128 ? TcCfg<128, 2>::kStages : TcCfg<256, 2>::kStages)
-                                     : (bn == 128 ? TcCfg<128, 1>::kStages : TcCfg<256, 1>::kStages);
+    const int stage_bytes = cg == 2 ? (bn == 64    ? TcCfg<64, 2>::kStageBytes
+                                       : bn == 128 ? TcCfg<128, 2>::kStageBytes
+                                                   : TcCfg<256, 2>::kStageBytes)
+                                    : (bn == 64    ? TcCfg<64, 1>::kStageBytes
+                                       : bn == 128 ? TcCfg<128, 1>::kStageBytes
+                                                   : TcCfg<256, 1>::kStageBytes);
+    const int def_stages = cg == 2 ? (bn == 64 ? TcCfg<64, 2>::kStages : bn == 128 ? TcCfg<128, 2>::kStages : TcCfg<256, 2>::kStages)
+                                   : (bn == 64 ? TcCfg<64, 1>::kStages : bn == 128 ? TcCfg<128, 1>::kStages : TcCfg<256, 1>::kStages);
     constexpr int kCapSmem = 227 * 1024;
     auto ring = [&](int st) { return 1024 + st * stage_bytes + 256; };
     p.stages = def_stages;
@@ -1312,10 +1337,20 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
         const int extra = off + kEpiStageBytes - 256;
         int st = p.stages;
         while (ring(st) + extra > kCapSmem && st > 4) --st;
+        static const bool no_dbuf = getenv("PPB_NO_STAGE_DBUF") != nullptr;  // A/B switch
         if (ring(st) + extra <= kCapSmem) {
             p.stages = st;
             p.ts.stage_off = off;
             p.db_smem = extra;
+            // second staging set when it fits without giving up ring stages
+            // (plain stores / split-K partials: the masked, pooled-merge and
+            // pool-from-staging epilogues read their box back)
+            const int extra2 = off + kEpiStageBytesDbuf - 256;
+            if (!p.ts.mask && !p.ts.pool2 && p.epi.pl_on != 2 && p.epi.pl_on != 3 && ring(st) + extra2 <= kCapSmem &&
+                !no_dbuf) {
+                p.ts.dbuf = 1;
+                p.db_smem = extra2;
+            }
         } else {
             p.ts = TmaStore{};
         }

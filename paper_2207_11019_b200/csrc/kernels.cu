@@ -717,6 +717,14 @@ __global__ void conv_merge_kernel(ConvMerge m, float* __restrict__ db_partial) {
 #pragma unroll
             for (int k = 0; k < VEC; ++k)
                 if (!(ap[k] > 0.f)) gr[k] = 0.f;
+        } else if (m.mask_kind == 3 && (h >> 1) < m.Ho / 2 && (w >> 1) < m.Wo / 2) {
+            // pooled activation at the window: the max = U at the argmax, the only
+            // position the routing above leaves non-zero
+            const ActLayout& a = m.act_layout;
+            const float* ap = m.act + ((n * a.hp + (h >> 1) + a.pad) * a.wp + (w >> 1) + a.pad) * a.ld + a.col0 + c0;
+#pragma unroll
+            for (int k = 0; k < VEC; ++k)
+                if (!(ap[k] > 0.f)) gr[k] = 0.f;
         }
         float* out = m.d_pad + ((n * hq + h + m.q) * wq + w + m.q) * m.ldd + c0;
         if (VEC == 4) {
@@ -771,6 +779,8 @@ __global__ void conv_merge_rows_kernel(ConvMerge m, float* __restrict__ db_parti
         const long long grow = (static_cast<long long>(n) * Hg + y) * Wg;
         const float* arow = m.mask_kind == 2
                                 ? m.act + ((static_cast<long long>(n) * a.hp + h + a.pad) * a.wp + a.pad) * a.ld + a.col0 + c0
+                            : m.mask_kind == 3 && row_in
+                                ? m.act + ((static_cast<long long>(n) * a.hp + y + a.pad) * a.wp + a.pad) * a.ld + a.col0 + c0
                                 : nullptr;
         const float* urow = m.mask_kind == 1 ? m.U + static_cast<long long>(r) * m.Wo * m.ldu + c0 : nullptr;
         float* orow = m.d_pad + ((static_cast<long long>(n) * hq + h + m.q) * wq + m.q) * m.ldd + c0;
@@ -797,6 +807,8 @@ __global__ void conv_merge_rows_kernel(ConvMerge m, float* __restrict__ db_parti
                     am[u] = 0xffffffffu;  // outside the pooled grid: no gradient
                 }
                 if (m.mask_kind == 2) mk[u] = __ldg(reinterpret_cast<const float4*>(arow + static_cast<long long>(w) * a.ld));
+                else if (m.mask_kind == 3 && row_in && x < Wg)
+                    mk[u] = __ldg(reinterpret_cast<const float4*>(arow + static_cast<long long>(x) * a.ld));
                 else if (m.mask_kind == 1) mk[u] = __ldg(reinterpret_cast<const float4*>(urow + static_cast<long long>(w) * m.ldu));
             }
 #pragma unroll
@@ -1012,7 +1024,7 @@ int conv_merge_blocks() { return 148 * 4; }
 cudaError_t launch_conv_merge(const ConvMerge& m, float* db_partial, cudaStream_t s) {
     const long long n = static_cast<long long>(m.imgs) * m.Ho * m.Wo * m.uch;
     bool v4 = m.slot_kind == 0 && vec4_ok(m.uch, m.lds, m.ldd) && (m.mask_kind != 1 || vec4_ok(m.ldu)) &&
-              (m.mask_kind != 2 || vec4_ok(m.act_layout.ld, m.act_layout.col0)) &&
+              ((m.mask_kind != 2 && m.mask_kind != 3) || vec4_ok(m.act_layout.ld, m.act_layout.col0)) &&
               reinterpret_cast<uintptr_t>(m.d_pad) % 16 == 0;
     for (int k = 0; k < m.slots.n; ++k) v4 = v4 && reinterpret_cast<uintptr_t>(m.slots.slot[k]) % 16 == 0;
     const int vec = v4 ? 4 : 1;

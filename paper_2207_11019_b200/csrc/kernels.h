@@ -118,7 +118,8 @@ cudaError_t launch_pool_fwd(const float* U, long long ldu, int imgs, int Ho, int
 // ascending device order (slot layout: 0 pixel-major [img*Hg*Wg x lds] over the
 // pooled grid, 1 CHW rows [img][lds]); routed through the pooling argmax;
 // masked by the ReLU of the layer's output (mask_kind 1: U rows, 2: the
-// padded consumer-layout activation, 0: none).
+// padded consumer-layout activation at the same pixel, 3: the pooled
+// activation at the window (its max, i.e. U at the argmax), 0: none).
 struct ConvMerge {
     ReduceSlots slots;
     int slot_kind = 0;

@@ -71,6 +71,7 @@ struct Session::WLayer {
     long long slot_ld = 0;               // row pitch of the slots
     long long delta_img = 0;             // floats of delta per sample (conv: padded grid)
     float* U = nullptr;                  // conv: pre-pool output of the shard [b*Ho*Wo x ldu]
+    bool u_written = true;               // false when the forward epilogue pools across warp pairs
     long long ldu = 0;
     unsigned char* argmax = nullptr;     // conv with pool: [b*Hq*Wq x u]
     float* cols = nullptr;               // generic conv: im2col rows of the input [b*Ho*Wo x ldc]
@@ -746,12 +747,17 @@ void Session::build_ops() {
                     // whole windows (grid width <= 16); the GEMM must end up unsplit and
                     // on the tc kernel, else the pool kernel runs as before
                     static const bool no_pool_fuse = getenv("PPB_NO_POOL_FUSE") != nullptr;
+                    // Grid width 32 (VGG conv2 / conv4 on the rank-4 path): 128-row tiles are
+                    // 4 image rows, the windows span warp pairs (pl_on 3, TMA-store staging)
                     const int Wo1 = li.Wo(), Ho1 = li.Ho();
+                    const bool in_warp = Wo1 >= 2 && 32 % (2 * Wo1) == 0 && (pix % 32 == 0 || 32 % pix == 0);
+                    static const bool no_pool_pair = getenv("PPB_NO_POOL_PAIR") != nullptr;  // A/B switch
+                    const bool pair = !no_pool_pair && Wo1 == 32 && pix % 128 == 0 && lay_[l].kind != 1 && wl.u >= 32;
                     if (tf32 && !no_pool_fuse && li.pool == 2 && wl.U != nullptr && !li.dense_conv && wl.argmax &&
-                        Wo1 >= 2 && 32 % (2 * Wo1) == 0 && Ho1 % 2 == 0 && (pix % 32 == 0 || 32 % pix == 0)) {
+                        Ho1 % 2 == 0 && (in_warp || pair)) {
                         const ActLayout& a = lay_[l];
                         const bool pool_smem = dev_knob("PPB_POOL_SMEM");
-                        d.epi.pl_on = pool_smem ? 2 : 1;
+                        d.epi.pl_on = !in_warp ? 3 : pool_smem ? 2 : 1;
                         d.epi.pl_wo = Wo1;
                         d.epi.pl_ho = Ho1;
                         for (int ord : dest_gpus) d.epi.pl_dst[d.epi.pl_ndst++] = act_buf(ord, l) + off * img_elems(l);
@@ -767,8 +773,10 @@ void Session::build_ops() {
                     prepare(d, wl.p_fwd[j], w.gpu);
                     bool pool_fused = false;
                     if (d.epi.pl_on) {
-                        pool_fused = wl.p_fwd[j].halo == 0 && wl.p_fwd[j].sk.splits == 1;
+                        pool_fused = wl.p_fwd[j].halo == 0 && wl.p_fwd[j].sk.splits == 1 &&
+                                     (d.epi.pl_on != 3 || wl.p_fwd[j].ts.n > 0);
                         if (!pool_fused) wl.p_fwd[j].epi.pl_on = 0;
+                        if (pool_fused && d.epi.pl_on == 3) wl.u_written = false;  // pre-pool rows never stored
                     }
                     const double fl = li.dense_conv ? 2.0 * rows * pix * wl.u * li.H * li.W * li.in_units  // executed
                                                     : 2.0 * rows * pix * wl.u * li.ksz * li.ksz * li.in_units;
@@ -1100,12 +1108,14 @@ void Session::build_ops() {
                     cm.pool = lb.pool;
                     cm.argmax = dl.argmax ? dl.argmax + off * hw * dl.u : nullptr;
                     if (relu_below) {
-                        if (dl.U != nullptr) {
+                        if (dl.U != nullptr && dl.u_written) {
                             cm.mask_kind = 1;
                             cm.U = dl.U + off * lb.Ho() * lb.Wo() * dl.ldu;
                             cm.ldu = dl.ldu;
                         } else {
-                            cm.mask_kind = 2;
+                            // pooled layers whose pre-pool rows were never stored (pool fused
+                            // across warp pairs) mask at the pooled pixel
+                            cm.mask_kind = lb.pool == 2 ? 3 : 2;
                             cm.act = act_buf(dw.gpu, l - 1) + off * img_elems(l - 1);
                             cm.act_layout = lay_[l - 1];
                             cm.act_layout.col0 = dl.lo;

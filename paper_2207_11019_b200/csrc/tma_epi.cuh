@@ -28,6 +28,11 @@ namespace ppb {
 
 constexpr int kEpiWarps = 8;                     // two warps per TMEM lane quarter (alternate column chunks)
 constexpr int kEpiStageBytes = kEpiWarps * 4096 + 128;  // one 32 rows x 128 B staging box per epilogue warp + mbarriers
+// Double-buffered staging (TmaStore::dbuf): a second set of boxes after the
+// mbarrier block (1 KB aligned for SW128), so a warp writes chunk c+1 while
+// the bulk store of chunk c is still reading its box (wait_group.read 1).
+constexpr int kEpiStage2Off = kEpiWarps * 4096 + 1024;
+constexpr int kEpiStageBytesDbuf = kEpiStage2Off + kEpiWarps * 4096;
 
 struct TmaStore {
     CUtensorMap map[kMaxDst];
@@ -43,7 +48,20 @@ struct TmaStore {
     // after the staging boxes), then applied from shared memory
     int mask = 0;
     CUtensorMap mmap;
+    int dbuf = 0;  // two staging boxes per warp (plain stores / split-K partials only)
 };
+
+// The staging box of epilogue warp `ewarp` for its `sel`-th buffer.
+__device__ __forceinline__ uint8_t* epi_box(uint8_t* stg, int ewarp, int sel) {
+    return stg + (sel ? kEpiStage2Off : 0) + ewarp * 4096;
+}
+
+// Before rewriting a box: its previous bulk store must have read it.  With
+// double buffering the newest group belongs to the other box.
+__device__ __forceinline__ void box_wait(int dbuf) {
+    if (dbuf) bulk_wait_read<1>();
+    else bulk_wait_read<0>();
+}
 
 // Host: split-K partial sums through the same staging path: a rank-3 map over
 // the workspace ([split][M][ld], or [split][N][ld] transposed).
@@ -63,7 +81,7 @@ __device__ __forceinline__ void epi_bar_sync() {
 // workspace (transposed boxes for the [n][m] layout).
 __device__ __forceinline__ void tma_store_partial(const TmaStore& ts, uint8_t* buf, int lane, const float (&v)[32],
                                                   int r0, int n, int split) {
-    if (lane == 0) bulk_wait_read<0>();
+    if (lane == 0) box_wait(ts.dbuf);
     __syncwarp();
     const uint32_t base = smem_u32(buf);
     if (ts.tr) {  // box row = column n + i, 32 consecutive m across the lanes
@@ -197,9 +215,26 @@ __device__ __forceinline__ void tma_merge_pool2_chunk(const TmaStore& ts, uint8_
 // Registers -> swizzled staging box -> bulk tensor store(s).  All 32 lanes
 // call it; lane 0 owns the bulk async-group state.  The warp's next chunk
 // (tcgen05.ld, transform) overlaps the store's smem read.
+// Stage a 32 x 32 chunk in its SWIZZLE_128B box without storing it (pool
+// pair mode: the partner warp reads it).
+__device__ __forceinline__ void stage_chunk(uint8_t* buf, int lane, const float (&v)[32]) {
+    if (lane == 0) bulk_wait_read<0>();  // a store issued from this box earlier has read it
+    __syncwarp();
+    const uint32_t row = smem_u32(buf) + lane * 128;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        st_shared_v4(row + ((j ^ (lane & 7)) << 4), v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+}
+
+// Named barrier of the epilogue warp pair (2i, 2i+1), i = (warp - 4) / 2:
+// ids 2..5 (0 = __syncthreads, 1 = all epilogue warps).
+__device__ __forceinline__ void pair_bar_sync(int epi_warp) {
+    asm volatile("bar.sync %0, 64;" ::"r"(2 + (epi_warp >> 1)) : "memory");
+}
+
 __device__ __forceinline__ void tma_store_chunk(const TmaStore& ts, uint8_t* buf, int lane, const float (&v)[32],
                                                 int r0, int n) {
-    if (lane == 0) bulk_wait_read<0>();  // the previous store has read the box
+    if (lane == 0) box_wait(ts.dbuf);  // the previous store from this box has read it
     __syncwarp();
     const uint32_t row = smem_u32(buf) + lane * 128;
 #pragma unroll

@@ -62,7 +62,7 @@ SHAPES = [  # N, H, W, Cin, u, k, p  (VGG-16 CIFAR geometries, scaled batch)
 
 
 @pytest.mark.parametrize("shape", SHAPES)
-@pytest.mark.parametrize("bn", [0, 64, -128])
+@pytest.mark.parametrize("bn", [0, 64, -64, -128])
 def test_conv_forward(shape, bn):
     N, H, W, Cin, u, k, p = shape
     x, wt, dy, x_pad, w, d_pad, ldx, ldd, ck, Ho, Wo = _setup(*shape)

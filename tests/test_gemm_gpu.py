@@ -100,7 +100,7 @@ def test_tc_gemm_store(shape, majors):
     assert et < 1e-4, (ef, et)
 
 
-@pytest.mark.parametrize("bn", [64, 128, 256, -128, -256])
+@pytest.mark.parametrize("bn", [64, 128, 256, -64, -128, -256])
 def test_tc_gemm_tile_widths(bn):
     """1-CTA tiles (bn > 0) and CTA-pair cta_group::2 tiles (bn < 0)."""
     ef, et, _ = _run(640, 700, 300, False, True, force_bn=bn, bias=True, relu=True)
@@ -109,13 +109,13 @@ def test_tc_gemm_tile_widths(bn):
 
 @pytest.mark.parametrize("majors", MAJORS)
 @pytest.mark.parametrize("shape", [(1000, 520, 777), (300, 260, 64), (2048, 1024, 512)])
-@pytest.mark.parametrize("bn", [-128, -256])
+@pytest.mark.parametrize("bn", [-64, -128, -256])
 def test_tc_gemm_pair_majors(majors, shape, bn):
     ef, et, _ = _run(*shape, *majors, force_bn=bn)
     assert ef < 2e-3 and et < 1e-4, (ef, et)
 
 
-@pytest.mark.parametrize("bn", [-256, 256])
+@pytest.mark.parametrize("bn", [-256, 256, -64])
 def test_gemm_sgd_epilogue_pairs(bn):
     ef, _, flag = _run(520, 600, 256, True, True, mode=2, force_bn=bn)
     assert ef < 2e-3 and flag == 0

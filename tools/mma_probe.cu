@@ -1,0 +1,109 @@
+// Probe (not part of the product library): kind::tf32 tcgen05.mma issue rate
+// with A from shared memory (SS) vs A from tensor memory (TS), and TS with
+// the A block copied smem -> TMEM by tcgen05.cp before every use -- does the
+// narrow-N operand-rate cap of the SS form lift when A comes from
+// TMEM?  One CTA per SM, one issuing thread, operands resident in smem (no
+// TMA), `iters` passes over `kb` K-blocks of 32.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -shared -Xcompiler -fPIC \
+//        -I paper_2207_11019_b200/csrc tools/mma_probe.cu -o tools/_mma_probe.so
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ptx.cuh"
+
+using namespace ppb;
+
+namespace {
+
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t s_desc) {
+    asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(s_desc) : "memory");
+}
+
+// mode 0: SS; 1: TS (A already in TMEM); 2: TS with tcgen05.cp of A per K-block
+template <int N>
+__global__ void __launch_bounds__(128, 1) probe_kernel(int mode, int kb, int iters, unsigned long long* cycles) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint32_t tmem_slot;
+    __shared__ __align__(8) uint64_t done_bar;
+    const int warp = threadIdx.x / 32;
+    // A blocks: kb x 16 KB (128 rows x 128 B), B blocks: kb x N x 128 B
+    uint8_t* A = smem;
+    uint8_t* B = smem + kb * 16384;
+    for (int i = threadIdx.x; i < kb * (16384 + N * 128) / 4; i += blockDim.x)
+        reinterpret_cast<float*>(smem)[i] = 0.001f * (i % 97);
+    if (warp == 0) tmem_alloc(&tmem_slot, 512);
+    if (threadIdx.x == 0) {
+        mbar_init(&done_bar, 1);
+        fence_mbar_init();
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    const uint32_t d_tmem = tmem;              // columns [0, N)
+    const uint32_t a_tmem0 = tmem + 256;       // A slots: 2 x 32 columns at 256
+    const uint32_t idesc = idesc_tf32(N, false, false);
+    if (threadIdx.x == 0) {
+        const long long t0 = clock64();
+        for (int it = 0; it < iters; ++it) {
+            for (int k = 0; k < kb; ++k) {
+                const uint32_t a_addr = smem_u32(A + k * 16384);
+                const uint32_t b_addr = smem_u32(B + k * N * 128);
+                const uint32_t a_slot = a_tmem0 + (k & 1) * 32;
+                if (mode == 2) {
+#pragma unroll
+                    for (int s = 0; s < 4; ++s) tmem_cp_128x256b(a_slot + s * 8, umma_desc(a_addr + s * 32, 16, 1024));
+                }
+#pragma unroll
+                for (int s = 0; s < 4; ++s) {
+                    const uint64_t bd = umma_desc(b_addr + s * 32, 16, 1024);
+                    const uint32_t acc = (it | k | s) != 0;
+                    if (mode == 0) mma_tf32(d_tmem, umma_desc(a_addr + s * 32, 16, 1024), bd, idesc, acc);
+                    else mma_tf32_ts(d_tmem, a_slot + s * 8, bd, idesc, acc);
+                }
+            }
+        }
+        mma_commit(&done_bar);
+        mbar_wait(&done_bar, 0);
+        cycles[blockIdx.x] = clock64() - t0;
+    }
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+}  // namespace
+
+extern "C" int mma_probe(int n, int mode, int kb, int iters, int ctas, unsigned long long* cycles, void* stream) {
+    const int smem = 1024 + kb * (16384 + n * 128);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e;
+    switch (n) {
+        case 64:
+            cudaFuncSetAttribute(probe_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            probe_kernel<64><<<ctas, 128, smem, s>>>(mode, kb, iters, cycles);
+            break;
+        case 128:
+            cudaFuncSetAttribute(probe_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            probe_kernel<128><<<ctas, 128, smem, s>>>(mode, kb, iters, cycles);
+            break;
+        default:
+            cudaFuncSetAttribute(probe_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            probe_kernel<256><<<ctas, 128, smem, s>>>(mode, kb, iters, cycles);
+    }
+    e = cudaGetLastError();
+    return static_cast<int>(e);
+}
