@@ -39,6 +39,21 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
                      const WsAlloc& ws_alloc = nullptr);
 cudaError_t tc_gemm_launch(const TcGemmPlan& p, cudaStream_t s);
 cudaError_t tc_gemm_init_device();
+// per operand-major combination (gemm_tc_inst_*.cu): launch / smem attributes
+template <bool A_MN, bool B_MN>
+cudaError_t tc_launch_mn(const TcGemmPlan& p, cudaStream_t s);
+template <bool A_MN, bool B_MN>
+cudaError_t tc_init_mn();
+#define PPB_TC_DECL(A, B)                                                     \
+    template <>                                                               \
+    cudaError_t tc_launch_mn<A, B>(const TcGemmPlan& p, cudaStream_t s);      \
+    template <>                                                               \
+    cudaError_t tc_init_mn<A, B>();
+PPB_TC_DECL(false, false)
+PPB_TC_DECL(false, true)
+PPB_TC_DECL(true, false)
+PPB_TC_DECL(true, true)
+#undef PPB_TC_DECL
 
 // Halo-reuse implicit conv (conv_halo.cu): a 3x3 stride-1 conv over a padded
 // NHWC grid computed in padded-position space; see halo_conv_prepare.

@@ -27,3 +27,9 @@ cp profiles/${TAG}_ncu.md profiles/${TAG}_gemm_wide_ncu.md profiles/gemm_traffic
 rm -f gpurun_out/${TAG}_gemm_wide.ncu-rep
 [ "${KEEP_REP:-0}" = "1" ] || rm -f gpurun_out/${TAG}_gemm.ncu-rep
 du -sh gpurun_out
+# plan-chooser calibration (profiles/calib_<workload>.json) and its predicted scaling
+if [ "${CALIB:-1}" = "1" ]; then
+  for W in vgg16 wide_mlp; do
+    timeout 900 python tools/calibrate.py $W gpurun_out/calib_${W}.json > gpurun_out/${TAG}_calib_${W}.txt 2>&1; echo "calib $W rc=$?"
+  done
+fi
