@@ -3,6 +3,8 @@ include/pipeplan_b200.h declares (no compute call without a GPU)."""
 import os
 import re
 
+import pytest
+
 from paper_2207_11019_b200 import _lib
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -45,3 +47,22 @@ def test_version_and_error_slot():
     L = _lib.lib()
     assert b"sm_100a" in L.ppb_version()
     assert L.ppb_last_error() is not None
+
+
+def test_cli_usage_errors_exit_2(tmp_path):
+    """pipeplan_b200 (dropin/cli_main.cpp): usage errors exit 2 without touching
+    a GPU; `plan` is pure host code (serialize_plan)."""
+    import json
+    import subprocess
+
+    exe = os.path.join(ROOT, "dropin", "_build", "pipeplan_b200")
+    if not os.path.exists(exe):
+        pytest.skip("dropin/_build/pipeplan_b200 not built (needs the reference sources)")
+    for args in (["demo", "-n", "0"], ["frobnicate"], [], ["demo", "--update", "maybe"], ["plan", "--dims", "5"]):
+        r = subprocess.run([exe, *args], capture_output=True, text=True, timeout=60)
+        assert r.returncode == 2 and "usage error" in r.stderr, (args, r.stderr)
+    r = subprocess.run([exe, "plan", "--dims", "8,6,4", "-n", "2", "-Z", "2", "--out", str(tmp_path)],
+                       capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0, r.stderr
+    doc = json.loads((tmp_path / "plan.json").read_text())
+    assert doc["n"] == 2 and len(doc["submodules"]) == 2 and len(doc["boundaries"]) == 1
