@@ -393,8 +393,9 @@ def run_ours(args, rank, world, dist):
                                f"{api.device_count()} GPU(s)")
         ctx = api.Context(list(range(n)))
     cfg = TrainConfig(alpha0=1e-4, decay=1e-2, iterations=1)
-    opts = PartitionedTrainOptions(multiclass_accuracy=True, use_graph=True, pipeline_gate=2)
+    opts = PartitionedTrainOptions(multiclass_accuracy=True, use_graph=True, pipeline_gate=2, memory_mode=args.memory)
     sess = api.Session(ctx, net, batch, plan, m, UpdateMode.async_per_module, cfg, opts)
+    mem_total, mem_stash = sess.memory()
     sess.load_batch(X, y)
     barrier(dist)
     # warm-up
@@ -485,6 +486,8 @@ def run_ours(args, rank, world, dist):
                        "gflop_per_step": algorithmic_flops(net, batch) / 1e9,
                        "plan": (f"plan_search choice: {choice}" if choice else
                                 f"build_plan n={plan_devs} Z=1, m={m}") + ", async_per_module, CUDA graph",
+                       "memory_mode": args.memory, "micro_batches": m,
+                       "device_bytes": mem_total, "stash_bytes": mem_stash,
                        "parallelism": f"layer-wise partition over {n} GPU(s)" + (
                            f" ({plan_devs} plan devices sharing cuda:0)" if plan_devs != n else ""),
                        "l2": {"wide_mlp": "inputs larger than L2 (weights 1 GiB + activations 0.5 GiB per step)",
@@ -504,6 +507,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="vgg16", choices=sorted(WORKLOADS))
     ap.add_argument("--m", type=int, default=1, help="micro-batches per step")
+    ap.add_argument("--memory", default="stash_all", choices=["stash_all", "proposed"],
+                    help="activation stash policy (proposed: min(m, gate) resident micro-batches, "
+                         "weight gradients per micro-batch)")
     ap.add_argument("--plan", default="auto", choices=["auto", "all"],
                     help="N>1: plan_search choice (auto) or every layer over all N GPUs (all)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

@@ -152,8 +152,21 @@ typedef struct {
                                   1: extension, ACC = #(pred == label) / b            */
     int use_graph;             /* capture the step in a CUDA graph (1) or launch eagerly (0) */
     int pipeline_gate;         /* F(i,j) waits for B(i,j-gate) (schedule.cpp:293-296); 0 = off */
-    int reserved[8];
+    int memory_mode;           /* PPB_MEMORY_*: activation stash policy (simulate.hpp:14-16 MemoryMode) */
+    int reserved[7];
 } ppb_options;
+
+/* Activation stash policy (the reference simulator's MemoryMode,
+ * include/pipeplan/simulate.hpp:14-16).  STASH_ALL is the reference
+ * executor: every micro-batch's activations stay live until the step's weight
+ * gradients, computed once over all b rows (train_partitioned.cpp:228-231,
+ * :504-512).  PROPOSED is the paper's schedule: the weight gradient of
+ * micro-batch j is accumulated as soon as its backward reaches the layer and
+ * its activation / error-signal slots are reused by micro-batch
+ * j + min(m, pipeline_gate), so only min(m, gate) micro-batches are resident
+ * (tf32 precision; with m = 1 both policies are the same step). */
+#define PPB_MEMORY_STASH_ALL 0
+#define PPB_MEMORY_PROPOSED 1
 
 /* Layer description for nets with convolution layers (the BASELINE CNN
  * configs; the reference itself is dense-only).  kind = PPB_LAYER_DENSE uses
@@ -194,6 +207,11 @@ int ppb_train_partitioned(ppb_context* ctx, const int* dims, const int* acts, in
                           int batch, const int* plan, int plan_len, int m, int mode,
                           const ppb_train_config* cfg, const ppb_options* opts, double* W_out,
                           double* b_out, double* loss_hist, double* acc_hist);
+
+/* Device bytes the session holds on all its GPUs: total, and the part that
+ * scales with the number of resident micro-batches (activations, pre-pool
+ * outputs, pool routing, error signals, merge slots, im2col rows). */
+int ppb_session_memory(ppb_session* s, size_t* total_bytes, size_t* stash_bytes);
 
 /* Session API: the same step with state resident on the GPUs, for callers
  * that stream batches (and for benchmarking).  A session is

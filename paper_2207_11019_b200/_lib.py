@@ -44,7 +44,8 @@ class OptionsC(C.Structure):
         ("multiclass_accuracy", C.c_int),
         ("use_graph", C.c_int),
         ("pipeline_gate", C.c_int),
-        ("reserved", C.c_int * 8),
+        ("memory_mode", C.c_int),
+        ("reserved", C.c_int * 7),
     ]
 
 
@@ -94,6 +95,7 @@ _SIGS = {
     "ppb_session_sync": (C.c_int, [C.c_void_p]),
     "ppb_session_history": (C.c_int, [C.c_void_p, _f64p, _f64p, C.c_int, _i32p]),
     "ppb_session_get_net": (C.c_int, [C.c_void_p, _f64p, _f64p]),
+    "ppb_session_memory": (C.c_int, [C.c_void_p, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
     "ppb_session_read_tensor": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, _f64p, C.c_size_t,
                                           C.POINTER(C.c_size_t)]),
     "ppb_session_kernels_per_step": (C.c_int, [C.c_void_p, _i32p]),

@@ -282,6 +282,11 @@ class PartitionedTrainOptions:  # train_partitioned.hpp:9-11 + GPU knobs
     multiclass_accuracy: bool = False
     use_graph: bool = True
     pipeline_gate: int = 2
+    # activation stash policy (simulate.hpp:14-16 MemoryMode): "stash_all" is
+    # the reference executor (every micro-batch resident, weight gradients over
+    # all b rows); "proposed" keeps min(m, pipeline_gate) micro-batches and
+    # accumulates weight gradients per micro-batch
+    memory_mode: str = "stash_all"
 
     def to_c(self) -> _lib.OptionsC:
         o = _lib.OptionsC()
@@ -290,6 +295,7 @@ class PartitionedTrainOptions:  # train_partitioned.hpp:9-11 + GPU knobs
         o.multiclass_accuracy = int(self.multiclass_accuracy)
         o.use_graph = int(self.use_graph)
         o.pipeline_gate = int(self.pipeline_gate)
+        o.memory_mode = {"stash_all": 0, "proposed": 1}[self.memory_mode]
         return o
 
 
@@ -602,6 +608,13 @@ class Session:
         k = C.c_int(0)
         check(_lib.lib().ppb_session_kernels_per_step(self._h, C.byref(k)))
         return k.value
+
+    def memory(self):
+        """(total device bytes, stash bytes): the stash part scales with the
+        resident micro-batches (activations, error signals, merge slots)."""
+        t, st = C.c_size_t(0), C.c_size_t(0)
+        check(_lib.lib().ppb_session_memory(self._h, C.byref(t), C.byref(st)))
+        return t.value, st.value
 
 
 _default_ctx = {}

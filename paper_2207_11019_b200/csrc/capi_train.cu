@@ -50,6 +50,9 @@ SessionConfig make_cfg(int batch, int m, int mode, const ppb_train_config* cfg, 
     c.multiclass = opts->multiclass_accuracy;
     c.use_graph = opts->use_graph;
     c.gate = opts->pipeline_gate;
+    c.stash = opts->memory_mode;
+    if (c.stash != PPB_MEMORY_STASH_ALL && c.stash != PPB_MEMORY_PROPOSED)
+        throw std::invalid_argument("unknown memory mode");
     if (c.loss != 0 && c.loss != 1) throw std::invalid_argument("unknown loss kind");
     if (c.precision != 0 && c.precision != 1) throw std::invalid_argument("unknown precision");
     return c;
@@ -187,6 +190,13 @@ extern "C" int ppb_session_sync(ppb_session* s) {
 
 extern "C" int ppb_session_history(ppb_session* s, double* loss_hist, double* acc_hist, int cap, int* count) {
     return ppb_guard([&] { s->s->history(loss_hist, acc_hist, cap, count); });
+}
+
+extern "C" int ppb_session_memory(ppb_session* s, size_t* total_bytes, size_t* stash_bytes) {
+    return ppb_guard([&] {
+        if (total_bytes) *total_bytes = s->s->device_bytes();
+        if (stash_bytes) *stash_bytes = s->s->stash_bytes();
+    });
 }
 
 extern "C" int ppb_session_get_net(ppb_session* s, double* W_out, double* b_out) {

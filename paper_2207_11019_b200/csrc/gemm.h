@@ -183,6 +183,9 @@ struct SplitK {
     int fixup = 0;
     int* counters = nullptr;
     int deferred = 0;  // reduction carried by the next GEMM's SideJob (no kernel here)
+    // raw partial sums into workspace slices even when splits == 1 (per
+    // micro-batch weight gradients, summed by one reduction after the last)
+    int partial = 0;
 };
 
 // Padded-position geometry of the halo conv kernel (conv_halo.cu): GEMM row
@@ -229,6 +232,12 @@ struct GemmDesc {
     Operand a, b;
     int M = 0, N = 0, K = 0;
     EpiParams epi;
+    // partial_out: store the raw accumulators into split-K workspace slices
+    // (ws_alloc provides them) and launch no reduction; `epi` is the epilogue
+    // the later reduction (tc_gemm_launch_reduce) applies.  force_splits > 0
+    // fixes the split count (every micro-batch's GEMM writes the same slices).
+    int partial_out = 0;
+    int force_splits = 0;
 };
 
 }  // namespace ppb

@@ -387,7 +387,7 @@ bool tma_store_setup_splitk(const SplitK& sk, int M, int N, TmaStore* ts) {
     }();
     auto enc = get_encode();
     static const bool off_sk = getenv("PPB_NO_TMA_SPLITK") != nullptr;
-    if (off || off_sk || enc == nullptr || sk.splits < 2 || sk.ws == nullptr) return false;
+    if (off || off_sk || enc == nullptr || (sk.splits < 2 && !sk.partial) || sk.ws == nullptr) return false;
     const int inner = sk.trans ? M : N, outer = sk.trans ? N : M;
     if (inner < 32 || sk.ld % 4 != 0 || sk.stride % 4 != 0 || (reinterpret_cast<uintptr_t>(sk.ws) & 15u) != 0)
         return false;
@@ -446,7 +446,8 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
         const char* e = getenv("PPB_NO_HALO");
         return e != nullptr && *e != '\0' && *e != '0';
     }();
-    if ((force_bn >= 1000 || (force_bn == 0 && !no_halo && halo_conv_preferred(d))) && halo_conv_eligible(d))
+    if (!d.partial_out && (force_bn >= 1000 || (force_bn == 0 && !no_halo && halo_conv_preferred(d))) &&
+        halo_conv_eligible(d))
         return halo_conv_prepare(d, out, force_bn, err, errlen);
     if (force_bn >= 1000) {
         snprintf(err, errlen, "halo conv tile forced on an ineligible GEMM");
@@ -549,8 +550,13 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
     // small C_out x 9*C_in output, K = every pixel of the batch); partial
     // sums are reduced in split order (deterministic).
     {
-        int splits = best_sp > 0 ? best_sp : splits_for(tiles, units);
-        if (splits >= 2) {
+        int splits = d.force_splits > 0 ? d.force_splits : best_sp > 0 ? best_sp : splits_for(tiles, units);
+        if (splits > nk) splits = nk;
+        if (d.partial_out && !ws_alloc) {
+            snprintf(err, errlen, "partial-sum GEMM without a workspace");
+            return false;
+        }
+        if (splits >= 2 || d.partial_out) {
             const int kps = (nk + splits - 1) / splits;
             splits = (nk + kps - 1) / kps;
             p.sk.splits = splits;
@@ -567,7 +573,8 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
             // last warp's serial row-per-thread reads sit on the tile's tail:
             // VGG step 2.54 -> 3.07 ms), so opt-in only
             const bool fixup_on = dev_knob("PPB_SPLITK_FIXUP");
-            if (splits <= 8 && fixup_on) {
+            p.sk.partial = d.partial_out;
+            if (splits <= 8 && fixup_on && !d.partial_out) {
                 const size_t nctr = static_cast<size_t>(tiles) * cg * 8;
                 float* c = ws_alloc(nctr);
                 if (c != nullptr && cudaMemset(c, 0, nctr * sizeof(int)) == cudaSuccess) {
@@ -597,7 +604,7 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
         if (p.sk.splits > 1 || ring(p.stages) + need > kCapSmem) p.epi.db_partial = nullptr;
         else p.db_smem = need;
     }
-    if (p.sk.splits == 1 ? tma_store_setup(p.epi, d.M, d.N, nullptr, &p.ts)
+    if (p.sk.splits == 1 && !p.sk.partial ? tma_store_setup(p.epi, d.M, d.N, nullptr, &p.ts)
                          : tma_store_setup_splitk(p.sk, d.M, d.N, &p.ts)) {
         // staging after the barrier block and the db rows, 1 KB aligned (SW128 boxes)
         const int off = 1024 + (p.db_smem + 1023) / 1024 * 1024;
@@ -644,6 +651,11 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
     }
     *out = p;
     return true;
+}
+
+cudaError_t tc_gemm_launch_reduce(const TcGemmPlan& p, cudaStream_t s) {
+    if (p.M <= 0 || p.N <= 0) return cudaSuccess;
+    return launch_splitk_reduce(p, s);
 }
 
 cudaError_t tc_gemm_launch(const TcGemmPlan& p, cudaStream_t s) {

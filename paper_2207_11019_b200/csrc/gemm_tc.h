@@ -38,6 +38,9 @@ using WsAlloc = std::function<float*(size_t)>;
 bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err, size_t errlen,
                      const WsAlloc& ws_alloc = nullptr);
 cudaError_t tc_gemm_launch(const TcGemmPlan& p, cudaStream_t s);
+// The reduction + epilogue of a partial-sum plan on its own: p.sk.splits
+// slices at p.sk.ws summed in slice order, then p.epi (and the bias job).
+cudaError_t tc_gemm_launch_reduce(const TcGemmPlan& p, cudaStream_t s);
 cudaError_t tc_gemm_init_device();
 // per operand-major combination (gemm_tc_inst_*.cu): launch / smem attributes
 template <bool A_MN, bool B_MN>

@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float v[32];
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-                if (sk.splits > 1) {  // raw partial sums for splitk_epilogue_kernel
+                if (sk.splits > 1 || sk.partial) {  // raw partial sums for splitk_epilogue_kernel
                     const int nn = n0 + c * 32;
                     if (ts.n) {
                         if (!(epi.dbg & 2)) tma_store_partial(ts, epi_box(stg, warp - 4, bsel), lane, v, m0 + q * 32, nn, split);
@@ -677,27 +677,10 @@ __global__ void __launch_bounds__(256) splitk_epilogue_kernel(
 }
 
 
-template <bool A_MN, bool B_MN, int BN, int CG>
-cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
-    using C = TcCfg<BN, CG>;
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(p.grid);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = 1024 + p.stages * C::kStageBytes + 256 + p.db_smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<A_MN, B_MN, BN, CG>, p.ta, p.tb, p.M, p.N, p.K, p.epi,
-                                       p.ga, p.gb, p.sk, p.ts, p.stages, p.sj);
-    const bool probe_no_reduce = dev_knob("PPB_PROBE_NO_REDUCE");  // timing probe (wrong results)
-    if (e != cudaSuccess || p.sk.splits <= 1 || p.sk.fixup || p.sk.deferred || probe_no_reduce) return e;
+// The split-K reduction + epilogue of a GEMM (p.sk.splits partial slices at
+// p.sk.ws, summed in slice order) as its own launch.
+cudaError_t launch_splitk_reduce(const TcGemmPlan& p, cudaStream_t s) {
+    cudaError_t e = cudaSuccess;
     const long long R = p.sk.trans ? p.N : p.M, Cc = p.sk.trans ? p.M : p.N;
     const long long items = R * ((Cc + 3) / 4);
     const unsigned bblocks = p.sk.bias != nullptr ? static_cast<unsigned>((p.sk.bu + 31) / 32) : 0u;
@@ -721,8 +704,34 @@ cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
         rc.blockDim = dim3(256, 1);
         e = cudaLaunchKernelEx(&rc, splitk_epilogue_kernel<1>, p.epi, p.sk, p.M, p.N);
     }
+
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
+}
+
+template <bool A_MN, bool B_MN, int BN, int CG>
+cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
+    using C = TcCfg<BN, CG>;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(p.grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 1024 + p.stages * C::kStageBytes + 256 + p.db_smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<A_MN, B_MN, BN, CG>, p.ta, p.tb, p.M, p.N, p.K, p.epi,
+                                       p.ga, p.gb, p.sk, p.ts, p.stages, p.sj);
+    const bool probe_no_reduce = dev_knob("PPB_PROBE_NO_REDUCE");  // timing probe (wrong results)
+    if (e != cudaSuccess || p.sk.splits <= 1 || p.sk.fixup || p.sk.deferred || p.sk.partial || probe_no_reduce)
+        return e;
+    return launch_splitk_reduce(p, s);
 }
 
 }  // namespace

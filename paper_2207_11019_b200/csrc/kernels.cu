@@ -896,6 +896,20 @@ cudaError_t launch_bias_update(const float* delta, long long ld, long long rows,
     return cudaGetLastError();
 }
 
+cudaError_t launch_colsum(const float* delta, long long ld, long long rows, int u, float* partial, cudaStream_t s) {
+    if (u <= 0 || rows <= 0) return cudaSuccess;
+    const int chunks = colsum_chunks(rows);
+    const bool v4 = u % 4 == 0 && ld % 4 == 0 && reinterpret_cast<uintptr_t>(delta) % 16 == 0;
+    const int groups = v4 ? u / 4 : u;
+    const int gpb = groups < 256 ? groups : 256;
+    const int block = (256 / gpb) * gpb;
+    const dim3 grid(chunks, (groups + gpb - 1) / gpb);
+    const size_t shmem = sizeof(float) * block * (v4 ? 4 : 1);
+    if (v4) pdl_launch(colsum_rows_kernel<4>, dim3(grid), dim3(block), shmem, s, delta, ld, rows, u, partial);
+    else pdl_launch(colsum_rows_kernel<1>, dim3(grid), dim3(block), shmem, s, delta, ld, rows, u, partial);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_convert_f64(const double* src, int rows, int cols, float* dst, long long ld,
                                cudaStream_t s) {
     const long long n = static_cast<long long>(rows) * cols;

@@ -52,6 +52,9 @@ inline int colsum_chunks(long long rows) {
 }
 cudaError_t launch_bias_update(const float* delta, long long ld, long long rows, int u, float* partial,
                                float* bias, const double* alpha, float inv_b, cudaStream_t s);
+// The first phase alone: colsum_chunks(rows) partial rows of column sums into
+// `partial` (per-micro-batch bias gradients, summed later in chunk order).
+cudaError_t launch_colsum(const float* delta, long long ld, long long rows, int u, float* partial, cudaStream_t s);
 
 // fp64 (host layout, dense) -> fp32 padded rows.
 cudaError_t launch_convert_f64(const double* src, int rows, int cols, float* dst, long long ld,

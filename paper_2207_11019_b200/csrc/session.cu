@@ -46,7 +46,12 @@ struct Session::Gpu {
     cudaEvent_t ev_done = nullptr;
     bool needs_x = false, needs_labels = false;
 
-    void* alloc(size_t bytes) {
+    size_t bytes_total = 0, bytes_stash = 0;
+
+    // stash: scales with the resident micro-batches (reported by ppb_session_memory)
+    void* alloc(size_t bytes, bool stash = false) {
+        bytes_total += bytes;
+        if (stash) bytes_stash += bytes;
         void* p = nullptr;
         cudaSetDevice(ordinal);
         cudaError_t e = cudaMalloc(&p, bytes < 16 ? 16 : bytes);
@@ -90,6 +95,16 @@ struct Session::WLayer {
     std::vector<int> fwd_op, dgrad_op;   // [j]
     TcGemmPlan p_wgrad;
     GemmDesc d_wgrad;
+    // proposed memory policy: per-micro-batch weight-gradient GEMMs writing
+    // raw partial sums into slices [j * acc_slices, (j + 1) * acc_slices) of
+    // acc_ws, one reduction (+ SGD) after the last micro-batch
+    std::vector<TcGemmPlan> p_wg;
+    std::vector<GemmDesc> d_wg;
+    std::vector<int> wg_op;  // [j]
+    TcGemmPlan p_red;
+    float* acc_ws = nullptr;
+    int acc_slices = 0;
+    int cc_mb = 1;  // colsum chunks of one micro-batch's error signal
     std::vector<TcGemmPlan> p_fwd, p_dgrad;
     std::vector<GemmDesc> d_fwd, d_dgrad;
 };
@@ -122,6 +137,18 @@ float* Session::act_buf(int ordinal, int layer) {
 }
 
 float* Session::q_buf(int ordinal) { return gpu_of(ordinal).q; }
+
+size_t Session::device_bytes() const {
+    size_t n = 0;
+    for (const auto& g : gpus_) n += g->bytes_total;
+    return n;
+}
+
+size_t Session::stash_bytes() const {
+    size_t n = 0;
+    for (const auto& g : gpus_) n += g->bytes_stash;
+    return n;
+}
 
 // ------------------------------------------------------------------ construction
 
@@ -216,6 +243,14 @@ Session::Session(const std::vector<int>& device_map, const NetDesc& net, const d
     mb_sizes_ = split_microbatches(cfg_.batch, cfg_.m);
     mb_off_.assign(cfg_.m + 1, 0);
     for (int j = 0; j < cfg_.m; ++j) mb_off_[j + 1] = mb_off_[j] + mb_sizes_[j];
+    // activation stash: every micro-batch resident (stash_all), or a ring of
+    // min(m, gate) slots (proposed: F(j) reuses the slots of micro-batch
+    // j - ring after its whole backward, weight gradients included)
+    if (cfg_.stash == 1 && cfg_.precision != 0)
+        throw std::invalid_argument("the proposed memory mode runs on the tf32 tensor-core path");
+    per_mb_wgrad_ = cfg_.stash == 1 && cfg_.m > 1;
+    ring_ = per_mb_wgrad_ && cfg_.gate > 0 ? std::min(cfg_.m, cfg_.gate) : cfg_.m;
+    ring_rows_ = ring_ == cfg_.m ? cfg_.batch : static_cast<long long>(ring_) * mb_sizes_[0];
     if (cfg_.loss == 1 && net_.acts[L - 1] != 2)
         throw std::runtime_error("cross_entropy needs probability outputs (softmax last layer required)");
     if (cfg_.loss == 0 && net_.acts[L - 1] == 2)
@@ -406,13 +441,14 @@ void Session::alloc_buffers() {
     for (auto& [l, set] : need)
         for (int ord : set) {
             Gpu& g = gpu_of(ord);
-            g.act[l] = static_cast<float*>(g.alloc(sizeof(float) * b * img_elems(l)));
+            const long long rows = l == 0 ? b : ring_rows_;  // the batch X stays resident
+            g.act[l] = static_cast<float*>(g.alloc(sizeof(float) * rows * img_elems(l), l > 0));
         }
     for (int wi : layer_workers_[1]) gpu_of(workers_[wi]->gpu).needs_x = true;
     for (int wi : layer_workers_[L]) {
         Gpu& g = gpu_of(workers_[wi]->gpu);
         g.needs_labels = true;
-        if (softmax && g.q == nullptr) g.q = static_cast<float*>(g.alloc(sizeof(float) * b * ld_of(F)));
+        if (softmax && g.q == nullptr) g.q = static_cast<float*>(g.alloc(sizeof(float) * ring_rows_ * ld_of(F), true));
     }
     for (auto& gp : gpus_) {
         Gpu& g = *gp;
@@ -446,17 +482,18 @@ void Session::alloc_buffers() {
                 const bool consumer_dense = wl.layer < L && net_.info[wl.layer].kind == 0;
                 if (li.pool == 2 || consumer_dense) {
                     wl.ldu = ld_of(wl.u);
-                    wl.U = static_cast<float*>(g.alloc(sizeof(float) * b * li.Ho() * li.Wo() * wl.ldu));
+                    wl.U = static_cast<float*>(g.alloc(sizeof(float) * ring_rows_ * li.Ho() * li.Wo() * wl.ldu, true));
                 }
                 if (li.pool == 2)
-                    wl.argmax = static_cast<unsigned char*>(g.alloc(static_cast<size_t>(b) * li.Hq() * li.Wq() * wl.u));
+                    wl.argmax = static_cast<unsigned char*>(
+                        g.alloc(static_cast<size_t>(ring_rows_) * li.Hq() * li.Wq() * wl.u, true));
                 if (li.dense_conv) {
                     const int P = li.Ho() * li.Wo(), Q = li.H * li.W;
                     wl.ldwx = static_cast<long long>(Q) * li.in_units;
                     wl.Wx = static_cast<float*>(g.alloc(sizeof(float) * P * wl.u * wl.ldwx));
                     wl.dWx = static_cast<float*>(g.alloc(sizeof(float) * P * wl.u * wl.ldwx));
                     wl.ldk = wl.ldwx;
-                    wl.dcols = static_cast<float*>(g.alloc(sizeof(float) * b * wl.ldk));
+                    wl.dcols = static_cast<float*>(g.alloc(sizeof(float) * ring_rows_ * wl.ldk, true));
                     DenseConvGeom& dg = wl.dcg;
                     dg.u = wl.u;
                     dg.C = li.in_units;
@@ -470,22 +507,25 @@ void Session::alloc_buffers() {
                     dg.ldx = wl.ldwx;
                 }
                 if (li.generic) {
-                    const long long pix = static_cast<long long>(b) * li.Ho() * li.Wo();
+                    const long long pix = ring_rows_ * li.Ho() * li.Wo();
                     const int kc = li.ksz * li.ksz * li.in_units;
                     wl.ldc = (kc + 31) / 32 * 32;
                     wl.ldk = ld_of(kc);
-                    wl.cols = static_cast<float*>(g.alloc(sizeof(float) * pix * wl.ldc));
-                    wl.dcols = static_cast<float*>(g.alloc(sizeof(float) * pix * wl.ldk));
+                    wl.cols = static_cast<float*>(g.alloc(sizeof(float) * pix * wl.ldc, true));
+                    wl.dcols = static_cast<float*>(g.alloc(sizeof(float) * pix * wl.ldk, true));
                 }
             } else {
                 wl.delta_img = wl.ldd;
             }
-            wl.delta = static_cast<float*>(g.alloc(sizeof(float) * b * wl.delta_img));
+            wl.delta = static_cast<float*>(g.alloc(sizeof(float) * ring_rows_ * wl.delta_img, true));
             // bias-gradient partials: dense colsum chunks, or one row per (micro-batch, merge block) for conv
-            const long long prow =
+            // (proposed policy: per-micro-batch column sums, [m][colsum chunks of one micro-batch])
+            wl.cc_mb = colsum_chunks(static_cast<long long>(mb_sizes_[0]) * (wl.delta_img / wl.ldd));
+            const long long prow = std::max<long long>(
                 li.kind == 1 ? std::max<long long>(static_cast<long long>(cfg_.m) * conv_merge_blocks() * li.Ho() * li.Wo(),
                                                    kColsumChunks)
-                             : kColsumChunks;
+                             : kColsumChunks,
+                static_cast<long long>(cfg_.m) * wl.cc_mb);
             wl.partial = static_cast<float*>(g.alloc(sizeof(float) * prow * wl.u));
             // upload the shard rows [lo, hi) (train_partitioned.cpp:168-169), fp64 -> fp32;
             // conv rows [k][k][C_in] go to the GEMM layout [k*k][ck] (zero-padded channels)
@@ -528,17 +568,17 @@ void Session::alloc_buffers() {
             Worker& w = *workers_[wi];
             WLayer& wl = w.at(l - 1);
             Gpu& g = gpu_of(w.gpu);
-            long long rows = b;
+            long long rows = ring_rows_;
             if (dl.kind == 0) {
                 wl.slot_ld = wl.ldd;
             } else if (cl.kind == 1) {  // conv consumer: pixel-major over the pooled grid
                 wl.slot_ld = ld_of(wl.u);
-                rows = static_cast<long long>(b) * dl.Hq() * dl.Wq();
+                rows = ring_rows_ * dl.Hq() * dl.Wq();
             } else {  // dense consumer: CHW-flatten columns of this shard's channels
                 wl.slot_ld = ld_of(wl.u * dl.Hq() * dl.Wq());
             }
             for (int k = 0; k < ncontrib; ++k)
-                wl.slots.push_back(static_cast<float*>(g.alloc(sizeof(float) * rows * wl.slot_ld)));
+                wl.slots.push_back(static_cast<float*>(g.alloc(sizeof(float) * rows * wl.slot_ld, true)));
         }
     }
     for (auto& gp : gpus_) {
@@ -622,10 +662,153 @@ void Session::build_ops() {
         L + 1, std::vector<std::map<int, std::vector<int>>>(m));
     std::vector<std::vector<int>> loss_ops(m);
 
+    // weight-gradient GEMM of one worker layer (dW = delta^T . a_{l-1}) over
+    // micro-batch j, or over all b rows of the batch when j < 0 (the
+    // stash_all executor: one GEMM per layer, K = every row); epilogue = the
+    // update (SGD on W, or plain dWx for a dense-conv layer)
+    auto wgrad_desc = [&](Worker& w, WLayer& wl, int j, GemmDesc& d, double* wfl, long long* bias_rows) {
+        const int l = wl.layer;
+        const int fi = net_.dims[l - 1];
+        const LayerInfo& li = net_.info[l - 1];
+        Gpu& g = gpu_of(w.gpu);
+        const int rows = j < 0 ? cfg_.batch : mb_sizes_[j];
+        const long long so = j < 0 ? 0 : soff(j);
+        const float* delta = wl.delta + so * wl.delta_img;
+        const float* ain = act_buf(w.gpu, l - 1) + (j < 0 ? 0 : aoff(l - 1, j)) * img_elems(l - 1);
+        d = GemmDesc{};
+        *bias_rows = rows;
+        if (li.kind == 1) {
+            ConvShape cs;
+            cs.N = rows;
+            cs.H = li.H;
+            cs.W = li.W;
+            cs.C = li.in_units;
+            cs.ksz = li.ksz;
+            cs.pad = li.pad;
+            cs.u = wl.u;
+            if (li.dense_conv) {  // dWx = delta^T . a over the images (K = images); folded by the update
+                const int P = li.Ho() * li.Wo(), Q = li.H * li.W;
+                d.a = Operand{delta, rows, P * wl.u, wl.delta_img, true};
+                d.b = Operand{ain, rows, Q * li.in_units, img_elems(l - 1), true};
+                d.M = P * wl.u;
+                d.N = Q * li.in_units;
+                d.K = rows;
+            } else if (li.dense_delta) {  // dense wgrad: K = output pixels, unpadded error signal x im2col rows
+                const int kc = li.ksz * li.ksz * li.in_units;
+                const int pix = rows * li.Ho() * li.Wo();
+                const float* colsp = li.generic ? wl.cols + so * li.Ho() * li.Wo() * wl.ldc : ain;
+                const long long ldc = li.generic ? wl.ldc : lay_[l - 1].ld;
+                d.a = Operand{delta, pix, wl.u, wl.ldd, true};
+                d.b = Operand{colsp, pix, kc, ldc, true};
+                d.M = wl.u;
+                d.N = kc;
+                d.K = pix;
+                if (wl.u < 128 && kc > wl.u) {  // dW^T: the wide side fills the 128-row tiles
+                    std::swap(d.a, d.b);
+                    std::swap(d.M, d.N);
+                }
+            } else if (li.im2col) {  // B = im2col rows (pixel-major, MN = k*k*C)
+                d = conv_wgrad_desc(cs, delta, wl.ldd, ain, lay_[l - 1].ld, false);
+                const int kc = li.ksz * li.ksz * li.in_units;
+                d.b = Operand{ain, rows * li.Ho() * li.Wo(), kc, lay_[l - 1].ld, true};
+                d.N = kc;
+            } else {
+                d = conv_wgrad_desc(cs, delta, wl.ldd, ain, lay_[l - 1].ld, wl.u < 128);
+            }
+            *wfl = li.dense_conv ? 2.0 * rows * li.Ho() * li.Wo() * wl.u * li.H * li.W * li.in_units  // executed
+                                 : 2.0 * rows * li.Ho() * li.Wo() * wl.u * li.ksz * li.ksz * li.in_units;
+            *bias_rows = static_cast<long long>(rows) * (wl.delta_img / wl.ldd);  // zero borders add nothing
+        } else {
+            d.a = Operand{delta, rows, wl.u, wl.ldd, true};
+            d.b = Operand{ain, rows, fi, lay_[l - 1].ld, true};
+            d.M = wl.u;
+            d.N = fi;
+            d.K = rows;
+            if (wl.u < 128 && fi > wl.u) {  // dW^T: the wide side fills the 128-row tiles
+                std::swap(d.a, d.b);
+                std::swap(d.M, d.N);
+            }
+            *wfl = 2.0 * wl.u * fi * static_cast<double>(rows);
+        }
+        const bool wt = d.M != wl.u;
+        d.epi = EpiParams{};
+        d.epi.mode = EPI_SGD;
+        d.epi.W = wl.W;
+        d.epi.ldw = wl.ldw;
+        d.epi.sgd_t = wt ? 1 : 0;
+        d.epi.alpha = &g.st->alpha;
+        d.epi.inv_b = 1.f / static_cast<float>(cfg_.batch);
+        d.epi.flag = &g.st->diverge_flag;
+        if (li.dense_conv) {  // plain dWx; the fold kernel applies SGD to W and re-expands Wx
+            d.epi = EpiParams{};
+            d.epi.mode = EPI_STORE;
+            d.epi.dst[d.epi.ndst++] = wl.dWx;
+            d.epi.ldd = wl.ldwx;
+        }
+    };
+    // conv layers whose bias-gradient partials come with the backward merges
+    // ([j][merge block][u] rows written by conv_merge / the EPI_MERGE epilogue)
+    auto bias_from_merge = [&](const WLayer& wl) { return net_.info[wl.layer - 1].kind == 1 && !wl.db_colsum; };
+    // proposed memory policy: micro-batch j's weight gradients as soon as its
+    // backward has produced every error signal (raw partial sums into the
+    // layer's slices for micro-batch j, no update), and its bias column sums
+    std::vector<int> bjoin(m, -1);
+    auto per_mb_wgrads = [&](int j, int first_op) {
+        for (auto& wp : workers_) {
+            Worker& w = *wp;
+            for (auto wit = w.layers.rbegin(); wit != w.layers.rend(); ++wit) {
+                WLayer& wl = *wit;
+                cur_layer_ = wl.layer;
+                if (wl.p_wg.empty()) {
+                    wl.p_wg.resize(m);
+                    wl.d_wg.resize(m);
+                    wl.wg_op.clear();
+                }
+                GemmDesc& d = wl.d_wg[j];
+                double wfl;
+                long long brows;
+                wgrad_desc(w, wl, j, d, &wfl, &brows);
+                d.partial_out = 1;
+                d.force_splits = j == 0 ? 0 : wl.acc_slices;
+                Gpu* g = &gpu_of(w.gpu);
+                WLayer* wlp = &wl;
+                const int mm = m;
+                WsAlloc ws = [g, wlp, j, mm](size_t n) -> float* {
+                    if (j == 0) {
+                        wlp->acc_ws = static_cast<float*>(g->alloc(sizeof(float) * n * mm));
+                        return wlp->acc_ws;
+                    }
+                    return wlp->acc_ws + static_cast<long long>(j) * wlp->acc_slices * wlp->p_wg[0].sk.stride;
+                };
+                char err[256];
+                if (!tc_gemm_prepare(d, &wl.p_wg[j], 0, err, sizeof(err), ws))
+                    throw std::runtime_error(std::string("GEMM setup: ") + err);
+                cur_info_ = wl.p_wg[j].bn | (wl.p_wg[j].cg << 10) | (wl.p_wg[j].sk.splits << 12);
+                if (j == 0) wl.acc_slices = wl.p_wg[0].sk.splits;
+                const int gop = add_op(w.gpu, w.su, gemm_launch(&wl.p_wg[j], &wl.d_wg[j], w.su), wl.delta_ready[j], 1,
+                                       OP_WGRAD_GEMM, wfl);
+                wl.wg_op.push_back(gop);
+                if (!bias_from_merge(wl)) {
+                    const float* dj = wl.delta + soff(j) * wl.delta_img;
+                    const long long ldd = wl.ldd;
+                    const int u = wl.u;
+                    float* part = wl.partial + static_cast<long long>(j) * wl.cc_mb * wl.u;
+                    cudaStream_t s = w.su;
+                    wl.wg_op.push_back(add_op(w.gpu, s, [=]() { return launch_colsum(dj, ldd, brows, u, part, s); },
+                                              wl.delta_ready[j], 1, OP_BIAS));
+                }
+            }
+        }
+        std::vector<int> all;
+        for (int i = first_op; i < static_cast<int>(ops_.size()); ++i) all.push_back(i);
+        bjoin[j] = add_op(g0.ordinal, g0.main, nullptr, all, 0);
+    };
+
     // ---------------- forward of micro-batch j (train_partitioned.cpp:245-419)
     auto forward = [&](int j) {
         const int rows = mb_sizes_[j];
-        const long long off = mb_off_[j];
+        const long long off = mb_off_[j];  // batch rows (X, labels, per-sample loss)
+        const long long so = soff(j);      // stash slot rows (activations l >= 1, error signals, ...)
         for (int l = 1; l <= L; ++l) {
             cur_layer_ = l;
             const SubModule& sm = module_of_layer(l);
@@ -661,6 +844,9 @@ void Session::build_ops() {
                 if (l == w.layers.front().layer && cfg_.gate > 0 && j - cfg_.gate >= 0 &&
                     w.last_bwd[j - cfg_.gate] >= 0)
                     deps.push_back(w.last_bwd[j - cfg_.gate]);  // schedule.cpp:293-296
+                // proposed policy: micro-batch j takes the stash slots of j - ring,
+                // free once that micro-batch's whole backward (wgrads included) ran
+                if (l == w.layers.front().layer && ring_ < m && j - ring_ >= 0) deps.push_back(bjoin[j - ring_]);
                 if (li.kind == 1) {
                     // implicit-GEMM conv over the padded NHWC input of this micro-batch
                     ConvShape cs;
@@ -674,7 +860,7 @@ void Session::build_ops() {
                     if (li.dense_conv) {  // dense layer over all positions with the expanded weight
                         const int P = li.Ho() * li.Wo(), Q = li.H * li.W;
                         d = GemmDesc{};
-                        d.a = Operand{act_buf(w.gpu, l - 1) + off * img_elems(l - 1), rows, Q * li.in_units,
+                        d.a = Operand{act_buf(w.gpu, l - 1) + aoff(l - 1, j) * img_elems(l - 1), rows, Q * li.in_units,
                                       img_elems(l - 1), false};
                         d.b = Operand{wl.Wx, P * wl.u, Q * li.in_units, wl.ldwx, false};
                         d.M = rows;
@@ -682,8 +868,8 @@ void Session::build_ops() {
                         d.K = Q * li.in_units;
                     } else if (li.generic) {  // per-step im2col rows of the padded input, then a dense GEMM
                         const ActLayout& a = lay_[l - 1];
-                        const float* x = act_buf(w.gpu, l - 1) + off * img_elems(l - 1);
-                        float* cols = wl.cols + off * li.Ho() * li.Wo() * wl.ldc;
+                        const float* x = act_buf(w.gpu, l - 1) + aoff(l - 1, j) * img_elems(l - 1);
+                        float* cols = wl.cols + so * li.Ho() * li.Wo() * wl.ldc;
                         const int hp = a.hp, wp = a.wp, C = li.in_units, k = li.ksz, Ho = li.Ho(), Wo = li.Wo();
                         const long long ldx = a.ld, ldc = wl.ldc;
                         cudaStream_t st = w.sf;
@@ -702,13 +888,13 @@ void Session::build_ops() {
                         const int kc = li.ksz * li.ksz * li.in_units;
                         const int prow = rows * li.Ho() * li.Wo();
                         d = GemmDesc{};
-                        d.a = Operand{act_buf(w.gpu, l - 1) + off * img_elems(l - 1), prow, kc, lay_[l - 1].ld, false};
+                        d.a = Operand{act_buf(w.gpu, l - 1) + aoff(l - 1, j) * img_elems(l - 1), prow, kc, lay_[l - 1].ld, false};
                         d.b = Operand{wl.W, wl.u, kc, wl.ldw, false};
                         d.M = prow;
                         d.N = wl.u;
                         d.K = kc;
                     } else {
-                        d = conv_fwd_desc(cs, act_buf(w.gpu, l - 1) + off * img_elems(l - 1), lay_[l - 1].ld, wl.W);
+                        d = conv_fwd_desc(cs, act_buf(w.gpu, l - 1) + aoff(l - 1, j) * img_elems(l - 1), lay_[l - 1].ld, wl.W);
                     }
                     d.epi = EpiParams{};
                     d.epi.mode = EPI_STORE;
@@ -716,7 +902,7 @@ void Session::build_ops() {
                     d.epi.relu = li.act == 1;
                     const long long pix = static_cast<long long>(li.Ho()) * li.Wo();
                     if (wl.U != nullptr) {  // pre-pool output, then pool / relayout
-                        d.epi.dst[d.epi.ndst++] = wl.U + off * pix * wl.ldu;
+                        d.epi.dst[d.epi.ndst++] = wl.U + so * pix * wl.ldu;
                         d.epi.ldd = wl.ldu;
                     } else {  // straight into every consumer GPU's padded NHWC input
                         const ActLayout& a = lay_[l];
@@ -728,7 +914,7 @@ void Session::build_ops() {
                         d.epi.r_pad = a.pad;
                         d.epi.ldd = a.ld;
                         d.epi.col0 = wl.lo;
-                        for (int ord : dest_gpus) d.epi.dst[d.epi.ndst++] = act_buf(ord, l) + off * img_elems(l);
+                        for (int ord : dest_gpus) d.epi.dst[d.epi.ndst++] = act_buf(ord, l) + so * img_elems(l);
                     }
                     if (li.dense_conv) {  // segmented columns (p, c): unpadded per-pixel rows of the destination
                         d.epi.remap = 0;
@@ -760,14 +946,14 @@ void Session::build_ops() {
                         d.epi.pl_on = !in_warp ? 3 : pool_smem ? 2 : 1;
                         d.epi.pl_wo = Wo1;
                         d.epi.pl_ho = Ho1;
-                        for (int ord : dest_gpus) d.epi.pl_dst[d.epi.pl_ndst++] = act_buf(ord, l) + off * img_elems(l);
+                        for (int ord : dest_gpus) d.epi.pl_dst[d.epi.pl_ndst++] = act_buf(ord, l) + so * img_elems(l);
                         d.epi.pl_kind = a.kind == 1 ? 1 : 0;
                         d.epi.pl_ld = a.ld;
                         d.epi.pl_hp = a.hp;
                         d.epi.pl_wp = a.wp;
                         d.epi.pl_pad = a.pad;
                         d.epi.pl_col0 = wl.lo;
-                        d.epi.pl_arg = wl.argmax + off * li.Hq() * li.Wq() * wl.u;
+                        d.epi.pl_arg = wl.argmax + so * li.Hq() * li.Wq() * wl.u;
                         d.epi.pl_uch = wl.u;
                     }
                     prepare(d, wl.p_fwd[j], w.gpu);
@@ -785,10 +971,10 @@ void Session::build_ops() {
                         ActLayout out = lay_[l];
                         out.col0 = wl.lo;
                         PoolDsts pd;
-                        for (int ord : dest_gpus) pd.ptr[pd.n++] = act_buf(ord, l) + off * img_elems(l);
-                        const float* U = wl.U + off * pix * wl.ldu;
+                        for (int ord : dest_gpus) pd.ptr[pd.n++] = act_buf(ord, l) + so * img_elems(l);
+                        const float* U = wl.U + so * pix * wl.ldu;
                         const long long ldu = wl.ldu;
-                        unsigned char* am = wl.argmax ? wl.argmax + off * li.Hq() * li.Wq() * wl.u : nullptr;
+                        unsigned char* am = wl.argmax ? wl.argmax + so * li.Hq() * li.Wq() * wl.u : nullptr;
                         const int Ho = li.Ho(), Wo = li.Wo(), u = wl.u, pool = li.pool;
                         cudaStream_t st = w.sf;
                         op = add_op(w.gpu, st, [=]() {
@@ -799,7 +985,7 @@ void Session::build_ops() {
                     produced.push_back(op);
                     continue;
                 }
-                d.a = Operand{act_buf(w.gpu, l - 1) + off * img_elems(l - 1), rows, fi, lay_[l - 1].ld, false};
+                d.a = Operand{act_buf(w.gpu, l - 1) + aoff(l - 1, j) * img_elems(l - 1), rows, fi, lay_[l - 1].ld, false};
                 d.b = Operand{wl.W, wl.u, fi, wl.ldw, false};
                 d.M = rows;
                 d.N = wl.u;
@@ -812,7 +998,7 @@ void Session::build_ops() {
                 d.epi.ldd = ld_of(net_.dims[l]);
                 for (int ord : dest_gpus) {
                     float* base = (l == L && softmax) ? q_buf(ord) : act_buf(ord, l);
-                    d.epi.dst[d.epi.ndst++] = base + off * d.epi.ldd;
+                    d.epi.dst[d.epi.ndst++] = base + so * d.epi.ldd;
                 }
                 prepare(d, wl.p_fwd[j], w.gpu);
                 const int op = add_op(w.gpu, w.sf, gemm_launch(&wl.p_fwd[j], &wl.d_fwd[j], w.sf), deps, nk(wl.p_fwd[j]),
@@ -830,8 +1016,8 @@ void Session::build_ops() {
                 const long long ld = img_elems(l);
                 for (int ord : consumers) {
                     if (ord == hub_gpu) continue;
-                    float* src = act_buf(hub_gpu, l) + off * ld;
-                    float* dst = act_buf(ord, l) + off * ld;
+                    float* src = act_buf(hub_gpu, l) + so * ld;
+                    float* dst = act_buf(ord, l) + so * ld;
                     const size_t bytes = sizeof(float) * rows * ld;
                     const int src_dev = hub_gpu, dst_dev = ord;
                     cudaStream_t s = hub.main;
@@ -853,11 +1039,11 @@ void Session::build_ops() {
                 WLayer& wl = w.at(L);
                 t.lo[t.n] = wl.lo;
                 t.hi[t.n] = wl.hi;
-                t.delta[t.n] = wl.delta + off * wl.ldd;
+                t.delta[t.n] = wl.delta + so * wl.ldd;
                 t.ld[t.n] = wl.ldd;
                 ++t.n;
             }
-            const float* in = (softmax ? g.q : act_buf(ord, L)) + off * ld_of(F);
+            const float* in = (softmax ? g.q : act_buf(ord, L)) + so * ld_of(F);
             const long long ldin = ld_of(F);
             const bool write = ord == main_gpu_;
             double* lr = write ? g.loss_row + off : nullptr;
@@ -880,7 +1066,8 @@ void Session::build_ops() {
     // ---------------- backward of micro-batch j (train_partitioned.cpp:422-630)
     auto backward = [&](int j) {
         const int rows = mb_sizes_[j];
-        const long long off = mb_off_[j];
+        const long long so = soff(j);  // stash slot rows of micro-batch j
+        const int first_op = static_cast<int>(ops_.size());
         for (int l = L; l >= 2; --l) {
             cur_layer_ = l;
             const std::vector<int> contrib = contributors(l);
@@ -915,17 +1102,17 @@ void Session::build_ops() {
                     cs.ksz = li.ksz;
                     cs.pad = li.pad;
                     cs.u = wl.u;
-                    d = conv_dgrad_desc(cs, wl.delta + off * wl.delta_img, wl.ldd, wl.W);
+                    d = conv_dgrad_desc(cs, wl.delta + so * wl.delta_img, wl.ldd, wl.W);
                     d.epi = EpiParams{};
                     d.epi.mode = EPI_MERGE;
                     d.epi.mg_pool = lb.pool;
                     d.epi.mg_hg = lb.Hq();
                     d.epi.mg_wg = lb.Wq();
-                    d.epi.mg_argmax = dl.argmax ? dl.argmax + off * hw * dl.u : nullptr;
+                    d.epi.mg_argmax = dl.argmax ? dl.argmax + so * hw * dl.u : nullptr;
                     d.epi.mg_uch = dl.u;
                     if (relu_below) {  // mask at the pooled pixel of the layer's output (consumer layout)
                         const ActLayout& a = lay_[l - 1];
-                        d.epi.mg_mask = act_buf(dw.gpu, l - 1) + off * img_elems(l - 1);
+                        d.epi.mg_mask = act_buf(dw.gpu, l - 1) + aoff(l - 1, j) * img_elems(l - 1);
                         d.epi.mg_mld = a.ld;
                         d.epi.mg_mhp = a.hp;
                         d.epi.mg_mwp = a.wp;
@@ -933,7 +1120,7 @@ void Session::build_ops() {
                         d.epi.mg_mcol0 = dl.lo;
                     }
                     const int q = lb.dq();
-                    d.epi.mg_d = dl.delta + off * dl.delta_img;
+                    d.epi.mg_d = dl.delta + so * dl.delta_img;
                     d.epi.mg_dld = dl.ldd;
                     d.epi.mg_dhp = lb.Ho() + 2 * q;
                     d.epi.mg_dwp = lb.Wo() + 2 * q;
@@ -970,14 +1157,14 @@ void Session::build_ops() {
                         const int Q = li.H * li.W;
                         d = GemmDesc{};
                         if (li.dense_conv) {
-                            d.a = Operand{wl.delta + off * wl.delta_img, rows, static_cast<int>(pix) * wl.u, wl.delta_img,
+                            d.a = Operand{wl.delta + so * wl.delta_img, rows, static_cast<int>(pix) * wl.u, wl.delta_img,
                                           false};
                             d.b = Operand{wl.Wx, static_cast<int>(pix) * wl.u, Q * li.in_units, wl.ldwx, true};
                             d.M = rows;
                             d.N = Q * li.in_units;
                             d.K = static_cast<int>(pix) * wl.u;
                         } else {
-                            d.a = Operand{wl.delta + off * wl.delta_img, static_cast<int>(rows * pix), wl.u, wl.ldd, false};
+                            d.a = Operand{wl.delta + so * wl.delta_img, static_cast<int>(rows * pix), wl.u, wl.ldd, false};
                             d.b = Operand{wl.W, wl.u, kc, wl.ldw, true};
                             d.M = static_cast<int>(rows * pix);
                             d.N = kc;
@@ -999,10 +1186,10 @@ void Session::build_ops() {
                         if (fused) {
                             Worker& dw = *workers_[dests[0]];
                             d.epi.mode = relu_below ? EPI_MASK : EPI_STORE;
-                            d.epi.dst[d.epi.ndst++] = d0.delta + off * d0.delta_img;
+                            d.epi.dst[d.epi.ndst++] = d0.delta + so * d0.delta_img;
                             d.epi.ldd = d0.delta_img;
                             if (relu_below) {
-                                d.epi.mask = act_buf(dw.gpu, l - 1) + off * img_elems(l - 1);
+                                d.epi.mask = act_buf(dw.gpu, l - 1) + aoff(l - 1, j) * img_elems(l - 1);
                                 d.epi.ldm = img_elems(l - 1);
                             }
                             d.epi.db_partial = d0.partial + static_cast<long long>(j) * conv_merge_blocks() * Q * d0.u;
@@ -1021,10 +1208,10 @@ void Session::build_ops() {
                             break;
                         }
                         if (direct) {
-                            d.epi.dst[d.epi.ndst++] = d0.slots[k] + off * Q * d0.slot_ld;
+                            d.epi.dst[d.epi.ndst++] = d0.slots[k] + so * Q * d0.slot_ld;
                             d.epi.ldd = static_cast<long long>(Q) * d0.slot_ld;
                         } else {
-                            d.epi.dst[d.epi.ndst++] = wl.dcols + off * drows * wl.ldk;
+                            d.epi.dst[d.epi.ndst++] = wl.dcols + so * drows * wl.ldk;
                             d.epi.ldd = wl.ldk;
                         }
                         prepare(d, wl.p_dgrad[j], w.gpu);
@@ -1033,13 +1220,13 @@ void Session::build_ops() {
                         int op = add_op(w.gpu, w.sb, gemm_launch(&wl.p_dgrad[j], &wl.d_dgrad[j], w.sb), wl.delta_ready[j],
                                         nk(wl.p_dgrad[j]), OP_DGRAD_GEMM, fl);
                         wl.dgrad_op[j] = op;
-                        const float* dc = wl.dcols + off * drows * wl.ldk;
+                        const float* dc = wl.dcols + so * drows * wl.ldk;
                         const bool dcv = li.dense_conv;
                         const long long ldk = dcv ? li.in_units : wl.ldk;  // dense conv: pixel-major [img*Q][C]
                         const int H = li.H, W = li.W, C = li.in_units, ks = dcv ? 1 : li.ksz, pd = dcv ? 0 : li.pad;
                         for (int di : direct ? std::vector<int>{} : dests) {
                             WLayer& dl = workers_[di]->at(l - 1);
-                            float* dst = dl.slots[k] + off * H * W * dl.slot_ld;
+                            float* dst = dl.slots[k] + so * H * W * dl.slot_ld;
                             const long long ldo = dl.slot_ld;
                             const int c0 = dl.lo, nc = dl.u;
                             cudaStream_t st = w.sb;
@@ -1060,11 +1247,11 @@ void Session::build_ops() {
                         cs.ksz = li.ksz;
                         cs.pad = li.pad;
                         cs.u = wl.u;
-                        d = conv_dgrad_desc(cs, wl.delta + off * wl.delta_img, wl.ldd, wl.W);
+                        d = conv_dgrad_desc(cs, wl.delta + so * wl.delta_img, wl.ldd, wl.W);
                         fl = 2.0 * rows * li.H * li.W * li.in_units * li.ksz * li.ksz * wl.u;
                         rows_per_img = static_cast<long long>(li.H) * li.W;
                     } else {
-                        d.a = Operand{wl.delta + off * wl.ldd, rows, wl.u, wl.ldd, false};
+                        d.a = Operand{wl.delta + so * wl.ldd, rows, wl.u, wl.ldd, false};
                         d.b = Operand{wl.W, wl.u, fi, wl.ldw, true};
                         d.M = rows;
                         d.N = fi;
@@ -1081,7 +1268,7 @@ void Session::build_ops() {
                         d.epi.seg_lo[sg] = dl.lo * scale;
                         d.epi.seg_hi[sg] = dl.hi * scale;
                         d.epi.seg_ld[sg] = dl.slot_ld;
-                        d.epi.seg_dst[sg] = dl.slots[k] + off * rows_per_img * dl.slot_ld;
+                        d.epi.seg_dst[sg] = dl.slots[k] + so * rows_per_img * dl.slot_ld;
                     }
                     prepare(d, wl.p_dgrad[j], w.gpu);
                     const int op = add_op(w.gpu, w.sb, gemm_launch(&wl.p_dgrad[j], &wl.d_dgrad[j], w.sb),
@@ -1096,7 +1283,7 @@ void Session::build_ops() {
                     WLayer& dl = dw.at(l - 1);
                     ConvMerge cm;
                     const long long rows_per_img = li.kind == 1 ? hw : 1;
-                    for (float* sp : dl.slots) cm.slots.slot[cm.slots.n++] = sp + off * rows_per_img * dl.slot_ld;
+                    for (float* sp : dl.slots) cm.slots.slot[cm.slots.n++] = sp + so * rows_per_img * dl.slot_ld;
                     // a dense consumer's CHW-flatten slot over a 1 x 1 pooled grid is
                     // the pixel-major layout (vectorised merge kernel)
                     cm.slot_kind = (li.kind == 1 || lb.Hq() * lb.Wq() == 1) ? 0 : 1;
@@ -1106,22 +1293,22 @@ void Session::build_ops() {
                     cm.Wo = lb.Wo();
                     cm.uch = dl.u;
                     cm.pool = lb.pool;
-                    cm.argmax = dl.argmax ? dl.argmax + off * hw * dl.u : nullptr;
+                    cm.argmax = dl.argmax ? dl.argmax + so * hw * dl.u : nullptr;
                     if (relu_below) {
                         if (dl.U != nullptr && dl.u_written) {
                             cm.mask_kind = 1;
-                            cm.U = dl.U + off * lb.Ho() * lb.Wo() * dl.ldu;
+                            cm.U = dl.U + so * lb.Ho() * lb.Wo() * dl.ldu;
                             cm.ldu = dl.ldu;
                         } else {
                             // pooled layers whose pre-pool rows were never stored (pool fused
                             // across warp pairs) mask at the pooled pixel
                             cm.mask_kind = lb.pool == 2 ? 3 : 2;
-                            cm.act = act_buf(dw.gpu, l - 1) + off * img_elems(l - 1);
+                            cm.act = act_buf(dw.gpu, l - 1) + aoff(l - 1, j) * img_elems(l - 1);
                             cm.act_layout = lay_[l - 1];
                             cm.act_layout.col0 = dl.lo;
                         }
                     }
-                    cm.d_pad = dl.delta + off * dl.delta_img;
+                    cm.d_pad = dl.delta + so * dl.delta_img;
                     cm.q = lb.dq();
                     cm.ldd = dl.ldd;
                     cudaStream_t st = dw.sb;
@@ -1137,7 +1324,7 @@ void Session::build_ops() {
                 Worker& w = *workers_[contrib[k]];
                 WLayer& wl = w.at(l);
                 GemmDesc& d = wl.d_dgrad[j];
-                d.a = Operand{wl.delta + off * wl.ldd, rows, wl.u, wl.ldd, false};
+                d.a = Operand{wl.delta + so * wl.ldd, rows, wl.u, wl.ldd, false};
                 d.b = Operand{wl.W, wl.u, fi, wl.ldw, true};
                 d.M = rows;
                 d.N = fi;
@@ -1152,13 +1339,13 @@ void Session::build_ops() {
                     d.epi.seg_hi[s] = dl.hi;
                     d.epi.seg_ld[s] = dl.ldd;
                     if (single) {
-                        d.epi.seg_dst[s] = dl.delta + off * dl.ldd;
+                        d.epi.seg_dst[s] = dl.delta + so * dl.ldd;
                         if (relu_below) {
-                            d.epi.seg_mask[s] = act_buf(dw.gpu, l - 1) + off * ld_of(fi);
+                            d.epi.seg_mask[s] = act_buf(dw.gpu, l - 1) + so * ld_of(fi);
                             d.epi.seg_mask_ld[s] = ld_of(fi);
                         }
                     } else {
-                        d.epi.seg_dst[s] = dl.slots[k] + off * dl.ldd;
+                        d.epi.seg_dst[s] = dl.slots[k] + so * dl.ldd;
                     }
                 }
                 prepare(d, wl.p_dgrad[j], w.gpu);
@@ -1177,10 +1364,10 @@ void Session::build_ops() {
                     continue;
                 }
                 ReduceSlots rs;
-                for (float* sp : dl.slots) rs.slot[rs.n++] = sp + off * dl.ldd;
-                const float* mask = relu_below ? act_buf(dw.gpu, l - 1) + off * ld_of(fi) + dl.lo : nullptr;
+                for (float* sp : dl.slots) rs.slot[rs.n++] = sp + so * dl.ldd;
+                const float* mask = relu_below ? act_buf(dw.gpu, l - 1) + so * ld_of(fi) + dl.lo : nullptr;
                 const long long ldm = ld_of(fi);
-                float* out = dl.delta + off * dl.ldd;
+                float* out = dl.delta + so * dl.ldd;
                 const long long ldd = dl.ldd;
                 const int u = dl.u;
                 cudaStream_t s = dw.sb;
@@ -1195,6 +1382,7 @@ void Session::build_ops() {
         for (int wi : layer_workers_[1])
             for (int op : workers_[wi]->at(1).delta_ready[j])
                 workers_[wi]->last_bwd[j] = std::max(workers_[wi]->last_bwd[j], op);
+        if (per_mb_wgrad_) per_mb_wgrads(j, first_op);
     };
 
     // interleave creation so every dependency already exists: F(1..gate), then
@@ -1220,6 +1408,53 @@ void Session::build_ops() {
     }
     const float inv_b = 1.f / static_cast<float>(cfg_.batch);
     static const bool no_side = getenv("PPB_NO_SIDE_JOB") != nullptr;
+    // proposed policy: the layer's update = one reduction over the m x
+    // acc_slices partial slices (micro-batch order, then split order) applying
+    // the real epilogue (SGD on W with the bias update in the same launch, or
+    // dWx for a dense-conv layer, then its fold + SGD)
+    auto reduce_update = [&](Worker& w, WLayer& wl, int join) {
+        Gpu& g = gpu_of(w.gpu);
+        const LayerInfo& li = net_.info[wl.layer - 1];
+        std::vector<int> deps = wl.wg_op;
+        for (int j = 0; j < m; ++j) {
+            deps.insert(deps.end(), wl.delta_ready[j].begin(), wl.delta_ready[j].end());
+            if (wl.dgrad_op[j] >= 0) deps.push_back(wl.dgrad_op[j]);  // dgrads read W
+        }
+        if (join >= 0) deps.push_back(join);
+        const bool fm = bias_from_merge(wl);
+        const int chunks = fm ? cfg_.m * conv_merge_blocks() * wl.db_q : cfg_.m * wl.cc_mb;
+        wl.p_red = wl.p_wg[0];
+        wl.p_red.sk.ws = wl.acc_ws;
+        wl.p_red.sk.splits = m * wl.acc_slices;
+        wl.p_red.sk.partial = 0;
+        wl.p_red.sk.deferred = 0;
+        wl.p_red.sk.fixup = 0;
+        wl.p_red.epi = wl.d_wg[0].epi;
+        wl.p_red.epi.M = wl.p_red.M;
+        wl.p_red.epi.N = wl.p_red.N;
+        cudaStream_t s = w.su;
+        const double* alpha = &g.st->alpha;
+        if (!li.dense_conv) {
+            wl.p_red.sk.bpart = wl.partial;
+            wl.p_red.sk.bias = wl.bias;
+            wl.p_red.sk.bchunks = chunks;
+            wl.p_red.sk.bu = wl.u;
+            const TcGemmPlan* pr = &wl.p_red;
+            add_op(w.gpu, s, [pr, s]() { return tc_gemm_launch_reduce(*pr, s); }, deps, 1, OP_BIAS);
+            return;
+        }
+        const TcGemmPlan* pr = &wl.p_red;
+        const int rop = add_op(w.gpu, s, [pr, s]() { return tc_gemm_launch_reduce(*pr, s); }, deps, 1, OP_BIAS);
+        const DenseConvGeom dg = wl.dcg;
+        const float* dWx = wl.dWx;
+        float* Wp = wl.W;
+        float* Wx = wl.Wx;
+        int* flag = &g.st->diverge_flag;
+        const float* bp = wl.partial;
+        float* bb = wl.bias;
+        add_op(w.gpu, s, [=]() { return launch_dense_conv_fold_sgd(dg, dWx, Wp, Wx, alpha, inv_b, flag, s, bp, chunks, bb); },
+               {rop}, 1, OP_BIAS);
+    };
     for (auto& wp : workers_) {
         Worker& w = *wp;
         Gpu& g = gpu_of(w.gpu);
@@ -1262,80 +1497,14 @@ void Session::build_ops() {
             WLayer& wl = *wit;
             const int l = wl.layer;
             cur_layer_ = l;
-            const int fi = net_.dims[l - 1];
             const LayerInfo& li = net_.info[l - 1];
             GemmDesc& d = wl.d_wgrad;
             double wfl;
-            long long bias_rows = cfg_.batch;
-            if (li.kind == 1) {
-                ConvShape cs;
-                cs.N = cfg_.batch;
-                cs.H = li.H;
-                cs.W = li.W;
-                cs.C = li.in_units;
-                cs.ksz = li.ksz;
-                cs.pad = li.pad;
-                cs.u = wl.u;
-                if (li.dense_conv) {  // dWx = delta^T . a over the batch (K = images); folded below
-                    const int P = li.Ho() * li.Wo(), Q = li.H * li.W;
-                    d = GemmDesc{};
-                    d.a = Operand{wl.delta, cfg_.batch, P * wl.u, wl.delta_img, true};
-                    d.b = Operand{act_buf(w.gpu, l - 1), cfg_.batch, Q * li.in_units, img_elems(l - 1), true};
-                    d.M = P * wl.u;
-                    d.N = Q * li.in_units;
-                    d.K = cfg_.batch;
-                } else if (li.dense_delta) {  // dense wgrad: K = output pixels, unpadded error signal x im2col rows
-                    const int kc = li.ksz * li.ksz * li.in_units;
-                    const int pix = cfg_.batch * li.Ho() * li.Wo();
-                    const float* colsp = li.generic ? wl.cols : act_buf(w.gpu, l - 1);
-                    const long long ldc = li.generic ? wl.ldc : lay_[l - 1].ld;
-                    d = GemmDesc{};
-                    d.a = Operand{wl.delta, pix, wl.u, wl.ldd, true};
-                    d.b = Operand{colsp, pix, kc, ldc, true};
-                    d.M = wl.u;
-                    d.N = kc;
-                    d.K = pix;
-                    if (wl.u < 128 && kc > wl.u) {  // dW^T: the wide side fills the 128-row tiles
-                        std::swap(d.a, d.b);
-                        std::swap(d.M, d.N);
-                    }
-                } else if (li.im2col) {  // B = im2col rows (pixel-major, MN = k*k*C)
-                    d = conv_wgrad_desc(cs, wl.delta, wl.ldd, act_buf(w.gpu, l - 1), lay_[l - 1].ld, false);
-                    const int kc = li.ksz * li.ksz * li.in_units;
-                    d.b = Operand{act_buf(w.gpu, l - 1), cfg_.batch * li.Ho() * li.Wo(), kc, lay_[l - 1].ld, true};
-                    d.N = kc;
-                } else {
-                    d = conv_wgrad_desc(cs, wl.delta, wl.ldd, act_buf(w.gpu, l - 1), lay_[l - 1].ld, wl.u < 128);
-                }
-                wfl = li.dense_conv ? 2.0 * cfg_.batch * li.Ho() * li.Wo() * wl.u * li.H * li.W * li.in_units  // executed
-                                    : 2.0 * cfg_.batch * li.Ho() * li.Wo() * wl.u * li.ksz * li.ksz * li.in_units;
-                bias_rows = static_cast<long long>(cfg_.batch) * (wl.delta_img / wl.ldd);  // zero borders add nothing
-            } else {
-                d.a = Operand{wl.delta, cfg_.batch, wl.u, wl.ldd, true};
-                d.b = Operand{act_buf(w.gpu, l - 1), cfg_.batch, fi, lay_[l - 1].ld, true};
-                d.M = wl.u;
-                d.N = fi;
-                d.K = cfg_.batch;
-                if (wl.u < 128 && fi > wl.u) {  // dW^T: the wide side fills the 128-row tiles
-                    std::swap(d.a, d.b);
-                    std::swap(d.M, d.N);
-                }
-                wfl = 2.0 * wl.u * fi * static_cast<double>(cfg_.batch);
-            }
-            const bool wt = d.M != wl.u;
-            d.epi = EpiParams{};
-            d.epi.mode = EPI_SGD;
-            d.epi.W = wl.W;
-            d.epi.ldw = wl.ldw;
-            d.epi.sgd_t = wt ? 1 : 0;
-            d.epi.alpha = &g.st->alpha;
-            d.epi.inv_b = inv_b;
-            d.epi.flag = &g.st->diverge_flag;
-            if (li.dense_conv) {  // plain dWx; the fold kernel applies SGD to W and re-expands Wx
-                d.epi = EpiParams{};
-                d.epi.mode = EPI_STORE;
-                d.epi.dst[d.epi.ndst++] = wl.dWx;
-                d.epi.ldd = wl.ldwx;
+            long long bias_rows;
+            wgrad_desc(w, wl, -1, d, &wfl, &bias_rows);
+            if (per_mb_wgrad_) {  // proposed policy: one reduction (+ SGD / dWx) over the micro-batch slices
+                reduce_update(w, wl, bwd_join);
+                continue;
             }
             prepare(d, wl.p_wgrad, w.gpu);
             std::vector<int> deps;

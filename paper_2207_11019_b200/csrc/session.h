@@ -92,6 +92,10 @@ struct SessionConfig {
     int multiclass = 0;
     int use_graph = 1;
     int gate = 2;
+    // 0 stash_all (the reference executor: all micro-batches resident, wgrad
+    // over all b rows); 1 proposed (ring of min(m, gate) micro-batch slots,
+    // weight gradients accumulated per micro-batch)
+    int stash = 0;
 };
 
 class Session {
@@ -108,6 +112,8 @@ class Session {
     void get_net(double* W, double* b);
     size_t read_tensor(int kind, int layer, int device, double* out, size_t cap);
     int kernels_per_step() const { return kernels_per_step_; }
+    size_t device_bytes() const;
+    size_t stash_bytes() const;
     // device time of `iterations` steps on the launching stream (CUDA events)
     float time_steps(int iterations);
     // one eager iteration per call with per-op CUDA events; accumulates the
@@ -149,6 +155,14 @@ class Session {
     long long img_elems(int layer) const;    // floats per sample of act layer `layer` (consumer layout)
     float* q_buf(int ordinal);               // gathered pre-activation of the softmax head
     long long ld_of(int cols) const { return (cols + 3) / 4 * 4; }
+    // row offset of micro-batch j in a stash buffer (activation l >= 1, error
+    // signal, pre-pool output, ...): its slot in the ring under the proposed
+    // memory policy, else its batch offset.  aoff: activation `l` (l = 0 is the
+    // batch itself, always resident).
+    long long soff(int j) const {
+        return ring_ == cfg_.m ? mb_off_[j] : static_cast<long long>(j % ring_) * mb_sizes_[0];
+    }
+    long long aoff(int l, int j) const { return l == 0 ? mb_off_[j] : soff(j); }
     void check(cudaError_t e, const char* what);
     void validate_labels(const int* labels) const;
 
@@ -157,6 +171,9 @@ class Session {
     SessionConfig cfg_;
     std::vector<int> device_map_;
     std::vector<int> mb_sizes_, mb_off_;
+    int ring_ = 1;              // resident micro-batch slots (m under stash_all)
+    long long ring_rows_ = 0;   // rows of every stash buffer (b, or ring_ x largest micro-batch)
+    bool per_mb_wgrad_ = false; // weight gradients accumulated per micro-batch (proposed)
     std::vector<std::unique_ptr<Gpu>> gpus_;
     std::vector<std::unique_ptr<Worker>> workers_;
     std::vector<std::vector<int>> layer_workers_;  // layer (1-based) -> worker indices (rank order)

@@ -90,12 +90,12 @@ def _oracle(workload, alpha0, steps, tf32_mode=None):
     return _oracle_cache[key]
 
 
-def _gpu(workload, n, alpha0, steps, m=1):
+def _gpu(workload, n, alpha0, steps, m=1, memory="stash_all"):
     """The bench's session (bench.run_ours) with n plan devices on cuda:0."""
     net, X, y = bench.synthetic_batch(workload, seed=1)
     ctx = api.Context([0] * n)
     plan = api.build_plan(net, n, 1)
-    opts = PartitionedTrainOptions(multiclass_accuracy=True, use_graph=True, pipeline_gate=2)
+    opts = PartitionedTrainOptions(multiclass_accuracy=True, use_graph=True, pipeline_gate=2, memory_mode=memory)
     s = api.Session(ctx, net, X.shape[0], plan, m, UpdateMode.async_per_module,
                     TrainConfig(alpha0=alpha0, decay=1e-2, iterations=1), opts)
     s.load_batch(X, y)
@@ -119,8 +119,8 @@ def _fmt(u):
     return [("%.1e" % a, "%.1e" % c) for a, c in u]
 
 
-def _check(workload, n, alpha0, steps=STEPS, m=1):
-    net, Wg, bg, lh = _gpu(workload, n, alpha0, steps, m)
+def _check(workload, n, alpha0, steps=STEPS, m=1, memory="stash_all"):
+    net, Wg, bg, lh = _gpu(workload, n, alpha0, steps, m, memory)
     Wr, br, lr = _oracle(workload, alpha0, steps)
     Wm, bm, _ = _oracle(workload, alpha0, steps, "trunc")
     W0, b0 = net.pack()
@@ -128,7 +128,7 @@ def _check(workload, n, alpha0, steps=STEPS, m=1):
     W32, b32 = W0.astype(np.float32).astype(np.float64), b0.astype(np.float32).astype(np.float64)
     rep = {"loss": [float(abs(a - r) / abs(r)) for a, r in zip(lh, lr)], "net_distance": net_distance(Wg, bg, Wr, br),
            "vs_f64": _upd(net, Wg, bg, Wr, br, W32, b32), "model_vs_f64": _upd(net, Wm, bm, Wr, br, W32, b32)}
-    print(f"\n{workload} n={n} alpha0={alpha0} m={m}: loss rel {['%.1e' % x for x in rep['loss']]}, "
+    print(f"\n{workload} n={n} alpha0={alpha0} m={m} {memory}: loss rel {['%.1e' % x for x in rep['loss']]}, "
           f"net_distance {rep['net_distance']:.2e}\n  per-layer update rel (W, b) vs fp64 {_fmt(rep['vs_f64'])}"
           f"\n  TF32 model vs fp64 {_fmt(rep['model_vs_f64'])}")
     assert len(lh) == steps
@@ -169,6 +169,14 @@ def test_wide_mlp_b4096_bench_config(n):
 def test_vgg16_b512_microbatched():
     """m = 4 micro-batches (the F/B-overlap schedule) reaches the same weights as m = 1."""
     _check("vgg16", 2, 1e-2, m=4)
+
+
+@pytest.mark.parametrize("workload,n,m", [("vgg16", 1, 4), ("vgg16", 2, 2), ("lenet5", 2, 4), ("wide_mlp", 2, 2)])
+def test_proposed_memory_bench_configs(workload, n, m):
+    """The proposed stash policy (per-micro-batch weight-gradient partials,
+    min(m, gate) resident micro-batches) at the benchmarked shapes against
+    the fp64 oracle, same tolerances as the stash_all runs."""
+    _check(workload, n, 1e-2, steps=1 if workload == "wide_mlp" else STEPS, m=m, memory="proposed")
 
 
 # ---------------------------------------------------------------- (2) per layer, teacher-forced

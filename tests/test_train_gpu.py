@@ -240,3 +240,83 @@ def test_mlp_config_one_step_and_50_step_curve(precision, alpha0, tol):
             d = net_distance(Wg, bg, Wo, bo)
             print(f"one-step net_distance {d:.2e}")
             assert d <= 1e-4, d
+
+
+# ---------------------------------------------------------------- proposed memory policy
+# (paper §III: backward of micro-batch j overlaps forward of j+1 and frees
+# micro-batch j's activations; simulate.hpp:14-16 MemoryMode::proposed).  The
+# weight gradient of every micro-batch is accumulated as soon as its backward
+# reaches the layer (raw partial sums per micro-batch, one reduction + SGD
+# after the last), and the activation / error-signal buffers hold only
+# min(m, gate) micro-batch slots.  Same arithmetic as the reference up to the
+# association of the micro-batch sum (fp32 partials summed in micro-batch
+# order, train_partitioned.cpp:505-511), so the tolerances are the ones above.
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("gate", [1, 2, 3])
+def test_proposed_memory_verify_instances(mode, gate):
+    """The reference's run_verification instances with m >= 2 (ragged
+    micro-batches, Z <= L modules, merged boundaries, replicated layers)
+    under the proposed policy match the reference within the TF32 bound."""
+    worst, ran = 0.0, 0
+    for e in golden()["verify_instances"]:
+        exp = e[f"partitioned_mode{mode}"]
+        if "error" in exp or e["m"] < 2:
+            continue
+        r = _run_instance(e, mode, "tf32", pipeline_gate=gate, memory_mode="proposed")
+        Wg, bg = r.net.pack()
+        d = net_distance(Wg, bg, np.array(exp["W"]), np.array(exp["b"]))
+        worst = max(worst, d)
+        ran += 1
+        assert d <= TOL["tf32"], (e["seed"], d)
+        for got, ref in zip(r.loss_history, exp["loss"]):
+            assert abs(got - ref) <= TOL["tf32"] * max(1.0, abs(ref)), (e["seed"], got, ref)
+    assert ran >= 10
+    print(f"proposed memory, gate {gate}, mode {mode}: {ran} instances, worst net_distance {worst:.3e}")
+
+
+@pytest.mark.parametrize("m,gate", [(2, 1), (4, 2), (3, 2), (8, 2)])
+def test_proposed_memory_mlp_config(m, gate):
+    """MLP 784-512-512-10, b=64, the n=2 plan and a staged Z=2 plan: proposed
+    policy vs the oracle at m micro-batches (one step: net_distance <= 1e-4;
+    5 steps of the loss curve within 1e-3), and the stash shrinks to
+    min(m, gate) / m of the stash_all buffers (up to the first micro-batch
+    being the larger one when b % m != 0)."""
+    g, O, W, b, X, y = _mlp()
+    net = TinyNet.unpack(g["dims"], g["acts"], W, b)
+    dims = g["dims"]
+    for plan in (api.build_plan(dims, 2, 1), api.build_plan(dims, 2, 2)):
+        n_dev = max(d for sm in plan.submodules for d in sm.devices)
+        for iters, tol in ((1, None), (5, 1e-3)):
+            cfg = TrainConfig(alpha0=1e-2, decay=0.01, iterations=iters)
+            r = api.train_partitioned(net, Batch(X, y), cfg, plan, m, UpdateMode.async_per_module,
+                                      PartitionedTrainOptions(pipeline_gate=gate, memory_mode="proposed"),
+                                      device_map=[0] * n_dev)
+            Wo, bo, lh, _ = O.train_partitioned(dims, g["acts"], W, b, X, y, plan.to_flat(), m, 2, 1e-2, 0.01, 1, iters)
+            if tol is None:
+                Wg, bg = r.net.pack()
+                assert net_distance(Wg, bg, Wo, bo) <= 1e-4
+            else:
+                rel = [abs(x - c) / abs(c) for x, c in zip(r.loss_history, lh)]
+                assert max(rel) <= tol, rel
+    ctx = api.Context([0, 0])
+    plan = api.build_plan(dims, 2, 1)
+    sizes = {}
+    for mm in ("stash_all", "proposed"):
+        s = api.Session(ctx, net, 64, plan, m, UpdateMode.async_per_module, TrainConfig(iterations=1),
+                        PartitionedTrainOptions(pipeline_gate=gate, memory_mode=mm))
+        sizes[mm] = s.memory()
+        del s
+    ring = min(m, gate)
+    mb0 = -(-64 // m)
+    assert sizes["proposed"][1] == pytest.approx(sizes["stash_all"][1] * ring * mb0 / 64, rel=0.02), sizes
+
+
+def test_proposed_memory_rejects_fp32_mode():
+    """The proposed policy runs on the tensor-core path (partial-sum GEMMs)."""
+    g, O, W, b, X, y = _mlp()
+    net = TinyNet.unpack(g["dims"], g["acts"], W, b)
+    with pytest.raises(ValueError, match="proposed memory mode"):
+        api.train_partitioned(net, Batch(X, y), TrainConfig(iterations=1), api.build_plan(g["dims"], 2, 1), 2,
+                              UpdateMode.sync_barrier, PartitionedTrainOptions(precision="fp32", memory_mode="proposed"),
+                              device_map=[0, 0])
