@@ -283,6 +283,14 @@ int ppb_session_profile(ppb_session* s, int iterations, double* ms, int* count, 
 int ppb_session_profile_ops(ppb_session* s, int* kind, int* layer, int* info, double* ms, double* flops, int cap,
                             int* count);
 
+/* Step structure, same op order as ppb_session_profile_ops: the op's
+ * micro-batch (0-based; -1 for once-per-step ops), the plan device of the
+ * worker that runs it (1-based; 0 for a GPU's main stream: loss head,
+ * hub copies, finalize) and its stream role (0 forward, 1 input gradient /
+ * merge, 2 weight gradient / update, 3 main).  The order is the enqueue order
+ * of the pipelined schedule (schedule.cpp:254-329). */
+int ppb_session_op_meta(ppb_session* s, int* microbatch, int* device, int* role, int cap, int* count);
+
 /* Timeline of the last ppb_session_profile iteration (same op order as
  * ppb_session_profile_ops): start of each op in ms from the first op on its
  * device, and a per-session stream index (eager launch order, not a graph). */

@@ -585,6 +585,17 @@ class Session:
                  "ms": float(ms[i]), "tflops": float(fl[i] / ms[i] / 1e9) if ms[i] > 0 else 0.0}
                 for i in range(n.value)]
 
+    def op_meta(self) -> list:
+        """(micro-batch, plan device, stream role) per op, profile_ops() order
+        (the enqueue order of the pipelined schedule)."""
+        n = C.c_int(0)
+        L = _lib.lib()
+        check(L.ppb_session_op_meta(self._h, None, None, None, 0, C.byref(n)))
+        mb, dev, role = (np.zeros(max(n.value, 1), np.int32) for _ in range(3))
+        check(L.ppb_session_op_meta(self._h, _ip(mb), _ip(dev), _ip(role), n.value, C.byref(n)))
+        roles = ("forward", "backward", "wgrad", "main")
+        return [{"mb": int(mb[i]), "device": int(dev[i]), "role": roles[role[i]]} for i in range(n.value)]
+
     def profile_timeline(self) -> list:
         """profile_ops() records with the op's start (ms from the first op) and stream index."""
         ops = self.profile_ops()

@@ -224,6 +224,10 @@ extern "C" int ppb_session_profile_starts(ppb_session* s, double* start_ms, int*
     return ppb_guard([&] { *count = s->s->profile_starts(start_ms, stream_id, cap); });
 }
 
+extern "C" int ppb_session_op_meta(ppb_session* s, int* microbatch, int* device, int* role, int cap, int* count) {
+    return ppb_guard([&] { *count = s->s->op_meta(microbatch, device, role, cap); });
+}
+
 extern "C" int ppb_session_profile_ops(ppb_session* s, int* kind, int* layer, int* info, double* ms, double* flops,
                                        int cap, int* count) {
     return ppb_guard([&] { *count = s->s->profile_ops(kind, layer, info, ms, flops, cap); });

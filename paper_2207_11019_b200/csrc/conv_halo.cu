@@ -223,6 +223,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                                 const uint64_t bd = B_MN ? umma_desc<kLayoutSW128Base32>(b_addr + kk * 1024, 4096, 512)
                                                          : umma_desc<kLayoutSW128>(b_addr + kk * 32, 16, 1024);
                                 const uint32_t accum = (cb != 0 || tap != 0 || kk != 0) ? 1u : 0u;
+                                if (hg.dbg & 8) continue;  // timing probe: no MMAs
                                 if (CG == 2) mma_tf32_pair(d_tmem, ad, bd, idesc, accum);
                                 else mma_tf32(d_tmem, ad, bd, idesc, accum);
                             }

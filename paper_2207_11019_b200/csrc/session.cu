@@ -606,6 +606,7 @@ int Session::add_op(int gpu, cudaStream_t s, std::function<cudaError_t()> f, std
     op.launch = std::move(f);
     op.deps = std::move(deps);
     op.kernels = kernels;
+    op.mb = cur_mb_;
     check(cudaSetDevice(gpu), "cudaSetDevice");
     check(cudaEventCreateWithFlags(&op.ev, cudaEventDisableTiming), "event");
     ops_.push_back(std::move(op));
@@ -806,6 +807,7 @@ void Session::build_ops() {
 
     // ---------------- forward of micro-batch j (train_partitioned.cpp:245-419)
     auto forward = [&](int j) {
+        cur_mb_ = j;
         const int rows = mb_sizes_[j];
         const long long off = mb_off_[j];  // batch rows (X, labels, per-sample loss)
         const long long so = soff(j);      // stash slot rows (activations l >= 1, error signals, ...)
@@ -1065,6 +1067,7 @@ void Session::build_ops() {
 
     // ---------------- backward of micro-batch j (train_partitioned.cpp:422-630)
     auto backward = [&](int j) {
+        cur_mb_ = j;
         const int rows = mb_sizes_[j];
         const long long so = soff(j);  // stash slot rows of micro-batch j
         const int first_op = static_cast<int>(ops_.size());
@@ -1394,6 +1397,7 @@ void Session::build_ops() {
     }
 
     // ---------------- updates (train_partitioned.cpp:632-651)
+    cur_mb_ = -1;
     int bwd_join = -1;
     if (cfg_.mode == 1) {
         std::vector<int> all;
@@ -1742,6 +1746,27 @@ int Session::profile_ops(int* kind, int* layer, int* info, double* ms, double* f
             info[k] = ops_[i].info;
             ms[k] = last_op_ms_[i];
             flops[k] = ops_[i].flops;
+        }
+        ++k;
+    }
+    return k;
+}
+
+int Session::op_meta(int* mb, int* device, int* role, int cap) {
+    std::map<cudaStream_t, std::pair<int, int>> who;  // stream -> (plan device, role)
+    for (const auto& w : workers_) {
+        who[w->sf] = {w->device, 0};
+        who[w->sb] = {w->device, 1};
+        who[w->su] = {w->device, 2};
+    }
+    int k = 0;
+    for (int i = 0; i < static_cast<int>(ops_.size()); ++i) {
+        if (!ops_[i].launch) continue;
+        if (k < cap) {
+            auto it = who.find(ops_[i].stream);
+            mb[k] = ops_[i].mb;
+            device[k] = it == who.end() ? 0 : it->second.first;
+            role[k] = it == who.end() ? 3 : it->second.second;
         }
         ++k;
     }

@@ -122,6 +122,10 @@ class Session {
     // per-op device times of the last profile() call
     int profile_ops(int* kind, int* layer, int* info, double* ms, double* flops, int cap);
     int profile_starts(double* start_ms, int* stream_id, int cap);
+    // same op order as profile_ops: micro-batch (-1: per-step op), plan
+    // device of the worker whose stream runs it (0: a GPU's main stream),
+    // stream role (0 forward, 1 input-gradient, 2 weight-gradient, 3 main)
+    int op_meta(int* mb, int* device, int* role, int cap);
     double last_loss();
     double step_host(const float* X, const int* labels);  // load + one step + loss, one stream sync
 
@@ -140,6 +144,7 @@ class Session {
         std::vector<int> deps;
         cudaEvent_t ev = nullptr;
         int kernels = 0;
+        int mb = -1;        // micro-batch the op belongs to (-1: once per step)
     };
 
     void build();
@@ -191,7 +196,7 @@ class Session {
     std::vector<const double*> host_W_, host_b_;
     std::vector<ActLayout> lay_;  // [0..L]: layout of a_l as its consumer reads it
     bool pending_acc_error_ = false;
-    int cur_layer_ = 0, cur_info_ = 0;
+    int cur_layer_ = 0, cur_info_ = 0, cur_mb_ = -1;
     std::vector<double> last_op_ms_;
     double* loss_pinned_ = nullptr;  // pinned host slot for step_host's loss read-back
     std::vector<double> last_op_start_;  // ms from the first timed op (same device), last profile iteration

@@ -160,7 +160,7 @@ def test_lenet5_b256_bench_config(n):
     _check("lenet5", n, 1e-2)
 
 
-@pytest.mark.parametrize("n", [1, 8])
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
 def test_wide_mlp_b4096_bench_config(n):
     """BASELINE configs[4]: 4 x (8192 -> 8192), b=4096, one step."""
     _check("wide_mlp", n, 1e-2, steps=1)

@@ -1,0 +1,174 @@
+"""Executed schedule vs the reference's simulator (reference
+schedule.cpp:207-371, simulate.cpp:45-143,159-298).
+
+For one workload / plan / micro-batch count, on the B200:
+  1. run the product's Session under both stash policies (stash_all, the
+     reference executor; proposed, the paper's schedule), time the CUDA-graph
+     step, read the device bytes of the activation stash (Session.memory), and
+     profile one serialised eager step (CUDA events around every op) with the
+     op structure (Session.op_meta: micro-batch, plan device, stream role);
+  2. price the reference's tasks with those measurements: tf[i][j] / tb[i][j]
+     = device ms of sub-module i's forward / backward ops of micro-batch j
+     (weight-gradient ops belong to B(i, j) under the proposed policy; the
+     stash_all executor's one-per-step weight gradients are U(i) tasks, which
+     the simulator does not price, reported as update_ms), tcomm = the hub
+     copies of a concat boundary;
+  3. hand plan + prices to dropin/_build/simulate_b200 (the reference's
+     build_schedule + attach_updates + simulate + memory_compare, compiled
+     unchanged) and compare: the per-device task order with the executor's
+     enqueue order, the peak resident micro-batches per module with the
+     executor's ring, the proposed / stash_all memory ratio with the measured
+     stash bytes, and the predicted makespan with the measured step.
+
+The simulator treats every plan device as its own processor; on this one-GPU
+box all plan devices share cuda:0, so the measured step is compared with the
+simulator's makespan AND with the serial sum of the priced tasks.
+
+    python tools/sim_crosscheck.py vgg16 --n 1 --Z 1 --m 4 [--gate 2]
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+from paper_2207_11019_b200 import api  # noqa: E402
+from paper_2207_11019_b200.api import PartitionedTrainOptions, TrainConfig, UpdateMode  # noqa: E402
+
+SIM = os.path.join(ROOT, "dropin", "_build", "simulate_b200")
+
+
+def model_doc(net):
+    """The reference's model document (model.cpp:105-121) for the net: the
+    chain over sharded units, parameters and per-sample output bytes (fp32)."""
+    g = api.model_graph_of(net)
+    layers = []
+    for spec, layer in zip(g.layers, net.layers):
+        out_feat = layer.fan_out()
+        if layer.conv is not None:
+            c = layer.conv
+            ho = c.height + 2 * c.pad - c.ksize + 1
+            wo = c.width + 2 * c.pad - c.ksize + 1
+            out_feat = layer.fan_out() * (ho // c.pool) * (wo // c.pool)
+        layers.append({"kind": "dense", "fan_in": spec.fan_in, "fan_out": spec.fan_out,
+                       "param_count": int(layer.weights.size + layer.bias.size),
+                       "fwd_flops": float(spec.fwd_flops), "bwd_flops": 2.0 * float(spec.fwd_flops),
+                       "act_bytes": 4.0 * out_feat})
+    return {"schema": 1, "name": "b200-measured", "layers": layers}
+
+
+def _gate_ok(seq, gate):
+    seen = set()
+    for t in seq:
+        k, (mod, j) = t[0], map(int, t[1:].split("."))
+        if k == "F" and j > gate and ("B%d.%d" % (mod, j - gate)) not in seen:
+            return False
+        seen.add(t)
+    return True
+
+
+def module_of(plan, layer):
+    for sm in plan.submodules:
+        if sm.first_layer <= layer <= sm.last_layer:
+            return sm.index
+    return plan.submodules[-1].index
+
+
+def measure(net, X, y, plan, n, m, gate, memory):
+    ctx = api.Context([0] * n)
+    s = api.Session(ctx, net, X.shape[0], plan, m, UpdateMode.async_per_module, TrainConfig(iterations=1),
+                    PartitionedTrainOptions(multiclass_accuracy=True, pipeline_gate=gate, memory_mode=memory))
+    s.load_batch(X, y)
+    s.step(3)
+    s.sync()
+    graph_ms = s.time_steps(20) / 20
+    s.profile(1)
+    ops, meta = s.profile_ops(), s.op_meta()
+    total, stash = s.memory()
+    del s
+    Z = len(plan.submodules)
+    tf = [[0.0] * m for _ in range(Z)]
+    tb = [[0.0] * m for _ in range(Z)]
+    tcomm = [[0.0] * m for _ in range(max(Z - 1, 0))]
+    update_ms, order = 0.0, {}
+    for o, mt in zip(ops, meta):
+        i = module_of(plan, max(o["layer"], 1)) - 1
+        j = mt["mb"]
+        if j < 0:
+            update_ms += o["ms"]
+            continue
+        if o["kind"] == "peer_copy":
+            tcomm[min(i, Z - 2)][j] += o["ms"] * 1e-3
+            continue
+        fwd = mt["role"] == "forward" or (mt["role"] == "main" and o["kind"] in ("loss_head", "pool_relayout"))
+        (tf if fwd else tb)[i][j] += o["ms"] * 1e-3
+        if mt["device"] > 0 and mt["role"] in ("forward", "backward"):
+            key = ("F" if fwd else "B", i + 1, j + 1)
+            seq = order.setdefault(mt["device"], [])
+            if key not in seq:
+                seq.append(key)
+    return {"graph_ms": graph_ms, "serial_ms": sum(o["ms"] for o in ops), "update_ms": update_ms,
+            "device_bytes": total, "stash_bytes": stash, "tf": tf, "tb": tb, "tcomm": tcomm, "order": order}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("workload", default="vgg16", nargs="?", choices=sorted(bench.WORKLOADS))
+    ap.add_argument("--n", type=int, default=1)
+    ap.add_argument("--Z", type=int, default=1)
+    ap.add_argument("--m", type=int, default=4)
+    ap.add_argument("--gate", type=int, default=2)
+    ap.add_argument("--staged", action="store_true", help="disjoint device groups per stage")
+    args = ap.parse_args()
+    net, X, y = bench.synthetic_batch(args.workload, seed=1)
+    if args.staged:  # Z stages of n / Z devices each (build_staged_plan)
+        per = args.n // args.Z
+        plan = api.build_staged_plan(net, [list(range(1 + z * per, 1 + (z + 1) * per)) for z in range(args.Z)])
+    else:
+        plan = api.build_plan(net, args.n, args.Z)
+    res = {mm: measure(net, X, y, plan, args.n, args.m, args.gate, mm) for mm in ("stash_all", "proposed")}
+    p = res["proposed"]
+    req = {"model": model_doc(net), "plan": json.loads(api.serialize_plan(plan)), "m": args.m,
+           "tf": p["tf"], "tb": p["tb"], "tcomm": p["tcomm"],
+           "samples_per_microbatch": X.shape[0] / args.m, "bytes_per_param": 4.0}
+    with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as f:
+        json.dump(req, f)
+    out = subprocess.run([SIM, f.name], capture_output=True, text=True, timeout=300)
+    os.unlink(f.name)
+    if out.returncode != 0:
+        raise SystemExit(out.stderr)
+    sim = json.loads(out.stdout)
+    sim_order = {d + 1: [tuple(t) for t in lst if t[0] in ("F", "B")] for d, lst in enumerate(sim["device_order"])}
+    ours = {d: [tuple(t) for t in seq] for d, seq in p["order"].items()}
+    ring = min(args.m, args.gate) if args.gate > 0 else args.m
+    report = {
+        "workload": args.workload, "n": args.n, "Z": args.Z, "m": args.m, "gate": args.gate,
+        # the executor enqueues F(0..gate-1) then B(j - gate) before F(j): the gate
+        # bound; the reference's list schedule runs a ready B first, so on a
+        # device shared by every module it holds one micro-batch, on staged
+        # device groups two (tests/test_schedule_sim.py)
+        "executor_gate_respected": all(_gate_ok(["%s%d.%d" % t for t in seq], args.gate) for seq in ours.values()),
+        "executor_order": {d: ["%s%d.%d" % t for t in seq] for d, seq in ours.items()},
+        "reference_order": {d: ["%s%d.%d" % t for t in seq] for d, seq in sim_order.items()},
+        "peak_live_microbatches_reference": sim["peak_live_microbatches"],
+        "executor_ring_slots": ring,
+        "memory_ratio_reference": sim["memory_ratio"],
+        "stash_bytes": {k: v["stash_bytes"] for k, v in res.items()},
+        "stash_ratio_measured": res["proposed"]["stash_bytes"] / res["stash_all"]["stash_bytes"],
+        "predicted_makespan_ms": sim["makespan_s"] * 1e3,
+        "priced_serial_ms": sum(map(sum, p["tf"])) * 1e3 + sum(map(sum, p["tb"])) * 1e3,
+        "measured_graph_ms": {k: v["graph_ms"] for k, v in res.items()},
+        "measured_serial_ms": {k: v["serial_ms"] for k, v in res.items()},
+        "stash_all_update_ms": res["stash_all"]["update_ms"],
+        "reference_utilization": sim["utilization"],
+    }
+    print(json.dumps(report))
+
+
+if __name__ == "__main__":
+    main()
