@@ -283,6 +283,13 @@ int ppb_session_profile(ppb_session* s, int iterations, double* ms, int* count, 
 int ppb_session_profile_ops(ppb_session* s, int* kind, int* layer, int* info, double* ms, double* flops, int cap,
                             int* count);
 
+/* Like ppb_session_profile, but the ops overlap as the CUDA graph lets them
+ * (every launch is queued behind a spin before the first kernel runs; no
+ * per-op serialisation): ppb_session_profile_ops / _starts then give each
+ * op's device start and duration on a shared clock (a concurrency timeline,
+ * e.g. forward of micro-batch j+1 against backward of micro-batch j). */
+int ppb_session_profile_concurrent(ppb_session* s, int iterations);
+
 /* Step structure, same op order as ppb_session_profile_ops: the op's
  * micro-batch (0-based; -1 for once-per-step ops), the plan device of the
  * worker that runs it (1-based; 0 for a GPU's main stream: loss head,

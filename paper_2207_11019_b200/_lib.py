@@ -103,6 +103,7 @@ _SIGS = {
     "ppb_session_profile": (C.c_int, [C.c_void_p, C.c_int, _f64p, _i32p, _f64p, C.c_int]),
     "ppb_session_profile_ops": (C.c_int, [C.c_void_p, _i32p, _i32p, _i32p, _f64p, _f64p, C.c_int, _i32p]),
     "ppb_session_profile_starts": (C.c_int, [C.c_void_p, _f64p, _i32p, C.c_int, _i32p]),
+    "ppb_session_profile_concurrent": (C.c_int, [C.c_void_p, C.c_int]),
     "ppb_session_op_meta": (C.c_int, [C.c_void_p, _i32p, _i32p, _i32p, C.c_int, _i32p]),
     "ppb_debug_gemm": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_longlong, C.c_int,
                                  C.c_void_p, C.c_int, C.c_int, C.c_longlong, C.c_int,

@@ -585,6 +585,11 @@ class Session:
                  "ms": float(ms[i]), "tflops": float(fl[i] / ms[i] / 1e9) if ms[i] > 0 else 0.0}
                 for i in range(n.value)]
 
+    def profile_concurrent(self, iterations: int = 1) -> None:
+        """One eager step with the streams overlapping as in the graph (per-op
+        start / end events); read it with profile_timeline() / op_meta()."""
+        check(_lib.lib().ppb_session_profile_concurrent(self._h, iterations))
+
     def op_meta(self) -> list:
         """(micro-batch, plan device, stream role) per op, profile_ops() order
         (the enqueue order of the pipelined schedule)."""

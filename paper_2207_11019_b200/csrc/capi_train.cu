@@ -224,6 +224,22 @@ extern "C" int ppb_session_profile_starts(ppb_session* s, double* start_ms, int*
     return ppb_guard([&] { *count = s->s->profile_starts(start_ms, stream_id, cap); });
 }
 
+extern "C" int ppb_session_profile_concurrent(ppb_session* s, int iterations) {
+    return ppb_guard([&] {
+        constexpr int kKinds = OP_NKINDS;
+        double ms[kKinds], fl[kKinds];
+        int cnt[kKinds];
+        s->s->set_profile_serialised(false);
+        try {
+            s->s->profile(iterations, ms, cnt, fl, kKinds);
+        } catch (...) {
+            s->s->set_profile_serialised(true);
+            throw;
+        }
+        s->s->set_profile_serialised(true);
+    });
+}
+
 extern "C" int ppb_session_op_meta(ppb_session* s, int* microbatch, int* device, int* role, int cap, int* count) {
     return ppb_guard([&] { *count = s->s->op_meta(microbatch, device, role, cap); });
 }

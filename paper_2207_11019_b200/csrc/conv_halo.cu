@@ -294,6 +294,10 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 const int hh = rem / hg.wp, ww = rem - hh * hg.wp;
                 if (hh >= 1 && hh <= hg.ho && ww >= 1 && ww <= hg.wo) m = (img * hg.ho + hh - 1) * hg.wo + ww - 1;
             }
+            // the first chunk's ReLU-mask box is loaded while the tile's MMAs run
+            const bool masked = ts.n && ts.mask;
+            if (masked && half < BN / 32)
+                tma_mask_issue(ts, stg + (warp - 4) * 4096, mbar, lane, static_cast<int>(p0) + q * 32, n0 + half * 32);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
 #pragma unroll 1
@@ -304,9 +308,12 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 float v[32];
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = m >= 0 ? __uint_as_float(rr[i]) : 0.f;
-                if (ts.n && ts.mask) {  // the mask is zero on the ring
-                    tma_store_chunk_masked(ts, stg + (warp - 4) * 4096, mbar, mphase, lane, v,
-                                           static_cast<int>(p0) + q * 32, n0 + c * 32);
+                if (masked) {  // the mask is zero on the ring
+                    if (c != half)
+                        tma_mask_issue(ts, stg + (warp - 4) * 4096, mbar, lane, static_cast<int>(p0) + q * 32,
+                                       n0 + c * 32);
+                    tma_store_masked_issued(ts, stg + (warp - 4) * 4096, mbar, mphase, lane, v,
+                                            static_cast<int>(p0) + q * 32, n0 + c * 32);
                 } else if (ts.n) {  // pad-ring rows store zeros (the destination's own ring)
                     epi_values32(epi, m, n0 + c * 32, v, lane);
                     if (m < 0) {

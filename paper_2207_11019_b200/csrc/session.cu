@@ -1650,6 +1650,13 @@ void Session::enqueue_iteration() {
 
 void Session::enqueue_iteration_timed(std::vector<cudaEvent_t>& t0, std::vector<cudaEvent_t>& t1) {
     std::set<cudaStream_t> joined;
+    if (!serialise_) {
+        // concurrent timeline: hold the step behind a spin so every launch is
+        // queued before the first kernel runs (as in the graph), then let the
+        // streams overlap; events record each op's start / end
+        check(cudaSetDevice(ops_[begin_op_].gpu), "cudaSetDevice");
+        check(launch_spin(3000000, ops_[begin_op_].stream), "spin");
+    }
     for (int i = 0; i < static_cast<int>(ops_.size()); ++i) {
         Op& op = ops_[i];
         check(cudaSetDevice(op.gpu), "cudaSetDevice");
@@ -1659,14 +1666,14 @@ void Session::enqueue_iteration_timed(std::vector<cudaEvent_t>& t0, std::vector<
         for (int d : op.deps)
             if (ops_[d].stream != op.stream) check(cudaStreamWaitEvent(op.stream, ops_[d].ev, 0), "wait");
         if (op.launch) {
-            check(launch_spin(30000, op.stream), "spin");  // absorbs the launch latency of what follows
+            if (serialise_) check(launch_spin(30000, op.stream), "spin");  // absorbs the launch latency of what follows
             check(cudaEventRecord(t0[i], op.stream), "record");
             check(op.launch(), "kernel launch");
             check(cudaEventRecord(t1[i], op.stream), "record");
             // serialised: every op runs alone, so its CUDA-event duration is the
             // kernel's own time (the graph overlaps streams; events cannot
             // separate concurrent kernels)
-            check(cudaEventSynchronize(t1[i]), "serialise");
+            if (serialise_) check(cudaEventSynchronize(t1[i]), "serialise");
         }
         check(cudaEventRecord(op.ev, op.stream), "record");
     }

@@ -122,6 +122,9 @@ class Session {
     // per-op device times of the last profile() call
     int profile_ops(int* kind, int* layer, int* info, double* ms, double* flops, int cap);
     int profile_starts(double* start_ms, int* stream_id, int cap);
+    // profile() variant: ops overlap as in the graph (every launch queued
+    // behind a spin first), per-op start / end events, no serialisation
+    void set_profile_serialised(bool on) { serialise_ = on; }
     // same op order as profile_ops: micro-batch (-1: per-step op), plan
     // device of the worker whose stream runs it (0: a GPU's main stream),
     // stream role (0 forward, 1 input-gradient, 2 weight-gradient, 3 main)
@@ -197,6 +200,7 @@ class Session {
     std::vector<ActLayout> lay_;  // [0..L]: layout of a_l as its consumer reads it
     bool pending_acc_error_ = false;
     int cur_layer_ = 0, cur_info_ = 0, cur_mb_ = -1;
+    bool serialise_ = true;
     std::vector<double> last_op_ms_;
     double* loss_pinned_ = nullptr;  // pinned host slot for step_host's loss read-back
     std::vector<double> last_op_start_;  // ms from the first timed op (same device), last profile iteration

@@ -111,12 +111,16 @@ __device__ __forceinline__ uint64_t* epi_mask_bar(uint8_t* stage_base, int ewarp
 // same rows / columns) is TMA-loaded into the staging box, each lane masks
 // its row from shared memory (conflict-free, same swizzle), writes the
 // result back in place and lane 0 stores it.  v is masked in place (db).
-__device__ __forceinline__ void tma_store_chunk_masked(const TmaStore& ts, uint8_t* buf, uint64_t* bar,
-                                                       uint32_t& phase, int lane, float (&v)[32], int r0, int n) {
+// Issue the ReLU-mask box load of a chunk (the layer's activation at the same
+// rows / columns) into the warp's staging box once its previous store has
+// read it (lane 0).  Split from tma_store_chunk_masked so an epilogue can
+// issue it before waiting for the accumulator and hide its latency.
+__device__ __forceinline__ void tma_mask_issue(const TmaStore& ts, uint8_t* buf, uint64_t* bar, int lane, int r0,
+                                               int n, bool rank4 = false) {
     if (lane == 0) {
         bulk_wait_read<0>();  // the previous store has read the box
         mbar_arrive_expect_tx(bar, 4096);
-        if (ts.rank == 2) {
+        if (ts.rank == 2 && !rank4) {
             tma_load_2d(buf, &ts.mmap, bar, n, r0);
         } else {
             const int img = r0 / ts.pix, rem = r0 - img * ts.pix;
@@ -124,6 +128,13 @@ __device__ __forceinline__ void tma_store_chunk_masked(const TmaStore& ts, uint8
             tma_load_4d(buf, &ts.mmap, bar, n, w, h, img);
         }
     }
+}
+
+// Second half of the masked store: wait for the issued mask box, mask each
+// lane's row from shared memory (conflict-free, same swizzle), write the
+// result back in place and lane 0 stores it.  v is masked in place (db).
+__device__ __forceinline__ void tma_store_masked_issued(const TmaStore& ts, uint8_t* buf, uint64_t* bar,
+                                                        uint32_t& phase, int lane, float (&v)[32], int r0, int n) {
     mbar_wait(bar, phase);
     phase ^= 1u;
     const uint32_t row = smem_u32(buf) + lane * 128;
@@ -152,16 +163,17 @@ __device__ __forceinline__ void tma_store_chunk_masked(const TmaStore& ts, uint8
     }
 }
 
-// ReLU mask of the chunk (TMA-loaded box) applied in registers, no store.
-__device__ __forceinline__ void tma_mask_chunk(const TmaStore& ts, uint8_t* buf, uint64_t* bar, uint32_t& phase,
-                                               int lane, float (&v)[32], int r0, int n) {
-    if (lane == 0) {
-        bulk_wait_read<0>();
-        mbar_arrive_expect_tx(bar, 4096);
-        const int img = r0 / ts.pix, rem = r0 - img * ts.pix;
-        const int h = rem / ts.wo, w = rem - h * ts.wo;
-        tma_load_4d(buf, &ts.mmap, bar, n, w, h, img);
-    }
+// Masked variant of tma_store_chunk: load the mask box, then mask and store.
+__device__ __forceinline__ void tma_store_chunk_masked(const TmaStore& ts, uint8_t* buf, uint64_t* bar,
+                                                       uint32_t& phase, int lane, float (&v)[32], int r0, int n) {
+    tma_mask_issue(ts, buf, bar, lane, r0, n);
+    tma_store_masked_issued(ts, buf, bar, phase, lane, v, r0, n);
+}
+
+// ReLU mask of the chunk (its rank-4 mask box already issued with
+// tma_mask_issue(..., rank4 = true)) applied in registers, no store.
+__device__ __forceinline__ void tma_mask_apply_issued(uint8_t* buf, uint64_t* bar, uint32_t& phase, int lane,
+                                                      float (&v)[32]) {
     mbar_wait(bar, phase);
     phase ^= 1u;
     const uint32_t row = smem_u32(buf) + lane * 128;
@@ -177,6 +189,13 @@ __device__ __forceinline__ void tma_mask_chunk(const TmaStore& ts, uint8_t* buf,
         v[4 * j + 3] = m3 > 0.f ? v[4 * j + 3] : 0.f;
     }
     __syncwarp();
+}
+
+// ReLU mask of the chunk (TMA-loaded box) applied in registers, no store.
+__device__ __forceinline__ void tma_mask_chunk(const TmaStore& ts, uint8_t* buf, uint64_t* bar, uint32_t& phase,
+                                               int lane, float (&v)[32], int r0, int n) {
+    tma_mask_issue(ts, buf, bar, lane, r0, n, true);
+    tma_mask_apply_issued(buf, bar, phase, lane, v);
 }
 
 // Backward merge through a 2x2 max-pool: row r0 + lane = pooled pixel, its 32
