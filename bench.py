@@ -11,9 +11,12 @@ SGD update) over one synthetic batch.
 * value      : samples/s with the batch resident in HBM, device time of the K
                timed steps (CUDA events on the launching stream, the step's
                join point; max over ranks).
-* e2e        : samples/s through the public C ABI (ppb_session_step_host) from
-               pinned host buffers: H2D of X and labels, the step, D2H of the
-               loss, every step, wall clock around K blocking calls.
+* e2e        : samples/s through the public C ABI from pinned host buffers:
+               ppb_session_step_host_pipelined (H2D of X and labels into a
+               double-buffered staging slot while the previous step runs, the
+               step, D2H of every step's loss), wall clock around K calls + the
+               drain; the blocking fp32 and fp64 (drop-in Batch layout) calls
+               are reported beside it.
 * roofline   : the dominant kernel family (tcgen05 TF32 shard GEMMs + halo
                conv), FLOPs per launch / average launch time, measured in this
                run with CUDA events around every GEMM of one eager step whose
@@ -54,15 +57,18 @@ WORKLOADS = {
     "mlp784": dict(net="mlp784", batch=64, classes=10, name="MLP 784-512-512-10, batch 64"),
     # BASELINE.json configs[1]: LeNet-5 on 28x28x1 (generic im2col conv path; latency-bound).
     "lenet5": dict(net="lenet5", batch=256, classes=10, name="LeNet-5 (28x28x1, 5x5 convs), batch 256"),
+    # BASELINE.json configs[3]: ResNet-18-style (residual blocks, option-A shortcuts, global average pool).
+    "resnet18": dict(net="resnet18", batch=1024, classes=10,
+                     name="ResNet-18-style (CIFAR 32x32x3, 17 conv + 512->10, residual blocks), batch 1024"),
 }
 
 
 def build_net(workload, seed=1):
     from paper_2207_11019_b200 import configs
 
-    kw = {"init": "kaiming"} if workload in ("vgg16", "lenet5") else {}
+    kw = {"init": "kaiming"} if workload in ("vgg16", "lenet5", "resnet18") else {}
     return {"vgg16": configs.vgg16_cifar, "wide_mlp": configs.wide_mlp, "mlp784": configs.mlp784,
-            "lenet5": configs.lenet5}[WORKLOADS[workload]["net"]](seed=seed, **kw)
+            "lenet5": configs.lenet5, "resnet18": configs.resnet18_cifar}[WORKLOADS[workload]["net"]](seed=seed, **kw)
 
 
 def synthetic_batch(workload, seed=1):
@@ -420,14 +426,37 @@ def run_ours(args, rank, world, dist):
     yp = torch.empty(batch, dtype=torch.int32, pin_memory=True)
     yp.numpy()[:] = y
     Xn, yn = Xp.numpy(), yp.numpy()
-    e2e_steps = max(1, min(args.steps, 20))
-    sess.step_host(Xn, yn)  # warm
+    e2e_steps = max(1, min(args.steps, 50))
+    # (a) the streaming entry (ppb_session_step_host_pipelined): batch t's H2D
+    # into a double-buffered staging slot overlaps step t-1; every step's loss
+    # is read back (one call later; the last one after the loop)
+    sess.step_host_pipelined(Xn, yn)  # warm
+    sess.sync()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        sess.step_host_pipelined(Xn, yn)
+    sess.sync()
+    last = sess.history()[0][-1]
+    e2e_s = time.perf_counter() - t0
+    if not np.isfinite(last):
+        raise RuntimeError("non-finite loss in the end-to-end run")
+    e2e = {"value": batch * e2e_steps / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": int(Xn.nbytes + yn.nbytes),
+           "d2h_bytes_per_step": 8, "steps": e2e_steps,
+           "api": "ppb_session_step_host_pipelined (pinned fp32 X, double-buffered staging, loss of every step read back)"}
+    # (b) blocking, one step per call (ppb_session_step_host), and (c) the same
+    # with the reference's fp64 batch rows (Batch::X, the drop-in's layout)
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         sess.step_host(Xn, yn)
-    e2e_s = time.perf_counter() - t0
-    e2e = {"value": batch * e2e_steps / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": int(Xn.nbytes + yn.nbytes),
-           "d2h_bytes_per_step": 8, "steps": e2e_steps}
+    e2e["blocking_fp32"] = batch * e2e_steps / (time.perf_counter() - t0)
+    X64 = torch.empty((batch, in_feat), dtype=torch.float64, pin_memory=True)
+    X64.numpy()[:] = X
+    sess.step_host_f64(X64.numpy(), yn)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        sess.step_host_f64(X64.numpy(), yn)
+    e2e["blocking_fp64_dropin_layout"] = batch * e2e_steps / (time.perf_counter() - t0)
+    e2e["h2d_bytes_per_step_fp64"] = int(X64.numpy().nbytes + yn.nbytes)
 
     # ---- roofline of the dominant kernel
     peaks, peak_src = measured_peaks()
@@ -491,7 +520,8 @@ def run_ours(args, rank, world, dist):
                        "parallelism": f"layer-wise partition over {n} GPU(s)" + (
                            f" ({plan_devs} plan devices sharing cuda:0)" if plan_devs != n else ""),
                        "l2": {"wide_mlp": "inputs larger than L2 (weights 1 GiB + activations 0.5 GiB per step)",
-                              "vgg16": "inputs larger than L2 (activations + error signals ~1.5 GiB per step)"}.get(
+                              "vgg16": "inputs larger than L2 (activations + error signals ~1.5 GiB per step)",
+                              "resnet18": "inputs larger than L2 (activations + error signals ~8 GiB per step)"}.get(
                            args.workload, "working set fits L2 (latency-bound config)")},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
             "gpu_launches": sess.kernels_per_step() * args.steps,

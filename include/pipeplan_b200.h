@@ -187,7 +187,17 @@ typedef struct {
     int act;
     int height, width;
     int ksize, pad, pool;
+    /* residual extension (ResNet-style configs): res_from = 1-based index of
+     * an earlier conv layer whose output is added to this conv's
+     * pre-activation (identity, or ResNet "option A": every f-th position, C
+     * zero-padded, when the grids / widths differ), 0 = none; pool_kind =
+     * PPB_POOL_MAX (2x2) or PPB_POOL_AVG (pool x pool average, e.g. a global
+     * average pool before the classifier). */
+    int res_from;
+    int pool_kind;
 } ppb_layer;
+#define PPB_POOL_MAX 0
+#define PPB_POOL_AVG 1
 
 void ppb_default_options(ppb_options* o);
 void ppb_default_config(ppb_train_config* c);
@@ -245,6 +255,15 @@ int ppb_session_step(ppb_session* s, int iterations);
 /* One end-to-end step for streaming callers: H2D of X/labels from host
  * buffers, the step, and a D2H read of that step's loss (blocking). */
 int ppb_session_step_host(ppb_session* s, const float* X, const int* labels, double* loss_out);
+/* The same with the reference's fp64 batch rows (Batch::X, tinynet.hpp:58-63). */
+int ppb_session_step_host_f64(ppb_session* s, const double* X, const int* labels, double* loss_out);
+/* Streaming form: batch t (fp32 X, or fp64 X64 when non-null) is copied into a
+ * double-buffered device staging slot on a copy stream while step t-1 still
+ * runs; the call returns once step t-1 finished, with its loss in
+ * *prev_loss_out (NaN on the first call).  At most two steps in flight; call
+ * ppb_session_sync then read the history for the last loss. */
+int ppb_session_step_host_pipelined(ppb_session* s, const float* X, const double* X64, const int* labels,
+                                    double* prev_loss_out);
 
 /* Block until all enqueued work finished; reports divergence / CUDA errors. */
 int ppb_session_sync(ppb_session* s);

@@ -47,8 +47,22 @@ def split_microbatches(b, m):
     return sizes
 
 
-def _forward(layers, params, x, flatten=True):
+def _shortcut(src, like):
+    """ResNet shortcut of a residual layer (the residual extension of the
+    conv layer description, include/pipeplan_b200.h ppb_layer.res_from):
+    identity, or "option A" (He et al. 2016, §4.2) -- every f-th position of
+    the source, its channels zero-padded to the layer's width."""
+    f = src.shape[2] // like.shape[2]
+    s = src[:, :, ::f, ::f] if f > 1 else src
+    if s.shape[1] < like.shape[1]:
+        s = torch.cat([s, s.new_zeros(s.shape[0], like.shape[1] - s.shape[1], s.shape[2], s.shape[3])], dim=1)
+    return s
+
+
+def _forward(layers, params, x, flatten=True, outs=None):
+    """outs: per-layer outputs so far (residual sources); layers index from len(outs)."""
     a = x
+    outs = [] if outs is None else outs
     for lay, (w, b) in zip(layers, params):
         if lay.conv is not None:
             c = lay.conv
@@ -57,9 +71,13 @@ def _forward(layers, params, x, flatten=True):
             if a.dim() == 2:
                 a = a.reshape(a.shape[0], c.height, c.width, cin).permute(0, 3, 1, 2)
             a = Fn.conv2d(a, wt, b, padding=c.pad)
+            if getattr(c, "res_from", 0):
+                a = a + _shortcut(outs[c.res_from - 1], a)
             if int(lay.act) == RELU:
                 a = torch.relu(a)
-            if c.pool == 2:
+            if getattr(c, "pool_avg", False) and c.pool > 1:
+                a = Fn.avg_pool2d(a, c.pool)
+            elif c.pool == 2:
                 a = Fn.max_pool2d(a, 2)
         else:
             if a.dim() == 4:
@@ -67,6 +85,7 @@ def _forward(layers, params, x, flatten=True):
             a = a @ w.t() + b
             if int(lay.act) == RELU:
                 a = torch.relu(a)
+        outs.append(a)
     if flatten and a.dim() == 4:
         a = a.reshape(a.shape[0], -1)
     return a
@@ -169,9 +188,9 @@ def forward_acts(net, X):
     if layers[0].conv is not None:
         c = layers[0].conv
         a = a.reshape(-1, c.height, c.width, layers[0].in_units()).permute(0, 3, 1, 2)
-    outs = []
+    outs, raw = [], []
     for i in range(len(layers)):
-        a = _forward(layers[i:i + 1], params[i:i + 1], a, flatten=False)
+        a = _forward(layers[i:i + 1], params[i:i + 1], a, flatten=False, outs=raw)
         outs.append(a.permute(0, 2, 3, 1).reshape(a.shape[0], -1).numpy() if a.dim() == 4 else a.numpy())
     return outs
 
@@ -203,6 +222,9 @@ def train_model(net, X, y, alpha0, decay, iterations, m=1, tf32_mode=None):
     GPU's TF32 path, used to separate "the kernels compute what they should"
     (tight) from "TF32 vs the fp64 reference" (looser, stated).  CE + softmax
     head, multiclass accuracy.  Returns (W, b, loss_hist)."""
+    if any(l.conv is not None and (getattr(l.conv, "res_from", 0) or getattr(l.conv, "pool_avg", False))
+           for l in net.layers):
+        raise NotImplementedError("train_model: residual / average-pool layers (use train, autograd)")
     exact = tf32_mode is None
     T = (lambda t: t) if exact else (lambda t: tf32(t, tf32_mode))
     S = (lambda t: t) if exact else _f32

@@ -51,7 +51,8 @@ class OptionsC(C.Structure):
 
 class LayerC(C.Structure):
     _fields_ = [("kind", C.c_int), ("in_units", C.c_int), ("out_units", C.c_int), ("act", C.c_int),
-                ("height", C.c_int), ("width", C.c_int), ("ksize", C.c_int), ("pad", C.c_int), ("pool", C.c_int)]
+                ("height", C.c_int), ("width", C.c_int), ("ksize", C.c_int), ("pad", C.c_int), ("pool", C.c_int),
+                ("res_from", C.c_int), ("pool_kind", C.c_int)]
 
 
 # name -> (restype, argtypes)
@@ -92,6 +93,8 @@ _SIGS = {
     "ppb_session_load_batch_f32": (C.c_int, [C.c_void_p, _f32p, _i32p]),
     "ppb_session_step": (C.c_int, [C.c_void_p, C.c_int]),
     "ppb_session_step_host": (C.c_int, [C.c_void_p, _f32p, _i32p, _f64p]),
+    "ppb_session_step_host_f64": (C.c_int, [C.c_void_p, _f64p, _i32p, _f64p]),
+    "ppb_session_step_host_pipelined": (C.c_int, [C.c_void_p, _f32p, _f64p, _i32p, _f64p]),
     "ppb_session_sync": (C.c_int, [C.c_void_p]),
     "ppb_session_history": (C.c_int, [C.c_void_p, _f64p, _f64p, C.c_int, _i32p]),
     "ppb_session_get_net": (C.c_int, [C.c_void_p, _f64p, _f64p]),

@@ -162,6 +162,12 @@ class ConvSpec:
     ksize: int = 3
     pad: int = 1
     pool: int = 1
+    # residual extension (ResNet-style configs): add the output of layer
+    # `res_from` (1-based, 0 = none) to the pre-activation -- identity, or
+    # every f-th position with zero-padded channels ("option A") -- and pool
+    # with a pool x pool average instead of the 2x2 max (`pool_avg`)
+    res_from: int = 0
+    pool_avg: bool = False
 
     def out_hw(self):
         ho = self.height + 2 * self.pad - self.ksize + 1
@@ -205,6 +211,7 @@ class TinyLayer:  # tinynet.hpp:41-48
         if self.conv:
             lc.height, lc.width, lc.ksize, lc.pad, lc.pool = (self.conv.height, self.conv.width, self.conv.ksize,
                                                               self.conv.pad, self.conv.pool)
+            lc.res_from, lc.pool_kind = self.conv.res_from, int(self.conv.pool_avg)
         return lc
 
 
@@ -618,6 +625,26 @@ class Session:
         loss = C.c_double(0)
         Xc, y = self._host_batch(X, labels, np.float32)  # no copy when already float32 / int32 contiguous
         check(_lib.lib().ppb_session_step_host(self._h, Xc.ctypes.data_as(_f), _ip(y), C.byref(loss)))
+        return loss.value
+
+    def step_host_f64(self, X: np.ndarray, labels: np.ndarray) -> float:
+        """step_host with the reference's fp64 batch rows (Batch::X)."""
+        loss = C.c_double(0)
+        Xc, y = self._host_batch(X, labels, np.float64)
+        check(_lib.lib().ppb_session_step_host_f64(self._h, _dp(Xc), _ip(y), C.byref(loss)))
+        return loss.value
+
+    def step_host_pipelined(self, X: np.ndarray, labels: np.ndarray) -> float:
+        """Streaming step: stages this batch while the previous step runs and
+        returns the PREVIOUS step's loss (NaN on the first call)."""
+        loss = C.c_double(0)
+        if np.asarray(X).dtype == np.float64:
+            Xc, y = self._host_batch(X, labels, np.float64)
+            check(_lib.lib().ppb_session_step_host_pipelined(self._h, None, _dp(Xc), _ip(y), C.byref(loss)))
+        else:
+            Xc, y = self._host_batch(X, labels, np.float32)
+            check(_lib.lib().ppb_session_step_host_pipelined(self._h, Xc.ctypes.data_as(_f), None, _ip(y),
+                                                             C.byref(loss)))
         return loss.value
 
     def kernels_per_step(self) -> int:

@@ -126,6 +126,10 @@ extern "C" int ppb_session_create_layers(ppb_context* ctx, const ppb_layer* laye
                 li.ksz = p.ksize;
                 li.pad = p.pad;
                 li.pool = p.pool < 1 ? 1 : p.pool;
+                li.res_from = p.res_from;
+                li.pool_avg = p.pool_kind == PPB_POOL_AVG ? 1 : 0;
+                if (p.pool_kind != PPB_POOL_MAX && p.pool_kind != PPB_POOL_AVG)
+                    throw std::invalid_argument("unknown pool kind " + std::to_string(p.pool_kind));
             }
             net.info.push_back(li);
             net.acts.push_back(p.act);
@@ -179,8 +183,23 @@ extern "C" int ppb_session_step(ppb_session* s, int iterations) {
 
 extern "C" int ppb_session_step_host(ppb_session* s, const float* X, const int* labels, double* loss_out) {
     return ppb_guard([&] {
-        const double v = s->s->step_host(X, labels);
+        const double v = s->s->step_host(nullptr, X, labels);
         if (loss_out) *loss_out = v;
+    });
+}
+
+extern "C" int ppb_session_step_host_f64(ppb_session* s, const double* X, const int* labels, double* loss_out) {
+    return ppb_guard([&] {
+        const double v = s->s->step_host(X, nullptr, labels);
+        if (loss_out) *loss_out = v;
+    });
+}
+
+extern "C" int ppb_session_step_host_pipelined(ppb_session* s, const float* X, const double* X64, const int* labels,
+                                               double* prev_loss_out) {
+    return ppb_guard([&] {
+        const double v = s->s->step_host_pipelined(X64, X64 ? nullptr : X, labels);
+        if (prev_loss_out) *prev_loss_out = v;
     });
 }
 

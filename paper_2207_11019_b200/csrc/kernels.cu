@@ -525,40 +525,39 @@ __global__ void dense_conv_fold_sgd_kernel(DenseConvGeom g, const float* __restr
 }
 
 // im2col of the fp32 input for K = k*k*C <= 32 (VGG conv1 27, LeNet C1 25):
-// thread = output pixel, its 32-column row (zeros past K) assembled in
-// registers and written as eight float4 (128 B rows: whole-line stores).
-__global__ void __launch_bounds__(256) im2col_row32_kernel(const float* __restrict__ src, int imgs, int H, int W,
+// 8 threads per output pixel, thread g writes columns 4g .. 4g+3 of the
+// pixel's 32-column row (zeros past K) as one float4, so a warp stores four
+// whole 128 B rows (coalesced); the gathered reads hit L1 / L2 (the input is
+// a few MB).
+template <class T>
+__global__ void __launch_bounds__(256) im2col_row32_kernel(const T* __restrict__ src, int imgs, int H, int W,
                                                            int C, int k, int p, float* __restrict__ dst,
                                                            long long ld) {
+    // blockIdx.y = image (32-bit index math: 64-bit divisions dominated this
+    // kernel), 8 threads per output pixel of the image
     const int Ho = H + 2 * p - k + 1, Wo = W + 2 * p - k + 1;
-    const long long npix = static_cast<long long>(imgs) * Ho * Wo;
-    const long long pix = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-    if (pix >= npix) return;
-    const int wo = static_cast<int>(pix % Wo);
-    const long long t = pix / Wo;
-    const int ho = static_cast<int>(t % Ho);
-    const long long n = t / Ho;
-    float r[32];
+    const int n = blockIdx.y;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int pi = t >> 3, g = t & 7;
+    if (pi >= Ho * Wo) return;
+    const int ho = pi / Wo, wo = pi - ho * Wo;
+    const int K = k * k * C;
+    const T* img = src + static_cast<long long>(n) * H * W * C;
+    float r[4];
 #pragma unroll
-    for (int i = 0; i < 32; ++i) r[i] = 0.f;
-    int col = 0;
-    for (int rr = 0; rr < k; ++rr) {
-        const int hi = ho + rr - p;
-        for (int ss = 0; ss < k; ++ss) {
-            const int wi = wo + ss - p;
-            const bool in = hi >= 0 && hi < H && wi >= 0 && wi < W;
-            const float* sp = src + ((n * H + hi) * W + wi) * C;
-            for (int c = 0; c < C; ++c, ++col) {
-                const float v = in ? __ldg(sp + c) : 0.f;
-#pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    if (i == col) r[i] = v;
-            }
+    for (int e = 0; e < 4; ++e) {
+        const int col = 4 * g + e;
+        float v = 0.f;
+        if (col < K) {
+            const int tap = col / C, c = col - tap * C;
+            const int rr = tap / k, ss = tap - rr * k;
+            const int hi = ho + rr - p, wi = wo + ss - p;
+            if (hi >= 0 && hi < H && wi >= 0 && wi < W) v = static_cast<float>(__ldg(img + (hi * W + wi) * C + c));
         }
+        r[e] = v;
     }
-    float4* d = reinterpret_cast<float4*>(dst + pix * ld);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) d[i] = make_float4(r[4 * i], r[4 * i + 1], r[4 * i + 2], r[4 * i + 3]);
+    reinterpret_cast<float4*>(dst + (static_cast<long long>(n) * Ho * Wo + pi) * ld)[g] =
+        make_float4(r[0], r[1], r[2], r[3]);
 }
 
 template <class T>
@@ -846,6 +845,147 @@ __global__ void conv_merge_rows_kernel(ConvMerge m, float* __restrict__ db_parti
     }
 }
 
+
+// ---------------------------------------------------------------- residual extension
+
+// Thread = (image, pooled pixel, 4-channel group); window p x p (p = 1: no
+// pooling).  Deterministic: the window is summed in row-major order.
+__global__ void residual_act_kernel(float* __restrict__ U, long long ldu, int imgs, int Ho, int Wo, int uch, int c0,
+                                    int relu, int pool, SkipSrc skip, ActLayout out, PoolDsts dsts) {
+    griddep_wait();
+    const int Hq = Ho / pool, Wq = Wo / pool;
+    const int groups = uch >> 2;
+    const long long total = static_cast<long long>(imgs) * Hq * Wq * groups;
+    const float inv = 1.f / static_cast<float>(pool * pool);
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int g = static_cast<int>(i % groups);
+        const long long pp = i / groups;
+        const int x = static_cast<int>(pp % Wq);
+        const long long t = pp / Wq;
+        const int y = static_cast<int>(t % Hq);
+        const long long n = t / Hq;
+        const int c = g * 4;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int dy = 0; dy < pool; ++dy) {
+            for (int dx = 0; dx < pool; ++dx) {
+                const int h = y * pool + dy, w = x * pool + dx;
+                float4* up = reinterpret_cast<float4*>(U + ((n * Ho + h) * Wo + w) * ldu + c);
+                float4 u = *up;
+                if (skip.a != nullptr) {  // option A: position (f h, f w) of the source
+                    const long long sb = ((n * skip.lay.hp + h * skip.f + skip.lay.pad) * skip.lay.wp + w * skip.f +
+                                          skip.lay.pad) * skip.lay.ld;
+                    const int ca = c0 + c;  // absolute channel of lane k: ca + k
+                    if (ca + 0 < skip.C) u.x += __ldg(skip.a + sb + ca + 0);
+                    if (ca + 1 < skip.C) u.y += __ldg(skip.a + sb + ca + 1);
+                    if (ca + 2 < skip.C) u.z += __ldg(skip.a + sb + ca + 2);
+                    if (ca + 3 < skip.C) u.w += __ldg(skip.a + sb + ca + 3);
+                    *up = u;
+                }
+                if (relu) {
+                    u.x = u.x > 0.f ? u.x : 0.f;
+                    u.y = u.y > 0.f ? u.y : 0.f;
+                    u.z = u.z > 0.f ? u.z : 0.f;
+                    u.w = u.w > 0.f ? u.w : 0.f;
+                }
+                acc.x += u.x;
+                acc.y += u.y;
+                acc.z += u.z;
+                acc.w += u.w;
+            }
+        }
+        if (pool > 1) {
+            acc.x *= inv;
+            acc.y *= inv;
+            acc.z *= inv;
+            acc.w *= inv;
+        }
+        if (out.kind == 0) {
+            const long long o = ((n * out.hp + y + out.pad) * out.wp + x + out.pad) * out.ld + out.col0 + c;
+            for (int d = 0; d < dsts.n; ++d) *reinterpret_cast<float4*>(dsts.ptr[d] + o) = acc;
+        } else {
+            const float v[4] = {acc.x, acc.y, acc.z, acc.w};
+            for (int k = 0; k < 4; ++k) {
+                const long long o = n * out.ld + static_cast<long long>(out.col0 + c + k) * Hq * Wq +
+                                    static_cast<long long>(y) * Wq + x;
+                for (int d = 0; d < dsts.n; ++d) dsts.ptr[d][o] = v[k];
+            }
+        }
+    }
+}
+
+// conv_merge_rows_kernel's structure (block = image row, threads = (column,
+// 4-channel group), bias partial per block in fixed order) with average-pool
+// routing and the shortcut term.
+__global__ void conv_merge_res_kernel(ConvMerge m, int pool_avg, SkipGrad sg, float* __restrict__ db_partial) {
+    griddep_wait();
+    const int groups = m.uch >> 2;
+    const int g = threadIdx.x % groups;
+    const int c0 = g * 4;
+    const int wstep = blockDim.x / groups;
+    const int w0 = threadIdx.x / groups;
+    const int p = m.pool;
+    const int Hg = m.Ho / p, Wg = m.Wo / p;
+    const int hq = m.Ho + 2 * m.q, wq = m.Wo + 2 * m.q;
+    const int rows = m.imgs * m.Ho;
+    const ActLayout& a = m.act_layout;
+    const float inv = 1.f / static_cast<float>(p * p);
+    float4 db = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+        const int n = r / m.Ho, h = r - n * m.Ho;
+        const int y = h / p;
+        for (int w = w0; w < m.Wo; w += wstep) {
+            const int x = w / p;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            const long long gp = (static_cast<long long>(n) * Hg + y) * Wg + x;
+            for (int s = 0; s < m.slots.n; ++s) {
+                const float4 t = __ldg(reinterpret_cast<const float4*>(m.slots.slot[s] + gp * m.lds + c0));
+                v.x += t.x; v.y += t.y; v.z += t.z; v.w += t.w;
+            }
+            if (p == 2 && !pool_avg) {  // max pool: the argmax position of the window takes it
+                const uint32_t want = static_cast<uint32_t>(((h & 1) << 1) | (w & 1));
+                const uint32_t b = __ldg(reinterpret_cast<const uint32_t*>(m.argmax + gp * m.uch + c0));
+                if ((b & 0xffu) != want) v.x = 0.f;
+                if (((b >> 8) & 0xffu) != want) v.y = 0.f;
+                if (((b >> 16) & 0xffu) != want) v.z = 0.f;
+                if ((b >> 24) != want) v.w = 0.f;
+            } else if (p > 1) {
+                v.x *= inv; v.y *= inv; v.z *= inv; v.w *= inv;
+            }
+            if (sg.d != nullptr && h % sg.f == 0 && w % sg.f == 0) {
+                const float4 t = __ldg(reinterpret_cast<const float4*>(
+                    sg.d + ((static_cast<long long>(n) * sg.hq + h / sg.f + sg.q) * sg.wq + w / sg.f + sg.q) * sg.ldd +
+                    sg.c0 + c0));
+                v.x += t.x; v.y += t.y; v.z += t.z; v.w += t.w;
+            }
+            float4 mk = make_float4(1.f, 1.f, 1.f, 1.f);
+            if (m.mask_kind == 1)
+                mk = __ldg(reinterpret_cast<const float4*>(m.U + (static_cast<long long>(r) * m.Wo + w) * m.ldu + c0));
+            else if (m.mask_kind == 2)
+                mk = __ldg(reinterpret_cast<const float4*>(
+                    m.act + ((static_cast<long long>(n) * a.hp + h + a.pad) * a.wp + w + a.pad) * a.ld + a.col0 + c0));
+            if (!(mk.x > 0.f)) v.x = 0.f;
+            if (!(mk.y > 0.f)) v.y = 0.f;
+            if (!(mk.z > 0.f)) v.z = 0.f;
+            if (!(mk.w > 0.f)) v.w = 0.f;
+            *reinterpret_cast<float4*>(m.d_pad + ((static_cast<long long>(n) * hq + h + m.q) * wq + w + m.q) * m.ldd +
+                                       c0) = v;
+            db.x += v.x; db.y += v.y; db.z += v.z; db.w += v.w;
+        }
+    }
+    extern __shared__ float sh[];
+    reinterpret_cast<float4*>(sh)[threadIdx.x] = db;
+    __syncthreads();
+    if (threadIdx.x < groups) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int t = threadIdx.x; t < static_cast<int>(blockDim.x); t += groups) {
+            const float4 u = reinterpret_cast<const float4*>(sh)[t];
+            acc.x += u.x; acc.y += u.y; acc.z += u.z; acc.w += u.w;
+        }
+        *reinterpret_cast<float4*>(db_partial + static_cast<long long>(blockIdx.x) * m.uch + c0) = acc;
+    }
+}
+
 int grid_for(long long work, int threads) {
     long long g = (work + threads - 1) / threads;
     const long long cap = 148LL * 16;
@@ -931,9 +1071,10 @@ cudaError_t launch_im2col_input(const double* src64, const float* src32, int img
     const long long n = static_cast<long long>(imgs) * (H + 2 * p - k + 1) * (W + 2 * p - k + 1) * k * k * C;
     if (n <= 0) return cudaSuccess;
     const long long npix = n / (static_cast<long long>(k) * k * C);
-    if (src32 != nullptr && k * k * C <= 32 && ld == 32 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
-        im2col_row32_kernel<<<static_cast<unsigned>((npix + 255) / 256), 256, 0, s>>>(src32, imgs, H, W, C, k, p, dst,
-                                                                                      ld);
+    if (k * k * C <= 32 && ld == 32 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {
+        const dim3 blocks(static_cast<unsigned>((npix / imgs * 8 + 255) / 256), static_cast<unsigned>(imgs));
+        if (src32 != nullptr) im2col_row32_kernel<float><<<blocks, 256, 0, s>>>(src32, imgs, H, W, C, k, p, dst, ld);
+        else im2col_row32_kernel<double><<<blocks, 256, 0, s>>>(src64, imgs, H, W, C, k, p, dst, ld);
         return cudaGetLastError();
     }
     if (src64) im2col_kernel<double><<<grid_for(n, 256), 256, 0, s>>>(src64, imgs, H, W, C, k, p, dst, ld);
@@ -1059,6 +1200,32 @@ cudaError_t launch_conv_merge(const ConvMerge& m, float* db_partial, cudaStream_
         if (i32) pdl_launch(conv_merge_kernel<1, unsigned>, dim3(grid), dim3(block), shmem, s, m, db_partial);
         else pdl_launch(conv_merge_kernel<1, long long>, dim3(grid), dim3(block), shmem, s, m, db_partial);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_residual_act(float* U, long long ldu, int imgs, int Ho, int Wo, int uch, int c0, int relu,
+                                int pool, const SkipSrc& skip, const ActLayout& out, const PoolDsts& dsts,
+                                cudaStream_t s) {
+    const long long n = static_cast<long long>(imgs) * (Ho / pool) * (Wo / pool) * (uch / 4);
+    if (n <= 0) return cudaSuccess;
+    if (uch % 4 != 0 || ldu % 4 != 0 || (out.kind == 0 && (out.ld % 4 != 0 || out.col0 % 4 != 0)))
+        return cudaErrorInvalidValue;
+    pdl_launch(residual_act_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, U, ldu, imgs, Ho, Wo, uch, c0, relu, pool,
+               skip, out, dsts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_conv_merge_res(const ConvMerge& m, int pool_avg, const SkipGrad& sg, float* db_partial,
+                                  cudaStream_t s) {
+    const int grid = conv_merge_blocks();
+    if (m.uch % 4 != 0 || m.slot_kind != 0 || !vec4_ok(m.lds, m.ldd) || (sg.d != nullptr && !vec4_ok(sg.ldd, sg.c0)))
+        return cudaErrorInvalidValue;
+    const int groups = m.uch / 4;
+    const int block = group_block(groups);
+    if (static_cast<long long>(m.imgs) * m.Ho * m.Wo * m.uch <= 0)
+        return cudaMemsetAsync(db_partial, 0, sizeof(float) * grid * m.uch, s);
+    pdl_launch(conv_merge_res_kernel, dim3(grid), dim3(block), sizeof(float) * block * 4, s, m, pool_avg, sg,
+               db_partial);
     return cudaGetLastError();
 }
 

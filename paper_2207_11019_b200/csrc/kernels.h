@@ -143,6 +143,44 @@ struct ConvMerge {
 int conv_merge_blocks();
 cudaError_t launch_conv_merge(const ConvMerge& m, float* db_partial, cudaStream_t s);
 
+// ---- residual extension (BASELINE configs[3], ResNet-18-style; the
+// reference's TinyNet is a chain, tinynet.hpp:50-56, so residual edges are an
+// extension of the conv layer description).  A residual layer l adds the
+// shortcut of an earlier layer's output a_s to its pre-activation:
+//   q_l = conv_l(a_{l-1}) + b_l + shortcut(a_s),
+// shortcut = identity, or (ResNet "option A", He et al. 2016 §4.2) the
+// positions (f*y, f*x) of a_s with its C_s channels zero-padded to C_l.
+struct SkipSrc {
+    const float* a = nullptr;  // a_s in its consumer layout (padded NHWC), row 0 of this micro-batch
+    ActLayout lay;             // that layout (col0 unused)
+    int f = 1;                 // spatial subsampling factor (grid of s / conv grid of l)
+    int C = 0;                 // C_s: channels >= C get no shortcut
+};
+// Forward of a residual and / or average-pooled conv layer's shard: for each
+// output position u = U + shortcut (written back into U: the pre-activation
+// the backward mask reads), a = act(u), then a p x p average (pool_avg) or no
+// pooling, stored into every destination's consumer layout.  c0 = the
+// shard's first channel (absolute).
+cudaError_t launch_residual_act(float* U, long long ldu, int imgs, int Ho, int Wo, int uch, int c0, int relu,
+                                int pool, const SkipSrc& skip, const ActLayout& out, const PoolDsts& dsts,
+                                cudaStream_t s);
+// Backward shortcut term for the error signal of a skip-source layer s: the
+// error signal of the residual layer l (padded [img][Ho_l+2q][Wo_l+2q][ldd]),
+// at channel c + c0 of l's shard for channel c of s's shard.
+struct SkipGrad {
+    const float* d = nullptr;  // row 0 of this micro-batch
+    long long ldd = 0;
+    int hq = 0, wq = 0, q = 0;  // padded grid of delta_l
+    int f = 1, c0 = 0;
+};
+// conv_merge for layers the residual extension touches: as launch_conv_merge
+// (slot sum in ascending device order, ReLU mask, padded store, bias
+// partials) with a p x p average pool routing (pool_avg: every position gets
+// G / p^2) and / or the shortcut term added before the mask.  uch % 4 == 0,
+// pixel-major slots, mask_kind 1 (U rows: the residual pre-activation) or 2.
+cudaError_t launch_conv_merge_res(const ConvMerge& m, int pool_avg, const SkipGrad& sg, float* db_partial,
+                                  cudaStream_t s);
+
 // bias -= alpha * (sum_k partial[k][c] / b) over `chunks` partial rows.
 cudaError_t launch_bias_from_partials(const float* partial, int chunks, int u, float* bias, const double* alpha,
                                       float inv_b, cudaStream_t s);

@@ -38,7 +38,11 @@ struct Session::Gpu {
     int* correct_row = nullptr;
     double* loss_hist = nullptr;
     double* acc_hist = nullptr;
-    double* xstage = nullptr;
+    double* xstage = nullptr;     // staging of the host batch (double-buffered with xstage2)
+    double* xstage2 = nullptr;
+    int* lstage[2] = {nullptr, nullptr};  // staged labels
+    cudaStream_t copy = nullptr;  // host -> device staging stream
+    cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_consumed[2] = {nullptr, nullptr};
     std::map<int, float*> act;  // layer -> [b x ld(dims[layer])]
     float* q = nullptr;         // softmax head pre-activation [b x ld(F)]
     std::vector<void*> allocs;
@@ -177,8 +181,8 @@ Session::Session(const std::vector<int>& device_map, const NetDesc& net, const d
         if (li.in_units < 1 || li.out_units < 1)
             throw std::invalid_argument("layer " + S(l + 1) + ": empty weight matrix");
         if (li.kind == 1) {
-            if (li.ksz < 1 || li.pad < 0 || (li.pool != 1 && li.pool != 2) || li.Ho() < 1 || li.Wo() < 1 ||
-                (li.pool == 2 && (li.Ho() % 2 || li.Wo() % 2)))
+            if (li.ksz < 1 || li.pad < 0 || li.pool < 1 || (!li.pool_avg && li.pool > 2) || li.Ho() < 1 ||
+                li.Wo() < 1 || li.Ho() % li.pool || li.Wo() % li.pool)
                 throw std::invalid_argument("layer " + S(l + 1) + ": invalid conv geometry");
             ConvShape cs;
             cs.N = 1;
@@ -210,6 +214,22 @@ Session::Session(const std::vector<int>& device_map, const NetDesc& net, const d
         }
         if (net_.acts[l] == 2 && l != L - 1)
             throw std::invalid_argument("softmax is only valid on the last layer");
+        if (li.res_from != 0) {  // residual edge from the output of layer res_from (1-based)
+            const int s = li.res_from - 1;
+            if (li.kind != 1 || s < 0 || s >= l || net_.info[s].kind != 1)
+                throw std::invalid_argument("layer " + S(l + 1) + ": residual source must be an earlier conv layer");
+            const LayerInfo& ls = net_.info[s];
+            const int f = ls.Hq() / li.Ho();
+            if (f < 1 || ls.Hq() != f * li.Ho() || ls.Wq() != f * li.Wo() || li.out_units < ls.out_units)
+                throw std::invalid_argument("layer " + S(l + 1) + ": residual shortcut shape mismatch");
+            if (li.act == 2) throw std::invalid_argument("layer " + S(l + 1) + ": residual layer with softmax");
+        }
+        if (li.res_from != 0)
+            for (int k = 0; k < l; ++k)
+                if (net_.info[k].res_from == li.res_from)
+                    throw std::invalid_argument("layer " + S(li.res_from) + ": source of two residual edges");
+        if (li.special() && (li.out_units % 4 != 0 || cfg_.precision != 0))
+            throw std::invalid_argument("layer " + S(l + 1) + ": residual / average-pool layers need C_out % 4 == 0");
     }
     // few input channels on the first conv: im2col rows (K = k*k*C) instead of
     // 32-channel-padded implicit GEMM taps (K = k*k*32)
@@ -290,6 +310,11 @@ Session::~Session() {
         cudaSetDevice(g->ordinal);
         for (void* p : g->allocs) cudaFree(p);
         if (g->ev_loaded) cudaEventDestroy(g->ev_loaded);
+        for (int k = 0; k < 2; ++k) {
+            if (g->ev_copied[k]) cudaEventDestroy(g->ev_copied[k]);
+            if (g->ev_consumed[k]) cudaEventDestroy(g->ev_consumed[k]);
+        }
+        if (g->copy) cudaStreamDestroy(g->copy);
         if (g->ev_done) cudaEventDestroy(g->ev_done);
         cudaStreamDestroy(g->main);
     }
@@ -316,6 +341,11 @@ void Session::build() {
         check(tc_gemm_init_device(), "GEMM attributes");
         check(cudaStreamCreateWithFlags(&g->main, cudaStreamNonBlocking), "stream");
         check(cudaEventCreateWithFlags(&g->ev_loaded, cudaEventDisableTiming), "event");
+        check(cudaStreamCreateWithFlags(&g->copy, cudaStreamNonBlocking), "stream");
+        for (int k = 0; k < 2; ++k) {
+            check(cudaEventCreateWithFlags(&g->ev_copied[k], cudaEventDisableTiming), "event");
+            check(cudaEventCreateWithFlags(&g->ev_consumed[k], cudaEventDisableTiming), "event");
+        }
         check(cudaEventCreateWithFlags(&g->ev_done, cudaEventDisableTiming), "event");
         gpus_.push_back(std::move(g));
     }
@@ -394,7 +424,7 @@ void Session::alloc_buffers() {
         for (int i = L - 1; i >= 1 && !off; --i) {
             LayerInfo& li = net_.info[i];
             if (li.kind != 1 || li.generic || li.im2col || li.H * li.W > 4 || li.in_units % 4 != 0 ||
-                li.ksz * li.ksz > 25 || cfg_.precision != 0)
+                li.ksz * li.ksz > 25 || cfg_.precision != 0 || li.special() || skip_source(i + 1))
                 continue;
             bool ok = true;
             for (int wi : layer_workers_[i + 1]) ok = ok && workers_[wi]->at(i + 1).u % 32 == 0;
@@ -438,6 +468,10 @@ void Session::alloc_buffers() {
     }
     if (!softmax)
         for (int wi : layer_workers_[L]) need[L].insert(workers_[wi]->gpu);
+    // a residual layer reads the shortcut source's full activation on its GPU
+    for (int l = 1; l <= L; ++l)
+        if (net_.info[l - 1].res_from > 0)
+            for (int wi : layer_workers_[l]) need[net_.info[l - 1].res_from].insert(workers_[wi]->gpu);
     for (auto& [l, set] : need)
         for (int ord : set) {
             Gpu& g = gpu_of(ord);
@@ -462,7 +496,11 @@ void Session::alloc_buffers() {
             g.loss_hist = static_cast<double*>(g.alloc(sizeof(double) * hist_cap_));
             g.acc_hist = static_cast<double*>(g.alloc(sizeof(double) * hist_cap_));
         }
-        if (g.needs_x) g.xstage = static_cast<double*>(g.alloc(sizeof(double) * b * net_.dims[0]));
+        if (g.needs_x) {
+            g.xstage = static_cast<double*>(g.alloc(sizeof(double) * b * net_.dims[0]));
+            g.xstage2 = static_cast<double*>(g.alloc(sizeof(double) * b * net_.dims[0]));
+        }
+        for (int k = 0; k < 2; ++k) g.lstage[k] = static_cast<int*>(g.alloc(sizeof(int) * b));
     }
     // shard weights, bias, error signals (+ conv pre-pool outputs / argmax)
     std::vector<float> tmp;
@@ -471,6 +509,9 @@ void Session::alloc_buffers() {
         Gpu& g = gpu_of(w.gpu);
         for (WLayer& wl : w.layers) {
             const LayerInfo& li = net_.info[wl.layer - 1];
+            if ((li.special() || skip_source(wl.layer)) && wl.u % 4 != 0)
+                throw std::invalid_argument("layer " + S(wl.layer) + ": residual-extension shards need a multiple of 4 "
+                                            "channels (shard of " + S(wl.u) + ")");
             const int hc = li.host_wcols();
             wl.ldw = li.kind ? li.dev_wcols() : ld_of(li.in_units);
             wl.W = static_cast<float*>(g.alloc(sizeof(float) * wl.u * wl.ldw));
@@ -480,11 +521,11 @@ void Session::alloc_buffers() {
                 const int q = li.dq();
                 wl.delta_img = static_cast<long long>(li.Ho() + 2 * q) * (li.Wo() + 2 * q) * wl.ldd;
                 const bool consumer_dense = wl.layer < L && net_.info[wl.layer].kind == 0;
-                if (li.pool == 2 || consumer_dense) {
+                if (li.pool == 2 || consumer_dense || li.special()) {
                     wl.ldu = ld_of(wl.u);
                     wl.U = static_cast<float*>(g.alloc(sizeof(float) * ring_rows_ * li.Ho() * li.Wo() * wl.ldu, true));
                 }
-                if (li.pool == 2)
+                if (li.pool == 2 && !li.pool_avg)
                     wl.argmax = static_cast<unsigned char*>(
                         g.alloc(static_cast<size_t>(ring_rows_) * li.Hq() * li.Wq() * wl.u, true));
                 if (li.dense_conv) {
@@ -901,7 +942,7 @@ void Session::build_ops() {
                     d.epi = EpiParams{};
                     d.epi.mode = EPI_STORE;
                     d.epi.bias = wl.bias;
-                    d.epi.relu = li.act == 1;
+                    d.epi.relu = li.act == 1 && !li.special();  // residual / avg: the activation follows the shortcut
                     const long long pix = static_cast<long long>(li.Ho()) * li.Wo();
                     if (wl.U != nullptr) {  // pre-pool output, then pool / relayout
                         d.epi.dst[d.epi.ndst++] = wl.U + so * pix * wl.ldu;
@@ -969,7 +1010,31 @@ void Session::build_ops() {
                     const double fl = li.dense_conv ? 2.0 * rows * pix * wl.u * li.H * li.W * li.in_units  // executed
                                                     : 2.0 * rows * pix * wl.u * li.ksz * li.ksz * li.in_units;
                     int op = add_op(w.gpu, w.sf, gemm_launch(&wl.p_fwd[j], &wl.d_fwd[j], w.sf), deps, nk(wl.p_fwd[j]), OP_FWD_GEMM, fl);
-                    if (wl.U != nullptr && !pool_fused) {
+                    if (wl.U != nullptr && !pool_fused && li.special()) {
+                        // residual extension: U + shortcut -> act -> (average pool) -> consumers
+                        ActLayout out = lay_[l];
+                        out.col0 = wl.lo;
+                        PoolDsts pd;
+                        for (int ord : dest_gpus) pd.ptr[pd.n++] = act_buf(ord, l) + so * img_elems(l);
+                        SkipSrc sk;
+                        std::vector<int> rdeps{op};
+                        if (li.res_from > 0) {
+                            const int sl = li.res_from;
+                            sk.a = act_buf(w.gpu, sl) + so * img_elems(sl);
+                            sk.lay = lay_[sl];
+                            sk.f = net_.info[sl - 1].Hq() / li.Ho();
+                            sk.C = net_.info[sl - 1].out_units;
+                            auto it = act_ready[sl][j].find(w.gpu);
+                            if (it != act_ready[sl][j].end()) rdeps.insert(rdeps.end(), it->second.begin(), it->second.end());
+                        }
+                        float* U = wl.U + so * pix * wl.ldu;
+                        const long long ldu = wl.ldu;
+                        const int Ho = li.Ho(), Wo = li.Wo(), u = wl.u, c0 = wl.lo, pool = li.pool, relu = li.act == 1;
+                        cudaStream_t st = w.sf;
+                        op = add_op(w.gpu, st, [=]() {
+                            return launch_residual_act(U, ldu, rows, Ho, Wo, u, c0, relu, pool, sk, out, pd, st);
+                        }, rdeps, 1, OP_POOL);
+                    } else if (wl.U != nullptr && !pool_fused) {
                         ActLayout out = lay_[l];
                         out.col0 = wl.lo;
                         PoolDsts pd;
@@ -1088,8 +1153,9 @@ void Session::build_ops() {
                 // destination sums them, routes through the pool argmax and
                 // masks by its ReLU into its padded error signal.
                 const int hw = lb.Hq() * lb.Wq();
+                const bool res_dest = lb.special() || skip_source(l - 1);  // residual-extension merge kernel
                 if (li.kind == 1 && !li.generic && !li.dense_conv && contrib.size() == 1 && dests.size() == 1 &&
-                    fuse_merge_) {
+                    fuse_merge_ && !res_dest) {
                     // one contributor, one destination: the merge (pool routing,
                     // ReLU mask, padded store) runs in the dgrad epilogue
                     Worker& w = *workers_[contrib[0]];
@@ -1185,7 +1251,7 @@ void Session::build_ops() {
                         // contributor: the whole merge (ReLU mask + bias partials, one
                         // partial row per (CTA, warp, position)) runs in the epilogue
                         const bool fused = direct && contrib.size() == 1 && fuse_merge_ && lb.pool == 1 &&
-                                           lb.dq() == 0 && d0.ldd == li.in_units && tf32;
+                                           lb.dq() == 0 && d0.ldd == li.in_units && tf32 && !res_dest;
                         if (fused) {
                             Worker& dw = *workers_[dests[0]];
                             d.epi.mode = relu_below ? EPI_MASK : EPI_STORE;
@@ -1316,8 +1382,38 @@ void Session::build_ops() {
                     cm.ldd = dl.ldd;
                     cudaStream_t st = dw.sb;
                     float* dbp = dl.partial + static_cast<long long>(j) * conv_merge_blocks() * dl.u;
-                    const int op = add_op(dw.gpu, st, [=]() { return launch_conv_merge(cm, dbp, st); }, dgrad_ops, 1,
-                                          OP_CONV_MERGE);
+                    int op;
+                    if (res_dest) {
+                        // average-pool routing and / or the shortcut term of the residual
+                        // layer reading this layer's output (added before the ReLU mask)
+                        SkipGrad sg;
+                        std::vector<int> mdeps = dgrad_ops;
+                        if (const int r = res_consumer(l - 1)) {
+                            const LayerInfo& lr = net_.info[r - 1];
+                            WLayer* src = nullptr;
+                            for (int wi : layer_workers_[r]) {
+                                WLayer& cand = workers_[wi]->at(r);
+                                if (cand.contributor && cand.lo <= dl.lo && dl.hi <= cand.hi) src = &cand;
+                            }
+                            if (src == nullptr)
+                                throw std::invalid_argument("layers " + S(l - 1) + "," + S(r) +
+                                                            ": residual shortcut crosses shard boundaries");
+                            sg.d = src->delta + so * src->delta_img;
+                            sg.ldd = src->ldd;
+                            sg.q = lr.dq();
+                            sg.hq = lr.Ho() + 2 * sg.q;
+                            sg.wq = lr.Wo() + 2 * sg.q;
+                            sg.f = lb.Hq() / lr.Ho();
+                            sg.c0 = dl.lo - src->lo;
+                            mdeps.insert(mdeps.end(), src->delta_ready[j].begin(), src->delta_ready[j].end());
+                        }
+                        const int pavg = lb.pool_avg;
+                        op = add_op(dw.gpu, st, [=]() { return launch_conv_merge_res(cm, pavg, sg, dbp, st); }, mdeps, 1,
+                                    OP_CONV_MERGE);
+                    } else {
+                        op = add_op(dw.gpu, st, [=]() { return launch_conv_merge(cm, dbp, st); }, dgrad_ops, 1,
+                                    OP_CONV_MERGE);
+                    }
                     dl.delta_ready[j] = {op};
                     dw.last_bwd[j] = std::max(dw.last_bwd[j], op);
                 }
@@ -1842,6 +1938,14 @@ void Session::validate_labels(const int* labels) const {
 }
 
 void Session::load_batch(const double* X64, const float* X32, const int* labels) {
+    stage_batch(X64, X32, labels, 0);
+    convert_staged(0, X64 != nullptr);
+}
+
+// Phase 1 of a batch load: the host batch (fp64 or fp32 rows, as given) and
+// its labels into device staging slot k on each GPU's copy stream, once the
+// batch that used slot k before has been converted out of it.
+void Session::stage_batch(const double* X64, const float* X32, const int* labels, int k) {
     validate_labels(labels);
     // accuracy() accepts binary labels only (tinynet.cpp:376-378); the
     // reference raises it from the history collector after the workers
@@ -1850,6 +1954,27 @@ void Session::load_batch(const double* X64, const float* X32, const int* labels)
     if (!cfg_.multiclass)
         for (int i = 0; i < cfg_.batch; ++i)
             if (labels[i] != 0 && labels[i] != 1) pending_acc_error_ = true;
+    const size_t n = static_cast<size_t>(cfg_.batch) * net_.dims[0];
+    for (auto& gp : gpus_) {
+        Gpu& g = *gp;
+        check(cudaSetDevice(g.ordinal), "cudaSetDevice");
+        check(cudaStreamWaitEvent(g.copy, g.ev_consumed[k], 0), "wait");
+        if (g.needs_x) {
+            void* dst = k ? g.xstage2 : g.xstage;
+            if (X64 != nullptr) check(cudaMemcpyAsync(dst, X64, sizeof(double) * n, cudaMemcpyHostToDevice, g.copy), "H2D X");
+            else check(cudaMemcpyAsync(dst, X32, sizeof(float) * n, cudaMemcpyHostToDevice, g.copy), "H2D X");
+        }
+        if (g.needs_labels)
+            check(cudaMemcpyAsync(g.lstage[k], labels, sizeof(int) * cfg_.batch, cudaMemcpyHostToDevice, g.copy),
+                  "H2D labels");
+        check(cudaEventRecord(g.ev_copied[k], g.copy), "record");
+    }
+}
+
+// Phase 2: staging slot k -> the step's input buffers (padded NHWC / im2col
+// rows / padded dense rows of X, the labels) on each GPU's main stream,
+// ordered after the previous step (whose first-layer weight gradient reads X).
+void Session::convert_staged(int k, bool is64) {
     const int I0 = net_.dims[0];
     const int b = cfg_.batch;
     Gpu& g0 = *gpus_[0];
@@ -1857,46 +1982,29 @@ void Session::load_batch(const double* X64, const float* X32, const int* labels)
         Gpu& g = *gp;
         check(cudaSetDevice(g.ordinal), "cudaSetDevice");
         if (g.ordinal != g0.ordinal) check(cudaStreamWaitEvent(g.main, g0.ev_done, 0), "wait");
+        check(cudaStreamWaitEvent(g.main, g.ev_copied[k], 0), "wait");
+        const double* x64 = is64 ? (k ? g.xstage2 : g.xstage) : nullptr;
+        const float* x32 = is64 ? nullptr : reinterpret_cast<const float*>(k ? g.xstage2 : g.xstage);
         if (g.needs_x && lay_[0].kind == 2) {
             const LayerInfo& c = net_.info[0];
-            float* x = g.act.at(0);
-            const size_t n = static_cast<size_t>(b) * I0;
-            if (X64 != nullptr) {
-                check(cudaMemcpyAsync(g.xstage, X64, sizeof(double) * n, cudaMemcpyHostToDevice, g.main), "H2D X");
-                check(launch_im2col_input(g.xstage, nullptr, b, c.H, c.W, c.in_units, c.ksz, c.pad, x, lay_[0].ld,
-                                          g.main), "im2col X");
-            } else {
-                float* st = reinterpret_cast<float*>(g.xstage);
-                check(cudaMemcpyAsync(st, X32, sizeof(float) * n, cudaMemcpyHostToDevice, g.main), "H2D X");
-                check(launch_im2col_input(nullptr, st, b, c.H, c.W, c.in_units, c.ksz, c.pad, x, lay_[0].ld, g.main),
-                      "im2col X");
-            }
+            check(launch_im2col_input(x64, x32, b, c.H, c.W, c.in_units, c.ksz, c.pad, g.act.at(0), lay_[0].ld, g.main),
+                  "im2col X");
         } else if (g.needs_x && lay_[0].kind == 0) {
             // conv input: host NHWC rows -> padded NHWC (zero border stays from allocation)
             const LayerInfo& c = net_.info[0];
-            float* x = g.act.at(0);
-            const size_t n = static_cast<size_t>(b) * I0;
-            if (X64 != nullptr) {
-                check(cudaMemcpyAsync(g.xstage, X64, sizeof(double) * n, cudaMemcpyHostToDevice, g.main), "H2D X");
-                check(launch_pad_input(g.xstage, nullptr, b, c.H, c.W, c.in_units, x, c.pad, lay_[0].ld, g.main),
-                      "pad X");
-            } else {
-                float* st = reinterpret_cast<float*>(g.xstage);
-                check(cudaMemcpyAsync(st, X32, sizeof(float) * n, cudaMemcpyHostToDevice, g.main), "H2D X");
-                check(launch_pad_input(nullptr, st, b, c.H, c.W, c.in_units, x, c.pad, lay_[0].ld, g.main), "pad X");
-            }
+            check(launch_pad_input(x64, x32, b, c.H, c.W, c.in_units, g.act.at(0), c.pad, lay_[0].ld, g.main), "pad X");
         } else if (g.needs_x) {
             float* x = g.act.at(0);
-            if (X64 != nullptr) {
-                check(cudaMemcpyAsync(g.xstage, X64, sizeof(double) * b * I0, cudaMemcpyHostToDevice, g.main), "H2D X");
-                check(launch_convert_f64(g.xstage, b, I0, x, ld_of(I0), g.main), "convert X");
+            if (is64) {
+                check(launch_convert_f64(x64, b, I0, x, ld_of(I0), g.main), "convert X");
             } else {
-                check(cudaMemcpy2DAsync(x, sizeof(float) * ld_of(I0), X32, sizeof(float) * I0, sizeof(float) * I0, b,
-                                        cudaMemcpyHostToDevice, g.main), "H2D X");
+                check(cudaMemcpy2DAsync(x, sizeof(float) * ld_of(I0), x32, sizeof(float) * I0, sizeof(float) * I0, b,
+                                        cudaMemcpyDeviceToDevice, g.main), "copy X");
             }
         }
         if (g.needs_labels)
-            check(cudaMemcpyAsync(g.labels, labels, sizeof(int) * b, cudaMemcpyHostToDevice, g.main), "H2D labels");
+            check(cudaMemcpyAsync(g.labels, g.lstage[k], sizeof(int) * b, cudaMemcpyDeviceToDevice, g.main), "labels");
+        check(cudaEventRecord(g.ev_consumed[k], g.main), "record");
         check(cudaEventRecord(g.ev_loaded, g.main), "record");
         if (g.ordinal != g0.ordinal) {
             check(cudaSetDevice(g0.ordinal), "cudaSetDevice");
@@ -1963,11 +2071,11 @@ void Session::history(double* loss, double* acc, int cap, int* count) {
     if (count) *count = n;
 }
 
-double Session::step_host(const float* X, const int* labels) {
-    load_batch(nullptr, X, labels);
+double Session::step_host(const double* X64, const float* X32, const int* labels) {
+    load_batch(X64, X32, labels);
     step(1);
     Gpu& g = gpu_of(main_gpu_);
-    if (loss_pinned_ == nullptr) check(cudaMallocHost(&loss_pinned_, sizeof(double)), "pinned loss");
+    if (loss_pinned_ == nullptr) check(cudaMallocHost(&loss_pinned_, 2 * sizeof(double)), "pinned loss");
     check(cudaSetDevice(g.ordinal), "cudaSetDevice");
     if (g.ordinal != gpus_[0]->ordinal) check(cudaStreamWaitEvent(g.main, gpus_[0]->ev_done, 0), "wait");
     check(cudaMemcpyAsync(loss_pinned_, g.loss_hist + (steps_enqueued_ - 1) % hist_cap_, sizeof(double),
@@ -1975,6 +2083,34 @@ double Session::step_host(const float* X, const int* labels) {
           "D2H loss");
     check(cudaStreamSynchronize(g.main), "sync");
     return *loss_pinned_;
+}
+
+// Streaming entry: batch t is staged into slot t % 2 on the copy streams
+// while step t - 1 still runs, converted and stepped behind it, and its loss
+// read back asynchronously; returns the loss of step t - 1 (NaN on the first
+// call of a stream), so at most two steps are in flight and the host -> device
+// copy of the next batch overlaps the current step.
+double Session::step_host_pipelined(const double* X64, const float* X32, const int* labels) {
+    Gpu& g = gpu_of(main_gpu_);
+    if (loss_pinned_ == nullptr) check(cudaMallocHost(&loss_pinned_, 2 * sizeof(double)), "pinned loss");
+    if (ev_loss_[0] == nullptr) {
+        check(cudaSetDevice(g.ordinal), "cudaSetDevice");
+        for (auto& e : ev_loss_) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    }
+    const int k = stream_steps_ & 1;
+    stage_batch(X64, X32, labels, k);
+    convert_staged(k, X64 != nullptr);
+    step(1);
+    check(cudaSetDevice(g.ordinal), "cudaSetDevice");
+    if (g.ordinal != gpus_[0]->ordinal) check(cudaStreamWaitEvent(g.main, gpus_[0]->ev_done, 0), "wait");
+    check(cudaMemcpyAsync(loss_pinned_ + k, g.loss_hist + (steps_enqueued_ - 1) % hist_cap_, sizeof(double),
+                          cudaMemcpyDeviceToHost, g.main),
+          "D2H loss");
+    check(cudaEventRecord(ev_loss_[k], g.main), "record");
+    ++stream_steps_;
+    if (stream_steps_ == 1) return std::nan("");
+    check(cudaEventSynchronize(ev_loss_[k ^ 1]), "loss of the previous step");
+    return loss_pinned_[k ^ 1];
 }
 
 double Session::last_loss() {

@@ -34,6 +34,12 @@ struct LayerInfo {
     int in_units = 0, out_units = 0;
     int act = 0;
     int H = 1, W = 1, ksz = 1, pad = 0, pool = 1;  // conv: input grid, kernel, padding, pool factor (1|2)
+    // residual extension (kernels.h SkipSrc): q += shortcut(a_res_from) before
+    // the activation (1-based layer, 0 = none); pool_avg: p x p average pool
+    // (p = pool, e.g. the global 4x4 pool of a ResNet) instead of 2x2 max
+    int res_from = 0;
+    int pool_avg = 0;
+    bool special() const { return res_from > 0 || pool_avg; }  // residual-extension forward / merge kernels
     bool im2col = false;  // first layer with few input channels: explicit im2col rows, dense GEMMs
     // generic conv (grids the 128/32-pixel TMA boxes cannot tile): per-step
     // im2col rows of the padded input, dense GEMMs, col2im of the dgrad partial
@@ -130,7 +136,8 @@ class Session {
     // stream role (0 forward, 1 input-gradient, 2 weight-gradient, 3 main)
     int op_meta(int* mb, int* device, int* role, int cap);
     double last_loss();
-    double step_host(const float* X, const int* labels);  // load + one step + loss, one stream sync
+    double step_host(const double* X64, const float* X32, const int* labels);  // load + one step + loss, one sync
+    double step_host_pipelined(const double* X64, const float* X32, const int* labels);  // returns step t-1's loss
 
   private:
     struct Gpu;
@@ -171,6 +178,13 @@ class Session {
         return ring_ == cfg_.m ? mb_off_[j] : static_cast<long long>(j % ring_) * mb_sizes_[0];
     }
     long long aoff(int l, int j) const { return l == 0 ? mb_off_[j] : soff(j); }
+    // residual extension: the layer whose shortcut reads layer s's output (0: none)
+    int res_consumer(int s) const {
+        for (int l = 1; l <= net_.L(); ++l)
+            if (net_.info[l - 1].res_from == s) return l;
+        return 0;
+    }
+    bool skip_source(int s) const { return res_consumer(s) > 0; }
     void check(cudaError_t e, const char* what);
     void validate_labels(const int* labels) const;
 
@@ -202,7 +216,11 @@ class Session {
     int cur_layer_ = 0, cur_info_ = 0, cur_mb_ = -1;
     bool serialise_ = true;
     std::vector<double> last_op_ms_;
-    double* loss_pinned_ = nullptr;  // pinned host slot for step_host's loss read-back
+    double* loss_pinned_ = nullptr;  // pinned host slots for step_host's loss read-back
+    cudaEvent_t ev_loss_[2] = {nullptr, nullptr};
+    int stream_steps_ = 0;
+    void stage_batch(const double* X64, const float* X32, const int* labels, int k);
+    void convert_staged(int k, bool is64);
     std::vector<double> last_op_start_;  // ms from the first timed op (same device), last profile iteration
 };
 

@@ -1,0 +1,55 @@
+"""Physical multi-GPU data plane (skipped with fewer GPUs than a test needs;
+every other test maps all plan devices onto cuda:0).
+
+With plan devices on distinct GPUs the same step runs with the epilogue
+all-gather storing into PEER buffers over NVLink (TMA tensor-map stores and
+st.global to peer-mapped pointers), the dgrad epilogues writing peer slots,
+cross-device CUDA-event edges inside the multi-device graph, and the hub
+cudaMemcpyPeerAsync of concat boundaries.  The arithmetic is identical to the
+one-GPU run of the same plan (same kernels, same reduction order), so the
+results must be bitwise equal."""
+import numpy as np
+import pytest
+
+from paper_2207_11019_b200 import api, configs
+from paper_2207_11019_b200.api import PartitionedTrainOptions, TrainConfig, UpdateMode
+
+pytestmark = pytest.mark.gpu
+
+
+def _need(k):
+    if api.device_count() < k:
+        pytest.skip(f"needs {k} GPUs (this box has {api.device_count()})")
+
+
+def _run(net, X, y, plan, dev_map, m=1, memory="stash_all"):
+    s = api.Session(api.Context(dev_map), net, X.shape[0], plan, m, UpdateMode.async_per_module,
+                    TrainConfig(alpha0=1e-2, decay=1e-2, iterations=1),
+                    PartitionedTrainOptions(multiclass_accuracy=True, memory_mode=memory))
+    s.load_batch(X, y)
+    s.step(3)
+    s.sync()
+    W, b = s.get_net().pack()
+    lh, _ = s.history()
+    return W, b, lh
+
+
+@pytest.mark.parametrize("k", [2, 4, 8])
+@pytest.mark.parametrize("net_name", ["small_cnn", "mlp", "small_resnet"])
+def test_peer_data_plane_matches_one_gpu(k, net_name):
+    _need(k)
+    rng = np.random.default_rng(0)
+    if net_name == "small_cnn":
+        net = configs.small_cnn(seed=2, hw=16, widths=(32, "M", 64, "M"))
+        X = rng.standard_normal((32, 16 * 16 * 3)).astype(np.float32)
+    elif net_name == "small_resnet":
+        net = configs.small_resnet(seed=3, hw=8, widths=(32, 64), blocks=(1, 1))
+        X = rng.standard_normal((32, 8 * 8 * 3)).astype(np.float32)
+    else:
+        net = configs.dense_net([256, 512, 512, 10], [1, 1, 2], seed=4)
+        X = rng.standard_normal((64, 256)).astype(np.float32)
+    y = rng.integers(0, 10, X.shape[0])
+    for plan, m, mem in ((api.build_plan(net, k, 1), 1, "stash_all"), (api.build_plan(net, k, 2), 2, "proposed")):
+        a = _run(net, X, y, plan, list(range(k)), m, mem)
+        b = _run(net, X, y, plan, [0] * k, m, mem)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])

@@ -108,7 +108,10 @@ def test_executor_order_respects_the_reference_gate_and_ring(tmp_path, groups, m
     s.profile(1)
     ours = {}
     for o, mt in zip(s.profile_ops(), s.op_meta()):
-        if mt["mb"] < 0 or mt["device"] == 0 or mt["role"] not in ("forward", "backward"):
+        # B(i, j): input gradients / merges and, under the proposed policy, the
+        # micro-batch's weight gradients (a module of only the first layer has
+        # no input gradient)
+        if mt["mb"] < 0 or mt["device"] == 0 or mt["role"] == "main":
             continue
         mod = next(sm.index for sm in plan.submodules if sm.first_layer <= o["layer"] <= sm.last_layer)
         key = "%s%d.%d" % ("F" if mt["role"] == "forward" else "B", mod, mt["mb"] + 1)

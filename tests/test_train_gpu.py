@@ -320,3 +320,30 @@ def test_proposed_memory_rejects_fp32_mode():
         api.train_partitioned(net, Batch(X, y), TrainConfig(iterations=1), api.build_plan(g["dims"], 2, 1), 2,
                               UpdateMode.sync_barrier, PartitionedTrainOptions(precision="fp32", memory_mode="proposed"),
                               device_map=[0, 0])
+
+
+def test_streaming_host_steps_match_blocking():
+    """ppb_session_step_host_pipelined (double-buffered staging, returns the
+    previous step's loss) computes exactly what the blocking step_host /
+    step_host_f64 calls compute, batch after batch (fp32 and fp64 rows)."""
+    g, O, W, b, X, y = _mlp()
+    net = TinyNet.unpack(g["dims"], g["acts"], W, b)
+    plan = api.build_plan(g["dims"], 2, 1)
+    rng = np.random.default_rng(3)
+    batches = [(rng.standard_normal(X.shape).astype(np.float32), rng.integers(0, 2, X.shape[0]).astype(np.int32))
+               for _ in range(5)]
+
+    def session():
+        return api.Session(api.Context([0, 0]), net, X.shape[0], plan, 2, UpdateMode.async_per_module,
+                           TrainConfig(alpha0=0.05, decay=0.01, iterations=1), PartitionedTrainOptions())
+
+    for dtype in (np.float32, np.float64):
+        a, p = session(), session()
+        blocking = [(a.step_host if dtype == np.float32 else a.step_host_f64)(Xb.astype(dtype), yb)
+                    for Xb, yb in batches]
+        streamed = [p.step_host_pipelined(Xb.astype(dtype), yb) for Xb, yb in batches]
+        p.sync()
+        lh, _ = p.history()
+        assert np.isnan(streamed[0])
+        assert streamed[1:] == blocking[:-1] and lh[-1] == blocking[-1], (streamed, blocking)
+        assert np.array_equal(a.get_net().pack()[0], p.get_net().pack()[0])

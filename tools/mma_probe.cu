@@ -148,6 +148,62 @@ __global__ void __launch_bounds__(128, 1) probe2_kernel(int kb, int iters, unsig
     if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
+
+// probe3: cheap issue.  Descriptors computed once (64-bit base + constant
+// start-address steps), GROUP k-blocks (4 * GROUP MMAs) per elect region.
+template <int N, int GROUP>
+__global__ void __launch_bounds__(128, 1) probe3_kernel(int kb, int iters, unsigned long long* cycles) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint32_t tmem_slot;
+    __shared__ __align__(8) uint64_t done_bar;
+    const int warp = threadIdx.x / 32;
+    uint8_t* A = smem;
+    uint8_t* B = smem + kb * 16384;
+    for (int i = threadIdx.x; i < kb * (16384 + N * 128) / 4; i += blockDim.x)
+        reinterpret_cast<float*>(smem)[i] = 0.001f * (i % 97);
+    if (warp == 0) tmem_alloc(&tmem_slot, 512);
+    if (threadIdx.x == 0) {
+        mbar_init(&done_bar, 1);
+        fence_mbar_init();
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_slot;
+    constexpr uint32_t idesc = idesc_tf32(N, false, false);
+    if (warp == 1) {
+        long long t0 = 0;
+        if (elect_one()) t0 = clock64();
+        const uint64_t a0 = umma_desc(smem_u32(A), 16, 1024), b0 = umma_desc(smem_u32(B), 16, 1024);
+        for (int it = 0; it < iters; ++it) {
+            for (int k = 0; k < kb; k += GROUP) {
+                if (elect_one()) {
+#pragma unroll
+                    for (int g = 0; g < GROUP; ++g) {
+#pragma unroll
+                        for (int s = 0; s < 4; ++s) {
+                            const uint64_t ad = a0 + static_cast<uint64_t>(((k + g) * 16384 + s * 32) >> 4);
+                            const uint64_t bd = b0 + static_cast<uint64_t>(((k + g) * N * 128 + s * 32) >> 4);
+                            mma_tf32(tmem, ad, bd, idesc, (it | k | g | s) != 0 ? 1u : 0u);
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        if (elect_one()) {
+            mma_commit(&done_bar);
+            mbar_wait(&done_bar, 0);
+            cycles[blockIdx.x] = clock64() - t0;
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
 }  // namespace
 
 extern "C" int mma_probe(int n, int mode, int kb, int iters, int ctas, unsigned long long* cycles, void* stream) {
@@ -182,5 +238,18 @@ extern "C" int mma_probe2(int n, int nacc, int kb, int iters, int ctas, unsigned
     }
     P2(64, 1) P2(64, 2) P2(64, 4) P2(128, 1) P2(128, 2) P2(128, 4) P2(256, 1) P2(256, 2)
 #undef P2
+    return -1;
+}
+
+extern "C" int mma_probe3(int n, int group, int kb, int iters, int ctas, unsigned long long* cycles) {
+    const int smem = 1024 + kb * (16384 + n * 128);
+#define P3(NN, GG)                                                                                   \
+    if (n == NN && group == GG) {                                                                    \
+        cudaFuncSetAttribute(probe3_kernel<NN, GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+        probe3_kernel<NN, GG><<<ctas, 128, smem>>>(kb, iters, cycles);                               \
+        return static_cast<int>(cudaGetLastError());                                                 \
+    }
+    P3(64, 1) P3(64, 2) P3(64, 4) P3(128, 1) P3(128, 2) P3(128, 4) P3(256, 1)
+#undef P3
     return -1;
 }

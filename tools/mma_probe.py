@@ -59,8 +59,29 @@ def main2():
                                   "frac_of_2048": 128 * n * 32 / (c / (kb * iters)) / 2048}))
 
 
+def main3():
+    """probe3: descriptors as base + constant steps, GROUP k-blocks (4 x GROUP
+    back-to-back MMAs) per elect region."""
+    lib = C.CDLL(os.path.join(HERE, "_mma_probe.so"))
+    lib.mma_probe3.argtypes = [C.c_int] * 5 + [C.c_void_p]
+    ctas = torch.cuda.get_device_properties(0).multi_processor_count
+    cyc = torch.zeros(ctas, dtype=torch.int64, device="cuda")
+    kb, iters = 4, 2000
+    for n, grp in ((64, 1), (64, 2), (64, 4), (128, 1), (128, 2), (128, 4), (256, 1)):
+        for rep in range(2):
+            rc = lib.mma_probe3(n, grp, kb, iters, ctas, C.c_void_p(cyc.data_ptr()))
+            torch.cuda.synchronize()
+            c = cyc.double().mean().item()
+            if rc == 0 and rep == 1:
+                print(json.dumps({"probe": "cheap-issue", "n": n, "kblocks_per_issue": grp,
+                                  "cycles_per_mma": c / (kb * iters * 4),
+                                  "frac_of_2048": 128 * n * 32 / (c / (kb * iters)) / 2048}))
+
+
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "2":
+    if len(sys.argv) > 1 and sys.argv[1] == "3":
+        main3()
+    elif len(sys.argv) > 1 and sys.argv[1] == "2":
         main2()
     else:
         main()

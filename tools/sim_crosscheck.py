@@ -107,7 +107,7 @@ def measure(net, X, y, plan, n, m, gate, memory):
             continue
         fwd = mt["role"] == "forward" or (mt["role"] == "main" and o["kind"] in ("loss_head", "pool_relayout"))
         (tf if fwd else tb)[i][j] += o["ms"] * 1e-3
-        if mt["device"] > 0 and mt["role"] in ("forward", "backward"):
+        if mt["device"] > 0 and mt["role"] != "main":
             key = ("F" if fwd else "B", i + 1, j + 1)
             seq = order.setdefault(mt["device"], [])
             if key not in seq:
