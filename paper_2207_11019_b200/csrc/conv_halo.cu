@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             epi_bar_sync();
         }
         int local = 0;
+        int msel = 0;  // staging box of the next masked chunk (alternates with ts.dbuf)
         for (int tile = unit; tile < num_tiles; tile += units, ++local) {
             const long long p0 = static_cast<long long>(tile % num_m) * TM + static_cast<long long>(rank) * kBM;
             const int n0 = (tile / num_m) * BN;
@@ -295,9 +296,12 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 if (hh >= 1 && hh <= hg.ho && ww >= 1 && ww <= hg.wo) m = (img * hg.ho + hh - 1) * hg.wo + ww - 1;
             }
             // the first chunk's ReLU-mask box is loaded while the tile's MMAs run
+            // (with two staging boxes per warp, while the previous chunk's store
+            // still reads the other box)
             const bool masked = ts.n && ts.mask;
-            if (masked && half < BN / 32)
-                tma_mask_issue(ts, stg + (warp - 4) * 4096, mbar, lane, static_cast<int>(p0) + q * 32, n0 + half * 32);
+            if (masked && ts.mask_pf && half < BN / 32)
+                tma_mask_issue(ts, epi_box(stg, warp - 4, msel), mbar, lane, static_cast<int>(p0) + q * 32,
+                               n0 + half * 32, false, ts.dbuf);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
 #pragma unroll 1
@@ -309,11 +313,13 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = m >= 0 ? __uint_as_float(rr[i]) : 0.f;
                 if (masked) {  // the mask is zero on the ring
-                    if (c != half)
-                        tma_mask_issue(ts, stg + (warp - 4) * 4096, mbar, lane, static_cast<int>(p0) + q * 32,
-                                       n0 + c * 32);
-                    tma_store_masked_issued(ts, stg + (warp - 4) * 4096, mbar, mphase, lane, v,
-                                            static_cast<int>(p0) + q * 32, n0 + c * 32);
+                    uint8_t* box = epi_box(stg, warp - 4, msel);
+                    if (c != half || !ts.mask_pf)
+                        tma_mask_issue(ts, box, mbar, lane, static_cast<int>(p0) + q * 32, n0 + c * 32, false,
+                                       ts.dbuf);
+                    tma_store_masked_issued(ts, box, mbar, mphase, lane, v, static_cast<int>(p0) + q * 32,
+                                            n0 + c * 32);
+                    msel ^= ts.dbuf;
                 } else if (ts.n) {  // pad-ring rows store zeros (the destination's own ring)
                     epi_values32(epi, m, n0 + c * 32, v, lane);
                     if (m < 0) {
@@ -509,12 +515,21 @@ bool halo_conv_prepare(const GemmDesc& d, TcGemmPlan* out, int force, char* err,
         const int db_need = p.epi.db_partial != nullptr ? 4 * ((d.N + 31) / 32 * 32) * 4 : 0;
         const bool tma = tma_store_setup(p.epi, d.M, d.N, &hg, &p.ts);
         int extra = db_need;
+        const bool one_col = d.N <= bn;
         if (tma) {
             p.ts.stage_off = 1024 + (db_need + 1023) / 1024 * 1024;
             extra = p.ts.stage_off - 1024 + kEpiStageBytes;
+            // masked merge: two staging boxes per warp (the next chunk's mask load
+            // does not wait for the previous chunk's store) when the resident B
+            // slice still fits next to 3 halo stages
+            const int extra2 = p.ts.stage_off - 1024 + kEpiStageBytesDbuf;
+            if (p.ts.mask && one_col && !dev_knob("PPB_NO_MASK_DBUF") &&
+                nkb * stage_b + 3 * hg.hstage_bytes <= kHaloSmemMax - kHaloReserve - extra2) {
+                p.ts.dbuf = 1;
+                extra = extra2;
+            }
         }
         const int avail = kHaloSmemMax - kHaloReserve - extra;
-        const bool one_col = d.N <= bn;
         if (one_col && nkb * stage_b + 2 * hg.hstage_bytes <= avail && !getenv("PPB_HALO_STREAM_B")) {
             hg.resident = 1;
             hg.bstages = nkb;

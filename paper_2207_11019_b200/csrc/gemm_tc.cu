@@ -219,6 +219,7 @@ static bool tma_store_setup_pool2(const EpiParams& e, int M, int N, TmaStore* ts
 }
 
 bool tma_store_setup(const EpiParams& e, int M, int N, const HaloGeom* hg, TmaStore* ts) {
+    ts->mask_pf = dev_knob("PPB_NO_MASK_PREFETCH") ? 0 : 1;  // A/B switch (DEV builds)
     ts->n = 0;
     ts->pool2 = 0;
     static const bool off = [] {

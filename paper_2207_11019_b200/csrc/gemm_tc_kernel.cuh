@@ -422,7 +422,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             // masked epilogues: the first chunk's ReLU-mask box is loaded while
             // the tile's MMAs run (its latency was exposed once per tile)
             const bool masked = ts.n && ts.mask && !(sk.splits > 1 || sk.partial) && !(epi.dbg & 4);
-            if (masked && c_first < BN / 32)
+            const bool pf = masked && ts.mask_pf;
+            if (pf && c_first < BN / 32)
                 tma_mask_issue(ts, stg + (warp - 4) * 4096, mbar, lane, m0 + q * 32, n0 + c_first * 32, ts.pool2 != 0);
             mbar_wait(&tfull_bar[acc], acc_phase);
             tc_fence_after();
@@ -455,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (ts.n && ts.pool2) {
                         uint8_t* buf = stg + (warp - 4) * 4096;
                         if (ts.mask) {
-                            if (c != c_first) tma_mask_issue(ts, buf, mbar, lane, m0 + q * 32, n0 + c * 32, true);
+                            if (c != c_first || !pf) tma_mask_issue(ts, buf, mbar, lane, m0 + q * 32, n0 + c * 32, true);
                             tma_mask_apply_issued(buf, mbar, mphase, lane, v);
                         }
                         uint32_t code[8];
@@ -465,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int i = 0; i < 8; ++i) code[i] = m < M ? __ldg(reinterpret_cast<const uint32_t*>(ap) + i) : 0u;
                         tma_merge_pool2_chunk(ts, buf, lane, v, code, m0 + q * 32, n0 + c * 32);
                     } else if (ts.n && ts.mask) {
-                        if (c != c_first) tma_mask_issue(ts, stg + (warp - 4) * 4096, mbar, lane, m0 + q * 32, n0 + c * 32);
+                        if (c != c_first || !pf) tma_mask_issue(ts, stg + (warp - 4) * 4096, mbar, lane, m0 + q * 32, n0 + c * 32);
                         tma_store_masked_issued(ts, stg + (warp - 4) * 4096, mbar, mphase, lane, v, m0 + q * 32,
                                                 n0 + c * 32);
                     } else if (ts.n && epi.pl_on == 3) {

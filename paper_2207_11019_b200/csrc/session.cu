@@ -116,6 +116,7 @@ struct Session::WLayer {
 struct Session::Worker {
     int module = 0, device = 0, rank = 0, gpu = 0;
     cudaStream_t sf = nullptr, sb = nullptr, su = nullptr;
+    cudaStream_t su2 = nullptr;  // second weight-gradient stream (alternate layers; see build_ops)
     std::vector<WLayer> layers;  // span order
     std::vector<int> last_bwd;   // [j] latest backward-side op of this worker
     WLayer& at(int layer) { return layers[layer - layers.front().layer]; }
@@ -141,6 +142,10 @@ float* Session::act_buf(int ordinal, int layer) {
 }
 
 float* Session::q_buf(int ordinal) { return gpu_of(ordinal).q; }
+
+// two weight-gradient streams: 2.293 vs 2.317 ms on the VGG-16 step (3 A/B
+// pairs on one box); PPB_WGRAD_ONE_STREAM=1 (DEV builds) restores one
+bool Session::wgrad_two_streams() { return !dev_knob("PPB_WGRAD_ONE_STREAM"); }
 
 size_t Session::device_bytes() const {
     size_t n = 0;
@@ -305,6 +310,7 @@ Session::~Session() {
         cudaStreamDestroy(w->sf);
         cudaStreamDestroy(w->sb);
         cudaStreamDestroy(w->su);
+        cudaStreamDestroy(w->su2);
     }
     for (auto& g : gpus_) {
         cudaSetDevice(g->ordinal);
@@ -381,6 +387,7 @@ void Session::build() {
             check(cudaStreamCreateWithPriority(&w->sf, cudaStreamNonBlocking, prio_hi), "stream");
             check(cudaStreamCreateWithPriority(&w->sb, cudaStreamNonBlocking, prio_hi), "stream");
             check(cudaStreamCreateWithPriority(&w->su, cudaStreamNonBlocking, prio_lo), "stream");
+            check(cudaStreamCreateWithPriority(&w->su2, cudaStreamNonBlocking, prio_lo), "stream");
             for (int l = sm.first_layer; l <= sm.last_layer; ++l) {
                 const Shard& s = sm.layer_shards(l)[r];
                 WLayer wl;
@@ -1563,12 +1570,28 @@ void Session::build_ops() {
         // next wgrad GEMM on the stream (SideJob) instead of its own kernel
         // pending side job: the previous split-K wgrad's reduction, or the
         // previous dense-conv layer's weight update (its op is then a no-op)
-        TcGemmPlan* prev_plan = nullptr;
-        int prev_op = -1;
-        SideJob pend_fold;
-        bool* pend_flag = nullptr;
-        int pend_fold_op = -1;
+        // two weight-gradient streams (alternate layers) so independent wgrads of
+        // the bottom layers -- which all become ready at the end of the dgrad
+        // chain -- overlap instead of queueing; each stream keeps its own
+        // side-job chain
+        static const bool two_su = wgrad_two_streams();
+        struct Chain {
+            TcGemmPlan* prev_plan = nullptr;
+            WLayer* prev_wl = nullptr;
+            int prev_op = -1;
+            SideJob pend_fold;
+            bool* pend_flag = nullptr;
+            int pend_fold_op = -1;
+        } chains[2];
+        int ci = 0;  // chain of the layer being built
+        WLayer* cur_wl = nullptr;
         auto link_side = [&](TcGemmPlan* p, int op, bool carrier_ok) {
+            TcGemmPlan*& prev_plan = chains[ci].prev_plan;
+            WLayer*& prev_wl = chains[ci].prev_wl;
+            int& prev_op = chains[ci].prev_op;
+            SideJob& pend_fold = chains[ci].pend_fold;
+            bool*& pend_flag = chains[ci].pend_flag;
+            int& pend_fold_op = chains[ci].pend_fold_op;
             if (!tf32) return;
             const bool can = carrier_ok && !no_side && p->halo == 0;
             if (pend_flag != nullptr) {
@@ -1578,7 +1601,8 @@ void Session::build_ops() {
                     ops_[pend_fold_op].kernels -= 1;
                 }
             } else if (prev_plan != nullptr && can && prev_plan->sk.splits > 1 && !prev_plan->sk.fixup &&
-                       !prev_plan->sk.deferred) {
+                       !prev_plan->sk.deferred &&
+                       !(prev_wl != nullptr && net_.info[prev_wl->layer - 1].dense_conv)) {  // its fold reads dWx
                 p->sj.on = 1;
                 static const bool side_scalar = getenv("PPB_SIDE_SCALAR") != nullptr;
                 p->sj.scalar = side_scalar ? 1 : 0;
@@ -1588,10 +1612,24 @@ void Session::build_ops() {
                 p->sj.epi = prev_plan->epi;
                 prev_plan->sk.deferred = 1;
                 ops_[prev_op].kernels -= 1;
+                // the deferred GEMM now writes only its split-K workspace: it no
+                // longer waits for its layer's dgrad (which reads W); the update
+                // rides in this GEMM, which follows that dgrad through its own
+                // error signal (produced after it)
+                // opt-in (DEV builds, PPB_WGRAD_EARLY=1): measured equal on the VGG-16 step
+                // (2.303 vs 2.306 ms, 3 A/B pairs): the early wgrad only contends with
+                // the dgrad for L2 bandwidth
+                static const bool strict = !dev_knob("PPB_WGRAD_EARLY");
+                if (prev_wl != nullptr && !strict) {
+                    auto& dv = ops_[prev_op].deps;
+                    for (int dg : prev_wl->dgrad_op)
+                        if (dg >= 0) dv.erase(std::remove(dv.begin(), dv.end(), dg), dv.end());
+                }
             }
             pend_flag = nullptr;
             prev_plan = p;
             prev_op = op;
+            prev_wl = cur_wl;
         };
         for (auto wit = w.layers.rbegin(); wit != w.layers.rend(); ++wit) {
             WLayer& wl = *wit;
@@ -1613,7 +1651,12 @@ void Session::build_ops() {
                 if (wl.dgrad_op[j] >= 0) deps.push_back(wl.dgrad_op[j]);
             }
             if (bwd_join >= 0) deps.push_back(bwd_join);
-            cudaStream_t s = w.su;
+            ci = two_su ? (l & 1) : 0;
+            cur_wl = &wl;
+            cudaStream_t s = ci ? w.su2 : w.su;
+            SideJob& pend_fold = chains[ci].pend_fold;
+            bool*& pend_flag = chains[ci].pend_flag;
+            int& pend_fold_op = chains[ci].pend_fold_op;
             const float* delta = wl.delta;
             const long long ldd = wl.ldd;
             const int b = static_cast<int>(bias_rows), u = wl.u;
@@ -1693,6 +1736,31 @@ void Session::build_ops() {
             const int gop = add_op(w.gpu, s, gemm_launch(&wl.p_wgrad, &wl.d_wgrad, s), {bop}, nk(wl.p_wgrad),
                                    OP_WGRAD_GEMM, wfl);
             link_side(&wl.p_wgrad, gop, true);
+        }
+        // the last split-K wgrad of each stream has no carrier: its GEMM still
+        // runs as soon as its error signal exists (concurrently with its own
+        // layer's dgrad, which reads W) and the reduction + update follows both
+        // opt-in (DEV builds, PPB_WGRAD_EARLY=1): measured equal on the VGG-16 step
+                // (2.303 vs 2.306 ms, 3 A/B pairs): the early wgrad only contends with
+                // the dgrad for L2 bandwidth
+                static const bool strict = !dev_knob("PPB_WGRAD_EARLY");
+        for (Chain& c : chains) {
+            TcGemmPlan* pp = c.prev_plan;
+            if (strict || !tf32 || pp == nullptr || c.prev_wl == nullptr || pp->sk.splits <= 1 || pp->sk.fixup ||
+                pp->sk.deferred || net_.info[c.prev_wl->layer - 1].dense_conv)
+                continue;
+            pp->sk.deferred = 1;
+            ops_[c.prev_op].kernels -= 1;
+            auto& dv = ops_[c.prev_op].deps;
+            std::vector<int> rdeps{c.prev_op};
+            for (int dg : c.prev_wl->dgrad_op)
+                if (dg >= 0) {
+                    dv.erase(std::remove(dv.begin(), dv.end(), dg), dv.end());
+                    rdeps.push_back(dg);
+                }
+            cur_layer_ = c.prev_wl->layer;
+            cudaStream_t s = ops_[c.prev_op].stream;
+            add_op(w.gpu, s, [pp, s]() { return tc_gemm_launch_reduce(*pp, s); }, rdeps, 1, OP_BIAS);
         }
     }
 
@@ -1861,6 +1929,7 @@ int Session::op_meta(int* mb, int* device, int* role, int cap) {
         who[w->sf] = {w->device, 0};
         who[w->sb] = {w->device, 1};
         who[w->su] = {w->device, 2};
+        who[w->su2] = {w->device, 2};
     }
     int k = 0;
     for (int i = 0; i < static_cast<int>(ops_.size()); ++i) {

@@ -185,6 +185,7 @@ class Session {
         return 0;
     }
     bool skip_source(int s) const { return res_consumer(s) > 0; }
+    static bool wgrad_two_streams();
     void check(cudaError_t e, const char* what);
     void validate_labels(const int* labels) const;
 

@@ -49,6 +49,7 @@ struct TmaStore {
     int mask = 0;
     CUtensorMap mmap;
     int dbuf = 0;  // two staging boxes per warp (plain stores / split-K partials only)
+    int mask_pf = 1;  // masked epilogues: issue the first chunk's mask load before the accumulator wait
 };
 
 // The staging box of epilogue warp `ewarp` for its `sel`-th buffer.
@@ -116,9 +117,9 @@ __device__ __forceinline__ uint64_t* epi_mask_bar(uint8_t* stage_base, int ewarp
 // read it (lane 0).  Split from tma_store_chunk_masked so an epilogue can
 // issue it before waiting for the accumulator and hide its latency.
 __device__ __forceinline__ void tma_mask_issue(const TmaStore& ts, uint8_t* buf, uint64_t* bar, int lane, int r0,
-                                               int n, bool rank4 = false) {
+                                               int n, bool rank4 = false, int dbuf = 0) {
     if (lane == 0) {
-        bulk_wait_read<0>();  // the previous store has read the box
+        box_wait(dbuf);  // the previous store from this box has read it
         mbar_arrive_expect_tx(bar, 4096);
         if (ts.rank == 2 && !rank4) {
             tma_load_2d(buf, &ts.mmap, bar, n, r0);
