@@ -543,6 +543,12 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
             }
         }
     }
+    // A/B probe (DEV builds): CTA-pair tiles for narrow wgrads (fewer M tiles,
+    // so the error signal is re-read fewer times through L2)
+    if (force_bn == 0 && cg == 1 && bn == 64 && d.epi.mode == EPI_SGD && d.M > 128 && dev_knob("PPB_WGRAD_PAIR")) {
+        cg = 2;
+        best_sp = -1;
+    }
     p.bn = bn;
     p.cg = cg;
     const int tiles = ((d.M + kBM * cg - 1) / (kBM * cg)) * ((d.N + bn - 1) / bn);

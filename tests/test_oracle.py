@@ -250,3 +250,69 @@ def test_cnn_oracle_explicit_backward_matches_autograd():
         _close(W2, W)
         _close(b2, b)
         _close(lh2, lh)
+
+
+def test_cnn_oracle_residual_matches_independent_restatement():
+    """The residual extension has no reference counterpart (TinyNet is a
+    chain), so its oracle (cnn_oracle._shortcut / avg pool) is checked against
+    a second, independent restatement: explicit per-position loops for the
+    option-A shortcut and the average pool, the reference's update rule
+    (train_partitioned.cpp:632-651) applied by hand, fp64, 2 steps."""
+    import torch
+    import torch.nn.functional as Fn
+
+    import cnn_oracle
+    from paper_2207_11019_b200 import configs
+
+    torch.manual_seed(0)
+    net = configs.small_resnet(seed=7, hw=8, widths=(4, 8), blocks=(1, 1))
+    rng = np.random.default_rng(3)
+    b = 6
+    X = rng.standard_normal((b, 8 * 8 * 3))
+    y = rng.integers(0, 10, b)
+    W_ref, b_ref, lh_ref, _ = cnn_oracle.train(net, X, y, 0.05, 0.01, 2, 1)
+
+    params = [(torch.tensor(l.weights, dtype=torch.float64, requires_grad=True),
+               torch.tensor(l.bias, dtype=torch.float64, requires_grad=True)) for l in net.layers]
+    x0 = torch.tensor(X).reshape(b, 8, 8, 3).permute(0, 3, 1, 2)
+    yt = torch.tensor(y)
+    alpha, losses = 0.05, []
+    for _ in range(2):
+        outs, a = [], x0
+        for lay, (w, bb) in zip(net.layers, params):
+            if lay.conv is None:
+                a = a.reshape(b, -1) @ w.t() + bb
+                outs.append(a)
+                continue
+            c = lay.conv
+            k = c.ksize
+            q = Fn.conv2d(a, w.reshape(w.shape[0], k, k, -1).permute(0, 3, 1, 2), bb, padding=c.pad)
+            if c.res_from:
+                src = outs[c.res_from - 1]
+                f = src.shape[2] // q.shape[2]
+                sc = torch.zeros_like(q)
+                for hh in range(q.shape[2]):
+                    for ww in range(q.shape[3]):
+                        sc[:, : src.shape[1], hh, ww] = src[:, :, f * hh, f * ww]
+                q = q + sc
+            a = torch.relu(q)
+            if c.pool_avg:
+                p = c.pool
+                a = torch.stack([torch.stack([a[:, :, p * i:p * i + p, p * j:p * j + p].mean(dim=(2, 3))
+                                              for j in range(a.shape[3] // p)], dim=-1)
+                                 for i in range(a.shape[2] // p)], dim=-2)
+            elif c.pool == 2:
+                a = Fn.max_pool2d(a, 2)
+            outs.append(a)
+        p_out = torch.softmax(a, dim=1)
+        ls = -torch.log(torch.clamp(p_out[torch.arange(b), yt], min=1e-300)).sum()
+        grads = torch.autograd.grad(ls, [t for pair in params for t in pair])
+        with torch.no_grad():
+            for t, g in zip([t for pair in params for t in pair], grads):
+                t -= alpha * (g / b)
+        alpha *= 0.99
+        losses.append(ls.item() / b)
+    W_ind = np.concatenate([w.detach().numpy().ravel() for w, _ in params])
+    b_ind = np.concatenate([bb.detach().numpy().ravel() for _, bb in params])
+    assert np.allclose(losses, lh_ref, rtol=1e-12, atol=0)
+    assert np.max(np.abs(W_ind - W_ref)) <= 1e-12 and np.max(np.abs(b_ind - b_ref)) <= 1e-12
