@@ -265,7 +265,15 @@ int ppb_session_step_host_f64(ppb_session* s, const double* X, const int* labels
 int ppb_session_step_host_pipelined(ppb_session* s, const float* X, const double* X64, const int* labels,
                                     double* prev_loss_out);
 
-/* Block until all enqueued work finished; reports divergence / CUDA errors. */
+/* Block until all enqueued work finished; reports divergence / CUDA errors.
+ * Divergence ("diverged at iteration t"): the update is fused into the
+ * weight-gradient GEMM epilogue, so the device weights of that step are
+ * already updated when the flag is read; the reference throws before its
+ * update (train_partitioned.cpp:640-644).  ppb_train_partitioned and the C++
+ * drop-in return the same error and no net, as the reference does; only a
+ * session caller reading the net after the error sees the difference.  The
+ * watchdog deadline is receive_timeout_s per enqueued step (the reference's
+ * deadline is per message). */
 int ppb_session_sync(ppb_session* s);
 
 /* Histories of all steps taken so far (count = steps); blocking. */
