@@ -100,6 +100,33 @@ def algorithmic_flops(net, batch):
     return sum(2.0 * layer_macs(l, batch) * (3 if i > 0 else 2) for i, l in enumerate(net.layers))
 
 
+def merge_traffic(net, plan, batch, n_gpus, plan_devs, step_ms):
+    """Bytes the plan's merges move per step (the forward all-gather of every
+    partitioned layer's output columns, the backward reduce-scatter of the
+    full-width input-gradient partials), counted from the plan: a layer over
+    g devices ships (g - 1) copies of its b x F output forward and (g - 1)
+    full-width b x F_in partials backward.  Both are fused into the producing
+    GEMM epilogues (peer stores) -- the transport the executor uses; with all
+    plan devices on one GPU they are same-GPU stores."""
+    fwd = bwd = 0
+    feats = [l.out_features() for l in net.layers]
+    ins = [net.layers[0].in_units() * (net.layers[0].conv.height * net.layers[0].conv.width
+                                       if net.layers[0].conv else 1)] + feats[:-1]
+    for sm in plan.submodules:
+        g = len(sm.devices)
+        for l in range(sm.first_layer, sm.last_layer + 1):
+            fwd += batch * feats[l - 1] * 4 * (g - 1)
+            if l > 1:
+                bwd += batch * ins[l - 1] * 4 * (g - 1)
+    total = fwd + bwd
+    return {"transport": "fused epilogue peer stores (NVLink P2P); no NCCL path (DESIGN §5)",
+            "fwd_allgather_bytes_per_step": fwd, "bwd_reduce_scatter_bytes_per_step": bwd,
+            "plan_devices": plan_devs, "gpus": n_gpus,
+            "effective_GBs_if_serial": total / (step_ms * 1e-3) / 1e9 if step_ms > 0 else None,
+            "note": ("same-GPU stores: plan devices share one GPU" if n_gpus < plan_devs else
+                     "bytes / step time: a lower bound on the link rate the fused merges sustained")}
+
+
 def by_tile_width(ops, peak):
     """GEMM launches grouped by output-tile width: the TF32 smem-operand rate
     caps N = 64 / 128 tiles at ~41 % / ~67 % of peak, N = 256
@@ -526,6 +553,7 @@ def run_ours(args, rank, world, dist):
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
             "gpu_launches": sess.kernels_per_step() * args.steps,
             "predicted_scaling": scaling,
+            "merges": merge_traffic(net, plan, batch, n, plan_devs, ms / args.steps) if plan_devs > 1 else None,
             "loss_last": float(lh[-1]) if len(lh) else None}
     print(json.dumps(line))
 
