@@ -463,8 +463,11 @@ class Context:
         self.device_map = list(device_map)
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _lib.lib().ppb_context_destroy(self._h)
+        if getattr(self, "_h", None) and _lib is not None and getattr(_lib, "lib", None) is not None:
+            try:
+                _lib.lib().ppb_context_destroy(self._h)
+            except Exception:  # noqa: BLE001  (interpreter shutdown)
+                pass
             self._h = None
 
 
