@@ -543,6 +543,21 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
             }
         }
     }
+    // A/B probe (DEV builds): PPB_FORCE_TILE="M,N,K,cg,bn,splits[;...]" forces
+    // the tiling of every GEMM of that shape (splits 0 = keep the chooser's)
+    if (const char* ft = dev_knob("PPB_FORCE_TILE") ? getenv("PPB_FORCE_TILE") : nullptr) {
+        int fm, fn, fk, fcg, fbn, fsp, used = 0;
+        for (const char* q = ft; sscanf(q, "%d,%d,%d,%d,%d,%d%n", &fm, &fn, &fk, &fcg, &fbn, &fsp, &used) == 6;) {
+            if (fm == d.M && fn == d.N && fk == d.K) {
+                cg = fcg;
+                bn = fbn;
+                best_sp = fsp > 0 ? fsp : -1;
+            }
+            q += used;
+            if (*q != ';') break;
+            ++q;
+        }
+    }
     // A/B probe (DEV builds): CTA-pair tiles for narrow wgrads (fewer M tiles,
     // so the error signal is re-read fewer times through L2)
     if (force_bn == 0 && cg == 1 && bn == 64 && d.epi.mode == EPI_SGD && d.M > 128 && dev_knob("PPB_WGRAD_PAIR")) {
