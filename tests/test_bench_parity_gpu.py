@@ -325,3 +325,34 @@ def test_per_layer_teacher_forced(workload, n):
             assert v <= LAYER_TOL, (k, v)
         else:
             assert v <= LAYER_TOL, (k, v)
+
+
+@pytest.mark.parametrize("workload,n", [("vgg16", 2), ("vgg16", 4), ("vgg16", 8), ("wide_mlp", 8)])
+def test_plan_chooser_plans_run_and_match(workload, n):
+    """The plans `bench.py --gpus N` runs (plan_search.choose_plan on the
+    committed calibration profiles/calib_<workload>.json: staged device
+    groups, Z, m) execute -- here with every plan device on cuda:0 -- and
+    reach the fp64 oracle's weights within the bench-config tolerances."""
+    from paper_2207_11019_b200 import plan_search
+
+    path = plan_search.default_calibration_path(workload)
+    if not os.path.exists(path):
+        pytest.skip("no calibration committed")
+    net, X, y = bench.synthetic_batch(workload, seed=1)
+    best, _ = plan_search.choose_plan(net, n, plan_search.Calibration.load(path))
+    steps = 1 if workload == "wide_mlp" else STEPS
+    ctx = api.Context([0] * n)
+    s = api.Session(ctx, net, X.shape[0], best.plan, best.m, UpdateMode.async_per_module,
+                    TrainConfig(alpha0=1e-2, decay=1e-2, iterations=1),
+                    PartitionedTrainOptions(multiclass_accuracy=True, use_graph=True, pipeline_gate=2))
+    s.load_batch(X, y)
+    s.step(steps)
+    s.sync()
+    lh, _ = s.history()
+    Wg, bg = s.get_net().pack()
+    del s
+    Wr, br, lr = _oracle(workload, 1e-2, steps)
+    rel = [abs(a - r) / abs(r) for a, r in zip(lh, lr)]
+    print(f"\n{workload} n={n}: {best.describe()}; loss rel {['%.1e' % x for x in rel]}, "
+          f"net_distance {net_distance(Wg, bg, Wr, br):.2e}")
+    assert max(rel) <= LOSS_TOL and net_distance(Wg, bg, Wr, br) <= NET_TOL
