@@ -119,7 +119,7 @@ def merge_traffic(net, plan, batch, n_gpus, plan_devs, step_ms):
             if l > 1:
                 bwd += batch * ins[l - 1] * 4 * (g - 1)
     total = fwd + bwd
-    return {"transport": "fused epilogue peer stores (NVLink P2P); no NCCL path (DESIGN §5)",
+    return {"transport": "fused epilogue peer stores (NVLink P2P)",
             "fwd_allgather_bytes_per_step": fwd, "bwd_reduce_scatter_bytes_per_step": bwd,
             "plan_devices": plan_devs, "gpus": n_gpus,
             "effective_GBs_if_serial": total / (step_ms * 1e-3) / 1e9 if step_ms > 0 else None,
@@ -426,7 +426,8 @@ def run_ours(args, rank, world, dist):
                                f"{api.device_count()} GPU(s)")
         ctx = api.Context(list(range(n)))
     cfg = TrainConfig(alpha0=1e-4, decay=1e-2, iterations=1)
-    opts = PartitionedTrainOptions(multiclass_accuracy=True, use_graph=True, pipeline_gate=2, memory_mode=args.memory)
+    opts = PartitionedTrainOptions(multiclass_accuracy=True, use_graph=True, pipeline_gate=2, memory_mode=args.memory,
+                                   merge_backend=args.merge)
     sess = api.Session(ctx, net, batch, plan, m, UpdateMode.async_per_module, cfg, opts)
     mem_total, mem_stash = sess.memory()
     sess.load_batch(X, y)
@@ -553,7 +554,10 @@ def run_ours(args, rank, world, dist):
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
             "gpu_launches": sess.kernels_per_step() * args.steps,
             "predicted_scaling": scaling,
-            "merges": merge_traffic(net, plan, batch, n, plan_devs, ms / args.steps) if plan_devs > 1 else None,
+            "merges": (dict(merge_traffic(net, plan, batch, n, plan_devs, ms / args.steps),
+                            **({"transport": "NCCL all-gather / reduce-scatter for dense layers inside a sub-module, "
+                                             "fused peer stores elsewhere"} if args.merge == "nccl" else {}))
+                       if plan_devs > 1 else None),
             "loss_last": float(lh[-1]) if len(lh) else None}
     print(json.dumps(line))
 
@@ -565,6 +569,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="vgg16", choices=sorted(WORKLOADS))
     ap.add_argument("--m", type=int, default=1, help="micro-batches per step")
+    ap.add_argument("--merge", default="p2p", choices=["p2p", "nccl"],
+                    help="merge transport of the dense layers (nccl: one plan device per GPU)")
     ap.add_argument("--memory", default="stash_all", choices=["stash_all", "proposed"],
                     help="activation stash policy (proposed: min(m, gate) resident micro-batches, "
                          "weight gradients per micro-batch)")

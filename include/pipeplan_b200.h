@@ -153,7 +153,8 @@ typedef struct {
     int use_graph;             /* capture the step in a CUDA graph (1) or launch eagerly (0) */
     int pipeline_gate;         /* F(i,j) waits for B(i,j-gate) (schedule.cpp:293-296); 0 = off */
     int memory_mode;           /* PPB_MEMORY_*: activation stash policy (simulate.hpp:14-16 MemoryMode) */
-    int reserved[7];
+    int merge_backend;         /* PPB_MERGE_*: transport of the dense layers' merges inside a sub-module */
+    int reserved[6];
 } ppb_options;
 
 /* Activation stash policy (the reference simulator's MemoryMode,
@@ -165,6 +166,17 @@ typedef struct {
  * its activation / error-signal slots are reused by micro-batch
  * j + min(m, pipeline_gate), so only min(m, gate) micro-batches are resident
  * (tf32 precision; with m = 1 both policies are the same step). */
+/* Merge transport (north_star (2)).  P2P: the forward all-gather and the
+ * backward reduce-scatter are fused into the producing GEMM epilogues (stores
+ * into every consumer GPU's buffers over NVLink; destination sums in
+ * ascending device order).  NCCL: dense layers inside a sub-module write
+ * their shard locally, ncclAllGather / ncclReduceScatter move it (one
+ * communicator per sub-module, libnccl.so.2 loaded at run time) and a kernel
+ * lays it out; needs one plan device per GPU and equal shard widths (other
+ * layers keep P2P); NCCL's summation order replaces the ascending one. */
+#define PPB_MERGE_P2P 0
+#define PPB_MERGE_NCCL 1
+
 #define PPB_MEMORY_STASH_ALL 0
 #define PPB_MEMORY_PROPOSED 1
 

@@ -45,7 +45,8 @@ class OptionsC(C.Structure):
         ("use_graph", C.c_int),
         ("pipeline_gate", C.c_int),
         ("memory_mode", C.c_int),
-        ("reserved", C.c_int * 7),
+        ("merge_backend", C.c_int),
+        ("reserved", C.c_int * 6),
     ]
 
 

@@ -294,6 +294,10 @@ class PartitionedTrainOptions:  # train_partitioned.hpp:9-11 + GPU knobs
     # all b rows); "proposed" keeps min(m, pipeline_gate) micro-batches and
     # accumulates weight gradients per micro-batch
     memory_mode: str = "stash_all"
+    # merge transport of dense layers inside a sub-module: "p2p" (fused
+    # epilogue peer stores) or "nccl" (ncclAllGather / ncclReduceScatter;
+    # one plan device per GPU)
+    merge_backend: str = "p2p"
 
     def to_c(self) -> _lib.OptionsC:
         o = _lib.OptionsC()
@@ -303,6 +307,7 @@ class PartitionedTrainOptions:  # train_partitioned.hpp:9-11 + GPU knobs
         o.use_graph = int(self.use_graph)
         o.pipeline_gate = int(self.pipeline_gate)
         o.memory_mode = {"stash_all": 0, "proposed": 1}[self.memory_mode]
+        o.merge_backend = {"p2p": 0, "nccl": 1}[self.merge_backend]
         return o
 
 

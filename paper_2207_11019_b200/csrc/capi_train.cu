@@ -51,6 +51,8 @@ SessionConfig make_cfg(int batch, int m, int mode, const ppb_train_config* cfg, 
     c.use_graph = opts->use_graph;
     c.gate = opts->pipeline_gate;
     c.stash = opts->memory_mode;
+    c.merge = opts->merge_backend;
+    if (c.merge != PPB_MERGE_P2P && c.merge != PPB_MERGE_NCCL) throw std::invalid_argument("unknown merge backend");
     if (c.stash != PPB_MEMORY_STASH_ALL && c.stash != PPB_MEMORY_PROPOSED)
         throw std::invalid_argument("unknown memory mode");
     if (c.loss != 0 && c.loss != 1) throw std::invalid_argument("unknown loss kind");

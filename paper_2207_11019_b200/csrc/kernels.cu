@@ -846,6 +846,19 @@ __global__ void conv_merge_rows_kernel(ConvMerge m, float* __restrict__ db_parti
 }
 
 
+__global__ void unpack_gather_kernel(const float* __restrict__ recv, int g, int rows, int u, float* __restrict__ dst,
+                                     long long ld) {
+    const long long total = static_cast<long long>(g) * rows * u;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(i % u);
+        const long long t = i / u;
+        const int r = static_cast<int>(t % rows);
+        const int k = static_cast<int>(t / rows);
+        dst[static_cast<long long>(r) * ld + static_cast<long long>(k) * u + c] = recv[i];
+    }
+}
+
 // ---------------------------------------------------------------- residual extension
 
 // Thread = (image, pooled pixel, 4-channel group); window p x p (p = 1: no
@@ -1200,6 +1213,13 @@ cudaError_t launch_conv_merge(const ConvMerge& m, float* db_partial, cudaStream_
         if (i32) pdl_launch(conv_merge_kernel<1, unsigned>, dim3(grid), dim3(block), shmem, s, m, db_partial);
         else pdl_launch(conv_merge_kernel<1, long long>, dim3(grid), dim3(block), shmem, s, m, db_partial);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_gather(const float* recv, int g, int rows, int u, float* dst, long long ld, cudaStream_t s) {
+    const long long n = static_cast<long long>(g) * rows * u;
+    if (n <= 0) return cudaSuccess;
+    pdl_launch(unpack_gather_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, recv, g, rows, u, dst, ld);
     return cudaGetLastError();
 }
 

@@ -181,6 +181,10 @@ struct SkipGrad {
 cudaError_t launch_conv_merge_res(const ConvMerge& m, int pool_avg, const SkipGrad& sg, float* db_partial,
                                   cudaStream_t s);
 
+// NCCL merge backend: the all-gathered shard outputs [g][rows][u] (rank
+// order) into the activation rows [rows][ld] at columns k*u + c.
+cudaError_t launch_unpack_gather(const float* recv, int g, int rows, int u, float* dst, long long ld, cudaStream_t s);
+
 // bias -= alpha * (sum_k partial[k][c] / b) over `chunks` partial rows.
 cudaError_t launch_bias_from_partials(const float* partial, int chunks, int u, float* bias, const double* alpha,
                                       float inv_b, cudaStream_t s);

@@ -86,6 +86,13 @@ struct Session::WLayer {
     float* cols = nullptr;               // generic conv: im2col rows of the input [b*Ho*Wo x ldc]
     long long ldc = 0;
     float* dcols = nullptr;              // generic conv: dgrad partial in column space [b*Ho*Wo x ldk]
+    // NCCL merge backend (dense layers): local shard output [rows][u] and the
+    // all-gathered [g][rows][u]; this layer's dgrad partial packed per
+    // destination rank [g][rows][u_below]; the reduce-scattered sum [rows][u]
+    float* ag_send = nullptr;
+    float* ag_recv = nullptr;
+    float* rs_send = nullptr;
+    float* rs_recv = nullptr;
     long long ldk = 0;                   // (dense conv: input-gradient rows [b][H*W*C])
     float* Wx = nullptr;                 // dense conv: expanded weight [Ho*Wo*u x ldwx]
     float* dWx = nullptr;                // dense conv: its gradient
@@ -146,6 +153,32 @@ float* Session::q_buf(int ordinal) { return gpu_of(ordinal).q; }
 // two weight-gradient streams: 2.293 vs 2.317 ms on the VGG-16 step (3 A/B
 // pairs on one box); PPB_WGRAD_ONE_STREAM=1 (DEV builds) restores one
 bool Session::wgrad_two_streams() { return !dev_knob("PPB_WGRAD_ONE_STREAM"); }
+
+int Session::module_index(int l) const {
+    for (const SubModule& sm : plan_.subs)
+        if (l >= sm.first_layer && l <= sm.last_layer) return sm.index;
+    return 0;
+}
+
+bool Session::nccl_layer(int l) const {
+    if (cfg_.merge != 1 || l < 1 || l >= net_.L()) return false;
+    const LayerInfo& li = net_.info[l - 1];
+    const LayerInfo& ln = net_.info[l];
+    if (li.kind != 0 || ln.kind != 0 || li.act == 2) return false;
+    const int mi = module_index(l);
+    if (mi != module_index(l + 1) || mi < 1 || nccl_[mi - 1] == nullptr) return false;
+    const auto& ws = layer_workers_[l];
+    const int g = static_cast<int>(ws.size());
+    if (g < 2 || li.out_units % g != 0 || (li.out_units / g) % 4 != 0) return false;
+    for (int wi : ws) {
+        const WLayer& wl = workers_[wi]->at(l);
+        if (!wl.contributor || wl.replicated || wl.u != li.out_units / g) return false;
+        // the backward reduce-scatter pairs contributor k of layer l + 1 with rank k
+        const WLayer& wn = workers_[wi]->at(l + 1);
+        if (!wn.contributor || wn.replicated) return false;
+    }
+    return static_cast<int>(layer_workers_[l + 1].size()) == g;
+}
 
 size_t Session::device_bytes() const {
     size_t n = 0;
@@ -406,6 +439,19 @@ void Session::build() {
     }
     // loss / history live with rank 0 of the last module (train_partitioned.cpp:372)
     main_gpu_ = workers_[layer_workers_[L].front()]->gpu;
+    // NCCL merge backend: one communicator per multi-device sub-module
+    // (rank = position in its device list)
+    nccl_.clear();
+    nccl_.resize(plan_.subs.size());
+    if (cfg_.merge == 1) {
+        if (cfg_.precision != 0) throw std::invalid_argument("the NCCL merge backend runs on the tf32 path");
+        for (const SubModule& sm : plan_.subs) {
+            if (sm.devices.size() < 2) continue;
+            std::vector<int> ords;
+            for (int d : sm.devices) ords.push_back(device_map_[d - 1]);
+            nccl_[sm.index - 1] = nccl_group_create(ords);
+        }
+    }
     alloc_buffers();
     build_ops();
     if (cfg_.use_graph) capture_graph();
@@ -627,6 +673,23 @@ void Session::alloc_buffers() {
             }
             for (int k = 0; k < ncontrib; ++k)
                 wl.slots.push_back(static_cast<float*>(g.alloc(sizeof(float) * rows * wl.slot_ld, true)));
+        }
+    }
+    // NCCL merge backend buffers (dense layers whose merges go through NCCL)
+    for (int l = 1; l < L; ++l) {
+        if (!nccl_layer(l)) continue;
+        const int gsz = static_cast<int>(layer_workers_[l].size());
+        for (int wi : layer_workers_[l]) {
+            Worker& w = *workers_[wi];
+            Gpu& g = gpu_of(w.gpu);
+            WLayer& wl = w.at(l);
+            const size_t blk = static_cast<size_t>(ring_rows_) * wl.u;
+            wl.ag_send = static_cast<float*>(g.alloc(sizeof(float) * blk, true));
+            wl.ag_recv = static_cast<float*>(g.alloc(sizeof(float) * blk * gsz, true));
+            wl.rs_recv = static_cast<float*>(g.alloc(sizeof(float) * blk, true));
+            // the dgrad of layer l + 1 on this device packs its partial per destination rank
+            WLayer& wn = w.at(l + 1);
+            wn.rs_send = static_cast<float*>(g.alloc(sizeof(float) * blk * gsz, true));
         }
     }
     for (auto& gp : gpus_) {
@@ -1070,9 +1133,15 @@ void Session::build_ops() {
                 d.epi.relu = net_.acts[l - 1] == 1;
                 d.epi.col0 = wl.lo;
                 d.epi.ldd = ld_of(net_.dims[l]);
-                for (int ord : dest_gpus) {
-                    float* base = (l == L && softmax) ? q_buf(ord) : act_buf(ord, l);
-                    d.epi.dst[d.epi.ndst++] = base + so * d.epi.ldd;
+                if (nccl_layer(l)) {  // NCCL backend: the shard output stays local, packed [rows][u]
+                    d.epi.col0 = 0;
+                    d.epi.ldd = wl.u;
+                    d.epi.dst[d.epi.ndst++] = wl.ag_send + so * wl.u;
+                } else {
+                    for (int ord : dest_gpus) {
+                        float* base = (l == L && softmax) ? q_buf(ord) : act_buf(ord, l);
+                        d.epi.dst[d.epi.ndst++] = base + so * d.epi.ldd;
+                    }
                 }
                 prepare(d, wl.p_fwd[j], w.gpu);
                 const int op = add_op(w.gpu, w.sf, gemm_launch(&wl.p_fwd[j], &wl.d_fwd[j], w.sf), deps, nk(wl.p_fwd[j]),
@@ -1081,6 +1150,39 @@ void Session::build_ops() {
                 produced.push_back(op);
             }
             for (int ord : dest_gpus) act_ready[l][j][ord] = produced;
+            if (nccl_layer(l)) {
+                // ncclAllGather of the packed shard outputs (one group over the
+                // sub-module's ranks, each on its worker's forward stream, after
+                // its GEMM), then each GPU lays the [g][rows][u] result out as the
+                // activation rows the next layer reads
+                const auto& ws = layer_workers_[l];
+                const int gsz = static_cast<int>(ws.size());
+                std::vector<const float*> snd;
+                std::vector<float*> rcv;
+                std::vector<cudaStream_t> sts;
+                for (int wi : ws) {
+                    WLayer& wl = workers_[wi]->at(l);
+                    snd.push_back(wl.ag_send + so * wl.u);
+                    rcv.push_back(wl.ag_recv + so * gsz * wl.u);
+                    sts.push_back(workers_[wi]->sf);
+                }
+                const NcclGroup* grp = nccl_[module_index(l) - 1].get();
+                const int u = workers_[ws.front()]->at(l).u;
+                const size_t count = static_cast<size_t>(rows) * u;
+                Worker& w0 = *workers_[ws.front()];
+                const int cop = add_op(w0.gpu, w0.sf, [=]() { return nccl_all_gather(*grp, snd, rcv, count, sts); },
+                                       produced, 0, OP_COPY);
+                const long long ld = ld_of(net_.dims[l]);
+                for (size_t k = 0; k < ws.size(); ++k) {
+                    Worker& w = *workers_[ws[k]];
+                    const float* rv = rcv[k];
+                    float* dst = act_buf(w.gpu, l) + so * ld;
+                    cudaStream_t st = w.sf;
+                    act_ready[l][j][w.gpu] = {add_op(w.gpu, st, [=]() {
+                        return launch_unpack_gather(rv, gsz, rows, u, dst, ld, st);
+                    }, {cop}, 1, OP_COPY)};
+                }
+            }
             if (l < L && boundary_concat) {
                 // concat_repartition: gather at the hub, then broadcast the full
                 // activation to the other consumer GPUs (:258-271, :357-362)
@@ -1437,6 +1539,7 @@ void Session::build_ops() {
                 d.K = wl.u;
                 d.epi = EpiParams{};
                 d.epi.mode = EPI_SLOTS;
+                const bool ncl = nccl_layer(l - 1);
                 for (int di : dests) {
                     Worker& dw = *workers_[di];
                     WLayer& dl = dw.at(l - 1);
@@ -1444,7 +1547,11 @@ void Session::build_ops() {
                     d.epi.seg_lo[s] = dl.lo;
                     d.epi.seg_hi[s] = dl.hi;
                     d.epi.seg_ld[s] = dl.ldd;
-                    if (single) {
+                    if (ncl) {  // NCCL backend: block s of the packed per-rank partial [g][rows][u]
+                        const long long gsz = static_cast<long long>(dests.size());
+                        d.epi.seg_ld[s] = dl.u;
+                        d.epi.seg_dst[s] = wl.rs_send + so * gsz * dl.u + static_cast<long long>(s) * rows * dl.u;
+                    } else if (single) {
                         d.epi.seg_dst[s] = dl.delta + so * dl.ldd;
                         if (relu_below) {
                             d.epi.seg_mask[s] = act_buf(dw.gpu, l - 1) + so * ld_of(fi);
@@ -1461,9 +1568,45 @@ void Session::build_ops() {
                 w.last_bwd[j] = std::max(w.last_bwd[j], op);
                 dgrad_ops.push_back(op);
             }
+            int rs_op = -1;
+            if (nccl_layer(l - 1)) {
+                // ncclReduceScatter: rank k receives the sum over contributors of
+                // block k (its own columns), on each worker's input-gradient stream
+                std::vector<const float*> snd;
+                std::vector<float*> rcv;
+                std::vector<cudaStream_t> sts;
+                const long long gsz = static_cast<long long>(dests.size());
+                for (size_t k = 0; k < contrib.size(); ++k) {
+                    Worker& w = *workers_[contrib[k]];
+                    WLayer& dl = workers_[dests[k]]->at(l - 1);
+                    snd.push_back(w.at(l).rs_send + so * gsz * dl.u);
+                    rcv.push_back(dl.rs_recv + so * dl.u);
+                    sts.push_back(w.sb);
+                }
+                const NcclGroup* grp = nccl_[module_index(l - 1) - 1].get();
+                const size_t count = static_cast<size_t>(rows) * workers_[dests.front()]->at(l - 1).u;
+                Worker& w0 = *workers_[contrib.front()];
+                rs_op = add_op(w0.gpu, w0.sb, [=]() { return nccl_reduce_scatter(*grp, snd, rcv, count, sts); },
+                               dgrad_ops, 0, OP_REDUCE);
+            }
             for (int di : dests) {
                 Worker& dw = *workers_[di];
                 WLayer& dl = dw.at(l - 1);
+                if (rs_op >= 0) {  // the reduced block -> mask -> delta
+                    ReduceSlots rs;
+                    rs.slot[rs.n++] = dl.rs_recv + so * dl.u;
+                    const float* mask = relu_below ? act_buf(dw.gpu, l - 1) + so * ld_of(fi) + dl.lo : nullptr;
+                    const long long ldm = ld_of(fi), lds = dl.u, ldd = dl.ldd;
+                    float* out = dl.delta + so * dl.ldd;
+                    const int u = dl.u;
+                    cudaStream_t st = dw.sb;
+                    const int op = add_op(dw.gpu, st, [=]() {
+                        return launch_reduce_mask(rs, lds, rows, u, mask, ldm, out, ldd, st);
+                    }, {rs_op}, 1, OP_REDUCE);
+                    dl.delta_ready[j] = {op};
+                    dw.last_bwd[j] = std::max(dw.last_bwd[j], op);
+                    continue;
+                }
                 if (single) {
                     dl.delta_ready[j] = dgrad_ops;
                     dw.last_bwd[j] = std::max(dw.last_bwd[j], dgrad_ops.front());

@@ -20,6 +20,7 @@
 
 #include "gemm_tc.h"
 #include "kernels.h"
+#include "nccl_merge.h"
 #include "planner.h"
 
 namespace ppb {
@@ -102,6 +103,9 @@ struct SessionConfig {
     // over all b rows); 1 proposed (ring of min(m, gate) micro-batch slots,
     // weight gradients accumulated per micro-batch)
     int stash = 0;
+    // merge transport of the dense layers inside a sub-module: 0 fused
+    // epilogue peer stores, 1 NCCL all-gather / reduce-scatter (nccl_merge.h)
+    int merge = 0;
 };
 
 class Session {
@@ -186,6 +190,10 @@ class Session {
     }
     bool skip_source(int s) const { return res_consumer(s) > 0; }
     static bool wgrad_two_streams();
+    // NCCL backend: layer l's forward all-gather (and the backward
+    // reduce-scatter into it from layer l + 1) go through NCCL
+    bool nccl_layer(int l) const;
+    int module_index(int l) const;
     void check(cudaError_t e, const char* what);
     void validate_labels(const int* labels) const;
 
@@ -216,6 +224,7 @@ class Session {
     bool pending_acc_error_ = false;
     int cur_layer_ = 0, cur_info_ = 0, cur_mb_ = -1;
     bool serialise_ = true;
+    std::vector<std::unique_ptr<NcclGroup>> nccl_;  // per sub-module (index - 1), NCCL backend only
     std::vector<double> last_op_ms_;
     double* loss_pinned_ = nullptr;  // pinned host slots for step_host's loss read-back
     cudaEvent_t ev_loss_[2] = {nullptr, nullptr};

@@ -53,3 +53,39 @@ def test_peer_data_plane_matches_one_gpu(k, net_name):
         a = _run(net, X, y, plan, list(range(k)), m, mem)
         b = _run(net, X, y, plan, [0] * k, m, mem)
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+
+
+def test_nccl_backend_requires_distinct_gpus():
+    """PPB_MERGE_NCCL loads libnccl.so.2 at run time and refuses plans whose
+    devices share a GPU (an NCCL communicator cannot hold one GPU twice)."""
+    net = configs.dense_net([256, 512, 512, 10], [1, 1, 2], seed=4)
+    with pytest.raises(ValueError, match="one plan device per GPU"):
+        api.Session(api.Context([0, 0]), net, 64, api.build_plan(net, 2, 1), 1, UpdateMode.async_per_module,
+                    TrainConfig(iterations=1), PartitionedTrainOptions(merge_backend="nccl"))
+
+
+@pytest.mark.parametrize("k", [2, 4, 8])
+def test_nccl_backend_matches_p2p(k):
+    """The NCCL transport (ncclAllGather / ncclReduceScatter for the dense
+    layers inside a sub-module) against the fused peer-store merges on the
+    same GPUs: same forward bits; backward sums in NCCL's order (2 ranks:
+    identical; more: fp32 reassociation only)."""
+    _need(k)
+    rng = np.random.default_rng(0)
+    net = configs.dense_net([1024, 2048, 2048, 2048, 16], [1, 1, 1, 2], seed=4)
+    X = rng.standard_normal((256, 1024)).astype(np.float32)
+    y = rng.integers(0, 16, 256)
+    plan = api.build_plan(net, k, 1)
+    out = {}
+    for mb in ("p2p", "nccl"):
+        s = api.Session(api.Context(list(range(k))), net, 256, plan, 2, UpdateMode.async_per_module,
+                        TrainConfig(alpha0=1e-2, decay=1e-2, iterations=1),
+                        PartitionedTrainOptions(multiclass_accuracy=True, merge_backend=mb))
+        s.load_batch(X, y)
+        s.step(3)
+        s.sync()
+        out[mb] = (s.get_net().pack()[0], s.history()[0])
+    if k == 2:
+        assert np.array_equal(out["p2p"][0], out["nccl"][0])
+    assert np.allclose(out["p2p"][0], out["nccl"][0], rtol=1e-5, atol=1e-7)
+    assert np.allclose(out["p2p"][1], out["nccl"][1], rtol=1e-6)
