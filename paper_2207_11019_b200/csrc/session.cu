@@ -1584,9 +1584,9 @@ void Session::build_ops() {
                     sts.push_back(w.sb);
                 }
                 const NcclGroup* grp = nccl_[module_index(l - 1) - 1].get();
-                const size_t count = static_cast<size_t>(rows) * workers_[dests.front()]->at(l - 1).u;
+                const int ud = workers_[dests.front()]->at(l - 1).u;
                 Worker& w0 = *workers_[contrib.front()];
-                rs_op = add_op(w0.gpu, w0.sb, [=]() { return nccl_reduce_scatter(*grp, snd, rcv, count, sts); },
+                rs_op = add_op(w0.gpu, w0.sb, [=]() { return nccl_reduce_scatter(*grp, snd, rcv, rows, ud, sts); },
                                dgrad_ops, 0, OP_REDUCE);
             }
             for (int di : dests) {

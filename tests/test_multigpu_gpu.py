@@ -55,13 +55,30 @@ def test_peer_data_plane_matches_one_gpu(k, net_name):
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
 
 
-def test_nccl_backend_requires_distinct_gpus():
-    """PPB_MERGE_NCCL loads libnccl.so.2 at run time and refuses plans whose
-    devices share a GPU (an NCCL communicator cannot hold one GPU twice)."""
-    net = configs.dense_net([256, 512, 512, 10], [1, 1, 2], seed=4)
-    with pytest.raises(ValueError, match="one plan device per GPU"):
-        api.Session(api.Context([0, 0]), net, 64, api.build_plan(net, 2, 1), 1, UpdateMode.async_per_module,
-                    TrainConfig(iterations=1), PartitionedTrainOptions(merge_backend="nccl"))
+@pytest.mark.parametrize("k,m,memory", [(2, 1, "stash_all"), (4, 2, "stash_all"), (4, 4, "proposed"), (8, 1, "stash_all")])
+def test_nccl_layout_loopback_matches_p2p(k, m, memory):
+    """PPB_MERGE_NCCL with every plan device on cuda:0 runs the NCCL data
+    layout (local packed shard outputs, [g][rows][u] gather + unpack, packed
+    per-rank dgrad partials + reduce-scatter + mask) with the collectives
+    emulated by device copies / the ascending-rank sum (an NCCL communicator
+    cannot hold one GPU twice): bitwise equal to the fused peer-store merges."""
+    rng = np.random.default_rng(0)
+    net = configs.dense_net([1024, 2048, 2048, 2048, 16], [1, 1, 1, 2], seed=4)
+    X = rng.standard_normal((256, 1024)).astype(np.float32)
+    y = rng.integers(0, 16, 256)
+    plan = api.build_plan(net, k, 1)
+    out = {}
+    for mb in ("p2p", "nccl"):
+        s = api.Session(api.Context([0] * k), net, 256, plan, m, UpdateMode.async_per_module,
+                        TrainConfig(alpha0=1e-2, decay=1e-2, iterations=1),
+                        PartitionedTrainOptions(multiclass_accuracy=True, merge_backend=mb, memory_mode=memory))
+        s.load_batch(X, y)
+        s.step(3)
+        s.sync()
+        out[mb] = (s.get_net().pack()[0], s.history()[0])
+        del s
+    assert np.array_equal(out["p2p"][0], out["nccl"][0])
+    assert np.array_equal(out["p2p"][1], out["nccl"][1])
 
 
 @pytest.mark.parametrize("k", [2, 4, 8])
