@@ -57,9 +57,9 @@ WORKLOADS = {
     "mlp784": dict(net="mlp784", batch=64, classes=10, name="MLP 784-512-512-10, batch 64"),
     # BASELINE.json configs[1]: LeNet-5 on 28x28x1 (generic im2col conv path; latency-bound).
     "lenet5": dict(net="lenet5", batch=256, classes=10, name="LeNet-5 (28x28x1, 5x5 convs), batch 256"),
-    # BASELINE.json configs[3]: ResNet-18-style (residual blocks, option-A shortcuts, global average pool).
+    # BASELINE.json configs[3]: ResNet-18 (residual blocks, stride-2 stage transitions, option-A shortcuts, global average pool).
     "resnet18": dict(net="resnet18", batch=1024, classes=10,
-                     name="ResNet-18-style (CIFAR 32x32x3, 17 conv + 512->10, residual blocks), batch 1024"),
+                     name="ResNet-18 (CIFAR 32x32x3, 17 conv + 512->10, residual blocks), batch 1024"),
 }
 
 
@@ -90,8 +90,7 @@ def layer_macs(layer, batch):
     if layer.conv is None:
         return layer.fan_in() * layer.fan_out() * batch
     c = layer.conv
-    ho = c.height + 2 * c.pad - c.ksize + 1
-    wo = c.width + 2 * c.pad - c.ksize + 1
+    ho, wo = c.conv_hw()
     return batch * ho * wo * layer.fan_out() * layer.fan_in()
 
 

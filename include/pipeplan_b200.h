@@ -207,6 +207,7 @@ typedef struct {
      * average pool before the classifier). */
     int res_from;
     int pool_kind;
+    int stride; /* conv stride (0 or 1: stride 1; > 1 runs on the generic im2col path) */
 } ppb_layer;
 #define PPB_POOL_MAX 0
 #define PPB_POOL_AVG 1

@@ -70,7 +70,7 @@ def _forward(layers, params, x, flatten=True, outs=None):
             wt = w.reshape(w.shape[0], c.ksize, c.ksize, cin).permute(0, 3, 1, 2)
             if a.dim() == 2:
                 a = a.reshape(a.shape[0], c.height, c.width, cin).permute(0, 3, 1, 2)
-            a = Fn.conv2d(a, wt, b, padding=c.pad)
+            a = Fn.conv2d(a, wt, b, padding=c.pad, stride=getattr(c, "stride", 1))
             if getattr(c, "res_from", 0):
                 a = a + _shortcut(outs[c.res_from - 1], a)
             if int(lay.act) == RELU:
@@ -222,9 +222,9 @@ def train_model(net, X, y, alpha0, decay, iterations, m=1, tf32_mode=None):
     GPU's TF32 path, used to separate "the kernels compute what they should"
     (tight) from "TF32 vs the fp64 reference" (looser, stated).  CE + softmax
     head, multiclass accuracy.  Returns (W, b, loss_hist)."""
-    if any(l.conv is not None and (getattr(l.conv, "res_from", 0) or getattr(l.conv, "pool_avg", False))
-           for l in net.layers):
-        raise NotImplementedError("train_model: residual / average-pool layers (use train, autograd)")
+    if any(l.conv is not None and (getattr(l.conv, "res_from", 0) or getattr(l.conv, "pool_avg", False) or
+                                   getattr(l.conv, "stride", 1) > 1) for l in net.layers):
+        raise NotImplementedError("train_model: residual / average-pool / strided layers (use train, autograd)")
     exact = tf32_mode is None
     T = (lambda t: t) if exact else (lambda t: tf32(t, tf32_mode))
     S = (lambda t: t) if exact else _f32

@@ -53,7 +53,7 @@ class OptionsC(C.Structure):
 class LayerC(C.Structure):
     _fields_ = [("kind", C.c_int), ("in_units", C.c_int), ("out_units", C.c_int), ("act", C.c_int),
                 ("height", C.c_int), ("width", C.c_int), ("ksize", C.c_int), ("pad", C.c_int), ("pool", C.c_int),
-                ("res_from", C.c_int), ("pool_kind", C.c_int)]
+                ("res_from", C.c_int), ("pool_kind", C.c_int), ("stride", C.c_int)]
 
 
 # name -> (restype, argtypes)

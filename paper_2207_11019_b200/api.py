@@ -168,10 +168,16 @@ class ConvSpec:
     # with a pool x pool average instead of the 2x2 max (`pool_avg`)
     res_from: int = 0
     pool_avg: bool = False
+    stride: int = 1
+
+    def conv_hw(self):
+        """Conv output grid before pooling."""
+        return ((self.height + 2 * self.pad - self.ksize) // self.stride + 1,
+                (self.width + 2 * self.pad - self.ksize) // self.stride + 1)
 
     def out_hw(self):
-        ho = self.height + 2 * self.pad - self.ksize + 1
-        wo = self.width + 2 * self.pad - self.ksize + 1
+        ho = (self.height + 2 * self.pad - self.ksize) // self.stride + 1
+        wo = (self.width + 2 * self.pad - self.ksize) // self.stride + 1
         return ho // self.pool, wo // self.pool
 
 
@@ -201,7 +207,7 @@ class TinyLayer:  # tinynet.hpp:41-48
         if self.conv is None:
             return 0.0  # default_costs (model.cpp:124-137) applies
         c = self.conv
-        ho, wo = c.height + 2 * c.pad - c.ksize + 1, c.width + 2 * c.pad - c.ksize + 1
+        ho, wo = c.conv_hw()
         return 2.0 * self.weights.shape[0] * self.weights.shape[1] * ho * wo
 
     def to_c(self) -> _lib.LayerC:
@@ -211,7 +217,7 @@ class TinyLayer:  # tinynet.hpp:41-48
         if self.conv:
             lc.height, lc.width, lc.ksize, lc.pad, lc.pool = (self.conv.height, self.conv.width, self.conv.ksize,
                                                               self.conv.pad, self.conv.pool)
-            lc.res_from, lc.pool_kind = self.conv.res_from, int(self.conv.pool_avg)
+            lc.res_from, lc.pool_kind, lc.stride = self.conv.res_from, int(self.conv.pool_avg), self.conv.stride
         return lc
 
 

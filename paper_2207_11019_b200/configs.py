@@ -92,22 +92,23 @@ def lenet5(seed=1, classes=10, hw=28, cin=1, init="reference") -> TinyNet:
 
 def resnet18_cifar(seed=1, classes=10, hw=32, cin=3, widths=(64, 128, 256, 512), blocks=(2, 2, 2, 2),
                    init="kaiming") -> TinyNet:
-    """BASELINE configs[3]: ResNet-18-style CNN on 32x32x3 (17 conv 3x3 + the
-    classifier).  A 3x3 stem (64), then four stages of two basic blocks (two
-    3x3 convs, ReLU after the residual add); each later stage opens with its
-    first conv followed by a 2x2 max pool (the chain's downsampling; the
-    reference has no strided conv) and its shortcut is ResNet "option A"
-    (every 2nd position, channels zero-padded: parameter-free, He et al.
-    2016 §4.2), the others are identities; the last conv ends in a global
-    average pool, then 512 -> classes.  No batch norm (SURVEY §8d counts
-    conv + fc only)."""
+    """BASELINE configs[3]: ResNet-18 on 32x32x3 (the CIFAR variant: 3x3 stem,
+    17 conv 3x3 + the classifier).  Four stages of two basic blocks (two 3x3
+    convs, ReLU after the residual add); each later stage opens with a
+    stride-2 conv and its shortcut is ResNet "option A" (every 2nd position,
+    channels zero-padded: parameter-free, He et al. 2016 §4.2), the other
+    shortcuts are identities; the last conv ends in a global average pool,
+    then 512 -> classes.  No batch norm (SURVEY §8d counts conv + fc only:
+    3.33 GFLOP / sample)."""
     rng = np.random.default_rng(seed)
     layers = [_conv(rng, cin, widths[0], (hw, hw), init=init)]
     c, h, prev = widths[0], hw, 1
     for st, wd in enumerate(widths):
         for blk in range(blocks[st]):
             down = st > 0 and blk == 0
-            layers.append(_conv(rng, c, wd, (h, h), pool=2 if down else 1, init=init))
+            la = _conv(rng, c, wd, (h, h), init=init)
+            la.conv.stride = 2 if down else 1
+            layers.append(la)
             h = h // 2 if down else h
             last = st == len(widths) - 1 and blk == blocks[st] - 1
             lb = _conv(rng, wd, wd, (h, h), pool=h if last else 1, init=init)
@@ -120,6 +121,6 @@ def resnet18_cifar(seed=1, classes=10, hw=32, cin=3, widths=(64, 128, 256, 512),
 
 
 def small_resnet(seed=1, hw=8, cin=3, widths=(8, 16), blocks=(1, 1), classes=10) -> TinyNet:
-    """A scaled-down ResNet-style net for parity tests (identity and option-A
-    shortcuts, max-pool downsampling, global average pool)."""
+    """A scaled-down ResNet for parity tests (identity and option-A
+    shortcuts, a stride-2 stage transition, global average pool)."""
     return resnet18_cifar(seed, classes, hw, cin, widths, blocks)

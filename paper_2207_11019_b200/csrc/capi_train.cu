@@ -129,6 +129,7 @@ extern "C" int ppb_session_create_layers(ppb_context* ctx, const ppb_layer* laye
                 li.pad = p.pad;
                 li.pool = p.pool < 1 ? 1 : p.pool;
                 li.res_from = p.res_from;
+                li.stride = p.stride < 1 ? 1 : p.stride;
                 li.pool_avg = p.pool_kind == PPB_POOL_AVG ? 1 : 0;
                 if (p.pool_kind != PPB_POOL_MAX && p.pool_kind != PPB_POOL_AVG)
                     throw std::invalid_argument("unknown pool kind " + std::to_string(p.pool_kind));

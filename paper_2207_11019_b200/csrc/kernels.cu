@@ -365,7 +365,7 @@ __global__ void im2col_kernel(const T* __restrict__ src, int imgs, int H, int W,
 // (tap, c) of output pixel (img, y, x) = x_pad[img][y + r][x + s][c] (the
 // tensor's own zero ring is the conv padding); columns >= k*k*C are zero.
 __global__ void im2col_act_kernel(const float* __restrict__ x, int imgs, int hp, int wp, long long ldx, int C, int k,
-                                  int Ho, int Wo, float* __restrict__ dst, long long ldc) {
+                                  int Ho, int Wo, float* __restrict__ dst, long long ldc, int st) {
     griddep_wait();  // programmatic launch: the predecessor's results are visible after this
     const int kc = k * k * C;
     const long long total = static_cast<long long>(imgs) * Ho * Wo * ldc;
@@ -379,7 +379,7 @@ __global__ void im2col_act_kernel(const float* __restrict__ x, int imgs, int hp,
             const int wo = static_cast<int>(pix % Wo);
             const int ho = static_cast<int>((pix / Wo) % Ho);
             const long long n = pix / (static_cast<long long>(Wo) * Ho);
-            v = x[((n * hp + ho + r) * wp + wo + s) * ldx + c];
+            v = x[((n * hp + ho * st + r) * wp + wo * st + s) * ldx + c];
         }
         dst[i] = v;
     }
@@ -390,7 +390,7 @@ __global__ void im2col_act_kernel(const float* __restrict__ x, int imgs, int hp,
 // [(r*k + s)*C + c] over valid output positions (fixed order: deterministic).
 // Channels [c0, c0 + nc) go to dst[(img*H + y)*W + x][c - c0] (a merge slot).
 __global__ void col2im_kernel(const float* __restrict__ dcols, long long ldk, int imgs, int H, int W, int C, int k,
-                              int p, int Ho, int Wo, int c0, int nc, float* __restrict__ dst, long long ldo) {
+                              int p, int Ho, int Wo, int c0, int nc, float* __restrict__ dst, long long ldo, int st) {
     griddep_wait();  // programmatic launch: the predecessor's results are visible after this
     const long long total = static_cast<long long>(imgs) * H * W * nc;
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
@@ -403,11 +403,15 @@ __global__ void col2im_kernel(const float* __restrict__ dcols, long long ldk, in
         const int c = c0 + cc;
         float g = 0.f;
         for (int r = 0; r < k; ++r) {
-            const int oy = y + p - r;
-            if (oy < 0 || oy >= Ho) continue;
+            const int sy = y + p - r;  // = oy * st
+            if (sy < 0 || sy % st) continue;
+            const int oy = sy / st;
+            if (oy >= Ho) continue;
             for (int s = 0; s < k; ++s) {
-                const int ox = x + p - s;
-                if (ox < 0 || ox >= Wo) continue;
+                const int sx = x + p - s;
+                if (sx < 0 || sx % st) continue;
+                const int ox = sx / st;
+                if (ox >= Wo) continue;
                 g += dcols[((n * Ho + oy) * Wo + ox) * ldk + (r * k + s) * C + c];
             }
         }
@@ -1096,19 +1100,21 @@ cudaError_t launch_im2col_input(const double* src64, const float* src32, int img
 }
 
 cudaError_t launch_im2col_act(const float* x, int imgs, int hp, int wp, long long ldx, int C, int k, int Ho, int Wo,
-                              float* dst, long long ldc, cudaStream_t s) {
+                              float* dst, long long ldc, cudaStream_t s, int stride) {
     const long long n = static_cast<long long>(imgs) * Ho * Wo * ldc;
     if (n <= 0) return cudaSuccess;
-    pdl_launch(im2col_act_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, x, imgs, hp, wp, ldx, C, k, Ho, Wo, dst, ldc);
+    pdl_launch(im2col_act_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, x, imgs, hp, wp, ldx, C, k, Ho, Wo, dst, ldc,
+               stride);
     return cudaGetLastError();
 }
 
 cudaError_t launch_col2im(const float* dcols, long long ldk, int imgs, int H, int W, int C, int k, int p, int c0,
-                          int nc, float* dst, long long ldo, cudaStream_t s) {
+                          int nc, float* dst, long long ldo, cudaStream_t s, int stride) {
     const long long n = static_cast<long long>(imgs) * H * W * nc;
     if (n <= 0) return cudaSuccess;
-    const int Ho = H + 2 * p - k + 1, Wo = W + 2 * p - k + 1;
-    pdl_launch(col2im_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, dcols, ldk, imgs, H, W, C, k, p, Ho, Wo, c0, nc, dst, ldo);
+    const int Ho = (H + 2 * p - k) / stride + 1, Wo = (W + 2 * p - k) / stride + 1;
+    pdl_launch(col2im_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, dcols, ldk, imgs, H, W, C, k, p, Ho, Wo, c0, nc, dst, ldo,
+               stride);
     return cudaGetLastError();
 }
 

@@ -76,9 +76,9 @@ cudaError_t launch_im2col_input(const double* src64, const float* src32, int img
 // (tap, c), zero beyond k*k*C) and the col2im of a partial input gradient into
 // a merge slot (channels [c0, c0 + nc)).  See kernels.cu.
 cudaError_t launch_im2col_act(const float* x, int imgs, int hp, int wp, long long ldx, int C, int k, int Ho, int Wo,
-                              float* dst, long long ldc, cudaStream_t s);
+                              float* dst, long long ldc, cudaStream_t s, int stride = 1);
 cudaError_t launch_col2im(const float* dcols, long long ldk, int imgs, int H, int W, int C, int k, int p, int c0,
-                          int nc, float* dst, long long ldo, cudaStream_t s);
+                          int nc, float* dst, long long ldo, cudaStream_t s, int stride = 1);
 
 // Small-grid conv as a dense layer (kernels.cu: DenseConvGeom): expansion of
 // W into Wx, and the fold of dWx + SGD on W + re-expansion.

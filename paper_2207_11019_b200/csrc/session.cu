@@ -219,8 +219,8 @@ Session::Session(const std::vector<int>& device_map, const NetDesc& net, const d
         if (li.in_units < 1 || li.out_units < 1)
             throw std::invalid_argument("layer " + S(l + 1) + ": empty weight matrix");
         if (li.kind == 1) {
-            if (li.ksz < 1 || li.pad < 0 || li.pool < 1 || (!li.pool_avg && li.pool > 2) || li.Ho() < 1 ||
-                li.Wo() < 1 || li.Ho() % li.pool || li.Wo() % li.pool)
+            if (li.ksz < 1 || li.pad < 0 || li.pool < 1 || (!li.pool_avg && li.pool > 2) || li.stride < 1 ||
+                li.Ho() < 1 || li.Wo() < 1 || li.Ho() % li.pool || li.Wo() % li.pool || (l == 0 && li.stride > 1))
                 throw std::invalid_argument("layer " + S(l + 1) + ": invalid conv geometry");
             ConvShape cs;
             cs.N = 1;
@@ -230,7 +230,7 @@ Session::Session(const std::vector<int>& device_map, const NetDesc& net, const d
             cs.ksz = li.ksz;
             cs.pad = li.pad;
             cs.u = li.out_units;
-            if (!conv_implicit_ok(cs)) {
+            if (!conv_implicit_ok(cs) || li.stride > 1) {
                 // generic path: explicit im2col rows + dense GEMMs (layer 1: the
                 // staged im2col of X), unpadded error signal
                 if (l == 0) li.im2col = true;
@@ -477,7 +477,7 @@ void Session::alloc_buffers() {
         for (int i = L - 1; i >= 1 && !off; --i) {
             LayerInfo& li = net_.info[i];
             if (li.kind != 1 || li.generic || li.im2col || li.H * li.W > 4 || li.in_units % 4 != 0 ||
-                li.ksz * li.ksz > 25 || cfg_.precision != 0 || li.special() || skip_source(i + 1))
+                li.ksz * li.ksz > 25 || cfg_.precision != 0 || li.special() || skip_source(i + 1) || li.stride > 1)
                 continue;
             bool ok = true;
             for (int wi : layer_workers_[i + 1]) ok = ok && workers_[wi]->at(i + 1).u % 32 == 0;
@@ -983,11 +983,12 @@ void Session::build_ops() {
                         const ActLayout& a = lay_[l - 1];
                         const float* x = act_buf(w.gpu, l - 1) + aoff(l - 1, j) * img_elems(l - 1);
                         float* cols = wl.cols + so * li.Ho() * li.Wo() * wl.ldc;
-                        const int hp = a.hp, wp = a.wp, C = li.in_units, k = li.ksz, Ho = li.Ho(), Wo = li.Wo();
+                        const int hp = a.hp, wp = a.wp, C = li.in_units, k = li.ksz, Ho = li.Ho(), Wo = li.Wo(),
+                                  st1 = li.stride;
                         const long long ldx = a.ld, ldc = wl.ldc;
                         cudaStream_t st = w.sf;
                         const int iop = add_op(w.gpu, st, [=]() {
-                            return launch_im2col_act(x, rows, hp, wp, ldx, C, k, Ho, Wo, cols, ldc, st);
+                            return launch_im2col_act(x, rows, hp, wp, ldx, C, k, Ho, Wo, cols, ldc, st, st1);
                         }, deps, 1, OP_POOL);
                         deps = {iop};
                         const int kc = k * k * C;
@@ -1401,7 +1402,8 @@ void Session::build_ops() {
                         const float* dc = wl.dcols + so * drows * wl.ldk;
                         const bool dcv = li.dense_conv;
                         const long long ldk = dcv ? li.in_units : wl.ldk;  // dense conv: pixel-major [img*Q][C]
-                        const int H = li.H, W = li.W, C = li.in_units, ks = dcv ? 1 : li.ksz, pd = dcv ? 0 : li.pad;
+                        const int H = li.H, W = li.W, C = li.in_units, ks = dcv ? 1 : li.ksz, pd = dcv ? 0 : li.pad,
+                                  strd = li.stride;
                         for (int di : direct ? std::vector<int>{} : dests) {
                             WLayer& dl = workers_[di]->at(l - 1);
                             float* dst = dl.slots[k] + so * H * W * dl.slot_ld;
@@ -1409,7 +1411,7 @@ void Session::build_ops() {
                             const int c0 = dl.lo, nc = dl.u;
                             cudaStream_t st = w.sb;
                             op = add_op(w.gpu, st, [=]() {
-                                return launch_col2im(dc, ldk, rows, H, W, C, ks, pd, c0, nc, dst, ldo, st);
+                                return launch_col2im(dc, ldk, rows, H, W, C, ks, pd, c0, nc, dst, ldo, st, strd);
                             }, {op}, 1, OP_CONV_MERGE);
                         }
                         w.last_bwd[j] = std::max(w.last_bwd[j], op);

@@ -51,8 +51,9 @@ struct LayerInfo {
     // input and output stored unpadded NHWC
     bool dense_conv = false;
     int dq() const { return dense_delta ? 0 : ksz - 1 - pad; }  // zero ring of the stored error signal
-    int Ho() const { return H + 2 * pad - ksz + 1; }
-    int Wo() const { return W + 2 * pad - ksz + 1; }
+    int stride = 1;  // conv stride (> 1: the generic im2col path)
+    int Ho() const { return (H + 2 * pad - ksz) / stride + 1; }
+    int Wo() const { return (W + 2 * pad - ksz) / stride + 1; }
     int Hq() const { return Ho() / pool; }
     int Wq() const { return Wo() / pool; }
     long long in_features() const { return kind ? static_cast<long long>(in_units) * H * W : in_units; }

@@ -286,7 +286,7 @@ def test_cnn_oracle_residual_matches_independent_restatement():
                 continue
             c = lay.conv
             k = c.ksize
-            q = Fn.conv2d(a, w.reshape(w.shape[0], k, k, -1).permute(0, 3, 1, 2), bb, padding=c.pad)
+            q = Fn.conv2d(a, w.reshape(w.shape[0], k, k, -1).permute(0, 3, 1, 2), bb, padding=c.pad, stride=c.stride)
             if c.res_from:
                 src = outs[c.res_from - 1]
                 f = src.shape[2] // q.shape[2]

@@ -52,9 +52,8 @@ def model_doc(net):
         out_feat = layer.fan_out()
         if layer.conv is not None:
             c = layer.conv
-            ho = c.height + 2 * c.pad - c.ksize + 1
-            wo = c.width + 2 * c.pad - c.ksize + 1
-            out_feat = layer.fan_out() * (ho // c.pool) * (wo // c.pool)
+            ho, wo = c.out_hw()
+            out_feat = layer.fan_out() * ho * wo
         layers.append({"kind": "dense", "fan_in": spec.fan_in, "fan_out": spec.fan_out,
                        "param_count": int(layer.weights.size + layer.bias.size),
                        "fwd_flops": float(spec.fwd_flops), "bwd_flops": 2.0 * float(spec.fwd_flops),
