@@ -385,6 +385,75 @@ __global__ void im2col_act_kernel(const float* __restrict__ x, int imgs, int hp,
     }
 }
 
+// Vectorised im2col for C % 4 == 0 (the generic path's strided convs, e.g.
+// ResNet-18's stage transitions): thread = (output pixel, tap, 4 channels),
+// one float4 load / store; consecutive threads walk a tap's contiguous
+// channels, so reads and writes coalesce.  Columns >= k*k*C (row padding)
+// are never written (zero since allocation).
+template <class IDX>
+__global__ void im2col_act_vec_kernel(const float* __restrict__ x, int imgs, int hp, int wp, long long ldx, int C,
+                                      int k, int Ho, int Wo, float* __restrict__ dst, long long ldc, int st) {
+    griddep_wait();
+    const int groups = C >> 2, kk = k * k;
+    const IDX total = static_cast<IDX>(imgs) * Ho * Wo * kk * groups;
+    for (IDX i = blockIdx.x * static_cast<IDX>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<IDX>(gridDim.x) * blockDim.x) {
+        const int c4 = static_cast<int>(i % groups);
+        const IDX t = i / groups;
+        const int tap = static_cast<int>(t % kk);
+        const IDX pix = t / kk;
+        const int wo = static_cast<int>(pix % Wo);
+        const IDX t2 = pix / Wo;
+        const int ho = static_cast<int>(t2 % Ho);
+        const long long n = static_cast<long long>(t2 / Ho);
+        const int r = tap / k, s = tap - r * k;
+        const float4 v = __ldg(reinterpret_cast<const float4*>(
+            x + ((n * hp + ho * st + r) * wp + wo * st + s) * ldx + c4 * 4));
+        *reinterpret_cast<float4*>(dst + static_cast<long long>(pix) * ldc + tap * C + c4 * 4) = v;
+    }
+}
+
+// Vectorised col2im (C, c0, nc, ldk, ldo multiples of 4): thread = (input
+// pixel, 4 channels of the destination slice); taps summed in ascending
+// (r, s) order as col2im_kernel (same result bits).
+template <class IDX>
+__global__ void col2im_vec_kernel(const float* __restrict__ dcols, long long ldk, int imgs, int H, int W, int C, int k,
+                                  int p, int Ho, int Wo, int c0, int nc, float* __restrict__ dst, long long ldo, int st) {
+    griddep_wait();
+    const int groups = nc >> 2;
+    const IDX total = static_cast<IDX>(imgs) * H * W * groups;
+    for (IDX i = blockIdx.x * static_cast<IDX>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<IDX>(gridDim.x) * blockDim.x) {
+        const int g = static_cast<int>(i % groups);
+        const IDX pix = i / groups;
+        const int x = static_cast<int>(pix % W);
+        const IDX t = pix / W;
+        const int y = static_cast<int>(t % H);
+        const long long n = static_cast<long long>(t / H);
+        const int c = c0 + g * 4;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int r = 0; r < k; ++r) {
+            const int sy = y + p - r;
+            if (sy < 0 || sy % st) continue;
+            const int oy = sy / st;
+            if (oy >= Ho) continue;
+            for (int s = 0; s < k; ++s) {
+                const int sx = x + p - s;
+                if (sx < 0 || sx % st) continue;
+                const int ox = sx / st;
+                if (ox >= Wo) continue;
+                const float4 v = __ldg(reinterpret_cast<const float4*>(
+                    dcols + ((n * Ho + oy) * Wo + ox) * ldk + (r * k + s) * C + c));
+                acc.x += v.x;
+                acc.y += v.y;
+                acc.z += v.z;
+                acc.w += v.w;
+            }
+        }
+        *reinterpret_cast<float4*>(dst + static_cast<long long>(pix) * ldo + g * 4) = acc;
+    }
+}
+
 // col2im of the partial input gradient: g(img, y, x, c) for the input grid
 // H x W = sum over taps (r, s) ascending of dcols[(img, y + p - r, x + p - s)]
 // [(r*k + s)*C + c] over valid output positions (fixed order: deterministic).
@@ -1103,6 +1172,17 @@ cudaError_t launch_im2col_act(const float* x, int imgs, int hp, int wp, long lon
                               float* dst, long long ldc, cudaStream_t s, int stride) {
     const long long n = static_cast<long long>(imgs) * Ho * Wo * ldc;
     if (n <= 0) return cudaSuccess;
+    if (C % 4 == 0 && ldx % 4 == 0 && ldc % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 &&
+        reinterpret_cast<uintptr_t>(dst) % 16 == 0) {
+        const long long nv = static_cast<long long>(imgs) * Ho * Wo * k * k * (C / 4);
+        if (nv < (1LL << 31))
+            pdl_launch(im2col_act_vec_kernel<unsigned>, dim3(grid_for(nv, 256)), dim3(256), 0, s, x, imgs, hp, wp, ldx,
+                       C, k, Ho, Wo, dst, ldc, stride);
+        else
+            pdl_launch(im2col_act_vec_kernel<long long>, dim3(grid_for(nv, 256)), dim3(256), 0, s, x, imgs, hp, wp,
+                       ldx, C, k, Ho, Wo, dst, ldc, stride);
+        return cudaGetLastError();
+    }
     pdl_launch(im2col_act_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, x, imgs, hp, wp, ldx, C, k, Ho, Wo, dst, ldc,
                stride);
     return cudaGetLastError();
@@ -1113,6 +1193,17 @@ cudaError_t launch_col2im(const float* dcols, long long ldk, int imgs, int H, in
     const long long n = static_cast<long long>(imgs) * H * W * nc;
     if (n <= 0) return cudaSuccess;
     const int Ho = (H + 2 * p - k) / stride + 1, Wo = (W + 2 * p - k) / stride + 1;
+    if (C % 4 == 0 && c0 % 4 == 0 && nc % 4 == 0 && ldk % 4 == 0 && ldo % 4 == 0 &&
+        reinterpret_cast<uintptr_t>(dcols) % 16 == 0 && reinterpret_cast<uintptr_t>(dst) % 16 == 0) {
+        const long long nv = n / 4;
+        if (nv < (1LL << 31))
+            pdl_launch(col2im_vec_kernel<unsigned>, dim3(grid_for(nv, 256)), dim3(256), 0, s, dcols, ldk, imgs, H, W, C,
+                       k, p, Ho, Wo, c0, nc, dst, ldo, stride);
+        else
+            pdl_launch(col2im_vec_kernel<long long>, dim3(grid_for(nv, 256)), dim3(256), 0, s, dcols, ldk, imgs, H, W,
+                       C, k, p, Ho, Wo, c0, nc, dst, ldo, stride);
+        return cudaGetLastError();
+    }
     pdl_launch(col2im_kernel, dim3(grid_for(n, 256)), dim3(256), 0, s, dcols, ldk, imgs, H, W, C, k, p, Ho, Wo, c0, nc, dst, ldo,
                stride);
     return cudaGetLastError();
