@@ -189,8 +189,26 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         }
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer (leader CTA)
-        if (leader) {
+        // One elected thread runs the whole issue loop; descriptors are built
+        // once and advanced by address adds (desc_advance).  Per tap the issue
+        // cost was ~124 instructions (descriptor re-derivation, re-election)
+        // against 4 x 58 tensor cycles at N = 64: the kernel was issue-bound
+        // (ncu source page: the MMA warp never waited, the epilogue and the
+        // halo producer waited on it).
+        if (leader && elect_one()) {
             constexpr uint32_t idesc = idesc_tf32(BN, false, B_MN, TM);
+            constexpr uint32_t b_kk = B_MN ? 1024 : 32;
+            const uint64_t h0 = umma_desc<kLayoutSW128>(smem_u32(sH), 16, 1024);
+            const uint64_t b0 = B_MN ? umma_desc<kLayoutSW128Base32>(smem_u32(sB), 4096, 512)
+                                     : umma_desc<kLayoutSW128>(smem_u32(sB), 16, 1024);
+            uint32_t roff[9];  // tap (r, s) = halo row shift r * wp + s, in bytes
+#pragma unroll
+            for (int tap = 0; tap < 9; ++tap) {
+                int ro = (tap / 3) * hg.wp + tap % 3;
+                if (hg.dbg & 1) ro &= ~7;  // timing probe only (wrong results)
+                roff[tap] = static_cast<uint32_t>(ro) * 128u;
+            }
+            const bool no_mma = (hg.dbg & 8) != 0;  // timing probe (DEV builds only)
             int hs = 0, bs = 0;
             uint32_t hph = 0, bph = 0;
             int local = 0;
@@ -202,9 +220,9 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 const uint32_t d_tmem = tmem_base + acc * BN;
                 for (int cb = 0; cb < cblocks; ++cb) {
                     if (!(hg.dbg & 4) || local == 0) mbar_wait(&hfull[hs], hph);
-                    const uint32_t h_addr = smem_u32(sH + hs * kHaloStageBytes);
+                    const uint64_t hd = desc_advance(h0, hs * kHaloStageBytes);
+#pragma unroll
                     for (int tap = 0; tap < 9; ++tap) {
-                        const int r = tap / 3, s = tap - 3 * (tap / 3);
                         const int kb = tap * cblocks + cb;
                         if (hg.resident) {
                             if (local == 0) mbar_wait(&bfull[kb], 0);
@@ -212,49 +230,41 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                             mbar_wait(&bfull[bs], bph);
                         }
                         tc_fence_after();
-                        if (elect_one()) {
-                            int roff = r * hg.wp + s;
-                            if (hg.dbg & 1) roff &= ~7;  // timing probe only (wrong results)
-                            const uint32_t a_addr = h_addr + static_cast<uint32_t>(roff) * 128u;
-                            const uint32_t b_addr = smem_u32(sB + (hg.resident ? kb : bs) * C::kStageB);
+                        const uint64_t ad = desc_advance(hd, roff[tap]);
+                        const uint64_t bd = desc_advance(b0, (hg.resident ? kb : bs) * C::kStageB);
+                        if (!no_mma) {
 #pragma unroll
                             for (int kk = 0; kk < kBK / 8; ++kk) {
-                                const uint64_t ad = umma_desc<kLayoutSW128>(a_addr + kk * 32, 16, 1024);
-                                const uint64_t bd = B_MN ? umma_desc<kLayoutSW128Base32>(b_addr + kk * 1024, 4096, 512)
-                                                         : umma_desc<kLayoutSW128>(b_addr + kk * 32, 16, 1024);
                                 const uint32_t accum = (cb != 0 || tap != 0 || kk != 0) ? 1u : 0u;
-                                if (hg.dbg & 8) continue;  // timing probe: no MMAs
-                                if (CG == 2) mma_tf32_pair(d_tmem, ad, bd, idesc, accum);
-                                else mma_tf32(d_tmem, ad, bd, idesc, accum);
-                            }
-                            if (!hg.resident) {
-                                if (CG == 2) mma_commit_pair(&bempty[bs]);
-                                else mma_commit(&bempty[bs]);
+                                if (CG == 2)
+                                    mma_tf32_pair(d_tmem, desc_advance(ad, kk * 32), desc_advance(bd, kk * b_kk),
+                                                  idesc, accum);
+                                else
+                                    mma_tf32(d_tmem, desc_advance(ad, kk * 32), desc_advance(bd, kk * b_kk), idesc,
+                                             accum);
                             }
                         }
-                        __syncwarp();
-                        if (!hg.resident && ++bs == kBStages) {
-                            bs = 0;
-                            bph ^= 1;
+                        if (!hg.resident) {
+                            if (CG == 2) mma_commit_pair(&bempty[bs]);
+                            else mma_commit(&bempty[bs]);
+                            if (++bs == kBStages) {
+                                bs = 0;
+                                bph ^= 1;
+                            }
                         }
                     }
-                    if (elect_one()) {
-                        if (CG == 2) mma_commit_pair(&hempty[hs]);
-                        else mma_commit(&hempty[hs]);
-                    }
-                    __syncwarp();
+                    if (CG == 2) mma_commit_pair(&hempty[hs]);
+                    else mma_commit(&hempty[hs]);
                     if (++hs == kHaloStages) {
                         hs = 0;
                         hph ^= 1;
                     }
                 }
-                if (elect_one()) {
-                    if (CG == 2) mma_commit_pair(&tfull[acc]);
-                    else mma_commit(&tfull[acc]);
-                }
-                __syncwarp();
+                if (CG == 2) mma_commit_pair(&tfull[acc]);
+                else mma_commit(&tfull[acc]);
             }
         }
+        __syncwarp();
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue
         const int q = warp & 3;              // TMEM lane quarter this warp may access

@@ -328,8 +328,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer (leader CTA)
-        if (leader) {
+        // The whole issue loop runs on ONE elected thread with the operand
+        // descriptors built once and advanced by adding to their start-address
+        // field (desc_advance): re-deriving 8 descriptors per K block and
+        // re-electing per block cost ~75 issue slots per 4 MMAs, more than
+        // the 4 x 58 tensor cycles of an N = 64 pair block.
+        if (leader && elect_one()) {
             constexpr uint32_t idesc = idesc_tf32(BN, A_MN, B_MN, TM);
+            // K-major (SW128): the K8 step advances 32 B inside the 128 B swizzle
+            // atom; 8-row groups 1 KB apart (SBO).  MN-major (SW128_BASE32B):
+            // the K8 step advances 8 K rows (1 KB); 4-row K groups 512 B apart
+            // (SBO), 32-wide MN atoms 4 KB apart (LBO).
+            const uint64_t a0 = A_MN ? umma_desc<kLayoutSW128Base32>(smem_u32(sA), 4096, 512)
+                                     : umma_desc<kLayoutSW128>(smem_u32(sA), 16, 1024);
+            const uint64_t b0 = B_MN ? umma_desc<kLayoutSW128Base32>(smem_u32(sB), 4096, 512)
+                                     : umma_desc<kLayoutSW128>(smem_u32(sB), 16, 1024);
+            constexpr uint32_t a_kk = A_MN ? 1024 : 32, b_kk = B_MN ? 1024 : 32;
+            const bool no_mma = (epi.dbg & 8) != 0;  // timing probe (DEV builds only)
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
@@ -344,41 +359,32 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kb = kb0; kb < kb_end; ++kb) {
                     mbar_wait(&full_bar[stage], phase);
                     tc_fence_after();
-                    if (elect_one()) {
-                        const uint32_t a_addr = smem_u32(sA + stage * C::kStageA);
-                        const uint32_t b_addr = smem_u32(sB + stage * C::kStageB);
+                    const uint64_t ad = desc_advance(a0, stage * C::kStageA);
+                    const uint64_t bd = desc_advance(b0, stage * C::kStageB);
+                    if (!no_mma) {
 #pragma unroll
                         for (int kk = 0; kk < kBK / 8; ++kk) {
-                            // K-major (SW128): advance 32 B inside the 128 B swizzle
-                            // atom; 8-row groups 1 KB apart (SBO).
-                            // MN-major (SW128_BASE32B): advance 8 K rows (1 KB);
-                            // 4-row K groups 512 B apart (SBO), 32-wide MN atoms
-                            // 4 KB apart (LBO).
-                            const uint64_t ad = A_MN ? umma_desc<kLayoutSW128Base32>(a_addr + kk * 1024, 4096, 512)
-                                                     : umma_desc<kLayoutSW128>(a_addr + kk * 32, 16, 1024);
-                            const uint64_t bd = B_MN ? umma_desc<kLayoutSW128Base32>(b_addr + kk * 1024, 4096, 512)
-                                                     : umma_desc<kLayoutSW128>(b_addr + kk * 32, 16, 1024);
                             const uint32_t accum = (kb != kb0 || kk != 0) ? 1u : 0u;
-                            if (epi.dbg & 8) continue;  // timing probe: no MMAs
-                            if (CG == 2) mma_tf32_pair(d_tmem, ad, bd, idesc, accum);
-                            else mma_tf32(d_tmem, ad, bd, idesc, accum);
+                            if (CG == 2)
+                                mma_tf32_pair(d_tmem, desc_advance(ad, kk * a_kk), desc_advance(bd, kk * b_kk), idesc,
+                                              accum);
+                            else
+                                mma_tf32(d_tmem, desc_advance(ad, kk * a_kk), desc_advance(bd, kk * b_kk), idesc,
+                                         accum);
                         }
-                        if (CG == 2) mma_commit_pair(&empty_bar[stage]);
-                        else mma_commit(&empty_bar[stage]);
                     }
-                    __syncwarp();
+                    if (CG == 2) mma_commit_pair(&empty_bar[stage]);
+                    else mma_commit(&empty_bar[stage]);
                     if (++stage == nst) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                if (elect_one()) {
-                    if (CG == 2) mma_commit_pair(&tfull_bar[acc]);
-                    else mma_commit(&tfull_bar[acc]);
-                }
-                __syncwarp();
+                if (CG == 2) mma_commit_pair(&tfull_bar[acc]);
+                else mma_commit(&tfull_bar[acc]);
             }
         }
+        __syncwarp();
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue
         const int q = warp & 3;              // TMEM lane quarter this warp may access

@@ -276,6 +276,13 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t smem_addr, uint32_t lbo_b
     return d;
 }
 
+// Move a descriptor's start address by `bytes` (a multiple of 16): the field
+// holds addr >> 4 in bits [0, 14) and shared-window addresses stay below
+// 256 KB, so the add never carries into the LBO field.
+__device__ __forceinline__ uint64_t desc_advance(uint64_t desc, uint32_t bytes) {
+    return desc + static_cast<uint64_t>(bytes >> 4);
+}
+
 // Instruction descriptor for kind::tf32, fp32 accumulator, M = 128 (1 CTA)
 // or 256 (CTA pair).
 __host__ __device__ constexpr uint32_t idesc_tf32(int n, bool a_mn, bool b_mn, int m = 128) {
