@@ -52,7 +52,10 @@ template <int BN, int CG>
 struct HaloCfg {
     static constexpr int kBNc = BN / CG;
     static constexpr int kStageB = kBNc * kBK * 4;
-    static constexpr int kTmemCols = 2 * BN;
+    // accumulator ring: 4 deep up to BN = 128 (the epilogue of a narrow tile
+    // can lag the MMAs by more than one tile), 2 at BN = 256 (512 columns)
+    static constexpr int kAcc = BN <= 128 ? 4 : 2;
+    static constexpr int kTmemCols = kAcc * BN;
 };
 
 template <bool B_MN, int BN, int CG>
@@ -72,9 +75,9 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
     uint64_t* hempty = hfull + kHaloStages;
     uint64_t* bfull = hempty + kHaloStages;
     uint64_t* bempty = bfull + kBStages;
-    uint64_t* tfull = bempty + kBStages;  // [2]
-    uint64_t* tempty = tfull + 2;            // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* tfull = bempty + kBStages;  // [kAcc]
+    uint64_t* tempty = tfull + C::kAcc;    // [kAcc]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + C::kAcc);
     float* db_s = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(hfull) + 1024);  // [4][ldb] (EPI_MERGE db)
     uint8_t* stg = reinterpret_cast<uint8_t*>(hfull) + ts.stage_off;                    // TMA-store staging
 
@@ -101,7 +104,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             mbar_init(&bfull[s], 1);
             mbar_init(&bempty[s], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < C::kAcc; ++i) {
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], kEpiWarps * CG);
         }
@@ -213,8 +216,8 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             uint32_t hph = 0, bph = 0;
             int local = 0;
             for (int tile = unit; tile < num_tiles; tile += units, ++local) {
-                const int acc = local & 1;
-                const uint32_t acc_phase = (local >> 1) & 1;
+                const int acc = local % C::kAcc;
+                const uint32_t acc_phase = (local / C::kAcc) & 1;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
@@ -291,11 +294,23 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         }
         int local = 0;
         int msel = 0;  // staging box of the next masked chunk (alternates with ts.dbuf)
+        const bool masked = ts.n && ts.mask;
+        // two staging boxes per warp: the mask box of this warp's NEXT chunk
+        // (the next tile's first chunk after the last) is loaded as soon as the
+        // current chunk's store is issued, so its latency hides behind a whole
+        // chunk of epilogue work, not only behind the tile's MMAs
+        const bool ahead = masked && ts.mask_pf && ts.dbuf;
+        auto mask_issue = [&](int t, int c) {
+            const long long pp = static_cast<long long>(t % num_m) * TM + static_cast<long long>(rank) * kBM;
+            tma_mask_issue(ts, epi_box(stg, warp - 4, msel), mbar, lane, static_cast<int>(pp) + q * 32,
+                           (t / num_m) * BN + c * 32, false, ts.dbuf);
+        };
+        if (ahead && unit < num_tiles && half < BN / 32) mask_issue(unit, half);
         for (int tile = unit; tile < num_tiles; tile += units, ++local) {
             const long long p0 = static_cast<long long>(tile % num_m) * TM + static_cast<long long>(rank) * kBM;
             const int n0 = (tile / num_m) * BN;
-            const int acc = local & 1;
-            const uint32_t acc_phase = (local >> 1) & 1;
+            const int acc = local % C::kAcc;
+            const uint32_t acc_phase = (local / C::kAcc) & 1;
             // padded position -> output pixel, -1 on the pad ring / past the end
             const long long pos = p0 + q * 32 + lane;
             int m = -1;
@@ -308,8 +323,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             // the first chunk's ReLU-mask box is loaded while the tile's MMAs run
             // (with two staging boxes per warp, while the previous chunk's store
             // still reads the other box)
-            const bool masked = ts.n && ts.mask;
-            if (masked && ts.mask_pf && half < BN / 32)
+            if (masked && ts.mask_pf && !ahead && half < BN / 32)
                 tma_mask_issue(ts, epi_box(stg, warp - 4, msel), mbar, lane, static_cast<int>(p0) + q * 32,
                                n0 + half * 32, false, ts.dbuf);
             mbar_wait(&tfull[acc], acc_phase);
@@ -324,12 +338,16 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 for (int i = 0; i < 32; ++i) v[i] = m >= 0 ? __uint_as_float(rr[i]) : 0.f;
                 if (masked) {  // the mask is zero on the ring
                     uint8_t* box = epi_box(stg, warp - 4, msel);
-                    if (c != half || !ts.mask_pf)
+                    if (!ahead && (c != half || !ts.mask_pf))
                         tma_mask_issue(ts, box, mbar, lane, static_cast<int>(p0) + q * 32, n0 + c * 32, false,
                                        ts.dbuf);
                     tma_store_masked_issued(ts, box, mbar, mphase, lane, v, static_cast<int>(p0) + q * 32,
                                             n0 + c * 32);
                     msel ^= ts.dbuf;
+                    if (ahead) {
+                        if (c + 2 < BN / 32) mask_issue(tile, c + 2);
+                        else if (tile + units < num_tiles) mask_issue(tile + units, half);
+                    }
                 } else if (ts.n) {  // pad-ring rows store zeros (the destination's own ring)
                     epi_values32(epi, m, n0 + c * 32, v, lane);
                     if (m < 0) {
@@ -346,7 +364,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                if (CG == 2) mbar_arrive_cluster(tempty_leader + acc * sizeof(uint64_t));
+                if (CG == 2) mbar_arrive_remote_n(tempty_leader + acc * sizeof(uint64_t), 1);
                 else mbar_arrive(&tempty[acc]);
             }
         }
@@ -457,13 +475,13 @@ bool halo_conv_eligible(const GemmDesc& d) {
 // MN-major (flipped-weight) B at N >= 128 streams B beside the halo (conv4
 // dgrad 113.7 vs 97.3 us).  Step 2.270 -> 2.244 ms.
 bool halo_conv_preferred(const GemmDesc& d) {
-    static const bool always = getenv("PPB_HALO_ALWAYS") != nullptr;
+    static const bool always = dev_knob("PPB_HALO_ALWAYS");
     if (always) return true;
     if (d.epi.mode == EPI_MERGE && d.epi.mg_pool == 2) return false;
     if (d.b.mn_major && d.N >= 128) return false;
     // pre-pool output rows (not a padded grid: the halo epilogue would fall back
     // to per-thread stores) at N <= 64: conv2 forward 158.7 vs 152.5 us
-    static const bool u64 = getenv("PPB_HALO_U64") == nullptr;
+    static const bool u64 = !dev_knob("PPB_HALO_U64");
     if (u64 && d.epi.mode == EPI_STORE && !d.epi.remap && d.N <= 64) return false;
     return true;
 }
@@ -540,7 +558,7 @@ bool halo_conv_prepare(const GemmDesc& d, TcGemmPlan* out, int force, char* err,
             }
         }
         const int avail = kHaloSmemMax - kHaloReserve - extra;
-        if (one_col && nkb * stage_b + 2 * hg.hstage_bytes <= avail && !getenv("PPB_HALO_STREAM_B")) {
+        if (one_col && nkb * stage_b + 2 * hg.hstage_bytes <= avail && !dev_knob("PPB_HALO_STREAM_B")) {
             hg.resident = 1;
             hg.bstages = nkb;
             hg.hstages = (avail - nkb * stage_b) / hg.hstage_bytes;
@@ -556,7 +574,7 @@ bool halo_conv_prepare(const GemmDesc& d, TcGemmPlan* out, int force, char* err,
             }
         }
         hg.smem = 1024 + hg.hstages * hg.hstage_bytes + hg.bstages * stage_b + 1024 + extra;
-        if (2 * (hg.hstages + hg.bstages + 2) * 8 + 8 > 1024) {
+        if (2 * (hg.hstages + hg.bstages + 4) * 8 + 8 > 1024) {
             snprintf(err, errlen, "halo conv: too many pipeline barriers");
             return false;
         }

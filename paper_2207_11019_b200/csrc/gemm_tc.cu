@@ -151,7 +151,7 @@ bool encode_conv_map(CUtensorMap* map, const Operand& o, char* err, size_t errle
 // (2y + dy, 2x + dx); the mask map covers the pooled activation.
 static bool tma_store_setup_pool2(const EpiParams& e, int M, int N, TmaStore* ts) {
     auto enc = get_encode();
-    static const bool off = getenv("PPB_NO_TMA_POOL2") != nullptr;
+    static const bool off = dev_knob("PPB_NO_TMA_POOL2");
     if (off || enc == nullptr || N % 32 != 0 || M <= 0 || e.mg_dld % 4 != 0 || e.mg_uch % 4 != 0 ||
         (reinterpret_cast<uintptr_t>(e.mg_argmax) & 3u) != 0)
         return false;
@@ -222,10 +222,7 @@ bool tma_store_setup(const EpiParams& e, int M, int N, const HaloGeom* hg, TmaSt
     ts->mask_pf = dev_knob("PPB_NO_MASK_PREFETCH") ? 0 : 1;  // A/B switch (DEV builds)
     ts->n = 0;
     ts->pool2 = 0;
-    static const bool off = [] {
-        const char* v = getenv("PPB_NO_TMA_STORE");
-        return v != nullptr && *v != '\0' && *v != '0';
-    }();
+    static const bool off = dev_knob("PPB_NO_TMA_STORE");
     auto enc = get_encode();
     if (off || enc == nullptr || N < 32 || M <= 0) return false;
     if (e.mode == EPI_MERGE && e.mg_pool == 2) return hg == nullptr && tma_store_setup_pool2(e, M, N, ts);
@@ -356,7 +353,7 @@ bool tma_store_setup(const EpiParams& e, int M, int N, const HaloGeom* hg, TmaSt
         mld = e.ldm;
     }
     ts->mask = 0;
-    static const bool no_mask = getenv("PPB_NO_TMA_MASK") != nullptr;
+    static const bool no_mask = dev_knob("PPB_NO_TMA_MASK");
     if (mptr != nullptr && no_mask) return false;
     if (mptr != nullptr) {
         if ((reinterpret_cast<uintptr_t>(mptr) & 15u) != 0 || mld % 4 != 0) return false;
@@ -382,12 +379,9 @@ bool tma_store_setup(const EpiParams& e, int M, int N, const HaloGeom* hg, TmaSt
 
 bool tma_store_setup_splitk(const SplitK& sk, int M, int N, TmaStore* ts) {
     ts->n = 0;
-    static const bool off = [] {
-        const char* v = getenv("PPB_NO_TMA_STORE");
-        return v != nullptr && *v != '\0' && *v != '0';
-    }();
+    static const bool off = dev_knob("PPB_NO_TMA_STORE");
     auto enc = get_encode();
-    static const bool off_sk = getenv("PPB_NO_TMA_SPLITK") != nullptr;
+    static const bool off_sk = dev_knob("PPB_NO_TMA_SPLITK");
     if (off || off_sk || enc == nullptr || (sk.splits < 2 && !sk.partial) || sk.ws == nullptr) return false;
     const int inner = sk.trans ? M : N, outer = sk.trans ? N : M;
     if (inner < 32 || sk.ld % 4 != 0 || sk.stride % 4 != 0 || (reinterpret_cast<uintptr_t>(sk.ws) & 15u) != 0)
@@ -443,10 +437,7 @@ cudaError_t tc_gemm_init_device() {
 bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err, size_t errlen,
                      const WsAlloc& ws_alloc) {
     // 3x3 convs over large padded grids: the halo-reuse kernel (conv_halo.cu)
-    static const bool no_halo = [] {
-        const char* e = getenv("PPB_NO_HALO");
-        return e != nullptr && *e != '\0' && *e != '0';
-    }();
+    static const bool no_halo = dev_knob("PPB_NO_HALO");
     if (!d.partial_out && (force_bn >= 1000 || (force_bn == 0 && !no_halo && halo_conv_preferred(d))) &&
         halo_conv_eligible(d))
         return halo_conv_prepare(d, out, force_bn, err, errlen);
@@ -510,10 +501,10 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
         // wgrad + SGD (reduction free as a side job): the operand-bound table
         // picks slightly better tiles (2.238 -> 2.233 ms); elsewhere it prefers
         // split-K whose reduction costs more than modelled
-        static const bool sgd_std = getenv("PPB_SGD_STDTABLE") != nullptr;
+        static const bool sgd_std = dev_knob("PPB_SGD_STDTABLE");
         const Cand* cands = (!sgd_std && d.epi.mode == EPI_SGD) ? cands_op : cands_std;
         double best = -1;
-        static const bool no_pair64 = getenv("PPB_NO_PAIR64") != nullptr;  // A/B switch
+        static const bool no_pair64 = dev_knob("PPB_NO_PAIR64");  // A/B switch
         for (int ci = 0; ci < 6; ++ci) {
             const Cand& c = cands[ci];
             if (no_pair64 && c.cg == 2 && c.bn == 64) continue;
@@ -633,7 +624,7 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
         const int extra = off + kEpiStageBytes - 256;
         int st = p.stages;
         while (ring(st) + extra > kCapSmem && st > 4) --st;
-        static const bool no_dbuf = getenv("PPB_NO_STAGE_DBUF") != nullptr;  // A/B switch
+        static const bool no_dbuf = dev_knob("PPB_NO_STAGE_DBUF");  // A/B switch
         if (ring(st) + extra <= kCapSmem) {
             p.stages = st;
             p.ts.stage_off = off;

@@ -48,7 +48,10 @@ struct TcCfg {
     static constexpr int kStageB = kBNc * kBK * 4;
     static constexpr int kStageBytes = kStageA + kStageB;
     static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
-    static constexpr int kTmemCols = 2 * BN;
+    // accumulator ring: 4 deep up to BN = 128 (512 TMEM columns at most), 2 at
+    // BN = 256; by-tile epilogues give each warp group every other accumulator
+    static constexpr int kAcc = BN <= 128 ? 4 : 2;
+    static constexpr int kTmemCols = kAcc * BN;
 };
 
 // One split-K work item (row r, columns c4..c4+3 of the workspace): sum the
@@ -234,9 +237,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* sB = smem + nst * C::kStageA;  // nst <= C::kStages ring stages (host: smem budget)
     uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + nst * C::kStageBytes);
     uint64_t* empty_bar = full_bar + nst;
-    uint64_t* tfull_bar = empty_bar + nst;   // [2]
-    uint64_t* tempty_bar = tfull_bar + 2;            // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+    uint64_t* tfull_bar = empty_bar + nst;       // [kAcc]
+    uint64_t* tempty_bar = tfull_bar + C::kAcc;  // [kAcc]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + C::kAcc);
     float* db_s = reinterpret_cast<float*>(smem + nst * C::kStageBytes + 256);  // [4][ldb] (EPI_MERGE db)
     uint8_t* stg = smem + nst * C::kStageBytes + ts.stage_off;                  // TMA-store staging
 
@@ -259,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&full_bar[s], 2);  // the A and the B producer each arrive (with their tx bytes)
             mbar_init(&empty_bar[s], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < C::kAcc; ++i) {  // nst <= 8: 2 * 8 + 2 * 4 barriers + slot fit the 256 B block
             mbar_init(&tfull_bar[i], 1);
             mbar_init(&tempty_bar[i], kEpiWarps * CG);  // one arrival per epilogue warp of the pair
         }
@@ -349,8 +352,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t phase = 0;
             int local = 0;
             for (int tile = unit; tile < num_tiles; tile += units, ++local) {
-                const int acc = local & 1;
-                const uint32_t acc_phase = (local >> 1) & 1;
+                const int acc = local % C::kAcc;
+                const uint32_t acc_phase = (local / C::kAcc) & 1;
                 mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
@@ -423,8 +426,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int mn = tile % num_mn, split = tile / num_mn;
             const int m0 = (mn % num_m) * TM + static_cast<int>(rank) * kBM;
             const int n0 = (mn / num_m) * BN;
-            const int acc = local & 1;
-            const uint32_t acc_phase = (local >> 1) & 1;
+            const int acc = local % C::kAcc;
+            const uint32_t acc_phase = (local / C::kAcc) & 1;
             // masked epilogues: the first chunk's ReLU-mask box is loaded while
             // the tile's MMAs run (its latency was exposed once per tile)
             const bool masked = ts.n && ts.mask && !(sk.splits > 1 || sk.partial) && !(epi.dbg & 4);
@@ -513,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) {
                 const uint32_t cnt = by_tile ? 2u : 1u;  // by_tile: 4 warps stand for all 8
-                if (CG == 2) mbar_arrive_cluster_n(tempty_leader + acc * sizeof(uint64_t), cnt);
+                if (CG == 2) mbar_arrive_remote_n(tempty_leader + acc * sizeof(uint64_t), cnt);
                 else mbar_arrive_n(&tempty_bar[acc], cnt);
             }
             if (sk.splits > 1 && sk.fixup && !(epi.dbg & 6)) {

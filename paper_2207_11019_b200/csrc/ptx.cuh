@@ -206,6 +206,13 @@ __device__ __forceinline__ void mbar_arrive_cluster_n(uint32_t cluster_addr, uin
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr), "r"(n)
                  : "memory");
 }
+// Accumulator-release arrival on the leader CTA's barrier: what it orders is
+// TMEM reads (tcgen05.wait::ld + fence::before_thread_sync), not memory the
+// peer reads, so CTA-scope release suffices (a cluster-scope release compiles
+// to MEMBAR.ALL.GPU, which waited on every epilogue warp's outstanding stores).
+__device__ __forceinline__ void mbar_arrive_remote_n(uint32_t cluster_addr, uint32_t n) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr), "r"(n) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_n(uint64_t* bar, uint32_t n) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(n) : "memory");
 }

@@ -415,7 +415,7 @@ void Session::build() {
             // the highest priority, the weight-gradient stream (fills the gaps) the lowest
             int prio_lo = 0, prio_hi = 0;
             cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-            static const bool no_prio = getenv("PPB_NO_PRIO") != nullptr;
+            static const bool no_prio = dev_knob("PPB_NO_PRIO");
             if (no_prio) prio_lo = prio_hi = 0;
             check(cudaStreamCreateWithPriority(&w->sf, cudaStreamNonBlocking, prio_hi), "stream");
             check(cudaStreamCreateWithPriority(&w->sb, cudaStreamNonBlocking, prio_hi), "stream");
@@ -473,7 +473,7 @@ void Session::alloc_buffers() {
     // (unpadded input rows are the K dimension); its output must feed a pool /
     // dense consumer or another dense-conv layer.  Decided from the top down.
     {
-        static const bool off = getenv("PPB_NO_DENSE_CONV") != nullptr;
+        static const bool off = dev_knob("PPB_NO_DENSE_CONV");
         for (int i = L - 1; i >= 1 && !off; --i) {
             LayerInfo& li = net_.info[i];
             if (li.kind != 1 || li.generic || li.im2col || li.H * li.W > 4 || li.in_units % 4 != 0 ||
@@ -1046,12 +1046,12 @@ void Session::build_ops() {
                     // 2x2 max-pool fused into the epilogue when each warp's 32 rows hold
                     // whole windows (grid width <= 16); the GEMM must end up unsplit and
                     // on the tc kernel, else the pool kernel runs as before
-                    static const bool no_pool_fuse = getenv("PPB_NO_POOL_FUSE") != nullptr;
+                    static const bool no_pool_fuse = dev_knob("PPB_NO_POOL_FUSE");
                     // Grid width 32 (VGG conv2 / conv4 on the rank-4 path): 128-row tiles are
                     // 4 image rows, the windows span warp pairs (pl_on 3, TMA-store staging)
                     const int Wo1 = li.Wo(), Ho1 = li.Ho();
                     const bool in_warp = Wo1 >= 2 && 32 % (2 * Wo1) == 0 && (pix % 32 == 0 || 32 % pix == 0);
-                    static const bool no_pool_pair = getenv("PPB_NO_POOL_PAIR") != nullptr;  // A/B switch
+                    static const bool no_pool_pair = dev_knob("PPB_NO_POOL_PAIR");  // A/B switch
                     const bool pair = !no_pool_pair && Wo1 == 32 && pix % 128 == 0 && lay_[l].kind != 1 && wl.u >= 32;
                     if (tf32 && !no_pool_fuse && li.pool == 2 && wl.U != nullptr && !li.dense_conv && wl.argmax &&
                         Ho1 % 2 == 0 && (in_warp || pair)) {
@@ -1659,7 +1659,7 @@ void Session::build_ops() {
         bwd_join = add_op(g0.ordinal, g0.main, nullptr, all, 0);  // std::barrier (:633)
     }
     const float inv_b = 1.f / static_cast<float>(cfg_.batch);
-    static const bool no_side = getenv("PPB_NO_SIDE_JOB") != nullptr;
+    static const bool no_side = dev_knob("PPB_NO_SIDE_JOB");
     // proposed policy: the layer's update = one reduction over the m x
     // acc_slices partial slices (micro-batch order, then split order) applying
     // the real epilogue (SGD on W with the bias update in the same launch, or
@@ -1749,7 +1749,7 @@ void Session::build_ops() {
                        !prev_plan->sk.deferred &&
                        !(prev_wl != nullptr && net_.info[prev_wl->layer - 1].dense_conv)) {  // its fold reads dWx
                 p->sj.on = 1;
-                static const bool side_scalar = getenv("PPB_SIDE_SCALAR") != nullptr;
+                static const bool side_scalar = dev_knob("PPB_SIDE_SCALAR");
                 p->sj.scalar = side_scalar ? 1 : 0;
                 p->sj.M = prev_plan->M;
                 p->sj.N = prev_plan->N;

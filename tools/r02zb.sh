@@ -1,7 +1,7 @@
 #!/bin/bash
 # Single-thread MMA issue loop with incremental descriptors: parity + timing.
 set -u
-TAG=r02zb
+TAG=${TAG:-r02zb}
 mkdir -p gpurun_out
 timeout 1200 python -m pytest tests/test_gemm_gpu.py tests/test_conv_gpu.py tests/test_cnn_gpu.py tests/test_bench_parity_gpu.py tests/test_resnet_gpu.py -q -x > gpurun_out/${TAG}_tests.txt 2>&1; echo "tests rc=$?"; tail -1 gpurun_out/${TAG}_tests.txt
 for rep in 1 2; do
@@ -12,7 +12,7 @@ line=$(timeout 300 python bench.py --workload resnet18 --no-cpu-baseline --steps
 python -c "import json,sys; d=json.loads(sys.argv[1]); print('resnet', round(d['ms_per_step'],4), d['value'])" "$line"
 timeout 300 python tools/profile_ops.py vgg16 > gpurun_out/${TAG}_ops_vgg16.jsonl 2>&1
 timeout 300 python tools/profile_ops.py resnet18 > gpurun_out/${TAG}_ops_resnet18.jsonl 2>&1
-python - <<'PY'
+TAG=$TAG python - <<'PY'
 import json
 def load(f):
     d={}
@@ -20,7 +20,7 @@ def load(f):
         if l.startswith('{"kind"'):
             r=json.loads(l); d[(r['layer'],r['kind'])]=d.get((r['layer'],r['kind']),0)+r['ms']
     return d
-a=load('profiles/r02/r02z_ops_vgg16.jsonl'); b=load('gpurun_out/r02zb_ops_vgg16.jsonl')
+a=load('profiles/r02/r02zb_ops_vgg16.jsonl'); import os; b=load('gpurun_out/'+os.environ.get('TAG','r02zb')+'_ops_vgg16.jsonl')
 print('total', round(sum(a.values())*1000,1), round(sum(b.values())*1000,1))
 for k in sorted(a):
     if abs(a[k]-b.get(k,0))*1000 > 2: print(k, round(a[k]*1000,1), round(b.get(k,0)*1000,1))
