@@ -148,6 +148,7 @@ struct ConvGeom {
     int off = 0;             // spatial offset into the padded tensor
     int ho = 1;              // output grid rows (howo / wo)
     int krows = 1, kimgs = 1;  // KPIX: rows (howo >= 32) or images (howo < 32) per 32-pixel K block
+    int rr = 0;                // ROWS, tc_gemm only: row reuse (box of bh + ksz - 1 rows serves the ksz row taps)
 };
 
 struct Operand {

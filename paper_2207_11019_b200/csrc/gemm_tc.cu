@@ -129,7 +129,7 @@ bool encode_conv_map(CUtensorMap* map, const Operand& o, char* err, size_t errle
         strides[2] = static_cast<cuuint64_t>(o.hp) * o.wp * o.ld * 4;
         box[0] = 32;
         box[1] = g.bw;
-        box[2] = g.bh;
+        box[2] = g.bh + (g.rr ? g.ksz - 1 : 0);
         box[3] = g.bn;
     }
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float*>(o.ptr), dims, strides, box,
@@ -601,14 +601,19 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
     p.grid = (work < units ? work : units) * cg;
     // shared memory: stage ring + barrier block, then the EPI_MERGE db rows,
     // then the TMA-store staging; the ring gives up stages (down to 4) to fit
-    const int stage_bytes = cg == 2 ? (bn == 64    ? TcCfg<64, 2>::kStageBytes
-                                       : bn == 128 ? TcCfg<128, 2>::kStageBytes
-                                                   : TcCfg<256, 2>::kStageBytes)
-                                    : (bn == 64    ? TcCfg<64, 1>::kStageBytes
-                                       : bn == 128 ? TcCfg<128, 1>::kStageBytes
-                                                   : TcCfg<256, 1>::kStageBytes);
-    const int def_stages = cg == 2 ? (bn == 64 ? TcCfg<64, 2>::kStages : bn == 128 ? TcCfg<128, 2>::kStages : TcCfg<256, 2>::kStages)
-                                   : (bn == 64 ? TcCfg<64, 1>::kStages : bn == 128 ? TcCfg<128, 1>::kStages : TcCfg<256, 1>::kStages);
+    // row reuse for 3x3 implicit convs whose 128-row tiles are whole image
+    // rows of one image: one A box of bh + 2 rows per (column tap, channel
+    // block) feeds the 3 row taps, so A crosses L2 -> SM 3x instead of 9x
+    // (conv2 forward: 1.5 GB of L2 reads for 0.17 GB of activations)
+    const ConvGeom& ag = d.a.geom;
+    static const bool no_rr = dev_knob("PPB_NO_ROW_REUSE");  // A/B switch
+    const bool rr = !no_rr && ag.mode == OP_CONV_ROWS && !d.a.mn_major && ag.ksz == 3 && ag.bn == 1 &&
+                    ag.bw % 8 == 0 && ag.bh + ag.ksz - 1 <= 256 && p.sk.splits == 1 && !p.sk.partial &&
+                    !d.partial_out;
+    const int stage_b = bn / cg * kBK * 4;
+    const int stage_bytes = rr ? (ag.bh + ag.ksz - 1) * ag.bw * 128 + ag.ksz * stage_b : kBM * kBK * 4 + stage_b;
+    const int def_stages = (200 * 1024) / stage_bytes > 8 ? 8 : (200 * 1024) / stage_bytes;
+    p.stage_bytes = stage_bytes;
     constexpr int kCapSmem = 227 * 1024;
     auto ring = [&](int st) { return 1024 + st * stage_bytes + 256; };
     p.stages = def_stages;
@@ -645,9 +650,12 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
     // A: M extent x K.  K-major: rows=M, cols=K, box {32, 128}.  MN-major:
     // stored K x M (rows=K, cols=M), box {32, 32}.  B rows per CTA = bn / cg.
     p.ga = d.a.geom;
+    p.ga.rr = rr ? 1 : 0;
     p.gb = d.b.geom;
     if (d.a.geom.mode != OP_DENSE) {
-        if (!encode_conv_map(&p.ta, d.a, err, errlen)) return false;
+        Operand a = d.a;
+        a.geom.rr = p.ga.rr;
+        if (!encode_conv_map(&p.ta, a, err, errlen)) return false;
     } else if (!encode_map(&p.ta, d.a.ptr, d.a.rows, d.a.cols, d.a.ld, d.a.mn_major ? 32 : kBM, d.a.mn_major, err,
                            errlen)) {
         return false;

@@ -27,6 +27,7 @@ struct TcGemmPlan {
     int halo = 0;  // 1: conv_halo.cu kernel (hg describes the padded grid)
     int db_smem = 0;  // extra dynamic smem past the ring: EPI_MERGE db rows + TMA-store staging
     int stages = 0;   // tc_gemm ring stages (<= TcCfg::kStages)
+    int stage_bytes = 0;  // tc_gemm bytes per ring stage (A + B; larger with row reuse)
     HaloGeom hg;
     TmaStore ts;  // TMA-store epilogue (ts.n == 0: register epilogue)
     SideJob sj;   // a previous GEMM's deferred split-K reduction

@@ -233,15 +233,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
+    // row reuse (ga.rr, 3x3 implicit conv over whole image rows): one A box of
+    // bh + ksz - 1 image rows serves the ksz row taps of one (column tap,
+    // channel block) pair, so a stage holds that box and ksz B blocks
+    const int tps = ga.rr ? ga.ksz : 1;                                        // K blocks per stage
+    const int stA = ga.rr ? (ga.bh + ga.ksz - 1) * ga.bw * 128 : C::kStageA;  // bw % 8 == 0: 1 KB multiple
+    const int stB = tps * C::kStageB;
     uint8_t* sA = smem;
-    uint8_t* sB = smem + nst * C::kStageA;  // nst <= C::kStages ring stages (host: smem budget)
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + nst * C::kStageBytes);
+    uint8_t* sB = smem + nst * stA;  // nst ring stages (host: smem budget)
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + nst * (stA + stB));
     uint64_t* empty_bar = full_bar + nst;
     uint64_t* tfull_bar = empty_bar + nst;       // [kAcc]
     uint64_t* tempty_bar = tfull_bar + C::kAcc;  // [kAcc]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + C::kAcc);
-    float* db_s = reinterpret_cast<float*>(smem + nst * C::kStageBytes + 256);  // [4][ldb] (EPI_MERGE db)
-    uint8_t* stg = smem + nst * C::kStageBytes + ts.stage_off;                  // TMA-store staging
+    float* db_s = reinterpret_cast<float*>(smem + nst * (stA + stB) + 256);  // [4][ldb] (EPI_MERGE db)
+    uint8_t* stg = smem + nst * (stA + stB) + ts.stage_off;                  // TMA-store staging
 
     const int warp = threadIdx.x / 32;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
@@ -317,17 +323,67 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     };
+    // row-reuse producers (no split-K): stage j of a tile = (column tap s,
+    // channel block cb), s outer; A box rows [h0 + off, h0 + off + bh + ksz - 1)
+    auto produce_rr = [&](bool is_a) {
+        int stage = 0;
+        uint32_t phase = 0;
+        const int nj = ga.ksz * ga.cblocks;
+        const int tx = is_a ? stA : stB;
+        for (int tile = unit; tile < num_tiles; tile += units) {
+            const int mn = tile % num_mn;
+            const int m0 = (mn % num_m) * TM + static_cast<int>(rank) * kBM;
+            const int n0 = (mn / num_m) * BN + static_cast<int>(rank) * C::kBNc;
+            const int img = m0 / ga.howo, h0 = (m0 - img * ga.howo) / ga.wo;
+            int sc = 0, cb = 0;
+            for (int j = 0; j < nj; ++j) {
+                mbar_wait(&empty_bar[stage], phase ^ 1);
+                Tma<CG> t;
+                t.bar = &full_bar[stage];
+                t.bar_c = 0;
+                if (CG == 1) {
+                    mbar_arrive_expect_tx(&full_bar[stage], tx);
+                } else {
+                    t.bar_c = mapa_shared(smem_u32(&full_bar[stage]), 0);
+                    if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * tx);
+                }
+                if (is_a) {
+                    t.d4(sA + stage * stA, &ta, cb * 32, sc + ga.off, h0 + ga.off, img);
+                } else {
+                    for (int r = 0; r < ga.ksz; ++r)
+                        load_operand<B_MN, C::kBNc, CG>(t, &tb, gb, sB + stage * stB + r * C::kStageB, n0,
+                                                        (r * ga.ksz + sc) * ga.cblocks + cb);
+                }
+                if (++cb == ga.cblocks) {
+                    cb = 0;
+                    ++sc;
+                }
+                if (++stage == nst) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    };
     if (warp == 0) {
         if (elect_one()) {
-            OperandCursor<A_MN, kBM, CG> ca;
-            produce(ca, &ta, ga, sA, C::kStageA, true);
+            if (ga.rr) {
+                produce_rr(true);
+            } else {
+                OperandCursor<A_MN, kBM, CG> ca;
+                produce(ca, &ta, ga, sA, C::kStageA, true);
+            }
         }
         __syncwarp();
         griddep_launch_dependents();  // every load issued: release the stream successor
     } else if (warp == 3) {
         if (elect_one()) {
-            OperandCursor<B_MN, C::kBNc, CG> cb;
-            produce(cb, &tb, gb, sB, C::kStageB, false);
+            if (ga.rr) {
+                produce_rr(false);
+            } else {
+                OperandCursor<B_MN, C::kBNc, CG> cb;
+                produce(cb, &tb, gb, sB, C::kStageB, false);
+            }
         }
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer (leader CTA)
@@ -358,13 +414,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
                 const int split = tile / num_mn;
-                const int kb0 = split * sk.kps, kb_end = min(nk, (split + 1) * sk.kps);
+                const int kb0 = ga.rr ? 0 : split * sk.kps;
+                const int kb_end = ga.rr ? ga.ksz * ga.cblocks : min(nk, (split + 1) * sk.kps);
                 for (int kb = kb0; kb < kb_end; ++kb) {
                     mbar_wait(&full_bar[stage], phase);
                     tc_fence_after();
-                    const uint64_t ad = desc_advance(a0, stage * C::kStageA);
-                    const uint64_t bd = desc_advance(b0, stage * C::kStageB);
-                    if (!no_mma) {
+                    const uint64_t ad = desc_advance(a0, stage * stA);
+                    const uint64_t bd = desc_advance(b0, stage * stB);
+                    if (ga.rr && !no_mma) {
+                        // row tap r: the box rows shifted by r image rows (r * bw * 128 B)
+                        for (int r = 0; r < ga.ksz; ++r) {
+                            const uint64_t ar = desc_advance(ad, r * ga.bw * 128);
+                            const uint64_t br = desc_advance(bd, r * C::kStageB);
+#pragma unroll
+                            for (int kk = 0; kk < kBK / 8; ++kk) {
+                                const uint32_t accum = (kb != 0 || r != 0 || kk != 0) ? 1u : 0u;
+                                if (CG == 2)
+                                    mma_tf32_pair(d_tmem, desc_advance(ar, kk * a_kk), desc_advance(br, kk * b_kk),
+                                                  idesc, accum);
+                                else
+                                    mma_tf32(d_tmem, desc_advance(ar, kk * a_kk), desc_advance(br, kk * b_kk), idesc,
+                                             accum);
+                            }
+                        }
+                    } else if (!no_mma) {
 #pragma unroll
                         for (int kk = 0; kk < kBK / 8; ++kk) {
                             const uint32_t accum = (kb != kb0 || kk != 0) ? 1u : 0u;
@@ -734,7 +807,7 @@ cudaError_t launch_t(const TcGemmPlan& p, cudaStream_t s) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(p.grid);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = 1024 + p.stages * C::kStageBytes + 256 + p.db_smem;
+    cfg.dynamicSmemBytes = 1024 + p.stages * (p.stage_bytes ? p.stage_bytes : C::kStageBytes) + 256 + p.db_smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
