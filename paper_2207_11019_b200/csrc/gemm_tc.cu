@@ -618,7 +618,7 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
     auto ring = [&](int st) { return 1024 + st * stage_bytes + 256; };
     p.stages = def_stages;
     if (p.epi.db_partial != nullptr) {  // in-epilogue bias partials: single-pass (no split-K) only
-        const int need = 4 * ((d.N + 31) / 32 * 32) * 4;
+        const int need = 8 * ((d.N + 31) / 32 * 32) * 4;  // one row per epilogue warp
         if (p.sk.splits > 1 || ring(p.stages) + need > kCapSmem) p.epi.db_partial = nullptr;
         else p.db_smem = need;
     }
@@ -638,8 +638,15 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
             // (plain stores / split-K partials: the masked, pooled-merge and
             // pool-from-staging epilogues read their box back)
             const int extra2 = off + kEpiStageBytesDbuf - 256;
-            if (!p.ts.mask && !p.ts.pool2 && p.epi.pl_on != 2 && p.epi.pl_on != 3 && ring(st) + extra2 <= kCapSmem &&
+            // a short K loop (conv1: one K block per tile) needs few ring
+            // stages; there the second staging set is worth more (each chunk
+            // otherwise waits for the previous chunk's bulk store to read its box)
+            const int kpt = p.sk.splits > 1 || p.sk.partial ? p.sk.kps : nk;
+            int st2 = st;
+            while (ring(st2) + extra2 > kCapSmem && st2 > 4 && st2 > 2 * kpt) --st2;
+            if (!p.ts.mask && !p.ts.pool2 && p.epi.pl_on != 2 && p.epi.pl_on != 3 && ring(st2) + extra2 <= kCapSmem &&
                 !no_dbuf) {
+                p.stages = st2;
                 p.ts.dbuf = 1;
                 p.db_smem = extra2;
             }

@@ -464,15 +464,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp >= 4) {
         // ------------------------------------------------ epilogue
         const int q = warp & 3;              // TMEM lane quarter this warp may access
-        const int half = (warp - 4) >> 2;    // 0 / 1: even / odd 32-column chunks  // TMEM lane quarter this warp may access
+        const int half = (warp - 4) >> 2;    // 0 / 1: even / odd 32-column chunks (or alternate tiles)
         const int lane = threadIdx.x & 31;
         const uint32_t tempty_leader = CG == 2 ? mapa_shared(smem_u32(&tempty_bar[0]), 0) : 0;
         const bool db = epi.db_partial != nullptr;
         const int ldb = (N + 31) & ~31;
-        float* db_row = db_s + q * ldb;
+        // one bias-gradient row per warp: with by-tile epilogues both warps of
+        // a lane quarter accumulate EVERY column (of different tiles), so a
+        // shared row was a read-modify-write race (intermittent db errors)
+        float* db_row = db_s + (q * 2 + half) * ldb;
         if (db) {
-            if (half == 0)
-                for (int i = lane; i < ldb; i += 32) db_row[i] = 0.f;
+            for (int i = lane; i < ldb; i += 32) db_row[i] = 0.f;
             epi_bar_sync();
         }
         // >= 2 tiles per CTA: the two warp groups take alternate tiles (two
@@ -646,11 +648,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-        if (db) {  // both warps of the quarter accumulated into db_row (disjoint columns)
+        if (db) {  // the quarter's two rows, in a fixed order
             epi_bar_sync();
             if (half == 0) {
                 float* out = epi.db_partial + (static_cast<long long>(blockIdx.x) * 4 + q) * N;
-                for (int i = lane; i < N; i += 32) out[i] = db_row[i];
+                for (int i = lane; i < N; i += 32) out[i] = db_row[i] + db_row[ldb + i];
             }
         }
         if (ts.n && lane == 0) bulk_wait<0>();

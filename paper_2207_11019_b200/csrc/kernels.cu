@@ -606,28 +606,42 @@ template <class T>
 __global__ void __launch_bounds__(256) im2col_row32_kernel(const T* __restrict__ src, int imgs, int H, int W,
                                                            int C, int k, int p, float* __restrict__ dst,
                                                            long long ld) {
-    // blockIdx.y = image (32-bit index math: 64-bit divisions dominated this
-    // kernel), 8 threads per output pixel of the image
+    // blockIdx.y = image, 8 threads per output pixel (one float4 of the
+    // 32-float row each).  The column -> (row tap, column tap, channel) map is
+    // a 32-entry shared table built once per block: the per-element integer
+    // divisions by the runtime C and k made this kernel instruction-bound
+    // (60 us for 67 MB of rows).
+    __shared__ int tap_off[32];  // (dh * W + dw) * C + c relative to (ho - p, wo - p); -1: padding column
+    __shared__ short tap_dh[32], tap_dw[32];
+    const int K = k * k * C;
+    if (threadIdx.x < 32) {
+        const int col = threadIdx.x;
+        if (col < K) {
+            const int tap = col / C, c = col - tap * C;
+            const int rr = tap / k, ss = tap - rr * k;
+            tap_off[col] = (rr * W + ss) * C + c;
+            tap_dh[col] = static_cast<short>(rr);
+            tap_dw[col] = static_cast<short>(ss);
+        } else {
+            tap_off[col] = -1;
+        }
+    }
+    __syncthreads();
     const int Ho = H + 2 * p - k + 1, Wo = W + 2 * p - k + 1;
     const int n = blockIdx.y;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int pi = t >> 3, g = t & 7;
     if (pi >= Ho * Wo) return;
     const int ho = pi / Wo, wo = pi - ho * Wo;
-    const int K = k * k * C;
     const T* img = src + static_cast<long long>(n) * H * W * C;
+    const int base = ((ho - p) * W + (wo - p)) * C;  // may be negative; only in-image taps are read
     float r[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
         const int col = 4 * g + e;
-        float v = 0.f;
-        if (col < K) {
-            const int tap = col / C, c = col - tap * C;
-            const int rr = tap / k, ss = tap - rr * k;
-            const int hi = ho + rr - p, wi = wo + ss - p;
-            if (hi >= 0 && hi < H && wi >= 0 && wi < W) v = static_cast<float>(__ldg(img + (hi * W + wi) * C + c));
-        }
-        r[e] = v;
+        const int off = tap_off[col];
+        const int hi = ho - p + tap_dh[col], wi = wo - p + tap_dw[col];
+        r[e] = (off >= 0 && hi >= 0 && hi < H && wi >= 0 && wi < W) ? static_cast<float>(__ldg(img + base + off)) : 0.f;
     }
     reinterpret_cast<float4*>(dst + (static_cast<long long>(n) * Ho * Wo + pi) * ld)[g] =
         make_float4(r[0], r[1], r[2], r[3]);

@@ -284,10 +284,25 @@ __device__ __forceinline__ void epi_values32(const EpiParams& p, int m, int n0, 
     if (n0 >= p.N) return;
     if (p.mode == EPI_STORE) {
         if (p.bias != nullptr) {
-            const int bi = p.seg_w > 0 ? (n0 + lane) % p.seg_w : n0 + lane;
-            const float bl = n0 + lane < p.N ? __ldg(p.bias + bi) : 0.f;
+            const float* b = p.bias + (p.seg_w > 0 ? n0 % p.seg_w : n0);
+            if (n0 + 32 <= p.N && (p.seg_w == 0 || n0 % p.seg_w + 32 <= p.seg_w) &&
+                (reinterpret_cast<uintptr_t>(b) & 15u) == 0) {
+                // the chunk's 32 bias values: warp-uniform float4 loads (L1
+                // broadcast), not a load + 32 shuffles per chunk
 #pragma unroll
-            for (int i = 0; i < 32; ++i) acc[i] += __shfl_sync(0xffffffffu, bl, i);
+                for (int i = 0; i < 32; i += 4) {
+                    const float4 t = __ldg(reinterpret_cast<const float4*>(b + i));
+                    acc[i] += t.x;
+                    acc[i + 1] += t.y;
+                    acc[i + 2] += t.z;
+                    acc[i + 3] += t.w;
+                }
+            } else {
+                const int bi = p.seg_w > 0 ? (n0 + lane) % p.seg_w : n0 + lane;
+                const float bl = n0 + lane < p.N ? __ldg(p.bias + bi) : 0.f;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) acc[i] += __shfl_sync(0xffffffffu, bl, i);
+            }
         }
         if (m < 0 || m >= p.M) return;
         if (p.relu) {

@@ -147,6 +147,18 @@ def test_vgg16_b512_bench_config(n):
     _check("vgg16", n, 1e-4)
 
 
+@pytest.mark.parametrize("workload", ["vgg16", "resnet18"])
+def test_bench_config_run_to_run_bitwise(workload):
+    """Every reduction is ordered (split-K slices, bias-gradient rows, merges):
+    repeated sessions on the same inputs give bitwise-identical weights.  A
+    shared bias-gradient row written by both by-tile epilogue warp groups was
+    an intermittent race that only this kind of repeat exposes."""
+    runs = [_gpu(workload, 1, 1e-2 if workload == "resnet18" else 1.0, 2) for _ in range(3)]
+    for _, W, b, lh in runs[1:]:
+        assert np.array_equal(W, runs[0][1]) and np.array_equal(b, runs[0][2])
+        assert lh == runs[0][3]
+
+
 @pytest.mark.parametrize("n", [1, 8])
 def test_vgg16_b512_large_step(n):
     """Same config at alpha0 = 0.01 (updates ~100x above fp32 weight
