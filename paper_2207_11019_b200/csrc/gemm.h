@@ -207,6 +207,14 @@ struct HaloGeom {
     int dbg = 0;  // timing probes (wrong results): 1 align taps, 2 no epilogue stores, 4 no halo waits
 };
 
+// Geometry of the halo weight-gradient kernel (wgrad_halo.cu): K blocks of 32
+// output pixels (one image row segment), kbs of them over the batch.
+struct WgradGeom {
+    int ho = 0, wo = 0;  // output grid (wo % 32 == 0)
+    int q = 0;           // ring offset of the error signal's padded layout
+    int kbs = 0;         // K blocks (imgs * ho * wo / 32)
+};
+
 // A split-K reduction carried by the NEXT GEMM on the stream ("side job"):
 // the wgrad + SGD of one layer has no reader before the next step's forward,
 // so its reduction (and bias update) runs in the following wgrad GEMM's

@@ -445,6 +445,7 @@ bool tc_gemm_prepare(const GemmDesc& d, TcGemmPlan* out, int force_bn, char* err
         snprintf(err, errlen, "halo conv tile forced on an ineligible GEMM");
         return false;
     }
+    if (force_bn == 0 && ws_alloc && wgrad_halo_eligible(d)) return wgrad_halo_prepare(d, out, err, errlen, ws_alloc);
     TcGemmPlan p;
     p.M = d.M;
     p.N = d.N;
@@ -688,6 +689,7 @@ cudaError_t tc_gemm_launch_reduce(const TcGemmPlan& p, cudaStream_t s) {
 
 cudaError_t tc_gemm_launch(const TcGemmPlan& p, cudaStream_t s) {
     if (p.M <= 0 || p.N <= 0) return cudaSuccess;
+    if (p.halo == 2) return wgrad_halo_launch(p, s);
     if (p.halo) return halo_conv_launch(p, s);
     int dev = 0;
     cudaGetDevice(&dev);

@@ -24,11 +24,12 @@ struct TcGemmPlan {
     EpiParams epi;
     ConvGeom ga, gb;
     SplitK sk;
-    int halo = 0;  // 1: conv_halo.cu kernel (hg describes the padded grid)
+    int halo = 0;  // 1: conv_halo.cu kernel (hg describes the padded grid); 2: wgrad_halo.cu kernel (wg)
     int db_smem = 0;  // extra dynamic smem past the ring: EPI_MERGE db rows + TMA-store staging
     int stages = 0;   // tc_gemm ring stages (<= TcCfg::kStages)
     int stage_bytes = 0;  // tc_gemm bytes per ring stage (A + B; larger with row reuse)
     HaloGeom hg;
+    WgradGeom wg;
     TmaStore ts;  // TMA-store epilogue (ts.n == 0: register epilogue)
     SideJob sj;   // a previous GEMM's deferred split-K reduction
 };
@@ -43,6 +44,10 @@ cudaError_t tc_gemm_launch(const TcGemmPlan& p, cudaStream_t s);
 // slices at p.sk.ws summed in slice order, then p.epi (and the bias job).
 cudaError_t tc_gemm_launch_reduce(const TcGemmPlan& p, cudaStream_t s);
 cudaError_t tc_gemm_init_device();
+// 3x3 / 64 -> 64-channel conv weight gradients (wgrad_halo.cu)
+bool wgrad_halo_eligible(const GemmDesc& d);
+bool wgrad_halo_prepare(const GemmDesc& d, TcGemmPlan* out, char* err, size_t errlen, const WsAlloc& ws_alloc);
+cudaError_t wgrad_halo_launch(const TcGemmPlan& p, cudaStream_t s);
 // per operand-major combination (gemm_tc_inst_*.cu): launch / smem attributes
 template <bool A_MN, bool B_MN>
 cudaError_t tc_launch_mn(const TcGemmPlan& p, cudaStream_t s);

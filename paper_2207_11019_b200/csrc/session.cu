@@ -1738,7 +1738,7 @@ void Session::build_ops() {
             bool*& pend_flag = chains[ci].pend_flag;
             int& pend_fold_op = chains[ci].pend_fold_op;
             if (!tf32) return;
-            const bool can = carrier_ok && !no_side && p->halo == 0;
+            const bool can = carrier_ok && !no_side && (p->halo == 0 || p->halo == 2);  // halo wgrads carry too
             if (pend_flag != nullptr) {
                 if (can) {
                     p->sj = pend_fold;

@@ -156,7 +156,7 @@ def test_bench_config_run_to_run_bitwise(workload):
     runs = [_gpu(workload, 1, 1e-2 if workload == "resnet18" else 1.0, 2) for _ in range(3)]
     for _, W, b, lh in runs[1:]:
         assert np.array_equal(W, runs[0][1]) and np.array_equal(b, runs[0][2])
-        assert lh == runs[0][3]
+        assert np.array_equal(np.asarray(lh), np.asarray(runs[0][3]))
 
 
 @pytest.mark.parametrize("n", [1, 8])

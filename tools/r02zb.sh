@@ -20,7 +20,7 @@ def load(f):
         if l.startswith('{"kind"'):
             r=json.loads(l); d[(r['layer'],r['kind'])]=d.get((r['layer'],r['kind']),0)+r['ms']
     return d
-a=load('profiles/r02/r02ze_ops_vgg16.jsonl'); import os; b=load('gpurun_out/'+os.environ.get('TAG','r02zb')+'_ops_vgg16.jsonl')
+a=load('profiles/r02/r02zh_ops_vgg16.jsonl'); import os; b=load('gpurun_out/'+os.environ.get('TAG','r02zb')+'_ops_vgg16.jsonl')
 print('total', round(sum(a.values())*1000,1), round(sum(b.values())*1000,1))
 for k in sorted(a):
     if abs(a[k]-b.get(k,0))*1000 > 2: print(k, round(a[k]*1000,1), round(b.get(k,0)*1000,1))
