@@ -518,8 +518,11 @@ class Session:
         self.in_features = _input_features(net)
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _lib.lib().ppb_session_destroy(self._h)
+        if getattr(self, "_h", None) and _lib is not None and getattr(_lib, "lib", None) is not None:
+            try:
+                _lib.lib().ppb_session_destroy(self._h)
+            except Exception:  # noqa: BLE001  (interpreter shutdown)
+                pass
             self._h = None
 
     def _host_batch(self, X, labels, dtype):

@@ -59,6 +59,30 @@ __device__ __forceinline__ void load_row32(const float* row, int n0, int nvalid,
     }
 }
 
+// acc[0..32) += the shortcut of row m (EpiParams::rs_src), m < M.
+__device__ __forceinline__ void epi_residual32(const EpiParams& p, int m, int n0, float (&acc)[32]) {
+    const int img = m / p.r_howo, rem = m - img * p.r_howo;
+    const int h = rem / p.r_wo, w = rem - h * p.r_wo;
+    const float* sp = p.rs_src + ((static_cast<long long>(img) * p.rs_hp + h * p.rs_f + p.rs_pad) * p.rs_wp +
+                                  w * p.rs_f + p.rs_pad) * p.rs_ld + p.rs_col0 + n0;
+    int nv = p.N - n0 < 32 ? p.N - n0 : 32;
+    if (p.rs_C - (p.rs_col0 + n0) < nv) nv = p.rs_C - (p.rs_col0 + n0);  // option A: zero-padded channels
+    if (nv >= 32 && (reinterpret_cast<uintptr_t>(sp) & 15u) == 0) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+            const float4 t = __ldg(reinterpret_cast<const float4*>(sp + i));
+            acc[i] += t.x;
+            acc[i + 1] += t.y;
+            acc[i + 2] += t.z;
+            acc[i + 3] += t.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            if (i < nv) acc[i] += __ldg(sp + i);
+    }
+}
+
 // Apply the epilogue to acc[0..32) = C(m, n0..n0+31).
 __device__ __forceinline__ void epilogue32(const EpiParams& p, int m, int n0, float (&acc)[32]) {
     if (m >= p.M || n0 >= p.N) return;
@@ -84,6 +108,7 @@ __device__ __forceinline__ void epilogue32(const EpiParams& p, int m, int n0, fl
 #pragma unroll
                 for (int i = 0; i < 32; ++i) acc[i] += (i < nvalid) ? __ldg(p.bias + n0 + i) : 0.f;
             }
+            if (p.rs_src != nullptr) epi_residual32(p, m, n0, acc);
             if (p.relu) {
 #pragma unroll
                 for (int i = 0; i < 32; ++i) acc[i] = acc[i] > 0.f ? acc[i] : 0.f;

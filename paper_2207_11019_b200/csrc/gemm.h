@@ -46,6 +46,14 @@ struct EpiParams {
     // an ho x wo grid lands at row ((img*hp + h + pad)*wp + w + pad).
     int remap = 0;
     int r_wo = 1, r_howo = 1, r_hp = 1, r_wp = 1, r_pad = 0;
+    // EPI_STORE + shortcut of a residual layer (remap only; kernels.h SkipSrc):
+    // before the ReLU, C(m, n) += rs_src[((img*rs_hp + f*h + rs_pad)*rs_wp + f*w
+    // + rs_pad)*rs_ld + rs_col0 + n] for rs_col0 + n < rs_C (f = rs_f: 1 identity,
+    // 2 ResNet option A), (img, h, w) of row m from r_howo / r_wo -- the order
+    // ((conv + b) + shortcut) of launch_residual_act in one pass.
+    const float* rs_src = nullptr;
+    long long rs_ld = 0;
+    int rs_hp = 1, rs_wp = 1, rs_pad = 0, rs_col0 = 0, rs_f = 1, rs_C = 0;
     // EPI_STORE + fused 2x2 max-pool (tc kernel; rows = pixels of a
     // pl_ho x pl_wo grid with pl_wo <= 16, so each warp's 32 rows hold whole
     // windows): the window's top-left lane writes the pooled value (first max

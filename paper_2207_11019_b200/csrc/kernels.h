@@ -157,8 +157,9 @@ struct SkipSrc {
     int C = 0;                 // C_s: channels >= C get no shortcut
 };
 // Forward of a residual and / or average-pooled conv layer's shard: for each
-// output position u = U + shortcut (written back into U: the pre-activation
-// the backward mask reads), a = act(u), then a p x p average (pool_avg) or no
+// output position u = U + shortcut (written back into U only for a pooled
+// output, where the backward mask needs the pre-activation; otherwise the mask
+// reads a = relu(u), since a > 0 <=> u > 0), a = act(u), then a p x p average (pool_avg) or no
 // pooling, stored into every destination's consumer layout.  c0 = the
 // shard's first channel (absolute).
 cudaError_t launch_residual_act(float* U, long long ldu, int imgs, int Ho, int Wo, int uch, int c0, int relu,

@@ -1015,7 +1015,39 @@ void Session::build_ops() {
                     d.epi.bias = wl.bias;
                     d.epi.relu = li.act == 1 && !li.special();  // residual / avg: the activation follows the shortcut
                     const long long pix = static_cast<long long>(li.Ho()) * li.Wo();
-                    if (wl.U != nullptr) {  // pre-pool output, then pool / relayout
+                    // residual layer without pooling: the shortcut add (identity or option A) and
+                    // the ReLU run in the GEMM epilogue, which stores straight into the
+                    // consumers (no U round trip, no residual_act pass); the backward mask
+                    // then reads the activation (relu(u) > 0 <=> u > 0)
+                    static const bool no_res_fuse = dev_knob("PPB_NO_RES_FUSE");  // A/B switch
+                    bool res_fuse = false;
+                    if (!no_res_fuse && li.res_from > 0 && !li.pool_avg && li.pool == 1 && li.act == 1 &&
+                        !li.dense_conv && lay_[l].kind == 0) {
+                        const int sl = li.res_from;
+                        const LayerInfo& ls = net_.info[sl - 1];
+                        // identity (f = 1, C_s = C_l) or option A (f = 2, C_s <= C_l)
+                        const int f = ls.Hq() / li.Ho();
+                        res_fuse = f >= 1 && ls.Hq() == f * li.Ho() && ls.Wq() == f * li.Wo() &&
+                                   ls.out_units <= li.out_units && lay_[sl].kind == 0;
+                    }
+                    if (res_fuse) {
+                        const int sl = li.res_from;
+                        const ActLayout& sa = lay_[sl];
+                        d.epi.relu = 1;
+                        d.epi.rs_src = act_buf(w.gpu, sl) + so * img_elems(sl);
+                        d.epi.rs_ld = sa.ld;
+                        d.epi.rs_hp = sa.hp;
+                        d.epi.rs_wp = sa.wp;
+                        d.epi.rs_pad = sa.pad;
+                        d.epi.rs_col0 = wl.lo;
+                        d.epi.rs_f = net_.info[sl - 1].Hq() / li.Ho();
+                        d.epi.rs_C = net_.info[sl - 1].out_units;
+                        d.force_splits = 1;  // the split-K reduction kernel has no shortcut term
+                        auto it = act_ready[sl][j].find(w.gpu);
+                        if (it != act_ready[sl][j].end()) deps.insert(deps.end(), it->second.begin(), it->second.end());
+                        wl.u_written = false;
+                    }
+                    if (wl.U != nullptr && !res_fuse) {  // pre-pool output, then pool / relayout
                         d.epi.dst[d.epi.ndst++] = wl.U + so * pix * wl.ldu;
                         d.epi.ldd = wl.ldu;
                     } else {  // straight into every consumer GPU's padded NHWC input
@@ -1081,7 +1113,7 @@ void Session::build_ops() {
                     const double fl = li.dense_conv ? 2.0 * rows * pix * wl.u * li.H * li.W * li.in_units  // executed
                                                     : 2.0 * rows * pix * wl.u * li.ksz * li.ksz * li.in_units;
                     int op = add_op(w.gpu, w.sf, gemm_launch(&wl.p_fwd[j], &wl.d_fwd[j], w.sf), deps, nk(wl.p_fwd[j]), OP_FWD_GEMM, fl);
-                    if (wl.U != nullptr && !pool_fused && li.special()) {
+                    if (wl.U != nullptr && !pool_fused && li.special() && !res_fuse) {
                         // residual extension: U + shortcut -> act -> (average pool) -> consumers
                         ActLayout out = lay_[l];
                         out.col0 = wl.lo;
@@ -1101,11 +1133,14 @@ void Session::build_ops() {
                         float* U = wl.U + so * pix * wl.ldu;
                         const long long ldu = wl.ldu;
                         const int Ho = li.Ho(), Wo = li.Wo(), u = wl.u, c0 = wl.lo, pool = li.pool, relu = li.act == 1;
+                        // launch_residual_act keeps U + shortcut only for pooled outputs: the
+                        // backward mask of the others reads the activation (mask_kind 2)
+                        if (relu && pool == 1) wl.u_written = false;
                         cudaStream_t st = w.sf;
                         op = add_op(w.gpu, st, [=]() {
                             return launch_residual_act(U, ldu, rows, Ho, Wo, u, c0, relu, pool, sk, out, pd, st);
                         }, rdeps, 1, OP_POOL);
-                    } else if (wl.U != nullptr && !pool_fused) {
+                    } else if (wl.U != nullptr && !pool_fused && !res_fuse) {
                         ActLayout out = lay_[l];
                         out.col0 = wl.lo;
                         PoolDsts pd;

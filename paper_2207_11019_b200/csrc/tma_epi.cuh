@@ -21,6 +21,7 @@
 
 #include <cstdint>
 
+#include "epilogue.cuh"
 #include "gemm.h"
 #include "ptx.cuh"
 
@@ -305,6 +306,7 @@ __device__ __forceinline__ void epi_values32(const EpiParams& p, int m, int n0, 
             }
         }
         if (m < 0 || m >= p.M) return;
+        if (p.rs_src != nullptr) epi_residual32(p, m, n0, acc);
         if (p.relu) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) acc[i] = acc[i] > 0.f ? acc[i] : 0.f;

@@ -3,7 +3,7 @@
 # workload, ncu launch list + --set full summaries, elementwise HBM GB/s,
 # overlap trace, simulator cross-check, plan-chooser calibration.
 set -u
-TAG=r02z
+TAG=${TAG:-r02z}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/${TAG}_smi.txt 2>&1
 timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_pytest_gpu.txt 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/${TAG}_pytest_gpu.txt
@@ -29,7 +29,7 @@ python tools/summarize_ncu.py ${TAG} vgg16 > /dev/null 2>&1
 python tools/summarize_ncu.py ${TAG} wide_mlp gemm_wide > /dev/null 2>&1
 cp profiles/${TAG}_ncu.md profiles/${TAG}_gemm_wide_ncu.md profiles/gemm_traffic.json gpurun_out/ 2>/dev/null
 rm -f gpurun_out/${TAG}_gemm_wide.ncu-rep gpurun_out/${TAG}_gemm.ncu-rep
-for W in vgg16 wide_mlp; do
+[ "${CALIB:-1}" = "1" ] && for W in vgg16 wide_mlp; do
   timeout 900 python tools/calibrate.py $W gpurun_out/calib_${W}.json > gpurun_out/${TAG}_calib_${W}.txt 2>&1; echo "calib $W rc=$?"
 done
 du -sh gpurun_out
