@@ -341,6 +341,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                     if (!ahead && (c != half || !ts.mask_pf))
                         tma_mask_issue(ts, box, mbar, lane, static_cast<int>(p0) + q * 32, n0 + c * 32, false,
                                        ts.dbuf);
+                    if (epi.mg_sg != nullptr && m >= 0) epi_merge_sg32(epi, m, n0 + c * 32, v);  // shortcut gradient
                     tma_store_masked_issued(ts, box, mbar, mphase, lane, v, static_cast<int>(p0) + q * 32,
                                             n0 + c * 32);
                     msel ^= ts.dbuf;

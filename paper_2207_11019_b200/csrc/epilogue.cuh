@@ -83,6 +83,29 @@ __device__ __forceinline__ void epi_residual32(const EpiParams& p, int m, int n0
     }
 }
 
+// acc[0..32) += the shortcut gradient of merge row m (EpiParams::mg_sg),
+// 0 <= m < M, columns < N.
+__device__ __forceinline__ void epi_merge_sg32(const EpiParams& p, int m, int n0, float (&acc)[32]) {
+    const int hw = p.mg_hg * p.mg_wg;
+    const int img = m / hw, rem = m - img * hw, y = rem / p.mg_wg, x = rem - y * p.mg_wg;
+    const float* sp = p.mg_sg + ((static_cast<long long>(img) * p.mg_shp + y + p.mg_spad) * p.mg_swp + x + p.mg_spad) *
+                                    p.mg_sld + p.mg_sc0 + n0;
+    if (n0 + 32 <= p.N && (reinterpret_cast<uintptr_t>(sp) & 15u) == 0) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+            const float4 t = __ldg(reinterpret_cast<const float4*>(sp + i));
+            acc[i] += t.x;
+            acc[i + 1] += t.y;
+            acc[i + 2] += t.z;
+            acc[i + 3] += t.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            if (n0 + i < p.N) acc[i] += __ldg(sp + i);
+    }
+}
+
 // Apply the epilogue to acc[0..32) = C(m, n0..n0+31).
 __device__ __forceinline__ void epilogue32(const EpiParams& p, int m, int n0, float (&acc)[32]) {
     if (m >= p.M || n0 >= p.N) return;
@@ -207,6 +230,7 @@ __device__ __forceinline__ void epilogue32(const EpiParams& p, int m, int n0, fl
                     }
                 }
             }
+            if (p.mg_sg != nullptr) epi_merge_sg32(p, m, n0, acc);
             // ReLU mask: the pooled activation (y, x) is the window max = U at the
             // argmax position, so one row of it masks every routed value
             if (p.mg_mask != nullptr) {
@@ -450,6 +474,9 @@ __device__ __forceinline__ void epilogue1(const EpiParams& p, int m, int n, floa
             const int hw = p.mg_hg * p.mg_wg;
             const int img = m / hw, rem = m - img * hw, y = rem / p.mg_wg, x = rem - y * p.mg_wg;
             const int code = p.mg_pool == 2 ? p.mg_argmax[static_cast<long long>(m) * p.mg_uch + n] : 0;
+            if (p.mg_sg != nullptr)
+                v += p.mg_sg[((static_cast<long long>(img) * p.mg_shp + y + p.mg_spad) * p.mg_swp + x + p.mg_spad) *
+                                 p.mg_sld + p.mg_sc0 + n];
             if (p.mg_mask != nullptr) {
                 const long long mrow = (static_cast<long long>(img) * p.mg_mhp + y + p.mg_mpad) * p.mg_mwp + x + p.mg_mpad;
                 if (!(p.mg_mask[mrow * p.mg_mld + p.mg_mcol0 + n] > 0.f)) v = 0.f;

@@ -118,6 +118,13 @@ struct EpiParams {
     float* mg_d = nullptr;                     // [img][dhp][dwp][dld]
     long long mg_dld = 0;
     int mg_dhp = 1, mg_dwp = 1, mg_dpad = 0;
+    // EPI_MERGE with mg_pool == 1, optional: the identity shortcut's gradient
+    // for a skip-source layer (kernels.h SkipGrad, f = 1), added before the
+    // ReLU mask as conv_merge_res_kernel does: acc += mg_sg[((img*mg_shp + y +
+    // mg_spad)*mg_swp + x + mg_spad)*mg_sld + mg_sc0 + n].
+    const float* mg_sg = nullptr;
+    long long mg_sld = 0;
+    int mg_shp = 1, mg_swp = 1, mg_spad = 0, mg_sc0 = 0;
     // EPI_MERGE, optional: column sums of the routed (masked) values, i.e. the
     // bias gradient of the layer below, one row per (CTA, epilogue warp):
     // db_partial[(blockIdx.x * 4 + warp) * N + n], accumulated in shared memory

@@ -551,6 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tma_merge_pool2_chunk(ts, buf, lane, v, code, m0 + q * 32, n0 + c * 32);
                     } else if (ts.n && ts.mask) {
                         if (c != c_first || !pf) tma_mask_issue(ts, stg + (warp - 4) * 4096, mbar, lane, m0 + q * 32, n0 + c * 32);
+                        if (epi.mg_sg != nullptr && m < M) epi_merge_sg32(epi, m, n0 + c * 32, v);  // shortcut gradient
                         tma_store_masked_issued(ts, stg + (warp - 4) * 4096, mbar, mphase, lane, v, m0 + q * 32,
                                                 n0 + c * 32);
                     } else if (ts.n && epi.pl_on == 3) {

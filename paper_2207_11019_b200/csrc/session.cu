@@ -1299,8 +1299,29 @@ void Session::build_ops() {
                 // masks by its ReLU into its padded error signal.
                 const int hw = lb.Hq() * lb.Wq();
                 const bool res_dest = lb.special() || skip_source(l - 1);  // residual-extension merge kernel
+                // a residual / skip-source destination merges in the dgrad epilogue too when
+                // it needs no average-pool routing and its shortcut gradient is an identity
+                // (EPI_MERGE + mg_sg); its ReLU mask then comes from its activation, which
+                // holds for residual layers (their U is not kept, relu(u) > 0 <=> u > 0)
+                static const bool no_sg_fuse = dev_knob("PPB_NO_SG_FUSE");  // A/B switch
+                WLayer* sg_src = nullptr;
+                bool res_fusable = false;
+                if (res_dest && !no_sg_fuse && !lb.pool_avg && lb.pool == 1 && contrib.size() == 1 &&
+                    dests.size() == 1 && (!lb.special() || !workers_[dests[0]]->at(l - 1).u_written)) {
+                    res_fusable = true;
+                    if (const int r = res_consumer(l - 1)) {
+                        const LayerInfo& lr = net_.info[r - 1];
+                        const WLayer& dl0 = workers_[dests[0]]->at(l - 1);
+                        for (int wi : layer_workers_[r]) {
+                            WLayer& cand = workers_[wi]->at(r);
+                            if (cand.contributor && cand.lo <= dl0.lo && dl0.hi <= cand.hi) sg_src = &cand;
+                        }
+                        res_fusable = sg_src != nullptr && lb.Hq() == lr.Ho() && lb.Wq() == lr.Wo() &&
+                                      workers_[dests[0]]->gpu == workers_[contrib[0]]->gpu;
+                    }
+                }
                 if (li.kind == 1 && !li.generic && !li.dense_conv && contrib.size() == 1 && dests.size() == 1 &&
-                    fuse_merge_ && !res_dest) {
+                    fuse_merge_ && (!res_dest || res_fusable)) {
                     // one contributor, one destination: the merge (pool routing,
                     // ReLU mask, padded store) runs in the dgrad epilogue
                     Worker& w = *workers_[contrib[0]];
@@ -1342,11 +1363,22 @@ void Session::build_ops() {
                     // bias-gradient partials of the layer below, same [j][merge block][u]
                     // layout the unfused conv_merge writes
                     d.epi.db_partial = dl.partial + static_cast<long long>(j) * conv_merge_blocks() * dl.u;
+                    std::vector<int> gdeps = wl.delta_ready[j];
+                    if (sg_src != nullptr) {  // the consuming residual layer's error signal (identity shortcut)
+                        const LayerInfo& lr = net_.info[res_consumer(l - 1) - 1];
+                        d.epi.mg_sg = sg_src->delta + so * sg_src->delta_img;
+                        d.epi.mg_sld = sg_src->ldd;
+                        d.epi.mg_spad = lr.dq();
+                        d.epi.mg_shp = lr.Ho() + 2 * lr.dq();
+                        d.epi.mg_swp = lr.Wo() + 2 * lr.dq();
+                        d.epi.mg_sc0 = dl.lo - sg_src->lo;
+                        gdeps.insert(gdeps.end(), sg_src->delta_ready[j].begin(), sg_src->delta_ready[j].end());
+                    }
                     prepare(d, wl.p_dgrad[j], w.gpu);
                     if (!tf32 || wl.p_dgrad[j].epi.db_partial == nullptr) dl.db_colsum = true;
                     const double fl = 2.0 * rows * li.H * li.W * li.in_units * li.ksz * li.ksz * wl.u;
                     const int op = add_op(w.gpu, w.sb, gemm_launch(&wl.p_dgrad[j], &wl.d_dgrad[j], w.sb),
-                                          wl.delta_ready[j], nk(wl.p_dgrad[j]), OP_DGRAD_GEMM, fl);
+                                          gdeps, nk(wl.p_dgrad[j]), OP_DGRAD_GEMM, fl);
                     wl.dgrad_op[j] = op;
                     w.last_bwd[j] = std::max(w.last_bwd[j], op);
                     dl.merge_fused = true;
