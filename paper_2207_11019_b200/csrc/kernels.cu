@@ -1157,7 +1157,11 @@ __global__ void residual_act_kernel(float* __restrict__ U, long long ldu, int im
 // conv_merge_rows_kernel's structure (block = image row, threads = (column,
 // 4-channel group), bias partial per block in fixed order) with average-pool
 // routing and the shortcut term.
-__global__ void conv_merge_res_kernel(ConvMerge m, int pool_avg, SkipGrad sg, float* __restrict__ db_partial) {
+// 592 blocks = 4 per SM: the register cap keeps all four resident (a fifth
+// wave of 3-per-SM residency measured +40 % on the 32x32 layers)
+template <bool COL2IM>
+__global__ void __launch_bounds__(256, 4)
+conv_merge_res_kernel(ConvMerge m, int pool_avg, SkipGrad sg, Col2imSrc cx, float* __restrict__ db_partial) {
     griddep_wait();
     const int groups = m.uch >> 2;
     const int g = threadIdx.x % groups;
@@ -1181,7 +1185,12 @@ __global__ void conv_merge_res_kernel(ConvMerge m, int pool_avg, SkipGrad sg, fl
             // every load of the position issued before the first use (one
             // round trip instead of three dependent ones)
             const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-            const float4 t0 = s0 != nullptr ? __ldg(reinterpret_cast<const float4*>(s0 + gp * m.lds + c0)) : zero;
+            float4 t0 = zero;
+            Col2imS2Taps ct;
+            if (COL2IM)
+                ct = col2im_s2_load(cx.dcols, cx.ldk, m.Ho, m.Wo, cx.C, cx.p, cx.Ho, cx.Wo, cx.c0 + c0, n, h, w);
+            else if (s0 != nullptr)
+                t0 = __ldg(reinterpret_cast<const float4*>(s0 + gp * m.lds + c0));
             const bool amax = p == 2 && !pool_avg;
             const uint32_t b = amax ? __ldg(reinterpret_cast<const uint32_t*>(m.argmax + gp * m.uch + c0)) : 0u;
             const bool has_sg = sg.d != nullptr && h % sg.f == 0 && w % sg.f == 0;
@@ -1195,6 +1204,7 @@ __global__ void conv_merge_res_kernel(ConvMerge m, int pool_avg, SkipGrad sg, fl
             else if (m.mask_kind == 2)
                 mk = __ldg(reinterpret_cast<const float4*>(
                     m.act + ((static_cast<long long>(n) * a.hp + h + a.pad) * a.wp + w + a.pad) * a.ld + a.col0 + c0));
+            if (COL2IM) t0 = col2im_s2_sum(ct);
             float4 v = zero;
             v.x += t0.x; v.y += t0.y; v.z += t0.z; v.w += t0.w;
             for (int s = 1; s < m.slots.n; ++s) {
@@ -1525,7 +1535,23 @@ cudaError_t launch_conv_merge_res(const ConvMerge& m, int pool_avg, const SkipGr
     const int block = group_block(groups);
     if (static_cast<long long>(m.imgs) * m.Ho * m.Wo * m.uch <= 0)
         return cudaMemsetAsync(db_partial, 0, sizeof(float) * grid * m.uch, s);
-    pdl_launch(conv_merge_res_kernel, dim3(grid), dim3(block), sizeof(float) * block * 4, s, m, pool_avg, sg,
+    pdl_launch(conv_merge_res_kernel<false>, dim3(grid), dim3(block), sizeof(float) * block * 4, s, m, pool_avg, sg,
+               Col2imSrc{}, db_partial);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_conv_merge_res_col2im(const ConvMerge& m, int pool_avg, const SkipGrad& sg, const Col2imSrc& cx,
+                                         float* db_partial, cudaStream_t s) {
+    const int grid = conv_merge_blocks();
+    if (m.uch % 4 != 0 || m.pool != 1 || !vec4_ok(m.ldd, 0) || (sg.d != nullptr && !vec4_ok(sg.ldd, sg.c0)) ||
+        cx.dcols == nullptr || cx.C % 4 != 0 || cx.c0 % 4 != 0 || cx.ldk % 4 != 0 ||
+        reinterpret_cast<uintptr_t>(cx.dcols) % 16 != 0)
+        return cudaErrorInvalidValue;
+    const int groups = m.uch / 4;
+    const int block = group_block(groups);
+    if (static_cast<long long>(m.imgs) * m.Ho * m.Wo * m.uch <= 0)
+        return cudaMemsetAsync(db_partial, 0, sizeof(float) * grid * m.uch, s);
+    pdl_launch(conv_merge_res_kernel<true>, dim3(grid), dim3(block), sizeof(float) * block * 4, s, m, pool_avg, sg, cx,
                db_partial);
     return cudaGetLastError();
 }

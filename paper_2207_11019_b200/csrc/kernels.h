@@ -181,6 +181,18 @@ struct SkipGrad {
 // pixel-major slots, mask_kind 1 (U rows: the residual pre-activation) or 2.
 cudaError_t launch_conv_merge_res(const ConvMerge& m, int pool_avg, const SkipGrad& sg, float* db_partial,
                                   cudaStream_t s);
+// The single-contributor slot of a 3x3 / stride-2 generic conv's dgrad read
+// straight from its column-space partial (launch_col2im's arguments, c0 = the
+// destination shard's first channel): the merge sums the <= 2 x 2 taps of
+// each position (col2im's ascending order, same bits) instead of reading a
+// slot col2im wrote.
+struct Col2imSrc {
+    const float* dcols = nullptr;
+    long long ldk = 0;
+    int C = 0, p = 0, Ho = 0, Wo = 0, c0 = 0;
+};
+cudaError_t launch_conv_merge_res_col2im(const ConvMerge& m, int pool_avg, const SkipGrad& sg, const Col2imSrc& cx,
+                                         float* db_partial, cudaStream_t s);
 
 // NCCL merge backend: the all-gathered shard outputs [g][rows][u] (rank
 // order) into the activation rows [rows][ld] at columns k*u + c.

@@ -1387,6 +1387,14 @@ void Session::build_ops() {
                     continue;
                 }
                 bool fused_dc = false;  // dense-conv dgrad performed the whole merge
+                // 3x3 stride-2 generic conv, one contributor and one residual-extension
+                // destination: the merge reads the column-space partial itself
+                // (launch_conv_merge_res_col2im), no col2im pass and no slot round trip
+                static const bool no_c2m_fuse = dev_knob("PPB_NO_COL2IM_MERGE");  // A/B switch
+                const bool c2m = !no_c2m_fuse && li.kind == 1 && li.generic && !li.dense_conv && li.ksz == 3 &&
+                                 li.stride == 2 && res_dest && lb.pool == 1 && !lb.pool_avg && contrib.size() == 1 &&
+                                 dests.size() == 1 && workers_[dests[0]]->gpu == workers_[contrib[0]]->gpu;
+                Col2imSrc c2m_src;
                 for (size_t k = 0; k < contrib.size(); ++k) {
                     Worker& w = *workers_[contrib[k]];
                     WLayer& wl = w.at(l);
@@ -1471,7 +1479,16 @@ void Session::build_ops() {
                         const long long ldk = dcv ? li.in_units : wl.ldk;  // dense conv: pixel-major [img*Q][C]
                         const int H = li.H, W = li.W, C = li.in_units, ks = dcv ? 1 : li.ksz, pd = dcv ? 0 : li.pad,
                                   strd = li.stride;
-                        for (int di : direct ? std::vector<int>{} : dests) {
+                        if (c2m) {
+                            c2m_src.dcols = dc;
+                            c2m_src.ldk = ldk;
+                            c2m_src.C = C;
+                            c2m_src.p = pd;
+                            c2m_src.Ho = li.Ho();
+                            c2m_src.Wo = li.Wo();
+                            c2m_src.c0 = workers_[dests[0]]->at(l - 1).lo;
+                        }
+                        for (int di : direct || c2m ? std::vector<int>{} : dests) {
                             WLayer& dl = workers_[di]->at(l - 1);
                             float* dst = dl.slots[k] + so * H * W * dl.slot_ld;
                             const long long ldo = dl.slot_ld;
@@ -1586,8 +1603,14 @@ void Session::build_ops() {
                             mdeps.insert(mdeps.end(), src->delta_ready[j].begin(), src->delta_ready[j].end());
                         }
                         const int pavg = lb.pool_avg;
-                        op = add_op(dw.gpu, st, [=]() { return launch_conv_merge_res(cm, pavg, sg, dbp, st); }, mdeps, 1,
-                                    OP_CONV_MERGE);
+                        if (c2m) {
+                            const Col2imSrc cx = c2m_src;
+                            op = add_op(dw.gpu, st, [=]() { return launch_conv_merge_res_col2im(cm, pavg, sg, cx, dbp, st); },
+                                        mdeps, 1, OP_CONV_MERGE);
+                        } else {
+                            op = add_op(dw.gpu, st, [=]() { return launch_conv_merge_res(cm, pavg, sg, dbp, st); }, mdeps, 1,
+                                        OP_CONV_MERGE);
+                        }
                     } else {
                         op = add_op(dw.gpu, st, [=]() { return launch_conv_merge(cm, dbp, st); }, dgrad_ops, 1,
                                     OP_CONV_MERGE);
