@@ -341,9 +341,19 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                     if (!ahead && (c != half || !ts.mask_pf))
                         tma_mask_issue(ts, box, mbar, lane, static_cast<int>(p0) + q * 32, n0 + c * 32, false,
                                        ts.dbuf);
-                    if (epi.mg_sg != nullptr && m >= 0) epi_merge_sg32(epi, m, n0 + c * 32, v);  // shortcut gradient
-                    tma_store_masked_issued(ts, box, mbar, mphase, lane, v, static_cast<int>(p0) + q * 32,
-                                            n0 + c * 32);
+                    if (ts.res) {  // residual forward: conv + bias here, shortcut + ReLU from the box
+                        epi_values32(epi, m, n0 + c * 32, v, lane, true);
+                        if (m < 0) {  // pad-ring rows keep the destination's zeros (the box's ring is zero)
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+                        }
+                        tma_store_res_issued(ts, box, mbar, mphase, lane, v, static_cast<int>(p0) + q * 32,
+                                             n0 + c * 32, epi.relu);
+                    } else {
+                        if (epi.mg_sg != nullptr && m >= 0) epi_merge_sg32(epi, m, n0 + c * 32, v);  // shortcut gradient
+                        tma_store_masked_issued(ts, box, mbar, mphase, lane, v, static_cast<int>(p0) + q * 32,
+                                                n0 + c * 32);
+                    }
                     msel ^= ts.dbuf;
                     if (ahead) {
                         if (c + 2 < BN / 32) mask_issue(tile, c + 2);

@@ -352,7 +352,19 @@ bool tma_store_setup(const EpiParams& e, int M, int N, const HaloGeom* hg, TmaSt
         mptr = e.mask + e.mcol0;
         mld = e.ldm;
     }
+    // residual layer, identity shortcut: the shortcut rows share the store's
+    // padded geometry, so they load as the "mask" box (TmaStore::res)
+    bool res = false;
+    static const bool no_res_box = dev_knob("PPB_NO_RES_BOX");  // A/B switch
+    if (e.mode == EPI_STORE && e.rs_src != nullptr && e.rs_f == 1 && e.remap && !no_res_box &&
+        e.rs_C - e.rs_col0 >= N && (hg != nullptr ? (e.rs_hp == hg->hp && e.rs_wp == hg->wp && e.rs_pad == 1)
+                                                  : (rank == 4 && e.rs_hp == hp && e.rs_wp == wp && e.rs_pad == pad))) {
+        mptr = e.rs_src + e.rs_col0;
+        mld = e.rs_ld;
+        res = true;
+    }
     ts->mask = 0;
+    ts->res = 0;
     static const bool no_mask = dev_knob("PPB_NO_TMA_MASK");
     if (mptr != nullptr && no_mask) return false;
     if (mptr != nullptr) {
@@ -365,6 +377,7 @@ bool tma_store_setup(const EpiParams& e, int M, int N, const HaloGeom* hg, TmaSt
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return false;
         ts->mask = 1;
+        ts->res = res ? 1 : 0;
     }
     ts->rank = static_cast<int>(rank);
     for (int d = 0; d < nd; ++d) {

@@ -551,9 +551,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tma_merge_pool2_chunk(ts, buf, lane, v, code, m0 + q * 32, n0 + c * 32);
                     } else if (ts.n && ts.mask) {
                         if (c != c_first || !pf) tma_mask_issue(ts, stg + (warp - 4) * 4096, mbar, lane, m0 + q * 32, n0 + c * 32);
-                        if (epi.mg_sg != nullptr && m < M) epi_merge_sg32(epi, m, n0 + c * 32, v);  // shortcut gradient
-                        tma_store_masked_issued(ts, stg + (warp - 4) * 4096, mbar, mphase, lane, v, m0 + q * 32,
-                                                n0 + c * 32);
+                        if (ts.res) {  // residual forward: conv + bias here, shortcut + ReLU from the box
+                            epi_values32(epi, m, n0 + c * 32, v, lane, true);
+                            tma_store_res_issued(ts, stg + (warp - 4) * 4096, mbar, mphase, lane, v, m0 + q * 32,
+                                                 n0 + c * 32, epi.relu);
+                        } else {
+                            if (epi.mg_sg != nullptr && m < M) epi_merge_sg32(epi, m, n0 + c * 32, v);  // shortcut gradient
+                            tma_store_masked_issued(ts, stg + (warp - 4) * 4096, mbar, mphase, lane, v, m0 + q * 32,
+                                                    n0 + c * 32);
+                        }
                     } else if (ts.n && epi.pl_on == 3) {
                         // 2x2 pool across the warp pair holding image rows 2y, 2y+1
                         // (pre-pool rows are not stored: nothing reads them)

@@ -51,6 +51,9 @@ struct TmaStore {
     CUtensorMap mmap;
     int dbuf = 0;  // two staging boxes per warp (plain stores / split-K partials only)
     int mask_pf = 1;  // masked epilogues: issue the first chunk's mask load before the accumulator wait
+    // EPI_STORE of a residual layer (identity shortcut): the "mask" box holds
+    // the shortcut rows, applied as v = relu(v + box) (tma_store_res_issued)
+    int res = 0;
 };
 
 // The staging box of epilogue warp `ewarp` for its `sel`-th buffer.
@@ -149,6 +152,43 @@ __device__ __forceinline__ void tma_store_masked_issued(const TmaStore& ts, uint
         v[4 * j + 1] = m1 > 0.f ? v[4 * j + 1] : 0.f;
         v[4 * j + 2] = m2 > 0.f ? v[4 * j + 2] : 0.f;
         v[4 * j + 3] = m3 > 0.f ? v[4 * j + 3] : 0.f;
+        st_shared_v4(a, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+        if (ts.rank == 2) {
+            for (int d = 0; d < ts.n; ++d) tma_store_2d(&ts.map[d], buf, n, r0);
+        } else {
+            const int img = r0 / ts.pix, rem = r0 - img * ts.pix;
+            const int h = rem / ts.wo, w = rem - h * ts.wo;
+            for (int d = 0; d < ts.n; ++d) tma_store_4d(&ts.map[d], buf, n, w, h, img);
+        }
+        bulk_commit();
+    }
+}
+
+// Residual variant of tma_store_masked_issued (TmaStore::res): v holds conv +
+// bias; the issued box holds the shortcut rows; v = act(v + shortcut) in the
+// reference order, written back in place and stored.
+__device__ __forceinline__ void tma_store_res_issued(const TmaStore& ts, uint8_t* buf, uint64_t* bar, uint32_t& phase,
+                                                     int lane, float (&v)[32], int r0, int n, int relu) {
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    const uint32_t row = smem_u32(buf) + lane * 128;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t a = row + ((j ^ (lane & 7)) << 4);
+        float s0, s1, s2, s3;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(s0), "=f"(s1), "=f"(s2), "=f"(s3) : "r"(a));
+        v[4 * j] += s0;
+        v[4 * j + 1] += s1;
+        v[4 * j + 2] += s2;
+        v[4 * j + 3] += s3;
+        if (relu) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) v[4 * j + i] = v[4 * j + i] > 0.f ? v[4 * j + i] : 0.f;
+        }
         st_shared_v4(a, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
     }
     fence_proxy_async();
@@ -281,7 +321,8 @@ __device__ __forceinline__ void tma_store_chunk(const TmaStore& ts, uint8_t* buf
 // EPI_STORE: bias + ReLU.  EPI_MERGE with pool 1 / EPI_MASK: ReLU mask.
 // Warp-uniform call (all lanes, any m): the bias row is loaded once per warp
 // (lane L holds bias[n0 + L]) and broadcast with shuffles.
-__device__ __forceinline__ void epi_values32(const EpiParams& p, int m, int n0, float (&acc)[32], int lane) {
+__device__ __forceinline__ void epi_values32(const EpiParams& p, int m, int n0, float (&acc)[32], int lane,
+                                             bool bias_only = false) {
     if (n0 >= p.N) return;
     if (p.mode == EPI_STORE) {
         if (p.bias != nullptr) {
@@ -305,7 +346,7 @@ __device__ __forceinline__ void epi_values32(const EpiParams& p, int m, int n0, 
                 for (int i = 0; i < 32; ++i) acc[i] += __shfl_sync(0xffffffffu, bl, i);
             }
         }
-        if (m < 0 || m >= p.M) return;
+        if (m < 0 || m >= p.M || bias_only) return;  // bias_only: shortcut + ReLU in tma_store_res_issued
         // per-lane shortcut rows: staging them through shared memory for
         // coalesced reads measured slower (+95 us on ResNet-18's 64-channel
         // residual layers: the epilogue's shared-memory traffic competes with
