@@ -299,7 +299,10 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
         // (the next tile's first chunk after the last) is loaded as soon as the
         // current chunk's store is issued, so its latency hides behind a whole
         // chunk of epilogue work, not only behind the tile's MMAs
-        const bool ahead = masked && ts.mask_pf && ts.dbuf;
+        // shortcut-gradient merge: the second box holds the shortcut rows, so no
+        // look-ahead mask load (box 0 only, both boxes loaded per chunk)
+        const bool sgbox = masked && ts.sg && ts.dbuf;
+        const bool ahead = masked && ts.mask_pf && ts.dbuf && !sgbox;
         auto mask_issue = [&](int t, int c) {
             const long long pp = static_cast<long long>(t % num_m) * TM + static_cast<long long>(rank) * kBM;
             tma_mask_issue(ts, epi_box(stg, warp - 4, msel), mbar, lane, static_cast<int>(pp) + q * 32,
@@ -323,9 +326,14 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
             // the first chunk's ReLU-mask box is loaded while the tile's MMAs run
             // (with two staging boxes per warp, while the previous chunk's store
             // still reads the other box)
-            if (masked && ts.mask_pf && !ahead && half < BN / 32)
-                tma_mask_issue(ts, epi_box(stg, warp - 4, msel), mbar, lane, static_cast<int>(p0) + q * 32,
-                               n0 + half * 32, false, ts.dbuf);
+            if (masked && ts.mask_pf && !ahead && half < BN / 32) {
+                if (sgbox)
+                    tma_mask_sg_issue(ts, epi_box(stg, warp - 4, 0), epi_box(stg, warp - 4, 1), mbar, lane,
+                                      static_cast<int>(p0) + q * 32, n0 + half * 32);
+                else
+                    tma_mask_issue(ts, epi_box(stg, warp - 4, msel), mbar, lane, static_cast<int>(p0) + q * 32,
+                                   n0 + half * 32, false, ts.dbuf);
+            }
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
 #pragma unroll 1
@@ -338,10 +346,19 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                 for (int i = 0; i < 32; ++i) v[i] = m >= 0 ? __uint_as_float(rr[i]) : 0.f;
                 if (masked) {  // the mask is zero on the ring
                     uint8_t* box = epi_box(stg, warp - 4, msel);
-                    if (!ahead && (c != half || !ts.mask_pf))
+                    if (sgbox) {
+                        uint8_t* box1 = epi_box(stg, warp - 4, 1);
+                        if (c != half || !ts.mask_pf)
+                            tma_mask_sg_issue(ts, box, box1, mbar, lane, static_cast<int>(p0) + q * 32, n0 + c * 32);
+                        tma_store_masked_sg_issued(ts, box, box1, mbar, mphase, lane, v, static_cast<int>(p0) + q * 32,
+                                                   n0 + c * 32);
+                    } else if (!ahead && (c != half || !ts.mask_pf)) {
                         tma_mask_issue(ts, box, mbar, lane, static_cast<int>(p0) + q * 32, n0 + c * 32, false,
                                        ts.dbuf);
-                    if (ts.res) {  // residual forward: conv + bias here, shortcut + ReLU from the box
+                    }
+                    if (sgbox) {
+                        // stored above
+                    } else if (ts.res) {  // residual forward: conv + bias here, shortcut + ReLU from the box
                         epi_values32(epi, m, n0 + c * 32, v, lane, true);
                         if (m < 0) {  // pad-ring rows keep the destination's zeros (the box's ring is zero)
 #pragma unroll
@@ -354,7 +371,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1)
                         tma_store_masked_issued(ts, box, mbar, mphase, lane, v, static_cast<int>(p0) + q * 32,
                                                 n0 + c * 32);
                     }
-                    msel ^= ts.dbuf;
+                    if (!sgbox) msel ^= ts.dbuf;
                     if (ahead) {
                         if (c + 2 < BN / 32) mask_issue(tile, c + 2);
                         else if (tile + units < num_tiles) mask_issue(tile + units, half);

@@ -378,6 +378,19 @@ bool tma_store_setup(const EpiParams& e, int M, int N, const HaloGeom* hg, TmaSt
             return false;
         ts->mask = 1;
         ts->res = res ? 1 : 0;
+        // halo merge with a shortcut gradient of the same padded geometry: its
+        // rows load as a second box (used when the kernel has two boxes per warp)
+        ts->sg = 0;
+        static const bool no_sg_box = dev_knob("PPB_NO_SG_BOX");  // A/B switch
+        if (e.mode == EPI_MERGE && e.mg_sg != nullptr && hg != nullptr && rank == 2 && !no_sg_box &&
+            e.mg_shp == hg->hp && e.mg_swp == hg->wp && e.mg_spad == 1 && e.mg_sld % 4 == 0 &&
+            (reinterpret_cast<uintptr_t>(e.mg_sg + e.mg_sc0) & 15u) == 0) {
+            cuuint64_t sstr[3] = {static_cast<cuuint64_t>(e.mg_sld) * 4, 0, 0};
+            if (enc(&ts->smap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<float*>(e.mg_sg + e.mg_sc0), dims,
+                    sstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+                ts->sg = 1;
+        }
     }
     ts->rank = static_cast<int>(rank);
     for (int d = 0; d < nd; ++d) {

@@ -54,6 +54,11 @@ struct TmaStore {
     // EPI_STORE of a residual layer (identity shortcut): the "mask" box holds
     // the shortcut rows, applied as v = relu(v + box) (tma_store_res_issued)
     int res = 0;
+    // EPI_MERGE with a shortcut gradient (EpiParams::mg_sg), halo kernel with
+    // two staging boxes per warp: the shortcut-gradient rows are TMA-loaded
+    // into the second box next to the mask box (tma_mask_sg_issue)
+    int sg = 0;
+    CUtensorMap smap;
 };
 
 // The staging box of epilogue warp `ewarp` for its `sel`-th buffer.
@@ -132,6 +137,51 @@ __device__ __forceinline__ void tma_mask_issue(const TmaStore& ts, uint8_t* buf,
             const int h = rem / ts.wo, w = rem - h * ts.wo;
             tma_load_4d(buf, &ts.mmap, bar, n, w, h, img);
         }
+    }
+}
+
+// Mask box -> box0 and shortcut-gradient box -> box1 on one mbarrier; box0
+// may still be read by this warp's previous bulk store (wait for all).
+__device__ __forceinline__ void tma_mask_sg_issue(const TmaStore& ts, uint8_t* box0, uint8_t* box1, uint64_t* bar,
+                                                  int lane, int r0, int n) {
+    if (lane == 0) {
+        box_wait(0);
+        mbar_arrive_expect_tx(bar, 8192);
+        tma_load_2d(box0, &ts.mmap, bar, n, r0);
+        tma_load_2d(box1, &ts.smap, bar, n, r0);
+    }
+}
+
+// Masked store with the shortcut gradient: v += box1 (shortcut gradient),
+// then the ReLU mask from box0, written into box0 and stored (conv_merge_res
+// order: sum, shortcut, mask).  v is masked in place (db).
+__device__ __forceinline__ void tma_store_masked_sg_issued(const TmaStore& ts, uint8_t* box0, uint8_t* box1,
+                                                           uint64_t* bar, uint32_t& phase, int lane, float (&v)[32],
+                                                           int r0, int n) {
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    const uint32_t row0 = smem_u32(box0) + lane * 128, row1 = smem_u32(box1) + lane * 128;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t off = (j ^ (lane & 7)) << 4;
+        float g0, g1, g2, g3, m0, m1, m2, m3;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(g0), "=f"(g1), "=f"(g2), "=f"(g3) : "r"(row1 + off));
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(m0), "=f"(m1), "=f"(m2), "=f"(m3) : "r"(row0 + off));
+        v[4 * j] += g0;
+        v[4 * j + 1] += g1;
+        v[4 * j + 2] += g2;
+        v[4 * j + 3] += g3;
+        v[4 * j] = m0 > 0.f ? v[4 * j] : 0.f;
+        v[4 * j + 1] = m1 > 0.f ? v[4 * j + 1] : 0.f;
+        v[4 * j + 2] = m2 > 0.f ? v[4 * j + 2] : 0.f;
+        v[4 * j + 3] = m3 > 0.f ? v[4 * j + 3] : 0.f;
+        st_shared_v4(row0 + off, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    }
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+        for (int d = 0; d < ts.n; ++d) tma_store_2d(&ts.map[d], box0, n, r0);
+        bulk_commit();
     }
 }
 
