@@ -116,6 +116,25 @@ __device__ __forceinline__ void splitk_item_seq(const EpiParams& epi, const Spli
 // thread index, nt = their count).  Bias job first: warp-group of 32 lanes =
 // 4 columns x 8 phases (phase p sums chunks p, p+8, ... in order), butterfly
 // over the phases (fixed tree), lane with phase 0 updates the column.
+// Sum of bpart[k * bu + col] over k = k0, k0 + 8, ... < chunks, added in
+// ascending k (the bias-gradient partials' fixed order) with eight loads in
+// flight per batch: the one-load-per-add loop the compiler emitted for the
+// plain form was a serial chain of L2 round trips (~74 per lane for a
+// 592-chunk merge), the longest part of conv1's wgrad side job.
+__device__ __forceinline__ float bias_chunk_sum(const float* __restrict__ bpart, int bu, int col, int k0, int chunks) {
+    float acc = 0.f;
+    int k = k0;
+    for (; k + 7 * 8 < chunks; k += 64) {
+        float t[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) t[i] = __ldcg(bpart + static_cast<long long>(k + 8 * i) * bu + col);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc += t[i];
+    }
+    for (; k < chunks; k += 8) acc += __ldcg(bpart + static_cast<long long>(k) * bu + col);
+    return acc;
+}
+
 __device__ __forceinline__ void run_side_job(const SideJob& sj, long long gt, long long nt, int lane) {
     const SplitK& sk = sj.sk;
     if (sk.bias != nullptr) {
@@ -123,11 +142,8 @@ __device__ __forceinline__ void run_side_job(const SideJob& sj, long long gt, lo
         const int groups = (sk.bu + 3) / 4;
         for (long long grp = gw; grp < groups; grp += nw) {
             const int col = static_cast<int>(grp) * 4 + (lane >> 3), ph = lane & 7;
-            float acc = 0.f;
-            if (col < sk.bu) {
-#pragma unroll 4
-                for (int k = ph; k < sk.bchunks; k += 8) acc += __ldcg(sk.bpart + static_cast<long long>(k) * sk.bu + col);
-            }
+            const float acc0 = col < sk.bu ? bias_chunk_sum(sk.bpart, sk.bu, col, ph, sk.bchunks) : 0.f;
+            float acc = acc0;
             acc += __shfl_xor_sync(0xffffffffu, acc, 1);
             acc += __shfl_xor_sync(0xffffffffu, acc, 2);
             acc += __shfl_xor_sync(0xffffffffu, acc, 4);
@@ -695,11 +711,7 @@ __global__ void __launch_bounds__(256) splitk_epilogue_kernel(
         __shared__ float bsh[8][33];
         const int t = threadIdx.y * blockDim.x + threadIdx.x;
         const int col = (blockIdx.x - (gridDim.x - bblocks)) * 32 + (t & 31), y = t >> 5;
-        float acc = 0.f;
-        if (col < sk.bu) {
-#pragma unroll 4
-            for (int k = y; k < sk.bchunks; k += 8) acc += __ldcg(sk.bpart + static_cast<long long>(k) * sk.bu + col);
-        }
+        const float acc = col < sk.bu ? bias_chunk_sum(sk.bpart, sk.bu, col, y, sk.bchunks) : 0.f;
         bsh[y][t & 31] = acc;
         __syncthreads();
         if (y == 0 && col < sk.bu) {

@@ -288,8 +288,17 @@ __global__ void __launch_bounds__(1024) bias_update_cols_kernel(const float* __r
     const int c = blockIdx.x * 32 + threadIdx.x;
     float s = 0.f;
     if (c < u) {
-#pragma unroll 4
-        for (int k = threadIdx.y; k < chunks; k += 32) s += __ldg(partial + static_cast<long long>(k) * u + c);
+        // ascending k (fixed order), eight loads in flight per batch (the
+        // plain loop compiled to one dependent L2 round trip per add)
+        int k = threadIdx.y;
+        for (; k + 7 * 32 < chunks; k += 8 * 32) {
+            float t[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) t[i] = __ldg(partial + static_cast<long long>(k + 32 * i) * u + c);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) s += t[i];
+        }
+        for (; k < chunks; k += 32) s += __ldg(partial + static_cast<long long>(k) * u + c);
     }
     sh[threadIdx.y][threadIdx.x] = s;
     __syncthreads();
