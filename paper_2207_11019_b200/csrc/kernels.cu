@@ -999,6 +999,7 @@ __global__ void conv_merge_rows_kernel(ConvMerge m, float* __restrict__ db_parti
     const int rows = m.imgs * m.Ho;
     const ActLayout& a = m.act_layout;
     float4 db = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float* s0 = m.slots.n > 0 ? m.slots.slot[0] : nullptr;
     for (int r = blockIdx.x; r < rows; r += gridDim.x) {
         const int n = r / m.Ho, h = r - n * m.Ho;
         const int y = m.pool == 2 ? h >> 1 : h;
@@ -1023,20 +1024,28 @@ __global__ void conv_merge_rows_kernel(ConvMerge m, float* __restrict__ db_parti
                 mk[u] = make_float4(1.f, 1.f, 1.f, 1.f);
                 if (w >= m.Wo) continue;
                 const int x = m.pool == 2 ? w >> 1 : w;
-                if (row_in && x < Wg) {
-                    const long long gp = grow + x;
-                    for (int s = 0; s < m.slots.n; ++s) {
-                        const float4 v = __ldg(reinterpret_cast<const float4*>(m.slots.slot[s] + gp * m.lds + c0));
-                        gr[u].x += v.x; gr[u].y += v.y; gr[u].z += v.z; gr[u].w += v.w;
-                    }
+                // first slot, argmax and mask issued before the extra slots' loop
+                // (the loop between them serialised the position's round trips)
+                float4 t0 = make_float4(0.f, 0.f, 0.f, 0.f);
+                const bool in = row_in && x < Wg;
+                const long long gp = grow + x;
+                if (in) {
+                    if (s0 != nullptr) t0 = __ldg(reinterpret_cast<const float4*>(s0 + gp * m.lds + c0));
                     if (m.pool == 2) am[u] = __ldg(reinterpret_cast<const uint32_t*>(m.argmax + gp * m.uch + c0));
                 } else {
                     am[u] = 0xffffffffu;  // outside the pooled grid: no gradient
                 }
                 if (m.mask_kind == 2) mk[u] = __ldg(reinterpret_cast<const float4*>(arow + static_cast<long long>(w) * a.ld));
-                else if (m.mask_kind == 3 && row_in && x < Wg)
+                else if (m.mask_kind == 3 && in)
                     mk[u] = __ldg(reinterpret_cast<const float4*>(arow + static_cast<long long>(x) * a.ld));
                 else if (m.mask_kind == 1) mk[u] = __ldg(reinterpret_cast<const float4*>(urow + static_cast<long long>(w) * m.ldu));
+                if (in) {
+                    gr[u].x += t0.x; gr[u].y += t0.y; gr[u].z += t0.z; gr[u].w += t0.w;
+                    for (int s = 1; s < m.slots.n; ++s) {
+                        const float4 v = __ldg(reinterpret_cast<const float4*>(m.slots.slot[s] + gp * m.lds + c0));
+                        gr[u].x += v.x; gr[u].y += v.y; gr[u].z += v.z; gr[u].w += v.w;
+                    }
+                }
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
